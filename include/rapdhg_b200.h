@@ -1,0 +1,318 @@
+/*
+ * rapdhg_b200.h — C-ABI of the B200-native rAPDHG (PDQP) solver.
+ *
+ * Drop-in boundary for the reference C++ solver's iteration path
+ * (/root/reference/proj/include/rapdhg/*.hpp). Every entry point below names
+ * the reference interface it replaces (file:line, paths relative to
+ * proj/include/rapdhg/). Plain pointers and sizes only: no C++ or torch types
+ * cross this boundary. All array arguments are HOST memory unless a function
+ * name says `_device`; the library uploads, runs the fp64 sm_100a kernels and
+ * copies results back.
+ *
+ * Error behaviour mirrors the reference's exceptions: a function returns
+ * RAPDHG_OK (0) or a negative code; the message the reference would have put
+ * in its std::invalid_argument / std::out_of_range is available from
+ * rapdhg_last_error() (thread-local). Numerical outcomes (iteration limit,
+ * NaN) are statuses in the result, not errors — as in solver.hpp:26,372.
+ *
+ * There is no CPU fallback: without a visible CUDA device every compute entry
+ * point returns RAPDHG_E_NO_DEVICE.
+ */
+#ifndef RAPDHG_B200_H_
+#define RAPDHG_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RAPDHG_ABI_VERSION 1
+
+/* ---- error codes (return values) ------------------------------------- */
+enum {
+  RAPDHG_OK = 0,
+  RAPDHG_E_INVALID_ARGUMENT = -1, /* std::invalid_argument in the reference */
+  RAPDHG_E_OUT_OF_RANGE = -2,     /* std::out_of_range (sparse.hpp:36)     */
+  RAPDHG_E_CUDA = -3,             /* CUDA runtime / kernel failure         */
+  RAPDHG_E_NO_DEVICE = -4,        /* no CUDA device: there is no fallback  */
+  RAPDHG_E_PARSE = -5,            /* QpsParseError (qps.hpp:30)            */
+  RAPDHG_E_INTERNAL = -6
+};
+
+/* ---- enums: values equal the reference enum order (solver.hpp:22-26) --- */
+enum { RAPDHG_ALG_PDHG = 0, RAPDHG_ALG_APDHG = 1 };
+enum {
+  RAPDHG_RESTART_NONE = 0,
+  RAPDHG_RESTART_FIXED = 1,
+  RAPDHG_RESTART_HALVING = 2,
+  RAPDHG_RESTART_PDQP = 3
+};
+enum { RAPDHG_STEP_THEORETICAL = 0, RAPDHG_STEP_ADAPTIVE = 1 };
+enum { RAPDHG_PW_FIXED = 0, RAPDHG_PW_ADAPTIVE = 1 };
+enum {
+  RAPDHG_STATUS_OPTIMAL = 0,
+  RAPDHG_STATUS_ITERATION_LIMIT = 1,
+  RAPDHG_STATUS_TIME_LIMIT = 2,
+  RAPDHG_STATUS_NUMERICAL_ERROR = 3
+};
+
+/* ---- problem ----------------------------------------------------------- */
+
+/* Compressed sparse row matrix. Replaces rapdhg::SparseMatrix
+ * (sparse.hpp:27-170), whose private storage is exactly this triple
+ * (sparse.hpp:165-169: int row_start_, int cols_, double values_). Input
+ * must be canonical as the reference constructor makes it (sparse.hpp:31-62):
+ * columns strictly increasing within a row, no explicit zeros. Use
+ * rapdhg_csr_from_triplets() to canonicalize raw triplets. */
+typedef struct {
+  int32_t n_rows;
+  int32_t n_cols;
+  int64_t nnz;
+  const int32_t* row_ptr; /* n_rows + 1 */
+  const int32_t* col_idx; /* nnz */
+  const double* values;   /* nnz */
+} rapdhg_csr;
+
+/* Canonical convex QP  min ½x'Qx + c'x  s.t. A_ineq x <= b_ineq, A_eq x = b_eq.
+ * Replaces rapdhg::QuadraticProgram (problem.hpp:24-56). Sizes are implied
+ * as in the reference: n = len(c) (num_vars), m_ineq = len(b_ineq), m_eq =
+ * len(b_eq) (problem.hpp:35-38). */
+typedef struct {
+  int32_t n;
+  int32_t m_ineq;
+  int32_t m_eq;
+  rapdhg_csr q;      /* n x n, symmetric, full (both triangles) storage */
+  const double* c;   /* n */
+  rapdhg_csr a_ineq; /* m_ineq x n */
+  const double* b_ineq;
+  rapdhg_csr a_eq;   /* m_eq x n */
+  const double* b_eq;
+  double obj_offset;
+} rapdhg_qp;
+
+/* ---- options ----------------------------------------------------------- */
+
+/* Mirrors rapdhg::SolverConfig field by field (solver.hpp:38-55) plus the
+ * B200 fields at the end. rapdhg_config_default() fills the reference
+ * defaults (APDHG, PDQP restart, adaptive step, adaptive omega, tol 1e-3,
+ * 200000 iterations, check every 40, scaling on, seed 1). */
+typedef struct {
+  int32_t algorithm;
+  int32_t restart;
+  int64_t restart_length;
+  int32_t step_rule;
+  int32_t primal_weight;
+  double fixed_primal_weight;
+  double tol;
+  int64_t max_iters;
+  double time_limit_s; /* +inf = none */
+  int32_t check_interval;
+  int32_t scaling;
+  uint64_t seed;
+  int64_t snapshot_interval;
+  int32_t record_restart_points;
+  /* --- B200 extensions --- */
+  int32_t device;        /* CUDA ordinal */
+  int32_t strict_parity; /* 1: sequential fp64 sums, no FMA -> bit-exact with
+                            the reference; 0: fast deterministic kernels */
+  int32_t use_graphs;    /* capture each check interval in a CUDA graph */
+  int32_t profile_kernels; /* record CUDA events around every hot kernel */
+} rapdhg_config;
+
+void rapdhg_config_default(rapdhg_config* cfg);
+
+/* ---- results ----------------------------------------------------------- */
+
+typedef struct { /* rapdhg::KktResiduals (kkt.hpp:11-17) */
+  double r_primal;
+  double r_dual;
+  double r_gap;
+} rapdhg_kkt;
+
+typedef struct { /* rapdhg::LogRecord (solver.hpp:66-74) */
+  int64_t iteration;
+  double r_primal;
+  double r_dual;
+  double r_gap;
+  double eta;
+  double omega;
+  int32_t restarted;
+} rapdhg_log_record;
+
+/* rapdhg::SolveResult (solver.hpp:76-89). Arrays are allocated by the library
+ * and released by rapdhg_result_free(). snapshots are stored row-major:
+ * snapshot s has x at snapshot_x + s*n and y (ineq then eq) at
+ * snapshot_y + s*(m_ineq+m_eq); restart points likewise. */
+typedef struct {
+  int32_t status;
+  int32_t n, m_ineq, m_eq;
+  double* x;      /* n       */
+  double* y_ineq; /* m_ineq  */
+  double* y_eq;   /* m_eq    */
+  rapdhg_kkt residuals;
+  int64_t iterations;
+  int64_t restarts;
+  double solve_seconds;
+  double norm_q;
+  double norm_a;
+  int32_t norm_fallback;
+  int64_t n_log;
+  rapdhg_log_record* log;
+  int64_t n_snapshots;
+  int64_t* snapshot_iters;
+  double* snapshot_x;
+  double* snapshot_y;
+  int64_t n_restart_points;
+  double* restart_x;
+  double* restart_y;
+  /* --- B200 instrumentation --- */
+  double setup_seconds;     /* upload + validate + scaling + norms */
+  double loop_seconds;      /* iterations + checks, device time    */
+  int64_t kernel_launches;  /* library kernels launched by this call */
+  /* profile_kernels=1: summed CUDA-event time (ms) and launch counts of the
+   * two hot kernels (0 = dual step A*w, 1 = primal step [Q|A']) */
+  double kernel_ms[2];
+  int64_t kernel_count[2];
+} rapdhg_result;
+
+void rapdhg_result_free(rapdhg_result* r);
+
+/* Thread-local message of the last failing call on this thread. */
+const char* rapdhg_last_error(void);
+int rapdhg_abi_version(void);
+/* Number of visible CUDA devices (0 on a CPU-only host). */
+int rapdhg_device_count(void);
+
+/* ---- main entry: rapdhg::solve (solver.hpp:272-471) -------------------- */
+int rapdhg_solve(const rapdhg_qp* qp, const rapdhg_config* cfg, rapdhg_result* out);
+
+/* Resident-data variant: upload + validate + scaling + norms once
+ * (solver.hpp:277-300), then solve repeatedly from the zero start on the
+ * HBM-resident problem. Used to time the iteration loop with inputs already
+ * in HBM. */
+typedef struct rapdhg_session rapdhg_session;
+int rapdhg_session_create(const rapdhg_qp* qp, const rapdhg_config* cfg, rapdhg_session** out);
+int rapdhg_session_solve(rapdhg_session* s, rapdhg_result* out);
+/* Algorithmic bytes of one iteration (SURVEY §8(d) B_iter) and of one launch
+ * of each hot kernel, for the roofline. */
+int rapdhg_session_bytes(const rapdhg_session* s, double* b_iter, double* b_dual,
+                         double* b_primal);
+void rapdhg_session_destroy(rapdhg_session* s);
+
+/* ---- secondary API used by the reference's tests ----------------------- */
+
+/* y = M x (sparse.hpp:79-88) and y = M' x (sparse.hpp:91-100). */
+int rapdhg_spmv(const rapdhg_csr* m, const double* x, int64_t x_len, double* y, int32_t strict);
+int rapdhg_spmv_t(const rapdhg_csr* m, const double* x, int64_t x_len, double* y, int32_t strict);
+
+/* rapdhg::StepParams (stepsize.hpp:13-18). */
+typedef struct {
+  double beta;
+  double theta;
+  double eta;
+  double tau;
+} rapdhg_step_params;
+
+/* rapdhg::IterateState (solver.hpp:125-143): x, x_prev, x_bar (n) and y,
+ * y_bar (m = m_ineq + m_eq, ineq first), updated in place. */
+typedef struct {
+  double* x;
+  double* x_prev;
+  double* y;
+  double* x_bar;
+  double* y_bar;
+  int64_t k;
+  int64_t n;
+} rapdhg_iterate;
+
+/* rapdhg::inner_step(s, p, sp) (solver.hpp:156-191): one unified PDHG/APDHG
+ * iteration on the (already scaled, if desired) problem, `steps` times with
+ * the same parameters. */
+int rapdhg_inner_step(const rapdhg_qp* p, rapdhg_iterate* s, const rapdhg_step_params* sp,
+                      int32_t steps, int32_t strict);
+/* rapdhg::pdhg_step (solver.hpp:195-203) */
+int rapdhg_pdhg_step(const rapdhg_qp* p, rapdhg_iterate* s, double eta, double tau,
+                     int32_t strict);
+
+/* rapdhg::rel_kkt (kkt.hpp:28-72). */
+int rapdhg_rel_kkt(const rapdhg_qp* p, const double* x, const double* y_ineq,
+                   const double* y_eq, rapdhg_kkt* out, int32_t strict);
+
+/* rapdhg::compute_scaling (scaling.hpp:171-180): d1 (m), d2 (n). */
+int rapdhg_compute_scaling(const rapdhg_qp* p, double* d1, double* d2, int32_t strict);
+/* rapdhg::ruiz_scaling (scaling.hpp:159-166) */
+int rapdhg_ruiz_scaling(const rapdhg_qp* p, int32_t iterations, double* d1, double* d2,
+                        int32_t strict);
+/* rapdhg::apply_scaling (scaling.hpp:183-197): writes the scaled values into
+ * caller buffers laid out like the input CSRs (same patterns). */
+int rapdhg_apply_scaling(const rapdhg_qp* p, const double* d1, const double* d2,
+                         double* q_values, double* a_ineq_values, double* a_eq_values,
+                         double* c, double* b_ineq, double* b_eq);
+
+/* rapdhg::estimate_op_norm / _symmetric (opnorm.hpp:36-87) with
+ * PowerIterOptions{max_iters, tol, seed} (opnorm.hpp:12-16). */
+int rapdhg_estimate_op_norm(const rapdhg_csr* m, int32_t max_iters, double tol, uint64_t seed,
+                            double* out, int32_t strict);
+int rapdhg_estimate_op_norm_symmetric(const rapdhg_csr* m, int32_t max_iters, double tol,
+                                      uint64_t seed, double* out, int32_t strict);
+
+/* ---- host scalar rules (stepsize.hpp, solver.hpp:218-235) ------------- */
+int rapdhg_step_schedule_theoretical(int32_t k, int32_t horizon, double norm_q, double norm_a,
+                                     rapdhg_step_params* out);
+int rapdhg_pdhg_constant_steps(double norm_q, double norm_a, rapdhg_step_params* out);
+int rapdhg_adaptive_eta(int32_t k, double prev_eta, double norm_q, double norm_a, double omega,
+                        double* out);
+int rapdhg_primal_weight_update(double delta_x, double delta_y, double omega_prev, double* out);
+/* RestartContext (solver.hpp:206-212) flattened. Returns 0/1, or <0 on error. */
+int rapdhg_restart_decision(int32_t policy, double relkkt_candidate, double relkkt_candidate_prev,
+                            double relkkt_epoch_start, int64_t k, int64_t total_iters,
+                            int64_t fixed_length);
+
+/* ---- host utilities ---------------------------------------------------- */
+
+/* Owned CSR / QP containers returned by the generators and converters. */
+typedef struct {
+  int32_t n_rows, n_cols;
+  int64_t nnz;
+  int32_t* row_ptr;
+  int32_t* col_idx;
+  double* values;
+} rapdhg_csr_owned;
+
+typedef struct {
+  int32_t n, m_ineq, m_eq;
+  rapdhg_csr_owned q, a_ineq, a_eq;
+  double* c;
+  double* b_ineq;
+  double* b_eq;
+  double obj_offset;
+} rapdhg_qp_owned;
+
+/* SparseMatrix(n_rows, n_cols, triplets) (sparse.hpp:31-62): sort by
+ * (row, col), sum duplicates, drop exact zeros. */
+int rapdhg_csr_from_triplets(int32_t n_rows, int32_t n_cols, int64_t nnz, const int32_t* rows,
+                             const int32_t* cols, const double* vals, rapdhg_csr_owned* out);
+void rapdhg_csr_free(rapdhg_csr_owned* m);
+void rapdhg_qp_free(rapdhg_qp_owned* p);
+/* Borrowed view of an owned QP, for passing to the compute entry points. */
+void rapdhg_qp_view(const rapdhg_qp_owned* p, rapdhg_qp* view);
+
+/* Synthetic instances of SURVEY §8(d) (no reference generator ships;
+ * SPEC.md:417-489 describes the classes). scale multiplies the headline
+ * sizes (1.0 = the BASELINE config). Deterministic in seed. */
+enum {
+  RAPDHG_GEN_RANDOM_QP = 1, /* C1: SPEC.md:431 random QP */
+  RAPDHG_GEN_LASSO = 2,     /* C2 */
+  RAPDHG_GEN_PORTFOLIO = 3, /* C3: Markowitz factor model */
+  RAPDHG_GEN_SVM = 4,       /* C4 */
+  RAPDHG_GEN_LARGE = 5,     /* C5: uniform columns */
+  RAPDHG_GEN_LARGE_LOCAL = 6 /* C5-L: 95% block-local columns */
+};
+int rapdhg_generate(int32_t kind, double scale, uint64_t seed, rapdhg_qp_owned* out);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* RAPDHG_B200_H_ */

@@ -1,0 +1,742 @@
+"""B200-native rAPDHG (PDQP, arXiv 2311.07710) — Python host mirror.
+
+Mirrors the reference C++ API of /root/reference/proj/include/rapdhg/
+(same names, argument meaning and error behaviour) over the C-ABI of
+include/rapdhg_b200.h, implemented by the fp64 sm_100a kernels in
+``librapdhg_b200.so``:
+
+====================================  =======================================
+reference (file:line)                 here
+====================================  =======================================
+SparseMatrix (sparse.hpp:27-170)      SparseMatrix (canonical CSR, numpy)
+QuadraticProgram (problem.hpp:24-56)  QuadraticProgram
+SolverConfig (solver.hpp:38-64)       SolverConfig
+solve (solver.hpp:272-471)            solve -> SolveResult
+inner_step / pdhg_step (:182-203)     inner_step / pdhg_step
+rel_kkt (kkt.hpp:28-72)               rel_kkt -> KktResiduals
+compute_scaling etc. (scaling.hpp)    compute_scaling, ruiz_scaling,
+                                      apply_scaling, unscale_point
+estimate_op_norm(_symmetric)          estimate_op_norm(_symmetric)
+stepsize.hpp scalar rules             step_schedule_theoretical, ...
+====================================  =======================================
+
+Errors: std::invalid_argument -> InvalidArgument (a ValueError),
+std::out_of_range -> IndexError, no CUDA device -> NoDeviceError. There is no
+CPU fallback: compute calls raise NoDeviceError on a host without a GPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import abi
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librapdhg_b200.so")
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument of the reference."""
+
+
+class NoDeviceError(RuntimeError):
+    """No CUDA device visible: the solver has no CPU fallback."""
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+class QpsParseError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def _load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `make -C paper_2311_07710_b200` "
+            "(or __graft_entry__.build()); there is no fallback implementation")
+    lib = C.CDLL(LIB_PATH)
+    d = abi.declare
+    P = C.POINTER
+    d(lib, "rapdhg_last_error", C.c_char_p)
+    d(lib, "rapdhg_abi_version", C.c_int)
+    d(lib, "rapdhg_device_count", C.c_int)
+    d(lib, "rapdhg_config_default", None, P(abi.Config))
+    d(lib, "rapdhg_result_free", None, P(abi.Result))
+    d(lib, "rapdhg_solve", C.c_int, P(abi.Qp), P(abi.Config), P(abi.Result))
+    d(lib, "rapdhg_session_create", C.c_int, P(abi.Qp), P(abi.Config), P(C.c_void_p))
+    d(lib, "rapdhg_session_solve", C.c_int, C.c_void_p, P(abi.Result))
+    d(lib, "rapdhg_session_bytes", C.c_int, C.c_void_p, P(C.c_double), P(C.c_double), P(C.c_double))
+    d(lib, "rapdhg_session_destroy", None, C.c_void_p)
+    d(lib, "rapdhg_spmv", C.c_int, P(abi.Csr), abi.P_f64, C.c_int64, abi.P_f64, C.c_int32)
+    d(lib, "rapdhg_spmv_t", C.c_int, P(abi.Csr), abi.P_f64, C.c_int64, abi.P_f64, C.c_int32)
+    d(lib, "rapdhg_inner_step", C.c_int, P(abi.Qp), P(abi.Iterate), P(abi.StepParams), C.c_int32, C.c_int32)
+    d(lib, "rapdhg_pdhg_step", C.c_int, P(abi.Qp), P(abi.Iterate), C.c_double, C.c_double, C.c_int32)
+    d(lib, "rapdhg_rel_kkt", C.c_int, P(abi.Qp), abi.P_f64, abi.P_f64, abi.P_f64, P(abi.Kkt), C.c_int32)
+    d(lib, "rapdhg_compute_scaling", C.c_int, P(abi.Qp), abi.P_f64, abi.P_f64, C.c_int32)
+    d(lib, "rapdhg_ruiz_scaling", C.c_int, P(abi.Qp), C.c_int32, abi.P_f64, abi.P_f64, C.c_int32)
+    d(lib, "rapdhg_apply_scaling", C.c_int, P(abi.Qp), abi.P_f64, abi.P_f64, abi.P_f64, abi.P_f64,
+      abi.P_f64, abi.P_f64, abi.P_f64, abi.P_f64)
+    d(lib, "rapdhg_estimate_op_norm", C.c_int, P(abi.Csr), C.c_int32, C.c_double, C.c_uint64,
+      abi.P_f64, C.c_int32)
+    d(lib, "rapdhg_estimate_op_norm_symmetric", C.c_int, P(abi.Csr), C.c_int32, C.c_double,
+      C.c_uint64, abi.P_f64, C.c_int32)
+    d(lib, "rapdhg_step_schedule_theoretical", C.c_int, C.c_int32, C.c_int32, C.c_double,
+      C.c_double, P(abi.StepParams))
+    d(lib, "rapdhg_pdhg_constant_steps", C.c_int, C.c_double, C.c_double, P(abi.StepParams))
+    d(lib, "rapdhg_adaptive_eta", C.c_int, C.c_int32, C.c_double, C.c_double, C.c_double,
+      C.c_double, abi.P_f64)
+    d(lib, "rapdhg_primal_weight_update", C.c_int, C.c_double, C.c_double, C.c_double, abi.P_f64)
+    d(lib, "rapdhg_restart_decision", C.c_int, C.c_int32, C.c_double, C.c_double, C.c_double,
+      C.c_int64, C.c_int64, C.c_int64)
+    d(lib, "rapdhg_csr_from_triplets", C.c_int, C.c_int32, C.c_int32, C.c_int64, abi.P_i32,
+      abi.P_i32, abi.P_f64, P(abi.CsrOwned))
+    d(lib, "rapdhg_csr_free", None, P(abi.CsrOwned))
+    d(lib, "rapdhg_qp_free", None, P(abi.QpOwned))
+    d(lib, "rapdhg_qp_view", None, P(abi.QpOwned), P(abi.Qp))
+    d(lib, "rapdhg_generate", C.c_int, C.c_int32, C.c_double, C.c_uint64, P(abi.QpOwned))
+    if lib.rapdhg_abi_version() != 1:
+        raise ImportError("librapdhg_b200.so ABI version mismatch")
+    _lib = lib
+    return lib
+
+
+def lib():
+    """The loaded C-ABI library (ctypes.CDLL)."""
+    return _load()
+
+
+def _check(rc: int):
+    if rc >= 0:
+        return rc
+    msg = _load().rapdhg_last_error().decode()
+    if rc == abi.E_INVALID_ARGUMENT:
+        raise InvalidArgument(msg)
+    if rc == abi.E_OUT_OF_RANGE:
+        raise IndexError(msg)
+    if rc == abi.E_NO_DEVICE:
+        raise NoDeviceError(msg)
+    if rc == abi.E_CUDA:
+        raise CudaError(msg)
+    if rc == abi.E_PARSE:
+        raise QpsParseError(msg)
+    raise RuntimeError(msg)
+
+
+def device_count() -> int:
+    return _load().rapdhg_device_count()
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _i32(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+def _pf(a: np.ndarray):
+    return a.ctypes.data_as(abi.P_f64)
+
+
+def _pi(a: np.ndarray):
+    return a.ctypes.data_as(abi.P_i32)
+
+
+# --------------------------------------------------------------------------
+# model types
+# --------------------------------------------------------------------------
+
+class SparseMatrix:
+    """Canonical CSR: rows sorted, no duplicates, no explicit zeros
+    (sparse.hpp:27-62). Storage: int32 row_ptr/col_idx, fp64 values."""
+
+    def __init__(self, n_rows: int, n_cols: int, triplets: Sequence[Tuple[int, int, float]] = ()):
+        if triplets is None:
+            triplets = ()
+        t = list(triplets)
+        r = _i32([e[0] for e in t]) if t else np.zeros(0, np.int32)
+        c = _i32([e[1] for e in t]) if t else np.zeros(0, np.int32)
+        v = _f64([e[2] for e in t]) if t else np.zeros(0, np.float64)
+        self._from_coo(int(n_rows), int(n_cols), r, c, v)
+
+    def _from_coo(self, n_rows, n_cols, r, c, v):
+        out = abi.CsrOwned()
+        L = _load()
+        _check(L.rapdhg_csr_from_triplets(n_rows, n_cols, len(v), _pi(r), _pi(c), _pf(v), C.byref(out)))
+        try:
+            self.n_rows, self.n_cols = n_rows, n_cols
+            nnz = int(out.nnz)
+            self.row_ptr = np.ctypeslib.as_array(out.row_ptr, (n_rows + 1,)).copy()
+            self.col_idx = (np.ctypeslib.as_array(out.col_idx, (nnz,)).copy() if nnz else np.zeros(0, np.int32))
+            self.values = (np.ctypeslib.as_array(out.values, (nnz,)).copy() if nnz else np.zeros(0, np.float64))
+        finally:
+            L.rapdhg_csr_free(C.byref(out))
+
+    @classmethod
+    def from_coo(cls, n_rows, n_cols, rows, cols, vals) -> "SparseMatrix":
+        m = cls.__new__(cls)
+        m._from_coo(int(n_rows), int(n_cols), _i32(rows), _i32(cols), _f64(vals))
+        return m
+
+    @classmethod
+    def from_csr(cls, n_rows, n_cols, row_ptr, col_idx, values) -> "SparseMatrix":
+        """Adopt arrays that are already canonical (not re-checked here; the
+        solver validates ordering and ranges)."""
+        m = cls.__new__(cls)
+        m.n_rows, m.n_cols = int(n_rows), int(n_cols)
+        m.row_ptr, m.col_idx, m.values = _i32(row_ptr), _i32(col_idx), _f64(values)
+        return m
+
+    @classmethod
+    def identity(cls, n: int) -> "SparseMatrix":
+        return cls.from_csr(n, n, np.arange(n + 1), np.arange(n), np.ones(n))
+
+    @classmethod
+    def zero(cls, n_rows: int, n_cols: int) -> "SparseMatrix":
+        return cls.from_csr(n_rows, n_cols, np.zeros(n_rows + 1), np.zeros(0), np.zeros(0))
+
+    def rows(self) -> int:
+        return self.n_rows
+
+    def cols(self) -> int:
+        return self.n_cols
+
+    def nnz(self) -> int:
+        return int(len(self.values))
+
+    def empty(self) -> bool:
+        return self.nnz() == 0
+
+    def _csr(self) -> abi.Csr:
+        return abi.Csr(self.n_rows, self.n_cols, self.nnz(), _pi(self.row_ptr), _pi(self.col_idx),
+                       _pf(self.values))
+
+    def multiply(self, x, strict: bool = False) -> np.ndarray:
+        """y = M x on the GPU (sparse.hpp:79-88)."""
+        x = _f64(x)
+        y = np.empty(self.n_rows, np.float64)
+        m = self._csr()
+        _check(_load().rapdhg_spmv(C.byref(m), _pf(x), len(x), _pf(y), int(strict)))
+        return y
+
+    def multiply_transpose(self, x, strict: bool = False) -> np.ndarray:
+        """y = M' x on the GPU (sparse.hpp:91-100)."""
+        x = _f64(x)
+        y = np.empty(self.n_cols, np.float64)
+        m = self._csr()
+        _check(_load().rapdhg_spmv_t(C.byref(m), _pf(x), len(x), _pf(y), int(strict)))
+        return y
+
+    def to_dense(self) -> np.ndarray:
+        d = np.zeros((self.n_rows, self.n_cols))
+        for r in range(self.n_rows):
+            s, e = self.row_ptr[r], self.row_ptr[r + 1]
+            d[r, self.col_idx[s:e]] = self.values[s:e]
+        return d
+
+
+def spmv(m: SparseMatrix, x, strict: bool = False) -> np.ndarray:
+    return m.multiply(x, strict)
+
+
+def spmv_t(m: SparseMatrix, x, strict: bool = False) -> np.ndarray:
+    return m.multiply_transpose(x, strict)
+
+
+@dataclass
+class QuadraticProgram:
+    """min ½x'Qx + c'x + obj_offset  s.t. A_ineq x <= b_ineq, A_eq x = b_eq
+    (problem.hpp:24-56)."""
+    q: SparseMatrix
+    c: np.ndarray
+    a_ineq: SparseMatrix
+    b_ineq: np.ndarray
+    a_eq: SparseMatrix
+    b_eq: np.ndarray
+    name: str = ""
+    obj_offset: float = 0.0
+    var_names: List[str] = field(default_factory=list)
+
+    def num_vars(self) -> int:
+        return len(self.c)
+
+    def num_ineq(self) -> int:
+        return len(self.b_ineq)
+
+    def num_eq(self) -> int:
+        return len(self.b_eq)
+
+    def num_rows(self) -> int:
+        return self.num_ineq() + self.num_eq()
+
+    def objective(self, x) -> float:
+        x = _f64(x)
+        qx = self.q.to_dense() @ x if self.q.nnz() < 4_000_000 else self.q.multiply(x)
+        return 0.5 * float(x @ qx) + float(self.c @ x) + self.obj_offset
+
+    def _struct(self) -> abi.Qp:
+        self.c, self.b_ineq, self.b_eq = _f64(self.c), _f64(self.b_ineq), _f64(self.b_eq)
+        return abi.Qp(len(self.c), len(self.b_ineq), len(self.b_eq), self.q._csr(), _pf(self.c),
+                      self.a_ineq._csr(), _pf(self.b_ineq), self.a_eq._csr(), _pf(self.b_eq),
+                      float(self.obj_offset))
+
+
+@dataclass
+class PrimalDualPoint:
+    x: np.ndarray
+    y_ineq: np.ndarray
+    y_eq: np.ndarray
+
+    @staticmethod
+    def zeros(p: QuadraticProgram) -> "PrimalDualPoint":
+        return PrimalDualPoint(np.zeros(p.num_vars()), np.zeros(p.num_ineq()), np.zeros(p.num_eq()))
+
+
+class Algorithm(enum.IntEnum):
+    kPdhg = 0
+    kApdhg = 1
+
+
+class RestartPolicy(enum.IntEnum):
+    kNone = 0
+    kFixed = 1
+    kAdaptiveHalving = 2
+    kPdqpAdaptive = 3
+
+
+class StepRule(enum.IntEnum):
+    kTheoretical = 0
+    kAdaptive = 1
+
+
+class PrimalWeightMode(enum.IntEnum):
+    kFixed = 0
+    kAdaptive = 1
+
+
+class SolveStatus(enum.IntEnum):
+    kOptimal = 0
+    kIterationLimit = 1
+    kTimeLimit = 2
+    kNumericalError = 3
+
+
+def to_string(s: SolveStatus) -> str:
+    return {0: "optimal", 1: "iteration_limit", 2: "time_limit", 3: "numerical_error"}.get(int(s), "unknown")
+
+
+@dataclass
+class SolverConfig:
+    """solver.hpp:38-55 plus the B200 fields."""
+    algorithm: Algorithm = Algorithm.kApdhg
+    restart: RestartPolicy = RestartPolicy.kPdqpAdaptive
+    restart_length: int = 0
+    step_rule: StepRule = StepRule.kAdaptive
+    primal_weight: PrimalWeightMode = PrimalWeightMode.kAdaptive
+    fixed_primal_weight: float = 1.0
+    tol: float = 1e-3
+    max_iters: int = 200000
+    time_limit_s: float = math.inf
+    check_interval: int = 40
+    scaling: bool = True
+    seed: int = 1
+    snapshot_interval: int = 0
+    record_restart_points: bool = False
+    # B200
+    device: int = 0
+    strict_parity: bool = False
+    use_graphs: bool = True
+    profile_kernels: bool = False
+
+    def _struct(self) -> abi.Config:
+        c = abi.Config()
+        c.algorithm, c.restart = int(self.algorithm), int(self.restart)
+        c.restart_length, c.step_rule = int(self.restart_length), int(self.step_rule)
+        c.primal_weight, c.fixed_primal_weight = int(self.primal_weight), float(self.fixed_primal_weight)
+        c.tol, c.max_iters, c.time_limit_s = float(self.tol), int(self.max_iters), float(self.time_limit_s)
+        c.check_interval, c.scaling, c.seed = int(self.check_interval), int(bool(self.scaling)), int(self.seed)
+        c.snapshot_interval = int(self.snapshot_interval)
+        c.record_restart_points = int(bool(self.record_restart_points))
+        c.device, c.strict_parity = int(self.device), int(bool(self.strict_parity))
+        c.use_graphs, c.profile_kernels = int(bool(self.use_graphs)), int(bool(self.profile_kernels))
+        return c
+
+
+@dataclass
+class KktResiduals:
+    r_primal: float = 0.0
+    r_dual: float = 0.0
+    r_gap: float = 0.0
+
+    def relkkt(self) -> float:
+        return max(self.r_primal, self.r_dual, self.r_gap)
+
+
+@dataclass
+class LogRecord:
+    iteration: int
+    r_primal: float
+    r_dual: float
+    r_gap: float
+    eta: float
+    omega: float
+    restarted: bool
+
+
+@dataclass
+class SolveResult:
+    status: SolveStatus
+    point: PrimalDualPoint
+    residuals: KktResiduals
+    iterations: int
+    restarts: int
+    solve_seconds: float
+    norm_q: float
+    norm_a: float
+    norm_fallback: bool
+    log: List[LogRecord]
+    snapshots: List[Tuple[int, PrimalDualPoint]]
+    restart_points: List[PrimalDualPoint]
+    # B200 instrumentation
+    setup_seconds: float = 0.0
+    loop_seconds: float = 0.0
+    kernel_launches: int = 0
+    kernel_ms: Tuple[float, float] = (0.0, 0.0)
+    kernel_count: Tuple[int, int] = (0, 0)
+
+
+def _arr(p, n) -> np.ndarray:
+    if n <= 0:
+        return np.zeros(0, np.float64)
+    return np.ctypeslib.as_array(p, (n,)).copy()
+
+
+def result_from_struct(r: abi.Result) -> SolveResult:
+    """Convert (and copy out of) a C result struct; the caller frees it."""
+    n, mi, me = r.n, r.m_ineq, r.m_eq
+    m = mi + me
+    point = PrimalDualPoint(_arr(r.x, n), _arr(r.y_ineq, mi), _arr(r.y_eq, me))
+    log = [LogRecord(int(L.iteration), L.r_primal, L.r_dual, L.r_gap, L.eta, L.omega, bool(L.restarted))
+           for L in (r.log[i] for i in range(r.n_log))]
+    snaps = []
+    for s in range(r.n_snapshots):
+        xs = np.ctypeslib.as_array(r.snapshot_x, ((s + 1) * n + 1,))[s * n:(s + 1) * n].copy() if n else np.zeros(0)
+        ys = np.ctypeslib.as_array(r.snapshot_y, ((s + 1) * m + 1,))[s * m:(s + 1) * m].copy() if m else np.zeros(0)
+        snaps.append((int(r.snapshot_iters[s]), PrimalDualPoint(xs, ys[:mi], ys[mi:])))
+    rps = []
+    for s in range(r.n_restart_points):
+        xs = np.ctypeslib.as_array(r.restart_x, ((s + 1) * n + 1,))[s * n:(s + 1) * n].copy() if n else np.zeros(0)
+        ys = np.ctypeslib.as_array(r.restart_y, ((s + 1) * m + 1,))[s * m:(s + 1) * m].copy() if m else np.zeros(0)
+        rps.append(PrimalDualPoint(xs, ys[:mi], ys[mi:]))
+    return SolveResult(SolveStatus(r.status), point,
+                       KktResiduals(r.residuals.r_primal, r.residuals.r_dual, r.residuals.r_gap),
+                       int(r.iterations), int(r.restarts), r.solve_seconds, r.norm_q, r.norm_a,
+                       bool(r.norm_fallback), log, snaps, rps, r.setup_seconds, r.loop_seconds,
+                       int(r.kernel_launches), (r.kernel_ms[0], r.kernel_ms[1]),
+                       (int(r.kernel_count[0]), int(r.kernel_count[1])))
+
+
+# --------------------------------------------------------------------------
+# solver entry points
+# --------------------------------------------------------------------------
+
+def solve(original: QuadraticProgram, cfg: Optional[SolverConfig] = None) -> SolveResult:
+    """rapdhg::solve (solver.hpp:272-471) on the GPU."""
+    cfg = cfg or SolverConfig()
+    L = _load()
+    qp = original._struct()
+    cs = cfg._struct()
+    out = abi.Result()
+    _check(L.rapdhg_solve(C.byref(qp), C.byref(cs), C.byref(out)))
+    try:
+        return result_from_struct(out)
+    finally:
+        L.rapdhg_result_free(C.byref(out))
+
+
+class Session:
+    """Problem uploaded and preprocessed once (validate, scaling, norms), then
+    solved from the zero start as often as wanted on HBM-resident data."""
+
+    def __init__(self, original: QuadraticProgram, cfg: Optional[SolverConfig] = None):
+        self.cfg = cfg or SolverConfig()
+        self._qp = original
+        L = _load()
+        h = C.c_void_p()
+        qp = original._struct()
+        cs = self.cfg._struct()
+        _check(L.rapdhg_session_create(C.byref(qp), C.byref(cs), C.byref(h)))
+        self._h = h
+
+    def solve(self) -> SolveResult:
+        L = _load()
+        out = abi.Result()
+        _check(L.rapdhg_session_solve(self._h, C.byref(out)))
+        try:
+            return result_from_struct(out)
+        finally:
+            L.rapdhg_result_free(C.byref(out))
+
+    def bytes(self) -> Tuple[float, float, float]:
+        """(B_iter, bytes of one dual-step launch, bytes of one primal-step launch)."""
+        a, b, c = C.c_double(), C.c_double(), C.c_double()
+        _check(_load().rapdhg_session_bytes(self._h, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _load().rapdhg_session_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+@dataclass
+class StepParams:
+    beta: float = 1.0
+    theta: float = 1.0
+    eta: float = 0.0
+    tau: float = 0.0
+
+
+@dataclass
+class IterateState:
+    """solver.hpp:125-143; y stacks [y_ineq | y_eq]."""
+    x: np.ndarray
+    x_prev: np.ndarray
+    y: np.ndarray
+    x_bar: np.ndarray
+    y_bar: np.ndarray
+    k: int = 0
+    n: int = 0
+
+    @staticmethod
+    def zeros(num_vars: int, num_rows: int) -> "IterateState":
+        return IterateState(np.zeros(num_vars), np.zeros(num_vars), np.zeros(num_rows),
+                            np.zeros(num_vars), np.zeros(num_rows))
+
+    def copy(self) -> "IterateState":
+        return IterateState(self.x.copy(), self.x_prev.copy(), self.y.copy(), self.x_bar.copy(),
+                            self.y_bar.copy(), self.k, self.n)
+
+
+def inner_step(s: IterateState, p: QuadraticProgram, sp: StepParams, steps: int = 1,
+               strict: bool = False) -> IterateState:
+    """rapdhg::inner_step(s, p, sp) (solver.hpp:156-191), `steps` times."""
+    o = s.copy()
+    for name in ("x", "x_prev", "y", "x_bar", "y_bar"):
+        setattr(o, name, _f64(getattr(o, name)).copy())
+    it = abi.Iterate(_pf(o.x), _pf(o.x_prev), _pf(o.y), _pf(o.x_bar), _pf(o.y_bar), o.k, o.n)
+    qp = p._struct()
+    spc = abi.StepParams(sp.beta, sp.theta, sp.eta, sp.tau)
+    _check(_load().rapdhg_inner_step(C.byref(qp), C.byref(it), C.byref(spc), int(steps), int(strict)))
+    o.k, o.n = int(it.k), int(it.n)
+    return o
+
+
+def pdhg_step(s: IterateState, p: QuadraticProgram, eta: float, tau: float,
+              strict: bool = False) -> IterateState:
+    """rapdhg::pdhg_step (solver.hpp:195-203): beta = theta = 1."""
+    return inner_step(s, p, StepParams(1.0, 1.0, eta, tau), 1, strict)
+
+
+def rel_kkt(p: QuadraticProgram, z: PrimalDualPoint, strict: bool = False) -> KktResiduals:
+    """rapdhg::rel_kkt (kkt.hpp:28-72) on the GPU."""
+    x, yi, ye = _f64(z.x), _f64(z.y_ineq), _f64(z.y_eq)
+    out = abi.Kkt()
+    qp = p._struct()
+    _check(_load().rapdhg_rel_kkt(C.byref(qp), _pf(x), _pf(yi), _pf(ye), C.byref(out), int(strict)))
+    return KktResiduals(out.r_primal, out.r_dual, out.r_gap)
+
+
+@dataclass
+class ScalingInfo:
+    d1: np.ndarray  # m dual factors
+    d2: np.ndarray  # n primal factors
+
+    @staticmethod
+    def identity(p: QuadraticProgram) -> "ScalingInfo":
+        return ScalingInfo(np.ones(p.num_rows()), np.ones(p.num_vars()))
+
+
+def compute_scaling(p: QuadraticProgram, strict: bool = False) -> ScalingInfo:
+    """scaling.hpp:171-180 on the GPU."""
+    d1, d2 = np.empty(p.num_rows()), np.empty(p.num_vars())
+    qp = p._struct()
+    _check(_load().rapdhg_compute_scaling(C.byref(qp), _pf(d1), _pf(d2), int(strict)))
+    return ScalingInfo(d1, d2)
+
+
+def ruiz_scaling(p: QuadraticProgram, iterations: int, strict: bool = False) -> ScalingInfo:
+    """scaling.hpp:159-166 on the GPU."""
+    d1, d2 = np.empty(p.num_rows()), np.empty(p.num_vars())
+    qp = p._struct()
+    _check(_load().rapdhg_ruiz_scaling(C.byref(qp), int(iterations), _pf(d1), _pf(d2), int(strict)))
+    return ScalingInfo(d1, d2)
+
+
+def apply_scaling(p: QuadraticProgram, s: ScalingInfo) -> QuadraticProgram:
+    """scaling.hpp:183-197 on the GPU (patterns kept)."""
+    if len(s.d2) != p.num_vars() or len(s.d1) != p.num_rows():
+        raise InvalidArgument("apply_scaling: dimension mismatch")
+    qv, aiv, aev = np.empty(p.q.nnz()), np.empty(p.a_ineq.nnz()), np.empty(p.a_eq.nnz())
+    c, bi, be = np.empty(p.num_vars()), np.empty(p.num_ineq()), np.empty(p.num_eq())
+    d1, d2 = _f64(s.d1), _f64(s.d2)
+    qp = p._struct()
+    _check(_load().rapdhg_apply_scaling(C.byref(qp), _pf(d1), _pf(d2), _pf(qv), _pf(aiv), _pf(aev),
+                                        _pf(c), _pf(bi), _pf(be)))
+    mk = lambda m, v: SparseMatrix.from_csr(m.n_rows, m.n_cols, m.row_ptr, m.col_idx, v)
+    return QuadraticProgram(mk(p.q, qv), c, mk(p.a_ineq, aiv), bi, mk(p.a_eq, aev), be, p.name,
+                            p.obj_offset, list(p.var_names))
+
+
+def unscale_point(z: PrimalDualPoint, s: ScalingInfo) -> PrimalDualPoint:
+    """scaling.hpp:126-133 (host; elementwise products)."""
+    mi = len(z.y_ineq)
+    return PrimalDualPoint(_f64(z.x) * s.d2, _f64(z.y_ineq) * s.d1[:mi], _f64(z.y_eq) * s.d1[mi:])
+
+
+def scale_point(z: PrimalDualPoint, s: ScalingInfo) -> PrimalDualPoint:
+    """scaling.hpp:136-143 (host)."""
+    mi = len(z.y_ineq)
+    return PrimalDualPoint(_f64(z.x) / s.d2, _f64(z.y_ineq) / s.d1[:mi], _f64(z.y_eq) / s.d1[mi:])
+
+
+@dataclass
+class PowerIterOptions:
+    max_iters: int = 5000
+    tol: float = 1e-4
+    seed: int = 20240601
+
+
+def estimate_op_norm(m: SparseMatrix, opts: Optional[PowerIterOptions] = None,
+                     strict: bool = False) -> float:
+    """opnorm.hpp:36-61 on the GPU."""
+    o = opts or PowerIterOptions()
+    out = C.c_double()
+    cm = m._csr()
+    _check(_load().rapdhg_estimate_op_norm(C.byref(cm), o.max_iters, o.tol, o.seed, C.byref(out), int(strict)))
+    return out.value
+
+
+def estimate_op_norm_symmetric(m: SparseMatrix, opts: Optional[PowerIterOptions] = None,
+                               strict: bool = False) -> float:
+    """opnorm.hpp:64-87 on the GPU."""
+    o = opts or PowerIterOptions()
+    out = C.c_double()
+    cm = m._csr()
+    _check(_load().rapdhg_estimate_op_norm_symmetric(C.byref(cm), o.max_iters, o.tol, o.seed,
+                                                     C.byref(out), int(strict)))
+    return out.value
+
+
+# --- scalar rules (host code of the library; stepsize.hpp) -------------------
+
+def step_schedule_theoretical(k: int, horizon: int, norm_q: float, norm_a: float) -> StepParams:
+    o = abi.StepParams()
+    _check(_load().rapdhg_step_schedule_theoretical(k, horizon, norm_q, norm_a, C.byref(o)))
+    return StepParams(o.beta, o.theta, o.eta, o.tau)
+
+
+def pdhg_constant_steps(norm_q: float, norm_a: float) -> StepParams:
+    o = abi.StepParams()
+    _check(_load().rapdhg_pdhg_constant_steps(norm_q, norm_a, C.byref(o)))
+    return StepParams(o.beta, o.theta, o.eta, o.tau)
+
+
+def adaptive_eta(k: int, prev_eta: float, norm_q: float, norm_a: float, omega: float) -> float:
+    o = C.c_double()
+    _check(_load().rapdhg_adaptive_eta(k, prev_eta, norm_q, norm_a, omega, C.byref(o)))
+    return o.value
+
+
+def primal_weight_init(c, b) -> float:
+    """stepsize.hpp:73-78 (host norms)."""
+    nc, nb = math.sqrt(sum(v * v for v in c)), math.sqrt(sum(v * v for v in b))
+    return nc / nb if (nc > 1e-10 and nb > 1e-10) else 1.0
+
+
+def primal_weight_update(delta_x: float, delta_y: float, omega_prev: float) -> float:
+    o = C.c_double()
+    _check(_load().rapdhg_primal_weight_update(delta_x, delta_y, omega_prev, C.byref(o)))
+    return o.value
+
+
+@dataclass
+class RestartContext:
+    relkkt_candidate: float = 0.0
+    relkkt_candidate_prev: float = 0.0
+    relkkt_epoch_start: float = 0.0
+    k: int = 0
+    total_iters: int = 0
+
+
+def restart_decision(policy: RestartPolicy, ctx: RestartContext, fixed_length: int = 0) -> bool:
+    rc = _check(_load().rapdhg_restart_decision(int(policy), ctx.relkkt_candidate,
+                                                ctx.relkkt_candidate_prev, ctx.relkkt_epoch_start,
+                                                ctx.k, ctx.total_iters, fixed_length))
+    return bool(rc)
+
+
+# --- synthetic instances --------------------------------------
+
+class Gen(enum.IntEnum):
+    RANDOM_QP = 1
+    LASSO = 2
+    PORTFOLIO = 3
+    SVM = 4
+    LARGE = 5
+    LARGE_LOCAL = 6
+
+
+def qp_from_owned(o: abi.QpOwned, name: str = "") -> QuadraticProgram:
+    def csr(m):
+        nnz = int(m.nnz)
+        rp = np.ctypeslib.as_array(m.row_ptr, (m.n_rows + 1,)).copy()
+        ci = np.ctypeslib.as_array(m.col_idx, (nnz,)).copy() if nnz else np.zeros(0, np.int32)
+        v = np.ctypeslib.as_array(m.values, (nnz,)).copy() if nnz else np.zeros(0)
+        return SparseMatrix.from_csr(m.n_rows, m.n_cols, rp, ci, v)
+    return QuadraticProgram(csr(o.q), _arr(o.c, o.n), csr(o.a_ineq), _arr(o.b_ineq, o.m_ineq),
+                            csr(o.a_eq), _arr(o.b_eq, o.m_eq), name, o.obj_offset)
+
+
+def generate(kind: Gen, scale: float = 1.0, seed: int = 1) -> QuadraticProgram:
+    """Deterministic synthetic QP of SURVEY §8(d) (C1..C5), host C++."""
+    L = _load()
+    o = abi.QpOwned()
+    _check(L.rapdhg_generate(int(kind), float(scale), int(seed), C.byref(o)))
+    try:
+        return qp_from_owned(o, f"{Gen(kind).name.lower()}-{scale:g}-{seed}")
+    finally:
+        L.rapdhg_qp_free(C.byref(o))
+
+
+__all__ = [
+    "SparseMatrix", "QuadraticProgram", "PrimalDualPoint", "SolverConfig", "SolveResult",
+    "SolveStatus", "Algorithm", "RestartPolicy", "StepRule", "PrimalWeightMode", "KktResiduals",
+    "LogRecord", "IterateState", "StepParams", "ScalingInfo", "PowerIterOptions", "RestartContext",
+    "Session", "Gen", "solve", "inner_step", "pdhg_step", "rel_kkt", "compute_scaling",
+    "ruiz_scaling", "apply_scaling", "unscale_point", "scale_point", "estimate_op_norm",
+    "estimate_op_norm_symmetric", "step_schedule_theoretical", "pdhg_constant_steps",
+    "adaptive_eta", "primal_weight_init", "primal_weight_update", "restart_decision", "generate",
+    "spmv", "spmv_t", "to_string", "device_count", "lib", "InvalidArgument", "NoDeviceError",
+    "CudaError", "QpsParseError",
+]

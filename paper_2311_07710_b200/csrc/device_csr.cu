@@ -1,0 +1,218 @@
+// device_csr.cu — structural CSR setup on the device (see device_csr.cuh).
+#include <cub/device/device_radix_sort.cuh>
+
+#include <cstring>
+
+#include "device_csr.cuh"
+
+namespace rb {
+
+namespace {
+
+__global__ void offset_rowptr_kernel(int32_t* out, const int32_t* in, int64_t n, int32_t offset) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) out[i] = in[i] + offset;
+}
+
+__global__ void iota_kernel(int32_t* p, int64_t n) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) p[i] = static_cast<int32_t>(i);
+}
+
+// row_of[k]: upper_bound(rp, k) - 1
+__global__ void expand_rows_kernel(int32_t* row_of, const int32_t* rp, int32_t rows, int64_t nnz) {
+  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (k >= nnz) return;
+  int lo = 0, hi = rows;  // find last r with rp[r] <= k
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (rp[mid] <= k) lo = mid;
+    else hi = mid;
+  }
+  row_of[k] = lo;
+}
+
+__global__ void transpose_fill_kernel(int32_t* out_ci, double* out_v, const int32_t* perm,
+                                      const int32_t* row_of, const double* v, int64_t nnz) {
+  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (k >= nnz) return;
+  const int32_t src = perm[k];
+  out_ci[k] = row_of[src];
+  out_v[k] = v[src];
+}
+
+// out_rp[c] = lower_bound(sorted_cols, c) for c in [0, cols]
+__global__ void rowptr_from_sorted_kernel(int32_t* out_rp, const int32_t* sorted, int64_t nnz,
+                                          int32_t cols) {
+  const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (c > cols) return;
+  int64_t lo = 0, hi = nnz;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (sorted[mid] < c) lo = mid + 1;
+    else hi = mid;
+  }
+  out_rp[c] = static_cast<int32_t>(lo);
+}
+
+__global__ void gather_values_kernel(double* dst, const double* src, const int32_t* perm,
+                                     int64_t nnz) {
+  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (k < nnz) dst[k] = src[perm[k]];
+}
+
+__global__ void row_lengths_kernel(int32_t* len, const int32_t* rp1, const int32_t* rp2,
+                                   int64_t rows) {
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (r >= rows) return;
+  len[r] = (rp1[r + 1] - rp1[r]) + (rp2 ? rp2[r + 1] - rp2[r] : 0);
+}
+
+__device__ __forceinline__ void atomic_max_nonneg(unsigned long long* p, double v) {
+  atomicMax(p, static_cast<unsigned long long>(__double_as_longlong(v)));
+}
+
+// One thread per row merges row r of M with row r of M' (both column-sorted).
+__global__ void symmetry_gap_kernel(CsrView m, CsrView t, int32_t rows, unsigned long long* gap,
+                                    unsigned long long* mabs) {
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (r >= rows) return;
+  int i = m.rp[r], ie = m.rp[r + 1], j = t.rp[r], je = t.rp[r + 1];
+  double g = 0.0, a = 0.0;
+  for (int k = i; k < ie; ++k) a = fmax(a, fabs(m.v[k]));
+  while (i < ie || j < je) {
+    if (j == je || (i < ie && m.ci[i] < t.ci[j])) {
+      g = fmax(g, fabs(m.v[i]));
+      ++i;
+    } else if (i == ie || t.ci[j] < m.ci[i]) {
+      g = fmax(g, fabs(t.v[j]));
+      ++j;
+    } else {
+      g = fmax(g, fabs(m.v[i] - t.v[j]));
+      ++i, ++j;
+    }
+  }
+  atomic_max_nonneg(gap, g);  // max is order-free: exact and deterministic
+  atomic_max_nonneg(mabs, a);
+}
+
+inline unsigned grid_for(int64_t n, int b = 256) { return static_cast<unsigned>(ceil_div(n > 0 ? n : 1, b)); }
+
+}  // namespace
+
+void upload_csr(DevCsr& d, const rapdhg_csr& h, cudaStream_t st) {
+  d.rows = h.n_rows;
+  d.cols = h.n_cols;
+  d.nnz = h.nnz;
+  d.rp.alloc(static_cast<std::size_t>(h.n_rows) + 1);
+  d.ci.alloc(static_cast<std::size_t>(h.nnz));
+  d.v.alloc(static_cast<std::size_t>(h.nnz));
+  d.rp.upload(h.row_ptr, static_cast<std::size_t>(h.n_rows) + 1, st);
+  d.ci.upload(h.col_idx, static_cast<std::size_t>(h.nnz), st);
+  d.v.upload(h.values, static_cast<std::size_t>(h.nnz), st);
+}
+
+void stack_csr(DevCsr& out, const DevCsr& top, const DevCsr& bot, cudaStream_t st) {
+  out.rows = top.rows + bot.rows;
+  out.cols = top.cols;
+  out.nnz = top.nnz + bot.nnz;
+  out.rp.alloc(static_cast<std::size_t>(out.rows) + 1);
+  out.ci.alloc(static_cast<std::size_t>(out.nnz));
+  out.v.alloc(static_cast<std::size_t>(out.nnz));
+  RB_CUDA(cudaMemcpyAsync(out.rp.get(), top.rp.get(), sizeof(int32_t) * (top.rows + 1),
+                          cudaMemcpyDeviceToDevice, st));
+  if (bot.rows > 0) {
+    offset_rowptr_kernel<<<grid_for(bot.rows), 256, 0, st>>>(out.rp.get() + top.rows + 1,
+                                                             bot.rp.get() + 1, bot.rows,
+                                                             static_cast<int32_t>(top.nnz));
+    RB_LAUNCH_CHECK();
+  }
+  if (top.nnz) {
+    RB_CUDA(cudaMemcpyAsync(out.ci.get(), top.ci.get(), sizeof(int32_t) * top.nnz, cudaMemcpyDeviceToDevice, st));
+    RB_CUDA(cudaMemcpyAsync(out.v.get(), top.v.get(), sizeof(double) * top.nnz, cudaMemcpyDeviceToDevice, st));
+  }
+  if (bot.nnz) {
+    RB_CUDA(cudaMemcpyAsync(out.ci.get() + top.nnz, bot.ci.get(), sizeof(int32_t) * bot.nnz, cudaMemcpyDeviceToDevice, st));
+    RB_CUDA(cudaMemcpyAsync(out.v.get() + top.nnz, bot.v.get(), sizeof(double) * bot.nnz, cudaMemcpyDeviceToDevice, st));
+  }
+}
+
+void expand_rows(DevBuf<int32_t>& row_of, const DevCsr& m, cudaStream_t st) {
+  row_of.alloc(static_cast<std::size_t>(m.nnz));
+  if (m.nnz) {
+    expand_rows_kernel<<<grid_for(m.nnz), 256, 0, st>>>(row_of.get(), m.rp.get(), m.rows, m.nnz);
+    RB_LAUNCH_CHECK();
+  }
+}
+
+void transpose_csr(DevCsr& out, const DevCsr& m, DevBuf<int32_t>* perm_out, cudaStream_t st) {
+  out.rows = m.cols;
+  out.cols = m.rows;
+  out.nnz = m.nnz;
+  out.rp.alloc(static_cast<std::size_t>(out.rows) + 1);
+  out.ci.alloc(static_cast<std::size_t>(m.nnz));
+  out.v.alloc(static_cast<std::size_t>(m.nnz));
+  DevBuf<int32_t> keys_sorted(static_cast<std::size_t>(m.nnz));
+  DevBuf<int32_t> iota(static_cast<std::size_t>(m.nnz));
+  DevBuf<int32_t> perm(static_cast<std::size_t>(m.nnz));
+  if (m.nnz) {
+    iota_kernel<<<grid_for(m.nnz), 256, 0, st>>>(iota.get(), m.nnz);
+    RB_LAUNCH_CHECK();
+    int end_bit = 1;
+    while (end_bit < 31 && (1LL << end_bit) <= m.cols) ++end_bit;
+    std::size_t temp_bytes = 0;
+    RB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, m.ci.get(), keys_sorted.get(),
+                                            iota.get(), perm.get(), static_cast<int>(m.nnz), 0,
+                                            end_bit, st));
+    DevBuf<unsigned char> temp(temp_bytes);
+    RB_CUDA(cub::DeviceRadixSort::SortPairs(temp.get(), temp_bytes, m.ci.get(), keys_sorted.get(),
+                                            iota.get(), perm.get(), static_cast<int>(m.nnz), 0,
+                                            end_bit, st));
+    DevBuf<int32_t> row_of;
+    expand_rows(row_of, m, st);
+    transpose_fill_kernel<<<grid_for(m.nnz), 256, 0, st>>>(out.ci.get(), out.v.get(), perm.get(),
+                                                           row_of.get(), m.v.get(), m.nnz);
+    RB_LAUNCH_CHECK();
+    // temporaries are freed at scope exit: make sure the stream is done with them
+    RB_CUDA(cudaStreamSynchronize(st));
+  }
+  rowptr_from_sorted_kernel<<<grid_for(static_cast<int64_t>(out.rows) + 1), 256, 0, st>>>(
+      out.rp.get(), keys_sorted.get(), m.nnz, out.rows);
+  RB_LAUNCH_CHECK();
+  RB_CUDA(cudaStreamSynchronize(st));
+  if (perm_out) *perm_out = std::move(perm);
+}
+
+void gather_values(double* dst, const double* src, const int32_t* perm, int64_t nnz,
+                   cudaStream_t st) {
+  if (!nnz) return;
+  gather_values_kernel<<<grid_for(nnz), 256, 0, st>>>(dst, src, perm, nnz);
+  RB_LAUNCH_CHECK();
+}
+
+void row_lengths(DevBuf<int32_t>& len, const int32_t* rp1, const int32_t* rp2, int64_t rows,
+                 cudaStream_t st) {
+  len.alloc(static_cast<std::size_t>(rows));
+  if (rows) {
+    row_lengths_kernel<<<grid_for(rows), 256, 0, st>>>(len.get(), rp1, rp2, rows);
+    RB_LAUNCH_CHECK();
+  }
+}
+
+void symmetry_gap(const DevCsr& m, const DevCsr& mt, double* gap, double* max_abs,
+                  cudaStream_t st) {
+  DevBuf<unsigned long long> acc(2);
+  acc.zero(st);
+  if (m.rows) {
+    symmetry_gap_kernel<<<grid_for(m.rows), 256, 0, st>>>(m.view(), mt.view(), m.rows, acc.get(),
+                                                          acc.get() + 1);
+    RB_LAUNCH_CHECK();
+  }
+  unsigned long long h[2];
+  RB_CUDA(cudaMemcpyAsync(h, acc.get(), sizeof(h), cudaMemcpyDeviceToHost, st));
+  RB_CUDA(cudaStreamSynchronize(st));
+  std::memcpy(gap, &h[0], sizeof(double));
+  std::memcpy(max_abs, &h[1], sizeof(double));
+}
+
+}  // namespace rb

@@ -1,0 +1,1100 @@
+// engine.cu — setup numerics and the iteration loop of the B200 rAPDHG solver.
+// See engine.hpp. Reference: /root/reference/proj/include/rapdhg/solver.hpp.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+
+#include "engine.hpp"
+#include "rules.hpp"
+
+namespace rb {
+
+namespace {
+
+inline unsigned grid1(int64_t n) { return static_cast<unsigned>(ceil_div(n > 0 ? n : 1, 256)); }
+
+// ---- elementwise kernels -----------------------------------------------------
+
+// w = theta (x - x_prev) + x ; x_md = (1 - 1/beta) xbar + (1/beta) x
+// (solver.hpp:163,169) for the first iteration of a chunk.
+__global__ void prologue_kernel(const double* __restrict__ x, const double* __restrict__ xp,
+                                const double* __restrict__ xb, double* __restrict__ w,
+                                double* __restrict__ xmd, const IterParams* P, int n) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const IterParams& q = P[0];
+  const double xj = x[j];
+  w[j] = q.theta * (xj - xp[j]) + xj;
+  xmd[j] = q.omib * xb[j] + q.ib * xj;
+}
+
+// unscale_point (scaling.hpp:126-133) of the current iterate and the average.
+__global__ void unscale_kernel(const double* x, const double* xb, const double* y,
+                               const double* yb, const double* d, double* xuc, double* xua,
+                               double* yuc, double* yua, int n, int m) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const double f = d[i];
+    xuc[i] = x[i] * f;
+    xua[i] = xb[i] * f;
+  } else if (i < n + m) {
+    const int r = i - n;
+    const double f = d[i];
+    yuc[r] = y[r] * f;
+    yua[r] = yb[r] * f;
+  }
+}
+
+// Restart (solver.hpp:442-448): optionally x <- xbar, y <- ybar; then
+// x_prev <- x, xbar <- x, ybar <- y.
+__global__ void restart_kernel(double* x, double* xp, double* xb, double* y, double* yb,
+                               int from_avg, int n, int m) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const double v = from_avg ? xb[i] : x[i];
+    x[i] = v;
+    xp[i] = v;
+    xb[i] = v;
+  } else if (i < n + m) {
+    const int r = i - n;
+    const double v = from_avg ? yb[r] : y[r];
+    y[r] = v;
+    yb[r] = v;
+  }
+}
+
+__global__ void scale_copy_kernel(double* v, const double* w, double s, int64_t n) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) v[i] = w[i] * s;  // v = w; scale(v, 1/nrm) (opnorm.hpp:52-53)
+}
+
+__global__ void fill_kernel(double* v, double s, int64_t n) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) v[i] = s;
+}
+
+// Ruiz/l2/l1 factor: f = measure > 0 ? 1/sqrt(measure) : 1; d *= f
+// (scaling.hpp:66-72)
+__global__ void factor_kernel(double* f, const double* meas, double* d, int64_t n) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const double mv = meas[i];
+  const double fi = mv > 0.0 ? 1.0 / sqrt(mv) : 1.0;
+  f[i] = fi;
+  d[i] *= fi;
+}
+
+// v *= f[row_off + row] * f[col_off + col] for every stored entry
+// (apply_pass, scaling.hpp:70). Product of factors first, as the reference.
+__global__ void apply_pass_kernel(double* v, const int32_t* row_of, const int32_t* ci,
+                                  const double* f, int row_off, int col_off, int64_t nnz) {
+  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (k >= nnz) return;
+  v[k] *= f[row_off + row_of[k]] * f[col_off + ci[k]];
+}
+
+// out = (d[row_off + row] * v) * d[col_off + col] (SparseMatrix::scaled,
+// sparse.hpp:154: r[row] * values_[k] * c[cols_[k]]).
+__global__ void scaled_values_kernel(double* out, const double* v, const int32_t* row_of,
+                                     const int32_t* ci, const double* d, int row_off, int col_off,
+                                     int64_t nnz) {
+  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (k >= nnz) return;
+  out[k] = d[row_off + row_of[k]] * v[k] * d[col_off + ci[k]];
+}
+
+// out[i] = d[off + i] * v[i] (c~ = D2 c, b~ = D1 b; scaling.hpp:193-195)
+__global__ void scale_vec_kernel(double* out, const double* v, const double* d, int off, int64_t n) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) out[i] = d[off + i] * v[i];
+}
+
+// ---- reduction functors (reduce.cuh) ----------------------------------------
+// Products are rounded before the add (--fmad=false), as the reference's
+// `s += a[i] * b[i]` (vec.hpp:16).
+
+struct SumSq {  // sum a_i^2 (norm2, vec.hpp:20)
+  const double* a;
+  __device__ void operator()(int64_t i, double* s, double*) const { s[0] += a[i] * a[i]; }
+};
+
+struct DotAndSumSq {  // s0 = v.w, s1 = w.w (opnorm.hpp:51-52, 77-78)
+  const double* v;
+  const double* w;
+  __device__ void operator()(int64_t i, double* s, double*) const {
+    s[0] += v[i] * w[i];
+    s[1] += w[i] * w[i];
+  }
+};
+
+// sum (x_i - e_i)^2 (dist2, vec.hpp:28-35), then e_i <- x_i (solver.hpp:459)
+struct DistAndAdvance {
+  const double* x;
+  double* e;
+  __device__ void operator()(int64_t i, double* s, double*) const {
+    const double d = x[i] - e[i];
+    s[0] += d * d;
+    e[i] = x[i];
+  }
+};
+
+// Dual-side relKKT terms for two points (kkt.hpp:44-53, 67):
+// sums  by_i(c), by_e(c), by_i(a), by_e(a)
+// maxes viol(c), viol(a), |ax|(c), |ax|(a), |b|
+struct KktDualTerms {
+  const double *axc, *axa, *b, *yc, *ya;
+  int mi;
+  __device__ void operator()(int64_t i, double* s, double* mx) const {
+    const double bi = b[i];
+    if (i < mi) {
+      s[0] += bi * yc[i];
+      s[2] += bi * ya[i];
+      mx[0] = fmax(mx[0], axc[i] - bi);
+      mx[1] = fmax(mx[1], axa[i] - bi);
+    } else {
+      s[1] += bi * yc[i];
+      s[3] += bi * ya[i];
+      mx[0] = fmax(mx[0], fabs(axc[i] - bi));
+      mx[1] = fmax(mx[1], fabs(axa[i] - bi));
+    }
+    mx[2] = fmax(mx[2], fabs(axc[i]));
+    mx[3] = fmax(mx[3], fabs(axa[i]));
+    mx[4] = fmax(mx[4], fabs(bi));
+  }
+};
+
+// Primal-side relKKT terms for two points (kkt.hpp:57-66):
+// sums  x.qx(c), x.qx(a), c.x(c), c.x(a)
+// maxes |qx+aty+c|(c), (a), |qx|(c), (a), |aty|(c), (a), |c|
+struct KktPrimalTerms {
+  const double *qxc, *qxa, *atc, *ata, *xc, *xa, *c;
+  __device__ void operator()(int64_t j, double* s, double* mx) const {
+    const double cj = c[j];
+    s[0] += xc[j] * qxc[j];
+    s[1] += xa[j] * qxa[j];
+    s[2] += cj * xc[j];
+    s[3] += cj * xa[j];
+    mx[0] = fmax(mx[0], fabs(qxc[j] + atc[j] + cj));
+    mx[1] = fmax(mx[1], fabs(qxa[j] + ata[j] + cj));
+    mx[2] = fmax(mx[2], fabs(qxc[j]));
+    mx[3] = fmax(mx[3], fabs(qxa[j]));
+    mx[4] = fmax(mx[4], fabs(atc[j]));
+    mx[5] = fmax(mx[5], fabs(ata[j]));
+    mx[6] = fmax(mx[6], fabs(cj));
+  }
+};
+
+template <class Op>
+inline void rowwise(const Op& op, const Schedule& s, cudaStream_t st, int64_t* launches) {
+  if (s.view.total_blocks > 0) {
+    launch_rowwise(op, s.view, st);
+    ++*launches;
+  }
+}
+
+}  // namespace
+
+// kkt.hpp:54,63,68-69 on the device-reduced terms. The maxima were reduced
+// exactly; the sums follow the mode's order.
+void finalize_kkt(const KktRaw& r, Kkt out[2]) {
+  for (int p = 0; p < 2; ++p) {
+    const double viol = r.viol[p];
+    out[p].r_primal = std::max(viol, 0.0) / (1.0 + std::max(r.ax_inf[p], r.b_inf));
+    out[p].r_dual = r.dn[p] / (1.0 + std::max({r.qx_inf[p], r.aty_inf[p], r.c_inf}));
+    const double xqx = r.xqx[p], cx = r.cx[p];
+    const double by = r.by_i[p] + r.by_e[p];
+    out[p].r_gap = std::fabs(xqx + cx + by) /
+                   (1.0 + std::max(std::fabs(0.5 * xqx + cx), std::fabs(0.5 * xqx + by)));
+  }
+}
+
+// ============================================================================
+// DeviceQP
+// ============================================================================
+
+void DeviceQP::validate_dims(const rapdhg_qp& p) {
+  // problem.hpp:40-46 messages
+  const int n = p.n;
+  if (p.q.n_rows != n || p.q.n_cols != n) invalid("Q dimension mismatch");
+  if (p.a_ineq.n_rows != p.m_ineq || p.a_ineq.n_cols != n)
+    invalid("inequality block dimension mismatch");
+  if (p.a_eq.n_rows != p.m_eq || p.a_eq.n_cols != n) invalid("equality block dimension mismatch");
+  auto check = [](const rapdhg_csr& a) {
+    if (a.n_rows < 0 || a.n_cols < 0) invalid("negative matrix dimension");
+    if (a.nnz > 0 && (!a.col_idx || !a.values)) invalid("null CSR arrays");
+    if (!a.row_ptr) invalid("null CSR row_ptr");
+    if (a.row_ptr[0] != 0 || a.row_ptr[a.n_rows] != a.nnz) invalid("CSR row_ptr inconsistent with nnz");
+    for (int r = 0; r < a.n_rows; ++r) {
+      const int b = a.row_ptr[r], e = a.row_ptr[r + 1];
+      if (e < b) invalid("CSR row_ptr not monotone");
+      for (int k = b; k < e; ++k) {
+        const int c = a.col_idx[k];
+        if (c < 0 || c >= a.n_cols) throw Error(RAPDHG_E_OUT_OF_RANGE, "sparse entry index out of range");
+        if (k > b && c <= a.col_idx[k - 1]) invalid("CSR columns must be strictly increasing within a row");
+      }
+    }
+  };
+  check(p.q);
+  check(p.a_ineq);
+  check(p.a_eq);
+}
+
+DeviceQP::DeviceQP(const rapdhg_qp& p, bool strict_, cudaStream_t st_)
+    : st(st_), strict(strict_), n(p.n), mi(p.m_ineq), me(p.m_eq), m(p.m_ineq + p.m_eq) {
+  upload_csr(Q, p.q, st);
+  DevCsr ai, ae;
+  upload_csr(ai, p.a_ineq, st);
+  upload_csr(ae, p.a_eq, st);
+  stack_csr(A, ai, ae, st);  // WorkingProblem::from (solver.hpp:106-108)
+  RB_CUDA(cudaStreamSynchronize(st));
+  transpose_csr(AT, A, &at_perm, st);
+  c.alloc(n);
+  c.upload(p.c, n, st);
+  b.alloc(m);
+  b.upload(p.b_ineq, mi, st);
+  if (me) RB_CUDA(cudaMemcpyAsync(b.get() + mi, p.b_eq, sizeof(double) * me, cudaMemcpyHostToDevice, st));
+  red.init(st);
+  red_out.alloc(64);
+  red_host.alloc(64);
+  // schedules (patterns only; shared by original and scaled values)
+  DevBuf<int32_t> len;
+  row_lengths(len, A.rp.get(), nullptr, A.rows, st);
+  build_schedule(sch_dual, len.get(), A.rows, strict, st);
+  row_lengths(len, Q.rp.get(), AT.rp.get(), n, st);
+  build_schedule(sch_primal, len.get(), n, strict, st);
+  row_lengths(len, Q.rp.get(), nullptr, n, st);
+  build_schedule(sch_q, len.get(), n, strict, st);
+  row_lengths(len, AT.rp.get(), nullptr, n, st);
+  build_schedule(sch_at, len.get(), n, strict, st);
+  RB_CUDA(cudaStreamSynchronize(st));
+}
+
+void DeviceQP::validate_symmetry() {
+  DevCsr qt;
+  transpose_csr(qt, Q, nullptr, st);
+  double gap = 0.0, mabs = 0.0;
+  symmetry_gap(Q, qt, &gap, &mabs, st);
+  if (gap > 1e-12 * std::max(1.0, mabs)) invalid("Q is not symmetric");  // problem.hpp:47-49
+}
+
+template <int NS, int NM, class F>
+void DeviceQP::reduce_to_host(const F& f, int64_t len, double* out) {
+  launch_reduce<NS, NM>(f, len, strict, red, red_out.get(), st);
+  ++launches;
+  RB_CUDA(cudaMemcpyAsync(red_host.get(), red_out.get(), sizeof(double) * (NS + NM),
+                          cudaMemcpyDeviceToHost, st));
+  RB_CUDA(cudaStreamSynchronize(st));
+  for (int k = 0; k < NS + NM; ++k) out[k] = red_host[k];
+}
+
+void DeviceQP::spmv(const DevCsr& mat, const Schedule& s, const double* vals, const double* x,
+                    double* y) {
+  if (strict) {
+    SpmvOp<true> op{mat.view(vals), x, y};
+    rowwise(op, s, st, &launches);
+  } else {
+    SpmvOp<false> op{mat.view(vals), x, y};
+    rowwise(op, s, st, &launches);
+  }
+}
+
+namespace {
+template <bool Strict, int Kind>
+void measures(DeviceQP& P, const double* qv, const double* av, const double* atv, double* meas) {
+  MeasureOp<Strict, Kind> prim{P.Q.view(qv), P.AT.view(atv), meas};
+  rowwise(prim, P.sch_primal, P.st, &P.launches);
+  MeasureOp<Strict, Kind> dual{P.A.view(av), CsrView{nullptr, nullptr, nullptr}, meas + P.n};
+  rowwise(dual, P.sch_dual, P.st, &P.launches);
+}
+template <int Kind>
+void measures_mode(DeviceQP& P, const double* qv, const double* av, const double* atv, double* meas) {
+  if (P.strict) measures<true, Kind>(P, qv, av, atv, meas);
+  else measures<false, Kind>(P, qv, av, atv, meas);
+}
+}  // namespace
+
+// compute_scaling (scaling.hpp:97-106): working copies of the values of Q, A
+// and A' evolve by identical products (each stacked entry and its mirror get
+// f_row * f_col, commutative), row measures are taken over [Q | A'] rows and
+// A rows in the triplet push order of stacked_triplets (scaling.hpp:30-45).
+void DeviceQP::compute_scaling(int ruiz_iters, bool full, DevBuf<double>& d) {
+  const int64_t N = static_cast<int64_t>(n) + m;
+  d.alloc(N);
+  fill_kernel<<<grid1(N), 256, 0, st>>>(d.get(), 1.0, N);
+  ++launches;
+  DevBuf<double> qw(Q.nnz), aw(A.nnz), atw(AT.nnz), meas(N), f(N);
+  if (Q.nnz) RB_CUDA(cudaMemcpyAsync(qw.get(), Q.v.get(), sizeof(double) * Q.nnz, cudaMemcpyDeviceToDevice, st));
+  if (A.nnz) RB_CUDA(cudaMemcpyAsync(aw.get(), A.v.get(), sizeof(double) * A.nnz, cudaMemcpyDeviceToDevice, st));
+  if (AT.nnz) RB_CUDA(cudaMemcpyAsync(atw.get(), AT.v.get(), sizeof(double) * AT.nnz, cudaMemcpyDeviceToDevice, st));
+  DevBuf<int32_t> q_row, a_row, at_row;
+  expand_rows(q_row, Q, st);
+  expand_rows(a_row, A, st);
+  expand_rows(at_row, AT, st);
+  auto pass = [&](int kind) {
+    if (kind == 0) measures_mode<0>(*this, qw.get(), aw.get(), atw.get(), meas.get());
+    else if (kind == 1) measures_mode<1>(*this, qw.get(), aw.get(), atw.get(), meas.get());
+    else measures_mode<2>(*this, qw.get(), aw.get(), atw.get(), meas.get());
+    factor_kernel<<<grid1(N), 256, 0, st>>>(f.get(), meas.get(), d.get(), N);
+    if (Q.nnz) apply_pass_kernel<<<grid1(Q.nnz), 256, 0, st>>>(qw.get(), q_row.get(), Q.ci.get(), f.get(), 0, 0, Q.nnz);
+    if (A.nnz) apply_pass_kernel<<<grid1(A.nnz), 256, 0, st>>>(aw.get(), a_row.get(), A.ci.get(), f.get(), n, 0, A.nnz);
+    if (AT.nnz) apply_pass_kernel<<<grid1(AT.nnz), 256, 0, st>>>(atw.get(), at_row.get(), AT.ci.get(), f.get(), 0, n, AT.nnz);
+    RB_LAUNCH_CHECK();
+    launches += 4;
+  };
+  for (int it = 0; it < ruiz_iters; ++it) pass(0);
+  if (full) {
+    pass(1);
+    pass(2);
+  }
+  RB_CUDA(cudaStreamSynchronize(st));
+}
+
+void DeviceQP::scale_values(const double* d, DevBuf<double>& qs, DevBuf<double>& as,
+                            DevBuf<double>& ats, DevBuf<double>& cs, DevBuf<double>& bs) {
+  qs.alloc(Q.nnz), as.alloc(A.nnz), ats.alloc(AT.nnz), cs.alloc(n), bs.alloc(m);
+  DevBuf<int32_t> q_row, a_row;
+  expand_rows(q_row, Q, st);
+  expand_rows(a_row, A, st);
+  if (Q.nnz) scaled_values_kernel<<<grid1(Q.nnz), 256, 0, st>>>(qs.get(), Q.v.get(), q_row.get(), Q.ci.get(), d, 0, 0, Q.nnz);
+  if (A.nnz) scaled_values_kernel<<<grid1(A.nnz), 256, 0, st>>>(as.get(), A.v.get(), a_row.get(), A.ci.get(), d, n, 0, A.nnz);
+  RB_LAUNCH_CHECK();
+  gather_values(ats.get(), as.get(), at_perm.get(), AT.nnz, st);  // same value at the mirror
+  scale_vec_kernel<<<grid1(n), 256, 0, st>>>(cs.get(), c.get(), d, 0, n);
+  if (m) scale_vec_kernel<<<grid1(m), 256, 0, st>>>(bs.get(), b.get(), d, n, m);
+  RB_LAUNCH_CHECK();
+  launches += 5;
+  RB_CUDA(cudaStreamSynchronize(st));
+}
+
+namespace {
+// random_unit (opnorm.hpp:20-30): host mt19937_64 stream, normalised on device.
+void random_unit(DeviceQP& P, DevBuf<double>& v, int len, std::mt19937_64& rng) {
+  std::vector<double> h(len);
+  for (double& x : h) x = 2.0 * (static_cast<double>(rng() >> 11) * 0x1.0p-53) - 1.0;
+  v.upload(h.data(), len, P.st);
+  double s[1];
+  P.reduce_to_host<1, 0>(SumSq{v.get()}, len, s);
+  const double nrm = std::sqrt(s[0]);
+  if (nrm > 0.0) {
+    scale_copy_kernel<<<grid1(len), 256, 0, P.st>>>(v.get(), v.get(), 1.0 / nrm, len);
+    RB_LAUNCH_CHECK();
+    ++P.launches;
+  }
+}
+}  // namespace
+
+// estimate_op_norm_symmetric (opnorm.hpp:64-87)
+double DeviceQP::op_norm_q(const double* qv, int max_iters, double tol, uint64_t seed) {
+  if (Q.nnz == 0) return 0.0;
+  std::mt19937_64 rng(seed);
+  DevBuf<double> v(n), w(n);
+  random_unit(*this, v, n, rng);
+  double lambda = 0.0;
+  const double* vp = v.get();
+  const double* wp = w.get();
+  for (int it = 0; it < max_iters; ++it) {
+    spmv(Q, sch_q, qv, v.get(), w.get());
+    double s[2];
+    reduce_to_host<2, 0>(DotAndSumSq{vp, wp}, n, s);
+    const double lambda_next = std::fabs(s[0]);
+    const double nrm = std::sqrt(s[1]);
+    if (nrm == 0.0) {
+      random_unit(*this, v, n, rng);
+      continue;
+    }
+    scale_copy_kernel<<<grid1(n), 256, 0, st>>>(v.get(), w.get(), 1.0 / nrm, n);
+    RB_LAUNCH_CHECK();
+    ++launches;
+    if (it > 0 && std::fabs(lambda_next - lambda) <= tol * std::fabs(lambda_next)) {
+      lambda = lambda_next;
+      break;
+    }
+    lambda = lambda_next;
+  }
+  return lambda;
+}
+
+// estimate_op_norm (opnorm.hpp:36-61): power iteration on A'A; A' v as the
+// gather over CSR(A').
+double DeviceQP::op_norm_a(const double* av, const double* atv, int max_iters, double tol,
+                           uint64_t seed) {
+  if (A.nnz == 0) return 0.0;
+  std::mt19937_64 rng(seed);
+  DevBuf<double> v(n), w(n), mv(m);
+  random_unit(*this, v, n, rng);
+  double lambda = 0.0;
+  const double* vp = v.get();
+  const double* wp = w.get();
+  for (int it = 0; it < max_iters; ++it) {
+    spmv(A, sch_dual, av, v.get(), mv.get());
+    spmv(AT, sch_at, atv, mv.get(), w.get());
+    double s[2];
+    reduce_to_host<2, 0>(DotAndSumSq{vp, wp}, n, s);
+    const double lambda_next = s[0];
+    const double nrm = std::sqrt(s[1]);
+    if (nrm == 0.0) {
+      random_unit(*this, v, n, rng);
+      continue;
+    }
+    scale_copy_kernel<<<grid1(n), 256, 0, st>>>(v.get(), w.get(), 1.0 / nrm, n);
+    RB_LAUNCH_CHECK();
+    ++launches;
+    if (it > 0 && std::fabs(lambda_next - lambda) <= tol * std::fabs(lambda_next)) {
+      lambda = lambda_next;
+      break;
+    }
+    lambda = lambda_next;
+  }
+  return std::sqrt(std::max(lambda, 0.0));
+}
+
+// ============================================================================
+// Engine
+// ============================================================================
+
+Engine::Engine(const rapdhg_qp& p, const rapdhg_config& cfg, Clock::time_point t0) : cfg_(cfg) {
+  DeviceQP::validate_dims(p);
+  RB_CUDA(cudaSetDevice(cfg.device));
+  RB_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  P_ = std::make_unique<DeviceQP>(p, cfg.strict_parity != 0, st_);
+  P_->validate_symmetry();  // original.validate() (solver.hpp:277)
+  validate_config(cfg);     // cfg.validate() (solver.hpp:278)
+  n_ = P_->n, m_ = P_->m, mi_ = P_->mi;
+
+  // scaling (solver.hpp:281-284)
+  if (cfg.scaling) {
+    P_->compute_scaling(10, true, d_);
+    P_->scale_values(d_.get(), qs_, as_, ats_, cs_, bs_);
+    qsv_ = qs_.get(), asv_ = as_.get(), atsv_ = ats_.get(), csv_ = cs_.get(), bsv_ = bs_.get();
+  } else {
+    d_.alloc(static_cast<std::size_t>(n_) + m_);
+    fill_kernel<<<grid1(n_ + m_), 256, 0, st_>>>(d_.get(), 1.0, n_ + m_);
+    RB_LAUNCH_CHECK();
+    qsv_ = P_->Q.v.get(), asv_ = P_->A.v.get(), atsv_ = P_->AT.v.get();
+    csv_ = P_->c.get(), bsv_ = P_->b.get();
+  }
+  // norms (solver.hpp:286-289)
+  norm_q = 1.01 * P_->op_norm_q(qsv_, 5000, 1e-4, cfg.seed);
+  norm_a = 1.01 * P_->op_norm_a(asv_, atsv_, 5000, 1e-4, cfg.seed);
+  // primal weight init on the scaled c, b (solver.hpp:296-300)
+  if (cfg.primal_weight == RAPDHG_PW_ADAPTIVE) {
+    double sc[1], sb[1];
+    P_->reduce_to_host<1, 0>(SumSq{csv_}, n_, sc);
+    P_->reduce_to_host<1, 0>(SumSq{bsv_}, m_, sb);
+    omega0 = primal_weight_init(std::sqrt(sc[0]), std::sqrt(sb[0]));
+  } else {
+    omega0 = cfg.fixed_primal_weight;
+  }
+
+  // iterate and check buffers
+  for (int i = 0; i < 2; ++i) {
+    X_[i].alloc(n_), XMD_[i].alloc(n_), xu_[i].alloc(n_), yu_[i].alloc(m_);
+    ax_[i].alloc(m_), qx_[i].alloc(n_), aty_[i].alloc(n_);
+  }
+  w_.alloc(n_), xb_.alloc(n_), y_.alloc(m_), yb_.alloc(m_), epx_.alloc(n_), epy_.alloc(m_);
+  best_x_.alloc(n_), best_y_.alloc(m_);
+  params_.alloc(kMaxChunk);
+  params_h_.alloc(kMaxChunk);
+  bad_.alloc(1);
+  bad_h_.alloc(1);
+  if (cfg.profile_kernels) {
+    events_.resize(2 * kMaxChunk + 1);
+    for (auto& e : events_) RB_CUDA(cudaEventCreate(&e));
+  }
+  RB_CUDA(cudaStreamSynchronize(st_));
+  setup_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
+}
+
+Engine::~Engine() {
+  for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
+  for (auto& e : events_) cudaEventDestroy(e);
+  P_.reset();
+  if (st_) cudaStreamDestroy(st_);
+}
+
+double Engine::bytes_dual() const {
+  // stream A~ (value + index) and row pointers; gather w (n); read y, b, ybar;
+  // write y, ybar (12 nnz(A) + 4(m+1) + 8(n + 5m))
+  return 12.0 * P_->A.nnz + 4.0 * (m_ + 1) + 8.0 * (n_ + 5.0 * m_);
+}
+double Engine::bytes_primal() const {
+  // stream Q~ and A~' with row pointers; gather x_md (n) and y (m); read x, c,
+  // xbar; write x+, xbar, w, x_md (12 (nnz(Q) + nnz(A)) + 8(n+1) + 8(8n + m))
+  return 12.0 * (P_->Q.nnz + P_->AT.nnz) + 4.0 * (2.0 * n_ + 2) + 8.0 * (8.0 * n_ + m_);
+}
+double Engine::bytes_iter() const {
+  // B_iter = 12 (2 nnz(A) + nnz(Q)) + 4 (m + 2n + 3) + 8 (9n + 6m)
+  return 12.0 * (2.0 * P_->A.nnz + P_->Q.nnz) + 4.0 * (m_ + 2.0 * n_ + 3) + 8.0 * (9.0 * n_ + 6.0 * m_);
+}
+
+void Engine::launch_chunk_body(int len, int cur) {
+  const bool prof = !events_.empty();
+  prologue_kernel<<<grid1(n_), 256, 0, st_>>>(X_[cur].get(), X_[cur ^ 1].get(), xb_.get(), w_.get(),
+                                              XMD_[cur].get(), params_.get(), n_);
+  RB_LAUNCH_CHECK();
+  ++launches_;
+  if (prof) RB_CUDA(cudaEventRecordWithFlags(events_[0], st_, cudaEventRecordExternal));
+  for (int it = 0; it < len; ++it) {
+    const int c = (cur + it) & 1;
+    if (P_->strict) {
+      DualStepOp<true> d{P_->A.view(asv_), w_.get(), bsv_, y_.get(), yb_.get(), mi_, params_.get(), it, bad_.get()};
+      rowwise(d, P_->sch_dual, st_, &launches_);
+    } else {
+      DualStepOp<false> d{P_->A.view(asv_), w_.get(), bsv_, y_.get(), yb_.get(), mi_, params_.get(), it, bad_.get()};
+      rowwise(d, P_->sch_dual, st_, &launches_);
+    }
+    if (prof) RB_CUDA(cudaEventRecordWithFlags(events_[2 * it + 1], st_, cudaEventRecordExternal));
+    if (P_->strict) {
+      PrimalStepOp<true> pr{P_->Q.view(qsv_), P_->AT.view(atsv_), XMD_[c].get(), y_.get(), X_[c].get(),
+                            X_[c ^ 1].get(), xb_.get(), csv_, w_.get(), XMD_[c ^ 1].get(), params_.get(), it, bad_.get()};
+      rowwise(pr, P_->sch_primal, st_, &launches_);
+    } else {
+      PrimalStepOp<false> pr{P_->Q.view(qsv_), P_->AT.view(atsv_), XMD_[c].get(), y_.get(), X_[c].get(),
+                             X_[c ^ 1].get(), xb_.get(), csv_, w_.get(), XMD_[c ^ 1].get(), params_.get(), it, bad_.get()};
+      rowwise(pr, P_->sch_primal, st_, &launches_);
+    }
+    if (prof) RB_CUDA(cudaEventRecordWithFlags(events_[2 * it + 2], st_, cudaEventRecordExternal));
+  }
+}
+
+void Engine::run_chunk(int len) {
+  params_.upload(params_h_.get(), len, st_);
+  if (cfg_.use_graphs) {
+    const auto key = std::make_pair(len, cur_);
+    auto it = graphs_.find(key);
+    if (it == graphs_.end()) {
+      cudaGraph_t g;
+      const int64_t before = launches_;
+      RB_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
+      launch_chunk_body(len, cur_);
+      RB_CUDA(cudaStreamEndCapture(st_, &g));
+      launches_ = before;  // counted at replay below
+      cudaGraphExec_t ge;
+      RB_CUDA(cudaGraphInstantiate(&ge, g, 0));
+      cudaGraphDestroy(g);
+      it = graphs_.emplace(key, ge).first;
+    }
+    RB_CUDA(cudaGraphLaunch(it->second, st_));
+    // prologue + one dual and one primal kernel per iteration (bins never empty
+    // for n, m > 0; counted as launched kernels)
+    launches_ += 1 + (P_->sch_dual.view.total_blocks > 0 ? len : 0) +
+                 (P_->sch_primal.view.total_blocks > 0 ? len : 0);
+  } else {
+    launch_chunk_body(len, cur_);
+  }
+  cur_ ^= (len & 1);
+  RB_CUDA(cudaStreamSynchronize(st_));
+  if (!events_.empty()) {
+    for (int it = 0; it < len; ++it) {
+      float a = 0.f, b = 0.f;
+      RB_CUDA(cudaEventElapsedTime(&a, events_[2 * it], events_[2 * it + 1]));
+      RB_CUDA(cudaEventElapsedTime(&b, events_[2 * it + 1], events_[2 * it + 2]));
+      kernel_ms_[0] += a;
+      kernel_ms_[1] += b;
+      ++kernel_count_[0];
+      ++kernel_count_[1];
+    }
+  }
+}
+
+// evaluate_candidate (solver.hpp:255-264) for the current iterate and the
+// average at once: unscale, the three KKT products over the ORIGINAL matrices
+// with both points per pass, then the reductions of kkt.hpp:43-69.
+Engine::Cand Engine::evaluate() {
+  const int cur = cur_;
+  unscale_kernel<<<grid1(n_ + m_), 256, 0, st_>>>(X_[cur].get(), xb_.get(), y_.get(), yb_.get(), d_.get(),
+                                                  xu_[0].get(), xu_[1].get(), yu_[0].get(), yu_[1].get(), n_, m_);
+  RB_LAUNCH_CHECK();
+  ++launches_;
+  DeviceQP& P = *P_;
+  if (P.strict) {
+    KktAxOp<true> ax{P.A.view(), xu_[0].get(), xu_[1].get(), ax_[0].get(), ax_[1].get()};
+    rowwise(ax, P.sch_dual, st_, &launches_);
+    KktQAtyOp<true> qa{P.Q.view(), P.AT.view(), mi_, xu_[0].get(), xu_[1].get(), yu_[0].get(), yu_[1].get(),
+                       qx_[0].get(), qx_[1].get(), aty_[0].get(), aty_[1].get()};
+    rowwise(qa, P.sch_primal, st_, &launches_);
+  } else {
+    KktAxOp<false> ax{P.A.view(), xu_[0].get(), xu_[1].get(), ax_[0].get(), ax_[1].get()};
+    rowwise(ax, P.sch_dual, st_, &launches_);
+    KktQAtyOp<false> qa{P.Q.view(), P.AT.view(), mi_, xu_[0].get(), xu_[1].get(), yu_[0].get(), yu_[1].get(),
+                        qx_[0].get(), qx_[1].get(), aty_[0].get(), aty_[1].get()};
+    rowwise(qa, P.sch_primal, st_, &launches_);
+  }
+  // dual-side terms (kkt.hpp:43-53, 67)
+  launch_reduce<4, 5>(KktDualTerms{ax_[0].get(), ax_[1].get(), P.b.get(), yu_[0].get(), yu_[1].get(), mi_},
+                      m_, P.strict, P.red, P.red_out.get(), st_);
+  // primal-side terms (kkt.hpp:56-66)
+  launch_reduce<4, 7>(KktPrimalTerms{qx_[0].get(), qx_[1].get(), aty_[0].get(), aty_[1].get(), xu_[0].get(),
+                                     xu_[1].get(), P.c.get()},
+                      n_, P.strict, P.red, P.red_out.get() + 16, st_);
+  launches_ += 2;
+  RB_CUDA(cudaMemcpyAsync(P.red_host.get(), P.red_out.get(), sizeof(double) * 32, cudaMemcpyDeviceToHost, st_));
+  RB_CUDA(cudaStreamSynchronize(st_));
+  const double* h = P.red_host.get();
+  KktRaw r;
+  r.by_i[0] = h[0], r.by_e[0] = h[1], r.by_i[1] = h[2], r.by_e[1] = h[3];
+  r.viol[0] = h[4], r.viol[1] = h[5], r.ax_inf[0] = h[6], r.ax_inf[1] = h[7], r.b_inf = h[8];
+  const double* g = h + 16;
+  r.xqx[0] = g[0], r.xqx[1] = g[1], r.cx[0] = g[2], r.cx[1] = g[3];
+  r.dn[0] = g[4], r.dn[1] = g[5], r.qx_inf[0] = g[6], r.qx_inf[1] = g[7];
+  r.aty_inf[0] = g[8], r.aty_inf[1] = g[9], r.c_inf = g[10];
+  Kkt k2[2];
+  finalize_kkt(r, k2);
+  Cand cd;
+  cd.cur = k2[0];
+  cd.avg = k2[1];
+  cd.is_avg = !(cd.cur.relkkt() < cd.avg.relkkt());  // ties -> average
+  return cd;
+}
+
+void Engine::restart(bool from_avg, double* dx, double* dy) {
+  const int cur = cur_;
+  restart_kernel<<<grid1(n_ + m_), 256, 0, st_>>>(X_[cur].get(), X_[cur ^ 1].get(), xb_.get(), y_.get(),
+                                                  yb_.get(), from_avg ? 1 : 0, n_, m_);
+  RB_LAUNCH_CHECK();
+  ++launches_;
+  // dist2 to the previous epoch start, then epoch_prev <- state (solver.hpp:454-460)
+  double sx[1], sy[1];
+  P_->reduce_to_host<1, 0>(DistAndAdvance{X_[cur].get(), epx_.get()}, n_, sx);
+  P_->reduce_to_host<1, 0>(DistAndAdvance{y_.get(), epy_.get()}, m_, sy);
+  launches_ += 2;
+  *dx = std::sqrt(sx[0]);
+  *dy = std::sqrt(sy[0]);
+}
+
+void Engine::download_point(const double* xu, const double* yu, double* x, double* y) {
+  if (n_) RB_CUDA(cudaMemcpyAsync(x, xu, sizeof(double) * n_, cudaMemcpyDeviceToHost, st_));
+  if (m_) RB_CUDA(cudaMemcpyAsync(y, yu, sizeof(double) * m_, cudaMemcpyDeviceToHost, st_));
+  RB_CUDA(cudaStreamSynchronize(st_));
+}
+
+namespace {
+template <typename T>
+T* xalloc(std::size_t n) {
+  T* p = static_cast<T*>(std::malloc(sizeof(T) * (n ? n : 1)));
+  if (!p) throw Error(RAPDHG_E_INTERNAL, "out of host memory");
+  return p;
+}
+template <typename T>
+void append(T*& arr, int64_t& count, const T& v) {
+  T* p = static_cast<T*>(std::realloc(arr, sizeof(T) * (count + 1)));
+  if (!p) throw Error(RAPDHG_E_INTERNAL, "out of host memory");
+  arr = p;
+  arr[count++] = v;
+}
+}  // namespace
+
+// solve(): the loop of solver.hpp:293-471, with inner steps batched into
+// chunks that end exactly where the reference would run a check.
+void Engine::solve(rapdhg_result* out, Clock::time_point t0) {
+  const rapdhg_config& cfg = cfg_;
+  auto elapsed = [&] { return std::chrono::duration<double>(Clock::now() - t0).count(); };
+  const int n = n_, m = m_;
+  std::memset(out, 0, sizeof(*out));
+  out->n = n, out->m_ineq = mi_, out->m_eq = m - mi_;
+  out->norm_q = norm_q;
+  out->norm_a = norm_a;
+  kernel_ms_[0] = kernel_ms_[1] = 0.0;
+  kernel_count_[0] = kernel_count_[1] = 0;
+  launches_ = P_->launches;
+  const auto loop_t0 = Clock::now();
+
+  // IterateState::zeros (solver.hpp:293)
+  cur_ = 0;
+  for (auto* buf : {&X_[0], &X_[1], &xb_, &epx_}) buf->zero(st_);
+  for (auto* buf : {&y_, &yb_, &epy_}) buf->zero(st_);
+  bad_h_[0] = std::numeric_limits<long long>::max();
+  bad_.upload(bad_h_.get(), 1, st_);
+
+  double omega = omega0;
+  long horizon = 1;
+  const bool theoretical = cfg.step_rule == RAPDHG_STEP_THEORETICAL;
+  const bool accelerated = cfg.algorithm == RAPDHG_ALG_APDHG;
+  if (theoretical && accelerated) {
+    if (cfg.restart == RAPDHG_RESTART_FIXED) horizon = cfg.restart_length;
+    else if (cfg.restart == RAPDHG_RESTART_NONE) horizon = std::max<long>(cfg.max_iters, 1);
+    else horizon = std::max<long>(4L * cfg.check_interval, 2);
+  }
+  out->norm_fallback = norm_a <= 0.0;
+  double eta = 0.0, prev_eta = 0.0;
+  long k = 0;
+
+  // candidates: index 0 = current (xu_[0], yu_[0]), 1 = average
+  Cand cand = evaluate();
+  Kkt best = cand.res();
+  auto copy_best = [&](const Cand& c) {
+    const int i = c.is_avg ? 1 : 0;
+    RB_CUDA(cudaMemcpyAsync(best_x_.get(), xu_[i].get(), sizeof(double) * n, cudaMemcpyDeviceToDevice, st_));
+    if (m) RB_CUDA(cudaMemcpyAsync(best_y_.get(), yu_[i].get(), sizeof(double) * m, cudaMemcpyDeviceToDevice, st_));
+  };
+  copy_best(cand);
+  double epoch_start = cand.res().relkkt();
+  double prev_candidate = std::numeric_limits<double>::infinity();
+  auto log = [&](long t, const Kkt& r, double e, double w, bool rs) {
+    append(out->log, out->n_log, rapdhg_log_record{t, r.r_primal, r.r_dual, r.r_gap, e, w, rs ? 1 : 0});
+  };
+  auto push_restart_point = [&](int idx) {
+    double* xs = static_cast<double*>(std::realloc(out->restart_x, sizeof(double) * ((out->n_restart_points + 1) * n + 1)));
+    double* ys = static_cast<double*>(std::realloc(out->restart_y, sizeof(double) * ((out->n_restart_points + 1) * m + 1)));
+    if (!xs || !ys) throw Error(RAPDHG_E_INTERNAL, "out of host memory");
+    out->restart_x = xs, out->restart_y = ys;
+    download_point(xu_[idx].get(), yu_[idx].get(), xs + out->n_restart_points * n, ys + out->n_restart_points * m);
+    ++out->n_restart_points;
+  };
+  log(0, cand.res(), 0.0, omega, false);
+  if (cfg.record_restart_points) push_restart_point(cand.is_avg ? 1 : 0);
+
+  int status = -1;
+  int fin_src = -1;  // 0/1 = candidate buffers, 2 = best
+  long fin_iters = 0;
+  Kkt fin_res;
+  auto finish = [&](int st, int src, long iters, const Kkt& r) {
+    status = st, fin_src = src, fin_iters = iters, fin_res = r;
+  };
+  if (cand.res().relkkt() <= cfg.tol) finish(RAPDHG_STATUS_OPTIMAL, cand.is_avg ? 1 : 0, 0, cand.res());
+  else if (norm_q <= 0.0 && norm_a <= 0.0) finish(RAPDHG_STATUS_ITERATION_LIMIT, 2, 0, best);
+
+  rapdhg_step_params sp{1.0, 1.0, 0.0, 0.0};
+  long t = 1;
+  while (status < 0 && t <= cfg.max_iters) {
+    // ---- plan a chunk: steps t .. t_end, ending at the next check ----------
+    int len = 0;
+    bool horizon_hit = false, fixed_due = false, snapshot_due = false, check_due = false;
+    long tt = t;
+    for (; len < kMaxChunk && tt <= cfg.max_iters; ++tt) {
+      if (theoretical) {
+        if (accelerated)
+          sp = step_schedule_theoretical(static_cast<int>(std::min<long>(k, horizon - 1)),
+                                         static_cast<int>(horizon), norm_q, norm_a);
+        else
+          sp = pdhg_constant_steps(norm_q, norm_a);
+      } else {
+        if (accelerated) {
+          eta = adaptive_eta(static_cast<int>(k), prev_eta, norm_q, norm_a, omega);
+          sp.beta = 0.5 * (k + 2);
+          sp.theta = static_cast<double>(k) / (k + 1);
+        } else {
+          if (k == 0) eta = adaptive_eta(0, 0.0, norm_q, norm_a, omega);
+          sp.beta = 1.0;
+          sp.theta = 1.0;
+        }
+        prev_eta = eta;
+        sp.eta = eta / omega;
+        sp.tau = eta * omega;
+      }
+      IterParams& q = params_h_[len];
+      const double inv_beta = 1.0 / sp.beta;
+      q.theta = sp.theta;
+      q.ib = inv_beta;
+      q.omib = 1.0 - inv_beta;
+      q.eta = sp.eta;
+      q.tau = sp.tau;
+      q.t = tt;
+      q.emit_next = 0;
+      if (len > 0) {
+        IterParams& pq = params_h_[len - 1];
+        pq.theta_n = q.theta, pq.ib_n = q.ib, pq.omib_n = q.omib, pq.emit_next = 1;
+      }
+      ++len;
+      ++k;
+      horizon_hit = theoretical && accelerated && cfg.restart != RAPDHG_RESTART_NONE && k >= horizon;
+      fixed_due = cfg.restart == RAPDHG_RESTART_FIXED && k >= cfg.restart_length;
+      snapshot_due = cfg.snapshot_interval > 0 && tt % cfg.snapshot_interval == 0;
+      check_due = tt % cfg.check_interval == 0 || fixed_due || horizon_hit || snapshot_due ||
+                  tt == cfg.max_iters;
+      if (check_due) break;
+    }
+    const long t_end = check_due ? tt : tt - 1;
+    run_chunk(len);
+    // all_finite after every step (solver.hpp:372-373): first bad iteration
+    bad_.download(bad_h_.get(), 1, st_);
+    RB_CUDA(cudaStreamSynchronize(st_));
+    if (bad_h_[0] <= t_end) {
+      finish(RAPDHG_STATUS_NUMERICAL_ERROR, 2, static_cast<long>(bad_h_[0]), best);
+      break;
+    }
+    t = t_end + 1;
+    if (!check_due) continue;
+    const long tc = t_end;
+    const double cur_eta = theoretical ? sp.eta : eta;
+
+    cand = evaluate();
+    const Kkt cres = cand.res();
+    if (cres.relkkt() < best.relkkt()) {
+      best = cres;
+      copy_best(cand);
+    }
+    if (snapshot_due) {
+      const int64_t s = out->n_snapshots;
+      append(out->snapshot_iters, out->n_snapshots, static_cast<int64_t>(tc));
+      out->snapshot_x = static_cast<double*>(std::realloc(out->snapshot_x, sizeof(double) * ((s + 1) * n + 1)));
+      out->snapshot_y = static_cast<double*>(std::realloc(out->snapshot_y, sizeof(double) * ((s + 1) * m + 1)));
+      download_point(xu_[1].get(), yu_[1].get(), out->snapshot_x + s * n, out->snapshot_y + s * m);
+    }
+    if (cres.relkkt() <= cfg.tol) {
+      log(tc, cres, cur_eta, omega, false);
+      finish(RAPDHG_STATUS_OPTIMAL, cand.is_avg ? 1 : 0, tc, cres);
+      break;
+    }
+    if (elapsed() > cfg.time_limit_s) {
+      log(tc, cres, cur_eta, omega, false);
+      finish(RAPDHG_STATUS_TIME_LIMIT, 2, tc, best);
+      break;
+    }
+    bool do_restart = false, from_avg = true;
+    if (cfg.restart != RAPDHG_RESTART_NONE) {
+      switch (cfg.restart) {
+        case RAPDHG_RESTART_FIXED: do_restart = fixed_due; break;
+        case RAPDHG_RESTART_HALVING:
+          do_restart = restart_decision(cfg.restart, cand.avg.relkkt(), prev_candidate, epoch_start, k, tc, 0);
+          break;
+        case RAPDHG_RESTART_PDQP:
+          do_restart = restart_decision(cfg.restart, cres.relkkt(), prev_candidate, epoch_start, k, tc, 0) ||
+                       horizon_hit;
+          from_avg = cand.is_avg;
+          break;
+        default: break;
+      }
+      if (horizon_hit) do_restart = true;
+      prev_candidate = cres.relkkt();
+    }
+    log(tc, cres, cur_eta, omega, do_restart);
+    if (!do_restart) continue;
+
+    if (horizon_hit && !fixed_due) horizon *= 2;
+    double dx = 0.0, dy = 0.0;
+    restart(from_avg, &dx, &dy);
+    k = 0;
+    out->restarts += 1;
+    prev_eta = 0.0;
+    if (cfg.primal_weight == RAPDHG_PW_ADAPTIVE) omega = primal_weight_update(dx, dy, omega);
+    // relKKT of the new epoch start == the average's when restarting from it
+    epoch_start = (from_avg && !cand.is_avg) ? cand.avg.relkkt() : cres.relkkt();
+    prev_candidate = std::numeric_limits<double>::infinity();
+    if (cfg.record_restart_points) push_restart_point(from_avg ? 1 : 0);
+  }
+  if (status < 0) finish(RAPDHG_STATUS_ITERATION_LIMIT, 2, cfg.max_iters, best);
+
+  out->status = status;
+  out->iterations = fin_iters;
+  out->residuals = {fin_res.r_primal, fin_res.r_dual, fin_res.r_gap};
+  out->x = xalloc<double>(n);
+  double* yall = xalloc<double>(m);
+  if (fin_src == 2) download_point(best_x_.get(), best_y_.get(), out->x, yall);
+  else download_point(xu_[fin_src].get(), yu_[fin_src].get(), out->x, yall);
+  out->y_ineq = xalloc<double>(mi_);
+  out->y_eq = xalloc<double>(m - mi_);
+  if (mi_) std::memcpy(out->y_ineq, yall, sizeof(double) * mi_);
+  if (m - mi_) std::memcpy(out->y_eq, yall + mi_, sizeof(double) * (m - mi_));
+  std::free(yall);
+  out->loop_seconds = std::chrono::duration<double>(Clock::now() - loop_t0).count();
+  out->setup_seconds = setup_seconds;
+  out->solve_seconds = elapsed();
+  out->kernel_launches = launches_;
+  out->kernel_ms[0] = kernel_ms_[0], out->kernel_ms[1] = kernel_ms_[1];
+  out->kernel_count[0] = kernel_count_[0], out->kernel_count[1] = kernel_count_[1];
+}
+
+// ============================================================================
+// secondary API helpers
+// ============================================================================
+
+namespace {
+struct StreamGuard {
+  cudaStream_t s = nullptr;
+  StreamGuard() { RB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
+  ~StreamGuard() {
+    if (s) cudaStreamDestroy(s);
+  }
+};
+
+rapdhg_qp single_matrix_qp(const rapdhg_csr& m, std::vector<int32_t>& zero_rp) {
+  // A problem wrapper whose A_ineq is m (rows x cols) and Q is the empty
+  // cols x cols matrix, so DeviceQP builds A, A' and their schedules.
+  zero_rp.assign(static_cast<std::size_t>(m.n_cols) + 1, 0);
+  rapdhg_qp p{};
+  p.n = m.n_cols;
+  p.m_ineq = m.n_rows;
+  p.m_eq = 0;
+  p.q = rapdhg_csr{m.n_cols, m.n_cols, 0, zero_rp.data(), nullptr, nullptr};
+  p.a_ineq = m;
+  p.a_eq = rapdhg_csr{0, m.n_cols, 0, zero_rp.data(), nullptr, nullptr};
+  return p;
+}
+}  // namespace
+
+void api_spmv(const rapdhg_csr& mat, const double* x, double* y, bool transpose, bool strict) {
+  std::vector<int32_t> zrp;
+  rapdhg_qp p = single_matrix_qp(mat, zrp);
+  std::vector<double> zeros(static_cast<std::size_t>(mat.n_cols) + static_cast<std::size_t>(mat.n_rows) + 1, 0.0);
+  p.c = zeros.data();
+  p.b_ineq = zeros.data();
+  DeviceQP::validate_dims(p);
+  StreamGuard sg;
+  DeviceQP P(p, strict, sg.s);
+  const int64_t in_len = transpose ? mat.n_rows : mat.n_cols;
+  const int64_t out_len = transpose ? mat.n_cols : mat.n_rows;
+  DevBuf<double> dx(in_len), dy(out_len);
+  dx.upload(x, in_len, sg.s);
+  if (transpose) P.spmv(P.AT, P.sch_at, P.AT.v.get(), dx.get(), dy.get());
+  else P.spmv(P.A, P.sch_dual, P.A.v.get(), dx.get(), dy.get());
+  dy.download(y, out_len, sg.s);
+  RB_CUDA(cudaStreamSynchronize(sg.s));
+}
+
+void api_rel_kkt(const rapdhg_qp& p, const double* x, const double* yi, const double* ye,
+                 bool strict, Kkt* out) {
+  for (int i = 0; i < p.m_ineq; ++i)
+    if (yi[i] < -1e-9) invalid("rel_kkt: negative inequality dual");  // kkt.hpp:29-30
+  DeviceQP::validate_dims(p);
+  StreamGuard sg;
+  DeviceQP P(p, strict, sg.s);
+  const int n = P.n, m = P.m, mi = P.mi;
+  DevBuf<double> xu(n), yu(m), ax(m), qx(n), aty(n), ax2(m), qx2(n), aty2(n);
+  xu.upload(x, n, sg.s);
+  yu.upload(yi, mi, sg.s);
+  if (m - mi) RB_CUDA(cudaMemcpyAsync(yu.get() + mi, ye, sizeof(double) * (m - mi), cudaMemcpyHostToDevice, sg.s));
+  int64_t l = 0;
+  if (strict) {
+    rowwise(KktAxOp<true>{P.A.view(), xu.get(), xu.get(), ax.get(), ax2.get()}, P.sch_dual, sg.s, &l);
+    rowwise(KktQAtyOp<true>{P.Q.view(), P.AT.view(), mi, xu.get(), xu.get(), yu.get(), yu.get(), qx.get(),
+                            qx2.get(), aty.get(), aty2.get()},
+            P.sch_primal, sg.s, &l);
+  } else {
+    rowwise(KktAxOp<false>{P.A.view(), xu.get(), xu.get(), ax.get(), ax2.get()}, P.sch_dual, sg.s, &l);
+    rowwise(KktQAtyOp<false>{P.Q.view(), P.AT.view(), mi, xu.get(), xu.get(), yu.get(), yu.get(), qx.get(),
+                             qx2.get(), aty.get(), aty2.get()},
+            P.sch_primal, sg.s, &l);
+  }
+  const double *axp = ax.get(), *b = P.b.get(), *yp = yu.get();
+  double h1[9];
+  P.reduce_to_host<4, 5>(KktDualTerms{axp, axp, b, yp, yp, mi}, m, h1);
+  const double *qxp = qx.get(), *atp = aty.get(), *xp = xu.get(), *c = P.c.get();
+  double h2[11];
+  P.reduce_to_host<4, 7>(KktPrimalTerms{qxp, qxp, atp, atp, xp, xp, c}, n, h2);
+  KktRaw r{};
+  r.by_i[0] = h1[0], r.by_e[0] = h1[1], r.viol[0] = h1[4], r.ax_inf[0] = h1[6], r.b_inf = h1[8];
+  r.xqx[0] = h2[0], r.cx[0] = h2[2], r.dn[0] = h2[4], r.qx_inf[0] = h2[6], r.aty_inf[0] = h2[8], r.c_inf = h2[10];
+  Kkt k2[2];
+  finalize_kkt(r, k2);
+  *out = k2[0];
+}
+
+void api_inner_step(const rapdhg_qp& p, rapdhg_iterate* s, const rapdhg_step_params& sp, int steps,
+                    bool strict) {
+  DeviceQP::validate_dims(p);
+  StreamGuard sg;
+  cudaStream_t st = sg.s;
+  DeviceQP P(p, strict, st);
+  const int n = P.n, m = P.m;
+  DevBuf<double> X[2], XMD[2], w(n), xb(n), y(m), yb(m);
+  for (int i = 0; i < 2; ++i) X[i].alloc(n), XMD[i].alloc(n);
+  X[0].upload(s->x, n, st);
+  X[1].upload(s->x_prev, n, st);
+  xb.upload(s->x_bar, n, st);
+  y.upload(s->y, m, st);
+  yb.upload(s->y_bar, m, st);
+  DevBuf<long long> bad(1);
+  long long big = std::numeric_limits<long long>::max();
+  bad.upload(&big, 1, st);
+  std::vector<IterParams> ph(std::max(steps, 1));
+  const double inv_beta = 1.0 / sp.beta;
+  for (int i = 0; i < steps; ++i) {
+    IterParams& q = ph[i];
+    q.theta = sp.theta, q.ib = inv_beta, q.omib = 1.0 - inv_beta, q.eta = sp.eta, q.tau = sp.tau;
+    q.theta_n = sp.theta, q.ib_n = inv_beta, q.omib_n = 1.0 - inv_beta;
+    q.t = i + 1;
+    q.emit_next = i + 1 < steps;
+  }
+  DevBuf<IterParams> params(ph.size());
+  params.upload(ph.data(), ph.size(), st);
+  int64_t l = 0;
+  if (steps > 0) {
+    prologue_kernel<<<grid1(n), 256, 0, st>>>(X[0].get(), X[1].get(), xb.get(), w.get(), XMD[0].get(), params.get(), n);
+    RB_LAUNCH_CHECK();
+  }
+  for (int it = 0; it < steps; ++it) {
+    const int c = it & 1;
+    if (strict) {
+      rowwise(DualStepOp<true>{P.A.view(), w.get(), P.b.get(), y.get(), yb.get(), P.mi, params.get(), it, bad.get()},
+              P.sch_dual, st, &l);
+      rowwise(PrimalStepOp<true>{P.Q.view(), P.AT.view(), XMD[c].get(), y.get(), X[c].get(), X[c ^ 1].get(), xb.get(),
+                                 P.c.get(), w.get(), XMD[c ^ 1].get(), params.get(), it, bad.get()},
+              P.sch_primal, st, &l);
+    } else {
+      rowwise(DualStepOp<false>{P.A.view(), w.get(), P.b.get(), y.get(), yb.get(), P.mi, params.get(), it, bad.get()},
+              P.sch_dual, st, &l);
+      rowwise(PrimalStepOp<false>{P.Q.view(), P.AT.view(), XMD[c].get(), y.get(), X[c].get(), X[c ^ 1].get(), xb.get(),
+                                  P.c.get(), w.get(), XMD[c ^ 1].get(), params.get(), it, bad.get()},
+              P.sch_primal, st, &l);
+    }
+  }
+  const int cur = steps & 1;  // x is X[cur], x_prev X[cur^1]
+  X[cur].download(s->x, n, st);
+  X[cur ^ 1].download(s->x_prev, n, st);
+  xb.download(s->x_bar, n, st);
+  y.download(s->y, m, st);
+  yb.download(s->y_bar, m, st);
+  RB_CUDA(cudaStreamSynchronize(st));
+  s->k += steps;
+}
+
+void api_scaling(const rapdhg_qp& p, int ruiz_iters, bool full, double* d1, double* d2, bool strict) {
+  DeviceQP::validate_dims(p);
+  StreamGuard sg;
+  DeviceQP P(p, strict, sg.s);
+  DevBuf<double> d;
+  P.compute_scaling(ruiz_iters, full, d);
+  RB_CUDA(cudaMemcpyAsync(d2, d.get(), sizeof(double) * P.n, cudaMemcpyDeviceToHost, sg.s));
+  if (P.m) RB_CUDA(cudaMemcpyAsync(d1, d.get() + P.n, sizeof(double) * P.m, cudaMemcpyDeviceToHost, sg.s));
+  RB_CUDA(cudaStreamSynchronize(sg.s));
+}
+
+void api_apply_scaling(const rapdhg_qp& p, const double* d1, const double* d2, double* qv,
+                       double* aiv, double* aev, double* c, double* bi, double* be) {
+  DeviceQP::validate_dims(p);
+  StreamGuard sg;
+  DeviceQP P(p, true, sg.s);
+  DevBuf<double> d(static_cast<std::size_t>(P.n) + P.m);
+  d.upload(d2, P.n, sg.s);
+  if (P.m) RB_CUDA(cudaMemcpyAsync(d.get() + P.n, d1, sizeof(double) * P.m, cudaMemcpyHostToDevice, sg.s));
+  DevBuf<double> qs, as, ats, cs, bs;
+  P.scale_values(d.get(), qs, as, ats, cs, bs);
+  qs.download(qv, P.Q.nnz, sg.s);
+  as.download(aiv, p.a_ineq.nnz, sg.s);
+  if (p.a_eq.nnz) RB_CUDA(cudaMemcpyAsync(aev, as.get() + p.a_ineq.nnz, sizeof(double) * p.a_eq.nnz, cudaMemcpyDeviceToHost, sg.s));
+  cs.download(c, P.n, sg.s);
+  bs.download(bi, P.mi, sg.s);
+  if (P.me) RB_CUDA(cudaMemcpyAsync(be, bs.get() + P.mi, sizeof(double) * P.me, cudaMemcpyDeviceToHost, sg.s));
+  RB_CUDA(cudaStreamSynchronize(sg.s));
+}
+
+double api_op_norm(const rapdhg_csr& mat, bool symmetric, int max_iters, double tol, uint64_t seed,
+                   bool strict) {
+  StreamGuard sg;
+  std::vector<int32_t> zrp;
+  if (symmetric) {
+    if (mat.n_rows != mat.n_cols) invalid("estimate_op_norm_symmetric: matrix must be square");
+    rapdhg_qp p{};
+    zrp.assign(static_cast<std::size_t>(mat.n_cols) + 1, 0);
+    std::vector<double> zeros(static_cast<std::size_t>(mat.n_cols) + 1, 0.0);
+    p.n = mat.n_cols;
+    p.q = mat;
+    p.a_ineq = rapdhg_csr{0, mat.n_cols, 0, zrp.data(), nullptr, nullptr};
+    p.a_eq = p.a_ineq;
+    p.c = zeros.data();
+    DeviceQP::validate_dims(p);
+    DeviceQP P(p, strict, sg.s);
+    return P.op_norm_q(P.Q.v.get(), max_iters, tol, seed);
+  }
+  rapdhg_qp p = single_matrix_qp(mat, zrp);
+  std::vector<double> zeros(static_cast<std::size_t>(mat.n_cols) + static_cast<std::size_t>(mat.n_rows) + 1, 0.0);
+  p.c = zeros.data();
+  p.b_ineq = zeros.data();
+  DeviceQP::validate_dims(p);
+  DeviceQP P(p, strict, sg.s);
+  return P.op_norm_a(P.A.v.get(), P.AT.v.get(), max_iters, tol, seed);
+}
+
+}  // namespace rb

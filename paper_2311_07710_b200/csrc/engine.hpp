@@ -1,0 +1,156 @@
+// engine.hpp — host-side driver of the B200 rAPDHG solver.
+//
+// DeviceQP: the problem resident in HBM (original CSRs, stacked A, its
+// transpose, schedules) plus the setup numerics (scaling, power iteration).
+// Engine: a DeviceQP after the full solve() setup (solver.hpp:277-300), and the
+// iteration loop (solver.hpp:318-471) driven as CUDA-graph chunks of at most
+// kMaxChunk iterations with one host synchronisation per chunk.
+#pragma once
+
+#include <chrono>
+#include <map>
+#include <memory>
+#include <random>
+#include <utility>
+#include <vector>
+
+#include "device_csr.cuh"
+#include "ops.cuh"
+#include "reduce.cuh"
+#include "rowwise.cuh"
+
+namespace rb {
+
+constexpr int kMaxChunk = 64;
+
+using Clock = std::chrono::steady_clock;
+
+struct Kkt {
+  double r_primal = 0.0, r_dual = 0.0, r_gap = 0.0;
+  double relkkt() const {
+    double m = r_primal;
+    if (m < r_dual) m = r_dual;
+    if (m < r_gap) m = r_gap;
+    return m;  // std::max({r_primal, r_dual, r_gap}) (kkt.hpp:16)
+  }
+};
+
+// Raw reduction outputs of one relKKT evaluation of two points (c, a).
+struct KktRaw {
+  double by_i[2], by_e[2], viol[2], ax_inf[2], b_inf;
+  double xqx[2], cx[2], dn[2], qx_inf[2], aty_inf[2], c_inf;
+};
+void finalize_kkt(const KktRaw& r, Kkt out[2]);  // kkt.hpp:54,63,68-69
+
+class DeviceQP {
+ public:
+  DeviceQP(const rapdhg_qp& p, bool strict, cudaStream_t st);
+
+  // QuadraticProgram::validate (problem.hpp:40-50): throws invalid_argument.
+  static void validate_dims(const rapdhg_qp& p);
+  void validate_symmetry();
+
+  // compute_scaling / ruiz_scaling (scaling.hpp:159-180). d: n + m factors
+  // (d2 = d[0:n], d1 = d[n:]).
+  void compute_scaling(int ruiz_iters, bool full, DevBuf<double>& d);
+  // apply_scaling (scaling.hpp:183-197) into value arrays with the original
+  // patterns; d as above.
+  void scale_values(const double* d, DevBuf<double>& qs, DevBuf<double>& as, DevBuf<double>& ats,
+                    DevBuf<double>& cs, DevBuf<double>& bs);
+  // estimate_op_norm_symmetric / estimate_op_norm (opnorm.hpp:36-87) on the
+  // given values (patterns of Q / A / A').
+  double op_norm_q(const double* qv, int max_iters, double tol, uint64_t seed);
+  double op_norm_a(const double* av, const double* atv, int max_iters, double tol, uint64_t seed);
+
+  // Deterministic reduction to host (strict: sequential).
+  template <int NS, int NM, class F>
+  void reduce_to_host(const F& f, int64_t n, double* out);
+
+  // Launch helpers for plain products with given values.
+  void spmv(const DevCsr& m, const Schedule& s, const double* vals, const double* x, double* y);
+
+  cudaStream_t st;
+  bool strict;
+  int n, mi, me, m;
+  DevCsr Q, A, AT;  // original values; A = [A_ineq; A_eq]
+  DevBuf<int32_t> at_perm;  // AT position -> A position
+  DevBuf<double> c, b;      // original c and stacked b
+  Schedule sch_dual;    // rows of A
+  Schedule sch_primal;  // rows of [Q | A']
+  Schedule sch_q;       // rows of Q
+  Schedule sch_at;      // rows of A'
+  ReduceScratch red;
+  DevBuf<double> red_out;
+  PinnedBuf<double> red_host;
+  int64_t launches = 0;
+};
+
+class Engine {
+ public:
+  Engine(const rapdhg_qp& p, const rapdhg_config& cfg, Clock::time_point t0);
+  ~Engine();
+  Engine(const Engine&) = delete;
+  Engine& operator=(const Engine&) = delete;
+
+  // Runs the iteration loop from the zero start (solver.hpp:293-471) and fills
+  // out (library-owned arrays). t0: the clock solve_seconds is measured from.
+  void solve(rapdhg_result* out, Clock::time_point t0);
+
+  double setup_seconds = 0.0;
+  double norm_q = 0.0, norm_a = 0.0, omega0 = 1.0;
+  // algorithmic bytes
+  double bytes_iter() const;
+  double bytes_dual() const;
+  double bytes_primal() const;
+
+ private:
+  struct Cand {
+    Kkt cur, avg;
+    bool is_avg;
+    const Kkt& res() const { return is_avg ? avg : cur; }
+  };
+  Cand evaluate();
+  void run_chunk(int len);
+  void launch_chunk_body(int len, int cur);
+  void restart(bool from_avg, double* dx, double* dy);
+  void download_point(const double* xu, const double* yu, double* x, double* y);
+
+  rapdhg_config cfg_;
+  std::unique_ptr<DeviceQP> P_;
+  cudaStream_t st_ = nullptr;
+  int n_, m_, mi_;
+  // scaled problem (values share the original patterns)
+  DevBuf<double> d_;  // n + m scaling factors (d2 then d1)
+  DevBuf<double> qs_, as_, ats_, cs_, bs_;
+  const double *qsv_, *asv_, *atsv_, *csv_, *bsv_;
+  // iterate state (scaled)
+  DevBuf<double> X_[2], XMD_[2], w_, xb_, y_, yb_, epx_, epy_;
+  int cur_ = 0;
+  // check workspace (unscaled)
+  DevBuf<double> xu_[2], yu_[2], ax_[2], qx_[2], aty_[2], best_x_, best_y_;
+  // per-chunk params
+  DevBuf<IterParams> params_;
+  PinnedBuf<IterParams> params_h_;
+  DevBuf<long long> bad_;
+  PinnedBuf<long long> bad_h_;
+  std::map<std::pair<int, int>, cudaGraphExec_t> graphs_;
+  std::vector<cudaEvent_t> events_;
+  double kernel_ms_[2] = {0, 0};
+  int64_t kernel_count_[2] = {0, 0};
+  int64_t launches_ = 0;
+};
+
+// ---- secondary API helpers (host buffers in/out) ----------------------------
+void api_spmv(const rapdhg_csr& m, const double* x, double* y, bool transpose, bool strict);
+void api_rel_kkt(const rapdhg_qp& p, const double* x, const double* yi, const double* ye,
+                 bool strict, Kkt* out);
+void api_inner_step(const rapdhg_qp& p, rapdhg_iterate* s, const rapdhg_step_params& sp,
+                    int steps, bool strict);
+void api_scaling(const rapdhg_qp& p, int ruiz_iters, bool full, double* d1, double* d2,
+                 bool strict);
+void api_apply_scaling(const rapdhg_qp& p, const double* d1, const double* d2, double* qv,
+                       double* aiv, double* aev, double* c, double* bi, double* be);
+double api_op_norm(const rapdhg_csr& m, bool symmetric, int max_iters, double tol, uint64_t seed,
+                   bool strict);
+
+}  // namespace rb

@@ -1,0 +1,261 @@
+// ops.cuh — the row operations run by rowwise_kernel (rowwise.cuh).
+//
+// Each Op describes, for one logical row r: its length (nnz over its one or two
+// CSR segments), how to accumulate a lane's share of positions
+// [lo, hi) (stride = lanes working on the row), and the epilogue `finish`
+// run once per row with the fully reduced sums. Epilogue arithmetic is written
+// exactly as the reference writes it; the library is compiled with
+// --fmad=false so `a*b + c` is never contracted and the epilogues are
+// bit-identical to the reference in both modes. Only the SpMV accumulation of
+// fast mode uses explicit fma() (madd<false>).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "rowwise.cuh"
+
+namespace rb {
+
+// Per-iteration scalars of one inner step, computed on the host for a whole
+// check interval (they depend only on k, eta_{k-1}, ||Q||, ||A||, omega:
+// solver.hpp:347-368) and uploaded once per chunk.
+struct IterParams {
+  double theta;           // extrapolation theta_k (solver.hpp:163)
+  double ib, omib;        // 1/beta_k and 1 - 1/beta_k (solver.hpp:160,169,177-178)
+  double eta, tau;        // primal / dual step (solver.hpp:166,175)
+  double theta_n;         // next iteration's theta, ...
+  double ib_n, omib_n;    // ... and weights, to emit w and x_md for it
+  long long t;            // global iteration index (NaN flag)
+  int emit_next;          // 0 on the last iteration of a chunk
+  int pad;
+};
+
+__device__ __forceinline__ void flag_nonfinite(double v, long long t, long long* bad) {
+  if (!isfinite(v)) atomicMin(bad, t);
+}
+
+struct CsrView {
+  const int32_t* rp;
+  const int32_t* ci;
+  const double* v;
+};
+
+// ---------------------------------------------------------------------------
+// Dual step over rows of the stacked scaled A (solver.hpp:164-167, 178):
+//   aw_i = sum A_ik w_k;  y_i += tau (aw_i - b_i);  y_i = max(y_i, 0) for
+//   i < m_ineq;  ybar_i = (1 - 1/beta) ybar_i + (1/beta) y_i.
+template <bool Strict>
+struct DualStepOp {
+  static constexpr bool kStrict = Strict;
+  using AccT = Acc<1>;
+  CsrView a;
+  const double* w;
+  const double* b;
+  double* y;
+  double* yb;
+  int m_ineq;
+  const IterParams* P;
+  int it;
+  long long* bad;
+  __device__ __forceinline__ int len(int r) const { return a.rp[r + 1] - a.rp[r]; }
+  __device__ __forceinline__ void accumulate(int r, int lo, int hi, int lane, int stride,
+                                             AccT& acc) const {
+    int p = lo + lane;
+    acc.v[0] = seg_dot<Strict>(a.v, a.ci, w, a.rp[r], p, hi, stride, acc.v[0]);
+  }
+  __device__ __forceinline__ void finish(int i, const AccT& acc) const {
+    const IterParams& q = P[it];
+    double yi = y[i];
+    yi += q.tau * (acc.v[0] - b[i]);
+    if (i < m_ineq) yi = yi > 0.0 ? yi : 0.0;
+    y[i] = yi;
+    yb[i] = q.omib * yb[i] + q.ib * yi;
+    flag_nonfinite(yi, q.t, bad);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Primal step over rows j of [Q~ | A~'] (solver.hpp:169-177):
+//   qx_j = sum Q_jk xmd_k;  aty_j = sum A'_ji y_i;
+//   x+_j = x_j - eta ((qx_j + c_j) + aty_j);  xbar_j = (1-1/b) xbar_j + (1/b) x+_j
+// and, when another iteration follows in the chunk, the next extrapolation
+// w_j = theta' (x+_j - x_j) + x+_j and x_md_j = (1-1/b') xbar_j + (1/b') x+_j
+// (solver.hpp:163,169 of the next call), so the next dual/primal kernels
+// gather them directly.
+template <bool Strict>
+struct PrimalStepOp {
+  static constexpr bool kStrict = Strict;
+  using AccT = Acc<2>;
+  CsrView q, at;
+  const double* xmd;  // gathered by Q
+  const double* y;    // gathered by A'
+  const double* x_in;
+  double* x_out;
+  double* xb;
+  const double* c;
+  double* w_out;
+  double* xmd_out;
+  const IterParams* P;
+  int it;
+  long long* bad;
+  __device__ __forceinline__ int len(int r) const {
+    return (q.rp[r + 1] - q.rp[r]) + (at.rp[r + 1] - at.rp[r]);
+  }
+  __device__ __forceinline__ void accumulate(int r, int lo, int hi, int lane, int stride,
+                                             AccT& acc) const {
+    const int q0 = q.rp[r];
+    const int L1 = q.rp[r + 1] - q0;
+    int p = lo + lane;
+    acc.v[0] = seg_dot<Strict>(q.v, q.ci, xmd, q0, p, hi < L1 ? hi : L1, stride, acc.v[0]);
+    acc.v[1] = seg_dot<Strict>(at.v, at.ci, y, static_cast<int64_t>(at.rp[r]) - L1, p, hi, stride,
+                               acc.v[1]);
+  }
+  __device__ __forceinline__ void finish(int j, const AccT& acc) const {
+    const IterParams& p = P[it];
+    const double xo = x_in[j];
+    const double xn = xo - p.eta * (acc.v[0] + c[j] + acc.v[1]);
+    x_out[j] = xn;
+    const double xbn = p.omib * xb[j] + p.ib * xn;
+    xb[j] = xbn;
+    if (p.emit_next) {
+      w_out[j] = p.theta_n * (xn - xo) + xn;
+      xmd_out[j] = p.omib_n * xbn + p.ib_n * xn;
+    }
+    flag_nonfinite(xn, p.t, bad);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Plain y = M x (sparse.hpp:79-88); M' x uses the transposed CSR, which is
+// bit-identical to the reference's scatter.
+template <bool Strict>
+struct SpmvOp {
+  static constexpr bool kStrict = Strict;
+  using AccT = Acc<1>;
+  CsrView m;
+  const double* x;
+  double* y;
+  __device__ __forceinline__ int len(int r) const { return m.rp[r + 1] - m.rp[r]; }
+  __device__ __forceinline__ void accumulate(int r, int lo, int hi, int lane, int stride,
+                                             AccT& acc) const {
+    int p = lo + lane;
+    acc.v[0] = seg_dot<Strict>(m.v, m.ci, x, m.rp[r], p, hi, stride, acc.v[0]);
+  }
+  __device__ __forceinline__ void finish(int r, const AccT& acc) const { y[r] = acc.v[0]; }
+};
+
+// ---------------------------------------------------------------------------
+// KKT products, two points (current and average) per matrix pass
+// (kkt.hpp:32-39, called twice by evaluate_candidate solver.hpp:255-264).
+// Rows of the ORIGINAL stacked A: ax_c = A xu_c, ax_a = A xu_a.
+template <bool Strict>
+struct KktAxOp {
+  static constexpr bool kStrict = Strict;
+  using AccT = Acc<2>;
+  CsrView a;
+  const double* xc;
+  const double* xa;
+  double* axc;
+  double* axa;
+  __device__ __forceinline__ int len(int r) const { return a.rp[r + 1] - a.rp[r]; }
+  __device__ __forceinline__ void accumulate(int r, int lo, int hi, int lane, int stride,
+                                             AccT& acc) const {
+    const int64_t base = a.rp[r];
+    for (int p = lo + lane; p < hi; p += stride) {
+      const double v = ld_stream(a.v + base + p);
+      const int32_t c = ld_stream(a.ci + base + p);
+      acc.v[0] = madd<Strict>(acc.v[0], v, ld_gather(xc + c));
+      acc.v[1] = madd<Strict>(acc.v[1], v, ld_gather(xa + c));
+    }
+  }
+  __device__ __forceinline__ void finish(int r, const AccT& acc) const {
+    axc[r] = acc.v[0];
+    axa[r] = acc.v[1];
+  }
+};
+
+// Rows j of the ORIGINAL [Q | A']: qx = Q xu, and A'y split into the
+// inequality and equality blocks (kkt.hpp:35-38: aty = aty_i + 1.0*aty_e),
+// for both points.
+template <bool Strict>
+struct KktQAtyOp {
+  static constexpr bool kStrict = Strict;
+  using AccT = Acc<6>;
+  CsrView q, at;
+  int m_ineq;
+  const double *xc, *xa, *yc, *ya;
+  double *qxc, *qxa, *atyc, *atya;
+  __device__ __forceinline__ int len(int r) const {
+    return (q.rp[r + 1] - q.rp[r]) + (at.rp[r + 1] - at.rp[r]);
+  }
+  __device__ __forceinline__ void accumulate(int r, int lo, int hi, int lane, int stride,
+                                             AccT& acc) const {
+    const int q0 = q.rp[r];
+    const int L1 = q.rp[r + 1] - q0;
+    int p = lo + lane;
+    const int e1 = hi < L1 ? hi : L1;
+    for (; p < e1; p += stride) {
+      const double v = ld_stream(q.v + q0 + p);
+      const int32_t c = ld_stream(q.ci + q0 + p);
+      acc.v[0] = madd<Strict>(acc.v[0], v, ld_gather(xc + c));
+      acc.v[1] = madd<Strict>(acc.v[1], v, ld_gather(xa + c));
+    }
+    const int64_t base = static_cast<int64_t>(at.rp[r]) - L1;
+    for (; p < hi; p += stride) {
+      const double v = ld_stream(at.v + base + p);
+      const int32_t i = ld_stream(at.ci + base + p);
+      const double vc = ld_gather(yc + i), va = ld_gather(ya + i);
+      if (i < m_ineq) {
+        acc.v[2] = madd<Strict>(acc.v[2], v, vc);
+        acc.v[4] = madd<Strict>(acc.v[4], v, va);
+      } else {
+        acc.v[3] = madd<Strict>(acc.v[3], v, vc);
+        acc.v[5] = madd<Strict>(acc.v[5], v, va);
+      }
+    }
+  }
+  __device__ __forceinline__ void finish(int j, const AccT& acc) const {
+    qxc[j] = acc.v[0];
+    qxa[j] = acc.v[1];
+    atyc[j] = acc.v[2] + 1.0 * acc.v[3];
+    atya[j] = acc.v[4] + 1.0 * acc.v[5];
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Row measures of the stacked symmetric [[Q, A'], [A, 0]] (scaling.hpp:49-62):
+// primal row j = Q row j then A' row j, dual row i = A row i. Kind 0 max-abs,
+// 1 l2 (sqrt of sum of squares), 2 l1.
+template <bool Strict, int Kind>
+struct MeasureOp {
+  static constexpr bool kStrict = Strict;
+  using AccT = Acc<1, Kind == 0>;
+  CsrView s1, s2;  // s2.rp == nullptr: single segment
+  double* out;
+  __device__ __forceinline__ int len1(int r) const { return s1.rp[r + 1] - s1.rp[r]; }
+  __device__ __forceinline__ int len(int r) const {
+    return len1(r) + (s2.rp ? s2.rp[r + 1] - s2.rp[r] : 0);
+  }
+  __device__ __forceinline__ static double term(double acc, double v) {
+    const double a = fabs(v);
+    if constexpr (Kind == 0) return acc < a ? a : acc;  // std::max(m, a)
+    else if constexpr (Kind == 1) return Strict ? __dadd_rn(acc, __dmul_rn(a, a)) : acc + a * a;
+    else return acc + a;
+  }
+  __device__ __forceinline__ void accumulate(int r, int lo, int hi, int lane, int stride,
+                                             AccT& acc) const {
+    const int L1 = len1(r);
+    int p = lo + lane;
+    const int e1 = hi < L1 ? hi : L1;
+    for (; p < e1; p += stride) acc.v[0] = term(acc.v[0], s1.v[s1.rp[r] + p]);
+    if (s2.rp)
+      for (; p < hi; p += stride) acc.v[0] = term(acc.v[0], s2.v[static_cast<int64_t>(s2.rp[r]) - L1 + p]);
+  }
+  __device__ __forceinline__ void finish(int r, const AccT& acc) const {
+    out[r] = Kind == 1 ? sqrt(acc.v[0]) : acc.v[0];
+  }
+};
+
+}  // namespace rb

@@ -698,7 +698,12 @@ void Engine::solve(rapdhg_result* out, Clock::time_point t0) {
   kernel_ms_[0] = kernel_ms_[1] = 0.0;
   kernel_count_[0] = kernel_count_[1] = 0;
   launches_ = P_->launches;
-  const auto loop_t0 = Clock::now();
+  // loop time on the device timeline: events on the solver's stream bracket
+  // everything from the first candidate evaluation to the final download
+  cudaEvent_t ev0, ev1;
+  RB_CUDA(cudaEventCreate(&ev0));
+  RB_CUDA(cudaEventCreate(&ev1));
+  RB_CUDA(cudaEventRecord(ev0, st_));
 
   // IterateState::zeros (solver.hpp:293)
   cur_ = 0;
@@ -888,7 +893,13 @@ void Engine::solve(rapdhg_result* out, Clock::time_point t0) {
   if (mi_) std::memcpy(out->y_ineq, yall, sizeof(double) * mi_);
   if (m - mi_) std::memcpy(out->y_eq, yall + mi_, sizeof(double) * (m - mi_));
   std::free(yall);
-  out->loop_seconds = std::chrono::duration<double>(Clock::now() - loop_t0).count();
+  RB_CUDA(cudaEventRecord(ev1, st_));
+  RB_CUDA(cudaEventSynchronize(ev1));
+  float loop_ms = 0.f;
+  RB_CUDA(cudaEventElapsedTime(&loop_ms, ev0, ev1));
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  out->loop_seconds = 1e-3 * loop_ms;
   out->setup_seconds = setup_seconds;
   out->solve_seconds = elapsed();
   out->kernel_launches = launches_;

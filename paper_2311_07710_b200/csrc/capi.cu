@@ -114,8 +114,14 @@ int rapdhg_solve(const rapdhg_qp* qp, const rapdhg_config* cfg, rapdhg_result* o
     null_check(out, "out");
     std::memset(out, 0, sizeof(*out));
     require_device();
-    rb::Engine e(*qp, *cfg, t0);
-    e.solve(out, t0);
+    rb::Tracer tr(nullptr);
+    {
+      rb::Engine e(*qp, *cfg, t0);
+      tr.mark("engine setup total");
+      e.solve(out, t0);
+      tr.mark("solve loop + download");
+    }
+    tr.mark("engine teardown");
   });
 }
 

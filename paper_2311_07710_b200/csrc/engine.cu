@@ -453,12 +453,29 @@ double DeviceQP::op_norm_a(const double* av, const double* atv, int max_iters, d
 // Engine
 // ============================================================================
 
+Tracer::Tracer(cudaStream_t s) : on(std::getenv("RAPDHG_TRACE") != nullptr), st(s), t(Clock::now()) {}
+
+void Tracer::mark(const char* what) {
+  if (!on) return;
+  if (st) cudaStreamSynchronize(st);
+  const auto now = Clock::now();
+  std::fprintf(stderr, "[rapdhg] %-30s %9.3f ms\n", what,
+               std::chrono::duration<double, std::milli>(now - t).count());
+  t = now;
+}
+
 Engine::Engine(const rapdhg_qp& p, const rapdhg_config& cfg, Clock::time_point t0) : cfg_(cfg) {
+  Tracer tr(nullptr);
   DeviceQP::validate_dims(p);
+  tr.mark("validate dims (host)");
   RB_CUDA(cudaSetDevice(cfg.device));
   RB_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  tr.st = st_;
+  tr.mark("device + stream");
   P_ = std::make_unique<DeviceQP>(p, cfg.strict_parity != 0, st_);
+  tr.mark("upload, stack, A', schedules");
   P_->validate_symmetry();  // original.validate() (solver.hpp:277)
+  tr.mark("symmetry check");
   validate_config(cfg);     // cfg.validate() (solver.hpp:278)
   n_ = P_->n, m_ = P_->m, mi_ = P_->mi;
 
@@ -474,9 +491,12 @@ Engine::Engine(const rapdhg_qp& p, const rapdhg_config& cfg, Clock::time_point t
     qsv_ = P_->Q.v.get(), asv_ = P_->A.v.get(), atsv_ = P_->AT.v.get();
     csv_ = P_->c.get(), bsv_ = P_->b.get();
   }
+  tr.mark("scaling");
   // norms (solver.hpp:286-289)
   norm_q = 1.01 * P_->op_norm_q(qsv_, 5000, 1e-4, cfg.seed);
+  tr.mark("norm Q (power iteration)");
   norm_a = 1.01 * P_->op_norm_a(asv_, atsv_, 5000, 1e-4, cfg.seed);
+  tr.mark("norm A (power iteration)");
   // primal weight init on the scaled c, b (solver.hpp:296-300)
   if (cfg.primal_weight == RAPDHG_PW_ADAPTIVE) {
     double sc[1], sb[1];
@@ -503,6 +523,7 @@ Engine::Engine(const rapdhg_qp& p, const rapdhg_config& cfg, Clock::time_point t
     for (auto& e : events_) RB_CUDA(cudaEventCreate(&e));
   }
   RB_CUDA(cudaStreamSynchronize(st_));
+  tr.mark("omega init + buffers");
   setup_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
 }
 

@@ -107,9 +107,10 @@ struct PrimalStepOp {
                                              AccT& acc) const {
     const int q0 = q.rp[r];
     const int L1 = q.rp[r + 1] - q0;
-    int p = lo + lane;
+    const int p = lo + lane;
     acc.v[0] = seg_dot<Strict>(q.v, q.ci, xmd, q0, p, hi < L1 ? hi : L1, stride, acc.v[0]);
-    acc.v[1] = seg_dot<Strict>(at.v, at.ci, y, static_cast<int64_t>(at.rp[r]) - L1, p, hi, stride,
+    acc.v[1] = seg_dot<Strict>(at.v, at.ci, y, static_cast<int64_t>(at.rp[r]) - L1,
+                               next_pos(p, stride, L1), hi, stride,
                                acc.v[1]);
   }
   __device__ __forceinline__ void finish(int j, const AccT& acc) const {
@@ -162,13 +163,7 @@ struct KktAxOp {
   __device__ __forceinline__ int len(int r) const { return a.rp[r + 1] - a.rp[r]; }
   __device__ __forceinline__ void accumulate(int r, int lo, int hi, int lane, int stride,
                                              AccT& acc) const {
-    const int64_t base = a.rp[r];
-    for (int p = lo + lane; p < hi; p += stride) {
-      const double v = ld_stream(a.v + base + p);
-      const int32_t c = ld_stream(a.ci + base + p);
-      acc.v[0] = madd<Strict>(acc.v[0], v, ld_gather(xc + c));
-      acc.v[1] = madd<Strict>(acc.v[1], v, ld_gather(xa + c));
-    }
+    seg_dot2<Strict, false>(a.v, a.ci, xc, xa, a.rp[r], lo + lane, hi, stride, 0, acc.v);
   }
   __device__ __forceinline__ void finish(int r, const AccT& acc) const {
     axc[r] = acc.v[0];
@@ -192,35 +187,19 @@ struct KktQAtyOp {
   }
   __device__ __forceinline__ void accumulate(int r, int lo, int hi, int lane, int stride,
                                              AccT& acc) const {
+    // acc: [0] Qx cur, [1] Qx avg, [2] A_i'y cur, [3] A_i'y avg, [4] A_e'y cur, [5] A_e'y avg
     const int q0 = q.rp[r];
     const int L1 = q.rp[r + 1] - q0;
-    int p = lo + lane;
-    const int e1 = hi < L1 ? hi : L1;
-    for (; p < e1; p += stride) {
-      const double v = ld_stream(q.v + q0 + p);
-      const int32_t c = ld_stream(q.ci + q0 + p);
-      acc.v[0] = madd<Strict>(acc.v[0], v, ld_gather(xc + c));
-      acc.v[1] = madd<Strict>(acc.v[1], v, ld_gather(xa + c));
-    }
-    const int64_t base = static_cast<int64_t>(at.rp[r]) - L1;
-    for (; p < hi; p += stride) {
-      const double v = ld_stream(at.v + base + p);
-      const int32_t i = ld_stream(at.ci + base + p);
-      const double vc = ld_gather(yc + i), va = ld_gather(ya + i);
-      if (i < m_ineq) {
-        acc.v[2] = madd<Strict>(acc.v[2], v, vc);
-        acc.v[4] = madd<Strict>(acc.v[4], v, va);
-      } else {
-        acc.v[3] = madd<Strict>(acc.v[3], v, vc);
-        acc.v[5] = madd<Strict>(acc.v[5], v, va);
-      }
-    }
+    const int p = lo + lane;
+    seg_dot2<Strict, false>(q.v, q.ci, xc, xa, q0, p, hi < L1 ? hi : L1, stride, 0, acc.v);
+    seg_dot2<Strict, true>(at.v, at.ci, yc, ya, static_cast<int64_t>(at.rp[r]) - L1,
+                           next_pos(p, stride, L1), hi, stride, m_ineq, acc.v + 2);
   }
   __device__ __forceinline__ void finish(int j, const AccT& acc) const {
     qxc[j] = acc.v[0];
     qxa[j] = acc.v[1];
-    atyc[j] = acc.v[2] + 1.0 * acc.v[3];
-    atya[j] = acc.v[4] + 1.0 * acc.v[5];
+    atyc[j] = acc.v[2] + 1.0 * acc.v[4];
+    atya[j] = acc.v[3] + 1.0 * acc.v[5];
   }
 };
 

@@ -80,17 +80,26 @@ __global__ void __launch_bounds__(kRedBlock) reduce_par_kernel(F f, int64_t n, d
     am_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (am_last && threadIdx.x == 0) {
+  if (am_last) {
     __threadfence();
-    for (int k = 0; k < NT; ++k) {
-      double t = __ldcg(&partials[k]);
-      for (unsigned b = 1; b < gridDim.x; ++b) {
+    // warp w combines outputs k = w, w + 8, ...: lane l sums partials
+    // l, l + 32, ... in order, then a fixed butterfly — deterministic.
+    const int lane = threadIdx.x & 31;
+    for (int k = w; k < NT; k += kRedBlock / 32) {
+      const bool is_sum = k < NS;
+      double t = 0.0;
+      for (unsigned b = lane; b < gridDim.x; b += 32) {
         const double v = __ldcg(&partials[static_cast<int64_t>(b) * NT + k]);
-        t = k < NS ? t + v : fmax(t, v);
+        t = is_sum ? t + v : fmax(t, v);
       }
-      out[k] = t;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const double o = __shfl_xor_sync(0xffffffffu, t, off);
+        t = is_sum ? t + o : fmax(t, o);
+      }
+      if (lane == 0) out[k] = t;
     }
-    *ticket = 0u;  // re-arm for the next launch / graph replay
+    if (threadIdx.x == 0) *ticket = 0u;  // re-arm for the next launch / graph replay
   }
 }
 

@@ -98,33 +98,81 @@ struct Acc {
   }
 };
 
-// Sequential-in-position accumulation of sum_k vals[k] * x[cols[k]] for the
-// positions p = start, start+stride, ... < end of one CSR segment (base = row
-// offset). Unrolled by 4 for memory-level parallelism; the adds stay in
-// position order.
+constexpr int kUnroll = 4;
+
+// First position >= target in the progression p0, p0 + stride, ... (p0 >= 0).
+__device__ __forceinline__ int next_pos(int p0, int stride, int target) {
+  return target <= p0 ? p0 : p0 + ((target - p0 + stride - 1) / stride) * stride;
+}
+
+// Accumulation of sum_k vals[k] * x[cols[k]] over positions p, p+stride, ...
+// < end of one CSR segment (index = base + position). Predicated unroll: all
+// kUnroll loads of a lane are issued together even when the lane has fewer
+// elements left (short rows keep their memory-level parallelism); inactive
+// slots contribute 0*0 = +0, which never changes a sum that started at +0.0
+// (such a sum is never -0), so the adds stay in position order and strict
+// mode remains the reference's sequential sum exactly.
 template <bool Strict>
 __device__ __forceinline__ double seg_dot(const double* __restrict__ vals,
                                           const int32_t* __restrict__ cols,
-                                          const double* __restrict__ x, int64_t base, int& p,
+                                          const double* __restrict__ x, int64_t base, int p,
                                           int end, int stride, double acc) {
-  for (; p + 3 * stride < end; p += 4 * stride) {
-    const int64_t i0 = base + p, i1 = i0 + stride, i2 = i1 + stride, i3 = i2 + stride;
-    const int32_t c0 = ld_stream(cols + i0), c1 = ld_stream(cols + i1);
-    const int32_t c2 = ld_stream(cols + i2), c3 = ld_stream(cols + i3);
-    const double v0 = ld_stream(vals + i0), v1 = ld_stream(vals + i1);
-    const double v2 = ld_stream(vals + i2), v3 = ld_stream(vals + i3);
-    const double x0 = ld_gather(x + c0), x1 = ld_gather(x + c1);
-    const double x2 = ld_gather(x + c2), x3 = ld_gather(x + c3);
-    acc = madd<Strict>(acc, v0, x0);
-    acc = madd<Strict>(acc, v1, x1);
-    acc = madd<Strict>(acc, v2, x2);
-    acc = madd<Strict>(acc, v3, x3);
-  }
-  for (; p < end; p += stride) {
-    const int64_t i = base + p;
-    acc = madd<Strict>(acc, ld_stream(vals + i), ld_gather(x + ld_stream(cols + i)));
+  for (; p < end; p += kUnroll * stride) {
+    int32_t c[kUnroll];
+    double v[kUnroll], xv[kUnroll];
+#pragma unroll
+    for (int k = 0; k < kUnroll; ++k) {
+      const bool ok = p + k * stride < end;
+      const int64_t i = base + p + k * stride;
+      c[k] = ok ? ld_stream(cols + i) : 0;
+      v[k] = ok ? ld_stream(vals + i) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < kUnroll; ++k) xv[k] = (p + k * stride < end) ? ld_gather(x + c[k]) : 0.0;
+#pragma unroll
+    for (int k = 0; k < kUnroll; ++k) acc = madd<Strict>(acc, v[k], xv[k]);
   }
   return acc;
+}
+
+// Two right-hand sides in one pass over the matrix (the relKKT products of the
+// current iterate and of the average, kkt.hpp:32-39). With Split, entries
+// whose column is < split go to (a[0], a[1]) and the others to (a[2], a[3])
+// — the inequality / equality blocks of A'y (kkt.hpp:35-38); otherwise
+// a[0] += v*xa, a[1] += v*xb. Same predicated unroll as seg_dot.
+template <bool Strict, bool Split>
+__device__ __forceinline__ void seg_dot2(const double* __restrict__ vals,
+                                         const int32_t* __restrict__ cols,
+                                         const double* __restrict__ xa,
+                                         const double* __restrict__ xb, int64_t base, int p,
+                                         int end, int stride, int split, double* a) {
+  for (; p < end; p += kUnroll * stride) {
+    int32_t c[kUnroll];
+    double v[kUnroll], ua[kUnroll], ub[kUnroll];
+#pragma unroll
+    for (int k = 0; k < kUnroll; ++k) {
+      const bool ok = p + k * stride < end;
+      const int64_t i = base + p + k * stride;
+      c[k] = ok ? ld_stream(cols + i) : 0;
+      v[k] = ok ? ld_stream(vals + i) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < kUnroll; ++k) {
+      const bool ok = p + k * stride < end;
+      ua[k] = ok ? ld_gather(xa + c[k]) : 0.0;
+      ub[k] = ok ? ld_gather(xb + c[k]) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < kUnroll; ++k) {
+      if (Split && c[k] >= split) {
+        a[2] = madd<Strict>(a[2], v[k], ua[k]);
+        a[3] = madd<Strict>(a[3], v[k], ub[k]);
+      } else {
+        a[0] = madd<Strict>(a[0], v[k], ua[k]);
+        a[1] = madd<Strict>(a[1], v[k], ub[k]);
+      }
+    }
+  }
 }
 
 // ---- the kernel --------------------------------------------------------------
@@ -250,17 +298,23 @@ struct Schedule {
   int32_t bin_rows[kNumBins] = {};
 };
 
-// Bin of a row of length L (fast mode).
-__host__ __device__ inline int bin_of_len(int64_t L) {
-  if (L <= 2) return 0;
-  if (L <= 4) return 1;
-  if (L <= 8) return 2;
-  if (L <= 16) return 3;
-  if (L <= 32) return 4;
-  if (L <= 2048) return 5;
+// Bin of a row of length L (fast mode): the fewest lanes V (power of two, up to
+// a warp) that leave each lane at most `epl` elements; rows longer than
+// `block_min` get a whole block, rows longer than kSplitLen several blocks.
+__host__ __device__ inline int bin_of_len(int64_t L, int epl, int block_min) {
+  for (int b = 0; b < kNumVBins - 1; ++b)
+    if (L <= static_cast<int64_t>(epl) << b) return b;
+  if (L <= block_min) return kNumVBins - 1;
   if (L <= kSplitLen) return kBinBlock;
   return kBinSplit;
 }
+
+// Schedule tuning (env RAPDHG_EPL / RAPDHG_BLOCK_MIN override the defaults).
+struct SchedParams {
+  int epl = 8;
+  int block_min = 4096;
+  static SchedParams from_env();
+};
 
 // lengths: device array of per-row lengths (int32). strict: single V=1 bin in
 // natural row order.

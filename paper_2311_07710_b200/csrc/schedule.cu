@@ -6,6 +6,8 @@
 // than kSplitLen.
 #include <cub/device/device_radix_sort.cuh>
 
+#include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "rowwise.cuh"
@@ -15,16 +17,24 @@ namespace rb {
 namespace {
 
 __global__ void bin_kernel(int32_t* bin, int32_t* idx, const int32_t* len, int64_t rows,
-                           int* counts) {
+                           int* counts, int epl, int block_min) {
   const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (r >= rows) return;
-  const int b = bin_of_len(len[r]);
+  const int b = bin_of_len(len[r], epl, block_min);
   bin[r] = b;
   idx[r] = static_cast<int32_t>(r);
   atomicAdd(&counts[b], 1);  // integer counts: exact
 }
 
 }  // namespace
+
+SchedParams SchedParams::from_env() {
+  SchedParams p;
+  if (const char* e = std::getenv("RAPDHG_EPL")) p.epl = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("RAPDHG_BLOCK_MIN")) p.block_min = std::max(32 * p.epl, std::atoi(e));
+  if (p.block_min > kSplitLen) p.block_min = kSplitLen;
+  return p;
+}
 
 void build_schedule(Schedule& sch, const int32_t* d_len, int64_t rows, bool strict,
                     cudaStream_t st) {
@@ -42,13 +52,14 @@ void build_schedule(Schedule& sch, const int32_t* d_len, int64_t rows, bool stri
     sch.bin_rows[0] = static_cast<int32_t>(rows);
     return;
   }
+  const SchedParams sp = SchedParams::from_env();
   DevBuf<int32_t> bins(rows), idx(rows), bins_sorted(rows);
   DevBuf<int> counts(kNumBins);
   counts.zero(st);
   sch.perm.alloc(rows);
   if (rows) {
     bin_kernel<<<static_cast<unsigned>(ceil_div(rows, 256)), 256, 0, st>>>(
-        bins.get(), idx.get(), d_len, rows, counts.get());
+        bins.get(), idx.get(), d_len, rows, counts.get(), sp.epl, sp.block_min);
     RB_LAUNCH_CHECK();
     std::size_t tb = 0;
     RB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, bins.get(), bins_sorted.get(), idx.get(),

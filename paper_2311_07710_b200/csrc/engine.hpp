@@ -22,6 +22,7 @@
 namespace rb {
 
 constexpr int kMaxChunk = 64;
+constexpr int kProfilePeriod = 8;  // profile_kernels: time every 8th chunk
 
 using Clock = std::chrono::steady_clock;
 
@@ -121,7 +122,7 @@ class Engine {
   };
   Cand evaluate();
   void run_chunk(int len);
-  void launch_chunk_body(int len, int cur);
+  void launch_chunk_body(int len, int cur, bool prof);
   void restart(bool from_avg, double* dx, double* dy);
   void download_point(const double* xu, const double* yu, double* x, double* y);
 
@@ -143,7 +144,8 @@ class Engine {
   PinnedBuf<IterParams> params_h_;
   DevBuf<long long> bad_;
   PinnedBuf<long long> bad_h_;
-  std::map<std::pair<int, int>, cudaGraphExec_t> graphs_;
+  std::map<int, cudaGraphExec_t> graphs_;  // key: len, parity, profiled
+  int64_t chunk_counter_ = 0;
   std::vector<cudaEvent_t> events_;
   double kernel_ms_[2] = {0, 0};
   int64_t kernel_count_[2] = {0, 0};

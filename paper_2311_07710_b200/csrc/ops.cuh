@@ -49,6 +49,7 @@ struct CsrView {
 template <bool Strict>
 struct DualStepOp {
   static constexpr bool kStrict = Strict;
+  static constexpr int kWideUnroll = 8;  // long A rows: 8 loads in flight per lane
   using AccT = Acc<1>;
   CsrView a;
   const double* w;
@@ -60,10 +61,11 @@ struct DualStepOp {
   int it;
   long long* bad;
   __device__ __forceinline__ int len(int r) const { return a.rp[r + 1] - a.rp[r]; }
+  template <int U>
   __device__ __forceinline__ void accumulate(int r, int lo, int hi, int lane, int stride,
                                              AccT& acc) const {
     int p = lo + lane;
-    acc.v[0] = seg_dot<Strict>(a.v, a.ci, w, a.rp[r], p, hi, stride, acc.v[0]);
+    acc.v[0] = seg_dot<Strict, U>(a.v, a.ci, w, a.rp[r], p, hi, stride, acc.v[0]);
   }
   __device__ __forceinline__ void finish(int i, const AccT& acc) const {
     const IterParams& q = P[it];
@@ -87,6 +89,7 @@ struct DualStepOp {
 template <bool Strict>
 struct PrimalStepOp {
   static constexpr bool kStrict = Strict;
+  static constexpr int kWideUnroll = kUnroll;
   using AccT = Acc<2>;
   CsrView q, at;
   const double* xmd;  // gathered by Q
@@ -103,13 +106,14 @@ struct PrimalStepOp {
   __device__ __forceinline__ int len(int r) const {
     return (q.rp[r + 1] - q.rp[r]) + (at.rp[r + 1] - at.rp[r]);
   }
+  template <int U>
   __device__ __forceinline__ void accumulate(int r, int lo, int hi, int lane, int stride,
                                              AccT& acc) const {
     const int q0 = q.rp[r];
     const int L1 = q.rp[r + 1] - q0;
     const int p = lo + lane;
-    acc.v[0] = seg_dot<Strict>(q.v, q.ci, xmd, q0, p, hi < L1 ? hi : L1, stride, acc.v[0]);
-    acc.v[1] = seg_dot<Strict>(at.v, at.ci, y, static_cast<int64_t>(at.rp[r]) - L1,
+    acc.v[0] = seg_dot<Strict, U>(q.v, q.ci, xmd, q0, p, hi < L1 ? hi : L1, stride, acc.v[0]);
+    acc.v[1] = seg_dot<Strict, U>(at.v, at.ci, y, static_cast<int64_t>(at.rp[r]) - L1,
                                next_pos(p, stride, L1), hi, stride,
                                acc.v[1]);
   }
@@ -134,15 +138,17 @@ struct PrimalStepOp {
 template <bool Strict>
 struct SpmvOp {
   static constexpr bool kStrict = Strict;
+  static constexpr int kWideUnroll = kUnroll;
   using AccT = Acc<1>;
   CsrView m;
   const double* x;
   double* y;
   __device__ __forceinline__ int len(int r) const { return m.rp[r + 1] - m.rp[r]; }
+  template <int U>
   __device__ __forceinline__ void accumulate(int r, int lo, int hi, int lane, int stride,
                                              AccT& acc) const {
     int p = lo + lane;
-    acc.v[0] = seg_dot<Strict>(m.v, m.ci, x, m.rp[r], p, hi, stride, acc.v[0]);
+    acc.v[0] = seg_dot<Strict, U>(m.v, m.ci, x, m.rp[r], p, hi, stride, acc.v[0]);
   }
   __device__ __forceinline__ void finish(int r, const AccT& acc) const { y[r] = acc.v[0]; }
 };
@@ -154,6 +160,7 @@ struct SpmvOp {
 template <bool Strict>
 struct KktAxOp {
   static constexpr bool kStrict = Strict;
+  static constexpr int kWideUnroll = kUnroll;
   using AccT = Acc<2>;
   CsrView a;
   const double* xc;
@@ -161,9 +168,10 @@ struct KktAxOp {
   double* axc;
   double* axa;
   __device__ __forceinline__ int len(int r) const { return a.rp[r + 1] - a.rp[r]; }
+  template <int U>
   __device__ __forceinline__ void accumulate(int r, int lo, int hi, int lane, int stride,
                                              AccT& acc) const {
-    seg_dot2<Strict, false>(a.v, a.ci, xc, xa, a.rp[r], lo + lane, hi, stride, 0, acc.v);
+    seg_dot2<Strict, false, U>(a.v, a.ci, xc, xa, a.rp[r], lo + lane, hi, stride, 0, acc.v);
   }
   __device__ __forceinline__ void finish(int r, const AccT& acc) const {
     axc[r] = acc.v[0];
@@ -177,6 +185,7 @@ struct KktAxOp {
 template <bool Strict>
 struct KktQAtyOp {
   static constexpr bool kStrict = Strict;
+  static constexpr int kWideUnroll = kUnroll;
   using AccT = Acc<6>;
   CsrView q, at;
   int m_ineq;
@@ -185,14 +194,15 @@ struct KktQAtyOp {
   __device__ __forceinline__ int len(int r) const {
     return (q.rp[r + 1] - q.rp[r]) + (at.rp[r + 1] - at.rp[r]);
   }
+  template <int U>
   __device__ __forceinline__ void accumulate(int r, int lo, int hi, int lane, int stride,
                                              AccT& acc) const {
     // acc: [0] Qx cur, [1] Qx avg, [2] A_i'y cur, [3] A_i'y avg, [4] A_e'y cur, [5] A_e'y avg
     const int q0 = q.rp[r];
     const int L1 = q.rp[r + 1] - q0;
     const int p = lo + lane;
-    seg_dot2<Strict, false>(q.v, q.ci, xc, xa, q0, p, hi < L1 ? hi : L1, stride, 0, acc.v);
-    seg_dot2<Strict, true>(at.v, at.ci, yc, ya, static_cast<int64_t>(at.rp[r]) - L1,
+    seg_dot2<Strict, false, U>(q.v, q.ci, xc, xa, q0, p, hi < L1 ? hi : L1, stride, 0, acc.v);
+    seg_dot2<Strict, true, U>(at.v, at.ci, yc, ya, static_cast<int64_t>(at.rp[r]) - L1,
                            next_pos(p, stride, L1), hi, stride, m_ineq, acc.v + 2);
   }
   __device__ __forceinline__ void finish(int j, const AccT& acc) const {
@@ -210,6 +220,7 @@ struct KktQAtyOp {
 template <bool Strict, int Kind>
 struct MeasureOp {
   static constexpr bool kStrict = Strict;
+  static constexpr int kWideUnroll = kUnroll;
   using AccT = Acc<1, Kind == 0>;
   CsrView s1, s2;  // s2.rp == nullptr: single segment
   double* out;
@@ -223,6 +234,7 @@ struct MeasureOp {
     else if constexpr (Kind == 1) return Strict ? __dadd_rn(acc, __dmul_rn(a, a)) : acc + a * a;
     else return acc + a;
   }
+  template <int U>
   __device__ __forceinline__ void accumulate(int r, int lo, int hi, int lane, int stride,
                                              AccT& acc) const {
     const int L1 = len1(r);

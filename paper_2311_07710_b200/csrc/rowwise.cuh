@@ -98,7 +98,9 @@ struct Acc {
   }
 };
 
-constexpr int kUnroll = 4;
+constexpr int kUnroll = 4;  // loads in flight per lane (narrow rows, block/split)
+// Ops whose long rows (>= 16 lanes) want more loads in flight declare
+// kWideUnroll = 8 (costs registers, so only where it measured faster).
 
 // First position >= target in the progression p0, p0 + stride, ... (p0 >= 0).
 __device__ __forceinline__ int next_pos(int p0, int stride, int target) {
@@ -112,25 +114,25 @@ __device__ __forceinline__ int next_pos(int p0, int stride, int target) {
 // slots contribute 0*0 = +0, which never changes a sum that started at +0.0
 // (such a sum is never -0), so the adds stay in position order and strict
 // mode remains the reference's sequential sum exactly.
-template <bool Strict>
+template <bool Strict, int U = kUnroll>
 __device__ __forceinline__ double seg_dot(const double* __restrict__ vals,
                                           const int32_t* __restrict__ cols,
                                           const double* __restrict__ x, int64_t base, int p,
                                           int end, int stride, double acc) {
-  for (; p < end; p += kUnroll * stride) {
-    int32_t c[kUnroll];
-    double v[kUnroll], xv[kUnroll];
+  for (; p < end; p += U * stride) {
+    int32_t c[U];
+    double v[U], xv[U];
 #pragma unroll
-    for (int k = 0; k < kUnroll; ++k) {
+    for (int k = 0; k < U; ++k) {
       const bool ok = p + k * stride < end;
       const int64_t i = base + p + k * stride;
       c[k] = ok ? ld_stream(cols + i) : 0;
       v[k] = ok ? ld_stream(vals + i) : 0.0;
     }
 #pragma unroll
-    for (int k = 0; k < kUnroll; ++k) xv[k] = (p + k * stride < end) ? ld_gather(x + c[k]) : 0.0;
+    for (int k = 0; k < U; ++k) xv[k] = (p + k * stride < end) ? ld_gather(x + c[k]) : 0.0;
 #pragma unroll
-    for (int k = 0; k < kUnroll; ++k) acc = madd<Strict>(acc, v[k], xv[k]);
+    for (int k = 0; k < U; ++k) acc = madd<Strict>(acc, v[k], xv[k]);
   }
   return acc;
 }
@@ -140,30 +142,30 @@ __device__ __forceinline__ double seg_dot(const double* __restrict__ vals,
 // whose column is < split go to (a[0], a[1]) and the others to (a[2], a[3])
 // — the inequality / equality blocks of A'y (kkt.hpp:35-38); otherwise
 // a[0] += v*xa, a[1] += v*xb. Same predicated unroll as seg_dot.
-template <bool Strict, bool Split>
+template <bool Strict, bool Split, int U = kUnroll>
 __device__ __forceinline__ void seg_dot2(const double* __restrict__ vals,
                                          const int32_t* __restrict__ cols,
                                          const double* __restrict__ xa,
                                          const double* __restrict__ xb, int64_t base, int p,
                                          int end, int stride, int split, double* a) {
-  for (; p < end; p += kUnroll * stride) {
-    int32_t c[kUnroll];
-    double v[kUnroll], ua[kUnroll], ub[kUnroll];
+  for (; p < end; p += U * stride) {
+    int32_t c[U];
+    double v[U], ua[U], ub[U];
 #pragma unroll
-    for (int k = 0; k < kUnroll; ++k) {
+    for (int k = 0; k < U; ++k) {
       const bool ok = p + k * stride < end;
       const int64_t i = base + p + k * stride;
       c[k] = ok ? ld_stream(cols + i) : 0;
       v[k] = ok ? ld_stream(vals + i) : 0.0;
     }
 #pragma unroll
-    for (int k = 0; k < kUnroll; ++k) {
+    for (int k = 0; k < U; ++k) {
       const bool ok = p + k * stride < end;
       ua[k] = ok ? ld_gather(xa + c[k]) : 0.0;
       ub[k] = ok ? ld_gather(xb + c[k]) : 0.0;
     }
 #pragma unroll
-    for (int k = 0; k < kUnroll; ++k) {
+    for (int k = 0; k < U; ++k) {
       if (Split && c[k] >= split) {
         a[2] = madd<Strict>(a[2], v[k], ua[k]);
         a[3] = madd<Strict>(a[3], v[k], ub[k]);
@@ -187,7 +189,7 @@ __device__ __forceinline__ void run_vlane(const Op& op, const SchedView& s, cons
   const int r = valid ? (s.perm ? s.perm[slot] : slot) : 0;
   typename Op::AccT a;
   a.zero();
-  if (valid) op.accumulate(r, 0, op.len(r), lane, V, a);
+  if (valid) op.template accumulate<(V >= 16 ? Op::kWideUnroll : kUnroll)>(r, 0, op.len(r), lane, V, a);
   a.template reduce_lanes<V>();  // all lanes participate (invalid ones hold 0)
   if (valid && lane == 0) op.finish(r, a);
 }
@@ -217,7 +219,7 @@ __device__ __forceinline__ void run_block_row(const Op& op, const SchedView& s, 
   const int r = s.perm ? s.perm[slot] : slot;
   typename Op::AccT a;
   a.zero();
-  op.accumulate(r, 0, op.len(r), threadIdx.x, kBlock, a);
+  op.template accumulate<kUnroll>(r, 0, op.len(r), threadIdx.x, kBlock, a);
   block_reduce<Op>(a);
   if (threadIdx.x == 0) op.finish(r, a);
 }
@@ -229,7 +231,7 @@ __device__ __forceinline__ void run_split(const Op& op, const SchedView& s, cons
   const int r = s.seg_row[seg];
   typename Op::AccT a;
   a.zero();
-  op.accumulate(r, s.seg_lo[seg], s.seg_hi[seg], threadIdx.x, kBlock, a);
+  op.template accumulate<kUnroll>(r, s.seg_lo[seg], s.seg_hi[seg], threadIdx.x, kBlock, a);
   block_reduce<Op>(a);
   __shared__ bool last;
   if (threadIdx.x == 0) {
@@ -255,10 +257,13 @@ __device__ __forceinline__ void run_split(const Op& op, const SchedView& s, cons
 
 template <class Op>
 __global__ void __launch_bounds__(kBlock) rowwise_kernel(const Op op, const SchedView s) {
+  // bins occupy disjoint block ranges (heavy bins first, see schedule.cu)
   int bin = 0;
 #pragma unroll
-  for (int b = 0; b < kNumBins - 1; ++b)
-    if (static_cast<int>(blockIdx.x) >= s.bins[bin].blk_end) ++bin;
+  for (int b = 1; b < kNumBins; ++b)
+    if (static_cast<int>(blockIdx.x) >= s.bins[b].blk_begin &&
+        static_cast<int>(blockIdx.x) < s.bins[b].blk_end)
+      bin = b;
   const BinDesc bd = s.bins[bin];
   if (static_cast<int>(blockIdx.x) < bd.blk_begin || static_cast<int>(blockIdx.x) >= bd.blk_end) return;
   if constexpr (Op::kStrict) {
@@ -311,7 +316,7 @@ __host__ __device__ inline int bin_of_len(int64_t L, int epl, int block_min) {
 
 // Schedule tuning (env RAPDHG_EPL / RAPDHG_BLOCK_MIN override the defaults).
 struct SchedParams {
-  int epl = 8;
+  int epl = 16;
   int block_min = 4096;
   static SchedParams from_env();
 };

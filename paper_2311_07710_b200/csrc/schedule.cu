@@ -75,16 +75,15 @@ void build_schedule(Schedule& sch, const int32_t* d_len, int64_t rows, bool stri
   RB_CUDA(cudaStreamSynchronize(st));
 
   int32_t row = 0, blk = 0;
+  int32_t nblk[kNumBins];
   for (int b = 0; b < kNumBins; ++b) {
     const int32_t cnt = h_counts[b];
     sch.bin_rows[b] = cnt;
-    int32_t nblk;
-    if (b < kNumVBins) nblk = static_cast<int32_t>(ceil_div(cnt, kBlock >> b));  // V = 1 << b
-    else if (b == kBinBlock) nblk = cnt;
-    else nblk = 0;  // split: set below
-    v.bins[b] = {row, row + cnt, blk, blk + nblk};
+    if (b < kNumVBins) nblk[b] = static_cast<int32_t>(ceil_div(cnt, kBlock >> b));  // V = 1 << b
+    else if (b == kBinBlock) nblk[b] = cnt;
+    else nblk[b] = 0;  // split: set below
+    v.bins[b] = {row, row + cnt, 0, 0};
     row += cnt;
-    blk += nblk;
   }
   // split rows: one block per kSplitLen-long segment
   const int32_t nsplit = h_counts[kBinSplit];
@@ -121,8 +120,15 @@ void build_schedule(Schedule& sch, const int32_t* d_len, int64_t rows, bool stri
     sch.seg_first.upload(sfirst.data(), nseg, st);
     sch.seg_count.upload(scount.data(), nseg, st);
     RB_CUDA(cudaStreamSynchronize(st));
-    v.bins[kBinSplit].blk_end = v.bins[kBinSplit].blk_begin + static_cast<int32_t>(nseg);
-    blk += static_cast<int32_t>(nseg);
+    nblk[kBinSplit] = static_cast<int32_t>(nseg);
+  }
+  // Heavy bins get the lowest block indices: blocks are dispatched roughly in
+  // index order, so the long rows start first and the many light blocks fill
+  // the tail instead of the heavy ones forming it.
+  for (int b = kNumBins - 1; b >= 0; --b) {
+    v.bins[b].blk_begin = blk;
+    v.bins[b].blk_end = blk + nblk[b];
+    blk += nblk[b];
   }
   v.perm = sch.perm.get();
   v.seg_row = sch.seg_row.get();

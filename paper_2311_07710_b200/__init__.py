@@ -38,7 +38,8 @@ import numpy as np
 from . import abi
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librapdhg_b200.so")
+# RAPDHG_LIB selects an alternative build of the same library (A/B kernel variants)
+LIB_PATH = os.environ.get("RAPDHG_LIB") or os.path.join(_HERE, "librapdhg_b200.so")
 
 
 class InvalidArgument(ValueError):

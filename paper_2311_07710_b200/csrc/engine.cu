@@ -254,19 +254,23 @@ DeviceQP::DeviceQP(const rapdhg_qp& p, bool strict_, cudaStream_t st_)
   b.alloc(m);
   b.upload(p.b_ineq, mi, st);
   if (me) RB_CUDA(cudaMemcpyAsync(b.get() + mi, p.b_eq, sizeof(double) * me, cudaMemcpyHostToDevice, st));
-  red.init(st);
+  red.init(std::max<int64_t>(n, m), st);
   red_out.alloc(64);
   red_host.alloc(64);
   // schedules (patterns only; shared by original and scaled values)
   DevBuf<int32_t> len;
   row_lengths(len, A.rp.get(), nullptr, A.rows, st);
   build_schedule(sch_dual, len.get(), A.rows, strict, st);
+  choose_windows(sch_dual, A.ci.get(), A.nnz, n, nullptr, 0, 0, st);
   row_lengths(len, Q.rp.get(), AT.rp.get(), n, st);
   build_schedule(sch_primal, len.get(), n, strict, st);
+  choose_windows(sch_primal, Q.ci.get(), Q.nnz, n, AT.ci.get(), AT.nnz, m, st);
   row_lengths(len, Q.rp.get(), nullptr, n, st);
   build_schedule(sch_q, len.get(), n, strict, st);
+  choose_windows(sch_q, Q.ci.get(), Q.nnz, n, nullptr, 0, 0, st);
   row_lengths(len, AT.rp.get(), nullptr, n, st);
   build_schedule(sch_at, len.get(), n, strict, st);
+  choose_windows(sch_at, AT.ci.get(), AT.nnz, m, nullptr, 0, 0, st);
   RB_CUDA(cudaStreamSynchronize(st));
 }
 

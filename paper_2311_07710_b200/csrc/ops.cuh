@@ -16,6 +16,10 @@
 
 #include "rowwise.cuh"
 
+#ifndef RB_DUAL_UNROLL
+#define RB_DUAL_UNROLL 4  // 8 measured slower on C2/C4 (register pressure)
+#endif
+
 namespace rb {
 
 // Per-iteration scalars of one inner step, computed on the host for a whole
@@ -49,7 +53,8 @@ struct CsrView {
 template <bool Strict>
 struct DualStepOp {
   static constexpr bool kStrict = Strict;
-  static constexpr int kWideUnroll = 8;  // long A rows: 8 loads in flight per lane
+  static constexpr int kWideUnroll = RB_DUAL_UNROLL;  // long A rows: loads in flight per lane
+  static constexpr bool kStageWindows = true;
   using AccT = Acc<1>;
   CsrView a;
   const double* w;
@@ -63,10 +68,10 @@ struct DualStepOp {
   __device__ __forceinline__ int len(int r) const { return a.rp[r + 1] - a.rp[r]; }
   template <int U>
   __device__ __forceinline__ void accumulate(int r, int lo, int hi, int lane, int stride,
-                                             AccT& acc) const {
-    int p = lo + lane;
-    acc.v[0] = seg_dot<Strict, U>(a.v, a.ci, w, a.rp[r], p, hi, stride, acc.v[0]);
+                                             AccT& acc, const Gather* g) const {
+    acc.v[0] = seg_dot<Strict, U>(a.v, a.ci, g[0], a.rp[r], lo + lane, hi, stride, acc.v[0]);
   }
+  __device__ __forceinline__ const double* gather_src(int) const { return w; }
   __device__ __forceinline__ void finish(int i, const AccT& acc) const {
     const IterParams& q = P[it];
     double yi = y[i];
@@ -90,6 +95,7 @@ template <bool Strict>
 struct PrimalStepOp {
   static constexpr bool kStrict = Strict;
   static constexpr int kWideUnroll = kUnroll;
+  static constexpr bool kStageWindows = true;
   using AccT = Acc<2>;
   CsrView q, at;
   const double* xmd;  // gathered by Q
@@ -108,15 +114,16 @@ struct PrimalStepOp {
   }
   template <int U>
   __device__ __forceinline__ void accumulate(int r, int lo, int hi, int lane, int stride,
-                                             AccT& acc) const {
+                                             AccT& acc, const Gather* g) const {
     const int q0 = q.rp[r];
     const int L1 = q.rp[r + 1] - q0;
     const int p = lo + lane;
-    acc.v[0] = seg_dot<Strict, U>(q.v, q.ci, xmd, q0, p, hi < L1 ? hi : L1, stride, acc.v[0]);
-    acc.v[1] = seg_dot<Strict, U>(at.v, at.ci, y, static_cast<int64_t>(at.rp[r]) - L1,
+    acc.v[0] = seg_dot<Strict, U>(q.v, q.ci, g[0], q0, p, hi < L1 ? hi : L1, stride, acc.v[0]);
+    acc.v[1] = seg_dot<Strict, U>(at.v, at.ci, g[1], static_cast<int64_t>(at.rp[r]) - L1,
                                next_pos(p, stride, L1), hi, stride,
                                acc.v[1]);
   }
+  __device__ __forceinline__ const double* gather_src(int slot) const { return slot ? y : xmd; }
   __device__ __forceinline__ void finish(int j, const AccT& acc) const {
     const IterParams& p = P[it];
     const double xo = x_in[j];
@@ -139,6 +146,7 @@ template <bool Strict>
 struct SpmvOp {
   static constexpr bool kStrict = Strict;
   static constexpr int kWideUnroll = kUnroll;
+  static constexpr bool kStageWindows = true;
   using AccT = Acc<1>;
   CsrView m;
   const double* x;
@@ -146,10 +154,10 @@ struct SpmvOp {
   __device__ __forceinline__ int len(int r) const { return m.rp[r + 1] - m.rp[r]; }
   template <int U>
   __device__ __forceinline__ void accumulate(int r, int lo, int hi, int lane, int stride,
-                                             AccT& acc) const {
-    int p = lo + lane;
-    acc.v[0] = seg_dot<Strict, U>(m.v, m.ci, x, m.rp[r], p, hi, stride, acc.v[0]);
+                                             AccT& acc, const Gather* g) const {
+    acc.v[0] = seg_dot<Strict, U>(m.v, m.ci, g[0], m.rp[r], lo + lane, hi, stride, acc.v[0]);
   }
+  __device__ __forceinline__ const double* gather_src(int) const { return x; }
   __device__ __forceinline__ void finish(int r, const AccT& acc) const { y[r] = acc.v[0]; }
 };
 
@@ -161,6 +169,8 @@ template <bool Strict>
 struct KktAxOp {
   static constexpr bool kStrict = Strict;
   static constexpr int kWideUnroll = kUnroll;
+  static constexpr bool kStageWindows = false;
+  __device__ __forceinline__ const double* gather_src(int) const { return nullptr; }
   using AccT = Acc<2>;
   CsrView a;
   const double* xc;
@@ -170,7 +180,7 @@ struct KktAxOp {
   __device__ __forceinline__ int len(int r) const { return a.rp[r + 1] - a.rp[r]; }
   template <int U>
   __device__ __forceinline__ void accumulate(int r, int lo, int hi, int lane, int stride,
-                                             AccT& acc) const {
+                                             AccT& acc, const Gather* g) const {
     seg_dot2<Strict, false, U>(a.v, a.ci, xc, xa, a.rp[r], lo + lane, hi, stride, 0, acc.v);
   }
   __device__ __forceinline__ void finish(int r, const AccT& acc) const {
@@ -186,6 +196,8 @@ template <bool Strict>
 struct KktQAtyOp {
   static constexpr bool kStrict = Strict;
   static constexpr int kWideUnroll = kUnroll;
+  static constexpr bool kStageWindows = false;
+  __device__ __forceinline__ const double* gather_src(int) const { return nullptr; }
   using AccT = Acc<6>;
   CsrView q, at;
   int m_ineq;
@@ -196,7 +208,7 @@ struct KktQAtyOp {
   }
   template <int U>
   __device__ __forceinline__ void accumulate(int r, int lo, int hi, int lane, int stride,
-                                             AccT& acc) const {
+                                             AccT& acc, const Gather* g) const {
     // acc: [0] Qx cur, [1] Qx avg, [2] A_i'y cur, [3] A_i'y avg, [4] A_e'y cur, [5] A_e'y avg
     const int q0 = q.rp[r];
     const int L1 = q.rp[r + 1] - q0;
@@ -221,6 +233,8 @@ template <bool Strict, int Kind>
 struct MeasureOp {
   static constexpr bool kStrict = Strict;
   static constexpr int kWideUnroll = kUnroll;
+  static constexpr bool kStageWindows = false;
+  __device__ __forceinline__ const double* gather_src(int) const { return nullptr; }
   using AccT = Acc<1, Kind == 0>;
   CsrView s1, s2;  // s2.rp == nullptr: single segment
   double* out;
@@ -236,7 +250,7 @@ struct MeasureOp {
   }
   template <int U>
   __device__ __forceinline__ void accumulate(int r, int lo, int hi, int lane, int stride,
-                                             AccT& acc) const {
+                                             AccT& acc, const Gather* g) const {
     const int L1 = len1(r);
     int p = lo + lane;
     const int e1 = hi < L1 ? hi : L1;

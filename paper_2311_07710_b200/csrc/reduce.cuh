@@ -3,11 +3,15 @@
 // The reference sums sequentially (vec.hpp:14-35, kkt.hpp:43-69). Two modes:
 //  * strict: one thread walks i = 0..N-1 in order — the reference's exact
 //    association, bit-identical results;
-//  * fast: a grid whose size is a fixed function of N; thread t sums i = t,
-//    t+G*256, ... in order, the block combines lanes by a fixed butterfly and
-//    warps in index order, and the LAST-arriving block (ticket counter) sums
-//    the per-block partials in block order. The result never depends on
-//    scheduling, so runs are bit-reproducible without float atomics.
+//  * fast: the index space is cut into fixed CHUNKS of kRedChunk elements
+//    (chunk c = [c*kRedChunk, (c+1)*kRedChunk) in GLOBAL indices). One block
+//    reduces one chunk with a fixed pattern (thread-sequential, lane butterfly,
+//    warps in order) into partial[c]; the partials are then combined by a
+//    fixed lane-strided pass + butterfly. The result depends only on N — not
+//    on scheduling, and not on how the index space is split across GPUs as
+//    long as shard boundaries are multiples of kRedChunk (the row-sharded
+//    solver aligns them), so a sharded solve reduces bit-identically to the
+//    single-GPU one. No float atomics.
 // Maxima are order-free and therefore identical in both modes.
 //
 // A functor F supplies the terms: `void operator()(int64_t i, double* s,
@@ -23,12 +27,10 @@
 namespace rb {
 
 constexpr int kRedBlock = 256;
-constexpr int kRedMaxGrid = 2 * kSMs;
+constexpr int kRedChunk = 2048;  // elements per chunk (8 per thread)
+constexpr int kRedMaxOut = 32;
 
-inline int reduce_grid(int64_t n) {
-  const int64_t g = ceil_div(n, kRedBlock * 4);
-  return static_cast<int>(g < 1 ? 1 : (g > kRedMaxGrid ? kRedMaxGrid : g));
-}
+inline int64_t reduce_chunks(int64_t n) { return n > 0 ? ceil_div(n, kRedChunk) : 1; }
 
 template <int NS, int NM, class F>
 __global__ void reduce_seq_kernel(F f, int64_t n, double* out) {
@@ -40,19 +42,48 @@ __global__ void reduce_seq_kernel(F f, int64_t n, double* out) {
   for (int k = 0; k < NM; ++k) out[NS + k] = mx[k];
 }
 
-template <int NS, int NM, class F>
-__global__ void __launch_bounds__(kRedBlock) reduce_par_kernel(F f, int64_t n, double* partials,
-                                                                unsigned* ticket, double* out) {
+// Fixed combine of partials[0..nchunks) (row-major, NT values each) into out,
+// run by one block: warp w handles outputs k = w, w+8, ...; lane l folds
+// partials l, l+32, ... in order, then a fixed butterfly.
+template <int NS, int NT>
+__device__ __forceinline__ void combine_partials(const double* partials, int64_t nchunks,
+                                                 double* out) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x / 32;
+  for (int k = w; k < NT; k += kRedBlock / 32) {
+    const bool is_sum = k < NS;
+    double t = 0.0;
+    for (int64_t b = lane; b < nchunks; b += 32) {
+      const double v = __ldcg(&partials[b * NT + k]);
+      t = is_sum ? t + v : fmax(t, v);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double o = __shfl_xor_sync(0xffffffffu, t, off);
+      t = is_sum ? t + o : fmax(t, o);
+    }
+    if (lane == 0) out[k] = t;
+  }
+}
+
+// Phase 1: block b reduces chunk (chunk0 + b) of the functor's index space
+// [0, n) into partials[(chunk0 + b) * NT ...]. With Combine (single launch),
+// the last-arriving block then runs the fixed combine over all chunks.
+template <int NS, int NM, class F, bool Combine>
+__global__ void __launch_bounds__(kRedBlock) reduce_chunks_kernel(F f, int64_t n, double* partials,
+                                                                   int64_t chunk0, unsigned* ticket,
+                                                                   double* out) {
   constexpr int NT = NS + NM;
   double s[NS > 0 ? NS : 1], mx[NM > 0 ? NM : 1];
 #pragma unroll
   for (int k = 0; k < NS; ++k) s[k] = 0.0;
 #pragma unroll
   for (int k = 0; k < NM; ++k) mx[k] = 0.0;
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * kRedBlock;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * kRedBlock + threadIdx.x; i < n; i += stride)
-    f(i, s, mx);
-  // warp butterfly
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kRedChunk;
+#pragma unroll
+  for (int j = 0; j < kRedChunk / kRedBlock; ++j) {
+    const int64_t i = base + j * kRedBlock + threadIdx.x;
+    if (i < n) f(i, s, mx);
+  }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
 #pragma unroll
@@ -70,61 +101,74 @@ __global__ void __launch_bounds__(kRedBlock) reduce_par_kernel(F f, int64_t n, d
     for (int k = 0; k < NM; ++k) sm[w][NS + k] = mx[k];
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int k = 0; k < NT; ++k) {
-      double t = sm[0][k];
-      for (int j = 1; j < kRedBlock / 32; ++j) t = k < NS ? t + sm[j][k] : fmax(t, sm[j][k]);
-      partials[static_cast<int64_t>(blockIdx.x) * NT + k] = t;
-    }
-    __threadfence();
-    am_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  if (threadIdx.x < NT) {
+    const int k = threadIdx.x;
+    double t = sm[0][k];
+    for (int j = 1; j < kRedBlock / 32; ++j) t = k < NS ? t + sm[j][k] : fmax(t, sm[j][k]);
+    partials[(chunk0 + blockIdx.x) * NT + k] = t;
   }
-  __syncthreads();
-  if (am_last) {
-    __threadfence();
-    // warp w combines outputs k = w, w + 8, ...: lane l sums partials
-    // l, l + 32, ... in order, then a fixed butterfly — deterministic.
-    const int lane = threadIdx.x & 31;
-    for (int k = w; k < NT; k += kRedBlock / 32) {
-      const bool is_sum = k < NS;
-      double t = 0.0;
-      for (unsigned b = lane; b < gridDim.x; b += 32) {
-        const double v = __ldcg(&partials[static_cast<int64_t>(b) * NT + k]);
-        t = is_sum ? t + v : fmax(t, v);
-      }
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        const double o = __shfl_xor_sync(0xffffffffu, t, off);
-        t = is_sum ? t + o : fmax(t, o);
-      }
-      if (lane == 0) out[k] = t;
+  if constexpr (Combine) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      am_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
     }
-    if (threadIdx.x == 0) *ticket = 0u;  // re-arm for the next launch / graph replay
+    __syncthreads();
+    if (am_last) {
+      __threadfence();
+      combine_partials<NS, NT>(partials, gridDim.x, out);
+      if (threadIdx.x == 0) *ticket = 0u;  // re-arm for the next launch / graph replay
+    }
   }
 }
 
-// Scratch for reductions: partials for up to kRedMaxGrid blocks x 32 values.
+template <int NS, int NT>
+__global__ void __launch_bounds__(kRedBlock) reduce_combine_kernel(const double* partials,
+                                                                    int64_t nchunks, double* out) {
+  combine_partials<NS, NT>(partials, nchunks, out);
+}
+
+// Scratch for reductions: partials for up to `max_elems` elements x 32 values.
 struct ReduceScratch {
   DevBuf<double> partials;
   DevBuf<unsigned> ticket;
-  void init(cudaStream_t st) {
-    partials.alloc(static_cast<std::size_t>(kRedMaxGrid) * 32);
+  void init(int64_t max_elems, cudaStream_t st) {
+    partials.alloc(static_cast<std::size_t>(reduce_chunks(max_elems)) * kRedMaxOut);
     ticket.alloc(1);
     ticket.zero(st);
   }
 };
 
-// Launch a reduction writing NS sums then NM maxima to d_out.
+// Launch a reduction over [0, n) writing NS sums then NM maxima to d_out.
 template <int NS, int NM, class F>
 inline void launch_reduce(const F& f, int64_t n, bool strict, ReduceScratch& rs, double* d_out,
                           cudaStream_t st) {
-  static_assert(NS + NM <= 32, "too many reduction outputs");
+  static_assert(NS + NM <= kRedMaxOut, "too many reduction outputs");
   if (strict) {
     reduce_seq_kernel<NS, NM, F><<<1, 1, 0, st>>>(f, n, d_out);
   } else {
-    reduce_par_kernel<NS, NM, F>
-        <<<reduce_grid(n), kRedBlock, 0, st>>>(f, n, rs.partials.get(), rs.ticket.get(), d_out);
+    reduce_chunks_kernel<NS, NM, F, true><<<static_cast<unsigned>(reduce_chunks(n)), kRedBlock, 0, st>>>(
+        f, n, rs.partials.get(), 0, rs.ticket.get(), d_out);
   }
+  RB_LAUNCH_CHECK();
+}
+
+// Sharded phase 1: the chunks of a local range that starts at global chunk
+// `chunk0` (shard offsets are multiples of kRedChunk); partials land in the
+// global partial array of `rs` at their global chunk index.
+template <int NS, int NM, class F>
+inline void launch_reduce_partials(const F& f, int64_t n_local, int64_t chunk0, ReduceScratch& rs,
+                                   cudaStream_t st) {
+  if (n_local <= 0) return;
+  reduce_chunks_kernel<NS, NM, F, false><<<static_cast<unsigned>(ceil_div(n_local, kRedChunk)), kRedBlock,
+                                           0, st>>>(f, n_local, rs.partials.get(), chunk0, nullptr, nullptr);
+  RB_LAUNCH_CHECK();
+}
+
+// Sharded phase 2: combine the full (exchanged) partial array.
+template <int NS, int NM>
+inline void launch_reduce_combine(int64_t n_global, ReduceScratch& rs, double* d_out, cudaStream_t st) {
+  reduce_combine_kernel<NS, NS + NM><<<1, kRedBlock, 0, st>>>(rs.partials.get(), reduce_chunks(n_global), d_out);
   RB_LAUNCH_CHECK();
 }
 

@@ -25,6 +25,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <vector>
 
@@ -44,6 +45,16 @@ struct BinDesc {
   int32_t blk_begin, blk_end;  // blocks of the launch
 };
 
+// A window [lo, lo + len) of a gathered vector's index space that the kernel
+// stages in shared memory (len = 0: none). Random fp64 gathers through L1TEX
+// cost one wavefront (~1 cycle/SM) per distinct 128 B line; from shared memory
+// a warp's 32 random 8 B reads cost ~a bank-conflict degree (~4-5 cycles), so
+// gathers that land in the window are ~6x cheaper. Chosen per matrix pattern at
+// setup from a column histogram (schedule.cu).
+struct Window {
+  int32_t lo = 0, len = 0;
+};
+
 struct SchedView {
   const int32_t* perm;  // row order by bin; nullptr = identity (strict)
   BinDesc bins[kNumBins];
@@ -55,7 +66,8 @@ struct SchedView {
   const int32_t* seg_count;  // segments of that row
   double* seg_partial;       // [nseg * kMaxAcc]
   unsigned* seg_ticket;      // [nseg], used at index seg_first
-  int32_t total_blocks;
+  int32_t total_blocks;      // tiles; the persistent grid strides over them
+  Window win[2];             // staged gather windows of segment 1 / 2 columns
 };
 
 constexpr int kMaxAcc = 8;
@@ -114,25 +126,58 @@ __device__ __forceinline__ int next_pos(int p0, int stride, int target) {
 // slots contribute 0*0 = +0, which never changes a sum that started at +0.0
 // (such a sum is never -0), so the adds stay in position order and strict
 // mode remains the reference's sequential sum exactly.
+#ifndef RB_PIPELINE
+#define RB_PIPELINE 1
+#endif
+
+template <int U>
+__device__ __forceinline__ void load_batch(const double* __restrict__ vals,
+                                           const int32_t* __restrict__ cols, int64_t base, int p,
+                                           int end, int stride, int32_t* c, double* v) {
+#pragma unroll
+  for (int k = 0; k < U; ++k) {
+    const bool ok = p + k * stride < end;
+    const int64_t i = base + p + k * stride;
+    c[k] = ok ? ld_stream(cols + i) : 0;
+    v[k] = ok ? ld_stream(vals + i) : 0.0;
+  }
+}
+
+// Gathered-vector access: the staged window from shared memory, the rest
+// through the read-only path.
+struct Gather {
+  const double* __restrict__ x;
+  const double* sm;
+  int32_t lo;
+  uint32_t len;
+  __device__ __forceinline__ double operator()(int32_t c) const {
+    const uint32_t k = static_cast<uint32_t>(c - lo);
+    return k < len ? sm[k] : ld_gather(x + c);
+  }
+};
+
 template <bool Strict, int U = kUnroll>
 __device__ __forceinline__ double seg_dot(const double* __restrict__ vals,
-                                          const int32_t* __restrict__ cols,
-                                          const double* __restrict__ x, int64_t base, int p,
-                                          int end, int stride, double acc) {
+                                          const int32_t* __restrict__ cols, const Gather& x,
+                                          int64_t base, int p, int end, int stride, double acc) {
+  if (p >= end) return acc;
+  int32_t c[U];
+  double v[U];
+  load_batch<U>(vals, cols, base, p, end, stride, c, v);
   for (; p < end; p += U * stride) {
-    int32_t c[U];
-    double v[U], xv[U];
+    // Software pipeline: the next batch's indices/values are requested before
+    // this batch's gathers, so a lane keeps two batches of streaming loads and
+    // one of gathers in flight instead of paying the two round trips in turn.
+    int32_t cn[U];
+    double vn[U], xv[U];
+    if (RB_PIPELINE) load_batch<U>(vals, cols, base, p + U * stride, end, stride, cn, vn);
 #pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const bool ok = p + k * stride < end;
-      const int64_t i = base + p + k * stride;
-      c[k] = ok ? ld_stream(cols + i) : 0;
-      v[k] = ok ? ld_stream(vals + i) : 0.0;
-    }
-#pragma unroll
-    for (int k = 0; k < U; ++k) xv[k] = (p + k * stride < end) ? ld_gather(x + c[k]) : 0.0;
+    for (int k = 0; k < U; ++k) xv[k] = (p + k * stride < end) ? x(c[k]) : 0.0;
 #pragma unroll
     for (int k = 0; k < U; ++k) acc = madd<Strict>(acc, v[k], xv[k]);
+    if (!RB_PIPELINE) load_batch<U>(vals, cols, base, p + U * stride, end, stride, cn, vn);
+#pragma unroll
+    for (int k = 0; k < U; ++k) c[k] = cn[k], v[k] = vn[k];
   }
   return acc;
 }
@@ -178,18 +223,26 @@ __device__ __forceinline__ void seg_dot2(const double* __restrict__ vals,
 }
 
 // ---- the kernel --------------------------------------------------------------
+//
+// Persistent: the grid is sized to the resident capacity and each CTA walks
+// tiles t = blockIdx.x, + gridDim.x, ... (heavy bins own the lowest tile
+// indices, so every CTA starts on heavy work). A tile's result never depends on
+// which CTA computes it, so the schedule stays deterministic. Each CTA stages
+// the Op's gathered-vector windows in shared memory once, before its first
+// tile.
 
 template <class Op, int V>
-__device__ __forceinline__ void run_vlane(const Op& op, const SchedView& s, const BinDesc& bd) {
+__device__ __forceinline__ void run_vlane(const Op& op, const SchedView& s, const BinDesc& bd,
+                                          int tile, const Gather* g) {
   constexpr int kRowsPerBlock = kBlock / V;
-  const int g = threadIdx.x / V;
+  const int grp = threadIdx.x / V;
   const int lane = threadIdx.x % V;
-  const int slot = bd.row_begin + (blockIdx.x - bd.blk_begin) * kRowsPerBlock + g;
+  const int slot = bd.row_begin + (tile - bd.blk_begin) * kRowsPerBlock + grp;
   const bool valid = slot < bd.row_end;
   const int r = valid ? (s.perm ? s.perm[slot] : slot) : 0;
   typename Op::AccT a;
   a.zero();
-  if (valid) op.template accumulate<(V >= 16 ? Op::kWideUnroll : kUnroll)>(r, 0, op.len(r), lane, V, a);
+  if (valid) op.template accumulate<(V >= 16 ? Op::kWideUnroll : kUnroll)>(r, 0, op.len(r), lane, V, a, g);
   a.template reduce_lanes<V>();  // all lanes participate (invalid ones hold 0)
   if (valid && lane == 0) op.finish(r, a);
 }
@@ -211,37 +264,38 @@ __device__ __forceinline__ void block_reduce(typename Op::AccT& a) {
       a.v[k] = t;
     }
   }
+  __syncthreads();  // sm is reused by the CTA's next tile
 }
 
 template <class Op>
-__device__ __forceinline__ void run_block_row(const Op& op, const SchedView& s, const BinDesc& bd) {
-  const int slot = bd.row_begin + (blockIdx.x - bd.blk_begin);
+__device__ __forceinline__ void run_block_row(const Op& op, const SchedView& s, const BinDesc& bd,
+                                              int tile, const Gather* g) {
+  const int slot = bd.row_begin + (tile - bd.blk_begin);
   const int r = s.perm ? s.perm[slot] : slot;
   typename Op::AccT a;
   a.zero();
-  op.template accumulate<kUnroll>(r, 0, op.len(r), threadIdx.x, kBlock, a);
+  op.template accumulate<kUnroll>(r, 0, op.len(r), threadIdx.x, kBlock, a, g);
   block_reduce<Op>(a);
   if (threadIdx.x == 0) op.finish(r, a);
 }
 
 template <class Op>
-__device__ __forceinline__ void run_split(const Op& op, const SchedView& s, const BinDesc& bd) {
+__device__ __forceinline__ void run_split(const Op& op, const SchedView& s, const BinDesc& bd,
+                                          int tile, const Gather* g) {
   constexpr int K = Op::AccT::kK;
-  const int seg = blockIdx.x - bd.blk_begin;
+  const int seg = tile - bd.blk_begin;
   const int r = s.seg_row[seg];
   typename Op::AccT a;
   a.zero();
-  op.template accumulate<kUnroll>(r, s.seg_lo[seg], s.seg_hi[seg], threadIdx.x, kBlock, a);
+  op.template accumulate<kUnroll>(r, s.seg_lo[seg], s.seg_hi[seg], threadIdx.x, kBlock, a, g);
   block_reduce<Op>(a);
-  __shared__ bool last;
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int k = 0; k < K; ++k) s.seg_partial[(int64_t)seg * kMaxAcc + k] = a.v[k];
     __threadfence();
     const int first = s.seg_first[seg], cnt = s.seg_count[seg];
     const unsigned t = atomicAdd(&s.seg_ticket[first], 1u);
-    last = (t == static_cast<unsigned>(cnt - 1));
-    if (last) {
+    if (t == static_cast<unsigned>(cnt - 1)) {  // last segment of the row to finish
       __threadfence();
       typename Op::AccT tot;
       tot.zero();
@@ -255,37 +309,63 @@ __device__ __forceinline__ void run_split(const Op& op, const SchedView& s, cons
   }
 }
 
-template <class Op>
+template <class Op, bool Win>
 __global__ void __launch_bounds__(kBlock) rowwise_kernel(const Op op, const SchedView s) {
-  // bins occupy disjoint block ranges (heavy bins first, see schedule.cu)
-  int bin = 0;
+  extern __shared__ double win_smem[];
+  Gather g[2];
+  int off = 0;
 #pragma unroll
-  for (int b = 1; b < kNumBins; ++b)
-    if (static_cast<int>(blockIdx.x) >= s.bins[b].blk_begin &&
-        static_cast<int>(blockIdx.x) < s.bins[b].blk_end)
-      bin = b;
-  const BinDesc bd = s.bins[bin];
-  if (static_cast<int>(blockIdx.x) < bd.blk_begin || static_cast<int>(blockIdx.x) >= bd.blk_end) return;
-  if constexpr (Op::kStrict) {
-    run_vlane<Op, 1>(op, s, bd);  // strict schedules hold a single V=1 bin
-  } else {
-    switch (bin) {
-      case 0: run_vlane<Op, 1>(op, s, bd); break;
-      case 1: run_vlane<Op, 2>(op, s, bd); break;
-      case 2: run_vlane<Op, 4>(op, s, bd); break;
-      case 3: run_vlane<Op, 8>(op, s, bd); break;
-      case 4: run_vlane<Op, 16>(op, s, bd); break;
-      case 5: run_vlane<Op, 32>(op, s, bd); break;
-      case 6: run_block_row<Op>(op, s, bd); break;
-      default: run_split<Op>(op, s, bd); break;
+  for (int slot = 0; slot < 2; ++slot) {
+    const Window w = s.win[slot];
+    const bool use = Win && w.len > 0;  // Win = false compiles the smem path out
+    const double* src = op.gather_src(slot);
+    g[slot] = Gather{src, win_smem + off, w.lo, use ? static_cast<uint32_t>(w.len) : 0u};
+    if (use) {
+      for (int k = threadIdx.x; k < w.len; k += kBlock) win_smem[off + k] = __ldcg(src + w.lo + k);
+      off += w.len;
+    }
+  }
+  if (Win) __syncthreads();
+  for (int tile = blockIdx.x; tile < s.total_blocks; tile += gridDim.x) {
+    int bin = 0;  // bins occupy disjoint tile ranges (heavy bins first, see schedule.cu)
+#pragma unroll
+    for (int b = 1; b < kNumBins; ++b)
+      if (tile >= s.bins[b].blk_begin && tile < s.bins[b].blk_end) bin = b;
+    const BinDesc bd = s.bins[bin];
+    if constexpr (Op::kStrict) {
+      run_vlane<Op, 1>(op, s, bd, tile, g);  // strict schedules hold a single V=1 bin
+    } else {
+      switch (bin) {
+        case 0: run_vlane<Op, 1>(op, s, bd, tile, g); break;
+        case 1: run_vlane<Op, 2>(op, s, bd, tile, g); break;
+        case 2: run_vlane<Op, 4>(op, s, bd, tile, g); break;
+        case 3: run_vlane<Op, 8>(op, s, bd, tile, g); break;
+        case 4: run_vlane<Op, 16>(op, s, bd, tile, g); break;
+        case 5: run_vlane<Op, 32>(op, s, bd, tile, g); break;
+        case 6: run_block_row<Op>(op, s, bd, tile, g); break;
+        default: run_split<Op>(op, s, bd, tile, g); break;
+      }
     }
   }
 }
 
+// Resident CTAs per SM for a kernel instance at a dynamic smem size (cached).
+int resident_ctas(const void* kernel, int smem_bytes);
+
 template <class Op>
 inline void launch_rowwise(const Op& op, const SchedView& s, cudaStream_t st) {
   if (s.total_blocks <= 0) return;
-  rowwise_kernel<Op><<<s.total_blocks, kBlock, 0, st>>>(op, s);
+  const int wins = Op::kStageWindows ? s.win[0].len + s.win[1].len : 0;
+  if (wins == 0) {
+    // one tile per CTA: the hardware scheduler balances heavy and light tiles
+    rowwise_kernel<Op, false><<<s.total_blocks, kBlock, 0, st>>>(op, s);
+  } else {
+    // persistent: each resident CTA stages the windows once, then strides tiles
+    const int smem = wins * static_cast<int>(sizeof(double));
+    const void* k = reinterpret_cast<const void*>(&rowwise_kernel<Op, true>);
+    const int grid = std::min(s.total_blocks, resident_ctas(k, smem) * kSMs);
+    rowwise_kernel<Op, true><<<grid, kBlock, smem, st>>>(op, s);
+  }
   RB_LAUNCH_CHECK();
 }
 
@@ -323,6 +403,15 @@ struct SchedParams {
 
 // lengths: device array of per-row lengths (int32). strict: single V=1 bin in
 // natural row order.
+// Pick the staged gather window of each segment (1: cols1 of a matrix with
+// ncols1 columns, 2: cols2 / ncols2; nnz2 = 0 for single-segment schedules)
+// from a device column histogram: the densest range of at most kWinMax
+// columns, kept only if it serves enough gathers to repay staging it in every
+// resident CTA. RAPDHG_WINDOW=off disables, =force keeps any non-empty window.
+constexpr int kWinMax = 12288;  // doubles (96 KB): 2 CTAs/SM
+void choose_windows(Schedule& sch, const int32_t* cols1, int64_t nnz1, int32_t ncols1,
+                    const int32_t* cols2, int64_t nnz2, int32_t ncols2, cudaStream_t st);
+
 void build_schedule(Schedule& sch, const int32_t* d_len, int64_t rows, bool strict,
                     cudaStream_t st);
 

@@ -8,6 +8,9 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <string>
 #include <vector>
 
 #include "rowwise.cuh"
@@ -26,7 +29,92 @@ __global__ void bin_kernel(int32_t* bin, int32_t* idx, const int32_t* len, int64
   atomicAdd(&counts[b], 1);  // integer counts: exact
 }
 
+constexpr int kWinBucket = 128;  // histogram granularity (columns)
+
+__global__ void col_hist_kernel(const int32_t* cols, int64_t nnz, int* hist) {
+  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (k < nnz) atomicAdd(&hist[cols[k] / kWinBucket], 1);  // integer counts: exact
+}
+
+struct WinChoice {
+  Window w;
+  int64_t covered = 0;
+};
+
+WinChoice best_window(const int32_t* cols, int64_t nnz, int32_t ncols, cudaStream_t st) {
+  WinChoice best;
+  if (nnz <= 0 || ncols <= 0) return best;
+  const int nb = static_cast<int>(ceil_div(ncols, kWinBucket));
+  DevBuf<int> hist(nb);
+  hist.zero(st);
+  col_hist_kernel<<<static_cast<unsigned>(ceil_div(nnz, 256)), 256, 0, st>>>(cols, nnz, hist.get());
+  RB_LAUNCH_CHECK();
+  std::vector<int> h(nb);
+  RB_CUDA(cudaMemcpyAsync(h.data(), hist.get(), sizeof(int) * nb, cudaMemcpyDeviceToHost, st));
+  RB_CUDA(cudaStreamSynchronize(st));
+  const int wb = std::min(nb, kWinMax / kWinBucket);
+  int64_t sum = 0;
+  for (int b = 0; b < wb; ++b) sum += h[b];
+  int64_t best_sum = sum;
+  int best_b = 0;
+  for (int b = wb; b < nb; ++b) {  // sliding window of wb buckets
+    sum += h[b] - h[b - wb];
+    if (sum > best_sum) best_sum = sum, best_b = b - wb + 1;
+  }
+  int lo_b = best_b, hi_b = best_b + wb;  // trim empty buckets at both ends
+  while (lo_b < hi_b && h[lo_b] == 0) ++lo_b;
+  while (hi_b > lo_b && h[hi_b - 1] == 0) --hi_b;
+  if (lo_b >= hi_b) return best;
+  best.w.lo = lo_b * kWinBucket;
+  best.w.len = std::min(hi_b * kWinBucket, ncols) - best.w.lo;
+  best.covered = best_sum;
+  return best;
+}
+
 }  // namespace
+
+int resident_ctas(const void* kernel, int smem_bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  const auto key = std::make_pair(kernel, smem_bytes);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  if (smem_bytes > 48 * 1024)
+    RB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
+  int n = 0;
+  RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, kBlock, smem_bytes));
+  if (n < 1) n = 1;
+  cache.emplace(key, n);
+  return n;
+}
+
+void choose_windows(Schedule& sch, const int32_t* cols1, int64_t nnz1, int32_t ncols1,
+                    const int32_t* cols2, int64_t nnz2, int32_t ncols2, cudaStream_t st) {
+  sch.view.win[0] = sch.view.win[1] = Window{};
+  const char* env = std::getenv("RAPDHG_WINDOW");
+  // Measured on B200 (C2/C3/C4): a window large enough to matter costs more in
+  // occupancy (2 CTAs/SM at 80-96 KB) than it saves in L1TEX wavefronts, so
+  // windows are opt-in (RAPDHG_WINDOW=auto|force) until a variant wins.
+  const std::string mode = env ? env : "off";
+  if (mode == "off") return;
+  WinChoice c[2] = {best_window(cols1, nnz1, ncols1, st), best_window(cols2, nnz2, ncols2, st)};
+  const int64_t nnz[2] = {nnz1, nnz2};
+  // staging costs len doubles per resident CTA (~2 per SM at a full window)
+  const int64_t grid = std::min<int64_t>(sch.view.total_blocks, 2 * kSMs);
+  bool keep[2];
+  for (int k = 0; k < 2; ++k) {
+    keep[k] = c[k].w.len > 0 &&
+              (mode == "force" ||
+               (c[k].covered * 4 >= nnz[k] && c[k].covered >= 2 * static_cast<int64_t>(c[k].w.len) * grid));
+  }
+  if (keep[0] && keep[1] && c[0].w.len + c[1].w.len > kWinMax) {
+    if (c[0].covered >= c[1].covered) keep[1] = false;
+    else keep[0] = false;
+  }
+  for (int k = 0; k < 2; ++k)
+    if (keep[k]) sch.view.win[k] = c[k].w;
+}
 
 SchedParams SchedParams::from_env() {
   SchedParams p;

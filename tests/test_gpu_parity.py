@@ -302,3 +302,31 @@ def test_reference_side_adapter_drop_in():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout.count("bit-identical") == 3
+
+
+@pytest.fixture
+def force_windows(monkeypatch):
+    monkeypatch.setenv("RAPDHG_WINDOW", "force")
+    yield
+
+
+def test_staged_windows_strict_bit_exact(O, force_windows):
+    """Shared-memory gather windows forced on every schedule: strict mode must
+    still be bit-identical (a window only changes where a value is read from)."""
+    for seed in (1, 2):
+        p = random_qp(seed, n=40, mi=20, me=6)
+        cfg = rb.SolverConfig(tol=1e-7, max_iters=1500, record_restart_points=True, strict_parity=True)
+        assert_results_identical(rb.solve(p, cfg), O.solve(p, cfg))
+
+
+def test_staged_windows_fast(O, force_windows, monkeypatch):
+    p = rb.generate(rb.Gen.LASSO, 0.02, 2)
+    cfg = rb.SolverConfig(tol=1e-12, max_iters=400, snapshot_interval=40)
+    a = rb.solve(p, cfg)
+    monkeypatch.setenv("RAPDHG_WINDOW", "off")
+    b = rb.solve(p, cfg)
+    for (ta, za), (tb, zb) in zip(a.snapshots, b.snapshots):
+        assert ta == tb
+        assert np.array_equal(za.x, zb.x), "windows must not change fast-mode results either"
+    a2, _, agree = _fast_vs_ref(O, long_row_qp(), dict(tol=1e-12), 160)
+    assert agree >= 2

@@ -49,6 +49,10 @@ def parse():
     ap.add_argument("--ref-iters", type=int, default=40)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--strict", action="store_true", help="bit-exact strict mode")
+    ap.add_argument("--shard", action="store_true",
+                    help="row-shard ONE instance across the torchrun ranks (NCCL) instead of replicas")
+    ap.add_argument("--shard-emulate", type=int, default=0,
+                    help="run this many shards in one process (single-GPU functional check)")
     return ap.parse_args()
 
 
@@ -180,6 +184,49 @@ def run_reference_arm(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def run_sharded(args, p, desc, rank, world, local, dist, barrier, allmax):
+    """Strong scaling: ONE instance row-sharded over the ranks:
+    NCCL allgather-v of y, w, x_md between the dual and primal steps. A step is
+    one full sharded solve; value = iterations / max-over-ranks loop time.
+    --shard-emulate P runs P shards in one process (single-GPU functional run)."""
+    import paper_2311_07710_b200 as rb
+
+    cfg = rb.SolverConfig(tol=args.tol, max_iters=args.max_iters, device=local)
+    if args.shard_emulate:
+        parts, kw = args.shard_emulate, dict(emulate=True)
+    else:
+        parts = world
+        uid = rb.nccl_unique_id() if rank == 0 else None
+        if dist:
+            obj = [uid]
+            dist[1].broadcast_object_list(obj, src=0)
+            uid = obj[0]
+        kw = dict(emulate=False, rank=rank, nccl_id=uid)
+    for _ in range(args.warmup):
+        rb.solve_sharded(p, cfg, parts, **kw)
+    barrier()
+    its, loop_s, wall = 0, 0.0, 0.0
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        r = rb.solve_sharded(p, cfg, parts, **kw)
+        wall += time.perf_counter() - t
+        its += r.iterations
+        loop_s += r.loop_seconds
+    barrier()
+    t_max = allmax(loop_s)
+    wall = allmax(wall)
+    if rank == 0:
+        line = {"metric": "rAPDHG iters/sec (row-sharded, one instance)", "value": its / t_max, "unit": "iter/s",
+                "n_gpus": world, "shards": parts, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": desc,
+                "iterations_per_step": its / args.steps, "status": rb.to_string(r.status),
+                "e2e": {"value": its / wall, "unit": "iter/s", "h2d_bytes_per_step": qp_bytes(p),
+                        "d2h_bytes_per_step": 8 * (p.num_vars() + p.num_rows())},
+                "gpu_launches": r.kernel_launches}
+        print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -218,6 +265,11 @@ def main():
 
     p, gen_s = make_instance(args)
     desc = workload_desc(args, p)
+    if args.shard or args.shard_emulate:
+        run_sharded(args, p, desc, rank, world, local, dist, barrier, allmax)
+        if dist:
+            dist[1].destroy_process_group()
+        return
     cfg = rb.SolverConfig(tol=args.tol, max_iters=args.max_iters, device=local, profile_kernels=True,
                           strict_parity=args.strict)
     sess = rb.Session(p, cfg)

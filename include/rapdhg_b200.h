@@ -200,6 +200,34 @@ int rapdhg_session_bytes(const rapdhg_session* s, double* b_iter, double* b_dual
                          double* b_primal);
 void rapdhg_session_destroy(rapdhg_session* s);
 
+/* ---- row-sharded multi-GPU solve (no reference counterpart:
+ * the reference is single-threaded) ------------------------- */
+
+/* nnz-balanced contiguous row blocks for `parts` ranks: dual rows of
+ * [A_ineq; A_eq] (dual_bounds, parts+1 entries over [0, m)) and primal rows
+ * of [Q | A'] (primal_bounds over [0, n)); inner bounds are multiples of the
+ * reduction chunk (2048). Host-only. */
+int rapdhg_shard_plan(const rapdhg_qp* qp, int32_t parts, int32_t* dual_bounds,
+                      int32_t* primal_bounds);
+
+typedef struct {
+  int32_t parts;    /* number of shards */
+  int32_t rank;     /* this process's shard (ignored when emulate = 1) */
+  int32_t emulate;  /* 1: all shards in this process on cfg->device */
+  int32_t pad;
+  uint8_t nccl_id[128]; /* ncclUniqueId from rank 0 (emulate = 0) */
+} rapdhg_shard_opts;
+
+/* 128-byte ncclUniqueId for rapdhg_shard_opts.nccl_id (call on rank 0 and
+ * broadcast it, e.g. with torch.distributed). */
+int rapdhg_nccl_unique_id(uint8_t* out128);
+
+/* Same contract as rapdhg_solve; every rank returns the full result. The
+ * result is bit-identical to rapdhg_solve in fast mode (strict mode is
+ * rejected: its sequential reductions do not shard). */
+int rapdhg_solve_sharded(const rapdhg_qp* qp, const rapdhg_config* cfg,
+                         const rapdhg_shard_opts* opts, rapdhg_result* out);
+
 /* ---- secondary API used by the reference's tests ----------------------- */
 
 /* y = M x (sparse.hpp:79-88) and y = M' x (sparse.hpp:91-100). */

@@ -109,6 +109,9 @@ def _load():
     d(lib, "rapdhg_qp_free", None, P(abi.QpOwned))
     d(lib, "rapdhg_qp_view", None, P(abi.QpOwned), P(abi.Qp))
     d(lib, "rapdhg_generate", C.c_int, C.c_int32, C.c_double, C.c_uint64, P(abi.QpOwned))
+    d(lib, "rapdhg_shard_plan", C.c_int, P(abi.Qp), C.c_int32, abi.P_i32, abi.P_i32)
+    d(lib, "rapdhg_nccl_unique_id", C.c_int, P(C.c_uint8))
+    d(lib, "rapdhg_solve_sharded", C.c_int, P(abi.Qp), P(abi.Config), P(abi.ShardOpts), P(abi.Result))
     if lib.rapdhg_abi_version() != 1:
         raise ImportError("librapdhg_b200.so ABI version mismatch")
     _lib = lib
@@ -469,6 +472,43 @@ def solve(original: QuadraticProgram, cfg: Optional[SolverConfig] = None) -> Sol
         L.rapdhg_result_free(C.byref(out))
 
 
+def shard_plan(p: QuadraticProgram, parts: int) -> Tuple[np.ndarray, np.ndarray]:
+    """(dual_bounds, primal_bounds): nnz-balanced contiguous row blocks of the
+    row-sharded solver (host computation, works without a GPU)."""
+    db, pb = np.zeros(parts + 1, np.int32), np.zeros(parts + 1, np.int32)
+    qp = p._struct()
+    _check(_load().rapdhg_shard_plan(C.byref(qp), int(parts), _pi(db), _pi(pb)))
+    return db, pb
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId for a multi-process sharded solve (rank 0)."""
+    buf = (C.c_uint8 * 128)()
+    _check(_load().rapdhg_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def solve_sharded(original: QuadraticProgram, cfg: Optional[SolverConfig] = None, parts: int = 2,
+                  emulate: bool = True, rank: int = 0, nccl_id: Optional[bytes] = None) -> SolveResult:
+    """Row-sharded solve. emulate=True runs all `parts` shards in
+    this process on cfg.device (exchanges as device copies); emulate=False is
+    one process per GPU, shard `rank`, NCCL communicator from `nccl_id`
+    (nccl_unique_id() on rank 0, broadcast by the caller). Bit-identical to
+    solve() in fast mode."""
+    cfg = cfg or SolverConfig()
+    opts = abi.ShardOpts()
+    opts.parts, opts.rank, opts.emulate = int(parts), int(rank), int(bool(emulate))
+    if nccl_id is not None:
+        C.memmove(opts.nccl_id, nccl_id, 128)
+    qp, cs, out = original._struct(), cfg._struct(), abi.Result()
+    L = _load()
+    _check(L.rapdhg_solve_sharded(C.byref(qp), C.byref(cs), C.byref(opts), C.byref(out)))
+    try:
+        return result_from_struct(out)
+    finally:
+        L.rapdhg_result_free(C.byref(out))
+
+
 class Session:
     """Problem uploaded and preprocessed once (validate, scaling, norms), then
     solved from the zero start as often as wanted on HBM-resident data."""
@@ -734,7 +774,7 @@ __all__ = [
     "SparseMatrix", "QuadraticProgram", "PrimalDualPoint", "SolverConfig", "SolveResult",
     "SolveStatus", "Algorithm", "RestartPolicy", "StepRule", "PrimalWeightMode", "KktResiduals",
     "LogRecord", "IterateState", "StepParams", "ScalingInfo", "PowerIterOptions", "RestartContext",
-    "Session", "Gen", "solve", "inner_step", "pdhg_step", "rel_kkt", "compute_scaling",
+    "Session", "Gen", "solve", "solve_sharded", "shard_plan", "nccl_unique_id", "inner_step", "pdhg_step", "rel_kkt", "compute_scaling",
     "ruiz_scaling", "apply_scaling", "unscale_point", "scale_point", "estimate_op_norm",
     "estimate_op_norm_symmetric", "step_schedule_theoretical", "pdhg_constant_steps",
     "adaptive_eta", "primal_weight_init", "primal_weight_update", "restart_decision", "generate",

@@ -85,6 +85,11 @@ class QpOwned(C.Structure):
                 ("obj_offset", f64)]
 
 
+class ShardOpts(C.Structure):
+    _fields_ = [("parts", i32), ("rank", i32), ("emulate", i32), ("pad", i32),
+                ("nccl_id", C.c_uint8 * 128)]
+
+
 def declare(lib, name, restype, *argtypes):
     """Bind a symbol's signature; raises AttributeError if it is missing."""
     fn = getattr(lib, name)

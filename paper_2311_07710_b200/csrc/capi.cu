@@ -1,6 +1,7 @@
 // capi.cu — extern "C" entry points declared in include/rapdhg_b200.h.
 // Exceptions never cross the boundary: each call returns a code and leaves the
 // message in rapdhg_last_error() (thread-local).
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -10,6 +11,7 @@
 
 #include "engine.hpp"
 #include "rules.hpp"
+#include "sharded.hpp"
 
 namespace {
 
@@ -122,6 +124,51 @@ int rapdhg_solve(const rapdhg_qp* qp, const rapdhg_config* cfg, rapdhg_result* o
       tr.mark("solve loop + download");
     }
     tr.mark("engine teardown");
+  });
+}
+
+int rapdhg_shard_plan(const rapdhg_qp* qp, int32_t parts, int32_t* dual_bounds, int32_t* primal_bounds) {
+  return guard([&] {
+    null_check(qp, "qp");
+    null_check(dual_bounds, "dual_bounds");
+    null_check(primal_bounds, "primal_bounds");
+    rb::DeviceQP::validate_dims(*qp);
+    const rb::ShardPlan plan = rb::make_shard_plan(*qp, parts);
+    std::copy(plan.dual.begin(), plan.dual.end(), dual_bounds);
+    std::copy(plan.primal.begin(), plan.primal.end(), primal_bounds);
+  });
+}
+
+int rapdhg_nccl_unique_id(uint8_t* out128) {
+  return guard([&] {
+    null_check(out128, "out");
+    rb::nccl_unique_id(out128);
+  });
+}
+
+int rapdhg_solve_sharded(const rapdhg_qp* qp, const rapdhg_config* cfg, const rapdhg_shard_opts* opts,
+                         rapdhg_result* out) {
+  return guard([&] {
+    const auto t0 = rb::Clock::now();
+    null_check(qp, "qp");
+    null_check(cfg, "cfg");
+    null_check(opts, "opts");
+    null_check(out, "out");
+    std::memset(out, 0, sizeof(*out));
+    require_device();
+    if (opts->parts < 1) rb::invalid("sharded solve: parts must be >= 1");
+    std::unique_ptr<rb::Transport> tr;
+    int rank = -1;
+    if (opts->emulate) {
+      tr = rb::make_emulated_transport(opts->parts);
+    } else {
+      if (opts->rank < 0 || opts->rank >= opts->parts) rb::invalid("sharded solve: rank out of range");
+      RB_CUDA(cudaSetDevice(cfg->device));
+      tr = rb::make_nccl_transport(opts->parts, opts->rank, opts->nccl_id);
+      rank = opts->rank;
+    }
+    rb::ShardedEngine e(*qp, *cfg, opts->parts, rank, std::move(tr), t0);
+    e.solve(out, t0);
   });
 }
 

@@ -7,6 +7,8 @@
 
 #include "engine.hpp"
 #include "rules.hpp"
+#include "terms.cuh"
+#include "elementwise.cuh"
 
 namespace rb {
 
@@ -15,54 +17,6 @@ namespace {
 inline unsigned grid1(int64_t n) { return static_cast<unsigned>(ceil_div(n > 0 ? n : 1, 256)); }
 
 // ---- elementwise kernels -----------------------------------------------------
-
-// w = theta (x - x_prev) + x ; x_md = (1 - 1/beta) xbar + (1/beta) x
-// (solver.hpp:163,169) for the first iteration of a chunk.
-__global__ void prologue_kernel(const double* __restrict__ x, const double* __restrict__ xp,
-                                const double* __restrict__ xb, double* __restrict__ w,
-                                double* __restrict__ xmd, const IterParams* P, int n) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n) return;
-  const IterParams& q = P[0];
-  const double xj = x[j];
-  w[j] = q.theta * (xj - xp[j]) + xj;
-  xmd[j] = q.omib * xb[j] + q.ib * xj;
-}
-
-// unscale_point (scaling.hpp:126-133) of the current iterate and the average.
-__global__ void unscale_kernel(const double* x, const double* xb, const double* y,
-                               const double* yb, const double* d, double* xuc, double* xua,
-                               double* yuc, double* yua, int n, int m) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) {
-    const double f = d[i];
-    xuc[i] = x[i] * f;
-    xua[i] = xb[i] * f;
-  } else if (i < n + m) {
-    const int r = i - n;
-    const double f = d[i];
-    yuc[r] = y[r] * f;
-    yua[r] = yb[r] * f;
-  }
-}
-
-// Restart (solver.hpp:442-448): optionally x <- xbar, y <- ybar; then
-// x_prev <- x, xbar <- x, ybar <- y.
-__global__ void restart_kernel(double* x, double* xp, double* xb, double* y, double* yb,
-                               int from_avg, int n, int m) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) {
-    const double v = from_avg ? xb[i] : x[i];
-    x[i] = v;
-    xp[i] = v;
-    xb[i] = v;
-  } else if (i < n + m) {
-    const int r = i - n;
-    const double v = from_avg ? yb[r] : y[r];
-    y[r] = v;
-    yb[r] = v;
-  }
-}
 
 __global__ void scale_copy_kernel(double* v, const double* w, double s, int64_t n) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -109,81 +63,6 @@ __global__ void scale_vec_kernel(double* out, const double* v, const double* d, 
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i < n) out[i] = d[off + i] * v[i];
 }
-
-// ---- reduction functors (reduce.cuh) ----------------------------------------
-// Products are rounded before the add (--fmad=false), as the reference's
-// `s += a[i] * b[i]` (vec.hpp:16).
-
-struct SumSq {  // sum a_i^2 (norm2, vec.hpp:20)
-  const double* a;
-  __device__ void operator()(int64_t i, double* s, double*) const { s[0] += a[i] * a[i]; }
-};
-
-struct DotAndSumSq {  // s0 = v.w, s1 = w.w (opnorm.hpp:51-52, 77-78)
-  const double* v;
-  const double* w;
-  __device__ void operator()(int64_t i, double* s, double*) const {
-    s[0] += v[i] * w[i];
-    s[1] += w[i] * w[i];
-  }
-};
-
-// sum (x_i - e_i)^2 (dist2, vec.hpp:28-35), then e_i <- x_i (solver.hpp:459)
-struct DistAndAdvance {
-  const double* x;
-  double* e;
-  __device__ void operator()(int64_t i, double* s, double*) const {
-    const double d = x[i] - e[i];
-    s[0] += d * d;
-    e[i] = x[i];
-  }
-};
-
-// Dual-side relKKT terms for two points (kkt.hpp:44-53, 67):
-// sums  by_i(c), by_e(c), by_i(a), by_e(a)
-// maxes viol(c), viol(a), |ax|(c), |ax|(a), |b|
-struct KktDualTerms {
-  const double *axc, *axa, *b, *yc, *ya;
-  int mi;
-  __device__ void operator()(int64_t i, double* s, double* mx) const {
-    const double bi = b[i];
-    if (i < mi) {
-      s[0] += bi * yc[i];
-      s[2] += bi * ya[i];
-      mx[0] = fmax(mx[0], axc[i] - bi);
-      mx[1] = fmax(mx[1], axa[i] - bi);
-    } else {
-      s[1] += bi * yc[i];
-      s[3] += bi * ya[i];
-      mx[0] = fmax(mx[0], fabs(axc[i] - bi));
-      mx[1] = fmax(mx[1], fabs(axa[i] - bi));
-    }
-    mx[2] = fmax(mx[2], fabs(axc[i]));
-    mx[3] = fmax(mx[3], fabs(axa[i]));
-    mx[4] = fmax(mx[4], fabs(bi));
-  }
-};
-
-// Primal-side relKKT terms for two points (kkt.hpp:57-66):
-// sums  x.qx(c), x.qx(a), c.x(c), c.x(a)
-// maxes |qx+aty+c|(c), (a), |qx|(c), (a), |aty|(c), (a), |c|
-struct KktPrimalTerms {
-  const double *qxc, *qxa, *atc, *ata, *xc, *xa, *c;
-  __device__ void operator()(int64_t j, double* s, double* mx) const {
-    const double cj = c[j];
-    s[0] += xc[j] * qxc[j];
-    s[1] += xa[j] * qxa[j];
-    s[2] += cj * xc[j];
-    s[3] += cj * xa[j];
-    mx[0] = fmax(mx[0], fabs(qxc[j] + atc[j] + cj));
-    mx[1] = fmax(mx[1], fabs(qxa[j] + ata[j] + cj));
-    mx[2] = fmax(mx[2], fabs(qxc[j]));
-    mx[3] = fmax(mx[3], fabs(qxa[j]));
-    mx[4] = fmax(mx[4], fabs(atc[j]));
-    mx[5] = fmax(mx[5], fabs(ata[j]));
-    mx[6] = fmax(mx[6], fabs(cj));
-  }
-};
 
 template <class Op>
 inline void rowwise(const Op& op, const Schedule& s, cudaStream_t st, int64_t* launches) {
@@ -628,7 +507,7 @@ void Engine::run_chunk(int len) {
 // evaluate_candidate (solver.hpp:255-264) for the current iterate and the
 // average at once: unscale, the three KKT products over the ORIGINAL matrices
 // with both points per pass, then the reductions of kkt.hpp:43-69.
-Engine::Cand Engine::evaluate() {
+Cand Engine::evaluate() {
   const int cur = cur_;
   unscale_kernel<<<grid1(n_ + m_), 256, 0, st_>>>(X_[cur].get(), xb_.get(), y_.get(), yb_.get(), d_.get(),
                                                   xu_[0].get(), xu_[1].get(), yu_[0].get(), yu_[1].get(), n_, m_);
@@ -712,34 +591,74 @@ void append(T*& arr, int64_t& count, const T& v) {
 }
 }  // namespace
 
-// solve(): the loop of solver.hpp:293-471, with inner steps batched into
-// chunks that end exactly where the reference would run a check.
-void Engine::solve(rapdhg_result* out, Clock::time_point t0) {
-  const rapdhg_config& cfg = cfg_;
-  auto elapsed = [&] { return std::chrono::duration<double>(Clock::now() - t0).count(); };
-  const int n = n_, m = m_;
-  std::memset(out, 0, sizeof(*out));
-  out->n = n, out->m_ineq = mi_, out->m_eq = m - mi_;
-  out->norm_q = norm_q;
-  out->norm_a = norm_a;
+// ---- Engine as the single-GPU loop backend -------------------------------------
+
+void Engine::loop_begin() {
   kernel_ms_[0] = kernel_ms_[1] = 0.0;
   kernel_count_[0] = kernel_count_[1] = 0;
   launches_ = P_->launches;
   // loop time on the device timeline: events on the solver's stream bracket
   // everything from the first candidate evaluation to the final download
-  cudaEvent_t ev0, ev1;
-  RB_CUDA(cudaEventCreate(&ev0));
-  RB_CUDA(cudaEventCreate(&ev1));
-  RB_CUDA(cudaEventRecord(ev0, st_));
-
+  RB_CUDA(cudaEventCreate(&ev0_));
+  RB_CUDA(cudaEventCreate(&ev1_));
+  RB_CUDA(cudaEventRecord(ev0_, st_));
   // IterateState::zeros (solver.hpp:293)
   cur_ = 0;
   for (auto* buf : {&X_[0], &X_[1], &xb_, &epx_}) buf->zero(st_);
   for (auto* buf : {&y_, &yb_, &epy_}) buf->zero(st_);
   bad_h_[0] = std::numeric_limits<long long>::max();
   bad_.upload(bad_h_.get(), 1, st_);
+}
 
-  double omega = omega0;
+long long Engine::first_bad() {
+  bad_.download(bad_h_.get(), 1, st_);
+  RB_CUDA(cudaStreamSynchronize(st_));
+  return bad_h_[0];
+}
+
+void Engine::keep_best(bool avg) {
+  const int i = avg ? 1 : 0;
+  RB_CUDA(cudaMemcpyAsync(best_x_.get(), xu_[i].get(), sizeof(double) * n_, cudaMemcpyDeviceToDevice, st_));
+  if (m_) RB_CUDA(cudaMemcpyAsync(best_y_.get(), yu_[i].get(), sizeof(double) * m_, cudaMemcpyDeviceToDevice, st_));
+}
+
+void Engine::download(int src, double* x, double* y) {
+  if (src == 2) download_point(best_x_.get(), best_y_.get(), x, y);
+  else download_point(xu_[src].get(), yu_[src].get(), x, y);
+}
+
+void Engine::loop_end(rapdhg_result* out) {
+  RB_CUDA(cudaEventRecord(ev1_, st_));
+  RB_CUDA(cudaEventSynchronize(ev1_));
+  float loop_ms = 0.f;
+  RB_CUDA(cudaEventElapsedTime(&loop_ms, ev0_, ev1_));
+  cudaEventDestroy(ev0_);
+  cudaEventDestroy(ev1_);
+  out->loop_seconds = 1e-3 * loop_ms;
+  out->kernel_launches = launches_;
+  out->kernel_ms[0] = kernel_ms_[0], out->kernel_ms[1] = kernel_ms_[1];
+  out->kernel_count[0] = kernel_count_[0], out->kernel_count[1] = kernel_count_[1];
+}
+
+void Engine::solve(rapdhg_result* out, Clock::time_point t0) {
+  run_loop(*this, cfg_, LoopScalars{norm_q, norm_a, omega0, setup_seconds, n_, mi_, m_ - mi_}, out, t0);
+}
+
+// run_loop(): the loop of solver.hpp:293-471 on any backend, with inner steps
+// batched into chunks that end exactly where the reference would run a check.
+void run_loop(LoopBackend& be, const rapdhg_config& cfg, const LoopScalars& sc, rapdhg_result* out,
+              Clock::time_point t0) {
+  auto elapsed = [&] { return std::chrono::duration<double>(Clock::now() - t0).count(); };
+  const int n = sc.n, mi_ = sc.mi, m = sc.mi + sc.me;
+  const double norm_q = sc.norm_q, norm_a = sc.norm_a;
+  std::memset(out, 0, sizeof(*out));
+  out->n = n, out->m_ineq = sc.mi, out->m_eq = sc.me;
+  out->norm_q = norm_q;
+  out->norm_a = norm_a;
+  be.loop_begin();
+  IterParams* params_h = be.host_params();
+
+  double omega = sc.omega0;
   long horizon = 1;
   const bool theoretical = cfg.step_rule == RAPDHG_STEP_THEORETICAL;
   const bool accelerated = cfg.algorithm == RAPDHG_ALG_APDHG;
@@ -753,13 +672,9 @@ void Engine::solve(rapdhg_result* out, Clock::time_point t0) {
   long k = 0;
 
   // candidates: index 0 = current (xu_[0], yu_[0]), 1 = average
-  Cand cand = evaluate();
+  Cand cand = be.evaluate();
   Kkt best = cand.res();
-  auto copy_best = [&](const Cand& c) {
-    const int i = c.is_avg ? 1 : 0;
-    RB_CUDA(cudaMemcpyAsync(best_x_.get(), xu_[i].get(), sizeof(double) * n, cudaMemcpyDeviceToDevice, st_));
-    if (m) RB_CUDA(cudaMemcpyAsync(best_y_.get(), yu_[i].get(), sizeof(double) * m, cudaMemcpyDeviceToDevice, st_));
-  };
+  auto copy_best = [&](const Cand& c) { be.keep_best(c.is_avg); };
   copy_best(cand);
   double epoch_start = cand.res().relkkt();
   double prev_candidate = std::numeric_limits<double>::infinity();
@@ -771,7 +686,7 @@ void Engine::solve(rapdhg_result* out, Clock::time_point t0) {
     double* ys = static_cast<double*>(std::realloc(out->restart_y, sizeof(double) * ((out->n_restart_points + 1) * m + 1)));
     if (!xs || !ys) throw Error(RAPDHG_E_INTERNAL, "out of host memory");
     out->restart_x = xs, out->restart_y = ys;
-    download_point(xu_[idx].get(), yu_[idx].get(), xs + out->n_restart_points * n, ys + out->n_restart_points * m);
+    be.download(idx, xs + out->n_restart_points * n, ys + out->n_restart_points * m);
     ++out->n_restart_points;
   };
   log(0, cand.res(), 0.0, omega, false);
@@ -815,7 +730,7 @@ void Engine::solve(rapdhg_result* out, Clock::time_point t0) {
         sp.eta = eta / omega;
         sp.tau = eta * omega;
       }
-      IterParams& q = params_h_[len];
+      IterParams& q = params_h[len];
       const double inv_beta = 1.0 / sp.beta;
       q.theta = sp.theta;
       q.ib = inv_beta;
@@ -825,7 +740,7 @@ void Engine::solve(rapdhg_result* out, Clock::time_point t0) {
       q.t = tt;
       q.emit_next = 0;
       if (len > 0) {
-        IterParams& pq = params_h_[len - 1];
+        IterParams& pq = params_h[len - 1];
         pq.theta_n = q.theta, pq.ib_n = q.ib, pq.omib_n = q.omib, pq.emit_next = 1;
       }
       ++len;
@@ -838,12 +753,11 @@ void Engine::solve(rapdhg_result* out, Clock::time_point t0) {
       if (check_due) break;
     }
     const long t_end = check_due ? tt : tt - 1;
-    run_chunk(len);
+    be.run_chunk(len);
     // all_finite after every step (solver.hpp:372-373): first bad iteration
-    bad_.download(bad_h_.get(), 1, st_);
-    RB_CUDA(cudaStreamSynchronize(st_));
-    if (bad_h_[0] <= t_end) {
-      finish(RAPDHG_STATUS_NUMERICAL_ERROR, 2, static_cast<long>(bad_h_[0]), best);
+    const long long bad = be.first_bad();
+    if (bad <= t_end) {
+      finish(RAPDHG_STATUS_NUMERICAL_ERROR, 2, static_cast<long>(bad), best);
       break;
     }
     t = t_end + 1;
@@ -851,7 +765,7 @@ void Engine::solve(rapdhg_result* out, Clock::time_point t0) {
     const long tc = t_end;
     const double cur_eta = theoretical ? sp.eta : eta;
 
-    cand = evaluate();
+    cand = be.evaluate();
     const Kkt cres = cand.res();
     if (cres.relkkt() < best.relkkt()) {
       best = cres;
@@ -862,7 +776,7 @@ void Engine::solve(rapdhg_result* out, Clock::time_point t0) {
       append(out->snapshot_iters, out->n_snapshots, static_cast<int64_t>(tc));
       out->snapshot_x = static_cast<double*>(std::realloc(out->snapshot_x, sizeof(double) * ((s + 1) * n + 1)));
       out->snapshot_y = static_cast<double*>(std::realloc(out->snapshot_y, sizeof(double) * ((s + 1) * m + 1)));
-      download_point(xu_[1].get(), yu_[1].get(), out->snapshot_x + s * n, out->snapshot_y + s * m);
+      be.download(1, out->snapshot_x + s * n, out->snapshot_y + s * m);
     }
     if (cres.relkkt() <= cfg.tol) {
       log(tc, cres, cur_eta, omega, false);
@@ -896,7 +810,7 @@ void Engine::solve(rapdhg_result* out, Clock::time_point t0) {
 
     if (horizon_hit && !fixed_due) horizon *= 2;
     double dx = 0.0, dy = 0.0;
-    restart(from_avg, &dx, &dy);
+    be.restart(from_avg, &dx, &dy);
     k = 0;
     out->restarts += 1;
     prev_eta = 0.0;
@@ -913,25 +827,15 @@ void Engine::solve(rapdhg_result* out, Clock::time_point t0) {
   out->residuals = {fin_res.r_primal, fin_res.r_dual, fin_res.r_gap};
   out->x = xalloc<double>(n);
   double* yall = xalloc<double>(m);
-  if (fin_src == 2) download_point(best_x_.get(), best_y_.get(), out->x, yall);
-  else download_point(xu_[fin_src].get(), yu_[fin_src].get(), out->x, yall);
+  be.download(fin_src, out->x, yall);
   out->y_ineq = xalloc<double>(mi_);
   out->y_eq = xalloc<double>(m - mi_);
   if (mi_) std::memcpy(out->y_ineq, yall, sizeof(double) * mi_);
   if (m - mi_) std::memcpy(out->y_eq, yall + mi_, sizeof(double) * (m - mi_));
   std::free(yall);
-  RB_CUDA(cudaEventRecord(ev1, st_));
-  RB_CUDA(cudaEventSynchronize(ev1));
-  float loop_ms = 0.f;
-  RB_CUDA(cudaEventElapsedTime(&loop_ms, ev0, ev1));
-  cudaEventDestroy(ev0);
-  cudaEventDestroy(ev1);
-  out->loop_seconds = 1e-3 * loop_ms;
-  out->setup_seconds = setup_seconds;
+  be.loop_end(out);
+  out->setup_seconds = sc.setup_seconds;
   out->solve_seconds = elapsed();
-  out->kernel_launches = launches_;
-  out->kernel_ms[0] = kernel_ms_[0], out->kernel_ms[1] = kernel_ms_[1];
-  out->kernel_count[0] = kernel_count_[0], out->kernel_count[1] = kernel_count_[1];
 }
 
 // ============================================================================

@@ -96,10 +96,46 @@ class DeviceQP {
   int64_t launches = 0;
 };
 
-class Engine {
+// relKKT of the current iterate and of the average at one check
+// (evaluate_candidate, solver.hpp:255-264): the candidate is the smaller,
+// ties to the average.
+struct Cand {
+  Kkt cur, avg;
+  bool is_avg = true;
+  const Kkt& res() const { return is_avg ? avg : cur; }
+};
+
+// Device side of the iteration loop. run_loop() (the host controller:
+// chunk planning, checks, restarts — solver.hpp:293-471) drives any backend:
+// the single-GPU Engine or the row-sharded ShardedEngine (sharded.cu).
+class LoopBackend {
+ public:
+  virtual ~LoopBackend() = default;
+  virtual void loop_begin() = 0;          // zero state (solver.hpp:293), start timers
+  virtual IterParams* host_params() = 0;  // kMaxChunk pinned entries
+  virtual void run_chunk(int len) = 0;    // len inner steps with host_params()[0..len)
+  virtual long long first_bad() = 0;      // first non-finite iteration (sticky), syncs
+  virtual Cand evaluate() = 0;            // unscale + relKKT of current and average
+  virtual void keep_best(bool avg) = 0;   // best <- that candidate's unscaled point
+  virtual void restart(bool from_avg, double* dx, double* dy) = 0;  // + dist2 for omega
+  virtual void download(int src, double* x, double* y) = 0;  // 0 cur, 1 avg, 2 best
+  virtual void loop_end(rapdhg_result* out) = 0;  // loop time, launch counts
+};
+
+struct LoopScalars {
+  double norm_q, norm_a, omega0, setup_seconds;
+  int n, mi, me;
+};
+
+void run_loop(LoopBackend& be, const rapdhg_config& cfg, const LoopScalars& sc, rapdhg_result* out,
+              Clock::time_point t0);
+
+class ShardedEngine;
+
+class Engine : public LoopBackend {
  public:
   Engine(const rapdhg_qp& p, const rapdhg_config& cfg, Clock::time_point t0);
-  ~Engine();
+  ~Engine() override;
   Engine(const Engine&) = delete;
   Engine& operator=(const Engine&) = delete;
 
@@ -114,17 +150,22 @@ class Engine {
   double bytes_dual() const;
   double bytes_primal() const;
 
+  // LoopBackend
+  void loop_begin() override;
+  IterParams* host_params() override { return params_h_.get(); }
+  void run_chunk(int len) override;
+  long long first_bad() override;
+  Cand evaluate() override;
+  void keep_best(bool avg) override;
+  void restart(bool from_avg, double* dx, double* dy) override;
+  void download(int src, double* x, double* y) override;
+  void loop_end(rapdhg_result* out) override;
+
  private:
-  struct Cand {
-    Kkt cur, avg;
-    bool is_avg;
-    const Kkt& res() const { return is_avg ? avg : cur; }
-  };
-  Cand evaluate();
-  void run_chunk(int len);
+  friend class ShardedEngine;
   void launch_chunk_body(int len, int cur, bool prof);
-  void restart(bool from_avg, double* dx, double* dy);
   void download_point(const double* xu, const double* yu, double* x, double* y);
+  cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
 
   rapdhg_config cfg_;
   std::unique_ptr<DeviceQP> P_;

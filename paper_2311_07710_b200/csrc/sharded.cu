@@ -1,0 +1,512 @@
+// sharded.cu — row-sharded multi-GPU rAPDHG; see sharded.hpp for the design.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <mutex>
+#include <string>
+
+#include "elementwise.cuh"
+#include "sharded.hpp"
+#include "terms.cuh"
+
+namespace rb {
+
+namespace {
+
+inline unsigned grid1(int64_t n) { return static_cast<unsigned>(ceil_div(n > 0 ? n : 1, 256)); }
+
+// Boundaries of `parts` contiguous blocks of rows with costs len[r] + 2,
+// inner boundaries rounded to multiples of kRedChunk (never decreasing).
+std::vector<int32_t> balanced_bounds(const std::vector<int64_t>& cost_prefix, int32_t rows, int parts) {
+  std::vector<int32_t> b(parts + 1, 0);
+  b[parts] = rows;
+  const double total = static_cast<double>(cost_prefix[rows]);
+  for (int k = 1; k < parts; ++k) {
+    const double target = total * k / parts;
+    const auto it = std::lower_bound(cost_prefix.begin(), cost_prefix.end(), static_cast<int64_t>(target));
+    int64_t r = std::distance(cost_prefix.begin(), it);
+    r = ((r + kRedChunk / 2) / kRedChunk) * kRedChunk;  // align for the chunked reductions
+    r = std::min<int64_t>(std::max<int64_t>(r, b[k - 1]), rows);
+    b[k] = static_cast<int32_t>(r);
+  }
+  return b;
+}
+
+}  // namespace
+
+ShardPlan make_shard_plan(const rapdhg_qp& p, int parts) {
+  if (parts < 1) invalid("shard plan: parts must be >= 1");
+  const int n = p.n, m = p.m_ineq + p.m_eq;
+  // dual rows: rows of [A_ineq; A_eq]
+  std::vector<int64_t> dp(static_cast<std::size_t>(m) + 1, 0);
+  for (int i = 0; i < p.m_ineq; ++i) dp[i + 1] = dp[i] + (p.a_ineq.row_ptr[i + 1] - p.a_ineq.row_ptr[i]) + 2;
+  for (int i = 0; i < p.m_eq; ++i)
+    dp[p.m_ineq + i + 1] = dp[p.m_ineq + i] + (p.a_eq.row_ptr[i + 1] - p.a_eq.row_ptr[i]) + 2;
+  // primal rows: rows of [Q | A'] (A' row j = column j of A)
+  std::vector<int64_t> colcnt(static_cast<std::size_t>(n), 0);
+  for (int64_t k = 0; k < p.a_ineq.nnz; ++k) ++colcnt[p.a_ineq.col_idx[k]];
+  for (int64_t k = 0; k < p.a_eq.nnz; ++k) ++colcnt[p.a_eq.col_idx[k]];
+  std::vector<int64_t> pp(static_cast<std::size_t>(n) + 1, 0);
+  for (int j = 0; j < n; ++j) pp[j + 1] = pp[j] + (p.q.row_ptr[j + 1] - p.q.row_ptr[j]) + colcnt[j] + 2;
+  ShardPlan plan;
+  plan.dual = balanced_bounds(dp, m, parts);
+  plan.primal = balanced_bounds(pp, n, parts);
+  return plan;
+}
+
+// ---- transports ----------------------------------------------------------------
+
+namespace {
+
+class EmulatedTransport : public Transport {
+ public:
+  explicit EmulatedTransport(int parts) : parts_(parts) {}
+  void allgatherv(const std::vector<double*>& bufs, const std::vector<int64_t>& b, cudaStream_t st) override {
+    for (int k = 0; k < parts_; ++k) {  // owner k's slice into every other shard's copy
+      const int64_t len = b[k + 1] - b[k];
+      if (len <= 0) continue;
+      for (int j = 0; j < parts_; ++j)
+        if (j != k)
+          RB_CUDA(cudaMemcpyAsync(bufs[j] + b[k], bufs[k] + b[k], sizeof(double) * len, cudaMemcpyDeviceToDevice, st));
+    }
+  }
+  long long allreduce_min(const std::vector<long long*>& vals, cudaStream_t st) override {
+    long long best = std::numeric_limits<long long>::max();
+    for (long long* v : vals) {
+      long long h = 0;
+      RB_CUDA(cudaMemcpyAsync(&h, v, sizeof(h), cudaMemcpyDeviceToHost, st));
+      RB_CUDA(cudaStreamSynchronize(st));
+      best = std::min(best, h);
+    }
+    return best;
+  }
+
+ private:
+  int parts_;
+};
+
+// libnccl is loaded on first use so the library itself has no NCCL
+// dependency (and coexists with whichever libnccl.so.2 torch loaded first).
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  static std::string err;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      err = std::string("cannot load libnccl: ") + dlerror();
+      return;
+    }
+    auto sym = [&](const char* name) {
+      void* f = dlsym(h, name);
+      if (!f) err = std::string("libnccl lacks ") + name;
+      return f;
+    };
+    api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
+    api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
+    api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+    api.Broadcast = reinterpret_cast<decltype(api.Broadcast)>(sym("ncclBroadcast"));
+    api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
+    api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+    api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
+    api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+  });
+  if (!err.empty()) throw Error(RAPDHG_E_CUDA, err);
+  return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess)
+    throw Error(RAPDHG_E_CUDA, std::string(what) + ": " + (nccl().GetErrorString ? nccl().GetErrorString(r) : "nccl error"));
+}
+
+class NcclTransport : public Transport {
+ public:
+  NcclTransport(int parts, int rank, const void* id) : parts_(parts), rank_(rank) {
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    nccl_check(nccl().CommInitRank(&comm_, parts, uid, rank), "ncclCommInitRank");
+    RB_CUDA(cudaMalloc(&scratch_, sizeof(long long)));
+  }
+  ~NcclTransport() override {
+    if (comm_) nccl().CommDestroy(comm_);
+    if (scratch_) cudaFree(scratch_);
+  }
+  // allgather-v: every owner broadcasts its slice in place, grouped
+  void allgatherv(const std::vector<double*>& bufs, const std::vector<int64_t>& b, cudaStream_t st) override {
+    double* buf = bufs.at(0);
+    nccl_check(nccl().GroupStart(), "ncclGroupStart");
+    for (int k = 0; k < parts_; ++k) {
+      const int64_t len = b[k + 1] - b[k];
+      if (len > 0)
+        nccl_check(nccl().Broadcast(buf + b[k], buf + b[k], static_cast<size_t>(len), ncclDouble, k, comm_, st),
+                   "ncclBroadcast");
+    }
+    nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
+  }
+  long long allreduce_min(const std::vector<long long*>& vals, cudaStream_t st) override {
+    nccl_check(nccl().AllReduce(vals.at(0), scratch_, 1, ncclInt64, ncclMin, comm_, st), "ncclAllReduce");
+    long long h = 0;
+    RB_CUDA(cudaMemcpyAsync(&h, scratch_, sizeof(h), cudaMemcpyDeviceToHost, st));
+    RB_CUDA(cudaStreamSynchronize(st));
+    return h;
+  }
+
+ private:
+  int parts_, rank_;
+  ncclComm_t comm_ = nullptr;
+  long long* scratch_ = nullptr;
+};
+
+}  // namespace
+
+std::unique_ptr<Transport> make_emulated_transport(int parts) {
+  return std::make_unique<EmulatedTransport>(parts);
+}
+std::unique_ptr<Transport> make_nccl_transport(int parts, int rank, const void* id) {
+  return std::make_unique<NcclTransport>(parts, rank, id);
+}
+void nccl_unique_id(void* out) {
+  ncclUniqueId uid;
+  nccl_check(nccl().GetUniqueId(&uid), "ncclGetUniqueId");
+  std::memcpy(out, &uid, sizeof(uid));
+}
+
+// ---- the sharded engine -----------------------------------------------------------
+
+struct ShardedEngine::Shard {
+  int id = 0;
+  int64_t d0 = 0, d1 = 0, p0 = 0, p1 = 0;  // dual / primal row blocks
+  Schedule sch_dual, sch_primal;
+  // full-length copies; only the owned slice is computed here, the rest is
+  // received by the exchanges
+  DevBuf<double> X[2], XMD[2], w, xb, y, yb, epx, epy, xu[2], yu[2], ax[2], qx[2], aty[2], best_x, best_y;
+  DevBuf<long long> bad;
+  ReduceScratch red;
+  DevBuf<double> red_out;
+};
+
+ShardedEngine::ShardedEngine(const rapdhg_qp& p, const rapdhg_config& cfg, int parts, int rank,
+                             std::unique_ptr<Transport> tr, Clock::time_point t0)
+    : cfg_(cfg), parts_(parts), tr_(std::move(tr)) {
+  if (cfg.strict_parity) invalid("sharded solve: strict_parity needs sequential reductions; use one GPU");
+  if (parts < 1) invalid("sharded solve: parts must be >= 1");
+  full_ = std::make_unique<Engine>(p, cfg, t0);  // validation, scaling, norms
+  plan_ = make_shard_plan(p, parts);
+  st_ = full_->st_;
+  DeviceQP& P = *full_->P_;
+  const int n = P.n, m = P.m;
+  pb_.assign(plan_.primal.begin(), plan_.primal.end());
+  db_.assign(plan_.dual.begin(), plan_.dual.end());
+  for (int s = 0; s < parts; ++s) {
+    if (rank >= 0 && s != rank) continue;
+    auto sh = std::make_unique<Shard>();
+    sh->id = s;
+    sh->d0 = db_[s], sh->d1 = db_[s + 1], sh->p0 = pb_[s], sh->p1 = pb_[s + 1];
+    DevBuf<int32_t> len;
+    row_lengths(len, P.A.rp.get() + sh->d0, nullptr, sh->d1 - sh->d0, st_);
+    build_schedule(sh->sch_dual, len.get(), sh->d1 - sh->d0, false, st_);
+    row_lengths(len, P.Q.rp.get() + sh->p0, P.AT.rp.get() + sh->p0, sh->p1 - sh->p0, st_);
+    build_schedule(sh->sch_primal, len.get(), sh->p1 - sh->p0, false, st_);
+    for (int i = 0; i < 2; ++i) {
+      sh->X[i].alloc(n), sh->XMD[i].alloc(n), sh->xu[i].alloc(n), sh->yu[i].alloc(m);
+      sh->ax[i].alloc(m), sh->qx[i].alloc(n), sh->aty[i].alloc(n);
+    }
+    sh->w.alloc(n), sh->xb.alloc(n), sh->y.alloc(m), sh->yb.alloc(m), sh->epx.alloc(n), sh->epy.alloc(m);
+    sh->best_x.alloc(n), sh->best_y.alloc(m);
+    sh->bad.alloc(1);
+    sh->red.init(std::max<int64_t>(n, m), st_);
+    sh->red_out.alloc(64);
+    shards_.push_back(std::move(sh));
+  }
+  params_.alloc(kMaxChunk);
+  params_h_.alloc(kMaxChunk);
+  red_h_.alloc(64);
+  RB_CUDA(cudaStreamSynchronize(st_));
+}
+
+ShardedEngine::~ShardedEngine() {
+  for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
+}
+
+void ShardedEngine::solve(rapdhg_result* out, Clock::time_point t0) {
+  const Engine& e = *full_;
+  run_loop(*this, cfg_, LoopScalars{e.norm_q, e.norm_a, e.omega0, e.setup_seconds, e.n_, e.mi_, e.m_ - e.mi_},
+           out, t0);
+}
+
+void ShardedEngine::exchange(double* (*pick)(Shard&), bool primal_space) {
+  std::vector<double*> bufs;
+  for (auto& sh : shards_) bufs.push_back(pick(*sh));
+  tr_->allgatherv(bufs, primal_space ? pb_ : db_, st_);
+}
+
+// One deterministic reduction over the primal (n) or dual (m) index space:
+// per-shard chunk partials, allgather-v of the partials, fixed combine.
+template <int NS, int NM, class MakeF>
+void ShardedEngine::reduce(bool primal_space, const MakeF& make, double* out_host) {
+  constexpr int NT = NS + NM;
+  const std::vector<int64_t>& b = primal_space ? pb_ : db_;
+  const int64_t total = b.back();
+  if (total == 0) {
+    for (int k = 0; k < NT; ++k) out_host[k] = 0.0;
+    return;
+  }
+  for (auto& sh : shards_) {
+    const int64_t lo = b[sh->id], hi = b[sh->id + 1];
+    launch_reduce_partials<NS, NM>(make(*sh, lo), hi - lo, lo / kRedChunk, sh->red, st_);
+    ++launches_;
+  }
+  std::vector<int64_t> cb(parts_ + 1);
+  for (int k = 0; k < parts_; ++k) cb[k] = (b[k] / kRedChunk) * NT;
+  cb[parts_] = reduce_chunks(total) * NT;
+  std::vector<double*> bufs;
+  for (auto& sh : shards_) bufs.push_back(sh->red.partials.get());
+  tr_->allgatherv(bufs, cb, st_);
+  Shard& s0 = *shards_[0];
+  launch_reduce_combine<NS, NM>(total, s0.red, s0.red_out.get(), st_);
+  ++launches_;
+  RB_CUDA(cudaMemcpyAsync(red_h_.get(), s0.red_out.get(), sizeof(double) * NT, cudaMemcpyDeviceToHost, st_));
+  RB_CUDA(cudaStreamSynchronize(st_));
+  for (int k = 0; k < NT; ++k) out_host[k] = red_h_[k];
+}
+
+void ShardedEngine::loop_begin() {
+  launches_ = 0;
+  cur_ = 0;
+  RB_CUDA(cudaEventCreate(&ev0_));
+  RB_CUDA(cudaEventCreate(&ev1_));
+  RB_CUDA(cudaEventRecord(ev0_, st_));
+  const long long big = std::numeric_limits<long long>::max();
+  for (auto& sh : shards_) {
+    for (auto* buf : {&sh->X[0], &sh->X[1], &sh->xb, &sh->epx, &sh->y, &sh->yb, &sh->epy}) buf->zero(st_);
+    RB_CUDA(cudaMemcpyAsync(sh->bad.get(), &big, sizeof(big), cudaMemcpyHostToDevice, st_));
+  }
+  RB_CUDA(cudaStreamSynchronize(st_));
+}
+
+void ShardedEngine::body(int len, int cur) {
+  DeviceQP& P = *full_->P_;
+  const Engine& e = *full_;
+  // chunk prologue: w and x_md of the first step on each slice, then exchange
+  for (auto& sh : shards_) {
+    const int64_t nl = sh->p1 - sh->p0;
+    if (nl > 0) {
+      prologue_kernel<<<grid1(nl), 256, 0, st_>>>(sh->X[cur].get() + sh->p0, sh->X[cur ^ 1].get() + sh->p0,
+                                                  sh->xb.get() + sh->p0, sh->w.get() + sh->p0,
+                                                  sh->XMD[cur].get() + sh->p0, params_.get(), static_cast<int>(nl));
+      RB_LAUNCH_CHECK();
+      ++launches_;
+    }
+  }
+  const int c0 = cur;
+  exchange([](Shard& s) { return s.w.get(); }, true);
+  if (c0 == 0) exchange([](Shard& s) { return s.XMD[0].get(); }, true);
+  else exchange([](Shard& s) { return s.XMD[1].get(); }, true);
+  for (int it = 0; it < len; ++it) {
+    const int c = (cur + it) & 1;
+    for (auto& sh : shards_) {
+      if (sh->d1 <= sh->d0) continue;
+      DualStepOp<false> d{CsrView{P.A.rp.get() + sh->d0, P.A.ci.get(), e.asv_}, sh->w.get(), e.bsv_ + sh->d0,
+                          sh->y.get() + sh->d0, sh->yb.get() + sh->d0, e.mi_ - static_cast<int>(sh->d0),
+                          params_.get(), it, sh->bad.get()};
+      launch_rowwise(d, sh->sch_dual.view, st_);
+      ++launches_;
+    }
+    exchange([](Shard& s) { return s.y.get(); }, false);
+    for (auto& sh : shards_) {
+      if (sh->p1 <= sh->p0) continue;
+      const int64_t o = sh->p0;
+      PrimalStepOp<false> pr{CsrView{P.Q.rp.get() + o, P.Q.ci.get(), e.qsv_},
+                             CsrView{P.AT.rp.get() + o, P.AT.ci.get(), e.atsv_},
+                             sh->XMD[c].get(), sh->y.get(), sh->X[c].get() + o, sh->X[c ^ 1].get() + o,
+                             sh->xb.get() + o, e.csv_ + o, sh->w.get() + o, sh->XMD[c ^ 1].get() + o,
+                             params_.get(), it, sh->bad.get()};
+      launch_rowwise(pr, sh->sch_primal.view, st_);
+      ++launches_;
+    }
+    if (it + 1 < len) {  // the next step gathers the new w and x_md
+      exchange([](Shard& s) { return s.w.get(); }, true);
+      if (c == 0) exchange([](Shard& s) { return s.XMD[1].get(); }, true);
+      else exchange([](Shard& s) { return s.XMD[0].get(); }, true);
+    }
+  }
+}
+
+void ShardedEngine::run_chunk(int len) {
+  params_.upload(params_h_.get(), len, st_);
+  if (cfg_.use_graphs) {
+    const int key = (len << 1) | cur_;
+    auto it = graphs_.find(key);
+    if (it == graphs_.end()) {
+      cudaGraph_t g;
+      const int64_t before = launches_;
+      RB_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
+      body(len, cur_);
+      RB_CUDA(cudaStreamEndCapture(st_, &g));
+      const int64_t per_replay = launches_ - before;
+      launches_ = before;
+      cudaGraphExec_t ge;
+      RB_CUDA(cudaGraphInstantiate(&ge, g, 0));
+      cudaGraphDestroy(g);
+      it = graphs_.emplace(key, ge).first;
+      replay_launches_[key] = per_replay;
+    }
+    RB_CUDA(cudaGraphLaunch(it->second, st_));
+    launches_ += replay_launches_[key];
+  } else {
+    body(len, cur_);
+  }
+  cur_ ^= (len & 1);
+  RB_CUDA(cudaStreamSynchronize(st_));
+}
+
+long long ShardedEngine::first_bad() {
+  std::vector<long long*> v;
+  for (auto& sh : shards_) v.push_back(sh->bad.get());
+  return tr_->allreduce_min(v, st_);
+}
+
+Cand ShardedEngine::evaluate() {
+  DeviceQP& P = *full_->P_;
+  const Engine& e = *full_;
+  const int n = e.n_, mi = e.mi_;
+  const double* d = e.d_.get();
+  for (auto& sh : shards_) {  // unscale the owned slices (scaling.hpp:126-133)
+    const int64_t nl = sh->p1 - sh->p0, ml = sh->d1 - sh->d0;
+    if (nl > 0)
+      unscale_kernel<<<grid1(nl), 256, 0, st_>>>(sh->X[cur_].get() + sh->p0, sh->xb.get() + sh->p0, nullptr, nullptr,
+                                                 d + sh->p0, sh->xu[0].get() + sh->p0, sh->xu[1].get() + sh->p0,
+                                                 nullptr, nullptr, static_cast<int>(nl), 0);
+    if (ml > 0)
+      unscale_kernel<<<grid1(ml), 256, 0, st_>>>(nullptr, nullptr, sh->y.get() + sh->d0, sh->yb.get() + sh->d0,
+                                                 d + n + sh->d0, nullptr, nullptr, sh->yu[0].get() + sh->d0,
+                                                 sh->yu[1].get() + sh->d0, 0, static_cast<int>(ml));
+    RB_LAUNCH_CHECK();
+    launches_ += 2;
+  }
+  exchange([](Shard& s) { return s.xu[0].get(); }, true);
+  exchange([](Shard& s) { return s.xu[1].get(); }, true);
+  exchange([](Shard& s) { return s.yu[0].get(); }, false);
+  exchange([](Shard& s) { return s.yu[1].get(); }, false);
+  for (auto& sh : shards_) {  // KKT products on the ORIGINAL matrices, owned rows
+    if (sh->d1 > sh->d0) {
+      KktAxOp<false> ax{CsrView{P.A.rp.get() + sh->d0, P.A.ci.get(), P.A.v.get()}, sh->xu[0].get(), sh->xu[1].get(),
+                        sh->ax[0].get() + sh->d0, sh->ax[1].get() + sh->d0};
+      launch_rowwise(ax, sh->sch_dual.view, st_);
+      ++launches_;
+    }
+    if (sh->p1 > sh->p0) {
+      const int64_t o = sh->p0;
+      KktQAtyOp<false> qa{CsrView{P.Q.rp.get() + o, P.Q.ci.get(), P.Q.v.get()},
+                          CsrView{P.AT.rp.get() + o, P.AT.ci.get(), P.AT.v.get()}, mi, sh->xu[0].get(),
+                          sh->xu[1].get(), sh->yu[0].get(), sh->yu[1].get(), sh->qx[0].get() + o,
+                          sh->qx[1].get() + o, sh->aty[0].get() + o, sh->aty[1].get() + o};
+      launch_rowwise(qa, sh->sch_primal.view, st_);
+      ++launches_;
+    }
+  }
+  double h[16], g[16];
+  const double* b = P.b.get();
+  const double* c = P.c.get();
+  reduce<4, 5>(false, [&](Shard& s, int64_t lo) {
+    return KktDualTerms{s.ax[0].get() + lo, s.ax[1].get() + lo, b + lo, s.yu[0].get() + lo, s.yu[1].get() + lo,
+                        mi - static_cast<int>(lo)};
+  }, h);
+  reduce<4, 7>(true, [&](Shard& s, int64_t lo) {
+    return KktPrimalTerms{s.qx[0].get() + lo, s.qx[1].get() + lo, s.aty[0].get() + lo, s.aty[1].get() + lo,
+                          s.xu[0].get() + lo, s.xu[1].get() + lo, c + lo};
+  }, g);
+  KktRaw r;
+  r.by_i[0] = h[0], r.by_e[0] = h[1], r.by_i[1] = h[2], r.by_e[1] = h[3];
+  r.viol[0] = h[4], r.viol[1] = h[5], r.ax_inf[0] = h[6], r.ax_inf[1] = h[7], r.b_inf = h[8];
+  r.xqx[0] = g[0], r.xqx[1] = g[1], r.cx[0] = g[2], r.cx[1] = g[3];
+  r.dn[0] = g[4], r.dn[1] = g[5], r.qx_inf[0] = g[6], r.qx_inf[1] = g[7];
+  r.aty_inf[0] = g[8], r.aty_inf[1] = g[9], r.c_inf = g[10];
+  Kkt k2[2];
+  finalize_kkt(r, k2);
+  Cand cd;
+  cd.cur = k2[0];
+  cd.avg = k2[1];
+  cd.is_avg = !(cd.cur.relkkt() < cd.avg.relkkt());  // ties -> average
+  return cd;
+}
+
+void ShardedEngine::keep_best(bool avg) {
+  const int i = avg ? 1 : 0;
+  for (auto& sh : shards_) {
+    const int64_t nl = sh->p1 - sh->p0, ml = sh->d1 - sh->d0;
+    if (nl > 0)
+      RB_CUDA(cudaMemcpyAsync(sh->best_x.get() + sh->p0, sh->xu[i].get() + sh->p0, sizeof(double) * nl,
+                              cudaMemcpyDeviceToDevice, st_));
+    if (ml > 0)
+      RB_CUDA(cudaMemcpyAsync(sh->best_y.get() + sh->d0, sh->yu[i].get() + sh->d0, sizeof(double) * ml,
+                              cudaMemcpyDeviceToDevice, st_));
+  }
+}
+
+void ShardedEngine::restart(bool from_avg, double* dx, double* dy) {
+  for (auto& sh : shards_) {  // solver.hpp:442-448 on the owned slices
+    const int64_t nl = sh->p1 - sh->p0, ml = sh->d1 - sh->d0;
+    if (nl > 0)
+      restart_kernel<<<grid1(nl), 256, 0, st_>>>(sh->X[cur_].get() + sh->p0, sh->X[cur_ ^ 1].get() + sh->p0,
+                                                 sh->xb.get() + sh->p0, nullptr, nullptr, from_avg ? 1 : 0,
+                                                 static_cast<int>(nl), 0);
+    if (ml > 0)
+      restart_kernel<<<grid1(ml), 256, 0, st_>>>(nullptr, nullptr, nullptr, sh->y.get() + sh->d0,
+                                                 sh->yb.get() + sh->d0, from_avg ? 1 : 0, 0, static_cast<int>(ml));
+    RB_LAUNCH_CHECK();
+    launches_ += 2;
+  }
+  const int cur = cur_;
+  double sx[1], sy[1];
+  reduce<1, 0>(true, [&](Shard& s, int64_t lo) { return DistAndAdvance{s.X[cur].get() + lo, s.epx.get() + lo}; }, sx);
+  reduce<1, 0>(false, [&](Shard& s, int64_t lo) { return DistAndAdvance{s.y.get() + lo, s.epy.get() + lo}; }, sy);
+  *dx = std::sqrt(sx[0]);
+  *dy = std::sqrt(sy[0]);
+}
+
+void ShardedEngine::download(int src, double* x, double* y) {
+  Shard& s0 = *shards_[0];
+  const double *xs, *ys;
+  if (src == 2) {
+    exchange([](Shard& s) { return s.best_x.get(); }, true);
+    exchange([](Shard& s) { return s.best_y.get(); }, false);
+    xs = s0.best_x.get(), ys = s0.best_y.get();
+  } else {  // the unscaled candidates were exchanged by evaluate()
+    xs = s0.xu[src].get(), ys = s0.yu[src].get();
+  }
+  const int64_t n = pb_.back(), m = db_.back();
+  if (n) RB_CUDA(cudaMemcpyAsync(x, xs, sizeof(double) * n, cudaMemcpyDeviceToHost, st_));
+  if (m) RB_CUDA(cudaMemcpyAsync(y, ys, sizeof(double) * m, cudaMemcpyDeviceToHost, st_));
+  RB_CUDA(cudaStreamSynchronize(st_));
+}
+
+void ShardedEngine::loop_end(rapdhg_result* out) {
+  RB_CUDA(cudaEventRecord(ev1_, st_));
+  RB_CUDA(cudaEventSynchronize(ev1_));
+  float ms = 0.f;
+  RB_CUDA(cudaEventElapsedTime(&ms, ev0_, ev1_));
+  cudaEventDestroy(ev0_);
+  cudaEventDestroy(ev1_);
+  out->loop_seconds = 1e-3 * ms;
+  out->kernel_launches = full_->P_->launches + launches_;
+}
+
+}  // namespace rb

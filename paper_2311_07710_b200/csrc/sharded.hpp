@@ -1,0 +1,101 @@
+// sharded.hpp — row-sharded multi-GPU rAPDHG.
+//
+// Rank k owns a contiguous block of the dual rows (rows of A = [A_ineq; A_eq])
+// and a contiguous block of the primal rows (rows of [Q | A']), balanced by
+// nnz and aligned to kRedChunk so the chunked reductions (reduce.cuh) see the
+// same chunks as on one GPU. Every rank runs the full setup (validation,
+// scaling, norms: identical on every rank), then iterates on its row blocks
+// only: shard matrices are zero-copy row views of the set-up matrices.
+//
+// Per inner step the exchange is one allgather-v of y (after the dual step)
+// and one of w and x_md (after the primal step, except on a chunk's last
+// step); checks exchange the unscaled points and the reduction partials. Each
+// row is computed exactly as on one GPU (same row, same length, same lanes),
+// and reductions combine the same chunk partials in the same order, so a
+// sharded solve is BIT-IDENTICAL to the single-GPU fast-mode solve.
+//
+// Transports: Emulated (all shards in one process on one GPU; exchanges are
+// D2D copies of the owner's slice into every other shard's buffer — used to
+// test the sharded path on a single B200) and NCCL (one process per GPU;
+// allgather-v as grouped in-place ncclBroadcast from each owner; libnccl is
+// dlopen'ed on first use).
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "engine.hpp"
+
+namespace rb {
+
+struct ShardPlan {
+  std::vector<int32_t> dual;    // parts + 1 bounds over [0, m)
+  std::vector<int32_t> primal;  // parts + 1 bounds over [0, n)
+};
+
+// nnz-balanced contiguous blocks; inner bounds are multiples of kRedChunk.
+ShardPlan make_shard_plan(const rapdhg_qp& p, int parts);
+
+class Transport {
+ public:
+  virtual ~Transport() = default;
+  // After the call, bufs[s] (one per LOCAL shard) holds every owner's slice
+  // [bounds[k], bounds[k+1]) of the vector (elements of 8 bytes).
+  virtual void allgatherv(const std::vector<double*>& bufs, const std::vector<int64_t>& bounds,
+                          cudaStream_t st) = 0;
+  // Minimum over all shards of one int64 per local shard, returned to host.
+  virtual long long allreduce_min(const std::vector<long long*>& vals, cudaStream_t st) = 0;
+};
+
+std::unique_ptr<Transport> make_emulated_transport(int parts);
+// NCCL communicator for `rank` of `parts` from a 128-byte ncclUniqueId.
+std::unique_ptr<Transport> make_nccl_transport(int parts, int rank, const void* unique_id);
+void nccl_unique_id(void* out128);
+
+class ShardedEngine : public LoopBackend {
+ public:
+  // rank < 0: emulate all `parts` shards in this process; else own shard `rank`.
+  ShardedEngine(const rapdhg_qp& p, const rapdhg_config& cfg, int parts, int rank,
+                std::unique_ptr<Transport> tr, Clock::time_point t0);
+  ~ShardedEngine() override;
+  void solve(rapdhg_result* out, Clock::time_point t0);
+
+  void loop_begin() override;
+  IterParams* host_params() override { return params_h_.get(); }
+  void run_chunk(int len) override;
+  long long first_bad() override;
+  Cand evaluate() override;
+  void keep_best(bool avg) override;
+  void restart(bool from_avg, double* dx, double* dy) override;
+  void download(int src, double* x, double* y) override;
+  void loop_end(rapdhg_result* out) override;
+
+  const ShardPlan& plan() const { return plan_; }
+
+ private:
+  struct Shard;
+  void body(int len, int cur);
+  void exchange(double* (*pick)(Shard&), bool primal_space);
+  template <int NS, int NM, class MakeF>
+  void reduce(bool primal_space, const MakeF& make, double* out_host);
+
+  rapdhg_config cfg_;
+  std::unique_ptr<Engine> full_;  // the set-up problem (matrices, scaling, norms)
+  ShardPlan plan_;
+  int parts_;
+  std::vector<std::unique_ptr<Shard>> shards_;  // local shards
+  std::unique_ptr<Transport> tr_;
+  cudaStream_t st_ = nullptr;
+  int cur_ = 0;
+  std::vector<int64_t> pb_, db_;  // primal / dual bounds as int64
+  DevBuf<IterParams> params_;
+  PinnedBuf<IterParams> params_h_;
+  PinnedBuf<double> red_h_;
+  ReduceScratch red_;  // partials over the full index space (chunks)
+  std::map<int, cudaGraphExec_t> graphs_;
+  std::map<int, int64_t> replay_launches_;
+  cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+  int64_t launches_ = 0;
+};
+
+}  // namespace rb

@@ -228,6 +228,15 @@ int rapdhg_nccl_unique_id(uint8_t* out128);
 int rapdhg_solve_sharded(const rapdhg_qp* qp, const rapdhg_config* cfg,
                          const rapdhg_shard_opts* opts, rapdhg_result* out);
 
+/* Persistent sharded session: setup and communicator once (an ncclUniqueId
+ * bootstraps exactly one communicator), then repeated solves from the zero
+ * start. Collective: every rank calls create / solve / destroy together. */
+typedef struct rapdhg_shard_session rapdhg_shard_session;
+int rapdhg_shard_session_create(const rapdhg_qp* qp, const rapdhg_config* cfg,
+                                const rapdhg_shard_opts* opts, rapdhg_shard_session** out);
+int rapdhg_shard_session_solve(rapdhg_shard_session* s, rapdhg_result* out);
+void rapdhg_shard_session_destroy(rapdhg_shard_session* s);
+
 /* ---- secondary API used by the reference's tests ----------------------- */
 
 /* y = M x (sparse.hpp:79-88) and y = M' x (sparse.hpp:91-100). */
@@ -325,6 +334,17 @@ void rapdhg_csr_free(rapdhg_csr_owned* m);
 void rapdhg_qp_free(rapdhg_qp_owned* p);
 /* Borrowed view of an owned QP, for passing to the compute entry points. */
 void rapdhg_qp_view(const rapdhg_qp_owned* p, rapdhg_qp* view);
+
+/* QPS (MPS + QUADOBJ/QMATRIX) text or file -> canonical QP: parse_qps
+ * (qps.hpp:69-298) then canonicalize (problem.hpp:131-198: G rows negated,
+ * ranges split, finite bounds as singleton <= rows, E rows kept). Parse errors
+ * return RAPDHG_E_PARSE with the reference's "qps parse error at line N: ..."
+ * message. Host-only. */
+int rapdhg_parse_qps(const char* text, rapdhg_qp_owned* out);
+int rapdhg_parse_qps_file(const char* path, rapdhg_qp_owned* out);
+/* write_qps (qps.hpp:320-381): *out is malloc'd text, release with rapdhg_free. */
+int rapdhg_write_qps(const rapdhg_qp* qp, char** out);
+void rapdhg_free(void* p);
 
 /* Synthetic instances of SURVEY §8(d) (no reference generator ships;
  * SPEC.md:417-489 describes the classes). scale multiplies the headline

@@ -79,6 +79,8 @@ class CpuSolver:
               abi.P_f64, abi.P_f64, abi.P_f64, abi.P_f64, abi.P_i64)
             d("parse_qps_canonical", C.c_int, C.c_char_p, P(abi.QpOwned))
             d("qp_free", None, P(abi.QpOwned))
+            d("write_qps", C.c_int, P(abi.Qp), P(C.c_void_p))
+            d("free", None, C.c_void_p)
         else:
             d("apply_scaling", C.c_int, P(abi.Qp), abi.P_f64, abi.P_f64, abi.P_f64, abi.P_f64,
               abi.P_f64, abi.P_f64, abi.P_f64, abi.P_f64)
@@ -213,6 +215,16 @@ class CpuSolver:
         cm = m._csr()
         self._check(self._fn("symmetry_gap")(C.byref(cm), C.byref(o)))
         return o.value
+
+    def write_qps(self, p: rb.QuadraticProgram) -> str:
+        """qps.hpp write_qps_string (reference build only)."""
+        ptr = C.c_void_p()
+        qp = p._struct()
+        self._check(self._fn("write_qps")(C.byref(qp), C.byref(ptr)))
+        try:
+            return C.string_at(ptr).decode()
+        finally:
+            self._fn("free")(ptr)
 
     def parse_qps(self, text: str) -> rb.QuadraticProgram:
         """qps.hpp parse + problem.hpp canonicalize (reference build only)."""

@@ -394,6 +394,17 @@ int ref_parse_qps_canonical(const char* text, rapdhg_qp_owned* out) {
   });
 }
 
+// write_qps (qps.hpp:320-381) of a canonical problem; free with ref_free.
+int ref_write_qps(const rapdhg_qp* p, char** out) {
+  return guard([&] {
+    const std::string s = write_qps_string(to_qp(p));
+    *out = static_cast<char*>(std::malloc(s.size() + 1));
+    std::memcpy(*out, s.c_str(), s.size() + 1);
+  });
+}
+
+void ref_free(void* p) { std::free(p); }
+
 void ref_csr_free(rapdhg_csr_owned* m) {
   if (!m) return;
   std::free(m->row_ptr);

@@ -110,8 +110,15 @@ def _load():
     d(lib, "rapdhg_qp_view", None, P(abi.QpOwned), P(abi.Qp))
     d(lib, "rapdhg_generate", C.c_int, C.c_int32, C.c_double, C.c_uint64, P(abi.QpOwned))
     d(lib, "rapdhg_shard_plan", C.c_int, P(abi.Qp), C.c_int32, abi.P_i32, abi.P_i32)
+    d(lib, "rapdhg_parse_qps", C.c_int, C.c_char_p, P(abi.QpOwned))
+    d(lib, "rapdhg_parse_qps_file", C.c_int, C.c_char_p, P(abi.QpOwned))
+    d(lib, "rapdhg_write_qps", C.c_int, P(abi.Qp), P(C.c_void_p))
+    d(lib, "rapdhg_free", None, C.c_void_p)
     d(lib, "rapdhg_nccl_unique_id", C.c_int, P(C.c_uint8))
     d(lib, "rapdhg_solve_sharded", C.c_int, P(abi.Qp), P(abi.Config), P(abi.ShardOpts), P(abi.Result))
+    d(lib, "rapdhg_shard_session_create", C.c_int, P(abi.Qp), P(abi.Config), P(abi.ShardOpts), P(C.c_void_p))
+    d(lib, "rapdhg_shard_session_solve", C.c_int, C.c_void_p, P(abi.Result))
+    d(lib, "rapdhg_shard_session_destroy", None, C.c_void_p)
     if lib.rapdhg_abi_version() != 1:
         raise ImportError("librapdhg_b200.so ABI version mismatch")
     _lib = lib
@@ -488,6 +495,47 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
+def _shard_opts(parts, emulate, rank, nccl_id) -> abi.ShardOpts:
+    opts = abi.ShardOpts()
+    opts.parts, opts.rank, opts.emulate = int(parts), int(rank), int(bool(emulate))
+    if nccl_id is not None:
+        C.memmove(opts.nccl_id, nccl_id, 128)
+    return opts
+
+
+class ShardSession:
+    """Persistent row-sharded solver: setup and (NCCL) communicator once, then
+    repeated solves. Collective across ranks when emulate=False."""
+
+    def __init__(self, original: QuadraticProgram, cfg: Optional[SolverConfig] = None, parts: int = 2,
+                 emulate: bool = True, rank: int = 0, nccl_id: Optional[bytes] = None):
+        self.cfg = cfg or SolverConfig()
+        h = C.c_void_p()
+        qp, cs, opts = original._struct(), self.cfg._struct(), _shard_opts(parts, emulate, rank, nccl_id)
+        _check(_load().rapdhg_shard_session_create(C.byref(qp), C.byref(cs), C.byref(opts), C.byref(h)))
+        self._h = h
+
+    def solve(self) -> SolveResult:
+        L = _load()
+        out = abi.Result()
+        _check(L.rapdhg_shard_session_solve(self._h, C.byref(out)))
+        try:
+            return result_from_struct(out)
+        finally:
+            L.rapdhg_result_free(C.byref(out))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _load().rapdhg_shard_session_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def solve_sharded(original: QuadraticProgram, cfg: Optional[SolverConfig] = None, parts: int = 2,
                   emulate: bool = True, rank: int = 0, nccl_id: Optional[bytes] = None) -> SolveResult:
     """Row-sharded solve. emulate=True runs all `parts` shards in
@@ -496,10 +544,7 @@ def solve_sharded(original: QuadraticProgram, cfg: Optional[SolverConfig] = None
     (nccl_unique_id() on rank 0, broadcast by the caller). Bit-identical to
     solve() in fast mode."""
     cfg = cfg or SolverConfig()
-    opts = abi.ShardOpts()
-    opts.parts, opts.rank, opts.emulate = int(parts), int(rank), int(bool(emulate))
-    if nccl_id is not None:
-        C.memmove(opts.nccl_id, nccl_id, 128)
+    opts = _shard_opts(parts, emulate, rank, nccl_id)
     qp, cs, out = original._struct(), cfg._struct(), abi.Result()
     L = _load()
     _check(L.rapdhg_solve_sharded(C.byref(qp), C.byref(cs), C.byref(opts), C.byref(out)))
@@ -737,6 +782,43 @@ def restart_decision(policy: RestartPolicy, ctx: RestartContext, fixed_length: i
     return bool(rc)
 
 
+# --- QPS I/O (qps.hpp + canonicalize, problem.hpp:131-198) -------------------
+
+def parse_qps(text: str) -> QuadraticProgram:
+    """parse_qps + canonicalize of QPS text (host; raises QpsParseError or
+    InvalidArgument with the reference's messages)."""
+    L = _load()
+    o = abi.QpOwned()
+    _check(L.rapdhg_parse_qps(text.encode(), C.byref(o)))
+    try:
+        return qp_from_owned(o)
+    finally:
+        L.rapdhg_qp_free(C.byref(o))
+
+
+def read_qps(path: str) -> QuadraticProgram:
+    """parse_qps_file (qps.hpp:300) + canonicalize."""
+    L = _load()
+    o = abi.QpOwned()
+    _check(L.rapdhg_parse_qps_file(os.fsencode(path), C.byref(o)))
+    try:
+        return qp_from_owned(o, os.path.basename(path))
+    finally:
+        L.rapdhg_qp_free(C.byref(o))
+
+
+def write_qps(p: QuadraticProgram) -> str:
+    """write_qps (qps.hpp:320-381) of a canonical problem."""
+    L = _load()
+    ptr = C.c_void_p()
+    qp = p._struct()
+    _check(L.rapdhg_write_qps(C.byref(qp), C.byref(ptr)))
+    try:
+        return C.string_at(ptr).decode()
+    finally:
+        L.rapdhg_free(ptr)
+
+
 # --- synthetic instances (SURVEY §8(d)) --------------------------------------
 
 class Gen(enum.IntEnum):
@@ -774,10 +856,10 @@ __all__ = [
     "SparseMatrix", "QuadraticProgram", "PrimalDualPoint", "SolverConfig", "SolveResult",
     "SolveStatus", "Algorithm", "RestartPolicy", "StepRule", "PrimalWeightMode", "KktResiduals",
     "LogRecord", "IterateState", "StepParams", "ScalingInfo", "PowerIterOptions", "RestartContext",
-    "Session", "Gen", "solve", "solve_sharded", "shard_plan", "nccl_unique_id", "inner_step", "pdhg_step", "rel_kkt", "compute_scaling",
+    "Session", "Gen", "solve", "solve_sharded", "ShardSession", "shard_plan", "nccl_unique_id", "inner_step", "pdhg_step", "rel_kkt", "compute_scaling",
     "ruiz_scaling", "apply_scaling", "unscale_point", "scale_point", "estimate_op_norm",
     "estimate_op_norm_symmetric", "step_schedule_theoretical", "pdhg_constant_steps",
     "adaptive_eta", "primal_weight_init", "primal_weight_update", "restart_decision", "generate",
-    "spmv", "spmv_t", "to_string", "device_count", "lib", "InvalidArgument", "NoDeviceError",
+    "spmv", "spmv_t", "to_string", "parse_qps", "read_qps", "write_qps", "device_count", "lib", "InvalidArgument", "NoDeviceError",
     "CudaError", "QpsParseError",
 ]

@@ -146,31 +146,67 @@ int rapdhg_nccl_unique_id(uint8_t* out128) {
   });
 }
 
+}  // extern "C"
+
+namespace {
+std::unique_ptr<rb::ShardedEngine> make_sharded(const rapdhg_qp* qp, const rapdhg_config* cfg,
+                                                const rapdhg_shard_opts* opts, rb::Clock::time_point t0) {
+  null_check(qp, "qp");
+  null_check(cfg, "cfg");
+  null_check(opts, "opts");
+  require_device();
+  if (opts->parts < 1) rb::invalid("sharded solve: parts must be >= 1");
+  std::unique_ptr<rb::Transport> tr;
+  int rank = -1;
+  if (opts->emulate) {
+    tr = rb::make_emulated_transport(opts->parts);
+  } else {
+    if (opts->rank < 0 || opts->rank >= opts->parts) rb::invalid("sharded solve: rank out of range");
+    RB_CUDA(cudaSetDevice(cfg->device));
+    tr = rb::make_nccl_transport(opts->parts, opts->rank, opts->nccl_id);
+    rank = opts->rank;
+  }
+  return std::make_unique<rb::ShardedEngine>(*qp, *cfg, opts->parts, rank, std::move(tr), t0);
+}
+}  // namespace
+
+struct rapdhg_shard_session {
+  std::unique_ptr<rb::ShardedEngine> engine;
+};
+
+extern "C" {
+
 int rapdhg_solve_sharded(const rapdhg_qp* qp, const rapdhg_config* cfg, const rapdhg_shard_opts* opts,
                          rapdhg_result* out) {
   return guard([&] {
     const auto t0 = rb::Clock::now();
-    null_check(qp, "qp");
-    null_check(cfg, "cfg");
-    null_check(opts, "opts");
     null_check(out, "out");
     std::memset(out, 0, sizeof(*out));
-    require_device();
-    if (opts->parts < 1) rb::invalid("sharded solve: parts must be >= 1");
-    std::unique_ptr<rb::Transport> tr;
-    int rank = -1;
-    if (opts->emulate) {
-      tr = rb::make_emulated_transport(opts->parts);
-    } else {
-      if (opts->rank < 0 || opts->rank >= opts->parts) rb::invalid("sharded solve: rank out of range");
-      RB_CUDA(cudaSetDevice(cfg->device));
-      tr = rb::make_nccl_transport(opts->parts, opts->rank, opts->nccl_id);
-      rank = opts->rank;
-    }
-    rb::ShardedEngine e(*qp, *cfg, opts->parts, rank, std::move(tr), t0);
-    e.solve(out, t0);
+    auto e = make_sharded(qp, cfg, opts, t0);
+    e->solve(out, t0);
   });
 }
+
+int rapdhg_shard_session_create(const rapdhg_qp* qp, const rapdhg_config* cfg, const rapdhg_shard_opts* opts,
+                                rapdhg_shard_session** out) {
+  return guard([&] {
+    null_check(out, "out");
+    *out = nullptr;
+    auto s = std::make_unique<rapdhg_shard_session>();
+    s->engine = make_sharded(qp, cfg, opts, rb::Clock::now());
+    *out = s.release();
+  });
+}
+
+int rapdhg_shard_session_solve(rapdhg_shard_session* s, rapdhg_result* out) {
+  return guard([&] {
+    null_check(s, "session");
+    null_check(out, "out");
+    s->engine->solve(out, rb::Clock::now());
+  });
+}
+
+void rapdhg_shard_session_destroy(rapdhg_shard_session* s) { delete s; }
 
 int rapdhg_session_create(const rapdhg_qp* qp, const rapdhg_config* cfg, rapdhg_session** out) {
   return guard([&] {

@@ -51,3 +51,18 @@ def test_sharded_rejects_strict():
     p = rb.generate(rb.Gen.LASSO, 0.02, 2)
     with pytest.raises(rb.InvalidArgument, match="strict_parity"):
         rb.solve_sharded(p, rb.SolverConfig(strict_parity=True), 2)
+
+
+def test_shard_session_repeated_solves():
+    p = rb.generate(rb.Gen.LASSO, 0.05, 2)
+    cfg = rb.SolverConfig(tol=1e-6, max_iters=2000)
+    base = rb.solve(p, cfg)
+    s = rb.ShardSession(p, cfg, parts=3)
+    for _ in range(2):
+        assert_results_identical(s.solve(), base)
+    s.close()
+    # one NCCL communicator, several solves
+    s = rb.ShardSession(p, cfg, parts=1, emulate=False, rank=0, nccl_id=rb.nccl_unique_id())
+    for _ in range(2):
+        assert_results_identical(s.solve(), base)
+    s.close()

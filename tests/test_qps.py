@@ -1,0 +1,151 @@
+"""CPU: QPS ingest against the reference's own parser
+(qps.hpp, compiled in place into oracle/_ref) — identical canonical problems,
+identical error messages — plus write/parse round trips."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2311_07710_b200 as rb
+from instances import random_qp
+
+pytestmark = pytest.mark.skipif(not oracle.have_ref(), reason="reference build absent")
+
+# SPEC.md:116 fixture: min x^2 - 2x s.t. x <= 0.5 (default bound x >= 0)
+ONE_D = """NAME          ONED
+ROWS
+ N  OBJ
+ L  C1
+COLUMNS
+    X  OBJ  -2.0  C1  1.0
+RHS
+    RHS  C1  0.5
+QUADOBJ
+    X  X  2.0
+ENDATA
+"""
+
+RICH = """* comment line
+NAME          RICH
+OBJSENSE
+    MIN
+ROWS
+ N  COST
+ L  LIM1
+ G  LIM2
+ E  MYEQN
+ E  REQ
+ L  RL
+COLUMNS
+    X1  COST  1.0   LIM1  1.0
+    X1  LIM2  1.0
+    X2  COST  2.0   LIM1  1.0
+    X2  MYEQN  -1.0  REQ  2.5
+    X3  COST  -1.0  MYEQN  1.0
+    X3  RL  3.0
+    X4  COST  0.5   REQ  1.0
+    X4  LIM2  -2.0  RL  -1.0
+RHS
+    RHS  COST  -3.5
+    RHS  LIM1  4.0   LIM2  1.0
+    RHS  MYEQN  7.0  REQ  1.5
+    RHS  RL  2.0
+RANGES
+    RNG  LIM1  2.5   LIM2  1.5
+    RNG  MYEQN  -2.0  REQ  3.0
+BOUNDS
+ UP BND  X1  4.0
+ MI BND  X2
+ UP BND  X3  -1.0
+ FX BND  X4  0.25
+QUADOBJ
+    X1  X1  2.0
+    X1  X2  0.5
+    X2  X2  3.0
+    X3  X3  1.0
+ENDATA
+"""
+
+
+def same_qp(a: rb.QuadraticProgram, b: rb.QuadraticProgram):
+    for ma, mb in ((a.q, b.q), (a.a_ineq, b.a_ineq), (a.a_eq, b.a_eq)):
+        assert (ma.n_rows, ma.n_cols) == (mb.n_rows, mb.n_cols)
+        assert np.array_equal(ma.row_ptr, mb.row_ptr) and np.array_equal(ma.col_idx, mb.col_idx)
+        assert np.array_equal(ma.values, mb.values)
+    assert np.array_equal(a.c, b.c) and np.array_equal(a.b_ineq, b.b_ineq) and np.array_equal(a.b_eq, b.b_eq)
+    assert a.obj_offset == b.obj_offset
+
+
+@pytest.mark.parametrize("text", [ONE_D, RICH])
+def test_parse_matches_reference(text):
+    same_qp(rb.parse_qps(text), oracle.ref().parse_qps(text))
+
+
+def test_one_d_fixture_shape():
+    p = rb.parse_qps(ONE_D)
+    # the default bound x >= 0 adds a second inequality row -x <= -0.0
+    assert p.num_vars() == 1 and p.num_ineq() == 2 and p.num_eq() == 0
+    assert list(p.b_ineq) == [0.5, -0.0] and np.signbit(p.b_ineq[1])
+    assert p.q.to_dense()[0, 0] == 2.0 and p.c[0] == -2.0
+
+
+def test_rich_semantics():
+    p = rb.parse_qps(RICH)
+    assert p.obj_offset == 3.5  # offset = -RHS on the objective row
+    # MYEQN with range -2 -> [5, 7]: two <= rows; REQ range 3 -> [1.5, 4.5]; no pure E rows
+    assert p.num_eq() == 0
+    Q = p.q.to_dense()
+    assert np.array_equal(Q, Q.T) and Q[0, 1] == 0.5
+
+
+def test_round_trip_write_parse():
+    for p in (random_qp(3, n=30, mi=12, me=4), rb.generate(rb.Gen.LASSO, 0.002, 1)):
+        p.obj_offset = 1.25
+        text = rb.write_qps(p)
+        assert text == _ref_write(p)
+        back = rb.parse_qps(text)
+        # canonical form written with FR bounds: parse+canonicalize reproduces it
+        same_qp(back, p)
+
+
+def _ref_write(p):
+    """The reference's own write_qps on the same problem."""
+    return oracle.ref().write_qps(p)
+
+
+@pytest.mark.parametrize("text,needle", [
+    ("NAME X\nROWS\n N OBJ\nCOLUMNS\n X OBJ 1.0 C9 2.0\nRHS\nENDATA\n", "undeclared row 'C9'"),
+    ("NAME X\nROWS\n N OBJ\nCOLUMNS\n X OBJ 1.0\n", "missing ENDATA"),
+    ("NAME X\nROWS\n N OBJ\n L C1\nCOLUMNS\n X C1 abc\nENDATA\n", "expected a numeric value, got 'abc'"),
+    ("NAME X\nNAME Y\nENDATA\n", "duplicate NAME section"),
+    ("NAME X\nROWS\n N OBJ\nCOLUMNS\n M1 'MARKER' 'INTORG'\nENDATA\n", "integer markers are not supported"),
+    ("NAME X\nROWS\n N OBJ\nCOLUMNS\n X OBJ 1.0\nBOUNDS\n BV B X\nENDATA\n", "unsupported bound type 'BV'"),
+    ("NAME X\nOBJSENSE\n MAX\nENDATA\n", "only minimization"),
+    ("NAME X\nROWS\n L C1\nCOLUMNS\n X C1 1.0\nENDATA\n", "no objective (N) row declared"),
+    ("NAME X\nFOO\nENDATA\n", "unknown section 'FOO'"),
+])
+def test_parse_errors_match_reference(text, needle):
+    with pytest.raises(rb.QpsParseError) as mine:
+        rb.parse_qps(text)
+    with pytest.raises(Exception) as ref:
+        oracle.ref().parse_qps(text)
+    assert needle in str(mine.value)
+    assert str(mine.value) == str(ref.value)
+
+
+def test_canonicalize_errors():
+    bad = ONE_D.replace("RHS\n", "BOUNDS\n LO BND X 2.0\n UP BND X 1.0\nRHS\n").replace(
+        "RHS\n    RHS  C1  0.5\n", "")
+    with pytest.raises(rb.InvalidArgument, match="infeasible bounds on variable X"):
+        rb.parse_qps(bad)
+    asym = ONE_D.replace("QUADOBJ\n    X  X  2.0\n", "QMATRIX\n    X  X  2.0\n    X  Y  1.0\n").replace(
+        "    X  OBJ  -2.0  C1  1.0\n", "    X  OBJ  -2.0  C1  1.0\n    Y  OBJ  1.0\n")
+    with pytest.raises(rb.InvalidArgument, match="Q is not symmetric"):
+        rb.parse_qps(asym)
+
+
+def test_read_file(tmp_path):
+    f = tmp_path / "oned.qps"
+    f.write_text(ONE_D)
+    same_qp(rb.read_qps(str(f)), rb.parse_qps(ONE_D))
+    with pytest.raises(rb.QpsParseError, match="cannot open"):
+        rb.read_qps(str(tmp_path / "missing.qps"))

@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--tol", type=float, default=1e-6)
     ap.add_argument("--max-iters", type=int, default=20000)
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--ref-iters", type=int, default=40)
+    ap.add_argument("--ref-iters", type=int, default=160)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--strict", action="store_true", help="bit-exact strict mode")
     ap.add_argument("--shard", action="store_true",
@@ -134,24 +134,35 @@ def workload_desc(args, p):
                          "(>= 250 MB) through the 126 MB L2"}
 
 
-def reference_sample(p, iters, seed_cfg):
-    """Reference CPU solver (oracle/_ref): setup-only run, then a bounded run."""
+def reference_solver():
     import oracle
-    import paper_2311_07710_b200 as rb
 
     oracle.build()
-    O = oracle.ref() if oracle.have_ref() else oracle.port()
-    kind = "reference" if oracle.have_ref() else "port"
-    cfg0 = rb.SolverConfig(tol=seed_cfg, max_iters=0)
+    if oracle.have_ref():
+        return oracle.ref(), "reference"
+    return oracle.port(), "port"
+
+
+def reference_setup_seconds(O, p, reps=2):
+    """Median wall time of the reference's solve() with max_iters = 0: its
+    setup (validate, scaling, norms, first candidate; solver.hpp:277-341)."""
+    import paper_2311_07710_b200 as rb
+
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        O.solve(p, rb.SolverConfig(max_iters=0))
+        ts.append(time.perf_counter() - t0)
+    return float(np.median(ts))
+
+
+def reference_sample(O, p, iters, setup):
+    """One bounded reference solve; loop time = wall - setup (median)."""
+    import paper_2311_07710_b200 as rb
+
     t0 = time.perf_counter()
-    O.solve(p, cfg0)
-    setup = time.perf_counter() - t0
-    cfg = rb.SolverConfig(tol=1e-12, max_iters=iters)
-    t0 = time.perf_counter()
-    r = O.solve(p, cfg)
-    total = time.perf_counter() - t0
-    loop = max(total - setup, 1e-9)
-    return r.iterations, loop, setup, kind
+    r = O.solve(p, rb.SolverConfig(tol=1e-12, max_iters=iters))
+    return r.iterations, max(time.perf_counter() - t0 - setup, 1e-9)
 
 
 def run_reference_arm(args, rank, world):
@@ -159,16 +170,16 @@ def run_reference_arm(args, rank, world):
         return
     p, _ = make_instance(args)
     desc = workload_desc(args, p)
-    for _ in range(args.warmup):
-        reference_sample(p, args.ref_iters, args.tol)
-    its = loop = setup = 0.0
-    kind = "reference"
+    O, kind = reference_solver()
+    setup = reference_setup_seconds(O, p)
+    for _ in range(min(args.warmup, 1)):  # CPU: one warm-up sample is enough
+        reference_sample(O, p, args.ref_iters, setup)
+    its = loop = 0.0
     t_wall = time.perf_counter()
     for _ in range(args.steps):
-        i, l_, s_, kind = reference_sample(p, args.ref_iters, args.tol)
+        i, l_ = reference_sample(O, p, args.ref_iters, setup)
         its += i
         loop += l_
-        setup += s_
     wall = time.perf_counter() - t_wall
     v = its / loop
     line = {
@@ -177,8 +188,8 @@ def run_reference_arm(args, rank, world):
         "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": desc,
         "cpu_baseline": {"value": v, "unit": "iter/s", "cores": 1, "kind": kind,
-                         "sample": f"{args.ref_iters} iterations per step after a setup-only run "
-                                   f"(setup {setup / args.steps:.2f} s subtracted), single thread"},
+                         "sample": f"C2, {args.ref_iters} iterations per step, the reference's setup "
+                                   f"({setup:.2f} s, median of 2 setup-only solves) subtracted, single thread"},
         "e2e": {"value": v, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -366,10 +377,13 @@ def main():
         "generator_s": gen_s,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        i, l_, s_, kind = reference_sample(p, args.ref_iters, args.tol)
+        O, kind = reference_solver()
+        s_ = reference_setup_seconds(O, p)
+        i, l_ = reference_sample(O, p, args.ref_iters, s_)
         line["cpu_baseline"] = {"value": i / l_, "unit": "iter/s", "cores": 1, "kind": kind,
-                                "sample": f"C2, {i} iterations after a setup-only run (setup {s_:.2f} s "
-                                          f"subtracted), single thread"}
+                                "setup_s": s_,
+                                "sample": f"C2, {i} iterations, the reference's setup ({s_:.2f} s, median of "
+                                          f"2 setup-only solves) subtracted, single thread"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:

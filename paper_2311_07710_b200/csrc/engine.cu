@@ -1,6 +1,7 @@
 // engine.cu — setup numerics and the iteration loop of the B200 rAPDHG solver.
 // See engine.hpp. Reference: /root/reference/proj/include/rapdhg/solver.hpp.
 #include <algorithm>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -407,10 +408,76 @@ Engine::Engine(const rapdhg_qp& p, const rapdhg_config& cfg, Clock::time_point t
   }
   RB_CUDA(cudaStreamSynchronize(st_));
   tr.mark("omega init + buffers");
+  if (!P_->strict) setup_slabs();
+  tr.mark("slab plans");
   setup_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
 }
 
+// Slab-staged gathers for the dual (rows of A gather w) and the primal (A' part
+// of [Q | A'] gathers y); slab.cuh. Rows outside a plan keep the regular kernel
+// through a complement schedule.
+#ifdef RB_SLAB_PROFILE
+namespace {
+// RB_SLAB_PROFILE builds: per-CTA phase times of the last slab launch, to stderr.
+void dump_slab_profile(const char* name, const SlabView& v) {
+  if (!v.prof) return;
+  std::vector<unsigned long long> h(static_cast<std::size_t>(v.grid) * kSlabProf);
+  RB_CUDA(cudaMemcpy(h.data(), v.prof, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost));
+  unsigned long long t0 = ~0ull, t1 = 0;
+  for (int b = 0; b < v.grid; ++b) t0 = std::min(t0, h[b * kSlabProf]), t1 = std::max(t1, h[b * kSlabProf + 6]);
+  std::vector<int> order(v.grid);
+  for (int b = 0; b < v.grid; ++b) order[b] = b;
+  std::sort(order.begin(), order.end(), [&](int a, int b) { return h[a * kSlabProf + 6] > h[b * kSlabProf + 6]; });
+  std::fprintf(stderr, "[slab %s] grid %d tiles %d span %.1f us\n", name, v.grid, v.tiles(), (t1 - t0) / 1e3);
+  auto row = [&](int b) {
+    const unsigned long long* p = &h[b * kSlabProf];
+    std::fprintf(stderr, "  cta %3d start %6.1f wait %6.1f compute %6.1f end %6.1f tiles %llu\n", b, (p[0] - t0) / 1e3,
+                 p[2] / 1e3, p[3] / 1e3, (p[6] - t0) / 1e3, p[7]);
+  };
+  for (int q = 0; q < 6 && q < v.grid; ++q) row(order[q]);
+  std::fprintf(stderr, "  ...\n");
+  for (int q = std::max(0, v.grid - 3); q < v.grid; ++q) row(order[q]);
+}
+}  // namespace
+#endif
+
+void Engine::setup_slabs() {
+  DeviceQP& P = *P_;
+  DevBuf<int32_t> len;
+  dual_choice_ = choose_slabs(P.A.rp.get(), P.A.ci.get(), P.A.rows, P.A.nnz, n_, st_);
+  row_lengths(len, P.A.rp.get(), nullptr, m_, st_);
+  build_slab_phase(dual_ph_, dual_choice_, 0, P.A.rp.get(), P.A.ci.get(), nullptr, nullptr, 0, m_, len.get(), st_);
+  if (dual_ph_.active()) {
+    fill_slab_values(dual_ph_.plan, asv_, nullptr, st_);
+    assign_slab_ctas(dual_ph_.plan, prepare_slab<DualStepOp<false>>(dual_ph_.plan.view.smem_bytes()), st_);
+  }
+  primal_choice_ = choose_slabs(P.AT.rp.get(), P.AT.ci.get(), n_, P.AT.nnz, m_, st_);
+  row_lengths(len, P.Q.rp.get(), P.AT.rp.get(), n_, st_);
+  build_slab_phase(primal_ph_, primal_choice_, 1, P.Q.rp.get(), P.Q.ci.get(), P.AT.rp.get(), P.AT.ci.get(), 0, n_,
+                   len.get(), st_);
+  if (primal_ph_.active()) {
+    fill_slab_values(primal_ph_.plan, qsv_, atsv_, st_);
+    assign_slab_ctas(primal_ph_.plan, prepare_slab<PrimalStepOp<false>>(primal_ph_.plan.view.smem_bytes()), st_);
+  }
+#ifdef RB_SLAB_PROFILE
+  for (SlabPlan* pl : {&dual_ph_.plan, &primal_ph_.plan})
+    if (pl->view.active()) {
+      pl->prof.alloc(static_cast<std::size_t>(pl->view.grid) * kSlabProf);
+      pl->prof.zero(st_);
+      pl->view.prof = pl->prof.get();
+    }
+#endif
+  RB_CUDA(cudaStreamSynchronize(st_));
+}
+
 Engine::~Engine() {
+#ifdef RB_SLAB_PROFILE
+  try {
+    dump_slab_profile("dual", dual_ph_.plan.view);
+    dump_slab_profile("primal", primal_ph_.plan.view);
+  } catch (...) {
+  }
+#endif
   for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
   for (auto& e : events_) cudaEventDestroy(e);
   P_.reset();
@@ -445,7 +512,11 @@ void Engine::launch_chunk_body(int len, int cur, bool prof) {
       rowwise(d, P_->sch_dual, st_, &launches_);
     } else {
       DualStepOp<false> d{P_->A.view(asv_), w_.get(), bsv_, y_.get(), yb_.get(), mi_, params_.get(), it, bad_.get()};
-      rowwise(d, P_->sch_dual, st_, &launches_);
+      if (dual_ph_.active()) {
+        launches_ += launch_slab_phase(d, dual_ph_, st_);
+      } else {
+        rowwise(d, P_->sch_dual, st_, &launches_);
+      }
     }
     if (prof) RB_CUDA(cudaEventRecordWithFlags(events_[2 * it + 1], st_, cudaEventRecordExternal));
     if (P_->strict) {
@@ -455,7 +526,11 @@ void Engine::launch_chunk_body(int len, int cur, bool prof) {
     } else {
       PrimalStepOp<false> pr{P_->Q.view(qsv_), P_->AT.view(atsv_), XMD_[c].get(), y_.get(), X_[c].get(),
                              X_[c ^ 1].get(), xb_.get(), csv_, w_.get(), XMD_[c ^ 1].get(), params_.get(), it, bad_.get()};
-      rowwise(pr, P_->sch_primal, st_, &launches_);
+      if (primal_ph_.active()) {
+        launches_ += launch_slab_phase(pr, primal_ph_, st_);
+      } else {
+        rowwise(pr, P_->sch_primal, st_, &launches_);
+      }
     }
     if (prof) RB_CUDA(cudaEventRecordWithFlags(events_[2 * it + 2], st_, cudaEventRecordExternal));
   }
@@ -475,6 +550,7 @@ void Engine::run_chunk(int len) {
       RB_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
       launch_chunk_body(len, cur_, prof);
       RB_CUDA(cudaStreamEndCapture(st_, &g));
+      graph_launches_[key] = launches_ - before;  // kernel nodes of this graph
       launches_ = before;  // counted at replay below
       cudaGraphExec_t ge;
       RB_CUDA(cudaGraphInstantiate(&ge, g, 0));
@@ -482,10 +558,7 @@ void Engine::run_chunk(int len) {
       it = graphs_.emplace(key, ge).first;
     }
     RB_CUDA(cudaGraphLaunch(it->second, st_));
-    // prologue + one dual and one primal kernel per iteration (bins never empty
-    // for n, m > 0; counted as launched kernels)
-    launches_ += 1 + (P_->sch_dual.view.total_blocks > 0 ? len : 0) +
-                 (P_->sch_primal.view.total_blocks > 0 ? len : 0);
+    launches_ += graph_launches_[key];
   } else {
     launch_chunk_body(len, cur_, prof);
   }

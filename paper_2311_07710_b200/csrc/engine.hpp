@@ -18,6 +18,7 @@
 #include "ops.cuh"
 #include "reduce.cuh"
 #include "rowwise.cuh"
+#include "slab.cuh"
 
 namespace rb {
 
@@ -185,7 +186,12 @@ class Engine : public LoopBackend {
   PinnedBuf<IterParams> params_h_;
   DevBuf<long long> bad_;
   PinnedBuf<long long> bad_h_;
+  // slab-staged gathers (fast mode, slab.cuh): plans + the complement schedules
+  void setup_slabs();
+  SlabChoice dual_choice_, primal_choice_;
+  SlabPhase dual_ph_, primal_ph_;
   std::map<int, cudaGraphExec_t> graphs_;  // key: len, parity, profiled
+  std::map<int, int64_t> graph_launches_;
   int64_t chunk_counter_ = 0;
   std::vector<cudaEvent_t> events_;
   double kernel_ms_[2] = {0, 0};

@@ -72,6 +72,12 @@ struct DualStepOp {
     acc.v[0] = seg_dot<Strict, U>(a.v, a.ci, g[0], a.rp[r], lo + lane, hi, stride, acc.v[0]);
   }
   __device__ __forceinline__ const double* gather_src(int) const { return w; }
+  // same op over other CSR arrays (the rest CSR of a slab plan)
+  DualStepOp with_views(CsrView s1, CsrView) const {
+    DualStepOp o = *this;
+    o.a = s1;
+    return o;
+  }
   __device__ __forceinline__ void finish(int i, const AccT& acc) const {
     const IterParams& q = P[it];
     double yi = y[i];
@@ -124,6 +130,12 @@ struct PrimalStepOp {
                                acc.v[1]);
   }
   __device__ __forceinline__ const double* gather_src(int slot) const { return slot ? y : xmd; }
+  PrimalStepOp with_views(CsrView s1, CsrView s2) const {
+    PrimalStepOp o = *this;
+    o.q = s1;
+    o.at = s2;
+    return o;
+  }
   __device__ __forceinline__ void finish(int j, const AccT& acc) const {
     const IterParams& p = P[it];
     const double xo = x_in[j];

@@ -309,6 +309,30 @@ __device__ __forceinline__ void run_split(const Op& op, const SchedView& s, cons
   }
 }
 
+// One tile of a schedule (all kBlock threads of the CTA take part).
+template <class Op>
+__device__ __forceinline__ void rowwise_tile(const Op& op, const SchedView& s, int tile, const Gather* g) {
+  int bin = 0;  // bins occupy disjoint tile ranges (heavy bins first, see schedule.cu)
+#pragma unroll
+  for (int b = 1; b < kNumBins; ++b)
+    if (tile >= s.bins[b].blk_begin && tile < s.bins[b].blk_end) bin = b;
+  const BinDesc bd = s.bins[bin];
+  if constexpr (Op::kStrict) {
+    run_vlane<Op, 1>(op, s, bd, tile, g);  // strict schedules hold a single V=1 bin
+  } else {
+    switch (bin) {
+      case 0: run_vlane<Op, 1>(op, s, bd, tile, g); break;
+      case 1: run_vlane<Op, 2>(op, s, bd, tile, g); break;
+      case 2: run_vlane<Op, 4>(op, s, bd, tile, g); break;
+      case 3: run_vlane<Op, 8>(op, s, bd, tile, g); break;
+      case 4: run_vlane<Op, 16>(op, s, bd, tile, g); break;
+      case 5: run_vlane<Op, 32>(op, s, bd, tile, g); break;
+      case 6: run_block_row<Op>(op, s, bd, tile, g); break;
+      default: run_split<Op>(op, s, bd, tile, g); break;
+    }
+  }
+}
+
 template <class Op, bool Win>
 __global__ void __launch_bounds__(kBlock) rowwise_kernel(const Op op, const SchedView s) {
   extern __shared__ double win_smem[];
@@ -326,27 +350,7 @@ __global__ void __launch_bounds__(kBlock) rowwise_kernel(const Op op, const Sche
     }
   }
   if (Win) __syncthreads();
-  for (int tile = blockIdx.x; tile < s.total_blocks; tile += gridDim.x) {
-    int bin = 0;  // bins occupy disjoint tile ranges (heavy bins first, see schedule.cu)
-#pragma unroll
-    for (int b = 1; b < kNumBins; ++b)
-      if (tile >= s.bins[b].blk_begin && tile < s.bins[b].blk_end) bin = b;
-    const BinDesc bd = s.bins[bin];
-    if constexpr (Op::kStrict) {
-      run_vlane<Op, 1>(op, s, bd, tile, g);  // strict schedules hold a single V=1 bin
-    } else {
-      switch (bin) {
-        case 0: run_vlane<Op, 1>(op, s, bd, tile, g); break;
-        case 1: run_vlane<Op, 2>(op, s, bd, tile, g); break;
-        case 2: run_vlane<Op, 4>(op, s, bd, tile, g); break;
-        case 3: run_vlane<Op, 8>(op, s, bd, tile, g); break;
-        case 4: run_vlane<Op, 16>(op, s, bd, tile, g); break;
-        case 5: run_vlane<Op, 32>(op, s, bd, tile, g); break;
-        case 6: run_block_row<Op>(op, s, bd, tile, g); break;
-        default: run_split<Op>(op, s, bd, tile, g); break;
-      }
-    }
-  }
+  for (int tile = blockIdx.x; tile < s.total_blocks; tile += gridDim.x) rowwise_tile(op, s, tile, g);
 }
 
 // Resident CTAs per SM for a kernel instance at a dynamic smem size (cached).
@@ -412,7 +416,9 @@ constexpr int kWinMax = 12288;  // doubles (96 KB): 2 CTAs/SM
 void choose_windows(Schedule& sch, const int32_t* cols1, int64_t nnz1, int32_t ncols1,
                     const int32_t* cols2, int64_t nnz2, int32_t ncols2, cudaStream_t st);
 
+// d_subset (optional, fast mode): schedule only these row ids (rows = their
+// count); d_len is indexed by row id.
 void build_schedule(Schedule& sch, const int32_t* d_len, int64_t rows, bool strict,
-                    cudaStream_t st);
+                    cudaStream_t st, const int32_t* d_subset = nullptr);
 
 }  // namespace rb

@@ -19,13 +19,14 @@ namespace rb {
 
 namespace {
 
-__global__ void bin_kernel(int32_t* bin, int32_t* idx, const int32_t* len, int64_t rows,
-                           int* counts, int epl, int block_min) {
-  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (r >= rows) return;
+__global__ void bin_kernel(int32_t* bin, int32_t* idx, const int32_t* len, const int32_t* subset,
+                           int64_t rows, int* counts, int epl, int block_min) {
+  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (k >= rows) return;
+  const int32_t r = subset ? subset[k] : static_cast<int32_t>(k);
   const int b = bin_of_len(len[r], epl, block_min);
-  bin[r] = b;
-  idx[r] = static_cast<int32_t>(r);
+  bin[k] = b;
+  idx[k] = r;
   atomicAdd(&counts[b], 1);  // integer counts: exact
 }
 
@@ -125,7 +126,8 @@ SchedParams SchedParams::from_env() {
 }
 
 void build_schedule(Schedule& sch, const int32_t* d_len, int64_t rows, bool strict,
-                    cudaStream_t st) {
+                    cudaStream_t st, const int32_t* d_subset) {
+  if (strict && d_subset) invalid("strict schedules cover all rows");
   sch.rows = rows;
   SchedView& v = sch.view;
   v = SchedView{};
@@ -147,7 +149,7 @@ void build_schedule(Schedule& sch, const int32_t* d_len, int64_t rows, bool stri
   sch.perm.alloc(rows);
   if (rows) {
     bin_kernel<<<static_cast<unsigned>(ceil_div(rows, 256)), 256, 0, st>>>(
-        bins.get(), idx.get(), d_len, rows, counts.get(), sp.epl, sp.block_min);
+        bins.get(), idx.get(), d_len, d_subset, rows, counts.get(), sp.epl, sp.block_min);
     RB_LAUNCH_CHECK();
     std::size_t tb = 0;
     RB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, bins.get(), bins_sorted.get(), idx.get(),

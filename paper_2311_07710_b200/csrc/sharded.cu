@@ -194,6 +194,9 @@ struct ShardedEngine::Shard {
   int id = 0;
   int64_t d0 = 0, d1 = 0, p0 = 0, p1 = 0;  // dual / primal row blocks
   Schedule sch_dual, sch_primal;
+  // slab plans restricted to the owned rows, built from the GLOBAL window
+  // choice so every row is computed as on one GPU; + complement schedules
+  SlabPhase dual_ph, primal_ph;
   // full-length copies; only the owned slice is computed here, the rest is
   // received by the exchanges
   DevBuf<double> X[2], XMD[2], w, xb, y, yb, epx, epy, xu[2], yu[2], ax[2], qx[2], aty[2], best_x, best_y;
@@ -222,8 +225,24 @@ ShardedEngine::ShardedEngine(const rapdhg_qp& p, const rapdhg_config& cfg, int p
     DevBuf<int32_t> len;
     row_lengths(len, P.A.rp.get() + sh->d0, nullptr, sh->d1 - sh->d0, st_);
     build_schedule(sh->sch_dual, len.get(), sh->d1 - sh->d0, false, st_);
+    if (!full_->dual_choice_.empty() && sh->d1 > sh->d0) {
+      build_slab_phase(sh->dual_ph, full_->dual_choice_, 0, P.A.rp.get(), P.A.ci.get(), nullptr, nullptr,
+                       static_cast<int32_t>(sh->d0), static_cast<int32_t>(sh->d1), len.get(), st_);
+      if (sh->dual_ph.active()) {
+        fill_slab_values(sh->dual_ph.plan, full_->asv_, nullptr, st_);
+        assign_slab_ctas(sh->dual_ph.plan, prepare_slab<DualStepOp<false>>(sh->dual_ph.plan.view.smem_bytes()), st_);
+      }
+    }
     row_lengths(len, P.Q.rp.get() + sh->p0, P.AT.rp.get() + sh->p0, sh->p1 - sh->p0, st_);
     build_schedule(sh->sch_primal, len.get(), sh->p1 - sh->p0, false, st_);
+    if (!full_->primal_choice_.empty() && sh->p1 > sh->p0) {
+      build_slab_phase(sh->primal_ph, full_->primal_choice_, 1, P.Q.rp.get(), P.Q.ci.get(), P.AT.rp.get(),
+                       P.AT.ci.get(), static_cast<int32_t>(sh->p0), static_cast<int32_t>(sh->p1), len.get(), st_);
+      if (sh->primal_ph.active()) {
+        fill_slab_values(sh->primal_ph.plan, full_->qsv_, full_->atsv_, st_);
+        assign_slab_ctas(sh->primal_ph.plan, prepare_slab<PrimalStepOp<false>>(sh->primal_ph.plan.view.smem_bytes()), st_);
+      }
+    }
     for (int i = 0; i < 2; ++i) {
       sh->X[i].alloc(n), sh->XMD[i].alloc(n), sh->xu[i].alloc(n), sh->yu[i].alloc(m);
       sh->ax[i].alloc(m), sh->qx[i].alloc(n), sh->aty[i].alloc(n);
@@ -326,8 +345,12 @@ void ShardedEngine::body(int len, int cur) {
       DualStepOp<false> d{CsrView{P.A.rp.get() + sh->d0, P.A.ci.get(), e.asv_}, sh->w.get(), e.bsv_ + sh->d0,
                           sh->y.get() + sh->d0, sh->yb.get() + sh->d0, e.mi_ - static_cast<int>(sh->d0),
                           params_.get(), it, sh->bad.get()};
-      launch_rowwise(d, sh->sch_dual.view, st_);
-      ++launches_;
+      if (sh->dual_ph.active()) {
+        launches_ += launch_slab_phase(d, sh->dual_ph, st_);
+      } else {
+        launch_rowwise(d, sh->sch_dual.view, st_);
+        ++launches_;
+      }
     }
     exchange([](Shard& s) { return s.y.get(); }, false);
     for (auto& sh : shards_) {
@@ -338,8 +361,12 @@ void ShardedEngine::body(int len, int cur) {
                              sh->XMD[c].get(), sh->y.get(), sh->X[c].get() + o, sh->X[c ^ 1].get() + o,
                              sh->xb.get() + o, e.csv_ + o, sh->w.get() + o, sh->XMD[c ^ 1].get() + o,
                              params_.get(), it, sh->bad.get()};
-      launch_rowwise(pr, sh->sch_primal.view, st_);
-      ++launches_;
+      if (sh->primal_ph.active()) {
+        launches_ += launch_slab_phase(pr, sh->primal_ph, st_);
+      } else {
+        launch_rowwise(pr, sh->sch_primal.view, st_);
+        ++launches_;
+      }
     }
     if (it + 1 < len) {  // the next step gathers the new w and x_md
       exchange([](Shard& s) { return s.w.get(); }, true);

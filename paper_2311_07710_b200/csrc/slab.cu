@@ -1,0 +1,441 @@
+// slab.cu — setup of the slab tile plans (see slab.cuh).
+#include <algorithm>
+#include <climits>
+#include <cstdio>
+#include <cstdlib>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "slab.cuh"
+
+namespace rb {
+
+namespace {
+
+__global__ void hist_kernel(const int32_t* ci, int64_t nnz, int width, int* hist) {
+  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (k < nnz) atomicAdd(&hist[ci[k] / width], 1);  // integer counts: exact
+}
+
+__device__ __forceinline__ int lower_pos(const int32_t* ci, int b, int e, int32_t key) {
+  while (b < e) {  // first position in [b, e) with ci >= key (rows are column-sorted)
+    const int mid = (b + e) >> 1;
+    if (ci[mid] < key) b = mid + 1;
+    else e = mid;
+  }
+  return b;
+}
+
+struct Wins {
+  Window w[kMaxSlabs];
+  int S;
+};
+
+// in-window entries of row r, per window (per may be null, stride apart) and
+// in total; *maxrun = the longest per-window run
+__device__ __forceinline__ int in_window_count(const int32_t* rp, const int32_t* ci, int r, const Wins& wins,
+                                               int* per, int64_t stride, int* maxrun = nullptr) {
+  const int b = rp[r], e = rp[r + 1];
+  int tot = 0, lo = b, mx = 0;
+  for (int s = 0; s < wins.S; ++s) {
+    lo = lower_pos(ci, lo, e, wins.w[s].lo);
+    const int hi = lower_pos(ci, lo, e, wins.w[s].lo + wins.w[s].len);
+    if (per) per[s * stride] = hi - lo;
+    tot += hi - lo;
+    mx = max(mx, hi - lo);
+    lo = hi;
+  }
+  if (maxrun) *maxrun = mx;
+  return tot;
+}
+
+// Rows [r0, r1): in-window entry count, or 0 when a window run or the rest
+// (other entries of both segments) exceeds cap — such rows stay on the
+// regular schedule, whose block/split bins spread long rows over a CTA.
+__global__ void count_kernel(const int32_t* rp, const int32_t* ci, const int32_t* rp_o, int32_t r0, int32_t r1,
+                             Wins wins, int cap, int32_t* cnt) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= r1 - r0) return;
+  const int r = r0 + static_cast<int>(i);
+  int mx = 0;
+  const int tot = in_window_count(rp, ci, r, wins, nullptr, 0, &mx);
+  const int rest = (rp[r + 1] - rp[r]) - tot + (rp_o ? rp_o[r + 1] - rp_o[r] : 0);
+  cnt[i] = (mx <= cap && rest <= cap) ? tot : 0;
+}
+
+// per-(window, W row) counts (window-major, cnt[s * nw + k]) and rest counts
+__global__ void seg_counts_kernel(const int32_t* rows, int32_t nw, const int32_t* rp_w, const int32_t* ci_w,
+                                  const int32_t* rp_o, Wins wins, int32_t* cnt, int32_t* rest_w, int32_t* rest_o) {
+  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (k >= nw) return;
+  const int r = rows[k];
+  const int tot = in_window_count(rp_w, ci_w, r, wins, cnt + k, nw);
+  rest_w[k] = (rp_w[r + 1] - rp_w[r]) - tot;
+  rest_o[k] = rp_o ? rp_o[r + 1] - rp_o[r] : 0;
+}
+
+// thread per W row: scatter its entries into its slice lanes (run (s, k)
+// starts at off[s * nw + k], entries 32 apart) and into the rest CSRs
+__global__ void fill_kernel(const int32_t* rows, int32_t nw, const int32_t* rp_w, const int32_t* ci_w,
+                            const int32_t* rp_o, const int32_t* ci_o, Wins wins, const int32_t* off,
+                            uint16_t* col, int32_t* pos, const int32_t* rrp_w, int32_t* rci_w, int32_t* rpos_w,
+                            const int32_t* rrp_o, int32_t* rci_o, int32_t* rpos_o) {
+  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (k >= nw) return;
+  const int r = rows[k];
+  int s = 0;
+  int64_t wp = wins.S > 0 ? off[k] : 0;
+  int rw = rrp_w[k];
+  for (int p = rp_w[r]; p < rp_w[r + 1]; ++p) {
+    const int32_t c = ci_w[p];
+    while (s < wins.S && c >= wins.w[s].lo + wins.w[s].len) {
+      ++s;
+      if (s < wins.S) wp = off[static_cast<int64_t>(s) * nw + k];
+    }
+    if (s < wins.S && c >= wins.w[s].lo) {
+      col[wp] = static_cast<uint16_t>(c - wins.w[s].lo);
+      pos[wp] = p;
+      wp += 32;
+    } else {
+      rci_w[rw] = c;
+      rpos_w[rw] = p;
+      ++rw;
+    }
+  }
+  if (rp_o) {
+    int ro = rrp_o[k];
+    for (int p = rp_o[r]; p < rp_o[r + 1]; ++p, ++ro) {
+      rci_o[ro] = ci_o[p];
+      rpos_o[ro] = p;
+    }
+  }
+}
+
+__global__ void gather_kernel(double* dst, const double* src, const int32_t* pos, int64_t n) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) dst[i] = pos[i] >= 0 ? src[pos[i]] : 0.0;
+}
+
+__global__ void finish_len_kernel(const int32_t* widx, const int32_t* rrp1, const int32_t* rrp2, int S,
+                                  const int32_t* len, int32_t nr, int32_t* out) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= nr) return;
+  const int w = widx[i];
+  out[i] = w < 0 ? len[i] : (rrp1[w + 1] - rrp1[w]) + (rrp2[w + 1] - rrp2[w]) + S;
+}
+
+inline unsigned g1(int64_t n) { return static_cast<unsigned>(ceil_div(n > 0 ? n : 1, 256)); }
+
+std::string slab_mode() {
+  const char* e = std::getenv("RAPDHG_SLAB");
+  return e ? e : "auto";
+}
+int slab_min_row() { return slab_mode() == "force" ? 1 : kSlabMinRow; }
+
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+
+template <class T>
+std::vector<T> download(const DevBuf<T>& d, int64_t n, cudaStream_t st) {
+  std::vector<T> h(static_cast<std::size_t>(n));
+  if (n > 0) RB_CUDA(cudaMemcpyAsync(h.data(), d.get(), sizeof(T) * n, cudaMemcpyDeviceToHost, st));
+  RB_CUDA(cudaStreamSynchronize(st));
+  return h;
+}
+
+std::vector<int32_t> scan_host(const std::vector<int32_t>& cnt) {
+  std::vector<int32_t> rp(cnt.size() + 1, 0);
+  for (std::size_t i = 0; i < cnt.size(); ++i) rp[i + 1] = rp[i] + cnt[i];
+  return rp;
+}
+
+// Sliced layout of one tile: rows [k0, k1) sorted by run length (descending,
+// stable), 32 per slice, each slice as wide as its longest run.
+struct TileLayout {
+  std::vector<int32_t> order;  // sorted rows (chunk-relative)
+  std::vector<int32_t> soff;   // slice starts (entries), nsl + 1
+};
+TileLayout layout_tile(const std::vector<int32_t>& c2, int64_t s_base, int32_t k0, int32_t k1) {
+  TileLayout L;
+  const int32_t nr = k1 - k0;
+  L.order.resize(nr);
+  std::iota(L.order.begin(), L.order.end(), 0);
+  std::stable_sort(L.order.begin(), L.order.end(),
+                   [&](int32_t a, int32_t b) { return c2[s_base + k0 + a] > c2[s_base + k0 + b]; });
+  const int nsl = (nr + 31) / 32;
+  L.soff.assign(nsl + 1, 0);
+  for (int q = 0; q < nsl; ++q) L.soff[q + 1] = L.soff[q] + 32 * c2[s_base + k0 + L.order[32 * q]];
+  return L;
+}
+
+}  // namespace
+
+int slab_grid(const void* kernel, int smem_bytes) {
+  int per_sm = 0;
+  RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kSlabThreads, smem_bytes));
+  return std::max(1, per_sm) * kSMs;
+}
+
+SlabChoice choose_slabs(const int32_t* rp, const int32_t* ci, int32_t rows, int64_t nnz, int32_t ncols,
+                        cudaStream_t st) {
+  (void)rp;
+  SlabChoice ch;
+  const std::string mode = slab_mode();
+  if (mode == "off" || nnz <= 0 || ncols <= 0 || rows <= 0) return ch;
+  // RAPDHG_SLAB_WIDTH: window width in columns (tuning; 16-bit offsets)
+  const int width = std::min(std::max(env_int("RAPDHG_SLAB_WIDTH", kSlabWidth), 128), 65536);
+  const int nb = static_cast<int>(ceil_div(ncols, width));
+  DevBuf<int> hist(nb);
+  hist.zero(st);
+  hist_kernel<<<g1(nnz), 256, 0, st>>>(ci, nnz, width, hist.get());
+  RB_LAUNCH_CHECK();
+  const std::vector<int> h = download(hist, nb, st);
+  // aligned windows, densest first, kept while they serve enough gathers per
+  // column to repay staging (force: any non-empty window)
+  const double min_density = mode == "force" ? 1e-9 : kSlabMinDensity;
+  // RAPDHG_SLAB_MIN_WINDOWS: below this many windows the gathered range is
+  // small enough for L1 to serve it (the regular kernel is as fast)
+  std::vector<int> order(nb);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return h[a] > h[b]; });
+  for (int b : order) {
+    if (static_cast<int>(ch.windows.size()) == kMaxSlabs) break;
+    const int32_t lo = b * width, len = std::min(width, ncols - lo) & ~1;  // even: 16 B bulk copies
+    if (len == 0 || h[b] == 0) continue;
+    if (h[b] < min_density * len) break;
+    ch.windows.push_back(Window{lo, len});
+  }
+  std::sort(ch.windows.begin(), ch.windows.end(), [](const Window& a, const Window& b) { return a.lo < b.lo; });
+  const int min_windows = mode == "force" ? 1 : env_int("RAPDHG_SLAB_MIN_WINDOWS", kSlabMinWindows);
+  if (static_cast<int>(ch.windows.size()) < min_windows) ch.windows.clear();
+  return ch;
+}
+
+void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const int32_t* rp1, const int32_t* ci1,
+                     const int32_t* rp2, const int32_t* ci2, int32_t r0, int32_t r1, cudaStream_t st) {
+  plan = SlabPlan{};
+  const int S = static_cast<int>(choice.windows.size());
+  if (S == 0 || r1 <= r0) return;
+  Wins wins{};
+  wins.S = S;
+  for (int s = 0; s < S; ++s) wins.w[s] = choice.windows[s];
+  const int32_t* rp_w = seg == 0 ? rp1 : rp2;  // windowed segment
+  const int32_t* ci_w = seg == 0 ? ci1 : ci2;
+  const int32_t* rp_o = seg == 0 ? rp2 : rp1;  // the other segment (rest only)
+  const int32_t* ci_o = seg == 0 ? ci2 : ci1;
+  const int32_t nr = r1 - r0;
+  std::vector<int32_t> hc;
+  {
+    DevBuf<int32_t> cnt(nr);
+    count_kernel<<<g1(nr), 256, 0, st>>>(rp_w, ci_w, rp_o, r0, r1, wins, kSlabRunCap, cnt.get());
+    RB_LAUNCH_CHECK();
+    hc = download(cnt, nr, st);
+  }
+  std::vector<int32_t> rows;
+  const int min_row = slab_min_row();
+  for (int32_t i = 0; i < nr; ++i)
+    if (hc[i] >= min_row) rows.push_back(r0 + i);
+  const int32_t nw = static_cast<int32_t>(rows.size());
+  if (nw == 0) return;
+  plan.rows.alloc(nw);
+  plan.rows.upload(rows.data(), nw, st);
+  // per-(window, row) run lengths and rest counts
+  const int64_t runs = static_cast<int64_t>(nw) * S;
+  DevBuf<int32_t> c2(runs), rw(nw), ro(nw);
+  seg_counts_kernel<<<g1(nw), 256, 0, st>>>(plan.rows.get(), nw, rp_w, ci_w, rp_o, wins, c2.get(), rw.get(), ro.get());
+  RB_LAUNCH_CHECK();
+  const std::vector<int32_t> hc2 = download(c2, runs, st), hrw = download(rw, nw, st), hro = download(ro, nw, st);
+  // Row chunks: greedy on entries (3/4 of the capacity, leaving room for the
+  // slice padding) and rows; chunks whose padded tiles still overflow are
+  // halved; then split further until there are enough tiles for every CTA.
+  const int ecap = (std::min(32736, std::max(256, env_int("RAPDHG_SLAB_TILE", kSlabTileCap))) + 31) & ~31;
+  const int rcap = kSlabRowCap;
+  std::vector<int32_t> chunk{0};
+  {
+    std::vector<int64_t> cur(S, 0);
+    for (int32_t k = 0; k < nw; ++k) {
+      bool fits = k - chunk.back() + 1 <= rcap;
+      for (int s = 0; s < S && fits; ++s) fits = cur[s] + hc2[static_cast<int64_t>(s) * nw + k] <= ecap * 3 / 4;
+      if (!fits && k > chunk.back()) {
+        chunk.push_back(k);
+        std::fill(cur.begin(), cur.end(), 0);
+      }
+      for (int s = 0; s < S; ++s) cur[s] += hc2[static_cast<int64_t>(s) * nw + k];
+    }
+    chunk.push_back(nw);
+  }
+  auto padded_ok = [&](int32_t k0, int32_t k1) {
+    for (int s = 0; s < S; ++s)
+      if (layout_tile(hc2, static_cast<int64_t>(s) * nw, k0, k1).soff.back() > ecap) return false;
+    return true;
+  };
+  for (std::size_t c = 0; c + 1 < chunk.size();) {
+    if (chunk[c + 1] - chunk[c] > 1 && !padded_ok(chunk[c], chunk[c + 1]))
+      chunk.insert(chunk.begin() + c + 1, (chunk[c] + chunk[c + 1]) / 2);
+    else
+      ++c;
+  }
+  {
+    const int64_t want = ceil_div(static_cast<int64_t>(4 * kSMs), S);
+    while (static_cast<int64_t>(chunk.size()) - 1 < want) {  // halve the widest chunk
+      std::size_t best = 0;
+      for (std::size_t c = 1; c + 1 < chunk.size(); ++c)
+        if (chunk[c + 1] - chunk[c] > chunk[best + 1] - chunk[best]) best = c;
+      if (chunk[best + 1] - chunk[best] < 64) break;
+      chunk.insert(chunk.begin() + best + 1, (chunk[best] + chunk[best + 1]) / 2);
+    }
+  }
+  const int32_t J = static_cast<int32_t>(chunk.size()) - 1;
+  // Tiles: window-major storage, each tile 32-entry aligned; run (s, k) starts
+  // at off[s * nw + k] (its lane in its slice), entries 32 apart.
+  std::vector<int32_t> off(runs, 0);
+  std::vector<SlabTile> tiles(static_cast<std::size_t>(S) * J);
+  std::vector<uint16_t> meta;
+  int64_t cursor = 0;
+  int max_tile = 0;
+  for (int s = 0; s < S; ++s)
+    for (int32_t j = 0; j < J; ++j) {
+      const int32_t k0 = chunk[j], k1 = chunk[j + 1], n_r = k1 - k0;
+      const TileLayout L = layout_tile(hc2, static_cast<int64_t>(s) * nw, k0, k1);
+      SlabTile& d = tiles[static_cast<std::size_t>(s) * J + j];
+      d.a = static_cast<int32_t>(cursor);
+      d.n = L.soff.back();
+      d.meta = static_cast<int32_t>(meta.size());
+      d.k0 = k0;
+      d.nr = n_r;
+      d.s = s;
+      max_tile = std::max(max_tile, d.n);
+      // staged bytes + a fixed per-tile cost (barrier round trip, descriptor)
+      plan.tile_bytes.push_back(10 * static_cast<int64_t>(d.n) + 4 * static_cast<int64_t>(n_r) + 16384);
+      for (int32_t slot = 0; slot < n_r; ++slot) {
+        const int32_t k = k0 + L.order[slot];
+        off[static_cast<int64_t>(s) * nw + k] = static_cast<int32_t>(cursor + L.soff[slot / 32] + slot % 32);
+      }
+      for (int32_t slot = 0; slot < n_r; ++slot) meta.push_back(static_cast<uint16_t>(L.order[slot]));
+      for (int32_t slot = 0; slot < n_r; ++slot)
+        meta.push_back(static_cast<uint16_t>(hc2[static_cast<int64_t>(s) * nw + k0 + L.order[slot]]));
+      for (int32_t v : L.soff) meta.push_back(static_cast<uint16_t>(v));
+      meta.resize((meta.size() + 7) & ~std::size_t{7}, 0);
+      cursor += d.n;
+    }
+  if (cursor > INT32_MAX || max_tile > ecap) {  // offsets are int32; tiles must fit a stage
+    plan = SlabPlan{};
+    return;
+  }
+  meta.resize(meta.size() + 8, 0);  // slack: a tile's metadata copy rounds up to 8
+  const int64_t total = std::max<int64_t>(cursor, 32);
+  DevBuf<int32_t> doff(runs);
+  doff.upload(off.data(), runs, st);
+  plan.tile.alloc(tiles.size());
+  plan.tile.upload(tiles.data(), tiles.size(), st);
+  plan.meta.alloc(meta.size());
+  plan.meta.upload(meta.data(), meta.size(), st);
+  plan.col.alloc(total), plan.pos.alloc(total), plan.val.alloc(total);
+  RB_CUDA(cudaMemsetAsync(plan.col.get(), 0, sizeof(uint16_t) * total, st));
+  RB_CUDA(cudaMemsetAsync(plan.pos.get(), 0xff, sizeof(int32_t) * total, st));  // padding: pos -1 -> 0.0
+  const std::vector<int32_t> rrw = scan_host(hrw), rro = scan_host(hro);
+  // rest CSRs keep the op's segment order: rest1 = segment 1, rest2 = segment 2
+  DevBuf<int32_t>& rrp_w = seg == 0 ? plan.rrp1 : plan.rrp2;
+  DevBuf<int32_t>& rci_w = seg == 0 ? plan.rci1 : plan.rci2;
+  DevBuf<int32_t>& rpos_w = seg == 0 ? plan.rpos1 : plan.rpos2;
+  DevBuf<int32_t>& rrp_o = seg == 0 ? plan.rrp2 : plan.rrp1;
+  DevBuf<int32_t>& rci_o = seg == 0 ? plan.rci2 : plan.rci1;
+  DevBuf<int32_t>& rpos_o = seg == 0 ? plan.rpos2 : plan.rpos1;
+  rrp_w.alloc(nw + 1), rrp_o.alloc(nw + 1);
+  rrp_w.upload(rrw.data(), nw + 1, st);
+  rrp_o.upload(rro.data(), nw + 1, st);
+  rci_w.alloc(rrw[nw]), rpos_w.alloc(rrw[nw]), rci_o.alloc(rro[nw]), rpos_o.alloc(rro[nw]);
+  (seg == 0 ? plan.rval1 : plan.rval2).alloc(rrw[nw]);
+  (seg == 0 ? plan.rval2 : plan.rval1).alloc(rro[nw]);
+  fill_kernel<<<g1(nw), 256, 0, st>>>(plan.rows.get(), nw, rp_w, ci_w, rp_o, ci_o, wins, doff.get(), plan.col.get(),
+                                      plan.pos.get(), rrp_w.get(), rci_w.get(), rpos_w.get(),
+                                      rp_o ? rrp_o.get() : nullptr, rci_o.get(), rpos_o.get());
+  RB_LAUNCH_CHECK();
+  plan.partial.alloc(runs);
+  {
+    std::vector<int32_t> widx(nr, -1);
+    for (int32_t k = 0; k < nw; ++k) widx[rows[k] - r0] = k;
+    plan.widx.alloc(nr);
+    plan.widx.upload(widx.data(), nr, st);
+  }
+  SlabView& v = plan.view;
+  v.nw = nw;
+  v.S = S;
+  v.J = J;
+  v.seg = seg;
+  v.ecap = ecap;
+  v.mcap = (slab_meta_len(rcap) + 7) & ~7;
+  v.win_max = 0;
+  for (int s = 0; s < S; ++s) {
+    v.win[s] = choice.windows[s];
+    v.win_max = std::max(v.win_max, choice.windows[s].len);
+  }
+  v.win_max = (v.win_max + 1) & ~1;  // keeps the value stage 16 B-aligned
+  v.tile = plan.tile.get();
+  v.meta = plan.meta.get();
+  v.col = plan.col.get();
+  v.val = plan.val.get();
+  v.partial = plan.partial.get();
+  v.widx = plan.widx.get();
+  v.rest1 = CsrView{plan.rrp1.get(), plan.rci1.get(), plan.rval1.get()};
+  v.rest2 = CsrView{plan.rrp2.get(), plan.rci2.get(), plan.rval2.get()};
+  RB_CUDA(cudaStreamSynchronize(st));
+  if (std::getenv("RAPDHG_TRACE"))
+    std::fprintf(stderr, "[slab] seg %d rows [%d,%d): W rows %d windows %d chunks %d tiles %d entries %lld (%.3f padded)\n",
+                 seg, r0, r1, nw, S, J, S * J, static_cast<long long>(cursor),
+                 static_cast<double>(cursor) / std::max<int64_t>(1, [&] {
+                   int64_t t = 0;
+                   for (int32_t c : hc2) t += c;
+                   return t;
+                 }()));
+}
+
+void fill_slab_values(SlabPlan& plan, const double* v1, const double* v2, cudaStream_t st) {
+  const SlabView& v = plan.view;
+  if (!v.active()) return;
+  const double* vw = v.seg == 0 ? v1 : v2;
+  const int64_t n = plan.val.size();
+  if (n) gather_kernel<<<g1(n), 256, 0, st>>>(plan.val.get(), vw, plan.pos.get(), n);
+  if (plan.rval1.size() && v1) gather_kernel<<<g1(plan.rval1.size()), 256, 0, st>>>(plan.rval1.get(), v1, plan.rpos1.get(), plan.rval1.size());
+  if (plan.rval2.size() && v2) gather_kernel<<<g1(plan.rval2.size()), 256, 0, st>>>(plan.rval2.get(), v2, plan.rpos2.get(), plan.rval2.size());
+  RB_LAUNCH_CHECK();
+}
+
+void build_slab_phase(SlabPhase& ph, const SlabChoice& choice, int seg, const int32_t* rp1, const int32_t* ci1,
+                      const int32_t* rp2, const int32_t* ci2, int32_t r0, int32_t r1, const int32_t* len,
+                      cudaStream_t st) {
+  ph = SlabPhase{};
+  build_slab_plan(ph.plan, choice, seg, rp1, ci1, rp2, ci2, r0, r1, st);
+  if (!ph.active()) return;
+  const SlabPlan& plan = ph.plan;
+  const int32_t nr = r1 - r0;
+  DevBuf<int32_t> flen(nr);
+  finish_len_kernel<<<g1(nr), 256, 0, st>>>(plan.widx.get(), plan.rrp1.get(), plan.rrp2.get(), plan.view.S, len, nr,
+                                            flen.get());
+  RB_LAUNCH_CHECK();
+  build_schedule(ph.fin, flen.get(), nr, false, st);
+  RB_CUDA(cudaStreamSynchronize(st));
+}
+
+void assign_slab_ctas(SlabPlan& plan, int grid, cudaStream_t st) {
+  SlabView& v = plan.view;
+  const int nt = v.tiles();
+  std::vector<int64_t> pre(nt + 1, 0);
+  for (int t = 0; t < nt; ++t) pre[t + 1] = pre[t] + plan.tile_bytes[t];
+  std::vector<int32_t> cta(grid + 1, 0);
+  for (int b = 1; b <= grid; ++b) {
+    cta[b] = b == grid ? nt
+                       : static_cast<int32_t>(std::lower_bound(pre.begin(), pre.end(), pre[nt] * b / grid) - pre.begin());
+    cta[b] = std::max(cta[b], cta[b - 1]);
+  }
+  plan.cta.alloc(grid + 1);
+  plan.cta.upload(cta.data(), grid + 1, st);
+  v.cta = plan.cta.get();
+  v.grid = grid;
+  RB_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace rb

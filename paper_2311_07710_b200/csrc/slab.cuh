@@ -1,0 +1,431 @@
+// slab.cuh — window-tiled SpMV with the gathered vector staged in shared
+// memory (fast mode).
+//
+// Why: a random fp64 gather touches its own 128 B line and the L1TEX tag stage
+// retires ~1 line per cycle per SM, so a gather-heavy SpMV is bound at ~1
+// gather/cycle/SM (C2: 1e7 gathers = 34 us) long before HBM. Shared memory
+// serves a warp's 32 random 8 B reads in a few wavefronts, so reading the
+// gathered vector from smem removes that bound whenever enough gathers land in
+// a column range to repay staging it.
+//
+// Layout (slab.cu): the columns of one segment of the op's pattern are cut
+// into aligned windows of kSlabWidth columns; windows receiving
+// >= kSlabMinDensity gathers per column are kept (at most kMaxSlabs). "W rows"
+// (>= kSlabMinRow in-window entries, every run and the rest <= kSlabRunCap)
+// are cut into chunks so that each (chunk j, window s) tile fits one shared-
+// memory stage. Inside a tile the chunk's rows are sorted by their run length
+// in window s and grouped into slices of 32 rows, one row per lane; a slice
+// stores its entries entry-major (entry e of its 32 rows contiguous; 16-bit
+// column offsets + fp64 values, 10 B/nnz), so a warp reads 32 values and 32
+// columns contiguously and only the window gather is random. Each W row also
+// has a "rest" CSR: its entries outside the windows and its other segment.
+//
+// slab_kernel is persistent (2 CTAs per SM), double-buffered and warp-
+// specialised: a producer warp bulk-copies (cp.async.bulk, mbarrier
+// complete_tx) the next tile's window slice, values, columns and slice
+// metadata into the free stage while 8 consumer warps compute the current
+// tile from shared memory, writing one partial per (window, row). Then the finish pass (SlabFinishOp through rowwise_kernel)
+// runs over all rows of the op: a W row sums its rest entries and its S
+// partials, a non-W row is the op's own row, and both run the op's epilogue.
+// A row's arithmetic depends only on the windows and its own entries (each
+// window run is summed sequentially in column order) — not on chunking,
+// slicing, tile order or CTA — so results are deterministic and a sharded
+// solve that reuses the global windows stays bit-identical.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "ops.cuh"
+
+namespace rb {
+
+constexpr int kMaxSlabs = 64;
+constexpr int kSlabWidth = 2048;        // columns per window (16 KB of fp64)
+constexpr int kSlabMinRow = 16;         // in-window entries that make a W row
+constexpr double kSlabMinDensity = 16;  // gathers per column that keep a window
+constexpr int kSlabTileCap = 3584;      // padded entries per tile (35 KB staged)
+constexpr int kSlabRowCap = 512;        // rows per chunk
+constexpr int kSlabRunCap = 512;        // W rows: every window run and the rest <= this
+constexpr int kSlabMinWindows = 1;     // RAPDHG_SLAB_MIN_WINDOWS overrides
+constexpr int kSlabProf = 10;           // per-CTA profile slots (RB_SLAB_PROFILE)
+
+// tile t = s * J + j (window-major: a CTA's contiguous tile range mostly
+// shares one window, staged once per stage)
+struct SlabTile {
+  int32_t a;     // first entry (8-aligned)
+  int32_t n;     // padded entries (multiple of 32)
+  int32_t meta;  // first metadata element in SlabView::meta (8-aligned)
+  int32_t k0;    // first W row of the chunk
+  int32_t nr;    // rows of the chunk
+  int32_t s;     // window
+  int32_t pad[2];
+};
+
+// Per-tile metadata (uint16): perm[nr] (sorted slot -> row of the chunk),
+// len[nr] (run length per sorted slot), soff[nsl + 1] (slice starts).
+__host__ __device__ inline int slab_meta_len(int nr) { return 2 * nr + (nr + 31) / 32 + 1; }
+
+struct SlabView {
+  int32_t nw = 0;                  // W rows
+  int32_t S = 0;                   // windows (even lengths)
+  int32_t J = 0;                   // row chunks
+  int32_t seg = 0;                 // accumulator the windows feed (0: segment 1, 1: segment 2)
+  int32_t win_max = 0;             // widest window (doubles, even)
+  int32_t ecap = 0;                // tile entry capacity (multiple of 32)
+  int32_t mcap = 0;                // tile metadata capacity (multiple of 8)
+  int32_t grid = 0;                // persistent CTAs
+  Window win[kMaxSlabs];
+  const SlabTile* tile = nullptr;   // [S * J]
+  const int32_t* cta = nullptr;     // [grid + 1] tile ranges per CTA (balanced by bytes)
+  const uint16_t* meta = nullptr;   // per-tile metadata
+  const uint16_t* col = nullptr;    // column offset inside the window
+  const double* val = nullptr;
+  double* partial = nullptr;        // [S * nw] (window-major: a tile's partials are contiguous)
+  const int32_t* widx = nullptr;    // [rows of the op] W-row index or -1
+  CsrView rest1{}, rest2{};         // rest CSRs over W rows (segment 1 / 2)
+  unsigned long long* prof = nullptr;  // [grid * kSlabProf] phase times (RB_SLAB_PROFILE builds)
+  bool active() const { return nw > 0 && S > 0; }
+  __host__ __device__ int tiles() const { return S * J; }
+  // stage: [header 16 B][window][values][columns][metadata]
+  __host__ __device__ int stage_bytes() const { return 16 + win_max * 8 + ecap * 10 + mcap * 2; }
+  int smem_bytes() const { return 2 * stage_bytes(); }
+};
+
+// Device arrays behind a SlabView (built by build_slab_plan).
+struct SlabPlan {
+  SlabView view;
+  DevBuf<int32_t> rows, pos, widx;
+  DevBuf<SlabTile> tile;
+  DevBuf<int32_t> cta;
+  std::vector<int64_t> tile_bytes;  // host: bytes each tile stages
+  DevBuf<uint16_t> col, meta;
+  DevBuf<double> val, partial;
+  DevBuf<int32_t> rrp1, rci1, rpos1, rrp2, rci2, rpos2;  // rest CSRs (pos = source position)
+  DevBuf<double> rval1, rval2;
+  DevBuf<unsigned long long> prof;
+};
+
+// Which windows a matrix segment gets: chosen once on the whole matrix, reused
+// unchanged for every shard so per-row arithmetic agrees.
+struct SlabChoice {
+  std::vector<Window> windows;
+  bool empty() const { return windows.empty(); }
+};
+
+// Windows over the columns of `m` (device CSR arrays, rows x ncols).
+// RAPDHG_SLAB=off disables; =force keeps every non-empty window and W rows
+// with a single in-window entry (tests reach the path at small sizes).
+SlabChoice choose_slabs(const int32_t* rp, const int32_t* ci, int32_t rows, int64_t nnz,
+                        int32_t ncols, cudaStream_t st);
+
+// Plan for rows [r0, r1) of the two-segment pattern (seg1 = rp1/ci1, may be
+// null; seg2 = rp2/ci2); the windows apply to segment `seg` (0 or 1). The
+// other segment goes entirely to the rest CSR. The op's rows are numbered
+// relative to r0 (a shard's ops index its slice); r0 = 0 on one GPU.
+void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const int32_t* rp1,
+                     const int32_t* ci1, const int32_t* rp2, const int32_t* ci2, int32_t r0,
+                     int32_t r1, cudaStream_t st);
+
+// (Re)fill the plan's values from value arrays laid out like seg1 / seg2.
+void fill_slab_values(SlabPlan& plan, const double* v1, const double* v2, cudaStream_t st);
+
+
+// Persistent grid for the slab kernel at this smem size.
+int slab_grid(const void* kernel, int smem_bytes);
+
+// ---- kernel -----------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// One-shot mbarrier + 1-D bulk copies (TMA engine): global -> shared.
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+// Streamed once: evict-first in L2, so the tiles do not displace the iterate
+// vectors the other kernels of the step gather.
+__device__ __forceinline__ void bulk_g2s_stream(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+}
+
+// Producer: arm `bar` and bulk-copy tile d into the stage at `base` (the
+// window only when the stage does not hold it already); the header is
+// published to the consumers by the mbarrier.
+template <class Op>
+__device__ __forceinline__ void slab_issue(const Op& op, const SlabView& sv, const SlabTile& d, unsigned char* base,
+                                           uint64_t* bar, bool copy_window) {
+  const Window w = sv.win[d.s];
+  int32_t* hdr = reinterpret_cast<int32_t*>(base);
+  double* win = reinterpret_cast<double*>(base + 16);
+  double* val = win + sv.win_max;
+  uint16_t* col = reinterpret_cast<uint16_t*>(val + sv.ecap);
+  uint16_t* meta = col + sv.ecap;
+  const uint32_t m8 = static_cast<uint32_t>(slab_meta_len(d.nr) + 7) & ~7u;
+  const uint32_t wbytes = copy_window ? static_cast<uint32_t>(w.len) * 8u : 0u;
+  hdr[0] = d.k0;
+  hdr[1] = d.nr;
+  hdr[2] = d.s;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic accesses of the stage before
+  mbar_expect_tx(bar, wbytes + static_cast<uint32_t>(d.n) * 10u + m8 * 2u);
+  if (wbytes) bulk_g2s(win, op.gather_src(sv.seg) + w.lo, wbytes, bar);
+  if (d.n) {
+    bulk_g2s_stream(val, sv.val + d.a, static_cast<uint32_t>(d.n) * 8u, bar);
+    bulk_g2s_stream(col, sv.col + d.a, static_cast<uint32_t>(d.n) * 2u, bar);
+  }
+  bulk_g2s_stream(meta, sv.meta + d.meta, m8 * 2u, bar);
+}
+
+#ifdef RB_SLAB_PROFILE
+// per-CTA phase times (thread 0, %globaltimer ns): [0] start, [2] waiting for
+// copies, [3] tile compute, [6] end, [7] tiles
+__device__ __forceinline__ unsigned long long slab_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define SLAB_T(var) const unsigned long long var = threadIdx.x == 0 && sv.prof ? slab_now() : 0ull
+#define SLAB_ADD(slot, v) \
+  if (threadIdx.x == 0 && sv.prof) sv.prof[blockIdx.x * kSlabProf + (slot)] += (v)
+#define SLAB_SET(slot, v) \
+  if (threadIdx.x == 0 && sv.prof) sv.prof[blockIdx.x * kSlabProf + (slot)] = (v)
+#else
+#define SLAB_T(var)
+#define SLAB_ADD(slot, v)
+#define SLAB_SET(slot, v)
+#endif
+
+constexpr int kSlabConsumers = 8;                        // consumer warps
+constexpr int kSlabThreads = 32 * (kSlabConsumers + 1);  // + one producer warp
+
+// Warp-specialised: warp kSlabConsumers (lane 0) bulk-copies tiles into the
+// two stages (full barrier: bytes landed); the consumer warps wait for a
+// stage, take every kSlabConsumers-th slice of it (dealt on a counter that
+// runs across tiles, so the warps share the work evenly without a CTA-wide
+// barrier) and arrive on the stage's empty barrier when done.
+template <class Op>
+__global__ void __launch_bounds__(kSlabThreads) slab_kernel(const Op op, const SlabView sv) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full[2], empty[2];
+  const int G = gridDim.x, nt = sv.tiles();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sb = sv.stage_bytes();
+  SLAB_T(t_start);
+#ifdef RB_SLAB_PROFILE
+  if (threadIdx.x == 0 && sv.prof)
+    for (int q = 0; q < kSlabProf; ++q) sv.prof[blockIdx.x * kSlabProf + q] = 0ull;
+#endif
+  SLAB_SET(0, t_start);
+  if (threadIdx.x == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    mbar_init(&empty[0], kSlabConsumers);
+    mbar_init(&empty[1], kSlabConsumers);
+  }
+  __syncthreads();  // barriers initialised
+  // this CTA's tiles: a contiguous range of the window-major tile order, so
+  // consecutive tiles mostly share their window
+  const int t0 = sv.cta[blockIdx.x], t1 = sv.cta[blockIdx.x + 1];
+  (void)G;
+  (void)nt;
+  // the finish kernel (a programmatic dependent launch) may start now: its
+  // rows that need no partials fill the SMs' remaining capacity
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (warp == kSlabConsumers) {  // producer
+    if (lane == 0 && t0 < t1) {
+      SlabTile d = sv.tile[t0];
+      int held[2] = {-1, -1};  // window each stage holds
+      for (int t = t0, i = 0; t < t1; ++t, ++i) {
+        const int st = i & 1;
+        const SlabTile cur = d;
+        if (t + 1 < t1) d = sv.tile[t + 1];  // prefetch the next descriptor
+        if (i >= 2) mbar_wait(&empty[st], ((i >> 1) - 1) & 1);  // tile i - 2 consumed
+        slab_issue(op, sv, cur, smem_raw + st * sb, &full[st], held[st] != cur.s);
+        held[st] = cur.s;
+      }
+    }
+    return;
+  }
+  int i = 0, deal = 0;  // deal: slices dealt so far, mod kSlabConsumers
+  for (int t = t0; t < t1; ++t, ++i) {
+    const int st = i & 1;
+    const unsigned char* base = smem_raw + st * sb;
+    SLAB_T(t_w0);
+    mbar_wait(&full[st], (i >> 1) & 1);
+    SLAB_T(t_w1);
+    SLAB_ADD(2, t_w1 - t_w0);
+    SLAB_ADD(7, 1);
+    const int32_t* hdr = reinterpret_cast<const int32_t*>(base);
+    const int k0 = hdr[0], nr = hdr[1], s = hdr[2];
+    const double* win = reinterpret_cast<const double*>(base + 16);
+    const double* val = win + sv.win_max;
+    const uint16_t* col = reinterpret_cast<const uint16_t*>(val + sv.ecap);
+    const uint16_t* perm = col + sv.ecap;
+    const uint16_t* len = perm + nr;
+    const uint16_t* soff = len + nr;
+    double* partial = sv.partial + static_cast<int64_t>(s) * sv.nw + k0;
+    const int nsl = (nr + 31) >> 5;
+    for (int q = (warp - deal + kSlabConsumers) % kSlabConsumers; q < nsl; q += kSlabConsumers) {
+      const int slot = (q << 5) + lane;
+      const bool valid = slot < nr;
+      const int L = valid ? len[slot] : 0;
+      const int b = soff[q], Lm = (soff[q + 1] - b) >> 5;  // slice width (its longest run)
+      const double* vq = val + b + lane;
+      const uint16_t* cq = col + b + lane;
+      double part = 0.0;
+      for (int e = 0; e < Lm; e += 4) {
+        double v[4], x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const bool ok = e + u < L;
+          v[u] = ok ? vq[(e + u) << 5] : 0.0;
+          x[u] = ok ? win[cq[(e + u) << 5]] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) part = fma(v[u], x[u], part);
+      }
+      if (valid) partial[perm[slot]] = part;
+    }
+    deal = (deal + nsl) % kSlabConsumers;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done reading the stage
+    SLAB_T(t_c1);
+    SLAB_ADD(3, t_c1 - t_w1);
+  }
+  SLAB_T(t_end);
+  SLAB_SET(6, t_end);
+}
+
+// The rows of Op after the slab kernel: W rows sum their rest entries, then
+// their S window partials (positions rest_len .. rest_len + S - 1 of the row,
+// lane-strided like entries), and run Op's epilogue; other rows are Op itself.
+// The per-row order depends only on the row's entries, S and its lane count,
+// which the schedule derives from this length.
+template <class Op>
+struct SlabFinishOp {
+  static constexpr bool kStrict = false;
+  static constexpr int kWideUnroll = Op::kWideUnroll;
+  static constexpr bool kStageWindows = false;
+  using AccT = typename Op::AccT;
+  Op op, rest;
+  const int32_t* widx;     // [rows of op] W-row index or -1
+  const double* partial;   // [S * nw]
+  int32_t S, nw, seg;
+  __device__ __forceinline__ int len(int r) const {
+    const int w = widx[r];
+    return w >= 0 ? rest.len(w) + S : op.len(r);
+  }
+  template <int U>
+  __device__ __forceinline__ void accumulate(int r, int lo, int hi, int lane, int stride, AccT& acc,
+                                             const Gather* g) const {
+    const int w = widx[r];
+    if (w < 0) {
+      op.template accumulate<U>(r, lo, hi, lane, stride, acc, g);
+      return;
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the slab kernel's partials are complete
+    const int rl = rest.len(w);
+    if (lo < rl) rest.template accumulate<U>(w, lo, hi < rl ? hi : rl, lane, stride, acc, g);
+    // partial q of this row at partial[q * nw + w]; 4 loads in flight, summed in order
+    const double* pr = partial + w - static_cast<int64_t>(rl) * nw;
+    const int64_t sn = static_cast<int64_t>(stride) * nw;
+    double t = 0.0;
+    int p = next_pos(lo + lane, stride, rl);
+    for (; p + 3 * stride < hi; p += 4 * stride) {
+      const double* q = pr + static_cast<int64_t>(p) * nw;
+      const double a0 = __ldcg(q), a1 = __ldcg(q + sn), a2 = __ldcg(q + 2 * sn), a3 = __ldcg(q + 3 * sn);
+      t += a0;
+      t += a1;
+      t += a2;
+      t += a3;
+    }
+    for (; p < hi; p += stride) t += __ldcg(pr + static_cast<int64_t>(p) * nw);
+    if (seg == 0) acc.v[0] += t;
+    else acc.v[AccT::kK - 1] += t;
+  }
+  __device__ __forceinline__ const double* gather_src(int slot) const { return op.gather_src(slot); }
+  __device__ __forceinline__ void finish(int r, const AccT& acc) const { op.finish(r, acc); }
+};
+
+// Raise the dynamic smem limit of the slab kernel of Op (once, outside stream
+// capture) and return the persistent grid for that smem size.
+template <class Op>
+inline int prepare_slab(int smem_bytes) {
+  const void* k = reinterpret_cast<const void*>(&slab_kernel<Op>);
+  RB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
+  return slab_grid(k, smem_bytes);
+}
+
+// A slab-tiled op: the plan and the finish schedule over all of its rows.
+struct SlabPhase {
+  SlabPlan plan;
+  Schedule fin;
+  bool active() const { return plan.view.active(); }
+};
+
+// Plan + finish schedule for rows [r0, r1) of the op (see build_slab_plan);
+// `len`: the op's row lengths for those rows. Leaves `ph` inactive when there
+// are no W rows.
+void build_slab_phase(SlabPhase& ph, const SlabChoice& choice, int seg, const int32_t* rp1, const int32_t* ci1,
+                      const int32_t* rp2, const int32_t* ci2, int32_t r0, int32_t r1, const int32_t* len,
+                      cudaStream_t st);
+
+// Per-CTA contiguous tile ranges for `grid` persistent CTAs, balanced by the
+// bytes each tile stages (after the grid is known).
+void assign_slab_ctas(SlabPlan& plan, int grid, cudaStream_t st);
+
+// One slab-tiled op: the slab kernel, then the finish kernel as a programmatic
+// dependent launch (rows without partials start while the slab kernel runs;
+// W rows wait for it). Returns kernels launched.
+template <class Op>
+inline int launch_slab_phase(const Op& op, const SlabPhase& ph, cudaStream_t st) {
+  const SlabView& sv = ph.plan.view;
+  slab_kernel<Op><<<sv.grid, kSlabThreads, sv.smem_bytes(), st>>>(op, sv);
+  RB_LAUNCH_CHECK();
+  const SchedView& s = ph.fin.view;
+  if (s.total_blocks <= 0) return 1;
+  const SlabFinishOp<Op> f{op, op.with_views(sv.rest1, sv.rest2), sv.widx, sv.partial, sv.S, sv.nw, sv.seg};
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(s.total_blocks));
+  cfg.blockDim = dim3(kBlock);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  RB_CUDA(cudaLaunchKernelEx(&cfg, rowwise_kernel<SlabFinishOp<Op>, false>, f, s));
+  return 2;
+}
+
+}  // namespace rb

@@ -1,0 +1,71 @@
+"""GPU: slab-staged gathers (csrc/slab.cuh). Forced on at test sizes
+(RAPDHG_SLAB=force) they must keep the fast-mode contract against the
+reference, agree with the unstaged kernels, keep the sharded solve
+bit-identical, and trigger by themselves on the full C2 Lasso."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2311_07710_b200 as rb
+from instances import long_row_qp, random_qp
+from test_gpu_parity import _fast_vs_ref, rel_err
+from test_oracle import assert_results_identical
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def O():
+    oracle.build()
+    return oracle.ref() if oracle.have_ref() else oracle.port()
+
+
+@pytest.mark.parametrize("seed", [1, 3])
+def test_slab_forced_fast_vs_reference(O, seed, monkeypatch):
+    monkeypatch.setenv("RAPDHG_SLAB", "force")
+    p = random_qp(seed, n=300, mi=120, me=30, dens=0.2)
+    a, b, agree = _fast_vs_ref(O, p, dict(tol=1e-12), 600)
+    assert agree >= 5
+
+
+def test_slab_forced_matches_unstaged(monkeypatch):
+    p = random_qp(5, n=500, mi=200, me=50, dens=0.15)
+    cfg = rb.SolverConfig(tol=1e-12, max_iters=400, snapshot_interval=40)
+    monkeypatch.setenv("RAPDHG_SLAB", "force")
+    a = rb.solve(p, cfg)
+    monkeypatch.setenv("RAPDHG_SLAB", "off")
+    b = rb.solve(p, cfg)
+    for (ta, za), (tb, zb) in zip(a.snapshots, b.snapshots):
+        assert ta == tb and rel_err(za.x, zb.x) < 1e-10
+    monkeypatch.setenv("RAPDHG_SLAB", "force")
+    c = rb.solve(p, cfg)
+    assert_results_identical(a, c)  # deterministic
+
+
+def test_slab_long_rows(O, monkeypatch):
+    monkeypatch.setenv("RAPDHG_SLAB", "force")
+    a, b, agree = _fast_vs_ref(O, long_row_qp(), dict(tol=1e-12), 160)
+    assert agree >= 2
+
+
+@pytest.mark.parametrize("parts", [2, 3])
+def test_slab_sharded_bit_identical(parts, monkeypatch):
+    monkeypatch.setenv("RAPDHG_SLAB", "force")
+    p = rb.generate(rb.Gen.LASSO, 0.05, 2)
+    cfg = rb.SolverConfig(tol=1e-6, max_iters=2000, snapshot_interval=80)
+    assert_results_identical(rb.solve_sharded(p, cfg, parts), rb.solve(p, cfg))
+
+
+def test_slab_auto_on_c2(monkeypatch):
+    """The full C2 Lasso gets slab plans by itself; iterates stay within the
+    fast-mode tolerance of the unstaged kernels at a fixed iteration count."""
+    p = rb.generate(rb.Gen.LASSO, 1.0, 2)
+    cfg = rb.SolverConfig(tol=1e-12, max_iters=200, snapshot_interval=40)
+    a = rb.solve(p, cfg)
+    monkeypatch.setenv("RAPDHG_SLAB", "off")
+    b = rb.solve(p, cfg)
+    same = True
+    for (ta, za), (tb, zb) in zip(a.snapshots, b.snapshots):
+        assert ta == tb and rel_err(za.x, zb.x) < 1e-9
+        same = same and np.array_equal(za.x, zb.x)
+    assert not same  # a different summation order ran: the slab tiles

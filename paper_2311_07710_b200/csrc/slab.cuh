@@ -44,7 +44,8 @@ constexpr int kMaxSlabs = 64;
 constexpr int kSlabWidth = 2048;        // columns per window (16 KB of fp64)
 constexpr int kSlabMinRow = 16;         // in-window entries that make a W row
 constexpr double kSlabMinDensity = 16;  // gathers per column that keep a window
-constexpr int kSlabTileCap = 3584;      // padded entries per tile (35 KB staged)
+constexpr int kSlabTileCap = 2560;      // padded entries per tile (25 KB staged)
+constexpr int kSlabStages = 3;          // tile stages per CTA (one shared window)
 constexpr int kSlabRowCap = 512;        // rows per chunk
 constexpr int kSlabRunCap = 512;        // W rows: every window run and the rest <= this
 constexpr int kSlabMinWindows = 1;     // RAPDHG_SLAB_MIN_WINDOWS overrides
@@ -88,8 +89,10 @@ struct SlabView {
   bool active() const { return nw > 0 && S > 0; }
   __host__ __device__ int tiles() const { return S * J; }
   // stage: [header 16 B][window][values][columns][metadata]
-  __host__ __device__ int stage_bytes() const { return 16 + win_max * 8 + ecap * 10 + mcap * 2; }
-  int smem_bytes() const { return 2 * stage_bytes(); }
+  // smem: [window][stage 0] .. [stage kSlabStages - 1];
+  // stage: [header 16 B][values][columns][metadata]
+  __host__ __device__ int stage_bytes() const { return 16 + ecap * 10 + mcap * 2; }
+  int smem_bytes() const;
 };
 
 // Device arrays behind a SlabView (built by build_slab_plan).
@@ -178,16 +181,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
         : "memory");
 }
 
-// Producer: arm `bar` and bulk-copy tile d into the stage at `base` (the
-// window only when the stage does not hold it already); the header is
-// published to the consumers by the mbarrier.
+// Producer: arm `bar` and bulk-copy tile d into the stage at `base` (and the
+// window into `win` when it changes); the header is published to the
+// consumers by the mbarrier.
 template <class Op>
-__device__ __forceinline__ void slab_issue(const Op& op, const SlabView& sv, const SlabTile& d, unsigned char* base,
-                                           uint64_t* bar, bool copy_window) {
+__device__ __forceinline__ void slab_issue(const Op& op, const SlabView& sv, const SlabTile& d, double* win,
+                                           unsigned char* base, uint64_t* bar, bool copy_window) {
   const Window w = sv.win[d.s];
   int32_t* hdr = reinterpret_cast<int32_t*>(base);
-  double* win = reinterpret_cast<double*>(base + 16);
-  double* val = win + sv.win_max;
+  double* val = reinterpret_cast<double*>(base + 16);
   uint16_t* col = reinterpret_cast<uint16_t*>(val + sv.ecap);
   uint16_t* meta = col + sv.ecap;
   const uint32_t m8 = static_cast<uint32_t>(slab_meta_len(d.nr) + 7) & ~7u;
@@ -195,7 +197,7 @@ __device__ __forceinline__ void slab_issue(const Op& op, const SlabView& sv, con
   hdr[0] = d.k0;
   hdr[1] = d.nr;
   hdr[2] = d.s;
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic accesses of the stage before
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic accesses of the buffers before
   mbar_expect_tx(bar, wbytes + static_cast<uint32_t>(d.n) * 10u + m8 * 2u);
   if (wbytes) bulk_g2s(win, op.gather_src(sv.seg) + w.lo, wbytes, bar);
   if (d.n) {
@@ -227,17 +229,20 @@ __device__ __forceinline__ unsigned long long slab_now() {
 constexpr int kSlabConsumers = 8;                        // consumer warps
 constexpr int kSlabThreads = 32 * (kSlabConsumers + 1);  // + one producer warp
 
-// Warp-specialised: warp kSlabConsumers (lane 0) bulk-copies tiles into the
-// two stages (full barrier: bytes landed); the consumer warps wait for a
+// Warp-specialised: warp kSlabConsumers (lane 0) bulk-copies tiles into
+// kSlabStages stages (full barrier: bytes landed) and, when a tile's window
+// differs from the one held, first waits until every issued tile is consumed
+// and then reloads the shared window with it; the consumer warps wait for a
 // stage, take every kSlabConsumers-th slice of it (dealt on a counter that
 // runs across tiles, so the warps share the work evenly without a CTA-wide
 // barrier) and arrive on the stage's empty barrier when done.
 template <class Op>
 __global__ void __launch_bounds__(kSlabThreads) slab_kernel(const Op op, const SlabView sv) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ __align__(8) uint64_t full[2], empty[2];
-  const int G = gridDim.x, nt = sv.tiles();
+  __shared__ __align__(8) uint64_t full[kSlabStages], empty[kSlabStages];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* win = reinterpret_cast<double*>(smem_raw);
+  unsigned char* stages = smem_raw + sv.win_max * 8;
   const int sb = sv.stage_bytes();
   SLAB_T(t_start);
 #ifdef RB_SLAB_PROFILE
@@ -245,49 +250,51 @@ __global__ void __launch_bounds__(kSlabThreads) slab_kernel(const Op op, const S
     for (int q = 0; q < kSlabProf; ++q) sv.prof[blockIdx.x * kSlabProf + q] = 0ull;
 #endif
   SLAB_SET(0, t_start);
-  if (threadIdx.x == 0) {
-    mbar_init(&full[0], 1);
-    mbar_init(&full[1], 1);
-    mbar_init(&empty[0], kSlabConsumers);
-    mbar_init(&empty[1], kSlabConsumers);
-  }
+  if (threadIdx.x == 0)
+    for (int q = 0; q < kSlabStages; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], kSlabConsumers);
+    }
   __syncthreads();  // barriers initialised
   // this CTA's tiles: a contiguous range of the window-major tile order, so
   // consecutive tiles mostly share their window
   const int t0 = sv.cta[blockIdx.x], t1 = sv.cta[blockIdx.x + 1];
-  (void)G;
-  (void)nt;
   // the finish kernel (a programmatic dependent launch) may start now: its
   // rows that need no partials fill the SMs' remaining capacity
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (warp == kSlabConsumers) {  // producer
     if (lane == 0 && t0 < t1) {
       SlabTile d = sv.tile[t0];
-      int held[2] = {-1, -1};  // window each stage holds
+      int held = -1;  // window in the shared buffer
       for (int t = t0, i = 0; t < t1; ++t, ++i) {
-        const int st = i & 1;
+        const int st = i % kSlabStages;
         const SlabTile cur = d;
         if (t + 1 < t1) d = sv.tile[t + 1];  // prefetch the next descriptor
-        if (i >= 2) mbar_wait(&empty[st], ((i >> 1) - 1) & 1);  // tile i - 2 consumed
-        slab_issue(op, sv, cur, smem_raw + st * sb, &full[st], held[st] != cur.s);
-        held[st] = cur.s;
+        if (i >= kSlabStages) mbar_wait(&empty[st], (i / kSlabStages - 1) & 1);  // stage free
+        const bool change = cur.s != held;
+        if (change && held >= 0)  // drain: the tiles in flight still read the old window
+          for (int q = 1; q < kSlabStages && i - q >= 0; ++q) {
+            const int p = i - q;
+            mbar_wait(&empty[p % kSlabStages], (p / kSlabStages) & 1);
+          }
+        slab_issue(op, sv, cur, win, stages + st * sb, &full[st], change);
+        held = cur.s;
       }
     }
     return;
   }
   int i = 0, deal = 0;  // deal: slices dealt so far, mod kSlabConsumers
   for (int t = t0; t < t1; ++t, ++i) {
-    const int st = i & 1;
-    const unsigned char* base = smem_raw + st * sb;
+    const int st = i % kSlabStages;
+    const unsigned char* base = stages + st * sb;
     SLAB_T(t_w0);
-    mbar_wait(&full[st], (i >> 1) & 1);
+    mbar_wait(&full[st], (i / kSlabStages) & 1);
     SLAB_T(t_w1);
     SLAB_ADD(2, t_w1 - t_w0);
     SLAB_ADD(7, 1);
     const int32_t* hdr = reinterpret_cast<const int32_t*>(base);
     const int k0 = hdr[0], nr = hdr[1], s = hdr[2];
-    const double* win = reinterpret_cast<const double*>(base + 16);
-    const double* val = win + sv.win_max;
+    const double* val = reinterpret_cast<const double*>(base + 16);
     const uint16_t* col = reinterpret_cast<const uint16_t*>(val + sv.ecap);
     const uint16_t* perm = col + sv.ecap;
     const uint16_t* len = perm + nr;
@@ -317,13 +324,15 @@ __global__ void __launch_bounds__(kSlabThreads) slab_kernel(const Op op, const S
     }
     deal = (deal + nsl) % kSlabConsumers;
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done reading the stage
+    if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done reading the stage (and the window)
     SLAB_T(t_c1);
     SLAB_ADD(3, t_c1 - t_w1);
   }
   SLAB_T(t_end);
   SLAB_SET(6, t_end);
 }
+
+inline int SlabView::smem_bytes() const { return win_max * 8 + kSlabStages * stage_bytes(); }
 
 // The rows of Op after the slab kernel: W rows sum their rest entries, then
 // their S window partials (positions rest_len .. rest_len + S - 1 of the row,

@@ -669,6 +669,7 @@ void append(T*& arr, int64_t& count, const T& v) {
 void Engine::loop_begin() {
   kernel_ms_[0] = kernel_ms_[1] = 0.0;
   kernel_count_[0] = kernel_count_[1] = 0;
+  chunk_counter_ = 0;  // every solve samples its first chunk
   launches_ = P_->launches;
   // loop time on the device timeline: events on the solver's stream bracket
   // everything from the first candidate evaluation to the final download

@@ -78,13 +78,19 @@ struct DualStepOp {
     o.a = s1;
     return o;
   }
-  __device__ __forceinline__ void finish(int i, const AccT& acc) const {
+  // epilogue inputs, loaded before the row's gathers so their latency overlaps
+  struct Pre {
+    double y, b, yb;
+  };
+  __device__ __forceinline__ Pre prefetch(int i) const { return Pre{y[i], b[i], yb[i]}; }
+  __device__ __forceinline__ void finish(int i, const AccT& acc) const { finish(i, acc, prefetch(i)); }
+  __device__ __forceinline__ void finish(int i, const AccT& acc, const Pre& pre) const {
     const IterParams& q = P[it];
-    double yi = y[i];
-    yi += q.tau * (acc.v[0] - b[i]);
+    double yi = pre.y;
+    yi += q.tau * (acc.v[0] - pre.b);
     if (i < m_ineq) yi = yi > 0.0 ? yi : 0.0;
     y[i] = yi;
-    yb[i] = q.omib * yb[i] + q.ib * yi;
+    yb[i] = q.omib * pre.yb + q.ib * yi;
     flag_nonfinite(yi, q.t, bad);
   }
 };
@@ -136,12 +142,18 @@ struct PrimalStepOp {
     o.at = s2;
     return o;
   }
-  __device__ __forceinline__ void finish(int j, const AccT& acc) const {
+  // epilogue inputs, loaded before the row's gathers so their latency overlaps
+  struct Pre {
+    double x, c, xb;
+  };
+  __device__ __forceinline__ Pre prefetch(int j) const { return Pre{x_in[j], c[j], xb[j]}; }
+  __device__ __forceinline__ void finish(int j, const AccT& acc) const { finish(j, acc, prefetch(j)); }
+  __device__ __forceinline__ void finish(int j, const AccT& acc, const Pre& pre) const {
     const IterParams& p = P[it];
-    const double xo = x_in[j];
-    const double xn = xo - p.eta * (acc.v[0] + c[j] + acc.v[1]);
+    const double xo = pre.x;
+    const double xn = xo - p.eta * (acc.v[0] + pre.c + acc.v[1]);
     x_out[j] = xn;
-    const double xbn = p.omib * xb[j] + p.ib * xn;
+    const double xbn = p.omib * pre.xb + p.ib * xn;
     xb[j] = xbn;
     if (p.emit_next) {
       w_out[j] = p.theta_n * (xn - xo) + xn;

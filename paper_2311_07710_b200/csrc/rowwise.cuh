@@ -23,6 +23,8 @@
 // is one kernel node in the per-chunk CUDA graph.
 #pragma once
 
+#include <type_traits>
+
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -231,6 +233,24 @@ __device__ __forceinline__ void seg_dot2(const double* __restrict__ vals,
 // the Op's gathered-vector windows in shared memory once, before its first
 // tile.
 
+// Ops may declare `Pre prefetch(r)` (epilogue inputs) and
+// `finish(r, acc, pre)`: the kernel loads them before the row's gathers.
+struct NoPre {};
+template <class Op, class = void>
+struct HasPre : std::false_type {};
+template <class Op>
+struct HasPre<Op, std::void_t<typename Op::Pre>> : std::true_type {};
+template <class Op>
+__device__ __forceinline__ auto prefetch_of(const Op& op, int r) {
+  if constexpr (HasPre<Op>::value) return op.prefetch(r);
+  else return NoPre{};
+}
+template <class Op, class P>
+__device__ __forceinline__ void finish_with(const Op& op, int r, const typename Op::AccT& a, const P& pre) {
+  if constexpr (HasPre<Op>::value) op.finish(r, a, pre);
+  else op.finish(r, a);
+}
+
 template <class Op, int V>
 __device__ __forceinline__ void run_vlane(const Op& op, const SchedView& s, const BinDesc& bd,
                                           int tile, const Gather* g) {
@@ -240,11 +260,13 @@ __device__ __forceinline__ void run_vlane(const Op& op, const SchedView& s, cons
   const int slot = bd.row_begin + (tile - bd.blk_begin) * kRowsPerBlock + grp;
   const bool valid = slot < bd.row_end;
   const int r = valid ? (s.perm ? s.perm[slot] : slot) : 0;
+  decltype(prefetch_of(op, r)) pre{};
+  if (valid && lane == 0) pre = prefetch_of(op, r);
   typename Op::AccT a;
   a.zero();
   if (valid) op.template accumulate<(V >= 16 ? Op::kWideUnroll : kUnroll)>(r, 0, op.len(r), lane, V, a, g);
   a.template reduce_lanes<V>();  // all lanes participate (invalid ones hold 0)
-  if (valid && lane == 0) op.finish(r, a);
+  if (valid && lane == 0) finish_with(op, r, a, pre);
 }
 
 template <class Op>
@@ -272,11 +294,13 @@ __device__ __forceinline__ void run_block_row(const Op& op, const SchedView& s, 
                                               int tile, const Gather* g) {
   const int slot = bd.row_begin + (tile - bd.blk_begin);
   const int r = s.perm ? s.perm[slot] : slot;
+  decltype(prefetch_of(op, r)) pre{};
+  if (threadIdx.x == 0) pre = prefetch_of(op, r);
   typename Op::AccT a;
   a.zero();
   op.template accumulate<kUnroll>(r, 0, op.len(r), threadIdx.x, kBlock, a, g);
   block_reduce<Op>(a);
-  if (threadIdx.x == 0) op.finish(r, a);
+  if (threadIdx.x == 0) finish_with(op, r, a, pre);
 }
 
 template <class Op>

@@ -382,7 +382,10 @@ struct SlabFinishOp {
     else acc.v[AccT::kK - 1] += t;
   }
   __device__ __forceinline__ const double* gather_src(int slot) const { return op.gather_src(slot); }
+  using Pre = typename Op::Pre;
+  __device__ __forceinline__ Pre prefetch(int r) const { return op.prefetch(r); }
   __device__ __forceinline__ void finish(int r, const AccT& acc) const { op.finish(r, acc); }
+  __device__ __forceinline__ void finish(int r, const AccT& acc, const Pre& pre) const { op.finish(r, acc, pre); }
 };
 
 // Raise the dynamic smem limit of the slab kernel of Op (once, outside stream

@@ -1,0 +1,162 @@
+// colblock.cu — setup of L2-sized column blocks (see colblock.cuh).
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <cstdlib>
+#include <string>
+
+#include "colblock.cuh"
+
+namespace rb {
+
+namespace {
+
+constexpr int kMaxColBlocks = 16;
+
+struct Cuts {
+  int32_t c[kMaxColBlocks + 1];
+  int nb;
+};
+
+__device__ __forceinline__ int lower_col(const int32_t* ci, int b, int e, int32_t key) {
+  while (b < e) {  // first position in [b, e) with ci >= key (rows are column-sorted)
+    const int mid = (b + e) >> 1;
+    if (ci[mid] < key) b = mid + 1;
+    else e = mid;
+  }
+  return b;
+}
+
+// cnt[b * rows + r] = entries of row r in block b
+__global__ void block_counts_kernel(const int32_t* rp, const int32_t* ci, int32_t rows, Cuts cuts, int32_t* cnt) {
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (r >= rows) return;
+  int lo = rp[r];
+  const int e = rp[r + 1];
+  for (int b = 0; b < cuts.nb; ++b) {
+    const int hi = b + 1 == cuts.nb ? e : lower_col(ci, lo, e, cuts.c[b + 1]);
+    cnt[static_cast<int64_t>(b) * rows + r] = hi - lo;
+    lo = hi;
+  }
+}
+
+// copy block b's entries of every row (columns and source positions)
+__global__ void block_fill_kernel(const int32_t* rp, const int32_t* ci, int32_t rows, const int32_t* brp,
+                                  const int32_t* skip, int32_t* bci, int32_t* bpos) {
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (r >= rows) return;
+  const int src = rp[r] + skip[r];
+  const int n = brp[r + 1] - brp[r];
+  for (int k = 0; k < n; ++k) {
+    bci[brp[r] + k] = ci[src + k];
+    bpos[brp[r] + k] = src + k;
+  }
+}
+
+__global__ void add_kernel(int32_t* acc, const int32_t* x, int64_t n) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) acc[i] += x[i];
+}
+
+__global__ void gather_vals_kernel(double* dst, const double* src, const int32_t* pos, int64_t n) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) dst[i] = src[pos[i]];
+}
+
+__global__ void locality_kernel(const int32_t* rp, const int32_t* ci, int32_t rows, int32_t ncols,
+                                unsigned long long* count) {
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  unsigned long long c = 0;
+  if (r < rows) {
+    const double diag = static_cast<double>(r) / rows * ncols, band = ncols / 16.0;
+    for (int p = rp[r]; p < rp[r + 1]; ++p) c += fabs(ci[p] - diag) <= band ? 1ull : 0ull;
+  }
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);  // integer: exact
+}
+
+inline unsigned g1(int64_t n) { return static_cast<unsigned>(ceil_div(n > 0 ? n : 1, 256)); }
+
+}  // namespace
+
+int colblock_count(int64_t ncols) {
+  const char* off = std::getenv("RAPDHG_L2BLOCK");
+  if (off && std::string(off) == "0") return 1;
+  std::size_t blk = kL2BlockBytes;
+  if (const char* kb = std::getenv("RAPDHG_L2BLOCK_KB")) blk = std::max<std::size_t>(1, std::atoll(kb)) << 10;
+  const std::size_t bytes = static_cast<std::size_t>(ncols) * sizeof(double);
+  const int nb = static_cast<int>((bytes + blk - 1) / blk);
+  return nb < 2 ? 1 : std::min(nb, kMaxColBlocks);
+}
+
+void build_colblocks(ColBlocks& cb, int nb, const int32_t* rp, const int32_t* ci, int32_t rows, int32_t ncols,
+                     cudaStream_t st) {
+  cb = ColBlocks{};
+  if (nb < 2 || rows <= 0) return;
+  cb.nb = nb;
+  Cuts cuts{};
+  cuts.nb = nb;
+  for (int b = 0; b <= nb; ++b) cuts.c[b] = static_cast<int32_t>(static_cast<int64_t>(ncols) * b / nb);
+  cb.cut.assign(cuts.c, cuts.c + nb + 1);
+  DevBuf<int32_t> cnt(static_cast<std::size_t>(nb) * rows);
+  block_counts_kernel<<<g1(rows), 256, 0, st>>>(rp, ci, rows, cuts, cnt.get());
+  RB_LAUNCH_CHECK();
+  // row pointers per block (exclusive scans), and per-row skips (entries of
+  // the earlier blocks) to locate each block's sub-run in the source row
+  DevBuf<int32_t> skip(rows);
+  skip.zero(st);
+  std::size_t temp_bytes = 0;
+  RB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp_bytes, cnt.get(), cnt.get(), rows + 1, st));
+  DevBuf<unsigned char> temp(temp_bytes);
+  cb.blk.resize(nb);
+  cb.pos.resize(nb);
+  for (int b = 0; b < nb; ++b) {
+    DevCsr& m = cb.blk[b];
+    m.rows = rows;
+    m.cols = ncols;
+    m.rp.alloc(rows + 1);
+    // scan rows + 1 counts: the (rows)-th input is the next block's first count
+    // or past the end, so scan `rows` items and append the total
+    RB_CUDA(cub::DeviceScan::ExclusiveSum(temp.get(), temp_bytes, cnt.get() + static_cast<int64_t>(b) * rows,
+                                          m.rp.get(), rows, st));
+    int32_t last_rp = 0, last_cnt = 0;
+    RB_CUDA(cudaMemcpyAsync(&last_rp, m.rp.get() + rows - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    RB_CUDA(cudaMemcpyAsync(&last_cnt, cnt.get() + static_cast<int64_t>(b) * rows + rows - 1, sizeof(int32_t),
+                            cudaMemcpyDeviceToHost, st));
+    RB_CUDA(cudaStreamSynchronize(st));
+    const int32_t total = last_rp + last_cnt;
+    RB_CUDA(cudaMemcpyAsync(m.rp.get() + rows, &total, sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    m.nnz = total;
+    m.ci.alloc(total);
+    m.v.alloc(total);
+    cb.pos[b].alloc(total);
+    block_fill_kernel<<<g1(rows), 256, 0, st>>>(rp, ci, rows, m.rp.get(), skip.get(), m.ci.get(), cb.pos[b].get());
+    RB_LAUNCH_CHECK();
+    add_kernel<<<g1(rows), 256, 0, st>>>(skip.get(), cnt.get() + static_cast<int64_t>(b) * rows, rows);
+    RB_LAUNCH_CHECK();
+    RB_CUDA(cudaStreamSynchronize(st));  // `total` lives on the host stack
+  }
+}
+
+double pattern_locality(const int32_t* rp, const int32_t* ci, int32_t rows, int32_t ncols, int64_t nnz,
+                        cudaStream_t st) {
+  if (rows <= 0 || nnz <= 0) return 0.0;
+  DevBuf<unsigned long long> cnt(1);
+  cnt.zero(st);
+  locality_kernel<<<g1(rows), 256, 0, st>>>(rp, ci, rows, ncols, cnt.get());
+  RB_LAUNCH_CHECK();
+  unsigned long long h = 0;
+  RB_CUDA(cudaMemcpyAsync(&h, cnt.get(), sizeof(h), cudaMemcpyDeviceToHost, st));
+  RB_CUDA(cudaStreamSynchronize(st));
+  return static_cast<double>(h) / static_cast<double>(nnz);
+}
+
+void fill_colblock_values(ColBlocks& cb, const double* vals, cudaStream_t st) {
+  for (int b = 0; b < cb.nb && cb.active(); ++b) {
+    DevCsr& m = cb.blk[b];
+    if (m.nnz) gather_vals_kernel<<<g1(m.nnz), 256, 0, st>>>(m.v.get(), vals, cb.pos[b].get(), m.nnz);
+    RB_LAUNCH_CHECK();
+  }
+}
+
+}  // namespace rb

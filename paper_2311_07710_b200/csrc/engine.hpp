@@ -18,6 +18,7 @@
 #include "ops.cuh"
 #include "reduce.cuh"
 #include "rowwise.cuh"
+#include "colblock.cuh"
 #include "slab.cuh"
 
 namespace rb {
@@ -190,6 +191,12 @@ class Engine : public LoopBackend {
   void setup_slabs();
   SlabChoice dual_choice_, primal_choice_;
   SlabPhase dual_ph_, primal_ph_;
+  // L2-sized column blocks (colblock.cuh) of the gather-bound ops without a slab plan
+  void setup_colblocks();
+  ColBlocks cb_dual_, cb_q_, cb_at_;
+  DevBuf<double> part_dual_, part_q_, part_at_;
+  std::vector<Schedule> sch_cb_dual_, sch_cb_q_, sch_cb_at_;
+  Schedule sch_cb_primal_;
   std::map<int, cudaGraphExec_t> graphs_;  // key: len, parity, profiled
   std::map<int, int64_t> graph_launches_;
   int64_t chunk_counter_ = 0;

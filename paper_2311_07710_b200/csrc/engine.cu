@@ -476,19 +476,36 @@ void Engine::setup_colblocks() {
         build_schedule(sch_cb_q_[b], len.get(), n_, false, st_);
       }
     }
+    // With Q blocked, A'y runs as partial passes too (all its blocks), so the
+    // last pass gathers from one L2-sized block only.
+    at_all_partial_ = nq >= 2;
+    if (at_all_partial_ && na < 2) {
+      sch_cb_at_.resize(1);
+      row_lengths(len, P.AT.rp.get(), nullptr, n_, st_);
+      build_schedule(sch_cb_at_[0], len.get(), n_, false, st_);
+      part_at_.alloc(n_);
+      zero_rp_.alloc(n_ + 1);
+      zero_rp_.zero(st_);
+    }
     if (na >= 2) {
       build_colblocks(cb_at_, na, P.AT.rp.get(), P.AT.ci.get(), n_, m_, st_);
       fill_colblock_values(cb_at_, atsv_, st_);
-      part_at_.alloc(static_cast<std::size_t>(na - 1) * n_);
-      sch_cb_at_.resize(na - 1);
-      for (int b = 0; b + 1 < na; ++b) {
+      const int np = at_all_partial_ ? na : na - 1;
+      part_at_.alloc(static_cast<std::size_t>(np) * n_);
+      sch_cb_at_.resize(np);
+      if (at_all_partial_) {
+        zero_rp_.alloc(n_ + 1);
+        zero_rp_.zero(st_);
+      }
+      for (int b = 0; b < np; ++b) {
         row_lengths(len, cb_at_.blk[b].rp.get(), nullptr, n_, st_);
         build_schedule(sch_cb_at_[b], len.get(), n_, false, st_);
       }
     }
     if (nq >= 2 || na >= 2) {
       row_lengths(len, nq >= 2 ? cb_q_.blk[nq - 1].rp.get() : P.Q.rp.get(),
-                  na >= 2 ? cb_at_.blk[na - 1].rp.get() : P.AT.rp.get(), n_, st_);
+                  at_all_partial_ ? zero_rp_.get() : na >= 2 ? cb_at_.blk[na - 1].rp.get() : P.AT.rp.get(), n_,
+                  st_);
       build_schedule(sch_cb_primal_, len.get(), n_, false, st_);
     }
   }
@@ -598,15 +615,18 @@ void Engine::launch_chunk_body(int len, int cur, bool prof) {
           const SpmvOp<false> sp{cb_q_.blk[b].view(), XMD_[c].get(), part_q_.get() + static_cast<int64_t>(b) * n_};
           rowwise(sp, sch_cb_q_[b], st_, &launches_);
         }
-        for (int b = 0; b + 1 < na && cb_at_.active(); ++b) {
-          const SpmvOp<false> sp{cb_at_.blk[b].view(), y_.get(), part_at_.get() + static_cast<int64_t>(b) * n_};
+        const int npa = static_cast<int>(sch_cb_at_.size());  // A'y partial passes
+        for (int b = 0; b < npa; ++b) {
+          const CsrView at = cb_at_.active() ? cb_at_.blk[b].view() : P_->AT.view(atsv_);
+          const SpmvOp<false> sp{at, y_.get(), part_at_.get() + static_cast<int64_t>(b) * n_};
           rowwise(sp, sch_cb_at_[b], st_, &launches_);
         }
         PrimalStepOp<false> pl = pr;
         if (cb_q_.active()) pl.q = cb_q_.blk[nq - 1].view();
-        if (cb_at_.active()) pl.at = cb_at_.blk[na - 1].view();
-        rowwise(PartialsOp<PrimalStepOp<false>>{pl, part_q_.get(), part_at_.get(), cb_q_.active() ? nq - 1 : 0,
-                                                cb_at_.active() ? na - 1 : 0, n_},
+        if (at_all_partial_) pl.at = CsrView{zero_rp_.get(), P_->AT.ci.get(), atsv_};
+        else if (cb_at_.active()) pl.at = cb_at_.blk[na - 1].view();
+        rowwise(PartialsOp<PrimalStepOp<false>>{pl, part_q_.get(), part_at_.get(), cb_q_.active() ? nq - 1 : 0, npa,
+                                                n_},
                 sch_cb_primal_, st_, &launches_);
       } else {
         rowwise(pr, P_->sch_primal, st_, &launches_);

@@ -197,6 +197,8 @@ class Engine : public LoopBackend {
   DevBuf<double> part_dual_, part_q_, part_at_;
   std::vector<Schedule> sch_cb_dual_, sch_cb_q_, sch_cb_at_;
   Schedule sch_cb_primal_;
+  bool at_all_partial_ = false;  // A'y entirely in partial passes (Q blocked)
+  DevBuf<int32_t> zero_rp_;      // empty CSR rows
   std::map<int, cudaGraphExec_t> graphs_;  // key: len, parity, profiled
   std::map<int, int64_t> graph_launches_;
   int64_t chunk_counter_ = 0;

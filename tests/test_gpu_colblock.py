@@ -53,3 +53,12 @@ def test_colblock_qp_with_q(O, blocked):
     p = random_qp(7, n=800, mi=500, me=100, dens=0.08)
     a, b, agree = _fast_vs_ref(O, p, dict(tol=1e-12), 400)
     assert agree >= 4
+
+
+def test_colblock_q_only(O, monkeypatch):
+    # n*8 over the block size, m*8 under it: A'y becomes a single partial pass
+    monkeypatch.setenv("RAPDHG_SLAB", "off")
+    monkeypatch.setenv("RAPDHG_L2BLOCK_KB", "4")
+    p = random_qp(11, n=900, mi=300, me=60, dens=0.08)
+    a, b, agree = _fast_vs_ref(O, p, dict(tol=1e-12), 400)
+    assert agree >= 4

@@ -159,4 +159,63 @@ void fill_colblock_values(ColBlocks& cb, const double* vals, cudaStream_t st) {
   }
 }
 
+void build_colblocked_dual(ColBlockedDual& d, int nb, const int32_t* rp, const int32_t* ci, int32_t rows,
+                           int32_t ncols, const double* vals, cudaStream_t st) {
+  d = ColBlockedDual{};
+  if (nb < 2 || rows <= 0) return;
+  d.rows = rows;
+  build_colblocks(d.cb, nb, rp, ci, rows, ncols, st);
+  fill_colblock_values(d.cb, vals, st);
+  d.part.alloc(static_cast<std::size_t>(nb - 1) * rows);
+  d.sch.resize(nb);
+  DevBuf<int32_t> len;
+  for (int b = 0; b < nb; ++b) {
+    row_lengths(len, d.cb.blk[b].rp.get(), nullptr, rows, st);
+    build_schedule(d.sch[b], len.get(), rows, false, st);
+  }
+  RB_CUDA(cudaStreamSynchronize(st));
+}
+
+void build_colblocked_primal(ColBlockedPrimal& p, int nq, int na, const int32_t* rpq, const int32_t* ciq,
+                             const double* qvals, const int32_t* rpat, const int32_t* ciat, const double* atvals,
+                             int32_t rows, int32_t n, int32_t m, cudaStream_t st) {
+  p = ColBlockedPrimal{};
+  if ((nq < 2 && na < 2) || rows <= 0) return;
+  p.on = true;
+  p.rows = rows;
+  DevBuf<int32_t> len;
+  if (nq >= 2) {
+    build_colblocks(p.q, nq, rpq, ciq, rows, n, st);
+    fill_colblock_values(p.q, qvals, st);
+    p.part_q.alloc(static_cast<std::size_t>(nq - 1) * rows);
+    p.sch_q.resize(nq - 1);
+    for (int b = 0; b + 1 < nq; ++b) {
+      row_lengths(len, p.q.blk[b].rp.get(), nullptr, rows, st);
+      build_schedule(p.sch_q[b], len.get(), rows, false, st);
+    }
+  }
+  p.at_all_partial = nq >= 2;
+  if (na >= 2) {
+    build_colblocks(p.at, na, rpat, ciat, rows, m, st);
+    fill_colblock_values(p.at, atvals, st);
+  }
+  const int npa = p.at_all_partial ? std::max(na, 1) : na - 1;
+  if (npa > 0) {
+    p.part_at.alloc(static_cast<std::size_t>(npa) * rows);
+    p.sch_at.resize(npa);
+    for (int b = 0; b < npa; ++b) {
+      row_lengths(len, na >= 2 ? p.at.blk[b].rp.get() : rpat, nullptr, rows, st);
+      build_schedule(p.sch_at[b], len.get(), rows, false, st);
+    }
+  }
+  if (p.at_all_partial) {
+    p.zero_rp.alloc(static_cast<std::size_t>(rows) + 1);
+    p.zero_rp.zero(st);
+  }
+  row_lengths(len, nq >= 2 ? p.q.blk[nq - 1].rp.get() : rpq,
+              p.at_all_partial ? p.zero_rp.get() : na >= 2 ? p.at.blk[na - 1].rp.get() : rpat, rows, st);
+  build_schedule(p.fin, len.get(), rows, false, st);
+  RB_CUDA(cudaStreamSynchronize(st));
+}
+
 }  // namespace rb

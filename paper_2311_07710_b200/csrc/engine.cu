@@ -446,70 +446,17 @@ void dump_slab_profile(const char* name, const SlabView& v) {
 
 void Engine::setup_colblocks() {
   DeviceQP& P = *P_;
-  DevBuf<int32_t> len;
   auto local = [&](const DevCsr& m) {
     return pattern_locality(m.rp.get(), m.ci.get(), m.rows, m.cols, m.nnz, st_) >= 0.5;
   };
-  if (!dual_ph_.active()) {
-    const int nb = colblock_count(n_);
-    if (nb >= 2 && !local(P.A)) {
-      build_colblocks(cb_dual_, nb, P.A.rp.get(), P.A.ci.get(), m_, n_, st_);
-      fill_colblock_values(cb_dual_, asv_, st_);
-      part_dual_.alloc(static_cast<std::size_t>(nb - 1) * m_);
-      sch_cb_dual_.resize(nb);
-      for (int b = 0; b < nb; ++b) {
-        row_lengths(len, cb_dual_.blk[b].rp.get(), nullptr, m_, st_);
-        build_schedule(sch_cb_dual_[b], len.get(), m_, false, st_);
-      }
-    }
-  }
+  if (!dual_ph_.active() && colblock_count(n_) >= 2 && !local(P.A)) cb_nb_dual_ = colblock_count(n_);
   if (!primal_ph_.active()) {
-    const int nq = colblock_count(n_) >= 2 && !local(P.Q) ? colblock_count(n_) : 1;
-    const int na = colblock_count(m_) >= 2 && !local(P.AT) ? colblock_count(m_) : 1;
-    if (nq >= 2) {
-      build_colblocks(cb_q_, nq, P.Q.rp.get(), P.Q.ci.get(), n_, n_, st_);
-      fill_colblock_values(cb_q_, qsv_, st_);
-      part_q_.alloc(static_cast<std::size_t>(nq - 1) * n_);
-      sch_cb_q_.resize(nq - 1);
-      for (int b = 0; b + 1 < nq; ++b) {
-        row_lengths(len, cb_q_.blk[b].rp.get(), nullptr, n_, st_);
-        build_schedule(sch_cb_q_[b], len.get(), n_, false, st_);
-      }
-    }
-    // With Q blocked, A'y runs as partial passes too (all its blocks), so the
-    // last pass gathers from one L2-sized block only.
-    at_all_partial_ = nq >= 2;
-    if (at_all_partial_ && na < 2) {
-      sch_cb_at_.resize(1);
-      row_lengths(len, P.AT.rp.get(), nullptr, n_, st_);
-      build_schedule(sch_cb_at_[0], len.get(), n_, false, st_);
-      part_at_.alloc(n_);
-      zero_rp_.alloc(n_ + 1);
-      zero_rp_.zero(st_);
-    }
-    if (na >= 2) {
-      build_colblocks(cb_at_, na, P.AT.rp.get(), P.AT.ci.get(), n_, m_, st_);
-      fill_colblock_values(cb_at_, atsv_, st_);
-      const int np = at_all_partial_ ? na : na - 1;
-      part_at_.alloc(static_cast<std::size_t>(np) * n_);
-      sch_cb_at_.resize(np);
-      if (at_all_partial_) {
-        zero_rp_.alloc(n_ + 1);
-        zero_rp_.zero(st_);
-      }
-      for (int b = 0; b < np; ++b) {
-        row_lengths(len, cb_at_.blk[b].rp.get(), nullptr, n_, st_);
-        build_schedule(sch_cb_at_[b], len.get(), n_, false, st_);
-      }
-    }
-    if (nq >= 2 || na >= 2) {
-      row_lengths(len, nq >= 2 ? cb_q_.blk[nq - 1].rp.get() : P.Q.rp.get(),
-                  at_all_partial_ ? zero_rp_.get() : na >= 2 ? cb_at_.blk[na - 1].rp.get() : P.AT.rp.get(), n_,
-                  st_);
-      build_schedule(sch_cb_primal_, len.get(), n_, false, st_);
-    }
+    if (colblock_count(n_) >= 2 && !local(P.Q)) cb_nq_ = colblock_count(n_);
+    if (colblock_count(m_) >= 2 && !local(P.AT)) cb_na_ = colblock_count(m_);
   }
-  RB_CUDA(cudaStreamSynchronize(st_));
+  build_colblocked_dual(cbd_, cb_nb_dual_, P.A.rp.get(), P.A.ci.get(), m_, n_, asv_, st_);
+  build_colblocked_primal(cbp_, cb_nq_, cb_na_, P.Q.rp.get(), P.Q.ci.get(), qsv_, P.AT.rp.get(), P.AT.ci.get(), atsv_,
+                          n_, n_, m_, st_);
 }
 
 void Engine::setup_slabs() {
@@ -585,16 +532,8 @@ void Engine::launch_chunk_body(int len, int cur, bool prof) {
       DualStepOp<false> d{P_->A.view(asv_), w_.get(), bsv_, y_.get(), yb_.get(), mi_, params_.get(), it, bad_.get()};
       if (dual_ph_.active()) {
         launches_ += launch_slab_phase(d, dual_ph_, st_);
-      } else if (cb_dual_.active()) {
-        const int nb = cb_dual_.nb;
-        for (int b = 0; b + 1 < nb; ++b) {
-          const SpmvOp<false> sp{cb_dual_.blk[b].view(), w_.get(), part_dual_.get() + static_cast<int64_t>(b) * m_};
-          rowwise(sp, sch_cb_dual_[b], st_, &launches_);
-        }
-        const DualStepOp<false> dl{cb_dual_.blk[nb - 1].view(), w_.get(), bsv_, y_.get(), yb_.get(), mi_,
-                                   params_.get(), it, bad_.get()};
-        rowwise(PartialsOp<DualStepOp<false>>{dl, part_dual_.get(), nullptr, nb - 1, 0, m_}, sch_cb_dual_[nb - 1],
-                st_, &launches_);
+      } else if (cbd_.active()) {
+        launches_ += launch_colblocked_dual(d, cbd_, st_);
       } else {
         rowwise(d, P_->sch_dual, st_, &launches_);
       }
@@ -609,25 +548,8 @@ void Engine::launch_chunk_body(int len, int cur, bool prof) {
                              X_[c ^ 1].get(), xb_.get(), csv_, w_.get(), XMD_[c ^ 1].get(), params_.get(), it, bad_.get()};
       if (primal_ph_.active()) {
         launches_ += launch_slab_phase(pr, primal_ph_, st_);
-      } else if (cb_q_.active() || cb_at_.active()) {
-        const int nq = cb_q_.nb, na = cb_at_.nb;
-        for (int b = 0; b + 1 < nq && cb_q_.active(); ++b) {
-          const SpmvOp<false> sp{cb_q_.blk[b].view(), XMD_[c].get(), part_q_.get() + static_cast<int64_t>(b) * n_};
-          rowwise(sp, sch_cb_q_[b], st_, &launches_);
-        }
-        const int npa = static_cast<int>(sch_cb_at_.size());  // A'y partial passes
-        for (int b = 0; b < npa; ++b) {
-          const CsrView at = cb_at_.active() ? cb_at_.blk[b].view() : P_->AT.view(atsv_);
-          const SpmvOp<false> sp{at, y_.get(), part_at_.get() + static_cast<int64_t>(b) * n_};
-          rowwise(sp, sch_cb_at_[b], st_, &launches_);
-        }
-        PrimalStepOp<false> pl = pr;
-        if (cb_q_.active()) pl.q = cb_q_.blk[nq - 1].view();
-        if (at_all_partial_) pl.at = CsrView{zero_rp_.get(), P_->AT.ci.get(), atsv_};
-        else if (cb_at_.active()) pl.at = cb_at_.blk[na - 1].view();
-        rowwise(PartialsOp<PrimalStepOp<false>>{pl, part_q_.get(), part_at_.get(), cb_q_.active() ? nq - 1 : 0, npa,
-                                                n_},
-                sch_cb_primal_, st_, &launches_);
+      } else if (cbp_.active()) {
+        launches_ += launch_colblocked_primal(pr, cbp_, st_);
       } else {
         rowwise(pr, P_->sch_primal, st_, &launches_);
       }

@@ -193,12 +193,10 @@ class Engine : public LoopBackend {
   SlabPhase dual_ph_, primal_ph_;
   // L2-sized column blocks (colblock.cuh) of the gather-bound ops without a slab plan
   void setup_colblocks();
-  ColBlocks cb_dual_, cb_q_, cb_at_;
-  DevBuf<double> part_dual_, part_q_, part_at_;
-  std::vector<Schedule> sch_cb_dual_, sch_cb_q_, sch_cb_at_;
-  Schedule sch_cb_primal_;
-  bool at_all_partial_ = false;  // A'y entirely in partial passes (Q blocked)
-  DevBuf<int32_t> zero_rp_;      // empty CSR rows
+  int cb_nb_dual_ = 1, cb_nq_ = 1, cb_na_ = 1;  // block counts (global: shards reuse them)
+  ColBlockedDual cbd_;
+  ColBlockedPrimal cbp_;
+
   std::map<int, cudaGraphExec_t> graphs_;  // key: len, parity, profiled
   std::map<int, int64_t> graph_launches_;
   int64_t chunk_counter_ = 0;

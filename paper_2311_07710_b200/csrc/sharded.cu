@@ -197,6 +197,8 @@ struct ShardedEngine::Shard {
   // slab plans restricted to the owned rows, built from the GLOBAL window
   // choice so every row is computed as on one GPU; + complement schedules
   SlabPhase dual_ph, primal_ph;
+  ColBlockedDual cbd;  // column blocks over the owned rows (same block counts as one GPU)
+  ColBlockedPrimal cbp;
   // full-length copies; only the owned slice is computed here, the rest is
   // received by the exchanges
   DevBuf<double> X[2], XMD[2], w, xb, y, yb, epx, epy, xu[2], yu[2], ax[2], qx[2], aty[2], best_x, best_y;
@@ -243,6 +245,13 @@ ShardedEngine::ShardedEngine(const rapdhg_qp& p, const rapdhg_config& cfg, int p
         assign_slab_ctas(sh->primal_ph.plan, prepare_slab<PrimalStepOp<false>>(sh->primal_ph.plan.view.smem_bytes()), st_);
       }
     }
+    if (!sh->dual_ph.active() && sh->d1 > sh->d0)
+      build_colblocked_dual(sh->cbd, full_->cb_nb_dual_, P.A.rp.get() + sh->d0, P.A.ci.get(),
+                            static_cast<int32_t>(sh->d1 - sh->d0), n, full_->asv_, st_);
+    if (!sh->primal_ph.active() && sh->p1 > sh->p0)
+      build_colblocked_primal(sh->cbp, full_->cb_nq_, full_->cb_na_, P.Q.rp.get() + sh->p0, P.Q.ci.get(), full_->qsv_,
+                              P.AT.rp.get() + sh->p0, P.AT.ci.get(), full_->atsv_,
+                              static_cast<int32_t>(sh->p1 - sh->p0), n, m, st_);
     for (int i = 0; i < 2; ++i) {
       sh->X[i].alloc(n), sh->XMD[i].alloc(n), sh->xu[i].alloc(n), sh->yu[i].alloc(m);
       sh->ax[i].alloc(m), sh->qx[i].alloc(n), sh->aty[i].alloc(n);
@@ -347,6 +356,8 @@ void ShardedEngine::body(int len, int cur) {
                           params_.get(), it, sh->bad.get()};
       if (sh->dual_ph.active()) {
         launches_ += launch_slab_phase(d, sh->dual_ph, st_);
+      } else if (sh->cbd.active()) {
+        launches_ += launch_colblocked_dual(d, sh->cbd, st_);
       } else {
         launch_rowwise(d, sh->sch_dual.view, st_);
         ++launches_;
@@ -363,6 +374,8 @@ void ShardedEngine::body(int len, int cur) {
                              params_.get(), it, sh->bad.get()};
       if (sh->primal_ph.active()) {
         launches_ += launch_slab_phase(pr, sh->primal_ph, st_);
+      } else if (sh->cbp.active()) {
+        launches_ += launch_colblocked_primal(pr, sh->cbp, st_);
       } else {
         launch_rowwise(pr, sh->sch_primal.view, st_);
         ++launches_;

@@ -62,3 +62,13 @@ def test_colblock_q_only(O, monkeypatch):
     p = random_qp(11, n=900, mi=300, me=60, dens=0.08)
     a, b, agree = _fast_vs_ref(O, p, dict(tol=1e-12), 400)
     assert agree >= 4
+
+
+@pytest.mark.parametrize("parts", [2, 3])
+@pytest.mark.parametrize("kb", ["1", "4"])
+def test_colblock_sharded_bit_identical(parts, kb, monkeypatch):
+    monkeypatch.setenv("RAPDHG_SLAB", "off")
+    monkeypatch.setenv("RAPDHG_L2BLOCK_KB", kb)
+    p = random_qp(13, n=900, mi=300, me=60, dens=0.08)
+    cfg = rb.SolverConfig(tol=1e-8, max_iters=600, snapshot_interval=80)
+    assert_results_identical(rb.solve_sharded(p, cfg, parts), rb.solve(p, cfg))

@@ -3,6 +3,14 @@
 // cores are involved (nothing on this path is a dense contraction).
 #pragma once
 
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <mutex>
+#include <utility>
+#include <vector>
+#include <cstdlib>
+
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -33,6 +41,47 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 #define RB_LAUNCH_CHECK() ::rb::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
 
 // Owning device allocation (cudaMalloc'd, freed on destruction). Not copyable.
+// Device memory comes from the device's default stream-ordered pool, which
+// keeps freed memory (release threshold: unlimited), so repeated solves do not
+// pay cudaMalloc/cudaFree (tens of ms each on large buffers). Allocation and
+// free are ordered on the legacy default stream, which every solver stream
+// (blocking streams) synchronises with. RAPDHG_POOL=0: plain cudaMalloc/Free.
+inline bool pool_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("RAPDHG_POOL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+inline void pool_prepare() {
+  static std::atomic<unsigned long long> done{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return;
+  const unsigned long long bit = 1ull << dev;
+  if (done.load() & bit) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    unsigned long long keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done.fetch_or(bit);
+}
+inline void* dev_alloc(std::size_t bytes) {
+  void* p = nullptr;
+  if (pool_enabled()) {
+    pool_prepare();
+    RB_CUDA(cudaMallocAsync(&p, bytes, cudaStreamLegacy));
+  } else {
+    RB_CUDA(cudaMalloc(&p, bytes));
+  }
+  return p;
+}
+inline void dev_free(void* p) {
+  if (!p) return;
+  if (pool_enabled()) cudaFreeAsync(p, cudaStreamLegacy);
+  else cudaFree(p);
+}
+
 template <typename T>
 class DevBuf {
  public:
@@ -54,10 +103,10 @@ class DevBuf {
     reset();
     n_ = n;
     // always allocate at least one element so pointers are valid for empty sets
-    RB_CUDA(cudaMalloc(&p_, sizeof(T) * (n ? n : 1)));
+    p_ = static_cast<T*>(dev_alloc(sizeof(T) * (n ? n : 1)));
   }
   void reset() {
-    if (p_) cudaFree(p_);
+    dev_free(p_);
     p_ = nullptr;
     n_ = 0;
   }
@@ -77,18 +126,58 @@ class DevBuf {
 };
 
 // Pinned host staging buffer.
+// Page-locked host blocks are expensive to create (cudaMallocHost pins pages:
+// milliseconds), so released blocks are cached for reuse (same size class:
+// next power of two >= 4 KB).
+struct PinnedCache {
+  std::mutex mu;
+  std::vector<std::pair<std::size_t, void*>> free;
+  ~PinnedCache() = default;  // process exit releases the pages
+};
+inline PinnedCache& pinned_cache() {
+  static PinnedCache* c = new PinnedCache();  // never destroyed (outlives static buffers)
+  return *c;
+}
+inline std::size_t pinned_class(std::size_t bytes) {
+  std::size_t c = 4096;
+  while (c < bytes) c <<= 1;
+  return c;
+}
+inline void* pinned_acquire(std::size_t bytes) {
+  const std::size_t cls = pinned_class(bytes);
+  PinnedCache& pc = pinned_cache();
+  {
+    std::lock_guard<std::mutex> g(pc.mu);
+    for (std::size_t i = 0; i < pc.free.size(); ++i)
+      if (pc.free[i].first == cls) {
+        void* p = pc.free[i].second;
+        pc.free[i] = pc.free.back();
+        pc.free.pop_back();
+        return p;
+      }
+  }
+  void* p = nullptr;
+  RB_CUDA(cudaMallocHost(&p, cls));
+  return p;
+}
+inline void pinned_release(void* p, std::size_t bytes) {
+  if (!p) return;
+  PinnedCache& pc = pinned_cache();
+  std::lock_guard<std::mutex> g(pc.mu);
+  pc.free.emplace_back(pinned_class(bytes), p);
+}
+
 template <typename T>
 class PinnedBuf {
  public:
   PinnedBuf() = default;
-  ~PinnedBuf() {
-    if (p_) cudaFreeHost(p_);
-  }
+  ~PinnedBuf() { pinned_release(p_, bytes_); }
   PinnedBuf(const PinnedBuf&) = delete;
   PinnedBuf& operator=(const PinnedBuf&) = delete;
   void alloc(std::size_t n) {
-    if (p_) cudaFreeHost(p_);
-    RB_CUDA(cudaMallocHost(&p_, sizeof(T) * (n ? n : 1)));
+    pinned_release(p_, bytes_);
+    bytes_ = sizeof(T) * (n ? n : 1);
+    p_ = static_cast<T*>(pinned_acquire(bytes_));
     n_ = n;
   }
   T* get() const { return p_; }
@@ -97,7 +186,25 @@ class PinnedBuf {
 
  private:
   T* p_ = nullptr;
-  std::size_t n_ = 0;
+  std::size_t n_ = 0, bytes_ = 0;
+};
+
+// Phase timer printed to stderr when RAPDHG_TRACE is set (synchronises the
+// stream at each mark, so only for diagnosis).
+struct Tracer {
+  bool on;
+  cudaStream_t st;
+  std::chrono::steady_clock::time_point t;
+  explicit Tracer(cudaStream_t s)
+      : on(std::getenv("RAPDHG_TRACE") != nullptr), st(s), t(std::chrono::steady_clock::now()) {}
+  void mark(const char* what) {
+    if (!on) return;
+    if (st) cudaStreamSynchronize(st);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[rapdhg] %-30s %9.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
 };
 
 constexpr int kSMs = 148;  // B200: 2 dies x 74 SMs

@@ -122,13 +122,16 @@ void DeviceQP::validate_dims(const rapdhg_qp& p) {
 
 DeviceQP::DeviceQP(const rapdhg_qp& p, bool strict_, cudaStream_t st_)
     : st(st_), strict(strict_), n(p.n), mi(p.m_ineq), me(p.m_eq), m(p.m_ineq + p.m_eq) {
+  Tracer tr(st);
   upload_csr(Q, p.q, st);
   DevCsr ai, ae;
   upload_csr(ai, p.a_ineq, st);
   upload_csr(ae, p.a_eq, st);
   stack_csr(A, ai, ae, st);  // WorkingProblem::from (solver.hpp:106-108)
   RB_CUDA(cudaStreamSynchronize(st));
+  tr.mark("  upload + stack");
   transpose_csr(AT, A, &at_perm, st);
+  tr.mark("  transpose");
   c.alloc(n);
   c.upload(p.c, n, st);
   b.alloc(m);
@@ -137,6 +140,7 @@ DeviceQP::DeviceQP(const rapdhg_qp& p, bool strict_, cudaStream_t st_)
   red.init(std::max<int64_t>(n, m), st);
   red_out.alloc(64);
   red_host.alloc(64);
+  tr.mark("  vectors + reduce scratch");
   // schedules (patterns only; shared by original and scaled values)
   DevBuf<int32_t> len;
   row_lengths(len, A.rp.get(), nullptr, A.rows, st);
@@ -152,6 +156,7 @@ DeviceQP::DeviceQP(const rapdhg_qp& p, bool strict_, cudaStream_t st_)
   build_schedule(sch_at, len.get(), n, strict, st);
   choose_windows(sch_at, AT.ci.get(), AT.nnz, m, nullptr, 0, 0, st);
   RB_CUDA(cudaStreamSynchronize(st));
+  tr.mark("  schedules");
 }
 
 void DeviceQP::validate_symmetry() {
@@ -337,23 +342,13 @@ double DeviceQP::op_norm_a(const double* av, const double* atv, int max_iters, d
 // Engine
 // ============================================================================
 
-Tracer::Tracer(cudaStream_t s) : on(std::getenv("RAPDHG_TRACE") != nullptr), st(s), t(Clock::now()) {}
-
-void Tracer::mark(const char* what) {
-  if (!on) return;
-  if (st) cudaStreamSynchronize(st);
-  const auto now = Clock::now();
-  std::fprintf(stderr, "[rapdhg] %-30s %9.3f ms\n", what,
-               std::chrono::duration<double, std::milli>(now - t).count());
-  t = now;
-}
 
 Engine::Engine(const rapdhg_qp& p, const rapdhg_config& cfg, Clock::time_point t0) : cfg_(cfg) {
   Tracer tr(nullptr);
   DeviceQP::validate_dims(p);
   tr.mark("validate dims (host)");
   RB_CUDA(cudaSetDevice(cfg.device));
-  RB_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  RB_CUDA(cudaStreamCreate(&st_));  // blocking: ordered with the pool's legacy-stream allocs/frees
   tr.st = st_;
   tr.mark("device + stream");
   P_ = std::make_unique<DeviceQP>(p, cfg.strict_parity != 0, st_);
@@ -461,6 +456,7 @@ void Engine::setup_colblocks() {
 
 void Engine::setup_slabs() {
   DeviceQP& P = *P_;
+  Tracer tr(st_);
   DevBuf<int32_t> len;
   dual_choice_ = choose_slabs(P.A.rp.get(), P.A.ci.get(), P.A.rows, P.A.nnz, n_, st_);
   row_lengths(len, P.A.rp.get(), nullptr, m_, st_);
@@ -469,6 +465,7 @@ void Engine::setup_slabs() {
     fill_slab_values(dual_ph_.plan, asv_, nullptr, st_);
     assign_slab_ctas(dual_ph_.plan, prepare_slab<DualStepOp<false>>(dual_ph_.plan.view.smem_bytes()), st_);
   }
+  tr.mark("  slab plan: dual");
   primal_choice_ = choose_slabs(P.AT.rp.get(), P.AT.ci.get(), n_, P.AT.nnz, m_, st_);
   row_lengths(len, P.Q.rp.get(), P.AT.rp.get(), n_, st_);
   build_slab_phase(primal_ph_, primal_choice_, 1, P.Q.rp.get(), P.Q.ci.get(), P.AT.rp.get(), P.AT.ci.get(), 0, n_,
@@ -477,6 +474,7 @@ void Engine::setup_slabs() {
     fill_slab_values(primal_ph_.plan, qsv_, atsv_, st_);
     assign_slab_ctas(primal_ph_.plan, prepare_slab<PrimalStepOp<false>>(primal_ph_.plan.view.smem_bytes()), st_);
   }
+  tr.mark("  slab plan: primal");
 #ifdef RB_SLAB_PROFILE
   for (SlabPlan* pl : {&dual_ph_.plan, &primal_ph_.plan})
     if (pl->view.active()) {
@@ -941,7 +939,7 @@ void run_loop(LoopBackend& be, const rapdhg_config& cfg, const LoopScalars& sc, 
 namespace {
 struct StreamGuard {
   cudaStream_t s = nullptr;
-  StreamGuard() { RB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
+  StreamGuard() { RB_CUDA(cudaStreamCreate(&s)); }
   ~StreamGuard() {
     if (s) cudaStreamDestroy(s);
   }

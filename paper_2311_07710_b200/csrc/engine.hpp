@@ -28,16 +28,6 @@ constexpr int kProfilePeriod = 8;  // profile_kernels: time every 8th chunk
 
 using Clock = std::chrono::steady_clock;
 
-// Phase timer printed to stderr when RAPDHG_TRACE is set (synchronises the
-// stream at each mark, so only for diagnosis).
-struct Tracer {
-  bool on;
-  cudaStream_t st;
-  Clock::time_point t;
-  explicit Tracer(cudaStream_t s);
-  void mark(const char* what);
-};
-
 struct Kkt {
   double r_primal = 0.0, r_dual = 0.0, r_gap = 0.0;
   double relkkt() const {

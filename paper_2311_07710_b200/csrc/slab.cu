@@ -5,6 +5,7 @@
 #include <cstdlib>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "slab.cuh"
@@ -75,28 +76,28 @@ __global__ void seg_counts_kernel(const int32_t* rows, int32_t nw, const int32_t
   rest_o[k] = rp_o ? rp_o[r + 1] - rp_o[r] : 0;
 }
 
-// thread per W row: scatter its entries into its slice lanes (run (s, k)
-// starts at off[s * nw + k], entries 32 apart) and into the rest CSRs
+// thread per W row: scatter its entries into its slice lane (run (s, k): tile
+// base off[s * nw + k]; jx = (index of its slice's jagged offsets in joff) *
+// 32 + lane; entry e at base + joff[jx / 32 + e] + lane) and into the rest CSRs
 __global__ void fill_kernel(const int32_t* rows, int32_t nw, const int32_t* rp_w, const int32_t* ci_w,
                             const int32_t* rp_o, const int32_t* ci_o, Wins wins, const int32_t* off,
-                            uint16_t* col, int32_t* pos, const int32_t* rrp_w, int32_t* rci_w, int32_t* rpos_w,
-                            const int32_t* rrp_o, int32_t* rci_o, int32_t* rpos_o) {
+                            const int32_t* jx, const int32_t* joff, uint16_t* col, int32_t* pos,
+                            const int32_t* rrp_w, int32_t* rci_w, int32_t* rpos_w, const int32_t* rrp_o,
+                            int32_t* rci_o, int32_t* rpos_o) {
   const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (k >= nw) return;
   const int r = rows[k];
-  int s = 0;
-  int64_t wp = wins.S > 0 ? off[k] : 0;
+  int s = 0, e = 0;
   int rw = rrp_w[k];
   for (int p = rp_w[r]; p < rp_w[r + 1]; ++p) {
     const int32_t c = ci_w[p];
-    while (s < wins.S && c >= wins.w[s].lo + wins.w[s].len) {
-      ++s;
-      if (s < wins.S) wp = off[static_cast<int64_t>(s) * nw + k];
-    }
+    while (s < wins.S && c >= wins.w[s].lo + wins.w[s].len) ++s, e = 0;
     if (s < wins.S && c >= wins.w[s].lo) {
+      const int64_t run = static_cast<int64_t>(s) * nw + k;
+      const int64_t wp = off[run] + joff[(jx[run] >> 5) + e] + (jx[run] & 31);
       col[wp] = static_cast<uint16_t>(c - wins.w[s].lo);
       pos[wp] = p;
-      wp += 32;
+      ++e;
     } else {
       rci_w[rw] = c;
       rpos_w[rw] = p;
@@ -152,23 +153,70 @@ std::vector<int32_t> scan_host(const std::vector<int32_t>& cnt) {
   return rp;
 }
 
-// Sliced layout of one tile: rows [k0, k1) sorted by run length (descending,
-// stable), 32 per slice, each slice as wide as its longest run.
+// Sliced, jagged layout of one tile: rows [k0, k1) sorted by run length
+// (descending, stable), 32 per slice; slice q stores entry e of its lanes
+// whose run exceeds e contiguously. meta = perm | len | soff (slab.cuh);
+// joff = per slice the start of each entry e (fill_kernel only); offsets are
+// relative to the tile's first entry; n = entries, padded to 8.
 struct TileLayout {
   std::vector<int32_t> order;  // sorted rows (chunk-relative)
-  std::vector<int32_t> soff;   // slice starts (entries), nsl + 1
+  std::vector<uint16_t> meta;
+  std::vector<int32_t> joff;   // slice q's offsets start at joff[sj[q]]
+  std::vector<int32_t> sj;
+  int32_t n = 0;
+  int64_t total = 0;  // entries before the 8-alignment (exact, unclamped)
+  bool fits(int ecap, int mcap) const { return n <= ecap && static_cast<int>(meta.size()) <= mcap; }
 };
-TileLayout layout_tile(const std::vector<int32_t>& c2, int64_t s_base, int32_t k0, int32_t k1) {
+TileLayout layout_tile(const std::vector<int32_t>& c2, int64_t s_base, int32_t k0, int32_t k1, bool jagged) {
   TileLayout L;
   const int32_t nr = k1 - k0;
+  const int32_t* len = c2.data() + s_base + k0;
+  // counting sort by run length, descending, stable (runs <= kSlabRunCap)
+  std::vector<int32_t> start(kSlabRunCap + 2, 0);
+  for (int32_t i = 0; i < nr; ++i) ++start[kSlabRunCap - len[i] + 1];
+  for (int v = 1; v <= kSlabRunCap + 1; ++v) start[v] += start[v - 1];
   L.order.resize(nr);
-  std::iota(L.order.begin(), L.order.end(), 0);
-  std::stable_sort(L.order.begin(), L.order.end(),
-                   [&](int32_t a, int32_t b) { return c2[s_base + k0 + a] > c2[s_base + k0 + b]; });
+  for (int32_t i = 0; i < nr; ++i) L.order[start[kSlabRunCap - len[i]]++] = i;
   const int nsl = (nr + 31) / 32;
-  L.soff.assign(nsl + 1, 0);
-  for (int q = 0; q < nsl; ++q) L.soff[q + 1] = L.soff[q] + 32 * c2[s_base + k0 + L.order[32 * q]];
+  L.meta.resize(2 * static_cast<std::size_t>(nr) + nsl + 1);
+  for (int32_t i = 0; i < nr; ++i) {
+    L.meta[i] = static_cast<uint16_t>(L.order[i]);
+    L.meta[nr + i] = static_cast<uint16_t>(len[L.order[i]]);
+  }
+  int64_t cur = 0;
+  for (int q = 0; q < nsl; ++q) {
+    L.meta[2 * nr + q] = static_cast<uint16_t>(std::min<int64_t>(cur, 65535));  // soff[q]
+    L.sj.push_back(static_cast<int32_t>(L.joff.size()));
+    const int lanes = std::min(32, nr - 32 * q);
+    const int Lm = len[L.order[32 * q]];
+    int cnt = lanes;  // lanes with a run longer than e (runs are sorted)
+    for (int e = 0; e < Lm; ++e) {
+      while (cnt > 0 && len[L.order[32 * q + cnt - 1]] <= e) --cnt;
+      L.joff.push_back(static_cast<int32_t>(cur));
+      cur += jagged ? cnt : 32;
+    }
+  }
+  L.meta[2 * nr + nsl] = static_cast<uint16_t>(std::min<int64_t>(cur, 65535));
+  L.total = cur;
+  L.n = static_cast<int32_t>((cur + 7) & ~int64_t{7});
+  if (cur > 65535) L.n = INT32_MAX;  // 16-bit offsets overflow: split
   return L;
+}
+
+// f(0 .. n-1) on up to 16 host threads
+template <class F>
+void parallel_for(int64_t n, const F& f) {
+  const int T = static_cast<int>(std::min<int64_t>(n, std::max(1u, std::min(16u, std::thread::hardware_concurrency()))));
+  if (T <= 1) {
+    for (int64_t i = 0; i < n; ++i) f(i);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int t = 0; t < T; ++t)
+    th.emplace_back([&, t] {
+      for (int64_t i = t; i < n; i += T) f(i);
+    });
+  for (auto& x : th) x.join();
 }
 
 }  // namespace
@@ -219,6 +267,7 @@ void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const in
   plan = SlabPlan{};
   const int S = static_cast<int>(choice.windows.size());
   if (S == 0 || r1 <= r0) return;
+  Tracer tr(st);
   Wins wins{};
   wins.S = S;
   for (int s = 0; s < S; ++s) wins.w[s] = choice.windows[s];
@@ -248,87 +297,130 @@ void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const in
   seg_counts_kernel<<<g1(nw), 256, 0, st>>>(plan.rows.get(), nw, rp_w, ci_w, rp_o, wins, c2.get(), rw.get(), ro.get());
   RB_LAUNCH_CHECK();
   const std::vector<int32_t> hc2 = download(c2, runs, st), hrw = download(rw, nw, st), hro = download(ro, nw, st);
-  // Row chunks: greedy on entries (3/4 of the capacity, leaving room for the
-  // slice padding) and rows; chunks whose padded tiles still overflow are
-  // halved; then split further until there are enough tiles for every CTA.
-  const int ecap = (std::min(32736, std::max(256, env_int("RAPDHG_SLAB_TILE", kSlabTileCap))) + 31) & ~31;
+  tr.mark("    counts");
+  // Row chunks: whole slices (multiples of 32 rows), grown while every
+  // window's entries stay under 7/8 of the capacity; split further until there
+  // are enough tiles for every CTA; a chunk whose padded tile still overflows
+  // is halved (at a multiple of 32) and laid out again.
+  const int ecap = (std::min(32736, std::max(256, env_int("RAPDHG_SLAB_TILE", kSlabTileCap))) + 7) & ~7;
   const int rcap = kSlabRowCap;
   std::vector<int32_t> chunk{0};
   {
-    std::vector<int64_t> cur(S, 0);
-    for (int32_t k = 0; k < nw; ++k) {
-      bool fits = k - chunk.back() + 1 <= rcap;
-      for (int s = 0; s < S && fits; ++s) fits = cur[s] + hc2[static_cast<int64_t>(s) * nw + k] <= ecap * 3 / 4;
+    std::vector<int64_t> cur(S, 0), add(S, 0);
+    for (int32_t k = 0; k < nw;) {
+      const int32_t g = std::min(nw, k + 32);
+      for (int s = 0; s < S; ++s) {
+        add[s] = 0;
+        for (int32_t q = k; q < g; ++q) add[s] += hc2[static_cast<int64_t>(s) * nw + q];
+      }
+      bool fits = g - chunk.back() <= rcap;
+      for (int s = 0; s < S && fits; ++s) fits = cur[s] + add[s] <= ecap * 7 / 8;
       if (!fits && k > chunk.back()) {
         chunk.push_back(k);
         std::fill(cur.begin(), cur.end(), 0);
       }
-      for (int s = 0; s < S; ++s) cur[s] += hc2[static_cast<int64_t>(s) * nw + k];
+      for (int s = 0; s < S; ++s) cur[s] += add[s];
+      k = g;
     }
     chunk.push_back(nw);
   }
-  auto padded_ok = [&](int32_t k0, int32_t k1) {
-    for (int s = 0; s < S; ++s)
-      if (layout_tile(hc2, static_cast<int64_t>(s) * nw, k0, k1).soff.back() > ecap) return false;
-    return true;
-  };
-  for (std::size_t c = 0; c + 1 < chunk.size();) {
-    if (chunk[c + 1] - chunk[c] > 1 && !padded_ok(chunk[c], chunk[c + 1]))
-      chunk.insert(chunk.begin() + c + 1, (chunk[c] + chunk[c + 1]) / 2);
-    else
-      ++c;
-  }
+  auto split_at = [](int32_t a, int32_t b) { return a + std::max<int32_t>(32, ((b - a) / 2) & ~31); };
   {
     const int64_t want = ceil_div(static_cast<int64_t>(4 * kSMs), S);
     while (static_cast<int64_t>(chunk.size()) - 1 < want) {  // halve the widest chunk
       std::size_t best = 0;
       for (std::size_t c = 1; c + 1 < chunk.size(); ++c)
         if (chunk[c + 1] - chunk[c] > chunk[best + 1] - chunk[best]) best = c;
-      if (chunk[best + 1] - chunk[best] < 64) break;
-      chunk.insert(chunk.begin() + best + 1, (chunk[best] + chunk[best + 1]) / 2);
+      if (chunk[best + 1] - chunk[best] < 128) break;
+      chunk.insert(chunk.begin() + best + 1, split_at(chunk[best], chunk[best + 1]));
     }
   }
+  // padded (32-wide slices) or jagged: padded unless padding would exceed
+  // kSlabJaggedPad (RAPDHG_SLAB_JAGGED=0/1 forces)
+  bool jagged = false;
+  {
+    int64_t actual = 0, padded = 0;
+    const int32_t Jc = static_cast<int32_t>(chunk.size()) - 1;
+    std::vector<int64_t> pad_t(static_cast<std::size_t>(S) * Jc, 0), act_t(pad_t.size(), 0);
+    parallel_for(static_cast<int64_t>(S) * Jc, [&](int64_t t) {
+      const int s = static_cast<int>(t / Jc), j = static_cast<int>(t % Jc);
+      const TileLayout L = layout_tile(hc2, static_cast<int64_t>(s) * nw, chunk[j], chunk[j + 1], false);
+      pad_t[t] = L.total;
+      for (int32_t k = chunk[j]; k < chunk[j + 1]; ++k) act_t[t] += hc2[static_cast<int64_t>(s) * nw + k];
+    });
+    for (std::size_t t = 0; t < pad_t.size(); ++t) padded += pad_t[t], actual += act_t[t];
+    jagged = static_cast<double>(padded) > kSlabJaggedPad * static_cast<double>(std::max<int64_t>(actual, 1));
+    const int force = env_int("RAPDHG_SLAB_JAGGED", -1);
+    if (force >= 0) jagged = force != 0;
+  }
+  // layouts of every (window, chunk) tile, on host threads; overflowing chunks split
+  std::vector<TileLayout> lay;
+  for (;;) {
+    const int32_t Jc = static_cast<int32_t>(chunk.size()) - 1;
+    lay.assign(static_cast<std::size_t>(S) * Jc, TileLayout{});
+    parallel_for(static_cast<int64_t>(S) * Jc, [&](int64_t t) {
+      const int s = static_cast<int>(t / Jc), j = static_cast<int>(t % Jc);
+      lay[t] = layout_tile(hc2, static_cast<int64_t>(s) * nw, chunk[j], chunk[j + 1], jagged);
+    });
+    std::vector<int32_t> bad;
+    for (int32_t j = 0; j < Jc; ++j)
+      for (int s = 0; s < S; ++s)
+        if (!lay[static_cast<std::size_t>(s) * Jc + j].fits(ecap, kSlabMetaCap) && chunk[j + 1] - chunk[j] > 32) {
+          bad.push_back(j);
+          break;
+        }
+    if (bad.empty()) break;
+    for (auto it = bad.rbegin(); it != bad.rend(); ++it)
+      chunk.insert(chunk.begin() + *it + 1, split_at(chunk[*it], chunk[*it + 1]));
+  }
   const int32_t J = static_cast<int32_t>(chunk.size()) - 1;
-  // Tiles: window-major storage, each tile 32-entry aligned; run (s, k) starts
-  // at off[s * nw + k] (its lane in its slice), entries 32 apart.
-  std::vector<int32_t> off(runs, 0);
+  tr.mark("    chunks + layouts");
+  // Tiles: window-major storage, each tile 8-entry aligned; run (s, k): tile
+  // base off[s * nw + k] and jx[s * nw + k] (see fill_kernel).
+  std::vector<int32_t> off(runs, 0), jx(runs, 0), joff;
   std::vector<SlabTile> tiles(static_cast<std::size_t>(S) * J);
   std::vector<uint16_t> meta;
   int64_t cursor = 0;
-  int max_tile = 0;
+  int max_tile = 0, max_meta = 0;
   for (int s = 0; s < S; ++s)
     for (int32_t j = 0; j < J; ++j) {
       const int32_t k0 = chunk[j], k1 = chunk[j + 1], n_r = k1 - k0;
-      const TileLayout L = layout_tile(hc2, static_cast<int64_t>(s) * nw, k0, k1);
+      const TileLayout& L = lay[static_cast<std::size_t>(s) * J + j];
       SlabTile& d = tiles[static_cast<std::size_t>(s) * J + j];
       d.a = static_cast<int32_t>(cursor);
-      d.n = L.soff.back();
+      d.n = L.n;
       d.meta = static_cast<int32_t>(meta.size());
       d.k0 = k0;
       d.nr = n_r;
       d.s = s;
+      d.m = static_cast<int32_t>(L.meta.size());
       max_tile = std::max(max_tile, d.n);
+      max_meta = std::max(max_meta, d.m);
       // staged bytes + a fixed per-tile cost (barrier round trip, descriptor)
-      plan.tile_bytes.push_back(10 * static_cast<int64_t>(d.n) + 4 * static_cast<int64_t>(n_r) + 16384);
+      plan.tile_bytes.push_back(10 * static_cast<int64_t>(d.n) + 2 * static_cast<int64_t>(d.m) + 16384);
+      const int64_t j0 = static_cast<int64_t>(joff.size());
       for (int32_t slot = 0; slot < n_r; ++slot) {
-        const int32_t k = k0 + L.order[slot];
-        off[static_cast<int64_t>(s) * nw + k] = static_cast<int32_t>(cursor + L.soff[slot / 32] + slot % 32);
+        const int64_t run = static_cast<int64_t>(s) * nw + k0 + L.order[slot];
+        off[run] = static_cast<int32_t>(cursor);
+        jx[run] = static_cast<int32_t>((j0 + L.sj[slot / 32]) * 32 + slot % 32);
       }
-      for (int32_t slot = 0; slot < n_r; ++slot) meta.push_back(static_cast<uint16_t>(L.order[slot]));
-      for (int32_t slot = 0; slot < n_r; ++slot)
-        meta.push_back(static_cast<uint16_t>(hc2[static_cast<int64_t>(s) * nw + k0 + L.order[slot]]));
-      for (int32_t v : L.soff) meta.push_back(static_cast<uint16_t>(v));
+      joff.insert(joff.end(), L.joff.begin(), L.joff.end());
+      meta.insert(meta.end(), L.meta.begin(), L.meta.end());
       meta.resize((meta.size() + 7) & ~std::size_t{7}, 0);
       cursor += d.n;
     }
-  if (cursor > INT32_MAX || max_tile > ecap) {  // offsets are int32; tiles must fit a stage
+  if (cursor > INT32_MAX || max_tile > ecap || max_meta > kSlabMetaCap ||
+      static_cast<int64_t>(joff.size()) * 32 > INT32_MAX) {  // int32 offsets; tiles must fit a stage
     plan = SlabPlan{};
     return;
   }
+  tr.mark("    tile arrays");
   meta.resize(meta.size() + 8, 0);  // slack: a tile's metadata copy rounds up to 8
   const int64_t total = std::max<int64_t>(cursor, 32);
-  DevBuf<int32_t> doff(runs);
+  DevBuf<int32_t> doff(runs), djx(runs), djoff(joff.size());
   doff.upload(off.data(), runs, st);
+  djx.upload(jx.data(), runs, st);
+  djoff.upload(joff.data(), joff.size(), st);
   plan.tile.alloc(tiles.size());
   plan.tile.upload(tiles.data(), tiles.size(), st);
   plan.meta.alloc(meta.size());
@@ -350,10 +442,11 @@ void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const in
   rci_w.alloc(rrw[nw]), rpos_w.alloc(rrw[nw]), rci_o.alloc(rro[nw]), rpos_o.alloc(rro[nw]);
   (seg == 0 ? plan.rval1 : plan.rval2).alloc(rrw[nw]);
   (seg == 0 ? plan.rval2 : plan.rval1).alloc(rro[nw]);
-  fill_kernel<<<g1(nw), 256, 0, st>>>(plan.rows.get(), nw, rp_w, ci_w, rp_o, ci_o, wins, doff.get(), plan.col.get(),
-                                      plan.pos.get(), rrp_w.get(), rci_w.get(), rpos_w.get(),
+  fill_kernel<<<g1(nw), 256, 0, st>>>(plan.rows.get(), nw, rp_w, ci_w, rp_o, ci_o, wins, doff.get(), djx.get(),
+                                      djoff.get(), plan.col.get(), plan.pos.get(), rrp_w.get(), rci_w.get(), rpos_w.get(),
                                       rp_o ? rrp_o.get() : nullptr, rci_o.get(), rpos_o.get());
   RB_LAUNCH_CHECK();
+  tr.mark("    upload + fill");
   plan.partial.alloc(runs);
   {
     std::vector<int32_t> widx(nr, -1);
@@ -367,7 +460,8 @@ void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const in
   v.J = J;
   v.seg = seg;
   v.ecap = ecap;
-  v.mcap = (slab_meta_len(rcap) + 7) & ~7;
+  v.mcap = kSlabMetaCap;
+  v.jagged = jagged ? 1 : 0;
   v.win_max = 0;
   for (int s = 0; s < S; ++s) {
     v.win[s] = choice.windows[s];
@@ -384,13 +478,14 @@ void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const in
   v.rest2 = CsrView{plan.rrp2.get(), plan.rci2.get(), plan.rval2.get()};
   RB_CUDA(cudaStreamSynchronize(st));
   if (std::getenv("RAPDHG_TRACE"))
-    std::fprintf(stderr, "[slab] seg %d rows [%d,%d): W rows %d windows %d chunks %d tiles %d entries %lld (%.3f padded)\n",
+    std::fprintf(stderr, "[slab] seg %d rows [%d,%d): W rows %d windows %d chunks %d tiles %d entries %lld (%.3f padded, %s)\n",
                  seg, r0, r1, nw, S, J, S * J, static_cast<long long>(cursor),
                  static_cast<double>(cursor) / std::max<int64_t>(1, [&] {
                    int64_t t = 0;
                    for (int32_t c : hc2) t += c;
                    return t;
-                 }()));
+                 }()),
+                 jagged ? "jagged" : "sliced");
 }
 
 void fill_slab_values(SlabPlan& plan, const double* v1, const double* v2, cudaStream_t st) {

@@ -15,9 +15,10 @@
 // are cut into chunks so that each (chunk j, window s) tile fits one shared-
 // memory stage. Inside a tile the chunk's rows are sorted by their run length
 // in window s and grouped into slices of 32 rows, one row per lane; a slice
-// stores its entries entry-major (entry e of its 32 rows contiguous; 16-bit
-// column offsets + fp64 values, 10 B/nnz), so a warp reads 32 values and 32
-// columns contiguously and only the window gather is random. Each W row also
+// stores its entries as jagged diagonals (entry e of the rows whose run is
+// longer than e, contiguous; no padding; 16-bit column offsets + fp64 values,
+// 10 B/nnz), so a warp reads its values and columns contiguously and only the
+// window gather is random. Each W row also
 // has a "rest" CSR: its entries outside the windows and its other segment.
 //
 // slab_kernel is persistent (2 CTAs per SM), double-buffered and warp-
@@ -44,7 +45,7 @@ constexpr int kMaxSlabs = 64;
 constexpr int kSlabWidth = 2048;        // columns per window (16 KB of fp64)
 constexpr int kSlabMinRow = 16;         // in-window entries that make a W row
 constexpr double kSlabMinDensity = 16;  // gathers per column that keep a window
-constexpr int kSlabTileCap = 2560;      // padded entries per tile (25 KB staged)
+constexpr int kSlabTileCap = 3072;      // entries per tile (30 KB staged)
 constexpr int kSlabStages = 3;          // tile stages per CTA (one shared window)
 constexpr int kSlabRowCap = 512;        // rows per chunk
 constexpr int kSlabRunCap = 512;        // W rows: every window run and the rest <= this
@@ -52,30 +53,39 @@ constexpr int kSlabMinWindows = 1;     // RAPDHG_SLAB_MIN_WINDOWS overrides
 constexpr int kSlabProf = 10;           // per-CTA profile slots (RB_SLAB_PROFILE)
 
 // tile t = s * J + j (window-major: a CTA's contiguous tile range mostly
-// shares one window, staged once per stage)
+// shares one window, staged once)
 struct SlabTile {
   int32_t a;     // first entry (8-aligned)
-  int32_t n;     // padded entries (multiple of 32)
+  int32_t n;     // entries (multiple of 8; jagged slices carry no padding)
   int32_t meta;  // first metadata element in SlabView::meta (8-aligned)
   int32_t k0;    // first W row of the chunk
   int32_t nr;    // rows of the chunk
   int32_t s;     // window
-  int32_t pad[2];
+  int32_t m;     // metadata elements
+  int32_t pad;
 };
 
 // Per-tile metadata (uint16): perm[nr] (sorted slot -> row of the chunk),
-// len[nr] (run length per sorted slot), soff[nsl + 1] (slice starts).
-__host__ __device__ inline int slab_meta_len(int nr) { return 2 * nr + (nr + 31) / 32 + 1; }
-
+// len[nr] (run length per sorted slot), soff[nsl + 1] (slice starts, entries
+// relative to the tile). Lane l's entry e of slice q sits at
+//   padded: soff[q] + 32 e + l (every slice as wide as its longest run), or
+//   jagged: soff[q] + sum_{e' < e} cnt_e' + l, where entry e of the lanes
+//   whose run is longer than e (lanes 0 .. cnt_e - 1: rows are sorted) is
+//   contiguous and cnt_e = popc(ballot(len > e)) — no padding, no stored
+//   offsets, but unaligned warp rows (more smem wavefronts): chosen per op
+//   when padding would exceed kSlabJaggedPad.
+constexpr double kSlabJaggedPad = 1.25;  // padded/actual entries above which tiles are jagged
+constexpr int kSlabMetaCap = 2 * kSlabRowCap + kSlabRowCap / 32 + 8;  // per tile (multiple of 8)
 struct SlabView {
   int32_t nw = 0;                  // W rows
   int32_t S = 0;                   // windows (even lengths)
   int32_t J = 0;                   // row chunks
   int32_t seg = 0;                 // accumulator the windows feed (0: segment 1, 1: segment 2)
   int32_t win_max = 0;             // widest window (doubles, even)
-  int32_t ecap = 0;                // tile entry capacity (multiple of 32)
+  int32_t ecap = 0;                // tile entry capacity (multiple of 8)
   int32_t mcap = 0;                // tile metadata capacity (multiple of 8)
   int32_t grid = 0;                // persistent CTAs
+  int32_t jagged = 0;              // 1: jagged slices (no padding), 0: 32-wide padded slices
   Window win[kMaxSlabs];
   const SlabTile* tile = nullptr;   // [S * J]
   const int32_t* cta = nullptr;     // [grid + 1] tile ranges per CTA (balanced by bytes)
@@ -192,7 +202,7 @@ __device__ __forceinline__ void slab_issue(const Op& op, const SlabView& sv, con
   double* val = reinterpret_cast<double*>(base + 16);
   uint16_t* col = reinterpret_cast<uint16_t*>(val + sv.ecap);
   uint16_t* meta = col + sv.ecap;
-  const uint32_t m8 = static_cast<uint32_t>(slab_meta_len(d.nr) + 7) & ~7u;
+  const uint32_t m8 = static_cast<uint32_t>(d.m + 7) & ~7u;
   const uint32_t wbytes = copy_window ? static_cast<uint32_t>(w.len) * 8u : 0u;
   hdr[0] = d.k0;
   hdr[1] = d.nr;
@@ -236,7 +246,7 @@ constexpr int kSlabThreads = 32 * (kSlabConsumers + 1);  // + one producer warp
 // stage, take every kSlabConsumers-th slice of it (dealt on a counter that
 // runs across tiles, so the warps share the work evenly without a CTA-wide
 // barrier) and arrive on the stage's empty barrier when done.
-template <class Op>
+template <class Op, bool Jagged>
 __global__ void __launch_bounds__(kSlabThreads) slab_kernel(const Op op, const SlabView sv) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[kSlabStages], empty[kSlabStages];
@@ -303,24 +313,24 @@ __global__ void __launch_bounds__(kSlabThreads) slab_kernel(const Op op, const S
     const int nsl = (nr + 31) >> 5;
     for (int q = (warp - deal + kSlabConsumers) % kSlabConsumers; q < nsl; q += kSlabConsumers) {
       const int slot = (q << 5) + lane;
-      const bool valid = slot < nr;
-      const int L = valid ? len[slot] : 0;
-      const int b = soff[q], Lm = (soff[q + 1] - b) >> 5;  // slice width (its longest run)
-      const double* vq = val + b + lane;
-      const uint16_t* cq = col + b + lane;
+      const int L = slot < nr ? len[slot] : 0;
+      const int Lm = len[q << 5];  // the slice's longest run (lane 0: sorted)
+      int a = soff[q];             // start of entry e's lanes
       double part = 0.0;
       for (int e = 0; e < Lm; e += 4) {
         double v[4], x[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const bool ok = e + u < L;
-          v[u] = ok ? vq[(e + u) << 5] : 0.0;
-          x[u] = ok ? win[cq[(e + u) << 5]] : 0.0;
+          const bool ok = L > e + u;
+          v[u] = ok ? val[a + lane] : 0.0;
+          x[u] = ok ? win[col[a + lane]] : 0.0;
+          if constexpr (Jagged) a += __popc(__ballot_sync(0xffffffffu, ok));
+          else a += 32;
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) part = fma(v[u], x[u], part);
       }
-      if (valid) partial[perm[slot]] = part;
+      if (slot < nr) partial[perm[slot]] = part;
     }
     deal = (deal + nsl) % kSlabConsumers;
     __syncwarp();
@@ -392,9 +402,11 @@ struct SlabFinishOp {
 // capture) and return the persistent grid for that smem size.
 template <class Op>
 inline int prepare_slab(int smem_bytes) {
-  const void* k = reinterpret_cast<const void*>(&slab_kernel<Op>);
-  RB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
-  return slab_grid(k, smem_bytes);
+  const void* k0 = reinterpret_cast<const void*>(&slab_kernel<Op, false>);
+  const void* k1 = reinterpret_cast<const void*>(&slab_kernel<Op, true>);
+  RB_CUDA(cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
+  RB_CUDA(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
+  return slab_grid(k0, smem_bytes);
 }
 
 // A slab-tiled op: the plan and the finish schedule over all of its rows.
@@ -421,7 +433,8 @@ void assign_slab_ctas(SlabPlan& plan, int grid, cudaStream_t st);
 template <class Op>
 inline int launch_slab_phase(const Op& op, const SlabPhase& ph, cudaStream_t st) {
   const SlabView& sv = ph.plan.view;
-  slab_kernel<Op><<<sv.grid, kSlabThreads, sv.smem_bytes(), st>>>(op, sv);
+  if (sv.jagged) slab_kernel<Op, true><<<sv.grid, kSlabThreads, sv.smem_bytes(), st>>>(op, sv);
+  else slab_kernel<Op, false><<<sv.grid, kSlabThreads, sv.smem_bytes(), st>>>(op, sv);
   RB_LAUNCH_CHECK();
   const SchedView& s = ph.fin.view;
   if (s.total_blocks <= 0) return 1;

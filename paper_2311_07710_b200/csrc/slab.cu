@@ -118,14 +118,6 @@ __global__ void gather_kernel(double* dst, const double* src, const int32_t* pos
   if (i < n) dst[i] = pos[i] >= 0 ? src[pos[i]] : 0.0;
 }
 
-__global__ void finish_len_kernel(const int32_t* widx, const int32_t* rrp1, const int32_t* rrp2, int S,
-                                  const int32_t* len, int32_t nr, int32_t* out) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i >= nr) return;
-  const int w = widx[i];
-  out[i] = w < 0 ? len[i] : (rrp1[w + 1] - rrp1[w]) + (rrp2[w + 1] - rrp2[w]) + S;
-}
-
 inline unsigned g1(int64_t n) { return static_cast<unsigned>(ceil_div(n > 0 ? n : 1, 256)); }
 
 std::string slab_mode() {
@@ -449,10 +441,12 @@ void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const in
   tr.mark("    upload + fill");
   plan.partial.alloc(runs);
   {
-    std::vector<int32_t> widx(nr, -1);
-    for (int32_t k = 0; k < nw; ++k) widx[rows[k] - r0] = k;
+    std::vector<int32_t> widx(nr, -1), wrow(nw);
+    for (int32_t k = 0; k < nw; ++k) widx[rows[k] - r0] = k, wrow[k] = rows[k] - r0;
     plan.widx.alloc(nr);
     plan.widx.upload(widx.data(), nr, st);
+    plan.wrow.alloc(nw);
+    plan.wrow.upload(wrow.data(), nw, st);
   }
   SlabView& v = plan.view;
   v.nw = nw;
@@ -473,7 +467,7 @@ void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const in
   v.col = plan.col.get();
   v.val = plan.val.get();
   v.partial = plan.partial.get();
-  v.widx = plan.widx.get();
+  v.wrow = plan.wrow.get();
   v.rest1 = CsrView{plan.rrp1.get(), plan.rci1.get(), plan.rval1.get()};
   v.rest2 = CsrView{plan.rrp2.get(), plan.rci2.get(), plan.rval2.get()};
   RB_CUDA(cudaStreamSynchronize(st));
@@ -505,13 +499,16 @@ void build_slab_phase(SlabPhase& ph, const SlabChoice& choice, int seg, const in
   ph = SlabPhase{};
   build_slab_plan(ph.plan, choice, seg, rp1, ci1, rp2, ci2, r0, r1, st);
   if (!ph.active()) return;
-  const SlabPlan& plan = ph.plan;
   const int32_t nr = r1 - r0;
-  DevBuf<int32_t> flen(nr);
-  finish_len_kernel<<<g1(nr), 256, 0, st>>>(plan.widx.get(), plan.rrp1.get(), plan.rrp2.get(), plan.view.S, len, nr,
-                                            flen.get());
-  RB_LAUNCH_CHECK();
-  build_schedule(ph.fin, flen.get(), nr, false, st);
+  const std::vector<int32_t> widx = download(ph.plan.widx, nr, st);
+  std::vector<int32_t> orr;
+  for (int32_t i = 0; i < nr; ++i)
+    if (widx[i] < 0) orr.push_back(i);
+  if (!orr.empty()) {
+    DevBuf<int32_t> d(orr.size());
+    d.upload(orr.data(), orr.size(), st);
+    build_schedule(ph.others, len, static_cast<int64_t>(orr.size()), false, st, d.get());
+  }
   RB_CUDA(cudaStreamSynchronize(st));
 }
 

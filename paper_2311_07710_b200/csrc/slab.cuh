@@ -45,7 +45,7 @@ constexpr int kMaxSlabs = 64;
 constexpr int kSlabWidth = 2048;        // columns per window (16 KB of fp64)
 constexpr int kSlabMinRow = 16;         // in-window entries that make a W row
 constexpr double kSlabMinDensity = 16;  // gathers per column that keep a window
-constexpr int kSlabTileCap = 3072;      // entries per tile (30 KB staged)
+constexpr int kSlabTileCap = 2816;      // entries per tile (28 KB staged)
 constexpr int kSlabStages = 3;          // tile stages per CTA (one shared window)
 constexpr int kSlabRowCap = 512;        // rows per chunk
 constexpr int kSlabRunCap = 512;        // W rows: every window run and the rest <= this
@@ -93,7 +93,7 @@ struct SlabView {
   const uint16_t* col = nullptr;    // column offset inside the window
   const double* val = nullptr;
   double* partial = nullptr;        // [S * nw] (window-major: a tile's partials are contiguous)
-  const int32_t* widx = nullptr;    // [rows of the op] W-row index or -1
+  const int32_t* wrow = nullptr;    // [nw] W rows' ids relative to the op's row base
   CsrView rest1{}, rest2{};         // rest CSRs over W rows (segment 1 / 2)
   unsigned long long* prof = nullptr;  // [grid * kSlabProf] phase times (RB_SLAB_PROFILE builds)
   bool active() const { return nw > 0 && S > 0; }
@@ -108,7 +108,7 @@ struct SlabView {
 // Device arrays behind a SlabView (built by build_slab_plan).
 struct SlabPlan {
   SlabView view;
-  DevBuf<int32_t> rows, pos, widx;
+  DevBuf<int32_t> rows, pos, wrow, widx;
   DevBuf<SlabTile> tile;
   DevBuf<int32_t> cta;
   std::vector<int64_t> tile_bytes;  // host: bytes each tile stages
@@ -344,59 +344,50 @@ __global__ void __launch_bounds__(kSlabThreads) slab_kernel(const Op op, const S
 
 inline int SlabView::smem_bytes() const { return win_max * 8 + kSlabStages * stage_bytes(); }
 
-// The rows of Op after the slab kernel: W rows sum their rest entries, then
-// their S window partials (positions rest_len .. rest_len + S - 1 of the row,
-// lane-strided like entries), and run Op's epilogue; other rows are Op itself.
-// The per-row order depends only on the row's entries, S and its lane count,
-// which the schedule derives from this length.
+// The rows of Op after the slab kernel, one launch (a programmatic dependent
+// launch of the slab kernel):
+//  * blocks [0, wblocks): W rows, one thread per row — epilogue inputs
+//    prefetched, then (after the slab grid completes) the row's rest entries
+//    in order, plus its S window partials summed in window order (a warp's
+//    32 consecutive W rows read each window's partials coalesced), then the
+//    epilogue; the per-row order is fixed, so results are deterministic and
+//    shard-invariant;
+//  * the other blocks: ordinary rowwise tiles of the rows without partials
+//    (no wait: they overlap the slab kernel).
 template <class Op>
-struct SlabFinishOp {
-  static constexpr bool kStrict = false;
-  static constexpr int kWideUnroll = Op::kWideUnroll;
-  static constexpr bool kStageWindows = false;
-  using AccT = typename Op::AccT;
-  Op op, rest;
-  const int32_t* widx;     // [rows of op] W-row index or -1
-  const double* partial;   // [S * nw]
-  int32_t S, nw, seg;
-  __device__ __forceinline__ int len(int r) const {
-    const int w = widx[r];
-    return w >= 0 ? rest.len(w) + S : op.len(r);
+__global__ void __launch_bounds__(kBlock) slab_finish_kernel(const Op op, const Op rest, const SlabView sv,
+                                                             const SchedView others, int wblocks) {
+  if (static_cast<int>(blockIdx.x) >= wblocks) {
+    const Gather g[2] = {Gather{op.gather_src(0), nullptr, 0, 0u}, Gather{op.gather_src(1), nullptr, 0, 0u}};
+    rowwise_tile(op, others, blockIdx.x - wblocks, g);
+    return;
   }
-  template <int U>
-  __device__ __forceinline__ void accumulate(int r, int lo, int hi, int lane, int stride, AccT& acc,
-                                             const Gather* g) const {
-    const int w = widx[r];
-    if (w < 0) {
-      op.template accumulate<U>(r, lo, hi, lane, stride, acc, g);
-      return;
-    }
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // the slab kernel's partials are complete
-    const int rl = rest.len(w);
-    if (lo < rl) rest.template accumulate<U>(w, lo, hi < rl ? hi : rl, lane, stride, acc, g);
-    // partial q of this row at partial[q * nw + w]; 4 loads in flight, summed in order
-    const double* pr = partial + w - static_cast<int64_t>(rl) * nw;
-    const int64_t sn = static_cast<int64_t>(stride) * nw;
-    double t = 0.0;
-    int p = next_pos(lo + lane, stride, rl);
-    for (; p + 3 * stride < hi; p += 4 * stride) {
-      const double* q = pr + static_cast<int64_t>(p) * nw;
-      const double a0 = __ldcg(q), a1 = __ldcg(q + sn), a2 = __ldcg(q + 2 * sn), a3 = __ldcg(q + 3 * sn);
-      t += a0;
-      t += a1;
-      t += a2;
-      t += a3;
-    }
-    for (; p < hi; p += stride) t += __ldcg(pr + static_cast<int64_t>(p) * nw);
-    if (seg == 0) acc.v[0] += t;
-    else acc.v[AccT::kK - 1] += t;
+  const int k = blockIdx.x * kBlock + threadIdx.x;
+  const bool valid = k < sv.nw;
+  const int r = valid ? sv.wrow[k] : 0;
+  typename Op::Pre pre{};
+  if (valid) pre = op.prefetch(r);
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the slab kernel's partials are complete
+  if (!valid) return;
+  const Gather gl[2] = {Gather{rest.gather_src(0), nullptr, 0, 0u}, Gather{rest.gather_src(1), nullptr, 0, 0u}};
+  typename Op::AccT a;
+  a.zero();
+  rest.template accumulate<kUnroll>(k, 0, rest.len(k), 0, 1, a, gl);
+  const double* p = sv.partial + k;
+  double t = 0.0;
+  int q = 0;
+  for (; q + 8 <= sv.S; q += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldcg(p + static_cast<int64_t>(q + u) * sv.nw);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) t += v[u];
   }
-  __device__ __forceinline__ const double* gather_src(int slot) const { return op.gather_src(slot); }
-  using Pre = typename Op::Pre;
-  __device__ __forceinline__ Pre prefetch(int r) const { return op.prefetch(r); }
-  __device__ __forceinline__ void finish(int r, const AccT& acc) const { op.finish(r, acc); }
-  __device__ __forceinline__ void finish(int r, const AccT& acc, const Pre& pre) const { op.finish(r, acc, pre); }
-};
+  for (; q < sv.S; ++q) t += __ldcg(p + static_cast<int64_t>(q) * sv.nw);
+  if (sv.seg == 0) a.v[0] += t;
+  else a.v[Op::AccT::kK - 1] += t;
+  op.finish(r, a, pre);
+}
 
 // Raise the dynamic smem limit of the slab kernel of Op (once, outside stream
 // capture) and return the persistent grid for that smem size.
@@ -412,7 +403,7 @@ inline int prepare_slab(int smem_bytes) {
 // A slab-tiled op: the plan and the finish schedule over all of its rows.
 struct SlabPhase {
   SlabPlan plan;
-  Schedule fin;
+  Schedule others;  // rows without partials (the op's own rows)
   bool active() const { return plan.view.active(); }
 };
 
@@ -436,11 +427,10 @@ inline int launch_slab_phase(const Op& op, const SlabPhase& ph, cudaStream_t st)
   if (sv.jagged) slab_kernel<Op, true><<<sv.grid, kSlabThreads, sv.smem_bytes(), st>>>(op, sv);
   else slab_kernel<Op, false><<<sv.grid, kSlabThreads, sv.smem_bytes(), st>>>(op, sv);
   RB_LAUNCH_CHECK();
-  const SchedView& s = ph.fin.view;
-  if (s.total_blocks <= 0) return 1;
-  const SlabFinishOp<Op> f{op, op.with_views(sv.rest1, sv.rest2), sv.widx, sv.partial, sv.S, sv.nw, sv.seg};
+  const SchedView& o = ph.others.view;
+  const int wblocks = static_cast<int>(ceil_div(sv.nw, kBlock));
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(static_cast<unsigned>(s.total_blocks));
+  cfg.gridDim = dim3(static_cast<unsigned>(wblocks + (o.total_blocks > 0 ? o.total_blocks : 0)));
   cfg.blockDim = dim3(kBlock);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = st;
@@ -449,7 +439,7 @@ inline int launch_slab_phase(const Op& op, const SlabPhase& ph, cudaStream_t st)
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  RB_CUDA(cudaLaunchKernelEx(&cfg, rowwise_kernel<SlabFinishOp<Op>, false>, f, s));
+  RB_CUDA(cudaLaunchKernelEx(&cfg, slab_finish_kernel<Op>, op, op.with_views(sv.rest1, sv.rest2), sv, o, wblocks));
   return 2;
 }
 

@@ -63,6 +63,13 @@ inline void pool_prepare() {
   if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
     unsigned long long keep = ~0ull;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    // RAPDHG_POOL_RESERVE_MB: map this much up front (growing the pool later
+    // maps pages synchronously, which can stall a setup for 100+ ms)
+    if (const char* r = std::getenv("RAPDHG_POOL_RESERVE_MB")) {
+      const std::size_t bytes = static_cast<std::size_t>(std::atoll(r)) << 20;
+      void* p = nullptr;
+      if (bytes && cudaMallocAsync(&p, bytes, cudaStreamLegacy) == cudaSuccess) cudaFreeAsync(p, cudaStreamLegacy);
+    }
   }
   done.fetch_or(bit);
 }
@@ -192,14 +199,16 @@ class PinnedBuf {
 // Phase timer printed to stderr when RAPDHG_TRACE is set (synchronises the
 // stream at each mark, so only for diagnosis).
 struct Tracer {
-  bool on;
+  bool on, sync;
   cudaStream_t st;
   std::chrono::steady_clock::time_point t;
-  explicit Tracer(cudaStream_t s)
-      : on(std::getenv("RAPDHG_TRACE") != nullptr), st(s), t(std::chrono::steady_clock::now()) {}
+  explicit Tracer(cudaStream_t s) : on(std::getenv("RAPDHG_TRACE") != nullptr), st(s), t(std::chrono::steady_clock::now()) {
+    const char* e = std::getenv("RAPDHG_TRACE");
+    sync = !(e && e[0] == 'h');  // RAPDHG_TRACE=host: host timestamps only, no stream syncs
+  }
   void mark(const char* what) {
     if (!on) return;
-    if (st) cudaStreamSynchronize(st);
+    if (st && sync) cudaStreamSynchronize(st);
     const auto now = std::chrono::steady_clock::now();
     std::fprintf(stderr, "[rapdhg] %-30s %9.3f ms\n", what,
                  std::chrono::duration<double, std::milli>(now - t).count());

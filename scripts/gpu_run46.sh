@@ -1,0 +1,6 @@
+export PYTHONUNBUFFERED=1
+python bench.py --steps 5 --warmup 3 > gpurun_out/bench46.log 2>&1; echo "bench rc=$?"; tail -1 gpurun_out/bench46.log | cut -c1-2500
+python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/bench46_short.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none -s 3000 -c 400 --csv \
+    --log-file gpurun_out/launches46.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_launch46.log 2>&1
+echo "launch list rc=$?"

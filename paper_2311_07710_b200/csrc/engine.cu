@@ -274,34 +274,70 @@ void random_unit(DeviceQP& P, DevBuf<double>& v, int len, std::mt19937_64& rng) 
 }  // namespace
 
 // estimate_op_norm_symmetric (opnorm.hpp:64-87)
+namespace {
+// v = w * (1.0 / sqrt(*sumsq)) with the norm read on the device — the same
+// IEEE operations as the host's `1.0 / std::sqrt(s)`; a zero norm leaves v
+// unchanged (the host then restarts from a random vector).
+__global__ void scale_by_norm_kernel(double* v, const double* w, const double* sumsq, int64_t n) {
+  const double s = *sumsq;
+  if (s == 0.0) return;
+  const double inv = 1.0 / sqrt(s);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    v[i] = w[i] * inv;
+}
+}  // namespace
+
+// Power iteration (opnorm.hpp:36-87) run in device batches: each step records
+// (v.w, ||w||^2) on the device and normalises v there; after a batch the host
+// replays the reference's loop over the recorded values (stopping rule,
+// zero-norm restart) — identical results, one host round trip per batch
+// (8, 16, .. 64 steps) instead of per step. Overshoot past convergence only
+// costs the batch's remaining steps (their v is never used).
+template <class Step>
+double DeviceQP::power_iteration(DevBuf<double>& v, DevBuf<double>& w, int len, const Step& step, bool absval,
+                                 int max_iters, double tol, std::mt19937_64& rng) {
+  constexpr int kMaxBatch = 64;
+  DevBuf<double> hist(2 * kMaxBatch);
+  PinnedBuf<double> hh;
+  hh.alloc(2 * kMaxBatch);
+  random_unit(*this, v, len, rng);
+  double lambda = 0.0;
+  int it = 0, batch = 8;
+  while (it < max_iters) {
+    const int K = std::min(batch, max_iters - it);
+    for (int i = 0; i < K; ++i) {
+      step();  // w = M v
+      launch_reduce<2, 0>(DotAndSumSq{v.get(), w.get()}, len, strict, red, hist.get() + 2 * i, st);
+      scale_by_norm_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(len, 256), 4 * kSMs)), 256, 0, st>>>(
+          v.get(), w.get(), hist.get() + 2 * i + 1, len);
+      RB_LAUNCH_CHECK();
+      launches += 2;
+    }
+    RB_CUDA(cudaMemcpyAsync(hh.get(), hist.get(), sizeof(double) * 2 * K, cudaMemcpyDeviceToHost, st));
+    RB_CUDA(cudaStreamSynchronize(st));
+    bool restarted = false;
+    for (int i = 0; i < K && !restarted; ++i, ++it) {
+      const double lambda_next = absval ? std::fabs(hh[2 * i]) : hh[2 * i];
+      const double nrm = std::sqrt(hh[2 * i + 1]);
+      if (nrm == 0.0) {  // v stayed frozen from here on in this batch
+        random_unit(*this, v, len, rng);
+        restarted = true;
+        continue;
+      }
+      if (it > 0 && std::fabs(lambda_next - lambda) <= tol * std::fabs(lambda_next)) return lambda_next;
+      lambda = lambda_next;
+    }
+    batch = std::min(batch * 2, kMaxBatch);
+  }
+  return lambda;
+}
+
 double DeviceQP::op_norm_q(const double* qv, int max_iters, double tol, uint64_t seed) {
   if (Q.nnz == 0) return 0.0;
   std::mt19937_64 rng(seed);
   DevBuf<double> v(n), w(n);
-  random_unit(*this, v, n, rng);
-  double lambda = 0.0;
-  const double* vp = v.get();
-  const double* wp = w.get();
-  for (int it = 0; it < max_iters; ++it) {
-    spmv(Q, sch_q, qv, v.get(), w.get());
-    double s[2];
-    reduce_to_host<2, 0>(DotAndSumSq{vp, wp}, n, s);
-    const double lambda_next = std::fabs(s[0]);
-    const double nrm = std::sqrt(s[1]);
-    if (nrm == 0.0) {
-      random_unit(*this, v, n, rng);
-      continue;
-    }
-    scale_copy_kernel<<<grid1(n), 256, 0, st>>>(v.get(), w.get(), 1.0 / nrm, n);
-    RB_LAUNCH_CHECK();
-    ++launches;
-    if (it > 0 && std::fabs(lambda_next - lambda) <= tol * std::fabs(lambda_next)) {
-      lambda = lambda_next;
-      break;
-    }
-    lambda = lambda_next;
-  }
-  return lambda;
+  return power_iteration(v, w, n, [&] { spmv(Q, sch_q, qv, v.get(), w.get()); }, true, max_iters, tol, rng);
 }
 
 // estimate_op_norm (opnorm.hpp:36-61): power iteration on A'A; A' v as the
@@ -311,30 +347,13 @@ double DeviceQP::op_norm_a(const double* av, const double* atv, int max_iters, d
   if (A.nnz == 0) return 0.0;
   std::mt19937_64 rng(seed);
   DevBuf<double> v(n), w(n), mv(m);
-  random_unit(*this, v, n, rng);
-  double lambda = 0.0;
-  const double* vp = v.get();
-  const double* wp = w.get();
-  for (int it = 0; it < max_iters; ++it) {
-    spmv(A, sch_dual, av, v.get(), mv.get());
-    spmv(AT, sch_at, atv, mv.get(), w.get());
-    double s[2];
-    reduce_to_host<2, 0>(DotAndSumSq{vp, wp}, n, s);
-    const double lambda_next = s[0];
-    const double nrm = std::sqrt(s[1]);
-    if (nrm == 0.0) {
-      random_unit(*this, v, n, rng);
-      continue;
-    }
-    scale_copy_kernel<<<grid1(n), 256, 0, st>>>(v.get(), w.get(), 1.0 / nrm, n);
-    RB_LAUNCH_CHECK();
-    ++launches;
-    if (it > 0 && std::fabs(lambda_next - lambda) <= tol * std::fabs(lambda_next)) {
-      lambda = lambda_next;
-      break;
-    }
-    lambda = lambda_next;
-  }
+  const double lambda = power_iteration(
+      v, w, n,
+      [&] {
+        spmv(A, sch_dual, av, v.get(), mv.get());
+        spmv(AT, sch_at, atv, mv.get(), w.get());
+      },
+      false, max_iters, tol, rng);
   return std::sqrt(std::max(lambda, 0.0));
 }
 

@@ -64,6 +64,9 @@ class DeviceQP {
   // given values (patterns of Q / A / A').
   double op_norm_q(const double* qv, int max_iters, double tol, uint64_t seed);
   double op_norm_a(const double* av, const double* atv, int max_iters, double tol, uint64_t seed);
+  template <class Step>
+  double power_iteration(DevBuf<double>& v, DevBuf<double>& w, int len, const Step& step, bool absval,
+                         int max_iters, double tol, std::mt19937_64& rng);
 
   // Deterministic reduction to host (strict: sequential).
   template <int NS, int NM, class F>

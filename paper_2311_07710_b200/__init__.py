@@ -295,8 +295,11 @@ class QuadraticProgram:
         return self.num_ineq() + self.num_eq()
 
     def objective(self, x) -> float:
+        """½x'Qx + c'x + obj_offset, evaluated on the host (reporting only)."""
         x = _f64(x)
-        qx = self.q.to_dense() @ x if self.q.nnz() < 4_000_000 else self.q.multiply(x)
+        q = self.q
+        rows = np.repeat(np.arange(q.n_rows), np.diff(q.row_ptr))
+        qx = np.bincount(rows, weights=q.values * x[q.col_idx], minlength=q.n_rows)
         return 0.5 * float(x @ qx) + float(self.c @ x) + self.obj_offset
 
     def _struct(self) -> abi.Qp:

@@ -346,23 +346,26 @@ inline int SlabView::smem_bytes() const { return win_max * 8 + kSlabStages * sta
 
 // The rows of Op after the slab kernel, one launch (a programmatic dependent
 // launch of the slab kernel):
-//  * blocks [0, wblocks): W rows, one thread per row — epilogue inputs
+//  * the last wblocks blocks: W rows, one thread per row — epilogue inputs
 //    prefetched, then (after the slab grid completes) the row's rest entries
 //    in order, plus its S window partials summed in window order (a warp's
 //    32 consecutive W rows read each window's partials coalesced), then the
 //    epilogue; the per-row order is fixed, so results are deterministic and
 //    shard-invariant;
-//  * the other blocks: ordinary rowwise tiles of the rows without partials
-//    (no wait: they overlap the slab kernel).
+//  * the first blocks: ordinary rowwise tiles of the rows without partials
+//    (no wait: they overlap the slab kernel; scheduled first so the waiting
+//    W blocks do not hold SM slots while the slab kernel still runs).
 template <class Op>
 __global__ void __launch_bounds__(kBlock) slab_finish_kernel(const Op op, const Op rest, const SlabView sv,
                                                              const SchedView others, int wblocks) {
-  if (static_cast<int>(blockIdx.x) >= wblocks) {
+  const int ob = others.total_blocks > 0 ? others.total_blocks : 0;
+  if (static_cast<int>(blockIdx.x) < ob) {  // first: the rows without partials (they start at once)
     const Gather g[2] = {Gather{op.gather_src(0), nullptr, 0, 0u}, Gather{op.gather_src(1), nullptr, 0, 0u}};
-    rowwise_tile(op, others, blockIdx.x - wblocks, g);
+    rowwise_tile(op, others, blockIdx.x, g);
     return;
   }
-  const int k = blockIdx.x * kBlock + threadIdx.x;
+  // last: the W rows, whose blocks wait for the slab grid
+  const int k = (blockIdx.x - ob) * kBlock + threadIdx.x;
   const bool valid = k < sv.nw;
   const int r = valid ? sv.wrow[k] : 0;
   typename Op::Pre pre{};

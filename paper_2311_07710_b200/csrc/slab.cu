@@ -145,53 +145,37 @@ std::vector<int32_t> scan_host(const std::vector<int32_t>& cnt) {
   return rp;
 }
 
-// Sliced, jagged layout of one tile: rows [k0, k1) sorted by run length
-// (descending, stable), 32 per slice; slice q stores entry e of its lanes
-// whose run exceeds e contiguously. meta = perm | len | soff (slab.cuh);
-// joff = per slice the start of each entry e (fill_kernel only); offsets are
-// relative to the tile's first entry; n = entries, padded to 8.
+// One tile: W rows (indices k, runs already sorted by length, descending),
+// 32 per slice, each slice as wide as its longest run (the per-window sort
+// makes slices nearly uniform). meta (uint16) = perm (uint32 row index k per
+// slot, 2 elements each) | len[nr] | soff[nsl + 1]; joff = per slice the start
+// of each entry e (fill_kernel only); offsets relative to the tile's first
+// entry.
 struct TileLayout {
-  std::vector<int32_t> order;  // sorted rows (chunk-relative)
   std::vector<uint16_t> meta;
-  std::vector<int32_t> joff;   // slice q's offsets start at joff[sj[q]]
+  std::vector<int32_t> joff;  // slice q's offsets start at joff[sj[q]]
   std::vector<int32_t> sj;
   int32_t n = 0;
-  int64_t total = 0;  // entries before the 8-alignment (exact, unclamped)
-  bool fits(int ecap, int mcap) const { return n <= ecap && static_cast<int>(meta.size()) <= mcap; }
 };
-TileLayout layout_tile(const std::vector<int32_t>& c2, int64_t s_base, int32_t k0, int32_t k1, bool jagged) {
+TileLayout layout_tile(const int32_t* rows, const int32_t* len, int32_t nr) {
   TileLayout L;
-  const int32_t nr = k1 - k0;
-  const int32_t* len = c2.data() + s_base + k0;
-  // counting sort by run length, descending, stable (runs <= kSlabRunCap)
-  std::vector<int32_t> start(kSlabRunCap + 2, 0);
-  for (int32_t i = 0; i < nr; ++i) ++start[kSlabRunCap - len[i] + 1];
-  for (int v = 1; v <= kSlabRunCap + 1; ++v) start[v] += start[v - 1];
-  L.order.resize(nr);
-  for (int32_t i = 0; i < nr; ++i) L.order[start[kSlabRunCap - len[i]]++] = i;
   const int nsl = (nr + 31) / 32;
-  L.meta.resize(2 * static_cast<std::size_t>(nr) + nsl + 1);
+  L.meta.resize(3 * static_cast<std::size_t>(nr) + nsl + 1);
   for (int32_t i = 0; i < nr; ++i) {
-    L.meta[i] = static_cast<uint16_t>(L.order[i]);
-    L.meta[nr + i] = static_cast<uint16_t>(len[L.order[i]]);
+    L.meta[2 * i] = static_cast<uint16_t>(static_cast<uint32_t>(rows[i]) & 0xffffu);
+    L.meta[2 * i + 1] = static_cast<uint16_t>(static_cast<uint32_t>(rows[i]) >> 16);
+    L.meta[2 * nr + i] = static_cast<uint16_t>(len[i]);
   }
   int64_t cur = 0;
   for (int q = 0; q < nsl; ++q) {
-    L.meta[2 * nr + q] = static_cast<uint16_t>(std::min<int64_t>(cur, 65535));  // soff[q]
+    L.meta[3 * nr + q] = static_cast<uint16_t>(cur);  // soff[q]
     L.sj.push_back(static_cast<int32_t>(L.joff.size()));
-    const int lanes = std::min(32, nr - 32 * q);
-    const int Lm = len[L.order[32 * q]];
-    int cnt = lanes;  // lanes with a run longer than e (runs are sorted)
-    for (int e = 0; e < Lm; ++e) {
-      while (cnt > 0 && len[L.order[32 * q + cnt - 1]] <= e) --cnt;
-      L.joff.push_back(static_cast<int32_t>(cur));
-      cur += jagged ? cnt : 32;
-    }
+    const int Lm = len[32 * q];
+    for (int e = 0; e < Lm; ++e) L.joff.push_back(static_cast<int32_t>(cur + 32 * e));
+    cur += 32 * static_cast<int64_t>(Lm);
   }
-  L.meta[2 * nr + nsl] = static_cast<uint16_t>(std::min<int64_t>(cur, 65535));
-  L.total = cur;
-  L.n = static_cast<int32_t>((cur + 7) & ~int64_t{7});
-  if (cur > 65535) L.n = INT32_MAX;  // 16-bit offsets overflow: split
+  L.meta[3 * nr + nsl] = static_cast<uint16_t>(cur);
+  L.n = static_cast<int32_t>(cur);  // a multiple of 32
   return L;
 }
 
@@ -290,117 +274,93 @@ void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const in
   RB_LAUNCH_CHECK();
   const std::vector<int32_t> hc2 = download(c2, runs, st), hrw = download(rw, nw, st), hro = download(ro, nw, st);
   tr.mark("    counts");
-  // Row chunks: whole slices (multiples of 32 rows), grown while every
-  // window's entries stay under 7/8 of the capacity; split further until there
-  // are enough tiles for every CTA; a chunk whose padded tile still overflows
-  // is halved (at a multiple of 32) and laid out again.
-  const int ecap = (std::min(32736, std::max(256, env_int("RAPDHG_SLAB_TILE", kSlabTileCap))) + 7) & ~7;
+  // Tiles, per window: the W rows with entries in the window, sorted by their
+  // run length there (descending, stable), cut into tiles of whole 32-row
+  // slices while the (slice-padded) entries fit the stage and the rows fit
+  // the row cap. Rows with an empty run in a window appear in none of its
+  // tiles (their partial stays the zero written at setup).
+  const int ecap = (std::min(32736, std::max(256, env_int("RAPDHG_SLAB_TILE", kSlabTileCap))) + 31) & ~31;
   const int rcap = kSlabRowCap;
-  std::vector<int32_t> chunk{0};
-  {
-    std::vector<int64_t> cur(S, 0), add(S, 0);
-    for (int32_t k = 0; k < nw;) {
-      const int32_t g = std::min(nw, k + 32);
-      for (int s = 0; s < S; ++s) {
-        add[s] = 0;
-        for (int32_t q = k; q < g; ++q) add[s] += hc2[static_cast<int64_t>(s) * nw + q];
+  std::vector<std::vector<int32_t>> order(S);  // per window: sorted W rows
+  parallel_for(S, [&](int64_t si) {
+    const int s = static_cast<int>(si);
+    const int32_t* len = hc2.data() + static_cast<int64_t>(s) * nw;
+    std::vector<int32_t> start(kSlabRunCap + 2, 0);
+    for (int32_t k = 0; k < nw; ++k) ++start[kSlabRunCap - len[k] + 1];
+    for (int v = 1; v <= kSlabRunCap + 1; ++v) start[v] += start[v - 1];
+    std::vector<int32_t> o(nw);
+    for (int32_t k = 0; k < nw; ++k) o[start[kSlabRunCap - len[k]]++] = k;
+    int32_t cnt = nw;
+    while (cnt > 0 && len[o[cnt - 1]] == 0) --cnt;  // empty runs last
+    o.resize(cnt);
+    order[s] = std::move(o);
+  });
+  struct TileSpan {
+    int s;
+    int32_t b, e;  // range of order[s]
+  };
+  std::vector<TileSpan> spans;
+  for (int s = 0; s < S; ++s) {
+    const std::vector<int32_t>& o = order[s];
+    const int32_t* len = hc2.data() + static_cast<int64_t>(s) * nw;
+    int32_t b = 0;
+    int64_t padded = 0;
+    for (int32_t q = 0; q < static_cast<int32_t>(o.size()); q += 32) {  // slice starting at q
+      const int64_t w = 32 * static_cast<int64_t>(len[o[q]]);
+      const int32_t qe = std::min<int32_t>(static_cast<int32_t>(o.size()), q + 32);
+      if (q > b && (padded + w > ecap || qe - b > rcap)) {
+        spans.push_back({s, b, q});
+        b = q;
+        padded = 0;
       }
-      bool fits = g - chunk.back() <= rcap;
-      for (int s = 0; s < S && fits; ++s) fits = cur[s] + add[s] <= ecap * 7 / 8;
-      if (!fits && k > chunk.back()) {
-        chunk.push_back(k);
-        std::fill(cur.begin(), cur.end(), 0);
-      }
-      for (int s = 0; s < S; ++s) cur[s] += add[s];
-      k = g;
+      padded += w;
     }
-    chunk.push_back(nw);
+    if (b < static_cast<int32_t>(o.size())) spans.push_back({s, b, static_cast<int32_t>(o.size())});
   }
-  auto split_at = [](int32_t a, int32_t b) { return a + std::max<int32_t>(32, ((b - a) / 2) & ~31); };
-  {
-    const int64_t want = ceil_div(static_cast<int64_t>(4 * kSMs), S);
-    while (static_cast<int64_t>(chunk.size()) - 1 < want) {  // halve the widest chunk
-      std::size_t best = 0;
-      for (std::size_t c = 1; c + 1 < chunk.size(); ++c)
-        if (chunk[c + 1] - chunk[c] > chunk[best + 1] - chunk[best]) best = c;
-      if (chunk[best + 1] - chunk[best] < 128) break;
-      chunk.insert(chunk.begin() + best + 1, split_at(chunk[best], chunk[best + 1]));
-    }
-  }
-  // padded (32-wide slices) or jagged: padded unless padding would exceed
-  // kSlabJaggedPad (RAPDHG_SLAB_JAGGED=0/1 forces)
-  bool jagged = false;
-  {
-    int64_t actual = 0, padded = 0;
-    const int32_t Jc = static_cast<int32_t>(chunk.size()) - 1;
-    std::vector<int64_t> pad_t(static_cast<std::size_t>(S) * Jc, 0), act_t(pad_t.size(), 0);
-    parallel_for(static_cast<int64_t>(S) * Jc, [&](int64_t t) {
-      const int s = static_cast<int>(t / Jc), j = static_cast<int>(t % Jc);
-      const TileLayout L = layout_tile(hc2, static_cast<int64_t>(s) * nw, chunk[j], chunk[j + 1], false);
-      pad_t[t] = L.total;
-      for (int32_t k = chunk[j]; k < chunk[j + 1]; ++k) act_t[t] += hc2[static_cast<int64_t>(s) * nw + k];
-    });
-    for (std::size_t t = 0; t < pad_t.size(); ++t) padded += pad_t[t], actual += act_t[t];
-    jagged = static_cast<double>(padded) > kSlabJaggedPad * static_cast<double>(std::max<int64_t>(actual, 1));
-    const int force = env_int("RAPDHG_SLAB_JAGGED", -1);
-    if (force >= 0) jagged = force != 0;
-  }
-  // layouts of every (window, chunk) tile, on host threads; overflowing chunks split
-  std::vector<TileLayout> lay;
-  for (;;) {
-    const int32_t Jc = static_cast<int32_t>(chunk.size()) - 1;
-    lay.assign(static_cast<std::size_t>(S) * Jc, TileLayout{});
-    parallel_for(static_cast<int64_t>(S) * Jc, [&](int64_t t) {
-      const int s = static_cast<int>(t / Jc), j = static_cast<int>(t % Jc);
-      lay[t] = layout_tile(hc2, static_cast<int64_t>(s) * nw, chunk[j], chunk[j + 1], jagged);
-    });
-    std::vector<int32_t> bad;
-    for (int32_t j = 0; j < Jc; ++j)
-      for (int s = 0; s < S; ++s)
-        if (!lay[static_cast<std::size_t>(s) * Jc + j].fits(ecap, kSlabMetaCap) && chunk[j + 1] - chunk[j] > 32) {
-          bad.push_back(j);
-          break;
-        }
-    if (bad.empty()) break;
-    for (auto it = bad.rbegin(); it != bad.rend(); ++it)
-      chunk.insert(chunk.begin() + *it + 1, split_at(chunk[*it], chunk[*it + 1]));
-  }
-  const int32_t J = static_cast<int32_t>(chunk.size()) - 1;
-  tr.mark("    chunks + layouts");
-  // Tiles: window-major storage, each tile 8-entry aligned; run (s, k): tile
-  // base off[s * nw + k] and jx[s * nw + k] (see fill_kernel).
+  const int32_t ntiles = static_cast<int32_t>(spans.size());
+  std::vector<TileLayout> lay(ntiles);
+  parallel_for(ntiles, [&](int64_t t) {
+    const TileSpan& sp = spans[t];
+    const int32_t nr_t = sp.e - sp.b;
+    std::vector<int32_t> rows_t(order[sp.s].begin() + sp.b, order[sp.s].begin() + sp.e), len_t(nr_t);
+    for (int32_t i = 0; i < nr_t; ++i) len_t[i] = hc2[static_cast<int64_t>(sp.s) * nw + rows_t[i]];
+    lay[t] = layout_tile(rows_t.data(), len_t.data(), nr_t);
+  });
+  tr.mark("    tiles + layouts");
+  // tile arrays: window-major, each tile 32-entry aligned; run (s, k): tile
+  // base off[s * nw + k] and jx[s * nw + k] (see fill_kernel)
   std::vector<int32_t> off(runs, 0), jx(runs, 0), joff;
-  std::vector<SlabTile> tiles(static_cast<std::size_t>(S) * J);
+  std::vector<SlabTile> tiles(ntiles);
   std::vector<uint16_t> meta;
   int64_t cursor = 0;
   int max_tile = 0, max_meta = 0;
-  for (int s = 0; s < S; ++s)
-    for (int32_t j = 0; j < J; ++j) {
-      const int32_t k0 = chunk[j], k1 = chunk[j + 1], n_r = k1 - k0;
-      const TileLayout& L = lay[static_cast<std::size_t>(s) * J + j];
-      SlabTile& d = tiles[static_cast<std::size_t>(s) * J + j];
-      d.a = static_cast<int32_t>(cursor);
-      d.n = L.n;
-      d.meta = static_cast<int32_t>(meta.size());
-      d.k0 = k0;
-      d.nr = n_r;
-      d.s = s;
-      d.m = static_cast<int32_t>(L.meta.size());
-      max_tile = std::max(max_tile, d.n);
-      max_meta = std::max(max_meta, d.m);
-      // staged bytes + a fixed per-tile cost (barrier round trip, descriptor)
-      plan.tile_bytes.push_back(10 * static_cast<int64_t>(d.n) + 2 * static_cast<int64_t>(d.m) + 16384);
-      const int64_t j0 = static_cast<int64_t>(joff.size());
-      for (int32_t slot = 0; slot < n_r; ++slot) {
-        const int64_t run = static_cast<int64_t>(s) * nw + k0 + L.order[slot];
-        off[run] = static_cast<int32_t>(cursor);
-        jx[run] = static_cast<int32_t>((j0 + L.sj[slot / 32]) * 32 + slot % 32);
-      }
-      joff.insert(joff.end(), L.joff.begin(), L.joff.end());
-      meta.insert(meta.end(), L.meta.begin(), L.meta.end());
-      meta.resize((meta.size() + 7) & ~std::size_t{7}, 0);
-      cursor += d.n;
+  for (int32_t t = 0; t < ntiles; ++t) {
+    const TileSpan& sp = spans[t];
+    const TileLayout& L = lay[t];
+    const int32_t n_r = sp.e - sp.b;
+    SlabTile& d = tiles[t];
+    d.a = static_cast<int32_t>(cursor);
+    d.n = L.n;
+    d.meta = static_cast<int32_t>(meta.size());
+    d.k0 = 0;
+    d.nr = n_r;
+    d.s = sp.s;
+    d.m = static_cast<int32_t>(L.meta.size());
+    max_tile = std::max(max_tile, d.n);
+    max_meta = std::max(max_meta, d.m);
+    // staged bytes + a fixed per-tile cost (barrier round trip, descriptor)
+    plan.tile_bytes.push_back(10 * static_cast<int64_t>(d.n) + 2 * static_cast<int64_t>(d.m) + 16384);
+    const int64_t j0 = static_cast<int64_t>(joff.size());
+    for (int32_t slot = 0; slot < n_r; ++slot) {
+      const int64_t run = static_cast<int64_t>(sp.s) * nw + order[sp.s][sp.b + slot];
+      off[run] = static_cast<int32_t>(cursor);
+      jx[run] = static_cast<int32_t>((j0 + L.sj[slot / 32]) * 32 + slot % 32);
     }
+    joff.insert(joff.end(), L.joff.begin(), L.joff.end());
+    meta.insert(meta.end(), L.meta.begin(), L.meta.end());
+    meta.resize((meta.size() + 7) & ~std::size_t{7}, 0);
+    cursor += d.n;
+  }
   if (cursor > INT32_MAX || max_tile > ecap || max_meta > kSlabMetaCap ||
       static_cast<int64_t>(joff.size()) * 32 > INT32_MAX) {  // int32 offsets; tiles must fit a stage
     plan = SlabPlan{};
@@ -440,6 +400,7 @@ void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const in
   RB_LAUNCH_CHECK();
   tr.mark("    upload + fill");
   plan.partial.alloc(runs);
+  plan.partial.zero(st);  // (window, row) pairs without entries keep 0
   {
     std::vector<int32_t> widx(nr, -1), wrow(nw);
     for (int32_t k = 0; k < nw; ++k) widx[rows[k] - r0] = k, wrow[k] = rows[k] - r0;
@@ -451,11 +412,10 @@ void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const in
   SlabView& v = plan.view;
   v.nw = nw;
   v.S = S;
-  v.J = J;
+  v.J = ntiles;
   v.seg = seg;
   v.ecap = ecap;
   v.mcap = kSlabMetaCap;
-  v.jagged = jagged ? 1 : 0;
   v.win_max = 0;
   for (int s = 0; s < S; ++s) {
     v.win[s] = choice.windows[s];
@@ -473,13 +433,13 @@ void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const in
   RB_CUDA(cudaStreamSynchronize(st));
   if (std::getenv("RAPDHG_TRACE"))
     std::fprintf(stderr, "[slab] seg %d rows [%d,%d): W rows %d windows %d chunks %d tiles %d entries %lld (%.3f padded, %s)\n",
-                 seg, r0, r1, nw, S, J, S * J, static_cast<long long>(cursor),
+                 seg, r0, r1, nw, S, ntiles, ntiles, static_cast<long long>(cursor),
                  static_cast<double>(cursor) / std::max<int64_t>(1, [&] {
                    int64_t t = 0;
                    for (int32_t c : hc2) t += c;
                    return t;
                  }()),
-                 jagged ? "jagged" : "sliced");
+                 "sliced");
 }
 
 void fill_slab_values(SlabPlan& plan, const double* v1, const double* v2, cudaStream_t st) {

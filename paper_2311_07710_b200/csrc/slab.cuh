@@ -65,29 +65,24 @@ struct SlabTile {
   int32_t pad;
 };
 
-// Per-tile metadata (uint16): perm[nr] (sorted slot -> row of the chunk),
-// len[nr] (run length per sorted slot), soff[nsl + 1] (slice starts, entries
-// relative to the tile). Lane l's entry e of slice q sits at
-//   padded: soff[q] + 32 e + l (every slice as wide as its longest run), or
-//   jagged: soff[q] + sum_{e' < e} cnt_e' + l, where entry e of the lanes
-//   whose run is longer than e (lanes 0 .. cnt_e - 1: rows are sorted) is
-//   contiguous and cnt_e = popc(ballot(len > e)) — no padding, no stored
-//   offsets, but unaligned warp rows (more smem wavefronts): chosen per op
-//   when padding would exceed kSlabJaggedPad.
-constexpr double kSlabJaggedPad = 1.25;  // padded/actual entries above which tiles are jagged
-constexpr int kSlabMetaCap = 2 * kSlabRowCap + kSlabRowCap / 32 + 8;  // per tile (multiple of 8)
+// Per-tile metadata (uint16 elements): perm (uint32 W-row index per slot, 2
+// elements each) | len[nr] (run length per slot) | soff[nsl + 1] (slice
+// starts, entries relative to the tile). Lane l's entry e of slice q sits at
+// soff[q] + 32 e + l. A window's tiles hold its W rows sorted by their run
+// length there, so the 32 rows of a slice have nearly equal runs (≈ no
+// padding) whatever the window.
+constexpr int kSlabMetaCap = 3 * kSlabRowCap + kSlabRowCap / 32 + 8;  // per tile (multiple of 8)
 struct SlabView {
   int32_t nw = 0;                  // W rows
   int32_t S = 0;                   // windows (even lengths)
-  int32_t J = 0;                   // row chunks
+  int32_t J = 0;                   // tiles
   int32_t seg = 0;                 // accumulator the windows feed (0: segment 1, 1: segment 2)
   int32_t win_max = 0;             // widest window (doubles, even)
   int32_t ecap = 0;                // tile entry capacity (multiple of 8)
   int32_t mcap = 0;                // tile metadata capacity (multiple of 8)
   int32_t grid = 0;                // persistent CTAs
-  int32_t jagged = 0;              // 1: jagged slices (no padding), 0: 32-wide padded slices
   Window win[kMaxSlabs];
-  const SlabTile* tile = nullptr;   // [S * J]
+  const SlabTile* tile = nullptr;   // [J]
   const int32_t* cta = nullptr;     // [grid + 1] tile ranges per CTA (balanced by bytes)
   const uint16_t* meta = nullptr;   // per-tile metadata
   const uint16_t* col = nullptr;    // column offset inside the window
@@ -97,7 +92,7 @@ struct SlabView {
   CsrView rest1{}, rest2{};         // rest CSRs over W rows (segment 1 / 2)
   unsigned long long* prof = nullptr;  // [grid * kSlabProf] phase times (RB_SLAB_PROFILE builds)
   bool active() const { return nw > 0 && S > 0; }
-  __host__ __device__ int tiles() const { return S * J; }
+  __host__ __device__ int tiles() const { return J; }
   // stage: [header 16 B][window][values][columns][metadata]
   // smem: [window][stage 0] .. [stage kSlabStages - 1];
   // stage: [header 16 B][values][columns][metadata]
@@ -204,7 +199,7 @@ __device__ __forceinline__ void slab_issue(const Op& op, const SlabView& sv, con
   uint16_t* meta = col + sv.ecap;
   const uint32_t m8 = static_cast<uint32_t>(d.m + 7) & ~7u;
   const uint32_t wbytes = copy_window ? static_cast<uint32_t>(w.len) * 8u : 0u;
-  hdr[0] = d.k0;
+  hdr[0] = 0;
   hdr[1] = d.nr;
   hdr[2] = d.s;
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic accesses of the buffers before
@@ -246,7 +241,7 @@ constexpr int kSlabThreads = 32 * (kSlabConsumers + 1);  // + one producer warp
 // stage, take every kSlabConsumers-th slice of it (dealt on a counter that
 // runs across tiles, so the warps share the work evenly without a CTA-wide
 // barrier) and arrive on the stage's empty barrier when done.
-template <class Op, bool Jagged>
+template <class Op>
 __global__ void __launch_bounds__(kSlabThreads) slab_kernel(const Op op, const SlabView sv) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[kSlabStages], empty[kSlabStages];
@@ -303,29 +298,28 @@ __global__ void __launch_bounds__(kSlabThreads) slab_kernel(const Op op, const S
     SLAB_ADD(2, t_w1 - t_w0);
     SLAB_ADD(7, 1);
     const int32_t* hdr = reinterpret_cast<const int32_t*>(base);
-    const int k0 = hdr[0], nr = hdr[1], s = hdr[2];
+    const int nr = hdr[1], s = hdr[2];
     const double* val = reinterpret_cast<const double*>(base + 16);
     const uint16_t* col = reinterpret_cast<const uint16_t*>(val + sv.ecap);
-    const uint16_t* perm = col + sv.ecap;
-    const uint16_t* len = perm + nr;
+    const uint32_t* perm = reinterpret_cast<const uint32_t*>(col + sv.ecap);
+    const uint16_t* len = reinterpret_cast<const uint16_t*>(perm + nr);
     const uint16_t* soff = len + nr;
-    double* partial = sv.partial + static_cast<int64_t>(s) * sv.nw + k0;
+    double* partial = sv.partial + static_cast<int64_t>(s) * sv.nw;
     const int nsl = (nr + 31) >> 5;
     for (int q = (warp - deal + kSlabConsumers) % kSlabConsumers; q < nsl; q += kSlabConsumers) {
       const int slot = (q << 5) + lane;
       const int L = slot < nr ? len[slot] : 0;
       const int Lm = len[q << 5];  // the slice's longest run (lane 0: sorted)
-      int a = soff[q];             // start of entry e's lanes
+      const double* vq = val + soff[q] + lane;
+      const uint16_t* cq = col + soff[q] + lane;
       double part = 0.0;
       for (int e = 0; e < Lm; e += 4) {
         double v[4], x[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const bool ok = L > e + u;
-          v[u] = ok ? val[a + lane] : 0.0;
-          x[u] = ok ? win[col[a + lane]] : 0.0;
-          if constexpr (Jagged) a += __popc(__ballot_sync(0xffffffffu, ok));
-          else a += 32;
+          v[u] = ok ? vq[(e + u) << 5] : 0.0;
+          x[u] = ok ? win[cq[(e + u) << 5]] : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) part = fma(v[u], x[u], part);
@@ -396,11 +390,9 @@ __global__ void __launch_bounds__(kBlock) slab_finish_kernel(const Op op, const 
 // capture) and return the persistent grid for that smem size.
 template <class Op>
 inline int prepare_slab(int smem_bytes) {
-  const void* k0 = reinterpret_cast<const void*>(&slab_kernel<Op, false>);
-  const void* k1 = reinterpret_cast<const void*>(&slab_kernel<Op, true>);
-  RB_CUDA(cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
-  RB_CUDA(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
-  return slab_grid(k0, smem_bytes);
+  const void* k = reinterpret_cast<const void*>(&slab_kernel<Op>);
+  RB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
+  return slab_grid(k, smem_bytes);
 }
 
 // A slab-tiled op: the plan and the finish schedule over all of its rows.
@@ -427,8 +419,7 @@ void assign_slab_ctas(SlabPlan& plan, int grid, cudaStream_t st);
 template <class Op>
 inline int launch_slab_phase(const Op& op, const SlabPhase& ph, cudaStream_t st) {
   const SlabView& sv = ph.plan.view;
-  if (sv.jagged) slab_kernel<Op, true><<<sv.grid, kSlabThreads, sv.smem_bytes(), st>>>(op, sv);
-  else slab_kernel<Op, false><<<sv.grid, kSlabThreads, sv.smem_bytes(), st>>>(op, sv);
+  slab_kernel<Op><<<sv.grid, kSlabThreads, sv.smem_bytes(), st>>>(op, sv);
   RB_LAUNCH_CHECK();
   const SchedView& o = ph.others.view;
   const int wblocks = static_cast<int>(ceil_div(sv.nw, kBlock));

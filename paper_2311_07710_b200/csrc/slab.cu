@@ -152,6 +152,7 @@ std::vector<int32_t> scan_host(const std::vector<int32_t>& cnt) {
 // of each entry e (fill_kernel only); offsets relative to the tile's first
 // entry.
 struct TileLayout {
+  std::vector<int32_t> rows;  // the tile's W rows in slot order
   std::vector<uint16_t> meta;
   std::vector<int32_t> joff;  // slice q's offsets start at joff[sj[q]]
   std::vector<int32_t> sj;
@@ -274,58 +275,116 @@ void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const in
   RB_LAUNCH_CHECK();
   const std::vector<int32_t> hc2 = download(c2, runs, st), hrw = download(rw, nw, st), hro = download(ro, nw, st);
   tr.mark("    counts");
-  // Tiles, per window: the W rows with entries in the window, sorted by their
-  // run length there (descending, stable), cut into tiles of whole 32-row
-  // slices while the (slice-padded) entries fit the stage and the rows fit
-  // the row cap. Rows with an empty run in a window appear in none of its
-  // tiles (their partial stays the zero written at setup).
+  // Tiles, per window, of whole 32-row slices (slice-padded entries within
+  // the stage, rows within the row cap), from one of two row orders:
+  //  * natural: the window's W rows in index order, each tile's rows sorted
+  //    by run length — neighbouring rows share tiles, so partial writes and
+  //    the finish pass stay coalesced;
+  //  * sorted: all the window's W rows sorted by run length first — slices of
+  //    nearly equal runs, no padding, but scattered partial writes.
+  // Natural unless its padding exceeds kSlabNaturalPad (RAPDHG_SLAB_ORDER=
+  // natural|sorted forces). Rows with an empty run in a window appear in none
+  // of its tiles (their partial stays the zero written at setup).
   const int ecap = (std::min(32736, std::max(256, env_int("RAPDHG_SLAB_TILE", kSlabTileCap))) + 31) & ~31;
   const int rcap = kSlabRowCap;
-  std::vector<std::vector<int32_t>> order(S);  // per window: sorted W rows
-  parallel_for(S, [&](int64_t si) {
-    const int s = static_cast<int>(si);
-    const int32_t* len = hc2.data() + static_cast<int64_t>(s) * nw;
-    std::vector<int32_t> start(kSlabRunCap + 2, 0);
-    for (int32_t k = 0; k < nw; ++k) ++start[kSlabRunCap - len[k] + 1];
-    for (int v = 1; v <= kSlabRunCap + 1; ++v) start[v] += start[v - 1];
-    std::vector<int32_t> o(nw);
-    for (int32_t k = 0; k < nw; ++k) o[start[kSlabRunCap - len[k]]++] = k;
-    int32_t cnt = nw;
-    while (cnt > 0 && len[o[cnt - 1]] == 0) --cnt;  // empty runs last
-    o.resize(cnt);
-    order[s] = std::move(o);
-  });
   struct TileSpan {
     int s;
     int32_t b, e;  // range of order[s]
   };
-  std::vector<TileSpan> spans;
-  for (int s = 0; s < S; ++s) {
-    const std::vector<int32_t>& o = order[s];
-    const int32_t* len = hc2.data() + static_cast<int64_t>(s) * nw;
-    int32_t b = 0;
-    int64_t padded = 0;
-    for (int32_t q = 0; q < static_cast<int32_t>(o.size()); q += 32) {  // slice starting at q
-      const int64_t w = 32 * static_cast<int64_t>(len[o[q]]);
-      const int32_t qe = std::min<int32_t>(static_cast<int32_t>(o.size()), q + 32);
-      if (q > b && (padded + w > ecap || qe - b > rcap)) {
-        spans.push_back({s, b, q});
-        b = q;
-        padded = 0;
+  auto build = [&](bool sorted, std::vector<std::vector<int32_t>>& order, std::vector<TileSpan>& spans,
+                   std::vector<TileLayout>& lay) {
+    order.assign(S, {});
+    parallel_for(S, [&](int64_t si) {
+      const int s = static_cast<int>(si);
+      const int32_t* len = hc2.data() + static_cast<int64_t>(s) * nw;
+      std::vector<int32_t> o;
+      o.reserve(nw);
+      if (sorted) {
+        std::vector<int32_t> start(kSlabRunCap + 2, 0);
+        for (int32_t k = 0; k < nw; ++k) ++start[kSlabRunCap - len[k] + 1];
+        for (int v = 1; v <= kSlabRunCap + 1; ++v) start[v] += start[v - 1];
+        o.resize(nw);
+        for (int32_t k = 0; k < nw; ++k) o[start[kSlabRunCap - len[k]]++] = k;
+        int32_t cnt = nw;
+        while (cnt > 0 && len[o[cnt - 1]] == 0) --cnt;  // empty runs last
+        o.resize(cnt);
+      } else {
+        for (int32_t k = 0; k < nw; ++k)
+          if (len[k] > 0) o.push_back(k);
       }
-      padded += w;
+      order[s] = std::move(o);
+    });
+    spans.clear();
+    for (int s = 0; s < S; ++s) {
+      const std::vector<int32_t>& o = order[s];
+      const int32_t* len = hc2.data() + static_cast<int64_t>(s) * nw;
+      const int32_t no = static_cast<int32_t>(o.size());
+      int32_t b = 0;
+      int64_t acc = 0;
+      for (int32_t q = 0; q < no; q += 32) {  // group of 32 rows starting at q
+        const int32_t qe = std::min(no, q + 32);
+        int64_t w = 0;  // sorted: the slice's padded width; natural: raw entries (7/8 budget below)
+        if (sorted) w = 32 * static_cast<int64_t>(len[o[q]]);
+        else
+          for (int32_t i = q; i < qe; ++i) w += len[o[i]];
+        const int64_t cap = sorted ? ecap : ecap * 7 / 8;
+        if (q > b && (acc + w > cap || qe - b > rcap)) {
+          spans.push_back({s, b, q});
+          b = q;
+          acc = 0;
+        }
+        acc += w;
+      }
+      if (b < no) spans.push_back({s, b, no});
     }
-    if (b < static_cast<int32_t>(o.size())) spans.push_back({s, b, static_cast<int32_t>(o.size())});
+    for (;;) {  // lay out (rows of a tile sorted by run); split tiles that overflow
+      lay.assign(spans.size(), TileLayout{});
+      parallel_for(static_cast<int64_t>(spans.size()), [&](int64_t t) {
+        const TileSpan& sp = spans[t];
+        const int32_t* len = hc2.data() + static_cast<int64_t>(sp.s) * nw;
+        std::vector<int32_t> rows_t(order[sp.s].begin() + sp.b, order[sp.s].begin() + sp.e);
+        std::stable_sort(rows_t.begin(), rows_t.end(), [&](int32_t x, int32_t y) { return len[x] > len[y]; });
+        std::vector<int32_t> len_t(rows_t.size());
+        for (std::size_t i = 0; i < rows_t.size(); ++i) len_t[i] = len[rows_t[i]];
+        lay[t] = layout_tile(rows_t.data(), len_t.data(), static_cast<int32_t>(rows_t.size()));
+        lay[t].rows = std::move(rows_t);
+      });
+      std::vector<TileSpan> next;
+      bool split = false;
+      for (std::size_t t = 0; t < spans.size(); ++t) {
+        const TileSpan& sp = spans[t];
+        if (lay[t].n > ecap && sp.e - sp.b > 32) {
+          const int32_t mid = sp.b + std::max<int32_t>(32, ((sp.e - sp.b) / 2) & ~31);
+          next.push_back({sp.s, sp.b, mid});
+          next.push_back({sp.s, mid, sp.e});
+          split = true;
+        } else {
+          next.push_back(sp);
+        }
+      }
+      if (!split) break;
+      spans.swap(next);
+    }
+  };
+  std::vector<std::vector<int32_t>> order;
+  std::vector<TileSpan> spans;
+  std::vector<TileLayout> lay;
+  bool sorted = false;
+  {
+    const char* mode = std::getenv("RAPDHG_SLAB_ORDER");
+    sorted = mode && std::string(mode) == "sorted";
+    build(sorted, order, spans, lay);
+    if (!mode) {  // natural unless it pads too much
+      int64_t padded = 0, actual = 0;
+      for (const TileLayout& L : lay) padded += L.n;
+      for (int32_t c : hc2) actual += c;
+      if (static_cast<double>(padded) > kSlabNaturalPad * static_cast<double>(std::max<int64_t>(actual, 1))) {
+        sorted = true;
+        build(true, order, spans, lay);
+      }
+    }
   }
   const int32_t ntiles = static_cast<int32_t>(spans.size());
-  std::vector<TileLayout> lay(ntiles);
-  parallel_for(ntiles, [&](int64_t t) {
-    const TileSpan& sp = spans[t];
-    const int32_t nr_t = sp.e - sp.b;
-    std::vector<int32_t> rows_t(order[sp.s].begin() + sp.b, order[sp.s].begin() + sp.e), len_t(nr_t);
-    for (int32_t i = 0; i < nr_t; ++i) len_t[i] = hc2[static_cast<int64_t>(sp.s) * nw + rows_t[i]];
-    lay[t] = layout_tile(rows_t.data(), len_t.data(), nr_t);
-  });
   tr.mark("    tiles + layouts");
   // tile arrays: window-major, each tile 32-entry aligned; run (s, k): tile
   // base off[s * nw + k] and jx[s * nw + k] (see fill_kernel)
@@ -352,7 +411,7 @@ void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const in
     plan.tile_bytes.push_back(10 * static_cast<int64_t>(d.n) + 2 * static_cast<int64_t>(d.m) + 16384);
     const int64_t j0 = static_cast<int64_t>(joff.size());
     for (int32_t slot = 0; slot < n_r; ++slot) {
-      const int64_t run = static_cast<int64_t>(sp.s) * nw + order[sp.s][sp.b + slot];
+      const int64_t run = static_cast<int64_t>(sp.s) * nw + L.rows[slot];
       off[run] = static_cast<int32_t>(cursor);
       jx[run] = static_cast<int32_t>((j0 + L.sj[slot / 32]) * 32 + slot % 32);
     }
@@ -439,7 +498,7 @@ void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const in
                    for (int32_t c : hc2) t += c;
                    return t;
                  }()),
-                 "sliced");
+                 sorted ? "sorted" : "natural");
 }
 
 void fill_slab_values(SlabPlan& plan, const double* v1, const double* v2, cudaStream_t st) {

@@ -71,6 +71,7 @@ struct SlabTile {
 // soff[q] + 32 e + l. A window's tiles hold its W rows sorted by their run
 // length there, so the 32 rows of a slice have nearly equal runs (≈ no
 // padding) whatever the window.
+constexpr double kSlabNaturalPad = 1.12;  // natural row order unless its slices pad more than this
 constexpr int kSlabMetaCap = 3 * kSlabRowCap + kSlabRowCap / 32 + 8;  // per tile (multiple of 8)
 struct SlabView {
   int32_t nw = 0;                  // W rows

@@ -71,6 +71,7 @@ struct SlabTile {
 // soff[q] + 32 e + l. A window's tiles hold its W rows sorted by their run
 // length there, so the 32 rows of a slice have nearly equal runs (≈ no
 // padding) whatever the window.
+constexpr int kSlabGroupedS = 16;        // finish: 8 warps share a row's partials from this many windows
 constexpr double kSlabNaturalPad = 1.12;  // natural row order unless its slices pad more than this
 constexpr int kSlabMetaCap = 3 * kSlabRowCap + kSlabRowCap / 32 + 8;  // per tile (multiple of 8)
 struct SlabView {
@@ -341,11 +342,10 @@ inline int SlabView::smem_bytes() const { return win_max * 8 + kSlabStages * sta
 
 // The rows of Op after the slab kernel, one launch (a programmatic dependent
 // launch of the slab kernel):
-//  * the last wblocks blocks: W rows, one thread per row — epilogue inputs
-//    prefetched, then (after the slab grid completes) the row's rest entries
-//    in order, plus its S window partials summed in window order (a warp's
-//    32 consecutive W rows read each window's partials coalesced), then the
-//    epilogue; the per-row order is fixed, so results are deterministic and
+//  * the last wblocks blocks: W rows, 32 per block — epilogue inputs and the
+//    rest entries before the wait, then the S window partials (warp g sums
+//    windows g, g + 8, ..., the 8 sums added in order), then the epilogue;
+//    the per-row order depends only on S, so results are deterministic and
 //    shard-invariant;
 //  * the first blocks: ordinary rowwise tiles of the rows without partials
 //    (no wait: they overlap the slab kernel; scheduled first so the waiting
@@ -359,31 +359,64 @@ __global__ void __launch_bounds__(kBlock) slab_finish_kernel(const Op op, const 
     rowwise_tile(op, others, blockIdx.x, g);
     return;
   }
-  // last: the W rows, whose blocks wait for the slab grid
-  const int k = (blockIdx.x - ob) * kBlock + threadIdx.x;
+  // last: the W rows, whose blocks wait for the slab grid. The epilogue
+  // inputs and the rest entries (independent of the slab kernel) are loaded
+  // and summed before the wait. With many windows (S >= kSlabGroupedS) a
+  // block takes 32 rows and warp g sums the partials of windows g, g + 8, ...
+  // (one round of independent loads; warp 0 adds the 8 sums in order); with
+  // few, a thread takes one row and sums its S partials in order.
+  const bool grouped = sv.S >= kSlabGroupedS;
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int k = grouped ? (blockIdx.x - ob) * 32 + lane : (blockIdx.x - ob) * kBlock + threadIdx.x;
   const bool valid = k < sv.nw;
-  const int r = valid ? sv.wrow[k] : 0;
-  typename Op::Pre pre{};
-  if (valid) pre = op.prefetch(r);
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // the slab kernel's partials are complete
-  if (!valid) return;
-  const Gather gl[2] = {Gather{rest.gather_src(0), nullptr, 0, 0u}, Gather{rest.gather_src(1), nullptr, 0, 0u}};
+  const bool owner = valid && (!grouped || g == 0);  // runs the row's epilogue
   typename Op::AccT a;
   a.zero();
-  rest.template accumulate<kUnroll>(k, 0, rest.len(k), 0, 1, a, gl);
-  const double* p = sv.partial + k;
-  double t = 0.0;
-  int q = 0;
-  for (; q + 8 <= sv.S; q += 8) {
-    double v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = __ldcg(p + static_cast<int64_t>(q + u) * sv.nw);
-#pragma unroll
-    for (int u = 0; u < 8; ++u) t += v[u];
+  typename Op::Pre pre{};
+  int r = 0;
+  if (owner) {
+    r = sv.wrow[k];
+    pre = op.prefetch(r);
+    const Gather gl[2] = {Gather{rest.gather_src(0), nullptr, 0, 0u}, Gather{rest.gather_src(1), nullptr, 0, 0u}};
+    rest.template accumulate<kUnroll>(k, 0, rest.len(k), 0, 1, a, gl);
   }
-  for (; q < sv.S; ++q) t += __ldcg(p + static_cast<int64_t>(q) * sv.nw);
-  if (sv.seg == 0) a.v[0] += t;
-  else a.v[Op::AccT::kK - 1] += t;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the slab kernel's partials are complete
+  double tot = 0.0;
+  if (grouped) {
+    __shared__ double grp[kBlock / 32][32];
+    constexpr int G = kBlock / 32;
+    double t = 0.0;
+    if (valid) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {  // S <= kMaxSlabs = 8 G
+        const int s = g + u * G;
+        v[u] = s < sv.S ? __ldcg(sv.partial + static_cast<int64_t>(s) * sv.nw + k) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) t += v[u];
+    }
+    grp[g][lane] = t;
+    __syncthreads();
+    if (!owner) return;
+    tot = grp[0][lane];
+#pragma unroll
+    for (int q = 1; q < G; ++q) tot += grp[q][lane];
+  } else {
+    if (!owner) return;
+    const double* p = sv.partial + k;
+    int q = 0;
+    for (; q + 8 <= sv.S; q += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcg(p + static_cast<int64_t>(q + u) * sv.nw);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) tot += v[u];
+    }
+    for (; q < sv.S; ++q) tot += __ldcg(p + static_cast<int64_t>(q) * sv.nw);
+  }
+  if (sv.seg == 0) a.v[0] += tot;
+  else a.v[Op::AccT::kK - 1] += tot;
   op.finish(r, a, pre);
 }
 
@@ -423,7 +456,7 @@ inline int launch_slab_phase(const Op& op, const SlabPhase& ph, cudaStream_t st)
   slab_kernel<Op><<<sv.grid, kSlabThreads, sv.smem_bytes(), st>>>(op, sv);
   RB_LAUNCH_CHECK();
   const SchedView& o = ph.others.view;
-  const int wblocks = static_cast<int>(ceil_div(sv.nw, kBlock));
+  const int wblocks = static_cast<int>(ceil_div(sv.nw, sv.S >= kSlabGroupedS ? 32 : kBlock));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(wblocks + (o.total_blocks > 0 ? o.total_blocks : 0)));
   cfg.blockDim = dim3(kBlock);

@@ -38,6 +38,12 @@ __global__ void unscale_kernel(const double* x, const double* xb, const double* 
   }
 }
 
+// (a[i], b[i]) pairs, so one 16 B gather serves both KKT points.
+__global__ void interleave_kernel(const double* a, const double* b, double2* out, int64_t n) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) out[i] = make_double2(a[i], b[i]);
+}
+
 // Restart (solver.hpp:442-448): optionally x <- xbar, y <- ybar; then
 // x_prev <- x, xbar <- x, ybar <- y.
 __global__ void restart_kernel(double* x, double* xp, double* xb, double* y, double* yb,

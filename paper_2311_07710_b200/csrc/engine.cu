@@ -408,6 +408,7 @@ Engine::Engine(const rapdhg_qp& p, const rapdhg_config& cfg, Clock::time_point t
   // iterate and check buffers
   for (int i = 0; i < 2; ++i) {
     X_[i].alloc(n_), XMD_[i].alloc(n_), xu_[i].alloc(n_), yu_[i].alloc(m_);
+    if (i == 0) xi_.alloc(n_), yi_.alloc(m_);
     ax_[i].alloc(m_), qx_[i].alloc(n_), aty_[i].alloc(n_);
   }
   w_.alloc(n_), xb_.alloc(n_), y_.alloc(m_), yb_.alloc(m_), epx_.alloc(n_), epy_.alloc(m_);
@@ -626,16 +627,20 @@ Cand Engine::evaluate() {
   RB_LAUNCH_CHECK();
   ++launches_;
   DeviceQP& P = *P_;
+  interleave_kernel<<<grid1(n_), 256, 0, st_>>>(xu_[0].get(), xu_[1].get(), xi_.get(), n_);
+  interleave_kernel<<<grid1(m_), 256, 0, st_>>>(yu_[0].get(), yu_[1].get(), yi_.get(), m_);
+  RB_LAUNCH_CHECK();
+  launches_ += 2;
   if (P.strict) {
-    KktAxOp<true> ax{P.A.view(), xu_[0].get(), xu_[1].get(), ax_[0].get(), ax_[1].get()};
+    KktAxOp<true> ax{P.A.view(), xi_.get(), ax_[0].get(), ax_[1].get()};
     rowwise(ax, P.sch_dual, st_, &launches_);
-    KktQAtyOp<true> qa{P.Q.view(), P.AT.view(), mi_, xu_[0].get(), xu_[1].get(), yu_[0].get(), yu_[1].get(),
+    KktQAtyOp<true> qa{P.Q.view(), P.AT.view(), mi_, xi_.get(), yi_.get(),
                        qx_[0].get(), qx_[1].get(), aty_[0].get(), aty_[1].get()};
     rowwise(qa, P.sch_primal, st_, &launches_);
   } else {
-    KktAxOp<false> ax{P.A.view(), xu_[0].get(), xu_[1].get(), ax_[0].get(), ax_[1].get()};
+    KktAxOp<false> ax{P.A.view(), xi_.get(), ax_[0].get(), ax_[1].get()};
     rowwise(ax, P.sch_dual, st_, &launches_);
-    KktQAtyOp<false> qa{P.Q.view(), P.AT.view(), mi_, xu_[0].get(), xu_[1].get(), yu_[0].get(), yu_[1].get(),
+    KktQAtyOp<false> qa{P.Q.view(), P.AT.view(), mi_, xi_.get(), yi_.get(),
                         qx_[0].get(), qx_[1].get(), aty_[0].get(), aty_[1].get()};
     rowwise(qa, P.sch_primal, st_, &launches_);
   }
@@ -1011,15 +1016,19 @@ void api_rel_kkt(const rapdhg_qp& p, const double* x, const double* yi, const do
   yu.upload(yi, mi, sg.s);
   if (m - mi) RB_CUDA(cudaMemcpyAsync(yu.get() + mi, ye, sizeof(double) * (m - mi), cudaMemcpyHostToDevice, sg.s));
   int64_t l = 0;
+  DevBuf<double2> xi(n), yi2(m);
+  interleave_kernel<<<grid1(n), 256, 0, sg.s>>>(xu.get(), xu.get(), xi.get(), n);
+  interleave_kernel<<<grid1(m), 256, 0, sg.s>>>(yu.get(), yu.get(), yi2.get(), m);
+  RB_LAUNCH_CHECK();
   if (strict) {
-    rowwise(KktAxOp<true>{P.A.view(), xu.get(), xu.get(), ax.get(), ax2.get()}, P.sch_dual, sg.s, &l);
-    rowwise(KktQAtyOp<true>{P.Q.view(), P.AT.view(), mi, xu.get(), xu.get(), yu.get(), yu.get(), qx.get(),
-                            qx2.get(), aty.get(), aty2.get()},
+    rowwise(KktAxOp<true>{P.A.view(), xi.get(), ax.get(), ax2.get()}, P.sch_dual, sg.s, &l);
+    rowwise(KktQAtyOp<true>{P.Q.view(), P.AT.view(), mi, xi.get(), yi2.get(), qx.get(), qx2.get(), aty.get(),
+                            aty2.get()},
             P.sch_primal, sg.s, &l);
   } else {
-    rowwise(KktAxOp<false>{P.A.view(), xu.get(), xu.get(), ax.get(), ax2.get()}, P.sch_dual, sg.s, &l);
-    rowwise(KktQAtyOp<false>{P.Q.view(), P.AT.view(), mi, xu.get(), xu.get(), yu.get(), yu.get(), qx.get(),
-                             qx2.get(), aty.get(), aty2.get()},
+    rowwise(KktAxOp<false>{P.A.view(), xi.get(), ax.get(), ax2.get()}, P.sch_dual, sg.s, &l);
+    rowwise(KktQAtyOp<false>{P.Q.view(), P.AT.view(), mi, xi.get(), yi2.get(), qx.get(), qx2.get(), aty.get(),
+                             aty2.get()},
             P.sch_primal, sg.s, &l);
   }
   const double *axp = ax.get(), *b = P.b.get(), *yp = yu.get();

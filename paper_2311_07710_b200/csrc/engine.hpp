@@ -175,6 +175,7 @@ class Engine : public LoopBackend {
   int cur_ = 0;
   // check workspace (unscaled)
   DevBuf<double> xu_[2], yu_[2], ax_[2], qx_[2], aty_[2], best_x_, best_y_;
+  DevBuf<double2> xi_, yi_;  // (current, average) interleaved for the KKT products
   // per-chunk params
   DevBuf<IterParams> params_;
   PinnedBuf<IterParams> params_h_;

@@ -197,15 +197,14 @@ struct KktAxOp {
   __device__ __forceinline__ const double* gather_src(int) const { return nullptr; }
   using AccT = Acc<2>;
   CsrView a;
-  const double* xc;
-  const double* xa;
+  const double2* x;  // (current, average) interleaved
   double* axc;
   double* axa;
   __device__ __forceinline__ int len(int r) const { return a.rp[r + 1] - a.rp[r]; }
   template <int U>
   __device__ __forceinline__ void accumulate(int r, int lo, int hi, int lane, int stride,
                                              AccT& acc, const Gather* g) const {
-    seg_dot2<Strict, false, U>(a.v, a.ci, xc, xa, a.rp[r], lo + lane, hi, stride, 0, acc.v);
+    seg_dot2<Strict, false, U>(a.v, a.ci, x, a.rp[r], lo + lane, hi, stride, 0, acc.v);
   }
   __device__ __forceinline__ void finish(int r, const AccT& acc) const {
     axc[r] = acc.v[0];
@@ -225,7 +224,7 @@ struct KktQAtyOp {
   using AccT = Acc<6>;
   CsrView q, at;
   int m_ineq;
-  const double *xc, *xa, *yc, *ya;
+  const double2 *x, *y;  // (current, average) interleaved
   double *qxc, *qxa, *atyc, *atya;
   __device__ __forceinline__ int len(int r) const {
     return (q.rp[r + 1] - q.rp[r]) + (at.rp[r + 1] - at.rp[r]);
@@ -237,8 +236,8 @@ struct KktQAtyOp {
     const int q0 = q.rp[r];
     const int L1 = q.rp[r + 1] - q0;
     const int p = lo + lane;
-    seg_dot2<Strict, false, U>(q.v, q.ci, xc, xa, q0, p, hi < L1 ? hi : L1, stride, 0, acc.v);
-    seg_dot2<Strict, true, U>(at.v, at.ci, yc, ya, static_cast<int64_t>(at.rp[r]) - L1,
+    seg_dot2<Strict, false, U>(q.v, q.ci, x, q0, p, hi < L1 ? hi : L1, stride, 0, acc.v);
+    seg_dot2<Strict, true, U>(at.v, at.ci, y, static_cast<int64_t>(at.rp[r]) - L1,
                            next_pos(p, stride, L1), hi, stride, m_ineq, acc.v + 2);
   }
   __device__ __forceinline__ void finish(int j, const AccT& acc) const {

@@ -192,8 +192,7 @@ __device__ __forceinline__ double seg_dot(const double* __restrict__ vals,
 template <bool Strict, bool Split, int U = kUnroll>
 __device__ __forceinline__ void seg_dot2(const double* __restrict__ vals,
                                          const int32_t* __restrict__ cols,
-                                         const double* __restrict__ xa,
-                                         const double* __restrict__ xb, int64_t base, int p,
+                                         const double2* __restrict__ x, int64_t base, int p,
                                          int end, int stride, int split, double* a) {
   for (; p < end; p += U * stride) {
     int32_t c[U];
@@ -208,8 +207,9 @@ __device__ __forceinline__ void seg_dot2(const double* __restrict__ vals,
 #pragma unroll
     for (int k = 0; k < U; ++k) {
       const bool ok = p + k * stride < end;
-      ua[k] = ok ? ld_gather(xa + c[k]) : 0.0;
-      ub[k] = ok ? ld_gather(xb + c[k]) : 0.0;
+      const double2 u = ok ? __ldg(x + c[k]) : make_double2(0.0, 0.0);  // one 16 B gather for both points
+      ua[k] = u.x;
+      ub[k] = u.y;
     }
 #pragma unroll
     for (int k = 0; k < U; ++k) {

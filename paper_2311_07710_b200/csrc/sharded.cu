@@ -202,6 +202,7 @@ struct ShardedEngine::Shard {
   // full-length copies; only the owned slice is computed here, the rest is
   // received by the exchanges
   DevBuf<double> X[2], XMD[2], w, xb, y, yb, epx, epy, xu[2], yu[2], ax[2], qx[2], aty[2], best_x, best_y;
+  DevBuf<double2> xi, yi;  // interleaved unscaled points for the KKT products
   DevBuf<long long> bad;
   ReduceScratch red;
   DevBuf<double> red_out;
@@ -257,6 +258,7 @@ ShardedEngine::ShardedEngine(const rapdhg_qp& p, const rapdhg_config& cfg, int p
       sh->ax[i].alloc(m), sh->qx[i].alloc(n), sh->aty[i].alloc(n);
     }
     sh->w.alloc(n), sh->xb.alloc(n), sh->y.alloc(m), sh->yb.alloc(m), sh->epx.alloc(n), sh->epy.alloc(m);
+    sh->xi.alloc(n), sh->yi.alloc(m);
     sh->best_x.alloc(n), sh->best_y.alloc(m);
     sh->bad.alloc(1);
     sh->red.init(std::max<int64_t>(n, m), st_);
@@ -426,7 +428,7 @@ long long ShardedEngine::first_bad() {
 Cand ShardedEngine::evaluate() {
   DeviceQP& P = *full_->P_;
   const Engine& e = *full_;
-  const int n = e.n_, mi = e.mi_;
+  const int n = e.n_, m = e.m_, mi = e.mi_;
   const double* d = e.d_.get();
   for (auto& sh : shards_) {  // unscale the owned slices (scaling.hpp:126-133)
     const int64_t nl = sh->p1 - sh->p0, ml = sh->d1 - sh->d0;
@@ -446,8 +448,12 @@ Cand ShardedEngine::evaluate() {
   exchange([](Shard& s) { return s.yu[0].get(); }, false);
   exchange([](Shard& s) { return s.yu[1].get(); }, false);
   for (auto& sh : shards_) {  // KKT products on the ORIGINAL matrices, owned rows
+    interleave_kernel<<<grid1(n), 256, 0, st_>>>(sh->xu[0].get(), sh->xu[1].get(), sh->xi.get(), n);
+    interleave_kernel<<<grid1(m), 256, 0, st_>>>(sh->yu[0].get(), sh->yu[1].get(), sh->yi.get(), m);
+    RB_LAUNCH_CHECK();
+    launches_ += 2;
     if (sh->d1 > sh->d0) {
-      KktAxOp<false> ax{CsrView{P.A.rp.get() + sh->d0, P.A.ci.get(), P.A.v.get()}, sh->xu[0].get(), sh->xu[1].get(),
+      KktAxOp<false> ax{CsrView{P.A.rp.get() + sh->d0, P.A.ci.get(), P.A.v.get()}, sh->xi.get(),
                         sh->ax[0].get() + sh->d0, sh->ax[1].get() + sh->d0};
       launch_rowwise(ax, sh->sch_dual.view, st_);
       ++launches_;
@@ -455,8 +461,8 @@ Cand ShardedEngine::evaluate() {
     if (sh->p1 > sh->p0) {
       const int64_t o = sh->p0;
       KktQAtyOp<false> qa{CsrView{P.Q.rp.get() + o, P.Q.ci.get(), P.Q.v.get()},
-                          CsrView{P.AT.rp.get() + o, P.AT.ci.get(), P.AT.v.get()}, mi, sh->xu[0].get(),
-                          sh->xu[1].get(), sh->yu[0].get(), sh->yu[1].get(), sh->qx[0].get() + o,
+                          CsrView{P.AT.rp.get() + o, P.AT.ci.get(), P.AT.v.get()}, mi, sh->xi.get(),
+                          sh->yi.get(), sh->qx[0].get() + o,
                           sh->qx[1].get() + o, sh->aty[0].get() + o, sh->aty[1].get() + o};
       launch_rowwise(qa, sh->sch_primal.view, st_);
       ++launches_;

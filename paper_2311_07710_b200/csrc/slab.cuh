@@ -46,7 +46,10 @@ constexpr int kSlabWidth = 2048;        // columns per window (16 KB of fp64)
 constexpr int kSlabMinRow = 16;         // in-window entries that make a W row
 constexpr double kSlabMinDensity = 16;  // gathers per column that keep a window
 constexpr int kSlabTileCap = 2816;      // entries per tile (28 KB staged)
-constexpr int kSlabStages = 3;          // tile stages per CTA (one shared window)
+#ifndef RB_SLAB_STAGES
+#define RB_SLAB_STAGES 3
+#endif
+constexpr int kSlabStages = RB_SLAB_STAGES;  // tile stages per CTA (one shared window)
 constexpr int kSlabRowCap = 512;        // rows per chunk
 constexpr int kSlabRunCap = 512;        // W rows: every window run and the rest <= this
 constexpr int kSlabMinWindows = 1;     // RAPDHG_SLAB_MIN_WINDOWS overrides

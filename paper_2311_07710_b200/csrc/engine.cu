@@ -449,12 +449,23 @@ void dump_slab_profile(const char* name, const SlabView& v) {
   std::fprintf(stderr, "[slab %s] grid %d tiles %d span %.1f us\n", name, v.grid, v.tiles(), (t1 - t0) / 1e3);
   auto row = [&](int b) {
     const unsigned long long* p = &h[b * kSlabProf];
-    std::fprintf(stderr, "  cta %3d start %6.1f wait %6.1f compute %6.1f end %6.1f tiles %llu\n", b, (p[0] - t0) / 1e3,
-                 p[2] / 1e3, p[3] / 1e3, (p[6] - t0) / 1e3, p[7]);
+    std::fprintf(stderr, "  cta %3d sm %3llu start %6.1f wait %6.1f compute %6.1f end %6.1f tiles %llu\n", b, p[8],
+                 (p[0] - t0) / 1e3, p[2] / 1e3, p[3] / 1e3, (p[6] - t0) / 1e3, p[7]);
   };
   for (int q = 0; q < 6 && q < v.grid; ++q) row(order[q]);
   std::fprintf(stderr, "  ...\n");
   for (int q = std::max(0, v.grid - 3); q < v.grid; ++q) row(order[q]);
+  // end time by SM (both CTAs of an SM), slowest / fastest SMs, and by SM id halves
+  std::vector<double> sm_end(kSMs, 0.0);
+  for (int b = 0; b < v.grid; ++b) {
+    const int sm = static_cast<int>(h[b * kSlabProf + 8]) % kSMs;
+    sm_end[sm] = std::max(sm_end[sm], (h[b * kSlabProf + 6] - t0) / 1e3);
+  }
+  double lo_half = 0, hi_half = 0;
+  for (int q = 0; q < kSMs; ++q) (q < kSMs / 2 ? lo_half : hi_half) += sm_end[q] / (kSMs / 2);
+  std::fprintf(stderr, "  mean end: SMs 0-73 %.1f us, SMs 74-147 %.1f us; by SM:", lo_half, hi_half);
+  for (int q = 0; q < kSMs; ++q) std::fprintf(stderr, "%s%.0f", q % 16 ? " " : "\n   ", sm_end[q]);
+  std::fprintf(stderr, "\n");
 }
 }  // namespace
 #endif

@@ -390,6 +390,7 @@ void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const in
   // base off[s * nw + k] and jx[s * nw + k] (see fill_kernel)
   std::vector<int32_t> off(runs, 0), jx(runs, 0), joff;
   std::vector<SlabTile> tiles(ntiles);
+  const int64_t row_cost = env_int("RAPDHG_SLAB_ROWCOST", kSlabRowCost);
   std::vector<uint16_t> meta;
   int64_t cursor = 0;
   int max_tile = 0, max_meta = 0;
@@ -407,8 +408,10 @@ void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const in
     d.m = static_cast<int32_t>(L.meta.size());
     max_tile = std::max(max_tile, d.n);
     max_meta = std::max(max_meta, d.m);
-    // staged bytes + a fixed per-tile cost (barrier round trip, descriptor)
-    plan.tile_bytes.push_back(10 * static_cast<int64_t>(d.n) + 2 * static_cast<int64_t>(d.m) + 16384);
+    // cost for balancing the CTAs' contiguous ranges: staged bytes, per-row
+    // work (length/perm loads, the partial store), a fixed per-tile cost
+    plan.tile_bytes.push_back(10 * static_cast<int64_t>(d.n) + 2 * static_cast<int64_t>(d.m) +
+                              row_cost * static_cast<int64_t>(n_r) + 16384);
     const int64_t j0 = static_cast<int64_t>(joff.size());
     for (int32_t slot = 0; slot < n_r; ++slot) {
       const int64_t run = static_cast<int64_t>(sp.s) * nw + L.rows[slot];

@@ -74,6 +74,7 @@ struct SlabTile {
 // soff[q] + 32 e + l. A window's tiles hold its W rows sorted by their run
 // length there, so the 32 rows of a slice have nearly equal runs (≈ no
 // padding) whatever the window.
+constexpr int kSlabRowCost = 0;          // CTA balance: cost per tile row, in staged-byte units
 constexpr int kSlabGroupedS = 16;        // finish: 8 warps share a row's partials from this many windows
 constexpr double kSlabNaturalPad = 1.12;  // natural row order unless its slices pad more than this
 constexpr int kSlabMetaCap = 3 * kSlabRowCap + kSlabRowCap / 32 + 8;  // per tile (multiple of 8)
@@ -339,6 +340,13 @@ __global__ void __launch_bounds__(kSlabThreads) slab_kernel(const Op op, const S
   }
   SLAB_T(t_end);
   SLAB_SET(6, t_end);
+#ifdef RB_SLAB_PROFILE
+  if (threadIdx.x == 0 && sv.prof) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    sv.prof[blockIdx.x * kSlabProf + 8] = smid;
+  }
+#endif
 }
 
 inline int SlabView::smem_bytes() const { return win_max * 8 + kSlabStages * stage_bytes(); }

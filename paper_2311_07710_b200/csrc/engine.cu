@@ -463,6 +463,13 @@ void dump_slab_profile(const char* name, const SlabView& v) {
   }
   double lo_half = 0, hi_half = 0;
   for (int q = 0; q < kSMs; ++q) (q < kSMs / 2 ? lo_half : hi_half) += sm_end[q] / (kSMs / 2);
+  {
+    unsigned long long f[4];
+    RB_CUDA(cudaMemcpy(f, v.fprof, sizeof(f), cudaMemcpyDeviceToHost));
+    std::fprintf(stderr, "  slab end %.1f | finish: other rows end %.1f, W wait done %.1f..%.1f, W end %.1f us\n",
+                 (t1 - t0) / 1e3, f[0] ? (f[0] - t0) / 1e3 : 0.0, (f[1] - t0) / 1e3, (f[2] - t0) / 1e3,
+                 (f[3] - t0) / 1e3);
+  }
   std::fprintf(stderr, "  mean end: SMs 0-73 %.1f us, SMs 74-147 %.1f us; by SM:", lo_half, hi_half);
   for (int q = 0; q < kSMs; ++q) std::fprintf(stderr, "%s%.0f", q % 16 ? " " : "\n   ", sm_end[q]);
   std::fprintf(stderr, "\n");
@@ -509,9 +516,10 @@ void Engine::setup_slabs() {
 #ifdef RB_SLAB_PROFILE
   for (SlabPlan* pl : {&dual_ph_.plan, &primal_ph_.plan})
     if (pl->view.active()) {
-      pl->prof.alloc(static_cast<std::size_t>(pl->view.grid) * kSlabProf);
+      pl->prof.alloc(static_cast<std::size_t>(pl->view.grid) * kSlabProf + 4);
       pl->prof.zero(st_);
       pl->view.prof = pl->prof.get();
+      pl->view.fprof = pl->prof.get() + static_cast<std::size_t>(pl->view.grid) * kSlabProf;
     }
 #endif
   RB_CUDA(cudaStreamSynchronize(st_));

@@ -97,6 +97,7 @@ struct SlabView {
   const int32_t* wrow = nullptr;    // [nw] W rows' ids relative to the op's row base
   CsrView rest1{}, rest2{};         // rest CSRs over W rows (segment 1 / 2)
   unsigned long long* prof = nullptr;  // [grid * kSlabProf] phase times (RB_SLAB_PROFILE builds)
+  unsigned long long* fprof = nullptr; // [4] finish kernel: max end of other rows, min/max W wait done, max W end
   bool active() const { return nw > 0 && S > 0; }
   __host__ __device__ int tiles() const { return J; }
   // stage: [header 16 B][window][values][columns][metadata]
@@ -259,6 +260,10 @@ __global__ void __launch_bounds__(kSlabThreads) slab_kernel(const Op op, const S
 #ifdef RB_SLAB_PROFILE
   if (threadIdx.x == 0 && sv.prof)
     for (int q = 0; q < kSlabProf; ++q) sv.prof[blockIdx.x * kSlabProf + q] = 0ull;
+  if (threadIdx.x == 0 && blockIdx.x == 0 && sv.fprof) {
+    sv.fprof[0] = 0ull, sv.fprof[1] = ~0ull, sv.fprof[2] = 0ull, sv.fprof[3] = 0ull;
+    __threadfence();
+  }
 #endif
   SLAB_SET(0, t_start);
   if (threadIdx.x == 0)
@@ -368,6 +373,9 @@ __global__ void __launch_bounds__(kBlock) slab_finish_kernel(const Op op, const 
   if (static_cast<int>(blockIdx.x) < ob) {  // first: the rows without partials (they start at once)
     const Gather g[2] = {Gather{op.gather_src(0), nullptr, 0, 0u}, Gather{op.gather_src(1), nullptr, 0, 0u}};
     rowwise_tile(op, others, blockIdx.x, g);
+#ifdef RB_SLAB_PROFILE
+    if (threadIdx.x == 0 && sv.fprof) atomicMax(&sv.fprof[0], slab_now());
+#endif
     return;
   }
   // last: the W rows, whose blocks wait for the slab grid. The epilogue
@@ -392,6 +400,13 @@ __global__ void __launch_bounds__(kBlock) slab_finish_kernel(const Op op, const 
     rest.template accumulate<kUnroll>(k, 0, rest.len(k), 0, 1, a, gl);
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the slab kernel's partials are complete
+#ifdef RB_SLAB_PROFILE
+  if (threadIdx.x == 0 && sv.fprof) {
+    const unsigned long long t = slab_now();
+    atomicMin(&sv.fprof[1], t);
+    atomicMax(&sv.fprof[2], t);
+  }
+#endif
   double tot = 0.0;
   if (grouped) {
     __shared__ double grp[kBlock / 32][32];
@@ -429,6 +444,9 @@ __global__ void __launch_bounds__(kBlock) slab_finish_kernel(const Op op, const 
   if (sv.seg == 0) a.v[0] += tot;
   else a.v[Op::AccT::kK - 1] += tot;
   op.finish(r, a, pre);
+#ifdef RB_SLAB_PROFILE
+  if (sv.fprof) atomicMax(&sv.fprof[3], slab_now());
+#endif
 }
 
 // Raise the dynamic smem limit of the slab kernel of Op (once, outside stream

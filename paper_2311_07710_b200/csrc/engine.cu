@@ -1,6 +1,8 @@
 // engine.cu — setup numerics and the iteration loop of the B200 rAPDHG solver.
 // See engine.hpp. Reference: /root/reference/proj/include/rapdhg/solver.hpp.
 #include <algorithm>
+#include <future>
+#include <thread>
 #include <cstdio>
 #include <cmath>
 #include <cstring>
@@ -105,14 +107,38 @@ void DeviceQP::validate_dims(const rapdhg_qp& p) {
     if (a.nnz > 0 && (!a.col_idx || !a.values)) invalid("null CSR arrays");
     if (!a.row_ptr) invalid("null CSR row_ptr");
     if (a.row_ptr[0] != 0 || a.row_ptr[a.n_rows] != a.nnz) invalid("CSR row_ptr inconsistent with nnz");
-    for (int r = 0; r < a.n_rows; ++r) {
-      const int b = a.row_ptr[r], e = a.row_ptr[r + 1];
-      if (e < b) invalid("CSR row_ptr not monotone");
-      for (int k = b; k < e; ++k) {
-        const int c = a.col_idx[k];
-        if (c < 0 || c >= a.n_cols) throw Error(RAPDHG_E_OUT_OF_RANGE, "sparse entry index out of range");
-        if (k > b && c <= a.col_idx[k - 1]) invalid("CSR columns must be strictly increasing within a row");
+    // rows in contiguous blocks on host threads; the error reported is the one a
+    // sequential scan meets first (lowest block)
+    enum { kOk, kMono, kRange, kOrder };
+    auto scan = [&](int r0, int r1) {
+      for (int r = r0; r < r1; ++r) {
+        const int b = a.row_ptr[r], e = a.row_ptr[r + 1];
+        if (e < b) return static_cast<int>(kMono);
+        for (int k = b; k < e; ++k) {
+          const int c = a.col_idx[k];
+          if (c < 0 || c >= a.n_cols) return static_cast<int>(kRange);
+          if (k > b && c <= a.col_idx[k - 1]) return static_cast<int>(kOrder);
+        }
       }
+      return static_cast<int>(kOk);
+    };
+    const int T = a.nnz < (1 << 20) ? 1 : static_cast<int>(std::min(16u, std::max(1u, std::thread::hardware_concurrency())));
+    std::vector<int> err(T, kOk);
+    if (T == 1) {
+      err[0] = scan(0, a.n_rows);
+    } else {
+      std::vector<std::thread> th;
+      for (int t = 0; t < T; ++t)
+        th.emplace_back([&, t] {
+          err[t] = scan(static_cast<int>(static_cast<int64_t>(a.n_rows) * t / T),
+                        static_cast<int>(static_cast<int64_t>(a.n_rows) * (t + 1) / T));
+        });
+      for (auto& x : th) x.join();
+    }
+    for (int e : err) {
+      if (e == kMono) invalid("CSR row_ptr not monotone");
+      if (e == kRange) throw Error(RAPDHG_E_OUT_OF_RANGE, "sparse entry index out of range");
+      if (e == kOrder) invalid("CSR columns must be strictly increasing within a row");
     }
   };
   check(p.q);
@@ -376,6 +402,7 @@ Engine::Engine(const rapdhg_qp& p, const rapdhg_config& cfg, Clock::time_point t
   tr.mark("symmetry check");
   validate_config(cfg);     // cfg.validate() (solver.hpp:278)
   n_ = P_->n, m_ = P_->m, mi_ = P_->mi;
+  if (!P_->strict) plan_slabs_async();  // reads n_, m_ and the device matrices only
 
   // scaling (solver.hpp:281-284)
   if (cfg.scaling) {
@@ -492,27 +519,51 @@ void Engine::setup_colblocks() {
                           n_, n_, m_, st_);
 }
 
+// The pattern-only part of the slab plans (windows, tiles, layouts: mostly
+// host work), on a host thread with its own stream, started once the matrices
+// are on the device so it overlaps the scaling and the power iterations.
+void Engine::plan_slabs_async() {
+  const int dev = cfg_.device;
+  plan_future_ = std::async(std::launch::async, [this, dev] {
+    RB_CUDA(cudaSetDevice(dev));
+    cudaStream_t s2;
+    RB_CUDA(cudaStreamCreate(&s2));
+    try {
+      DeviceQP& P = *P_;
+      Tracer tr(s2);
+      DevBuf<int32_t> len;
+      dual_choice_ = choose_slabs(P.A.rp.get(), P.A.ci.get(), P.A.rows, P.A.nnz, n_, s2);
+      row_lengths(len, P.A.rp.get(), nullptr, m_, s2);
+      build_slab_phase(dual_ph_, dual_choice_, 0, P.A.rp.get(), P.A.ci.get(), nullptr, nullptr, 0, m_, len.get(), s2);
+      tr.mark("  slab plan: dual (async)");
+      primal_choice_ = choose_slabs(P.AT.rp.get(), P.AT.ci.get(), n_, P.AT.nnz, m_, s2);
+      row_lengths(len, P.Q.rp.get(), P.AT.rp.get(), n_, s2);
+      build_slab_phase(primal_ph_, primal_choice_, 1, P.Q.rp.get(), P.Q.ci.get(), P.AT.rp.get(), P.AT.ci.get(), 0,
+                       n_, len.get(), s2);
+      tr.mark("  slab plan: primal (async)");
+      RB_CUDA(cudaStreamSynchronize(s2));
+    } catch (...) {
+      cudaStreamSynchronize(s2);
+      cudaStreamDestroy(s2);
+      throw;
+    }
+    RB_CUDA(cudaStreamDestroy(s2));
+  });
+}
+
 void Engine::setup_slabs() {
-  DeviceQP& P = *P_;
   Tracer tr(st_);
-  DevBuf<int32_t> len;
-  dual_choice_ = choose_slabs(P.A.rp.get(), P.A.ci.get(), P.A.rows, P.A.nnz, n_, st_);
-  row_lengths(len, P.A.rp.get(), nullptr, m_, st_);
-  build_slab_phase(dual_ph_, dual_choice_, 0, P.A.rp.get(), P.A.ci.get(), nullptr, nullptr, 0, m_, len.get(), st_);
+  plan_future_.get();  // the pattern part (plan_slabs_async)
+  tr.mark("  slab plans joined");
   if (dual_ph_.active()) {
     fill_slab_values(dual_ph_.plan, asv_, nullptr, st_);
     assign_slab_ctas(dual_ph_.plan, prepare_slab<DualStepOp<false>>(dual_ph_.plan.view.smem_bytes()), st_);
   }
-  tr.mark("  slab plan: dual");
-  primal_choice_ = choose_slabs(P.AT.rp.get(), P.AT.ci.get(), n_, P.AT.nnz, m_, st_);
-  row_lengths(len, P.Q.rp.get(), P.AT.rp.get(), n_, st_);
-  build_slab_phase(primal_ph_, primal_choice_, 1, P.Q.rp.get(), P.Q.ci.get(), P.AT.rp.get(), P.AT.ci.get(), 0, n_,
-                   len.get(), st_);
   if (primal_ph_.active()) {
     fill_slab_values(primal_ph_.plan, qsv_, atsv_, st_);
     assign_slab_ctas(primal_ph_.plan, prepare_slab<PrimalStepOp<false>>(primal_ph_.plan.view.smem_bytes()), st_);
   }
-  tr.mark("  slab plan: primal");
+  tr.mark("  slab values + launch setup");
 #ifdef RB_SLAB_PROFILE
   for (SlabPlan* pl : {&dual_ph_.plan, &primal_ph_.plan})
     if (pl->view.active()) {

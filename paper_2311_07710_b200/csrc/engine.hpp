@@ -8,6 +8,7 @@
 #pragma once
 
 #include <chrono>
+#include <future>
 #include <map>
 #include <memory>
 #include <random>
@@ -183,6 +184,8 @@ class Engine : public LoopBackend {
   PinnedBuf<long long> bad_h_;
   // slab-staged gathers (fast mode, slab.cuh): plans + the complement schedules
   void setup_slabs();
+  void plan_slabs_async();
+  std::future<void> plan_future_;
   SlabChoice dual_choice_, primal_choice_;
   SlabPhase dual_ph_, primal_ph_;
   // L2-sized column blocks (colblock.cuh) of the gather-bound ops without a slab plan

@@ -357,10 +357,12 @@ def main():
     e2e_res = None
     ecfg = rb.SolverConfig(tol=args.tol, max_iters=args.max_iters, device=local, strict_parity=args.strict)
     rb.solve(p, ecfg)  # warm-up (untimed), like the device-timed arm
+    e2e_each = []
     for _ in range(args.e2e_steps):
         t = time.perf_counter()
         e2e_res = rb.solve(p, ecfg)
-        e2e_wall += time.perf_counter() - t
+        e2e_each.append(time.perf_counter() - t)
+        e2e_wall += e2e_each[-1]
         e2e_its += e2e_res.iterations
     e2e_wall = allmax(e2e_wall)
     h2d = qp_bytes(p)
@@ -377,7 +379,8 @@ def main():
                           "1e-4": t4.solve_seconds, "iters_1e-6": e2e_res.iterations, "iters_1e-4": t4.iterations,
                           "setup_s": e2e_res.setup_seconds},
         "e2e": {"value": world * e2e_its / e2e_wall, "unit": "iter/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "wall_s_per_step": e2e_wall / max(args.e2e_steps, 1)},
+                "d2h_bytes_per_step": d2h, "wall_s_per_step": e2e_wall / max(args.e2e_steps, 1),
+                "wall_s_each": [round(w, 4) for w in e2e_each]},
         "roofline": roof, "gpu_launches": launches, "clocks": clk,
         "mode": "strict (bit-exact)" if args.strict else "fast (deterministic)",
         "generator_s": gen_s,

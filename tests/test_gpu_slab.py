@@ -69,3 +69,34 @@ def test_slab_auto_on_c2(monkeypatch):
         assert ta == tb and rel_err(za.x, zb.x) < 1e-9
         same = same and np.array_equal(za.x, zb.x)
     assert not same  # a different summation order ran: the slab tiles
+
+
+@pytest.mark.parametrize("mode", ["slab", "colblock"])
+def test_forced_paths_edge_problems(O, mode, monkeypatch):
+    """Equality-only and unconstrained problems (m = 0: no dual rows, an empty
+    A') through the forced slab / column-block paths, against the reference."""
+    if mode == "slab":
+        monkeypatch.setenv("RAPDHG_SLAB", "force")
+    else:
+        monkeypatch.setenv("RAPDHG_SLAB", "off")
+        monkeypatch.setenv("RAPDHG_L2BLOCK_KB", "1")
+    for seed, mi, me in [(9, 0, 10), (10, 0, 0), (12, 40, 0)]:
+        p = random_qp(seed, n=300, mi=mi, me=me, bounds=False)
+        cfg = rb.SolverConfig(tol=1e-8, max_iters=4000)
+        a, b = rb.solve(p, cfg), O.solve(p, cfg)
+        assert a.status == b.status
+        assert abs(a.iterations - b.iterations) <= 2 * cfg.check_interval
+        assert rel_err(a.point.x, b.point.x) < 1e-5
+
+
+def test_forced_slab_numerical_error(O, monkeypatch):
+    """A non-finite iterate under the slab path stops at the reference's
+    first bad iteration (the NaN flag sits in the finish epilogue)."""
+    monkeypatch.setenv("RAPDHG_SLAB", "force")
+    p = random_qp(6, n=300, mi=100, me=30)
+    p.c = p.c.copy()
+    p.c[0] = 1e308
+    cfg = rb.SolverConfig(tol=1e-9, max_iters=500, scaling=False)
+    a, b = rb.solve(p, cfg), O.solve(p, cfg)
+    assert a.status == b.status == rb.SolveStatus.kNumericalError
+    assert a.iterations == b.iterations

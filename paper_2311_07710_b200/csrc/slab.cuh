@@ -163,6 +163,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void mbar_expect_tx_only(uint64_t* bar, uint32_t bytes) {  // no arrival
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    smem_u32(dst)),
@@ -193,30 +196,37 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
         : "memory");
 }
 
-// Producer: arm `bar` and bulk-copy tile d into the stage at `base` (and the
-// window into `win` when it changes); the header is published to the
-// consumers by the mbarrier.
-template <class Op>
-__device__ __forceinline__ void slab_issue(const Op& op, const SlabView& sv, const SlabTile& d, double* win,
-                                           unsigned char* base, uint64_t* bar, bool copy_window) {
-  const Window w = sv.win[d.s];
+// Producer, in two parts so the entries of the first tiles can be in flight
+// before the previous kernel of the step has finished (they do not depend on
+// it): slab_entries bulk-copies tile d's values, columns and metadata into the
+// stage at `base` and announces their bytes; slab_commit adds the window when
+// it changes and arrives, completing the stage's phase. The header is
+// published to the consumers by the mbarrier.
+__device__ __forceinline__ void slab_entries(const SlabView& sv, const SlabTile& d, unsigned char* base,
+                                             uint64_t* bar) {
   int32_t* hdr = reinterpret_cast<int32_t*>(base);
   double* val = reinterpret_cast<double*>(base + 16);
   uint16_t* col = reinterpret_cast<uint16_t*>(val + sv.ecap);
   uint16_t* meta = col + sv.ecap;
   const uint32_t m8 = static_cast<uint32_t>(d.m + 7) & ~7u;
-  const uint32_t wbytes = copy_window ? static_cast<uint32_t>(w.len) * 8u : 0u;
   hdr[0] = 0;
   hdr[1] = d.nr;
   hdr[2] = d.s;
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic accesses of the buffers before
-  mbar_expect_tx(bar, wbytes + static_cast<uint32_t>(d.n) * 10u + m8 * 2u);
-  if (wbytes) bulk_g2s(win, op.gather_src(sv.seg) + w.lo, wbytes, bar);
+  mbar_expect_tx_only(bar, static_cast<uint32_t>(d.n) * 10u + m8 * 2u);
   if (d.n) {
     bulk_g2s_stream(val, sv.val + d.a, static_cast<uint32_t>(d.n) * 8u, bar);
     bulk_g2s_stream(col, sv.col + d.a, static_cast<uint32_t>(d.n) * 2u, bar);
   }
   bulk_g2s_stream(meta, sv.meta + d.meta, m8 * 2u, bar);
+}
+template <class Op>
+__device__ __forceinline__ void slab_commit(const Op& op, const SlabView& sv, const SlabTile& d, double* win,
+                                            uint64_t* bar, bool copy_window) {
+  const Window w = sv.win[d.s];
+  const uint32_t wbytes = copy_window ? static_cast<uint32_t>(w.len) * 8u : 0u;
+  mbar_expect_tx(bar, wbytes);  // arrive (+ the window's bytes)
+  if (wbytes) bulk_g2s(win, op.gather_src(sv.seg) + w.lo, wbytes, bar);
 }
 
 #ifdef RB_SLAB_PROFILE
@@ -275,26 +285,53 @@ __global__ void __launch_bounds__(kSlabThreads) slab_kernel(const Op op, const S
   // this CTA's tiles: a contiguous range of the window-major tile order, so
   // consecutive tiles mostly share their window
   const int t0 = sv.cta[blockIdx.x], t1 = sv.cta[blockIdx.x + 1];
-  // the finish kernel (a programmatic dependent launch) may start now: its
-  // rows that need no partials fill the SMs' remaining capacity
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (warp == kSlabConsumers) {  // producer
-    if (lane == 0 && t0 < t1) {
-      SlabTile d = sv.tile[t0];
+    if (lane == 0) {
+      // This launch may start while the previous kernel of the step still
+      // runs (programmatic dependent launch): the entries of the first tiles
+      // sharing the first window go out at once; the window (written by the
+      // previous kernels) only after griddepcontrol.wait. Consumers cannot
+      // pass stage 0 before its window lands, so everything they do follows
+      // the previous kernels.
+      SlabTile pend[kSlabStages];
+      int pre = 0;
+      if (t0 < t1) {
+        SlabTile d = sv.tile[t0];
+        while (true) {
+          pend[pre] = d;
+          slab_entries(sv, d, stages + pre * sb, &full[pre]);
+          ++pre;
+          if (pre == kSlabStages || t0 + pre >= t1) break;
+          d = sv.tile[t0 + pre];
+          if (d.s != pend[0].s) break;
+        }
+      }
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      // the finish kernel may launch once every CTA is past the wait (so its
+      // rows without partials see this step's inputs complete)
+      asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
       int held = -1;  // window in the shared buffer
-      for (int t = t0, i = 0; t < t1; ++t, ++i) {
-        const int st = i % kSlabStages;
-        const SlabTile cur = d;
-        if (t + 1 < t1) d = sv.tile[t + 1];  // prefetch the next descriptor
-        if (i >= kSlabStages) mbar_wait(&empty[st], (i / kSlabStages - 1) & 1);  // stage free
-        const bool change = cur.s != held;
-        if (change && held >= 0)  // drain: the tiles in flight still read the old window
-          for (int q = 1; q < kSlabStages && i - q >= 0; ++q) {
-            const int p = i - q;
-            mbar_wait(&empty[p % kSlabStages], (p / kSlabStages) & 1);
-          }
-        slab_issue(op, sv, cur, win, stages + st * sb, &full[st], change);
-        held = cur.s;
+      for (int q = 0; q < pre; ++q) {
+        slab_commit(op, sv, pend[q], win, &full[q], q == 0);
+        held = pend[0].s;
+      }
+      if (t0 + pre < t1) {
+        SlabTile d = sv.tile[t0 + pre];
+        for (int t = t0 + pre, i = pre; t < t1; ++t, ++i) {
+          const int st = i % kSlabStages;
+          const SlabTile cur = d;
+          if (t + 1 < t1) d = sv.tile[t + 1];  // prefetch the next descriptor
+          if (i >= kSlabStages) mbar_wait(&empty[st], (i / kSlabStages - 1) & 1);  // stage free
+          const bool change = cur.s != held;
+          if (change && held >= 0)  // drain: the tiles in flight still read the old window
+            for (int q = 1; q < kSlabStages && i - q >= 0; ++q) {
+              const int p = i - q;
+              mbar_wait(&empty[p % kSlabStages], (p / kSlabStages) & 1);
+            }
+          slab_entries(sv, cur, stages + st * sb, &full[st]);
+          slab_commit(op, sv, cur, win, &full[st], change);
+          held = cur.s;
+        }
       }
     }
     return;
@@ -369,6 +406,9 @@ inline int SlabView::smem_bytes() const { return win_max * 8 + kSlabStages * sta
 template <class Op>
 __global__ void __launch_bounds__(kBlock) slab_finish_kernel(const Op op, const Op rest, const SlabView sv,
                                                              const SchedView others, int wblocks) {
+  // the next kernel (the next slab kernel, a programmatic dependent launch)
+  // may start prefetching its tiles; it waits for this grid before using y / w
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int ob = others.total_blocks > 0 ? others.total_blocks : 0;
   if (static_cast<int>(blockIdx.x) < ob) {  // first: the rows without partials (they start at once)
     const Gather g[2] = {Gather{op.gather_src(0), nullptr, 0, 0u}, Gather{op.gather_src(1), nullptr, 0, 0u}};
@@ -482,8 +522,19 @@ void assign_slab_ctas(SlabPlan& plan, int grid, cudaStream_t st);
 template <class Op>
 inline int launch_slab_phase(const Op& op, const SlabPhase& ph, cudaStream_t st) {
   const SlabView& sv = ph.plan.view;
-  slab_kernel<Op><<<sv.grid, kSlabThreads, sv.smem_bytes(), st>>>(op, sv);
-  RB_LAUNCH_CHECK();
+  {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(sv.grid));
+    cfg.blockDim = dim3(kSlabThreads);
+    cfg.dynamicSmemBytes = static_cast<std::size_t>(sv.smem_bytes());
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    RB_CUDA(cudaLaunchKernelEx(&cfg, slab_kernel<Op>, op, sv));
+  }
   const SchedView& o = ph.others.view;
   const int wblocks = static_cast<int>(ceil_div(sv.nw, sv.S >= kSlabGroupedS ? 32 : kBlock));
   cudaLaunchConfig_t cfg{};

@@ -524,7 +524,8 @@ void Engine::setup_colblocks() {
 // are on the device so it overlaps the scaling and the power iterations.
 void Engine::plan_slabs_async() {
   const int dev = cfg_.device;
-  plan_future_ = std::async(std::launch::async, [this, dev] {
+  // one host thread (and stream) per op's plan
+  auto task = [this, dev](bool dual) {
     RB_CUDA(cudaSetDevice(dev));
     cudaStream_t s2;
     RB_CUDA(cudaStreamCreate(&s2));
@@ -532,15 +533,19 @@ void Engine::plan_slabs_async() {
       DeviceQP& P = *P_;
       Tracer tr(s2);
       DevBuf<int32_t> len;
-      dual_choice_ = choose_slabs(P.A.rp.get(), P.A.ci.get(), P.A.rows, P.A.nnz, n_, s2);
-      row_lengths(len, P.A.rp.get(), nullptr, m_, s2);
-      build_slab_phase(dual_ph_, dual_choice_, 0, P.A.rp.get(), P.A.ci.get(), nullptr, nullptr, 0, m_, len.get(), s2);
-      tr.mark("  slab plan: dual (async)");
-      primal_choice_ = choose_slabs(P.AT.rp.get(), P.AT.ci.get(), n_, P.AT.nnz, m_, s2);
-      row_lengths(len, P.Q.rp.get(), P.AT.rp.get(), n_, s2);
-      build_slab_phase(primal_ph_, primal_choice_, 1, P.Q.rp.get(), P.Q.ci.get(), P.AT.rp.get(), P.AT.ci.get(), 0,
-                       n_, len.get(), s2);
-      tr.mark("  slab plan: primal (async)");
+      if (dual) {
+        dual_choice_ = choose_slabs(P.A.rp.get(), P.A.ci.get(), P.A.rows, P.A.nnz, n_, s2);
+        row_lengths(len, P.A.rp.get(), nullptr, m_, s2);
+        build_slab_phase(dual_ph_, dual_choice_, 0, P.A.rp.get(), P.A.ci.get(), nullptr, nullptr, 0, m_, len.get(),
+                         s2);
+        tr.mark("  slab plan: dual (async)");
+      } else {
+        primal_choice_ = choose_slabs(P.AT.rp.get(), P.AT.ci.get(), n_, P.AT.nnz, m_, s2);
+        row_lengths(len, P.Q.rp.get(), P.AT.rp.get(), n_, s2);
+        build_slab_phase(primal_ph_, primal_choice_, 1, P.Q.rp.get(), P.Q.ci.get(), P.AT.rp.get(), P.AT.ci.get(), 0,
+                         n_, len.get(), s2);
+        tr.mark("  slab plan: primal (async)");
+      }
       RB_CUDA(cudaStreamSynchronize(s2));
     } catch (...) {
       cudaStreamSynchronize(s2);
@@ -548,12 +553,15 @@ void Engine::plan_slabs_async() {
       throw;
     }
     RB_CUDA(cudaStreamDestroy(s2));
-  });
+  };
+  plan_future_ = std::async(std::launch::async, task, true);
+  plan_future2_ = std::async(std::launch::async, task, false);
 }
 
 void Engine::setup_slabs() {
   Tracer tr(st_);
   plan_future_.get();  // the pattern part (plan_slabs_async)
+  plan_future2_.get();
   tr.mark("  slab plans joined");
   if (dual_ph_.active()) {
     fill_slab_values(dual_ph_.plan, asv_, nullptr, st_);

@@ -185,7 +185,7 @@ class Engine : public LoopBackend {
   // slab-staged gathers (fast mode, slab.cuh): plans + the complement schedules
   void setup_slabs();
   void plan_slabs_async();
-  std::future<void> plan_future_;
+  std::future<void> plan_future_, plan_future2_;
   SlabChoice dual_choice_, primal_choice_;
   SlabPhase dual_ph_, primal_ph_;
   // L2-sized column blocks (colblock.cuh) of the gather-bound ops without a slab plan

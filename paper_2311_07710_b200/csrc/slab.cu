@@ -1,6 +1,7 @@
 // slab.cu — setup of the slab tile plans (see slab.cuh).
 #include <algorithm>
 #include <climits>
+#include <functional>
 #include <cstdio>
 #include <cstdlib>
 #include <numeric>
@@ -372,57 +373,86 @@ void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const in
   bool sorted = false;
   {
     const char* mode = std::getenv("RAPDHG_SLAB_ORDER");
-    sorted = mode && std::string(mode) == "sorted";
-    build(sorted, order, spans, lay);
-    if (!mode) {  // natural unless it pads too much
+    if (mode) {
+      sorted = std::string(mode) == "sorted";
+    } else {
+      // natural unless it pads too much: the padding of natural tiles from the
+      // run lengths alone (each tile's runs sorted, 32-row slices)
       int64_t padded = 0, actual = 0;
-      for (const TileLayout& L : lay) padded += L.n;
       for (int32_t c : hc2) actual += c;
-      if (static_cast<double>(padded) > kSlabNaturalPad * static_cast<double>(std::max<int64_t>(actual, 1))) {
-        sorted = true;
-        build(true, order, spans, lay);
-      }
+      std::vector<int64_t> pad_w(S, 0);
+      parallel_for(S, [&](int64_t si) {
+        const int32_t* len = hc2.data() + si * nw;
+        std::vector<int32_t> buf;
+        int64_t raw = 0, pad = 0;
+        auto flush = [&] {
+          std::sort(buf.begin(), buf.end(), std::greater<int32_t>());
+          for (std::size_t q = 0; q < buf.size(); q += 32) pad += 32 * static_cast<int64_t>(buf[q]);
+          buf.clear();
+          raw = 0;
+        };
+        for (int32_t k = 0; k < nw; ++k) {
+          if (len[k] == 0) continue;
+          if (buf.size() % 32 == 0 && !buf.empty() &&
+              (raw + len[k] > ecap * 7 / 8 || static_cast<int>(buf.size()) + 1 > rcap))
+            flush();
+          buf.push_back(len[k]);
+          raw += len[k];
+        }
+        flush();
+        pad_w[si] = pad;
+      });
+      for (int64_t v : pad_w) padded += v;
+      sorted = static_cast<double>(padded) > kSlabNaturalPad * static_cast<double>(std::max<int64_t>(actual, 1));
     }
+    build(sorted, order, spans, lay);
   }
   const int32_t ntiles = static_cast<int32_t>(spans.size());
   tr.mark("    tiles + layouts");
   // tile arrays: window-major, each tile 32-entry aligned; run (s, k): tile
   // base off[s * nw + k] and jx[s * nw + k] (see fill_kernel)
-  std::vector<int32_t> off(runs, 0), jx(runs, 0), joff;
+  std::vector<int32_t> off(runs, 0), jx(runs, 0);
   std::vector<SlabTile> tiles(ntiles);
   const int64_t row_cost = env_int("RAPDHG_SLAB_ROWCOST", kSlabRowCost);
-  std::vector<uint16_t> meta;
+  std::vector<int64_t> joff_at(ntiles + 1, 0), meta_at(ntiles + 1, 0);
   int64_t cursor = 0;
   int max_tile = 0, max_meta = 0;
-  for (int32_t t = 0; t < ntiles; ++t) {
+  plan.tile_bytes.resize(ntiles);
+  for (int32_t t = 0; t < ntiles; ++t) {  // offsets (sequential prefix)
     const TileSpan& sp = spans[t];
     const TileLayout& L = lay[t];
-    const int32_t n_r = sp.e - sp.b;
     SlabTile& d = tiles[t];
     d.a = static_cast<int32_t>(cursor);
     d.n = L.n;
-    d.meta = static_cast<int32_t>(meta.size());
+    d.meta = static_cast<int32_t>(meta_at[t]);
     d.k0 = 0;
-    d.nr = n_r;
+    d.nr = sp.e - sp.b;
     d.s = sp.s;
     d.m = static_cast<int32_t>(L.meta.size());
     max_tile = std::max(max_tile, d.n);
     max_meta = std::max(max_meta, d.m);
     // cost for balancing the CTAs' contiguous ranges: staged bytes, per-row
     // work (length/perm loads, the partial store), a fixed per-tile cost
-    plan.tile_bytes.push_back(10 * static_cast<int64_t>(d.n) + 2 * static_cast<int64_t>(d.m) +
-                              row_cost * static_cast<int64_t>(n_r) + 16384);
-    const int64_t j0 = static_cast<int64_t>(joff.size());
-    for (int32_t slot = 0; slot < n_r; ++slot) {
-      const int64_t run = static_cast<int64_t>(sp.s) * nw + L.rows[slot];
-      off[run] = static_cast<int32_t>(cursor);
-      jx[run] = static_cast<int32_t>((j0 + L.sj[slot / 32]) * 32 + slot % 32);
-    }
-    joff.insert(joff.end(), L.joff.begin(), L.joff.end());
-    meta.insert(meta.end(), L.meta.begin(), L.meta.end());
-    meta.resize((meta.size() + 7) & ~std::size_t{7}, 0);
+    plan.tile_bytes[t] = 10 * static_cast<int64_t>(d.n) + 2 * static_cast<int64_t>(d.m) +
+                         row_cost * static_cast<int64_t>(d.nr) + 16384;
+    joff_at[t + 1] = joff_at[t] + static_cast<int64_t>(L.joff.size());
+    meta_at[t + 1] = meta_at[t] + ((static_cast<int64_t>(L.meta.size()) + 7) & ~int64_t{7});
     cursor += d.n;
   }
+  std::vector<int32_t> joff(joff_at[ntiles]);
+  std::vector<uint16_t> meta(meta_at[ntiles], 0);
+  parallel_for(ntiles, [&](int64_t t) {  // contents (disjoint per tile)
+    const TileSpan& sp = spans[t];
+    const TileLayout& L = lay[t];
+    const int32_t n_r = sp.e - sp.b;
+    for (int32_t slot = 0; slot < n_r; ++slot) {
+      const int64_t run = static_cast<int64_t>(sp.s) * nw + L.rows[slot];
+      off[run] = tiles[t].a;
+      jx[run] = static_cast<int32_t>((joff_at[t] + L.sj[slot / 32]) * 32 + slot % 32);
+    }
+    std::copy(L.joff.begin(), L.joff.end(), joff.begin() + joff_at[t]);
+    std::copy(L.meta.begin(), L.meta.end(), meta.begin() + meta_at[t]);
+  });
   if (cursor > INT32_MAX || max_tile > ecap || max_meta > kSlabMetaCap ||
       static_cast<int64_t>(joff.size()) * 32 > INT32_MAX) {  // int32 offsets; tiles must fit a stage
     plan = SlabPlan{};

@@ -12,9 +12,14 @@
 #include <vector>
 
 #include "rapdhg_b200.h"
+#include "crng.h"
 
 // rapdhg_last_error() storage lives in capi.cu
 void rb_set_error(const char* msg);
+
+namespace rb {
+bool gen_large_device(double scale, uint64_t seed, bool local, rapdhg_qp_owned* out);  // gen_device.cu
+}
 
 namespace {
 
@@ -363,55 +368,101 @@ void gen_svm(double scale, uint64_t seed, rapdhg_qp_owned* out) {
 }
 
 // ---- C5: large random QP, uniform (U) or 95%-block-local (L) columns --------
+// C5: A m x n with 12 draws per row, Q with 1.5 n mirrored
+// off-diagonal pairs and a dominant diagonal, pattern U (uniform columns) or L
+// (95% of a row's columns in its home block of n / 8). Counter-based
+// (crng.h): every draw is a function of (seed, tag, index), so the device
+// generator (gen_device.cu) produces bit-identical arrays; this host version
+// is its reference. Exact algorithm (both sides):
+//  * A row r: 12 (column, value) draws, sorted by (column, draw), duplicate
+//    columns merged by summing their values in draw order;
+//  * Q: pair p draws (i, j != i, v); triplets (i, j, v), (j, i, v) sorted by
+//    (row, column, triplet index), duplicates summed in that order; Q_ii =
+//    1e-2 + the sum of |v| over row i's triplets in that order;
+//  * x0_i, c_i ~ normal; b_r = (A x0)_r (sequential, unfused) + uniform slack.
 void gen_large(double scale, uint64_t seed, bool local, rapdhg_qp_owned* out) {
-  Rng g(seed);
+  using namespace rb::crng;
   const int32_t n = std::max<int32_t>(16, static_cast<int32_t>(std::lround(1e7 * scale)));
   const int32_t m = std::max<int32_t>(8, n / 2);
   const int32_t blocks = 8;
-  auto col_for = [&](int32_t home_block) -> int32_t {
-    if (local && g.uniform() < 0.95) {
-      const int32_t lo = static_cast<int32_t>(static_cast<int64_t>(n) * home_block / blocks);
-      const int32_t hi = static_cast<int32_t>(static_cast<int64_t>(n) * (home_block + 1) / blocks);
-      return lo + static_cast<int32_t>(g.below(hi - lo));
-    }
-    return static_cast<int32_t>(g.below(n));
-  };
-  // A: 12 per row
-  Triplets a(m, n);
-  a.reserve(static_cast<std::size_t>(m) * 12);
-  std::vector<int32_t> cols;
+  // A
+  std::vector<int32_t> arp(static_cast<std::size_t>(m) + 1, 0), aci;
+  std::vector<double> av;
+  aci.reserve(static_cast<std::size_t>(m) * 12);
+  av.reserve(static_cast<std::size_t>(m) * 12);
   for (int32_t r = 0; r < m; ++r) {
     const int32_t home = static_cast<int32_t>(static_cast<int64_t>(blocks) * r / m);
-    cols.clear();
-    for (int i = 0; i < 12; ++i) cols.push_back(col_for(home));
-    std::sort(cols.begin(), cols.end());
-    cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
-    for (int32_t c : cols) a.add(r, c, g.normal());
+    std::pair<int32_t, int32_t> e[12];
+    for (int k = 0; k < 12; ++k) e[k] = {large_col(seed, kACol, r, k, n, home, blocks, local), k};
+    std::sort(e, e + 12);
+    for (int k = 0; k < 12;) {
+      double v = normal(seed, kAVal, r, e[k].second);
+      int q = k + 1;
+      for (; q < 12 && e[q].first == e[k].first; ++q) v = v + normal(seed, kAVal, r, e[q].second);
+      if (v != 0.0) aci.push_back(e[k].first), av.push_back(v);
+      k = q;
+    }
+    arp[r + 1] = static_cast<int32_t>(aci.size());
   }
-  // Q: 1.5 n off-diagonal pairs, mirrored; diagonal 1e-2 + sum |Q_ij|
+  // Q
   const int64_t pairs = static_cast<int64_t>(1.5 * n);
-  Triplets q(n, n);
-  q.reserve(static_cast<std::size_t>(2 * pairs + n));
-  std::vector<double> diag(n, 1e-2);
+  std::vector<std::pair<uint64_t, int64_t>> trip;  // ((row << 32) | col, triplet index)
+  trip.reserve(static_cast<std::size_t>(2 * pairs));
   for (int64_t p = 0; p < pairs; ++p) {
-    const int32_t i = static_cast<int32_t>(g.below(n));
+    const int32_t i = static_cast<int32_t>(below(uniform(seed, kQPair, p, 0), n));
     const int32_t home = static_cast<int32_t>(static_cast<int64_t>(blocks) * i / n);
-    int32_t j = col_for(home);
+    const int32_t j = large_col(seed, kQPair, p, 1, n, home, blocks, local);
     if (j == i) continue;
-    const double v = g.normal();
-    q.add(i, j, v);
-    q.add(j, i, v);
-    diag[i] += std::fabs(v);
-    diag[j] += std::fabs(v);
+    trip.push_back({(static_cast<uint64_t>(i) << 32) | static_cast<uint32_t>(j), 2 * p});
+    trip.push_back({(static_cast<uint64_t>(j) << 32) | static_cast<uint32_t>(i), 2 * p + 1});
   }
-  for (int32_t i = 0; i < n; ++i) q.add(i, i, diag[i]);
-  std::vector<double> x0(n), c(n);
-  for (auto& v : x0) v = g.normal();
-  for (auto& v : c) v = g.normal();
-  build_csr(q, &out->q);
-  build_csr(a, &out->a_ineq);
-  std::vector<double> b = host_mv(out->a_ineq, x0);
-  for (auto& v : b) v += g.uniform();
+  std::stable_sort(trip.begin(), trip.end(),
+                   [](const std::pair<uint64_t, int64_t>& x, const std::pair<uint64_t, int64_t>& y) {
+                     return x.first < y.first;
+                   });
+  std::vector<int32_t> qrp(static_cast<std::size_t>(n) + 1, 0), qci;
+  std::vector<double> qv;
+  qci.reserve(trip.size() + n);
+  qv.reserve(trip.size() + n);
+  std::size_t t = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    std::size_t te = t;
+    while (te < trip.size() && static_cast<int32_t>(trip[te].first >> 32) == i) ++te;
+    double diag = 1e-2;
+    for (std::size_t q = t; q < te; ++q) diag = diag + std::fabs(normal(seed, kQVal, trip[q].second >> 1, 0));
+    bool placed = false;
+    for (std::size_t q = t; q < te;) {
+      const int32_t col = static_cast<int32_t>(trip[q].first & 0xffffffffu);
+      if (!placed && col > i) qci.push_back(i), qv.push_back(diag), placed = true;
+      double v = normal(seed, kQVal, trip[q].second >> 1, 0);
+      std::size_t r2 = q + 1;
+      for (; r2 < te && trip[r2].first == trip[q].first; ++r2) v = v + normal(seed, kQVal, trip[r2].second >> 1, 0);
+      if (v != 0.0) qci.push_back(col), qv.push_back(v);
+      q = r2;
+    }
+    if (!placed) qci.push_back(i), qv.push_back(diag);
+    qrp[i + 1] = static_cast<int32_t>(qci.size());
+    t = te;
+  }
+  // c, b
+  std::vector<double> c(n), b(m);
+  for (int32_t i = 0; i < n; ++i) c[i] = normal(seed, kC, i, 0);
+  for (int32_t r = 0; r < m; ++r) {
+    double acc = 0.0;
+    for (int32_t k = arp[r]; k < arp[r + 1]; ++k) acc = acc + av[k] * normal(seed, kX0, aci[k], 0);
+    b[r] = acc + uniform(seed, kSlack, r, 0);
+  }
+  auto own = [](int32_t rows, int32_t cols, std::vector<int32_t>& rp, std::vector<int32_t>& ci,
+                std::vector<double>& v, rapdhg_csr_owned* o) {
+    o->n_rows = rows, o->n_cols = cols, o->nnz = static_cast<int64_t>(ci.size());
+    o->row_ptr = xalloc<int32_t>(rp.size());
+    std::memcpy(o->row_ptr, rp.data(), sizeof(int32_t) * rp.size());
+    o->col_idx = xalloc<int32_t>(ci.size());
+    if (!ci.empty()) std::memcpy(o->col_idx, ci.data(), sizeof(int32_t) * ci.size());
+    o->values = vec_copy(v);
+  };
+  own(n, n, qrp, qci, qv, &out->q);
+  own(m, n, arp, aci, av, &out->a_ineq);
   empty_csr(0, n, &out->a_eq);
   out->n = n, out->m_ineq = m, out->m_eq = 0;
   out->c = vec_copy(c);
@@ -470,8 +521,17 @@ int rapdhg_generate(int32_t kind, double scale, uint64_t seed, rapdhg_qp_owned* 
       case RAPDHG_GEN_LASSO: gen_lasso(scale, seed, out); break;
       case RAPDHG_GEN_PORTFOLIO: gen_portfolio(scale, seed, out); break;
       case RAPDHG_GEN_SVM: gen_svm(scale, seed, out); break;
-      case RAPDHG_GEN_LARGE: gen_large(scale, seed, false, out); break;
-      case RAPDHG_GEN_LARGE_LOCAL: gen_large(scale, seed, true, out); break;
+      case RAPDHG_GEN_LARGE:
+      case RAPDHG_GEN_LARGE_LOCAL: {
+        // the device generator (gen_device.cu) makes the same arrays; it is
+        // used for large instances when a device is visible
+        // (RAPDHG_GEN_DEVICE=1 / 0 forces it on / off)
+        const bool local = kind == RAPDHG_GEN_LARGE_LOCAL;
+        const char* e = std::getenv("RAPDHG_GEN_DEVICE");
+        const bool want = e ? e[0] == '1' : scale >= 0.02;
+        if (!(want && rb::gen_large_device(scale, seed, local, out))) gen_large(scale, seed, local, out);
+        break;
+      }
       default: throw HostError(RAPDHG_E_INVALID_ARGUMENT, "unknown generator kind");
     }
   });

@@ -1,0 +1,65 @@
+"""C5 generator (counter-based; csrc/host.cpp gen_large + csrc/gen_device.cu).
+CPU: the host reference yields valid, deterministic instances with a
+symmetric, diagonally dominant Q. GPU: the device generator's arrays are
+bit-identical to the host reference."""
+import numpy as np
+import pytest
+
+import paper_2311_07710_b200 as rb
+
+
+def arrays(p):
+    return [p.q.row_ptr, p.q.col_idx, p.q.values, p.a_ineq.row_ptr, p.a_ineq.col_idx, p.a_ineq.values, p.c,
+            p.b_ineq, p.a_eq.row_ptr]
+
+
+@pytest.mark.parametrize("kind", [rb.Gen.LARGE, rb.Gen.LARGE_LOCAL])
+def test_host_large_valid_and_deterministic(kind, monkeypatch):
+    monkeypatch.setenv("RAPDHG_GEN_DEVICE", "0")
+    p = rb.generate(kind, 0.002, 5)
+    n, m = p.num_vars(), p.num_rows()
+    assert n == 20000 and m == 10000 and p.num_eq() == 0
+    for mat in (p.q, p.a_ineq):
+        rp, ci = mat.row_ptr, mat.col_idx
+        assert rp[0] == 0 and rp[-1] == len(ci) and np.all(np.diff(rp) >= 0)
+        for r in range(0, mat.n_rows, 997):  # strictly increasing columns within rows
+            assert np.all(np.diff(ci[rp[r]:rp[r + 1]]) > 0)
+    rows = np.repeat(np.arange(n), np.diff(p.q.row_ptr))
+    dense_key = rows.astype(np.int64) * n + p.q.col_idx
+    mirror = p.q.col_idx.astype(np.int64) * n + rows
+    order = np.argsort(mirror)
+    assert np.array_equal(np.sort(dense_key), mirror[order])          # pattern symmetric
+    assert np.array_equal(p.q.values[np.argsort(dense_key)], p.q.values[order])  # values symmetric
+    diag = p.q.values[rows == p.q.col_idx]
+    off = np.bincount(rows[rows != p.q.col_idx], weights=np.abs(p.q.values[rows != p.q.col_idx]), minlength=n)
+    assert len(diag) == n and np.all(diag >= off)                     # diagonally dominant
+    q = rb.generate(kind, 0.002, 5)
+    assert all(np.array_equal(a, b) for a, b in zip(arrays(p), arrays(q)))
+    r = rb.generate(kind, 0.002, 6)
+    assert not np.array_equal(p.c, r.c)
+
+
+def test_host_large_local_pattern(monkeypatch):
+    monkeypatch.setenv("RAPDHG_GEN_DEVICE", "0")
+    n = 20000
+    u = rb.generate(rb.Gen.LARGE, 0.002, 5)
+    l = rb.generate(rb.Gen.LARGE_LOCAL, 0.002, 5)
+
+    def home_fraction(p):
+        a = p.a_ineq
+        rows = np.repeat(np.arange(a.n_rows), np.diff(a.row_ptr))
+        return np.mean(8 * rows // a.n_rows == 8 * a.col_idx.astype(np.int64) // n)
+
+    assert home_fraction(l) > 0.9 and home_fraction(u) < 0.2
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", [rb.Gen.LARGE, rb.Gen.LARGE_LOCAL])
+@pytest.mark.parametrize("scale", [0.0005, 0.01])
+def test_device_generator_bit_identical(kind, scale, monkeypatch):
+    monkeypatch.setenv("RAPDHG_GEN_DEVICE", "1")
+    d = rb.generate(kind, scale, 5)
+    monkeypatch.setenv("RAPDHG_GEN_DEVICE", "0")
+    h = rb.generate(kind, scale, 5)
+    for a, b in zip(arrays(d), arrays(h)):
+        assert a.shape == b.shape and np.array_equal(a, b)

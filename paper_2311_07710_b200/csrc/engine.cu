@@ -681,8 +681,11 @@ void Engine::run_chunk(int len) {
     launch_chunk_body(len, cur_, prof);
   }
   cur_ ^= (len & 1);
-  RB_CUDA(cudaStreamSynchronize(st_));
+  bad_fresh_ = false;
+  // no sync: the check's kernels queue behind the chunk (first_bad() or
+  // evaluate() synchronise); sampled chunks read their events now
   if (prof) {
+    RB_CUDA(cudaStreamSynchronize(st_));
     for (int it = 0; it < len; ++it) {
       float a = 0.f, b = 0.f;
       RB_CUDA(cudaEventElapsedTime(&a, events_[2 * it], events_[2 * it + 1]));
@@ -731,7 +734,9 @@ Cand Engine::evaluate() {
                       n_, P.strict, P.red, P.red_out.get() + 16, st_);
   launches_ += 2;
   RB_CUDA(cudaMemcpyAsync(P.red_host.get(), P.red_out.get(), sizeof(double) * 32, cudaMemcpyDeviceToHost, st_));
+  bad_.download(bad_h_.get(), 1, st_);  // the chunk's numerical-error flag, with the same sync
   RB_CUDA(cudaStreamSynchronize(st_));
+  bad_fresh_ = true;
   const double* h = P.red_host.get();
   KktRaw r;
   r.by_i[0] = h[0], r.by_e[0] = h[1], r.by_i[1] = h[2], r.by_e[1] = h[3];
@@ -807,6 +812,10 @@ void Engine::loop_begin() {
 }
 
 long long Engine::first_bad() {
+  if (bad_fresh_) {  // read back with the last evaluate()'s results, after the chunk
+    bad_fresh_ = false;
+    return bad_h_[0];
+  }
   bad_.download(bad_h_.get(), 1, st_);
   RB_CUDA(cudaStreamSynchronize(st_));
   return bad_h_[0];
@@ -950,6 +959,10 @@ void run_loop(LoopBackend& be, const rapdhg_config& cfg, const LoopScalars& sc, 
     }
     const long t_end = check_due ? tt : tt - 1;
     be.run_chunk(len);
+    // a check's evaluation is queued right behind the chunk (one sync for
+    // both); its results are only used once the chunk proved finite
+    Cand next;
+    if (check_due) next = be.evaluate();
     // all_finite after every step (solver.hpp:372-373): first bad iteration
     const long long bad = be.first_bad();
     if (bad <= t_end) {
@@ -961,7 +974,7 @@ void run_loop(LoopBackend& be, const rapdhg_config& cfg, const LoopScalars& sc, 
     const long tc = t_end;
     const double cur_eta = theoretical ? sp.eta : eta;
 
-    cand = be.evaluate();
+    cand = next;
     const Kkt cres = cand.res();
     if (cres.relkkt() < best.relkkt()) {
       best = cres;

@@ -111,6 +111,7 @@ class LoopBackend {
   virtual IterParams* host_params() = 0;  // kMaxChunk pinned entries
   virtual void run_chunk(int len) = 0;    // len inner steps with host_params()[0..len)
   virtual long long first_bad() = 0;      // first non-finite iteration (sticky), syncs
+                                          // (after evaluate(): may reuse its read-back)
   virtual Cand evaluate() = 0;            // unscale + relKKT of current and average
   virtual void keep_best(bool avg) = 0;   // best <- that candidate's unscaled point
   virtual void restart(bool from_avg, double* dx, double* dy) = 0;  // + dist2 for omega
@@ -182,6 +183,7 @@ class Engine : public LoopBackend {
   PinnedBuf<IterParams> params_h_;
   DevBuf<long long> bad_;
   PinnedBuf<long long> bad_h_;
+  bool bad_fresh_ = false;  // bad_h_ was read back by the last evaluate()
   // slab-staged gathers (fast mode, slab.cuh): plans + the complement schedules
   void setup_slabs();
   void plan_slabs_async();

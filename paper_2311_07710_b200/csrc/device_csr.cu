@@ -1,7 +1,11 @@
 // device_csr.cu — structural CSR setup on the device (see device_csr.cuh).
 #include <cub/device/device_radix_sort.cuh>
 
+#include <atomic>
+#include <cstdlib>
 #include <cstring>
+#include <thread>
+#include <vector>
 
 #include "device_csr.cuh"
 
@@ -100,16 +104,81 @@ inline unsigned grid_for(int64_t n, int b = 256) { return static_cast<unsigned>(
 
 }  // namespace
 
-void upload_csr(DevCsr& d, const rapdhg_csr& h, cudaStream_t st) {
+HostStager::HostStager() {
+  const char* e = std::getenv("RAPDHG_STAGE");
+  on_ = !(e && e[0] == '0');
+}
+
+HostStager::~HostStager() {
+  if (last_) cudaStreamSynchronize(last_);  // the DMAs out of the buffers are done
+  for (int s = 0; s < 2 * kMaxThreads; ++s) {
+    if (ev_[s]) cudaEventDestroy(ev_[s]);
+    pinned_release(buf_[s], kChunk);
+  }
+}
+
+void HostStager::upload(void* dst, const void* src, std::size_t bytes, cudaStream_t st) {
+  if (!on_ || bytes < 2 * kChunk) {
+    if (bytes) RB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+    return;
+  }
+  last_ = st;
+  const std::size_t nch = (bytes + kChunk - 1) / kChunk;
+  const int T = static_cast<int>(std::min<std::size_t>(
+      nch, std::min<unsigned>(kMaxThreads, std::max(1u, std::thread::hardware_concurrency() / 2))));
+  for (int s = 0; s < 2 * T; ++s)
+    if (!buf_[s]) {
+      buf_[s] = pinned_acquire(kChunk);
+      RB_CUDA(cudaEventCreateWithFlags(&ev_[s], cudaEventDisableTiming));
+    }
+  int dev = 0;
+  RB_CUDA(cudaGetDevice(&dev));
+  std::atomic<int> failed{0};
+  // thread t takes chunks t, t + T, ... alternating its two buffers; a buffer
+  // is refilled once the event recorded after its previous DMA has passed
+  auto work = [&](int t) {
+    if (cudaSetDevice(dev) != cudaSuccess) {
+      failed = 1;
+      return;
+    }
+    int use = 0;
+    for (std::size_t c = t; c < nch && !failed; c += T, ++use) {
+      const int s = 2 * t + (use & 1);
+      if (used_[s] && cudaEventSynchronize(ev_[s]) != cudaSuccess) failed = 1;  // its last DMA (any call)
+      used_[s] = true;
+      const std::size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
+      std::memcpy(buf_[s], static_cast<const char*>(src) + off, len);
+      if (cudaMemcpyAsync(static_cast<char*>(dst) + off, buf_[s], len, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+          cudaEventRecord(ev_[s], st) != cudaSuccess)
+        failed = 1;
+    }
+  };
+  std::vector<std::thread> th;
+  for (int t = 1; t < T; ++t) th.emplace_back(work, t);
+  work(0);
+  for (auto& x : th) x.join();
+  if (failed) {
+    const cudaError_t e = cudaGetLastError();
+    RB_CUDA(e != cudaSuccess ? e : cudaErrorUnknown);
+  }
+}
+
+void upload_csr(DevCsr& d, const rapdhg_csr& h, cudaStream_t st, HostStager* sg) {
   d.rows = h.n_rows;
   d.cols = h.n_cols;
   d.nnz = h.nnz;
   d.rp.alloc(static_cast<std::size_t>(h.n_rows) + 1);
   d.ci.alloc(static_cast<std::size_t>(h.nnz));
   d.v.alloc(static_cast<std::size_t>(h.nnz));
-  d.rp.upload(h.row_ptr, static_cast<std::size_t>(h.n_rows) + 1, st);
-  d.ci.upload(h.col_idx, static_cast<std::size_t>(h.nnz), st);
-  d.v.upload(h.values, static_cast<std::size_t>(h.nnz), st);
+  if (!sg) {
+    d.rp.upload(h.row_ptr, static_cast<std::size_t>(h.n_rows) + 1, st);
+    d.ci.upload(h.col_idx, static_cast<std::size_t>(h.nnz), st);
+    d.v.upload(h.values, static_cast<std::size_t>(h.nnz), st);
+    return;
+  }
+  sg->upload(d.rp.get(), h.row_ptr, sizeof(int32_t) * (static_cast<std::size_t>(h.n_rows) + 1), st);
+  sg->upload(d.ci.get(), h.col_idx, sizeof(int32_t) * static_cast<std::size_t>(h.nnz), st);
+  sg->upload(d.v.get(), h.values, sizeof(double) * static_cast<std::size_t>(h.nnz), st);
 }
 
 void stack_csr(DevCsr& out, const DevCsr& top, const DevCsr& bot, cudaStream_t st) {

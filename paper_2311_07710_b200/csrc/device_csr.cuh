@@ -20,8 +20,33 @@ struct DevCsr {
   CsrView view(const double* vals) const { return CsrView{rp.get(), ci.get(), vals}; }
 };
 
+// Host -> device copies of large pageable arrays through pinned staging: up
+// to 8 host threads copy 8 MB chunks into per-thread double buffers (pinned,
+// cached across solves, 128 MB at most) and enqueue each chunk's DMA as soon
+// as it is copied, so the memcpys run in parallel and overlap the transfers
+// (the driver's own pageable path is one serial bounce buffer, ~11 GB/s).
+// Copies are complete when the stream is; the destructor waits for them
+// before the buffers go back to the cache. RAPDHG_STAGE=0: plain copies.
+class HostStager {
+ public:
+  HostStager();
+  ~HostStager();
+  HostStager(const HostStager&) = delete;
+  HostStager& operator=(const HostStager&) = delete;
+  void upload(void* dst, const void* src, std::size_t bytes, cudaStream_t st);
+
+ private:
+  static constexpr int kMaxThreads = 8;
+  static constexpr std::size_t kChunk = std::size_t{8} << 20;
+  bool on_ = true;
+  cudaStream_t last_ = nullptr;
+  void* buf_[2 * kMaxThreads] = {};
+  cudaEvent_t ev_[2 * kMaxThreads] = {};
+  bool used_[2 * kMaxThreads] = {};  // a DMA out of the buffer was enqueued (ev_ recorded after it)
+};
+
 // Host CSR (validated for shape/index ranges by the caller) -> device.
-void upload_csr(DevCsr& d, const rapdhg_csr& h, cudaStream_t st);
+void upload_csr(DevCsr& d, const rapdhg_csr& h, cudaStream_t st, HostStager* sg = nullptr);
 
 // [top; bottom] row stacking of two CSRs with equal column counts.
 void stack_csr(DevCsr& out, const DevCsr& top, const DevCsr& bottom, cudaStream_t st);

@@ -149,12 +149,15 @@ void DeviceQP::validate_dims(const rapdhg_qp& p) {
 DeviceQP::DeviceQP(const rapdhg_qp& p, bool strict_, cudaStream_t st_)
     : st(st_), strict(strict_), n(p.n), mi(p.m_ineq), me(p.m_eq), m(p.m_ineq + p.m_eq) {
   Tracer tr(st);
-  upload_csr(Q, p.q, st);
-  DevCsr ai, ae;
-  upload_csr(ai, p.a_ineq, st);
-  upload_csr(ae, p.a_eq, st);
-  stack_csr(A, ai, ae, st);  // WorkingProblem::from (solver.hpp:106-108)
-  RB_CUDA(cudaStreamSynchronize(st));
+  {
+    HostStager sg;
+    upload_csr(Q, p.q, st, &sg);
+    DevCsr ai, ae;
+    upload_csr(ai, p.a_ineq, st, &sg);
+    upload_csr(ae, p.a_eq, st, &sg);
+    stack_csr(A, ai, ae, st);  // WorkingProblem::from (solver.hpp:106-108)
+    RB_CUDA(cudaStreamSynchronize(st));
+  }
   tr.mark("  upload + stack");
   transpose_csr(AT, A, &at_perm, st);
   tr.mark("  transpose");

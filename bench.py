@@ -105,6 +105,23 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(sm)}
 
 
+def ncu_traffic(dom):
+    """DRAM bytes (read + write) per launch of the dominant step's kernels (its
+    slab kernel + finish kernel) from the committed `ncu --set full` capture of
+    this code (profiles/r01_slab_ncu_full.json, values in MB), or None."""
+    path = os.path.join(ROOT, "profiles", "r01_slab_ncu_full.json")
+    try:
+        with open(path) as f:
+            rows = json.load(f)
+    except (OSError, ValueError):
+        return None
+    op = ["DualStepOp", "PrimalStepOp"][dom]
+    hit = [r for r in rows if op in r.get("Kernel Name", "")]
+    if not hit:
+        return None
+    return 1e6 * sum(float(r["dram__bytes_read.sum"]) + float(r["dram__bytes_write.sum"]) for r in hit)
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -340,7 +357,9 @@ def main():
     it_rate_dev = its / loop_s
     roof = {"bound": "hbm", "kernel": ["dual_step(A*w+projection)", "primal_step([Q|A']*[x_md;y]+update)"][dom],
             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)", "traffic": None,
+            "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)", "traffic": ncu_traffic(dom),
+            "traffic_source": "profiles/r01_slab_ncu_full.json (slab + finish kernel of the step, one ncu --set full "
+                              "capture; tiles carry 16-bit window offsets, so DRAM bytes < algorithmic bytes)",
             "bytes_per_launch": k_bytes, "avg_launch_ms": k_avg[dom],
             "share_of_loop": k_avg[dom] * 1e-3 * its / loop_s,  # sampled launches x all iterations
             "iteration": {"B_iter": b_iter, "achieved_GBs": b_iter * it_rate_dev / 1e9,

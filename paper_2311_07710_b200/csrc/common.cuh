@@ -73,11 +73,27 @@ inline void pool_prepare() {
   }
   done.fetch_or(bit);
 }
+// The stream pool allocations and frees of this host thread are ordered on:
+// the legacy stream by default; a host thread that works on its own
+// non-blocking stream (the slab planners) orders them on that stream instead,
+// so its allocations do not wait behind the solver stream's queued kernels
+// (legacy-stream operations synchronise with every blocking stream).
+inline cudaStream_t& alloc_stream() {
+  thread_local cudaStream_t s = cudaStreamLegacy;
+  return s;
+}
+struct AllocStreamScope {
+  cudaStream_t prev;
+  explicit AllocStreamScope(cudaStream_t s) : prev(alloc_stream()) { alloc_stream() = s; }
+  ~AllocStreamScope() { alloc_stream() = prev; }
+  AllocStreamScope(const AllocStreamScope&) = delete;
+  AllocStreamScope& operator=(const AllocStreamScope&) = delete;
+};
 inline void* dev_alloc(std::size_t bytes) {
   void* p = nullptr;
   if (pool_enabled()) {
     pool_prepare();
-    RB_CUDA(cudaMallocAsync(&p, bytes, cudaStreamLegacy));
+    RB_CUDA(cudaMallocAsync(&p, bytes, alloc_stream()));
   } else {
     RB_CUDA(cudaMalloc(&p, bytes));
   }
@@ -85,7 +101,7 @@ inline void* dev_alloc(std::size_t bytes) {
 }
 inline void dev_free(void* p) {
   if (!p) return;
-  if (pool_enabled()) cudaFreeAsync(p, cudaStreamLegacy);
+  if (pool_enabled()) cudaFreeAsync(p, alloc_stream());
   else cudaFree(p);
 }
 

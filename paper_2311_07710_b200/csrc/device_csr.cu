@@ -107,6 +107,7 @@ inline unsigned grid_for(int64_t n, int b = 256) { return static_cast<unsigned>(
 HostStager::HostStager() {
   const char* e = std::getenv("RAPDHG_STAGE");
   on_ = !(e && e[0] == '0');
+  if (const char* t = std::getenv("RAPDHG_STAGE_THREADS")) threads_ = std::min(kMaxThreads, std::max(1, std::atoi(t)));
 }
 
 HostStager::~HostStager() {
@@ -125,7 +126,7 @@ void HostStager::upload(void* dst, const void* src, std::size_t bytes, cudaStrea
   last_ = st;
   const std::size_t nch = (bytes + kChunk - 1) / kChunk;
   const int T = static_cast<int>(std::min<std::size_t>(
-      nch, std::min<unsigned>(kMaxThreads, std::max(1u, std::thread::hardware_concurrency() / 2))));
+      nch, std::min<unsigned>(threads_, std::max(1u, std::thread::hardware_concurrency() / 2))));
   for (int s = 0; s < 2 * T; ++s)
     if (!buf_[s]) {
       buf_[s] = pinned_acquire(kChunk);

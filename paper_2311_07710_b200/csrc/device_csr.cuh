@@ -21,7 +21,7 @@ struct DevCsr {
 };
 
 // Host -> device copies of large pageable arrays through pinned staging: up
-// to 8 host threads copy 8 MB chunks into per-thread double buffers (pinned,
+// to 8 host threads (RAPDHG_STAGE_THREADS) copy 8 MB chunks into per-thread double buffers (pinned,
 // cached across solves, 128 MB at most) and enqueue each chunk's DMA as soon
 // as it is copied, so the memcpys run in parallel and overlap the transfers
 // (the driver's own pageable path is one serial bounce buffer, ~11 GB/s).
@@ -36,9 +36,10 @@ class HostStager {
   void upload(void* dst, const void* src, std::size_t bytes, cudaStream_t st);
 
  private:
-  static constexpr int kMaxThreads = 8;
+  static constexpr int kMaxThreads = 16;
   static constexpr std::size_t kChunk = std::size_t{8} << 20;
   bool on_ = true;
+  int threads_ = 8;  // RAPDHG_STAGE_THREADS
   cudaStream_t last_ = nullptr;
   void* buf_[2 * kMaxThreads] = {};
   cudaEvent_t ev_[2 * kMaxThreads] = {};

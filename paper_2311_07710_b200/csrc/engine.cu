@@ -530,9 +530,17 @@ void Engine::plan_slabs_async() {
   // one host thread (and stream) per op's plan
   auto task = [this, dev](bool dual) {
     RB_CUDA(cudaSetDevice(dev));
+    // high priority: the plans' few short kernels (counts, fills) are
+    // scheduled ahead of the scaling / power-iteration blocks they overlap,
+    // instead of queueing behind them
+    int lo = 0, hi = 0;
+    RB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     cudaStream_t s2;
-    RB_CUDA(cudaStreamCreate(&s2));
+    RB_CUDA(cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, hi));
     try {
+      // this thread's allocations and frees are ordered on s2 (its buffers
+      // that outlive it are used after the join, which follows s2's sync)
+      AllocStreamScope scope(s2);
       DeviceQP& P = *P_;
       Tracer tr(s2);
       DevBuf<int32_t> len;

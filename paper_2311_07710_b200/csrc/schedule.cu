@@ -182,9 +182,9 @@ void build_schedule(Schedule& sch, const int32_t* d_len, int64_t rows, bool stri
     RB_CUDA(cudaMemcpyAsync(rows_h.data(), sch.perm.get() + v.bins[kBinSplit].row_begin,
                             sizeof(int32_t) * nsplit, cudaMemcpyDeviceToHost, st));
     RB_CUDA(cudaStreamSynchronize(st));
-    for (int32_t i = 0; i < nsplit; ++i) {
-      RB_CUDA(cudaMemcpy(&len_h[i], d_len + rows_h[i], sizeof(int32_t), cudaMemcpyDeviceToHost));
-    }
+    for (int32_t i = 0; i < nsplit; ++i)
+      RB_CUDA(cudaMemcpyAsync(&len_h[i], d_len + rows_h[i], sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    RB_CUDA(cudaStreamSynchronize(st));
     std::vector<int32_t> srow, slo, shi, sfirst, scount;
     for (int32_t i = 0; i < nsplit; ++i) {
       const int32_t L = len_h[i];

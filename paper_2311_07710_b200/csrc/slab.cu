@@ -198,10 +198,19 @@ TileLayout layout_tile(const int32_t* rows, const int32_t* len, int32_t nr) {
   return L;
 }
 
-// f(0 .. n-1) on up to 16 host threads
+// f(0 .. n-1) on host threads: half the cores by default, as the two ops'
+// plans are built concurrently (RAPDHG_PLAN_THREADS overrides)
+int plan_threads() {
+  static const int t = [] {
+    const char* e = std::getenv("RAPDHG_PLAN_THREADS");
+    const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+    return std::max(1, std::min(32, e ? std::atoi(e) : std::max(1, hw / 2)));
+  }();
+  return t;
+}
 template <class F>
 void parallel_for(int64_t n, const F& f) {
-  const int T = static_cast<int>(std::min<int64_t>(n, std::max(1u, std::min(16u, std::thread::hardware_concurrency()))));
+  const int T = static_cast<int>(std::min<int64_t>(n, plan_threads()));
   if (T <= 1) {
     for (int64_t i = 0; i < n; ++i) f(i);
     return;
@@ -332,6 +341,7 @@ void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const in
       }
       order[s] = std::move(o);
     });
+    tr.mark("    row orders");
     spans.clear();
     for (int s = 0; s < S; ++s) {
       const std::vector<int32_t>& o = order[s];
@@ -355,6 +365,7 @@ void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const in
       }
       if (b < no) spans.push_back({s, b, no});
     }
+    tr.mark("    spans");
     for (;;) {  // lay out (rows of a tile sorted by run); split tiles that overflow
       lay.assign(spans.size(), TileLayout{});
       parallel_for(static_cast<int64_t>(spans.size()), [&](int64_t t) {
@@ -422,6 +433,7 @@ void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const in
       for (int64_t v : pad_w) padded += v;
       sorted = static_cast<double>(padded) > kSlabNaturalPad * static_cast<double>(std::max<int64_t>(actual, 1));
     }
+    tr.mark("    padding estimate");
     build(sorted, order, spans, lay);
   }
   const int32_t ntiles = static_cast<int32_t>(spans.size());

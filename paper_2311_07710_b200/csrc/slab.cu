@@ -37,34 +37,39 @@ __global__ void hist_kernel(const int32_t* ci, int64_t nnz, int width, int nb, i
     if (sh[b]) atomicAdd(&hist[b], sh[b]);
 }
 
-__device__ __forceinline__ int lower_pos(const int32_t* ci, int b, int e, int32_t key) {
-  while (b < e) {  // first position in [b, e) with ci >= key (rows are column-sorted)
-    const int mid = (b + e) >> 1;
-    if (ci[mid] < key) b = mid + 1;
-    else e = mid;
-  }
-  return b;
-}
-
+// The plan's windows on the device. Windows start at multiples of `width`, so
+// a column's window is one table lookup (lut: window of each aligned block of
+// columns, or -1).
 struct Wins {
-  Window w[kMaxSlabs];
-  int S;
+  const Window* w;
+  const int32_t* lut;
+  int width, nlut, S;
+  __device__ __forceinline__ int of(int32_t c) const {
+    const int b = c / width;
+    if (b >= nlut) return -1;
+    const int s = lut[b];
+    return (s >= 0 && c - w[s].lo < w[s].len) ? s : -1;
+  }
 };
 
-// in-window entries of row r, per window (per may be null, stride apart) and
-// in total; *maxrun = the longest per-window run
+// in-window entries of row r, per window (per: zeroed, stride apart; may be
+// null) and in total; *maxrun = the longest per-window run. Columns are
+// sorted, so a window's entries are one contiguous run.
 __device__ __forceinline__ int in_window_count(const int32_t* rp, const int32_t* ci, int r, const Wins& wins,
                                                int* per, int64_t stride, int* maxrun = nullptr) {
   const int b = rp[r], e = rp[r + 1];
-  int tot = 0, lo = b, mx = 0;
-  for (int s = 0; s < wins.S; ++s) {
-    lo = lower_pos(ci, lo, e, wins.w[s].lo);
-    const int hi = lower_pos(ci, lo, e, wins.w[s].lo + wins.w[s].len);
-    if (per) per[s * stride] = hi - lo;
-    tot += hi - lo;
-    mx = max(mx, hi - lo);
-    lo = hi;
+  int tot = 0, mx = 0, cur = -1, run = 0;
+  for (int p = b; p < e; ++p) {
+    const int s = wins.of(ci[p]);
+    if (s < 0) continue;
+    if (s != cur) {
+      if (cur >= 0 && per) per[cur * stride] = run;
+      cur = s, run = 0;
+    }
+    ++run, ++tot;
+    mx = max(mx, run);
   }
+  if (cur >= 0 && per) per[cur * stride] = run;
   if (maxrun) *maxrun = mx;
   return tot;
 }
@@ -105,12 +110,13 @@ __global__ void fill_kernel(const int32_t* rows, int32_t nw, const int32_t* rp_w
   const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (k >= nw) return;
   const int r = rows[k];
-  int s = 0, e = 0;
+  int cur = -1, e = 0;
   int rw = rrp_w[k];
   for (int p = rp_w[r]; p < rp_w[r + 1]; ++p) {
     const int32_t c = ci_w[p];
-    while (s < wins.S && c >= wins.w[s].lo + wins.w[s].len) ++s, e = 0;
-    if (s < wins.S && c >= wins.w[s].lo) {
+    const int s = wins.of(c);
+    if (s >= 0) {
+      if (s != cur) cur = s, e = 0;
       const int64_t run = static_cast<int64_t>(s) * nw + k;
       const int64_t wp = off[run] + joff[(jx[run] >> 5) + e] + (jx[run] & 31);
       col[wp] = static_cast<uint16_t>(c - wins.w[s].lo);
@@ -260,9 +266,12 @@ SlabChoice choose_slabs(const int32_t* rp, const int32_t* ci, int32_t rows, int6
     if (h[b] < min_density * len) break;
     ch.windows.push_back(Window{lo, len});
   }
+  ch.width = width;
   std::sort(ch.windows.begin(), ch.windows.end(), [](const Window& a, const Window& b) { return a.lo < b.lo; });
   const int min_windows = mode == "force" ? 1 : env_int("RAPDHG_SLAB_MIN_WINDOWS", kSlabMinWindows);
   if (static_cast<int>(ch.windows.size()) < min_windows) ch.windows.clear();
+  if (std::getenv("RAPDHG_TRACE"))
+    std::fprintf(stderr, "[slab] %d columns: %zu windows of %d\n", ncols, ch.windows.size(), width);
   return ch;
 }
 
@@ -272,9 +281,16 @@ void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const in
   const int S = static_cast<int>(choice.windows.size());
   if (S == 0 || r1 <= r0) return;
   Tracer tr(st);
-  Wins wins{};
-  wins.S = S;
-  for (int s = 0; s < S; ++s) wins.w[s] = choice.windows[s];
+  {
+    const int nlut = choice.windows.back().lo / choice.width + 1;
+    std::vector<int32_t> lut(nlut, -1);
+    for (int s = 0; s < S; ++s) lut[choice.windows[s].lo / choice.width] = s;
+    plan.win.alloc(S);
+    plan.win.upload(choice.windows.data(), S, st);
+    plan.lut.alloc(nlut);
+    plan.lut.upload(lut.data(), nlut, st);
+  }
+  const Wins wins{plan.win.get(), plan.lut.get(), choice.width, choice.windows.back().lo / choice.width + 1, S};
   const int32_t* rp_w = seg == 0 ? rp1 : rp2;  // windowed segment
   const int32_t* ci_w = seg == 0 ? ci1 : ci2;
   const int32_t* rp_o = seg == 0 ? rp2 : rp1;  // the other segment (rest only)
@@ -292,12 +308,23 @@ void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const in
   for (int32_t i = 0; i < nr; ++i)
     if (hc[i] >= min_row) rows.push_back(r0 + i);
   const int32_t nw = static_cast<int32_t>(rows.size());
-  if (nw == 0) return;
+  if (nw == 0) {
+    if (std::getenv("RAPDHG_TRACE"))
+      std::fprintf(stderr, "[slab] seg %d rows [%d,%d): %d windows, no W rows\n", seg, r0, r1, S);
+    return;
+  }
   plan.rows.alloc(nw);
   plan.rows.upload(rows.data(), nw, st);
   // per-(window, row) run lengths and rest counts
   const int64_t runs = static_cast<int64_t>(nw) * S;
+  if (runs > kSlabMaxRuns) {  // ~20 B of plan state per (window, W row) pair
+    if (std::getenv("RAPDHG_TRACE"))
+      std::fprintf(stderr, "[slab] seg %d: %d W rows x %d windows exceeds the plan budget\n", seg, nw, S);
+    plan = SlabPlan{};
+    return;
+  }
   DevBuf<int32_t> c2(runs), rw(nw), ro(nw);
+  c2.zero(st);
   seg_counts_kernel<<<g1(nw), 256, 0, st>>>(plan.rows.get(), nw, rp_w, ci_w, rp_o, wins, c2.get(), rw.get(), ro.get());
   RB_LAUNCH_CHECK();
   const std::vector<int32_t> hc2 = download(c2, runs, st), hrw = download(rw, nw, st), hro = download(ro, nw, st);
@@ -538,10 +565,8 @@ void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const in
   v.ecap = ecap;
   v.mcap = kSlabMetaCap;
   v.win_max = 0;
-  for (int s = 0; s < S; ++s) {
-    v.win[s] = choice.windows[s];
-    v.win_max = std::max(v.win_max, choice.windows[s].len);
-  }
+  for (int s = 0; s < S; ++s) v.win_max = std::max(v.win_max, choice.windows[s].len);
+  v.win = plan.win.get();
   v.win_max = (v.win_max + 1) & ~1;  // keeps the value stage 16 B-aligned
   v.tile = plan.tile.get();
   v.meta = plan.meta.get();

@@ -41,7 +41,8 @@
 
 namespace rb {
 
-constexpr int kMaxSlabs = 64;
+constexpr int kMaxSlabs = 1024;     // windows per op (in device memory)
+constexpr int64_t kSlabMaxRuns = int64_t{16} << 20;  // (window, W row) pairs per plan
 constexpr int kSlabWidth = 2048;        // columns per window (16 KB of fp64)
 constexpr int kSlabMinRow = 16;         // in-window entries that make a W row
 constexpr double kSlabMinDensity = 16;  // gathers per column that keep a window
@@ -87,7 +88,7 @@ struct SlabView {
   int32_t ecap = 0;                // tile entry capacity (multiple of 8)
   int32_t mcap = 0;                // tile metadata capacity (multiple of 8)
   int32_t grid = 0;                // persistent CTAs
-  Window win[kMaxSlabs];
+  const Window* win = nullptr;     // [S] (device)
   const SlabTile* tile = nullptr;   // [J]
   const int32_t* cta = nullptr;     // [grid + 1] tile ranges per CTA (balanced by bytes)
   const uint16_t* meta = nullptr;   // per-tile metadata
@@ -110,7 +111,8 @@ struct SlabView {
 // Device arrays behind a SlabView (built by build_slab_plan).
 struct SlabPlan {
   SlabView view;
-  DevBuf<int32_t> rows, pos, wrow, widx;
+  DevBuf<int32_t> rows, pos, wrow, widx, lut;
+  DevBuf<Window> win;
   DevBuf<SlabTile> tile;
   DevBuf<int32_t> cta;
   std::vector<int64_t> tile_bytes;  // host: bytes each tile stages
@@ -124,7 +126,8 @@ struct SlabPlan {
 // Which windows a matrix segment gets: chosen once on the whole matrix, reused
 // unchanged for every shard so per-row arithmetic agrees.
 struct SlabChoice {
-  std::vector<Window> windows;
+  std::vector<Window> windows;  // each starts at a multiple of width
+  int width = kSlabWidth;
   bool empty() const { return windows.empty(); }
 };
 
@@ -223,8 +226,8 @@ __device__ __forceinline__ void slab_entries(const SlabView& sv, const SlabTile&
 template <class Op>
 __device__ __forceinline__ void slab_commit(const Op& op, const SlabView& sv, const SlabTile& d, double* win,
                                             uint64_t* bar, bool copy_window) {
-  const Window w = sv.win[d.s];
-  const uint32_t wbytes = copy_window ? static_cast<uint32_t>(w.len) * 8u : 0u;
+  const Window w = copy_window ? sv.win[d.s] : Window{};
+  const uint32_t wbytes = static_cast<uint32_t>(w.len) * 8u;
   mbar_expect_tx(bar, wbytes);  // arrive (+ the window's bytes)
   if (wbytes) bulk_g2s(win, op.gather_src(sv.seg) + w.lo, wbytes, bar);
 }
@@ -452,16 +455,17 @@ __global__ void __launch_bounds__(kBlock) slab_finish_kernel(const Op op, const 
     __shared__ double grp[kBlock / 32][32];
     constexpr int G = kBlock / 32;
     double t = 0.0;
-    if (valid) {
-      double v[8];
+    if (valid)
+      for (int s0 = g; s0 < sv.S; s0 += 8 * G) {  // windows g, g + G, ... in order, 8 loads in flight
+        double v[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {  // S <= kMaxSlabs = 8 G
-        const int s = g + u * G;
-        v[u] = s < sv.S ? __ldcg(sv.partial + static_cast<int64_t>(s) * sv.nw + k) : 0.0;
+        for (int u = 0; u < 8; ++u) {
+          const int s = s0 + u * G;
+          v[u] = s < sv.S ? __ldcg(sv.partial + static_cast<int64_t>(s) * sv.nw + k) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) t += v[u];
       }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) t += v[u];
-    }
     grp[g][lane] = t;
     __syncthreads();
     if (!owner) return;

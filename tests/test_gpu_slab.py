@@ -100,3 +100,20 @@ def test_forced_slab_numerical_error(O, monkeypatch):
     a, b = rb.solve(p, cfg), O.solve(p, cfg)
     assert a.status == b.status == rb.SolveStatus.kNumericalError
     assert a.iterations == b.iterations
+
+
+def test_slab_many_windows(monkeypatch):
+    """More than 64 windows per op (the window table lives in device memory;
+    the finish pass sums the partials of 8 windows per warp per round)."""
+    monkeypatch.setenv("RAPDHG_SLAB", "force")
+    monkeypatch.setenv("RAPDHG_SLAB_WIDTH", "128")
+    p = rb.generate(rb.Gen.LASSO, 0.05, 2)
+    assert p.num_vars() // 128 > 64
+    cfg = rb.SolverConfig(tol=1e-12, max_iters=400, snapshot_interval=40)
+    a = rb.solve(p, cfg)
+    assert_results_identical(a, rb.solve(p, cfg))  # deterministic
+    assert_results_identical(rb.solve_sharded(p, cfg, 2), a)  # shard-invariant
+    monkeypatch.setenv("RAPDHG_SLAB", "off")
+    b = rb.solve(p, cfg)
+    for (ta, za), (tb, zb) in zip(a.snapshots, b.snapshots):
+        assert ta == tb and rel_err(za.x, zb.x) < 1e-10 and rel_err(za.y_eq, zb.y_eq) < 1e-10

@@ -606,6 +606,9 @@ Engine::~Engine() {
   for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
   for (auto& e : events_) cudaEventDestroy(e);
   P_.reset();
+  if (evf_) cudaEventDestroy(evf_);
+  if (evj_) cudaEventDestroy(evj_);
+  if (st2_) cudaStreamDestroy(st2_);
   if (st_) cudaStreamDestroy(st_);
 }
 
@@ -729,20 +732,37 @@ Cand Engine::evaluate() {
     KktQAtyOp<true> qa{P.Q.view(), P.AT.view(), mi_, xi_.get(), yi_.get(),
                        qx_[0].get(), qx_[1].get(), aty_[0].get(), aty_[1].get()};
     rowwise(qa, P.sch_primal, st_, &launches_);
+    launch_reduce<4, 5>(KktDualTerms{ax_[0].get(), ax_[1].get(), P.b.get(), yu_[0].get(), yu_[1].get(), mi_},
+                        m_, true, P.red, P.red_out.get(), st_);
+    launch_reduce<4, 7>(KktPrimalTerms{qx_[0].get(), qx_[1].get(), aty_[0].get(), aty_[1].get(), xu_[0].get(),
+                                       xu_[1].get(), P.c.get()},
+                        n_, true, P.red, P.red_out.get() + 16, st_);
   } else {
-    KktAxOp<false> ax{P.A.view(), xi_.get(), ax_[0].get(), ax_[1].get()};
-    rowwise(ax, P.sch_dual, st_, &launches_);
+    // primal side on st2_ (own reduction scratch), dual side on st_, joined
+    // before the read-back; the results do not depend on the overlap
+    if (!st2_) {
+      RB_CUDA(cudaStreamCreateWithFlags(&st2_, cudaStreamNonBlocking));
+      RB_CUDA(cudaEventCreateWithFlags(&evf_, cudaEventDisableTiming));
+      RB_CUDA(cudaEventCreateWithFlags(&evj_, cudaEventDisableTiming));
+      red2_.init(std::max(n_, m_), st_);
+    }
+    RB_CUDA(cudaEventRecord(evf_, st_));
+    RB_CUDA(cudaStreamWaitEvent(st2_, evf_, 0));
     KktQAtyOp<false> qa{P.Q.view(), P.AT.view(), mi_, xi_.get(), yi_.get(),
                         qx_[0].get(), qx_[1].get(), aty_[0].get(), aty_[1].get()};
-    rowwise(qa, P.sch_primal, st_, &launches_);
+    rowwise(qa, P.sch_primal, st2_, &launches_);
+    // primal-side terms (kkt.hpp:56-66)
+    launch_reduce<4, 7>(KktPrimalTerms{qx_[0].get(), qx_[1].get(), aty_[0].get(), aty_[1].get(), xu_[0].get(),
+                                       xu_[1].get(), P.c.get()},
+                        n_, false, red2_, P.red_out.get() + 16, st2_);
+    RB_CUDA(cudaEventRecord(evj_, st2_));
+    KktAxOp<false> ax{P.A.view(), xi_.get(), ax_[0].get(), ax_[1].get()};
+    rowwise(ax, P.sch_dual, st_, &launches_);
+    // dual-side terms (kkt.hpp:43-53, 67)
+    launch_reduce<4, 5>(KktDualTerms{ax_[0].get(), ax_[1].get(), P.b.get(), yu_[0].get(), yu_[1].get(), mi_},
+                        m_, false, P.red, P.red_out.get(), st_);
+    RB_CUDA(cudaStreamWaitEvent(st_, evj_, 0));
   }
-  // dual-side terms (kkt.hpp:43-53, 67)
-  launch_reduce<4, 5>(KktDualTerms{ax_[0].get(), ax_[1].get(), P.b.get(), yu_[0].get(), yu_[1].get(), mi_},
-                      m_, P.strict, P.red, P.red_out.get(), st_);
-  // primal-side terms (kkt.hpp:56-66)
-  launch_reduce<4, 7>(KktPrimalTerms{qx_[0].get(), qx_[1].get(), aty_[0].get(), aty_[1].get(), xu_[0].get(),
-                                     xu_[1].get(), P.c.get()},
-                      n_, P.strict, P.red, P.red_out.get() + 16, st_);
   launches_ += 2;
   RB_CUDA(cudaMemcpyAsync(P.red_host.get(), P.red_out.get(), sizeof(double) * 32, cudaMemcpyDeviceToHost, st_));
   bad_.download(bad_h_.get(), 1, st_);  // the chunk's numerical-error flag, with the same sync

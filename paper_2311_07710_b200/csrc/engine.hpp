@@ -163,6 +163,11 @@ class Engine : public LoopBackend {
   void launch_chunk_body(int len, int cur, bool prof);
   void download_point(const double* xu, const double* yu, double* x, double* y);
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+  // fast-mode checks: the primal-side KKT product and its reduction run on a
+  // second stream beside the dual side (each alone is latency-bound)
+  cudaStream_t st2_ = nullptr;
+  cudaEvent_t evf_ = nullptr, evj_ = nullptr;
+  ReduceScratch red2_;
 
   rapdhg_config cfg_;
   std::unique_ptr<DeviceQP> P_;

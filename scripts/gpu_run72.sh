@@ -1,0 +1,3 @@
+export PYTHONUNBUFFERED=1
+timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -2
+for r in 1 2; do timeout 300 python scripts/check_cost.py 2>&1 | head -2; done

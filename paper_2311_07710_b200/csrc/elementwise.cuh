@@ -22,19 +22,26 @@ __global__ void prologue_kernel(const double* __restrict__ x, const double* __re
 }
 
 // unscale_point (scaling.hpp:126-133) of the current iterate and the average.
+// (xi / yi, when given: the same pairs interleaved for the KKT products'
+// 16 B gathers)
 __global__ void unscale_kernel(const double* x, const double* xb, const double* y,
                                const double* yb, const double* d, double* xuc, double* xua,
-                               double* yuc, double* yua, int n, int m) {
+                               double* yuc, double* yua, int n, int m, double2* xi = nullptr,
+                               double2* yi = nullptr) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) {
     const double f = d[i];
-    xuc[i] = x[i] * f;
-    xua[i] = xb[i] * f;
+    const double c = x[i] * f, a = xb[i] * f;
+    xuc[i] = c;
+    xua[i] = a;
+    if (xi) xi[i] = make_double2(c, a);
   } else if (i < n + m) {
     const int r = i - n;
     const double f = d[i];
-    yuc[r] = y[r] * f;
-    yua[r] = yb[r] * f;
+    const double c = y[r] * f, a = yb[r] * f;
+    yuc[r] = c;
+    yua[r] = a;
+    if (yi) yi[r] = make_double2(c, a);
   }
 }
 

@@ -718,14 +718,11 @@ void Engine::run_chunk(int len) {
 Cand Engine::evaluate() {
   const int cur = cur_;
   unscale_kernel<<<grid1(n_ + m_), 256, 0, st_>>>(X_[cur].get(), xb_.get(), y_.get(), yb_.get(), d_.get(),
-                                                  xu_[0].get(), xu_[1].get(), yu_[0].get(), yu_[1].get(), n_, m_);
+                                                  xu_[0].get(), xu_[1].get(), yu_[0].get(), yu_[1].get(), n_, m_,
+                                                  xi_.get(), yi_.get());
   RB_LAUNCH_CHECK();
   ++launches_;
   DeviceQP& P = *P_;
-  interleave_kernel<<<grid1(n_), 256, 0, st_>>>(xu_[0].get(), xu_[1].get(), xi_.get(), n_);
-  interleave_kernel<<<grid1(m_), 256, 0, st_>>>(yu_[0].get(), yu_[1].get(), yi_.get(), m_);
-  RB_LAUNCH_CHECK();
-  launches_ += 2;
   if (P.strict) {
     KktAxOp<true> ax{P.A.view(), xi_.get(), ax_[0].get(), ax_[1].get()};
     rowwise(ax, P.sch_dual, st_, &launches_);

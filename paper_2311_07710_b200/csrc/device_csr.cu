@@ -2,6 +2,7 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include <atomic>
+#include <climits>
 #include <cstdlib>
 #include <cstring>
 #include <thread>
@@ -162,6 +163,43 @@ void HostStager::upload(void* dst, const void* src, std::size_t bytes, cudaStrea
     const cudaError_t e = cudaGetLastError();
     RB_CUDA(e != cudaSuccess ? e : cudaErrorUnknown);
   }
+}
+
+namespace {
+__global__ void csr_check_kernel(const int32_t* rp, const int32_t* ci, int32_t rows, int32_t ncols, int64_t nnz,
+                                 unsigned long long* slot) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x / 32);
+  for (int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32; r < rows; r += warps) {
+    const int64_t b = rp[r], e = rp[r + 1];
+    unsigned long long key = kCsrOk;
+    if (e < b || b < 0 || e > nnz) {
+      key = (static_cast<unsigned long long>(r) << 2) | 1u;
+    } else {
+      int64_t first = INT64_MAX;  // first offending position of the row (this lane's, then the warp's)
+      int kind = 0;
+      for (int64_t k = b + lane; k < e && k < first; k += 32) {
+        const int32_t c = ci[k];
+        if (c < 0 || c >= ncols) first = k, kind = 2;
+        else if (k > b && c <= ci[k - 1]) first = k, kind = 3;
+      }
+      for (int off = 16; off > 0; off >>= 1) {
+        const int64_t f2 = __shfl_xor_sync(0xffffffffu, first, off);
+        const int k2 = __shfl_xor_sync(0xffffffffu, kind, off);
+        if (f2 < first) first = f2, kind = k2;
+      }
+      if (kind) key = (static_cast<unsigned long long>(r) << 2) | static_cast<unsigned>(kind);
+    }
+    if (lane == 0 && key != kCsrOk) atomicMin(slot, key);
+  }
+}
+}  // namespace
+
+void csr_check_async(const DevCsr& m, unsigned long long* slot, cudaStream_t st) {
+  if (m.rows <= 0) return;
+  const int64_t blocks = std::min<int64_t>(ceil_div(static_cast<int64_t>(m.rows) * 32, 256), 16 * kSMs);
+  csr_check_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(m.rp.get(), m.ci.get(), m.rows, m.cols, m.nnz, slot);
+  RB_LAUNCH_CHECK();
 }
 
 void upload_csr(DevCsr& d, const rapdhg_csr& h, cudaStream_t st, HostStager* sg) {

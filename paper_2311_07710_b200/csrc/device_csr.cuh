@@ -49,6 +49,15 @@ class HostStager {
 // Host CSR (validated for shape/index ranges by the caller) -> device.
 void upload_csr(DevCsr& d, const rapdhg_csr& h, cudaStream_t st, HostStager* sg = nullptr);
 
+// Structural check of an uploaded CSR (the per-row part of
+// QuadraticProgram::validate, problem.hpp:40-46): *slot (preset to ~0) gets
+// min over bad rows of (row << 2 | kind), kind 1 = row_ptr not monotone (or
+// outside [0, nnz]), 2 = column out of range, 3 = columns not strictly
+// increasing — within a row the first offending entry decides, as in a
+// sequential scan. One warp per row.
+constexpr unsigned long long kCsrOk = ~0ull;
+void csr_check_async(const DevCsr& m, unsigned long long* slot, cudaStream_t st);
+
 // [top; bottom] row stacking of two CSRs with equal column counts.
 void stack_csr(DevCsr& out, const DevCsr& top, const DevCsr& bottom, cudaStream_t st);
 

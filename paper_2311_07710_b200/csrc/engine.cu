@@ -95,18 +95,28 @@ void finalize_kkt(const KktRaw& r, Kkt out[2]) {
 // DeviceQP
 // ============================================================================
 
-void DeviceQP::validate_dims(const rapdhg_qp& p) {
+namespace {
+// the per-row errors of a CSR, as validate_dims reports them
+[[noreturn]] void csr_error(int kind) {
+  if (kind == 2) throw Error(RAPDHG_E_OUT_OF_RANGE, "sparse entry index out of range");
+  if (kind == 3) invalid("CSR columns must be strictly increasing within a row");
+  invalid("CSR row_ptr not monotone");
+}
+}  // namespace
+
+void DeviceQP::validate_dims(const rapdhg_qp& p, bool structure) {
   // problem.hpp:40-46 messages
   const int n = p.n;
   if (p.q.n_rows != n || p.q.n_cols != n) invalid("Q dimension mismatch");
   if (p.a_ineq.n_rows != p.m_ineq || p.a_ineq.n_cols != n)
     invalid("inequality block dimension mismatch");
   if (p.a_eq.n_rows != p.m_eq || p.a_eq.n_cols != n) invalid("equality block dimension mismatch");
-  auto check = [](const rapdhg_csr& a) {
+  auto check = [structure](const rapdhg_csr& a) {
     if (a.n_rows < 0 || a.n_cols < 0) invalid("negative matrix dimension");
     if (a.nnz > 0 && (!a.col_idx || !a.values)) invalid("null CSR arrays");
     if (!a.row_ptr) invalid("null CSR row_ptr");
     if (a.row_ptr[0] != 0 || a.row_ptr[a.n_rows] != a.nnz) invalid("CSR row_ptr inconsistent with nnz");
+    if (!structure) return;
     // rows in contiguous blocks on host threads; the error reported is the one a
     // sequential scan meets first (lowest block)
     enum { kOk, kMono, kRange, kOrder };
@@ -135,18 +145,15 @@ void DeviceQP::validate_dims(const rapdhg_qp& p) {
         });
       for (auto& x : th) x.join();
     }
-    for (int e : err) {
-      if (e == kMono) invalid("CSR row_ptr not monotone");
-      if (e == kRange) throw Error(RAPDHG_E_OUT_OF_RANGE, "sparse entry index out of range");
-      if (e == kOrder) invalid("CSR columns must be strictly increasing within a row");
-    }
+    for (int e : err)
+      if (e != kOk) csr_error(e == kMono ? 1 : e == kRange ? 2 : 3);
   };
   check(p.q);
   check(p.a_ineq);
   check(p.a_eq);
 }
 
-DeviceQP::DeviceQP(const rapdhg_qp& p, bool strict_, cudaStream_t st_)
+DeviceQP::DeviceQP(const rapdhg_qp& p, bool strict_, cudaStream_t st_, bool check_structure)
     : st(st_), strict(strict_), n(p.n), mi(p.m_ineq), me(p.m_eq), m(p.m_ineq + p.m_eq) {
   Tracer tr(st);
   {
@@ -155,6 +162,18 @@ DeviceQP::DeviceQP(const rapdhg_qp& p, bool strict_, cudaStream_t st_)
     DevCsr ai, ae;
     upload_csr(ai, p.a_ineq, st, &sg);
     upload_csr(ae, p.a_eq, st, &sg);
+    if (check_structure) {  // before any kernel indexes with the uploaded arrays
+      DevBuf<unsigned long long> slot(3);
+      RB_CUDA(cudaMemsetAsync(slot.get(), 0xff, sizeof(unsigned long long) * 3, st));
+      csr_check_async(Q, slot.get(), st);
+      csr_check_async(ai, slot.get() + 1, st);
+      csr_check_async(ae, slot.get() + 2, st);
+      unsigned long long h[3];
+      RB_CUDA(cudaMemcpyAsync(h, slot.get(), sizeof(h), cudaMemcpyDeviceToHost, st));
+      RB_CUDA(cudaStreamSynchronize(st));
+      for (unsigned long long k : h)  // Q, A_ineq, A_eq: the order validate_dims checks them in
+        if (k != kCsrOk) csr_error(static_cast<int>(k & 3u));
+    }
     stack_csr(A, ai, ae, st);  // WorkingProblem::from (solver.hpp:106-108)
     RB_CUDA(cudaStreamSynchronize(st));
   }
@@ -393,13 +412,13 @@ double DeviceQP::op_norm_a(const double* av, const double* atv, int max_iters, d
 
 Engine::Engine(const rapdhg_qp& p, const rapdhg_config& cfg, Clock::time_point t0) : cfg_(cfg) {
   Tracer tr(nullptr);
-  DeviceQP::validate_dims(p);
+  DeviceQP::validate_dims(p, false);  // the per-row scan runs on the device after the upload
   tr.mark("validate dims (host)");
   RB_CUDA(cudaSetDevice(cfg.device));
   RB_CUDA(cudaStreamCreate(&st_));  // blocking: ordered with the pool's legacy-stream allocs/frees
   tr.st = st_;
   tr.mark("device + stream");
-  P_ = std::make_unique<DeviceQP>(p, cfg.strict_parity != 0, st_);
+  P_ = std::make_unique<DeviceQP>(p, cfg.strict_parity != 0, st_, true);
   tr.mark("upload, stack, A', schedules");
   P_->validate_symmetry();  // original.validate() (solver.hpp:277)
   tr.mark("symmetry check");

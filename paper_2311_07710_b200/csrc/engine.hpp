@@ -48,10 +48,14 @@ void finalize_kkt(const KktRaw& r, Kkt out[2]);  // kkt.hpp:54,63,68-69
 
 class DeviceQP {
  public:
-  DeviceQP(const rapdhg_qp& p, bool strict, cudaStream_t st);
+  // check_structure: run the per-row CSR checks of validate_dims on the
+  // device after the upload (validate_dims(p, false) ran on the host).
+  DeviceQP(const rapdhg_qp& p, bool strict, cudaStream_t st, bool check_structure = false);
 
   // QuadraticProgram::validate (problem.hpp:40-50): throws invalid_argument.
-  static void validate_dims(const rapdhg_qp& p);
+  // structure = false: shapes and row_ptr endpoints only (the per-row scan is
+  // left to the device, see the constructor).
+  static void validate_dims(const rapdhg_qp& p, bool structure = true);
   void validate_symmetry();
 
   // compute_scaling / ruiz_scaling (scaling.hpp:159-180). d: n + m factors

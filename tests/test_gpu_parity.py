@@ -255,6 +255,22 @@ def test_solve_edge_cases(O):
     dim.b_ineq = np.array([0.5, 1.0])
     with pytest.raises(rb.InvalidArgument, match="inequality block dimension mismatch"):
         rb.solve(dim, rb.SolverConfig())
+    # per-row CSR structure (checked on the device after the upload, the
+    # first offending row as a sequential scan meets it; problem.hpp:40-46)
+    def with_a(rp, ci, v, n_rows=3):
+        q = random_qp(11, n=6, mi=3, me=0, bounds=False)
+        q.a_ineq = rb.SparseMatrix.from_csr(n_rows, 6, rp, ci, v)
+        q.b_ineq = np.zeros(n_rows)
+        return q
+    with pytest.raises(rb.InvalidArgument, match="strictly increasing"):
+        rb.solve(with_a([0, 2, 4, 5], [0, 3, 2, 2, 1], [1.0] * 5), rb.SolverConfig())
+    with pytest.raises(IndexError, match="out of range"):
+        rb.solve(with_a([0, 2, 4, 5], [0, 3, 2, 6, 1], [1.0] * 5), rb.SolverConfig())
+    with pytest.raises(rb.InvalidArgument, match="not monotone"):
+        rb.solve(with_a([0, 3, 2, 5], [0, 3, 5, 2, 4], [1.0] * 5), rb.SolverConfig())
+    # first row wins: an order error in row 0 before a range error in row 2
+    with pytest.raises(rb.InvalidArgument, match="strictly increasing"):
+        rb.solve(with_a([0, 2, 4, 5], [3, 1, 2, 4, 9], [1.0] * 5), rb.SolverConfig())
 
 
 def test_numerical_error_status(O):

@@ -25,7 +25,8 @@
 namespace rb {
 
 constexpr int kMaxChunk = 64;
-constexpr int kProfilePeriod = 8;  // profile_kernels: time every 8th chunk
+constexpr int kProfilePeriod = 32;  // profile_kernels: time every 32nd chunk (events between
+                                    // the steps cost the programmatic overlap of that chunk)
 
 using Clock = std::chrono::steady_clock;
 

@@ -374,7 +374,7 @@ class SolverConfig:
     device: int = 0
     strict_parity: bool = False
     use_graphs: bool = True
-    profile_kernels: bool = False
+    profile_kernels: int = 0  # 1: CUDA events around the steps of sampled chunks; 2: in-loop step stamps
 
     def _struct(self) -> abi.Config:
         c = abi.Config()
@@ -386,7 +386,7 @@ class SolverConfig:
         c.snapshot_interval = int(self.snapshot_interval)
         c.record_restart_points = int(bool(self.record_restart_points))
         c.device, c.strict_parity = int(self.device), int(bool(self.strict_parity))
-        c.use_graphs, c.profile_kernels = int(bool(self.use_graphs)), int(bool(self.profile_kernels))
+        c.use_graphs, c.profile_kernels = int(bool(self.use_graphs)), int(self.profile_kernels)
         return c
 
 

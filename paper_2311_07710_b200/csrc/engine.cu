@@ -469,6 +469,8 @@ Engine::Engine(const rapdhg_qp& p, const rapdhg_config& cfg, Clock::time_point t
   if (cfg.profile_kernels) {
     events_.resize(2 * kMaxChunk + 1);
     for (auto& e : events_) RB_CUDA(cudaEventCreate(&e));
+    span_mode_ = cfg.profile_kernels == 2;
+    if (span_mode_) span_.alloc(2 * kMaxChunk);
   }
   RB_CUDA(cudaStreamSynchronize(st_));
   tr.mark("omega init + buffers");
@@ -647,6 +649,12 @@ double Engine::bytes_iter() const {
 }
 
 void Engine::launch_chunk_body(int len, int cur, bool prof) {
+  unsigned long long* span = nullptr;
+  if (prof && span_mode_) {  // stamps instead of events
+    span = span_.get();
+    RB_CUDA(cudaMemsetAsync(span, 0xff, sizeof(unsigned long long) * 2 * len, st_));
+    prof = false;
+  }
   prologue_kernel<<<grid1(n_), 256, 0, st_>>>(X_[cur].get(), X_[cur ^ 1].get(), xb_.get(), w_.get(),
                                               XMD_[cur].get(), params_.get(), n_);
   RB_LAUNCH_CHECK();
@@ -660,7 +668,7 @@ void Engine::launch_chunk_body(int len, int cur, bool prof) {
     } else {
       DualStepOp<false> d{P_->A.view(asv_), w_.get(), bsv_, y_.get(), yb_.get(), mi_, params_.get(), it, bad_.get()};
       if (dual_ph_.active()) {
-        launches_ += launch_slab_phase(d, dual_ph_, st_);
+        launches_ += launch_slab_phase(d, dual_ph_, st_, span);
       } else if (cbd_.active()) {
         launches_ += launch_colblocked_dual(d, cbd_, st_);
       } else {
@@ -676,7 +684,7 @@ void Engine::launch_chunk_body(int len, int cur, bool prof) {
       PrimalStepOp<false> pr{P_->Q.view(qsv_), P_->AT.view(atsv_), XMD_[c].get(), y_.get(), X_[c].get(),
                              X_[c ^ 1].get(), xb_.get(), csv_, w_.get(), XMD_[c ^ 1].get(), params_.get(), it, bad_.get()};
       if (primal_ph_.active()) {
-        launches_ += launch_slab_phase(pr, primal_ph_, st_);
+        launches_ += launch_slab_phase(pr, primal_ph_, st_, span);
       } else if (cbp_.active()) {
         launches_ += launch_colblocked_primal(pr, cbp_, st_);
       } else {
@@ -717,7 +725,16 @@ void Engine::run_chunk(int len) {
   bad_fresh_ = false;
   // no sync: the check's kernels queue behind the chunk (first_bad() or
   // evaluate() synchronise); sampled chunks read their events now
-  if (prof) {
+  if (prof && span_mode_) {  // step k lasts from its start to step k + 1's start
+    std::vector<unsigned long long> h(2 * static_cast<std::size_t>(len));
+    span_.download(h.data(), h.size(), st_);
+    RB_CUDA(cudaStreamSynchronize(st_));
+    for (std::size_t k = 0; k + 1 < h.size(); ++k)
+      if (h[k] != ~0ull && h[k + 1] != ~0ull && h[k + 1] > h[k]) {
+        kernel_ms_[k & 1] += static_cast<double>(h[k + 1] - h[k]) * 1e-6;
+        ++kernel_count_[k & 1];
+      }
+  } else if (prof) {
     RB_CUDA(cudaStreamSynchronize(st_));
     for (int it = 0; it < len; ++it) {
       float a = 0.f, b = 0.f;

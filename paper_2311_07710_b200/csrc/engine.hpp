@@ -210,6 +210,10 @@ class Engine : public LoopBackend {
   std::map<int, int64_t> graph_launches_;
   int64_t chunk_counter_ = 0;
   std::vector<cudaEvent_t> events_;
+  // profile_kernels = 2: in-loop step times from the slab kernels' start
+  // stamps (no events between the steps, so the programmatic overlap stays)
+  bool span_mode_ = false;
+  DevBuf<unsigned long long> span_;
   double kernel_ms_[2] = {0, 0};
   int64_t kernel_count_[2] = {0, 0};
   int64_t launches_ = 0;

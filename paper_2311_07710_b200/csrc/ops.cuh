@@ -53,6 +53,7 @@ struct CsrView {
 template <bool Strict>
 struct DualStepOp {
   static constexpr bool kStrict = Strict;
+  static constexpr int kPhase = 0;  // slot of the step in an iteration (in-loop timing)
   static constexpr int kWideUnroll = RB_DUAL_UNROLL;  // long A rows: loads in flight per lane
   static constexpr bool kStageWindows = true;
   using AccT = Acc<1>;
@@ -106,6 +107,7 @@ struct DualStepOp {
 template <bool Strict>
 struct PrimalStepOp {
   static constexpr bool kStrict = Strict;
+  static constexpr int kPhase = 1;
   static constexpr int kWideUnroll = kUnroll;
   static constexpr bool kStageWindows = true;
   using AccT = Acc<2>;

@@ -99,6 +99,7 @@ struct SlabView {
   CsrView rest1{}, rest2{};         // rest CSRs over W rows (segment 1 / 2)
   unsigned long long* prof = nullptr;  // [grid * kSlabProf] phase times (RB_SLAB_PROFILE builds)
   unsigned long long* fprof = nullptr; // [4] finish kernel: max end of other rows, min/max W wait done, max W end
+  unsigned long long* span = nullptr;  // [2 kMaxChunk] in-loop timing: step start (%globaltimer, min over CTAs)
   bool active() const { return nw > 0 && S > 0; }
   __host__ __device__ int tiles() const { return J; }
   // stage: [header 16 B][window][values][columns][metadata]
@@ -313,6 +314,11 @@ __global__ void __launch_bounds__(kSlabThreads) slab_kernel(const Op op, const S
       // the finish kernel may launch once every CTA is past the wait (so its
       // rows without partials see this step's inputs complete)
       asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+      if (sv.span) {  // in-loop timing: the step starts when its inputs are complete
+        unsigned long long now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        atomicMin(&sv.span[2 * op.it + Op::kPhase], now);
+      }
       int held = -1;  // window in the shared buffer
       for (int q = 0; q < pre; ++q) {
         slab_commit(op, sv, pend[q], win, &full[q], q == 0);
@@ -524,8 +530,10 @@ void assign_slab_ctas(SlabPlan& plan, int grid, cudaStream_t st);
 // dependent launch (rows without partials start while the slab kernel runs;
 // W rows wait for it). Returns kernels launched.
 template <class Op>
-inline int launch_slab_phase(const Op& op, const SlabPhase& ph, cudaStream_t st) {
-  const SlabView& sv = ph.plan.view;
+inline int launch_slab_phase(const Op& op, const SlabPhase& ph, cudaStream_t st,
+                             unsigned long long* span = nullptr) {
+  SlabView sv = ph.plan.view;
+  sv.span = span;
   {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(sv.grid));

@@ -117,3 +117,16 @@ def test_slab_many_windows(monkeypatch):
     b = rb.solve(p, cfg)
     for (ta, za), (tb, zb) in zip(a.snapshots, b.snapshots):
         assert ta == tb and rel_err(za.x, zb.x) < 1e-10 and rel_err(za.y_eq, zb.y_eq) < 1e-10
+
+
+def test_inloop_step_stamps(monkeypatch):
+    """profile_kernels=2 times the slab steps in-loop (no events between the
+    steps) and leaves the iterates unchanged."""
+    monkeypatch.setenv("RAPDHG_SLAB", "force")
+    p = rb.generate(rb.Gen.LASSO, 0.05, 2)
+    cfg = dict(tol=1e-9, max_iters=800, snapshot_interval=80)
+    a = rb.solve(p, rb.SolverConfig(**cfg))
+    b = rb.solve(p, rb.SolverConfig(profile_kernels=2, **cfg))
+    assert_results_identical(a, b)
+    assert b.kernel_count[0] > 0 and b.kernel_count[1] > 0
+    assert 0.0 < b.kernel_ms[0] / b.kernel_count[0] < 10.0 and 0.0 < b.kernel_ms[1] / b.kernel_count[1] < 10.0

@@ -117,7 +117,8 @@ typedef struct {
   int32_t strict_parity; /* 1: sequential fp64 sums, no FMA -> bit-exact with
                             the reference; 0: fast deterministic kernels */
   int32_t use_graphs;    /* capture each check interval in a CUDA graph */
-  int32_t profile_kernels; /* record CUDA events around every hot kernel */
+  int32_t profile_kernels; /* 1: CUDA events around the two steps of every 32nd chunk;
+                             2: in-loop step times from %globaltimer stamps (slab path) */
 } rapdhg_config;
 
 void rapdhg_config_default(rapdhg_config* cfg);
@@ -170,8 +171,8 @@ typedef struct {
   double setup_seconds;     /* upload + validate + scaling + norms */
   double loop_seconds;      /* iterations + checks, device time    */
   int64_t kernel_launches;  /* library kernels launched by this call */
-  /* profile_kernels=1: summed CUDA-event time (ms) and launch counts of the
-   * two hot kernels (0 = dual step A*w, 1 = primal step [Q|A']) */
+  /* profile_kernels=1|2: summed time (ms) and sample counts of the two
+   * steps (0 = dual step A*w, 1 = primal step [Q|A']) in sampled chunks */
   double kernel_ms[2];
   int64_t kernel_count[2];
 } rapdhg_result;

@@ -127,7 +127,7 @@ void HostStager::upload(void* dst, const void* src, std::size_t bytes, cudaStrea
   last_ = st;
   const std::size_t nch = (bytes + kChunk - 1) / kChunk;
   const int T = static_cast<int>(std::min<std::size_t>(
-      nch, std::min<unsigned>(threads_, std::max(1u, std::thread::hardware_concurrency() / 2))));
+      nch, std::min<unsigned>(threads_, std::max(1u, std::thread::hardware_concurrency()))));
   for (int s = 0; s < 2 * T; ++s)
     if (!buf_[s]) {
       buf_[s] = pinned_acquire(kChunk);

@@ -1,9 +1,12 @@
 // sharded.cu — row-sharded multi-GPU rAPDHG; see sharded.hpp for the design.
+#include <cub/device/device_select.cuh>
+#include <thrust/iterator/counting_iterator.h>
 #include <dlfcn.h>
 #include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <mutex>
@@ -18,6 +21,49 @@ namespace rb {
 namespace {
 
 inline unsigned grid1(int64_t n) { return static_cast<unsigned>(ceil_div(n > 0 ? n : 1, 256)); }
+
+__global__ void halo_pack_kernel(double* dst, const double* src, const int32_t* idx, int64_t n) {
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[k] = src[idx[k]];
+}
+__global__ void halo_unpack_kernel(double* dst, const double* src, const int32_t* idx, int64_t n) {
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[idx[k]] = src[k];
+}
+inline unsigned gridn(int64_t n) { return static_cast<unsigned>(std::min<int64_t>(ceil_div(n > 0 ? n : 1, 256), 8 * kSMs)); }
+void halo_pack(const HaloSide& h, const double* buf, cudaStream_t st) {
+  const int64_t n = h.send_off.back();
+  if (n > 0) halo_pack_kernel<<<gridn(n), 256, 0, st>>>(h.send_buf.get(), buf, h.send_idx.get(), n);
+  RB_LAUNCH_CHECK();
+}
+void halo_unpack(const HaloSide& h, double* buf, cudaStream_t st) {
+  const int64_t n = h.recv_off.back();
+  if (n > 0) halo_unpack_kernel<<<gridn(n), 256, 0, st>>>(buf, h.recv_buf.get(), h.recv_idx.get(), n);
+  RB_LAUNCH_CHECK();
+}
+
+// flags[ci[k]] = 1 for the entries of rows [r0, r1)
+__global__ void halo_mark_kernel(const int32_t* rp, const int32_t* ci, int64_t r0, int64_t r1, uint8_t* flags) {
+  const int64_t b = rp[r0], e = rp[r1];
+  for (int64_t k = b + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < e;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    flags[ci[k]] = 1;
+}
+// pos[j] = first position in the sorted list with value >= keys[j]
+__global__ void lower_bounds_kernel(const int32_t* list, const int32_t* count, const int64_t* keys, int nk,
+                                    int64_t* pos) {
+  const int j = threadIdx.x;
+  if (j >= nk) return;
+  int64_t lo = 0, hi = *count;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) / 2;
+    if (list[mid] < keys[j]) lo = mid + 1;
+    else hi = mid;
+  }
+  pos[j] = lo;
+}
 
 // Boundaries of `parts` contiguous blocks of rows with costs len[r] + 2,
 // inner boundaries rounded to multiples of kRedChunk (never decreasing).
@@ -74,6 +120,22 @@ class EmulatedTransport : public Transport {
           RB_CUDA(cudaMemcpyAsync(bufs[j] + b[k], bufs[k] + b[k], sizeof(double) * len, cudaMemcpyDeviceToDevice, st));
     }
   }
+  // the NCCL protocol with device copies between the shards' packed buffers
+  void halo(const std::vector<double*>& bufs, const std::vector<HaloSide*>& sides, cudaStream_t st) override {
+    for (int j = 0; j < parts_; ++j) halo_pack(*sides[j], bufs[j], st);
+    for (int i = 0; i < parts_; ++i)
+      for (int j = 0; j < parts_; ++j) {
+        if (i == j) continue;
+        const int64_t cnt = sides[i]->recv_off[j + 1] - sides[i]->recv_off[j];
+        if (cnt != sides[j]->send_off[i + 1] - sides[j]->send_off[i])
+          throw Error(RAPDHG_E_INTERNAL, "halo lists disagree");
+        if (cnt > 0)
+          RB_CUDA(cudaMemcpyAsync(sides[i]->recv_buf.get() + sides[i]->recv_off[j],
+                                  sides[j]->send_buf.get() + sides[j]->send_off[i], sizeof(double) * cnt,
+                                  cudaMemcpyDeviceToDevice, st));
+      }
+    for (int i = 0; i < parts_; ++i) halo_unpack(*sides[i], bufs[i], st);
+  }
   long long allreduce_min(const std::vector<long long*>& vals, cudaStream_t st) override {
     long long best = std::numeric_limits<long long>::max();
     for (long long* v : vals) {
@@ -97,6 +159,8 @@ struct NcclApi {
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -123,6 +187,8 @@ const NcclApi& nccl() {
     api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
     api.Broadcast = reinterpret_cast<decltype(api.Broadcast)>(sym("ncclBroadcast"));
     api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
+    api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
+    api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
     api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
     api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
     api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
@@ -159,6 +225,24 @@ class NcclTransport : public Transport {
                    "ncclBroadcast");
     }
     nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
+  }
+  // pack, grouped point-to-point sends/receives with every peer, unpack
+  void halo(const std::vector<double*>& bufs, const std::vector<HaloSide*>& sides, cudaStream_t st) override {
+    const HaloSide& h = *sides.at(0);
+    halo_pack(h, bufs.at(0), st);
+    nccl_check(nccl().GroupStart(), "ncclGroupStart");
+    for (int p = 0; p < parts_; ++p) {
+      if (p == rank_) continue;
+      const int64_t ns = h.send_off[p + 1] - h.send_off[p], nr = h.recv_off[p + 1] - h.recv_off[p];
+      if (ns > 0)
+        nccl_check(nccl().Send(h.send_buf.get() + h.send_off[p], static_cast<size_t>(ns), ncclDouble, p, comm_, st),
+                   "ncclSend");
+      if (nr > 0)
+        nccl_check(nccl().Recv(h.recv_buf.get() + h.recv_off[p], static_cast<size_t>(nr), ncclDouble, p, comm_, st),
+                   "ncclRecv");
+    }
+    nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
+    halo_unpack(h, bufs.at(0), st);
   }
   long long allreduce_min(const std::vector<long long*>& vals, cudaStream_t st) override {
     nccl_check(nccl().AllReduce(vals.at(0), scratch_, 1, ncclInt64, ncclMin, comm_, st), "ncclAllReduce");
@@ -268,7 +352,113 @@ ShardedEngine::ShardedEngine(const rapdhg_qp& p, const rapdhg_config& cfg, int p
   params_.alloc(kMaxChunk);
   params_h_.alloc(kMaxChunk);
   red_h_.alloc(64);
+  build_halos();
   RB_CUDA(cudaStreamSynchronize(st_));
+}
+
+// Halo lists of the three per-step exchanges: w (gathered by the dual rows
+// through A, owned by the primal blocks), x_md (primal rows through Q) and y
+// (primal rows through A', owned by the dual blocks). For every shard p the
+// sorted set of indices its rows reference (a flag pass over its entries + a
+// select), cut at the owners' bounds; shard s receives its segments from the
+// other owners and sends every peer p the segment of p's set that s owns.
+void ShardedEngine::build_halos() {
+  const char* env = std::getenv("RAPDHG_HALO");
+  const std::string mode = env ? env : "auto";
+  halo_.clear();
+  halo_.resize(3);
+  if (mode == "off" || parts_ < 2) return;
+  DeviceQP& P = *full_->P_;
+  struct Spec {
+    const DevCsr* mat;
+    const std::vector<int64_t>* rows;    // row blocks of the shards
+    const std::vector<int64_t>* owners;  // owner blocks of the gathered vector
+    int64_t N;
+  };
+  const Spec spec[3] = {{&P.A, &db_, &pb_, P.n}, {&P.Q, &pb_, &pb_, P.n}, {&P.AT, &pb_, &db_, P.m}};
+  for (int kind = 0; kind < 3; ++kind) {
+    const Spec& sp = spec[kind];
+    const int64_t N = sp.N;
+    if (N <= 0) continue;
+    const std::vector<int64_t>& ob = *sp.owners;
+    std::vector<DevBuf<int32_t>> L(parts_);
+    std::vector<std::vector<int64_t>> off(parts_, std::vector<int64_t>(parts_ + 1, 0));
+    DevBuf<uint8_t> flags(N);
+    DevBuf<int32_t> cnt(1);
+    DevBuf<int64_t> keys(parts_ + 1), pos(parts_ + 1);
+    keys.upload(ob.data(), parts_ + 1, st_);
+    const thrust::counting_iterator<int32_t> idx(0);
+    std::size_t tmp_bytes = 0;
+    RB_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp_bytes, idx, flags.get(), static_cast<int32_t*>(nullptr), cnt.get(),
+                                       static_cast<int>(N), st_));
+    DevBuf<unsigned char> tmp(tmp_bytes);
+    int64_t moved = 0, gathered = 0;
+    for (int p = 0; p < parts_; ++p) {
+      flags.zero(st_);
+      const int64_t r0 = (*sp.rows)[p], r1 = (*sp.rows)[p + 1];
+      if (r1 > r0) {
+        halo_mark_kernel<<<4 * kSMs, 256, 0, st_>>>(sp.mat->rp.get(), sp.mat->ci.get(), r0, r1, flags.get());
+        RB_LAUNCH_CHECK();
+      }
+      L[p].alloc(N);
+      RB_CUDA(cub::DeviceSelect::Flagged(tmp.get(), tmp_bytes, idx, flags.get(), L[p].get(), cnt.get(),
+                                         static_cast<int>(N), st_));
+      lower_bounds_kernel<<<1, 32, 0, st_>>>(L[p].get(), cnt.get(), keys.get(), parts_ + 1, pos.get());
+      RB_LAUNCH_CHECK();
+      pos.download(off[p].data(), parts_ + 1, st_);
+      RB_CUDA(cudaStreamSynchronize(st_));
+      for (int j = 0; j < parts_; ++j)
+        if (j != p) moved += off[p][j + 1] - off[p][j];
+      gathered += N - (ob[p + 1] - ob[p]);
+    }
+    halo_entries_[kind] = moved;
+    halo_on_[kind] = mode == "on" || 2 * moved <= gathered;
+    if (!halo_on_[kind]) continue;
+    halo_[kind].resize(shards_.size());
+    for (std::size_t li = 0; li < shards_.size(); ++li) {
+      const int sid = shards_[li]->id;
+      HaloSide& h = halo_[kind][li];
+      h.recv_off.assign(parts_ + 1, 0);
+      h.send_off.assign(parts_ + 1, 0);
+      for (int j = 0; j < parts_; ++j) {
+        h.recv_off[j + 1] = h.recv_off[j] + (j == sid ? 0 : off[sid][j + 1] - off[sid][j]);
+        h.send_off[j + 1] = h.send_off[j] + (j == sid ? 0 : off[j][sid + 1] - off[j][sid]);
+      }
+      const int64_t nr = h.recv_off[parts_], ns = h.send_off[parts_];
+      h.recv_idx.alloc(std::max<int64_t>(nr, 1)), h.recv_buf.alloc(std::max<int64_t>(nr, 1));
+      h.send_idx.alloc(std::max<int64_t>(ns, 1)), h.send_buf.alloc(std::max<int64_t>(ns, 1));
+      for (int j = 0; j < parts_; ++j) {
+        if (j == sid) continue;
+        const int64_t cr = h.recv_off[j + 1] - h.recv_off[j], cs = h.send_off[j + 1] - h.send_off[j];
+        if (cr > 0)
+          RB_CUDA(cudaMemcpyAsync(h.recv_idx.get() + h.recv_off[j], L[sid].get() + off[sid][j], sizeof(int32_t) * cr,
+                                  cudaMemcpyDeviceToDevice, st_));
+        if (cs > 0)
+          RB_CUDA(cudaMemcpyAsync(h.send_idx.get() + h.send_off[j], L[j].get() + off[j][sid], sizeof(int32_t) * cs,
+                                  cudaMemcpyDeviceToDevice, st_));
+      }
+    }
+    RB_CUDA(cudaStreamSynchronize(st_));
+  }
+  if (std::getenv("RAPDHG_TRACE"))
+    std::fprintf(stderr, "[shard] halo (w, x_md, y): %s %s %s, entries per exchange %lld %lld %lld\n",
+                 halo_on_[0] ? "on" : "off", halo_on_[1] ? "on" : "off", halo_on_[2] ? "on" : "off",
+                 static_cast<long long>(halo_entries_[0]), static_cast<long long>(halo_entries_[1]),
+                 static_cast<long long>(halo_entries_[2]));
+}
+
+void ShardedEngine::step_exchange(double* (*pick)(Shard&), HaloKind kind) {
+  if (!halo_on_[kind]) {
+    exchange(pick, kind != kHaloY);
+    return;
+  }
+  std::vector<double*> bufs;
+  std::vector<HaloSide*> sides;
+  for (std::size_t li = 0; li < shards_.size(); ++li) {
+    bufs.push_back(pick(*shards_[li]));
+    sides.push_back(&halo_[kind][li]);
+  }
+  tr_->halo(bufs, sides, st_);
 }
 
 ShardedEngine::~ShardedEngine() {
@@ -346,9 +536,9 @@ void ShardedEngine::body(int len, int cur) {
     }
   }
   const int c0 = cur;
-  exchange([](Shard& s) { return s.w.get(); }, true);
-  if (c0 == 0) exchange([](Shard& s) { return s.XMD[0].get(); }, true);
-  else exchange([](Shard& s) { return s.XMD[1].get(); }, true);
+  step_exchange([](Shard& s) { return s.w.get(); }, kHaloW);
+  if (c0 == 0) step_exchange([](Shard& s) { return s.XMD[0].get(); }, kHaloX);
+  else step_exchange([](Shard& s) { return s.XMD[1].get(); }, kHaloX);
   for (int it = 0; it < len; ++it) {
     const int c = (cur + it) & 1;
     for (auto& sh : shards_) {
@@ -365,7 +555,7 @@ void ShardedEngine::body(int len, int cur) {
         ++launches_;
       }
     }
-    exchange([](Shard& s) { return s.y.get(); }, false);
+    step_exchange([](Shard& s) { return s.y.get(); }, kHaloY);
     for (auto& sh : shards_) {
       if (sh->p1 <= sh->p0) continue;
       const int64_t o = sh->p0;
@@ -384,9 +574,9 @@ void ShardedEngine::body(int len, int cur) {
       }
     }
     if (it + 1 < len) {  // the next step gathers the new w and x_md
-      exchange([](Shard& s) { return s.w.get(); }, true);
-      if (c == 0) exchange([](Shard& s) { return s.XMD[1].get(); }, true);
-      else exchange([](Shard& s) { return s.XMD[0].get(); }, true);
+      step_exchange([](Shard& s) { return s.w.get(); }, kHaloW);
+      if (c == 0) step_exchange([](Shard& s) { return s.XMD[1].get(); }, kHaloX);
+      else step_exchange([](Shard& s) { return s.XMD[0].get(); }, kHaloX);
     }
   }
 }

@@ -36,9 +36,23 @@ struct ShardPlan {
 // nnz-balanced contiguous blocks; inner bounds are multiples of kRedChunk.
 ShardPlan make_shard_plan(const rapdhg_qp& p, int parts);
 
+// Halo exchange of one gathered vector: per local shard, the
+// entries its rows reference that other shards own (recv_idx, grouped by owner,
+// ascending) and the owned entries each peer references (send_idx, grouped by
+// peer) — every rank derives both from the full patterns it holds, so no
+// metadata is exchanged. Values travel packed (send_buf / recv_buf).
+struct HaloSide {
+  DevBuf<int32_t> recv_idx, send_idx;
+  std::vector<int64_t> recv_off, send_off;  // parts + 1 each
+  DevBuf<double> recv_buf, send_buf;
+};
+
 class Transport {
  public:
   virtual ~Transport() = default;
+  // After the call, bufs[s] holds every entry sides[s]->recv_idx names
+  // (from its owner); other non-owned entries are left as they were.
+  virtual void halo(const std::vector<double*>& bufs, const std::vector<HaloSide*>& sides, cudaStream_t st) = 0;
   // After the call, bufs[s] (one per LOCAL shard) holds every owner's slice
   // [bounds[k], bounds[k+1]) of the vector (elements of 8 bytes).
   virtual void allgatherv(const std::vector<double*>& bufs, const std::vector<int64_t>& bounds,
@@ -71,11 +85,20 @@ class ShardedEngine : public LoopBackend {
   void loop_end(rapdhg_result* out) override;
 
   const ShardPlan& plan() const { return plan_; }
+  bool halo_on(int kind) const { return halo_on_[kind]; }
 
  private:
   struct Shard;
   void body(int len, int cur);
   void exchange(double* (*pick)(Shard&), bool primal_space);
+  // per-step exchanges: the halo of the gathered entries when that moves at
+  // most half of an allgather (RAPDHG_HALO=on|off|auto), else the allgather
+  enum HaloKind { kHaloW = 0, kHaloX = 1, kHaloY = 2 };
+  void build_halos();
+  void step_exchange(double* (*pick)(Shard&), HaloKind kind);
+  bool halo_on_[3] = {false, false, false};
+  std::vector<std::vector<HaloSide>> halo_;  // [kind][local shard]
+  int64_t halo_entries_[3] = {0, 0, 0};      // entries moved per exchange (all shards)
   template <int NS, int NM, class MakeF>
   void reduce(bool primal_space, const MakeF& make, double* out_host);
 

@@ -55,7 +55,8 @@ def step_full(Q, A, AT, b, c, mi, s, prm):
     return [xn, x, y, xb, yb]
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, halo=False):
+    import torch
     import torch.distributed as dist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -74,6 +75,26 @@ def _worker(rank, world, port, q):
             out[l_:h_] = v
         return out
 
+    def needed(M, r0, r1):  # sorted columns the rows [r0, r1) of M reference
+        return np.unique(M.indices[M.indptr[r0]:M.indptr[r1]])
+
+    def halo_x(vec, M, rows, owners):
+        """Halo protocol of sharded.cu (world 2): send the peer the entries of
+        its reference set this rank owns, receive the owned-by-peer entries of
+        this rank's set; every other non-owned entry stays stale."""
+        peer = 1 - rank
+        mine = needed(M, rows[rank], rows[rank + 1])
+        theirs = needed(M, rows[peer], rows[peer + 1])
+        send = theirs[(theirs >= owners[rank]) & (theirs < owners[rank + 1])]
+        recv = mine[(mine >= owners[peer]) & (mine < owners[peer + 1])]
+        out = vec.copy()
+        rb_ = torch.zeros(len(recv), dtype=torch.float64)
+        reqs = [dist.isend(torch.from_numpy(vec[send].copy()), peer), dist.irecv(rb_, peer)]
+        for r_ in reqs:
+            r_.wait()
+        out[recv] = rb_.numpy()
+        return out
+
     n, m = p.num_vars(), p.num_rows()
     g = np.random.default_rng(5)
     state = [g.standard_normal(n) * 0.1, np.zeros(n), np.abs(g.standard_normal(m)) * 0.1, np.zeros(n), np.zeros(m)]
@@ -83,11 +104,16 @@ def _worker(rank, world, port, q):
         prm = (k / (k + 1), 2.0 / (k + 2), 1 - 2.0 / (k + 2), 0.01, 0.02)
         th, ib, omib, eta, tau = prm
         ref = step_full(Q, A, AT, b, c, mi, ref, prm)
-        # primal-owned slices of w and x_md, then exchange (prologue / previous step)
-        w, xmd = np.zeros(n), np.zeros(n)
+        # primal-owned slices of w and x_md, then exchange (prologue / previous step);
+        # halo mode: non-owned entries start as NaN, so any use of an entry the
+        # lists missed poisons the result
+        w, xmd = np.full(n, np.nan if halo else 0.0), np.full(n, np.nan if halo else 0.0)
         w[p0:p1] = th * (x[p0:p1] - xp[p0:p1]) + x[p0:p1]
         xmd[p0:p1] = omib * xb[p0:p1] + ib * x[p0:p1]
-        w, xmd = allgatherv(w, p0, p1), allgatherv(xmd, p0, p1)
+        if halo:
+            w, xmd = halo_x(w, A, db, pb), halo_x(xmd, Q, pb, pb)
+        else:
+            w, xmd = allgatherv(w, p0, p1), allgatherv(xmd, p0, p1)
         # dual step on owned dual rows, exchange y
         yn = y.copy()
         yn[d0:d1] = y[d0:d1] + tau * (A[d0:d1] @ w - b[d0:d1])
@@ -95,10 +121,16 @@ def _worker(rank, world, port, q):
         if hi > lo:
             yn[lo:hi] = np.maximum(yn[lo:hi], 0.0)
         yb[d0:d1] = omib * yb[d0:d1] + ib * yn[d0:d1]
-        y = allgatherv(yn, d0, d1)
+        if halo:
+            ys = np.full(m, np.nan)
+            ys[d0:d1] = yn[d0:d1]
+            y_used = halo_x(ys, AT, pb, db)
+        else:
+            y_used = allgatherv(yn, d0, d1)
+        y = allgatherv(yn, d0, d1)  # the full y for the comparison (checks allgather it too)
         # primal step on owned primal rows
         xn = x.copy()
-        xn[p0:p1] = x[p0:p1] - eta * ((Q[p0:p1] @ xmd + c[p0:p1]) + AT[p0:p1] @ y)
+        xn[p0:p1] = x[p0:p1] - eta * ((Q[p0:p1] @ xmd + c[p0:p1]) + AT[p0:p1] @ y_used)
         xb[p0:p1] = omib * xb[p0:p1] + ib * xn[p0:p1]
         xp, x = x, xn
     x, xb = allgatherv(x, p0, p1), allgatherv(xb, p0, p1)
@@ -116,12 +148,13 @@ def _free_port():
     return port
 
 
-def test_two_rank_gloo_protocol_matches_unsharded():
+@pytest.mark.parametrize("halo", [False, True])
+def test_two_rank_gloo_protocol_matches_unsharded(halo):
     torch_mp = pytest.importorskip("torch.multiprocessing")
     ctx = torch_mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, halo)) for r in range(2)]
     for pr in procs:
         pr.start()
     res = [q.get(timeout=240) for _ in procs]

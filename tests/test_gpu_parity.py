@@ -346,3 +346,31 @@ def test_staged_windows_fast(O, force_windows, monkeypatch):
         assert np.array_equal(za.x, zb.x), "windows must not change fast-mode results either"
     a2, _, agree = _fast_vs_ref(O, long_row_qp(), dict(tol=1e-12), 160)
     assert agree >= 2
+
+
+def test_concurrent_solves_are_independent():
+    """concurrent solves on independent data are allowed — two
+    host threads solving at once (each solve has its own stream, plan threads,
+    staging buffers) give exactly the sequential results."""
+    import threading
+    probs = [rb.generate(rb.Gen.LASSO, 0.05, 2), random_qp(41, n=3000, mi=1200, me=300, dens=0.004, q_rank=800)]
+    cfgs = [rb.SolverConfig(tol=1e-6, max_iters=3000), rb.SolverConfig(tol=1e-7, max_iters=2000, strict_parity=True)]
+    seq = [rb.solve(p, c) for p, c in zip(probs, cfgs)]
+    out = [None, None]
+    errs = []
+
+    def run(i):
+        try:
+            for _ in range(2):
+                out[i] = rb.solve(probs[i], cfgs[i])
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=run, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for a, b in zip(out, seq):
+        assert_results_identical(a, b)

@@ -163,3 +163,22 @@ def test_two_rank_gloo_protocol_matches_unsharded(halo):
     res.sort()
     assert all(ok for _, ok, _, _ in res), res
     assert all(nd > 0 and np_ > 0 for _, _, nd, np_ in res), res  # both ranks own rows
+
+
+def test_host_structure_validation_messages():
+    """The host-side per-row CSR scan (used where no device is involved, e.g.
+    the shard plan) reports what the device scan does: the first offending row
+    of a sequential scan, with the reference's messages (problem.hpp:40-46)."""
+    def with_a(rp, ci):
+        q = random_qp(11, n=6, mi=3, me=0, bounds=False)
+        q.a_ineq = rb.SparseMatrix.from_csr(3, 6, rp, ci, [1.0] * len(ci))
+        q.b_ineq = np.zeros(3)
+        return q
+    with pytest.raises(rb.InvalidArgument, match="strictly increasing"):
+        rb.shard_plan(with_a([0, 2, 4, 5], [0, 3, 2, 2, 1]), 2)
+    with pytest.raises(IndexError, match="out of range"):
+        rb.shard_plan(with_a([0, 2, 4, 5], [0, 3, 2, 6, 1]), 2)
+    with pytest.raises(rb.InvalidArgument, match="not monotone"):
+        rb.shard_plan(with_a([0, 3, 2, 5], [0, 3, 5, 2, 4]), 2)
+    with pytest.raises(rb.InvalidArgument, match="strictly increasing"):
+        rb.shard_plan(with_a([0, 2, 4, 5], [3, 1, 2, 4, 9]), 2)

@@ -403,7 +403,8 @@ void ShardedEngine::build_halos() {
       L[p].alloc(N);
       RB_CUDA(cub::DeviceSelect::Flagged(tmp.get(), tmp_bytes, idx, flags.get(), L[p].get(), cnt.get(),
                                          static_cast<int>(N), st_));
-      lower_bounds_kernel<<<1, 32, 0, st_>>>(L[p].get(), cnt.get(), keys.get(), parts_ + 1, pos.get());
+      lower_bounds_kernel<<<1, static_cast<unsigned>((parts_ + 32) / 32 * 32), 0, st_>>>(L[p].get(), cnt.get(), keys.get(),
+                                                                                     parts_ + 1, pos.get());
       RB_LAUNCH_CHECK();
       pos.download(off[p].data(), parts_ + 1, st_);
       RB_CUDA(cudaStreamSynchronize(st_));

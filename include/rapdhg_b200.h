@@ -142,7 +142,9 @@ typedef struct { /* rapdhg::LogRecord (solver.hpp:66-74) */
 } rapdhg_log_record;
 
 /* rapdhg::SolveResult (solver.hpp:76-89). Arrays are allocated by the library
- * and released by rapdhg_result_free(). snapshots are stored row-major:
+ * and released by rapdhg_result_free(). Every call that fills a result zeroes
+ * it first and, when it fails, releases what it had filled: a failed call
+ * leaves an all-zero result (nothing to free). snapshots are stored row-major:
  * snapshot s has x at snapshot_x + s*n and y (ineq then eq) at
  * snapshot_y + s*(m_ineq+m_eq); restart points likewise. */
 typedef struct {

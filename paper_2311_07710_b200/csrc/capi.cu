@@ -34,6 +34,21 @@ int guard(F&& f) {
   }
 }
 
+}  // namespace
+extern "C" void rapdhg_result_free(rapdhg_result* r);
+namespace {
+
+// Entry points that fill a rapdhg_result: `out` starts zeroed, and on any
+// error its partly filled arrays are released again, so a failed call leaves
+// nothing to free.
+template <typename F>
+int result_guard(rapdhg_result* out, F&& f) {
+  if (out) std::memset(out, 0, sizeof(*out));
+  const int rc = guard(std::forward<F>(f));
+  if (rc != RAPDHG_OK && out) rapdhg_result_free(out);
+  return rc;
+}
+
 void require_device() {
   int count = 0;
   if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
@@ -109,12 +124,11 @@ void rapdhg_result_free(rapdhg_result* r) {
 }
 
 int rapdhg_solve(const rapdhg_qp* qp, const rapdhg_config* cfg, rapdhg_result* out) {
-  return guard([&] {
-    const auto t0 = rb::Clock::now();  // solve_seconds counts from entry (solver.hpp:274)
+  const auto t0 = rb::Clock::now();  // solve_seconds counts from entry (solver.hpp:274)
+  return result_guard(out, [&] {
     null_check(qp, "qp");
     null_check(cfg, "cfg");
     null_check(out, "out");
-    std::memset(out, 0, sizeof(*out));
     require_device();
     rb::Tracer tr(nullptr);
     {
@@ -178,10 +192,9 @@ extern "C" {
 
 int rapdhg_solve_sharded(const rapdhg_qp* qp, const rapdhg_config* cfg, const rapdhg_shard_opts* opts,
                          rapdhg_result* out) {
-  return guard([&] {
-    const auto t0 = rb::Clock::now();
+  const auto t0 = rb::Clock::now();
+  return result_guard(out, [&] {
     null_check(out, "out");
-    std::memset(out, 0, sizeof(*out));
     auto e = make_sharded(qp, cfg, opts, t0);
     e->solve(out, t0);
   });
@@ -199,7 +212,7 @@ int rapdhg_shard_session_create(const rapdhg_qp* qp, const rapdhg_config* cfg, c
 }
 
 int rapdhg_shard_session_solve(rapdhg_shard_session* s, rapdhg_result* out) {
-  return guard([&] {
+  return result_guard(out, [&] {
     null_check(s, "session");
     null_check(out, "out");
     s->engine->solve(out, rb::Clock::now());
@@ -223,7 +236,7 @@ int rapdhg_session_create(const rapdhg_qp* qp, const rapdhg_config* cfg, rapdhg_
 }
 
 int rapdhg_session_solve(rapdhg_session* s, rapdhg_result* out) {
-  return guard([&] {
+  return result_guard(out, [&] {
     null_check(s, "session");
     null_check(out, "out");
     s->engine->solve(out, rb::Clock::now());

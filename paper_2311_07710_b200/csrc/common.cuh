@@ -68,18 +68,25 @@ inline void pool_prepare() {
     if (const char* r = std::getenv("RAPDHG_POOL_RESERVE_MB")) {
       const std::size_t bytes = static_cast<std::size_t>(std::atoll(r)) << 20;
       void* p = nullptr;
-      if (bytes && cudaMallocAsync(&p, bytes, cudaStreamLegacy) == cudaSuccess) cudaFreeAsync(p, cudaStreamLegacy);
+      if (bytes && cudaMallocAsync(&p, bytes, cudaStreamPerThread) == cudaSuccess) {
+        cudaFreeAsync(p, cudaStreamPerThread);
+        cudaStreamSynchronize(cudaStreamPerThread);
+      }
     }
   }
   done.fetch_or(bit);
 }
-// The stream pool allocations and frees of this host thread are ordered on:
-// the legacy stream by default; a host thread that works on its own
-// non-blocking stream (the slab planners) orders them on that stream instead,
-// so its allocations do not wait behind the solver stream's queued kernels
-// (legacy-stream operations synchronise with every blocking stream).
+// The stream pool allocations and frees of this host thread are ordered on
+// the stream of the work they serve: every solver object runs on its own
+// NON-BLOCKING stream and enters an AllocStreamScope of it for each call, so
+// a temporary freed at the end of a setup function is ordered after the
+// kernels that read it. Outside any scope (objects destroyed after their
+// stream was synchronised) the per-thread default stream is used. Nothing in
+// the library touches the legacy stream: a legacy-stream operation would
+// synchronise with (and invalidate the graph capture of) any blocking stream
+// of the process, ours or the caller's.
 inline cudaStream_t& alloc_stream() {
-  thread_local cudaStream_t s = cudaStreamLegacy;
+  thread_local cudaStream_t s = cudaStreamPerThread;
   return s;
 }
 struct AllocStreamScope {
@@ -89,6 +96,43 @@ struct AllocStreamScope {
   AllocStreamScope(const AllocStreamScope&) = delete;
   AllocStreamScope& operator=(const AllocStreamScope&) = delete;
 };
+// A non-blocking stream owned by a solver object: declared before the
+// object's device buffers, so it is destroyed after them (they are freed on
+// the alloc stream once the owner has synchronised it).
+class OwnedStream {
+ public:
+  OwnedStream() = default;
+  ~OwnedStream() { reset(); }
+  OwnedStream(const OwnedStream&) = delete;
+  OwnedStream& operator=(const OwnedStream&) = delete;
+  cudaStream_t create(int priority = 0) {
+    reset();
+    RB_CUDA(cudaStreamCreateWithPriority(&s_, cudaStreamNonBlocking, priority));
+    return s_;
+  }
+  void reset() {
+    if (s_) {
+      cudaStreamSynchronize(s_);
+      cudaStreamDestroy(s_);
+      s_ = nullptr;
+    }
+  }
+  cudaStream_t get() const { return s_; }
+
+ private:
+  cudaStream_t s_ = nullptr;
+};
+// Declared LAST in a solver object: synchronises its streams before any of
+// the object's buffers are freed (also when its constructor throws).
+struct SyncBeforeFree {
+  const cudaStream_t* a;
+  const cudaStream_t* b;
+  ~SyncBeforeFree() {
+    if (a && *a) cudaStreamSynchronize(*a);
+    if (b && *b) cudaStreamSynchronize(*b);
+  }
+};
+
 inline void* dev_alloc(std::size_t bytes) {
   void* p = nullptr;
   if (pool_enabled()) {

@@ -415,7 +415,8 @@ Engine::Engine(const rapdhg_qp& p, const rapdhg_config& cfg, Clock::time_point t
   DeviceQP::validate_dims(p, false);  // the per-row scan runs on the device after the upload
   tr.mark("validate dims (host)");
   RB_CUDA(cudaSetDevice(cfg.device));
-  RB_CUDA(cudaStreamCreate(&st_));  // blocking: ordered with the pool's legacy-stream allocs/frees
+  st_ = own_st_.create();  // non-blocking; this object's allocations are ordered on it
+  AllocStreamScope scope(st_);
   tr.st = st_;
   tr.mark("device + stream");
   P_ = std::make_unique<DeviceQP>(p, cfg.strict_parity != 0, st_, true);
@@ -624,13 +625,14 @@ Engine::~Engine() {
   } catch (...) {
   }
 #endif
+  if (st_) cudaStreamSynchronize(st_);  // buffers are freed below / after this body
+  if (st2_) cudaStreamSynchronize(st2_);
   for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
   for (auto& e : events_) cudaEventDestroy(e);
   P_.reset();
   if (evf_) cudaEventDestroy(evf_);
   if (evj_) cudaEventDestroy(evj_);
-  if (st2_) cudaStreamDestroy(st2_);
-  if (st_) cudaStreamDestroy(st_);
+  // own_st_ / own_st2_ are destroyed after the remaining buffers
 }
 
 double Engine::bytes_dual() const {
@@ -774,7 +776,7 @@ Cand Engine::evaluate() {
     // primal side on st2_ (own reduction scratch), dual side on st_, joined
     // before the read-back; the results do not depend on the overlap
     if (!st2_) {
-      RB_CUDA(cudaStreamCreateWithFlags(&st2_, cudaStreamNonBlocking));
+      st2_ = own_st2_.create();
       RB_CUDA(cudaEventCreateWithFlags(&evf_, cudaEventDisableTiming));
       RB_CUDA(cudaEventCreateWithFlags(&evj_, cudaEventDisableTiming));
       red2_.init(std::max(n_, m_), st_);
@@ -910,6 +912,7 @@ void Engine::loop_end(rapdhg_result* out) {
 }
 
 void Engine::solve(rapdhg_result* out, Clock::time_point t0) {
+  AllocStreamScope scope(st_);
   run_loop(*this, cfg_, LoopScalars{norm_q, norm_a, omega0, setup_seconds, n_, mi_, m_ - mi_}, out, t0);
 }
 
@@ -950,11 +953,17 @@ void run_loop(LoopBackend& be, const rapdhg_config& cfg, const LoopScalars& sc, 
   auto log = [&](long t, const Kkt& r, double e, double w, bool rs) {
     append(out->log, out->n_log, rapdhg_log_record{t, r.r_primal, r.r_dual, r.r_gap, e, w, rs ? 1 : 0});
   };
+  // result arrays grow in place; the block stays owned by `out` (freed by
+  // rapdhg_result_free) whether or not the realloc succeeds
+  auto grow = [](double*& arr, int64_t count) {
+    double* p = static_cast<double*>(std::realloc(arr, sizeof(double) * static_cast<std::size_t>(count)));
+    if (!p) throw Error(RAPDHG_E_INTERNAL, "out of host memory");
+    arr = p;
+    return p;
+  };
   auto push_restart_point = [&](int idx) {
-    double* xs = static_cast<double*>(std::realloc(out->restart_x, sizeof(double) * ((out->n_restart_points + 1) * n + 1)));
-    double* ys = static_cast<double*>(std::realloc(out->restart_y, sizeof(double) * ((out->n_restart_points + 1) * m + 1)));
-    if (!xs || !ys) throw Error(RAPDHG_E_INTERNAL, "out of host memory");
-    out->restart_x = xs, out->restart_y = ys;
+    double* xs = grow(out->restart_x, (out->n_restart_points + 1) * n + 1);
+    double* ys = grow(out->restart_y, (out->n_restart_points + 1) * m + 1);
     be.download(idx, xs + out->n_restart_points * n, ys + out->n_restart_points * m);
     ++out->n_restart_points;
   };
@@ -1047,8 +1056,8 @@ void run_loop(LoopBackend& be, const rapdhg_config& cfg, const LoopScalars& sc, 
     if (snapshot_due) {
       const int64_t s = out->n_snapshots;
       append(out->snapshot_iters, out->n_snapshots, static_cast<int64_t>(tc));
-      out->snapshot_x = static_cast<double*>(std::realloc(out->snapshot_x, sizeof(double) * ((s + 1) * n + 1)));
-      out->snapshot_y = static_cast<double*>(std::realloc(out->snapshot_y, sizeof(double) * ((s + 1) * m + 1)));
+      grow(out->snapshot_x, (s + 1) * n + 1);
+      grow(out->snapshot_y, (s + 1) * m + 1);
       be.download(1, out->snapshot_x + s * n, out->snapshot_y + s * m);
     }
     if (cres.relkkt() <= cfg.tol) {
@@ -1056,7 +1065,8 @@ void run_loop(LoopBackend& be, const rapdhg_config& cfg, const LoopScalars& sc, 
       finish(RAPDHG_STATUS_OPTIMAL, cand.is_avg ? 1 : 0, tc, cres);
       break;
     }
-    if (elapsed() > cfg.time_limit_s) {
+    // (an infinite limit is never reached: no vote needed)
+    if (std::isfinite(cfg.time_limit_s) && be.any_rank(elapsed() > cfg.time_limit_s)) {
       log(tc, cres, cur_eta, omega, false);
       finish(RAPDHG_STATUS_TIME_LIMIT, 2, tc, best);
       break;
@@ -1116,12 +1126,14 @@ void run_loop(LoopBackend& be, const rapdhg_config& cfg, const LoopScalars& sc, 
 // ============================================================================
 
 namespace {
+// The stream of one secondary-API call: non-blocking, and the call's
+// allocations are ordered on it. Declared before the call's buffers, which are
+// therefore freed on it in stream order before it is drained and destroyed.
 struct StreamGuard {
-  cudaStream_t s = nullptr;
-  StreamGuard() { RB_CUDA(cudaStreamCreate(&s)); }
-  ~StreamGuard() {
-    if (s) cudaStreamDestroy(s);
-  }
+  OwnedStream own;
+  cudaStream_t s = own.create();
+  AllocStreamScope scope{s};
+  ~StreamGuard() { cudaStreamSynchronize(s); }
 };
 
 rapdhg_qp single_matrix_qp(const rapdhg_csr& m, std::vector<int32_t>& zero_rp) {

@@ -122,6 +122,9 @@ class LoopBackend {
   virtual void restart(bool from_avg, double* dx, double* dy) = 0;  // + dist2 for omega
   virtual void download(int src, double* x, double* y) = 0;  // 0 cur, 1 avg, 2 best
   virtual void loop_end(rapdhg_result* out) = 0;  // loop time, launch counts
+  // Collective OR of a host decision taken at a check (the time limit): every
+  // rank must leave the loop at the same check, or their collectives diverge.
+  virtual bool any_rank(bool flag) { return flag; }
 };
 
 struct LoopScalars {
@@ -165,6 +168,8 @@ class Engine : public LoopBackend {
 
  private:
   friend class ShardedEngine;
+  // the streams outlive every buffer below (declared first, destroyed last)
+  OwnedStream own_st_, own_st2_;
   void launch_chunk_body(int len, int cur, bool prof);
   void download_point(const double* xu, const double* yu, double* x, double* y);
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
@@ -217,6 +222,7 @@ class Engine : public LoopBackend {
   double kernel_ms_[2] = {0, 0};
   int64_t kernel_count_[2] = {0, 0};
   int64_t launches_ = 0;
+  SyncBeforeFree sync_{&st_, &st2_};  // last member: runs first on destruction
 };
 
 // ---- secondary API helpers (host buffers in/out) ----------------------------

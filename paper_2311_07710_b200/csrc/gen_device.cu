@@ -166,8 +166,9 @@ bool gen_large_device(double scale, uint64_t seed, bool local, rapdhg_qp_owned* 
   }
   const int32_t n = std::max<int32_t>(16, static_cast<int32_t>(std::lround(1e7 * scale)));
   const int32_t m = std::max<int32_t>(8, n / 2);
-  cudaStream_t st;
-  RB_CUDA(cudaStreamCreate(&st));
+  OwnedStream own;  // destroyed after the buffers below, which are freed on it
+  cudaStream_t st = own.create();
+  AllocStreamScope scope(st);
   // A
   DevBuf<int32_t> acnt(m), tc(static_cast<std::size_t>(m) * 12), arp, aci;
   DevBuf<double> tv(static_cast<std::size_t>(m) * 12), av, b(m), c(n);
@@ -228,7 +229,6 @@ bool gen_large_device(double scale, uint64_t seed, bool local, rapdhg_qp_owned* 
   out->b_ineq = to_host(b, m, st);
   out->b_eq = static_cast<double*>(std::malloc(sizeof(double)));
   RB_CUDA(cudaStreamSynchronize(st));
-  RB_CUDA(cudaStreamDestroy(st));
   return true;
 }
 

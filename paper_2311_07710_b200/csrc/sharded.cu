@@ -76,7 +76,9 @@ std::vector<int32_t> balanced_bounds(const std::vector<int64_t>& cost_prefix, in
     const auto it = std::lower_bound(cost_prefix.begin(), cost_prefix.end(), static_cast<int64_t>(target));
     int64_t r = std::distance(cost_prefix.begin(), it);
     r = ((r + kRedChunk / 2) / kRedChunk) * kRedChunk;  // align for the chunked reductions
-    r = std::min<int64_t>(std::max<int64_t>(r, b[k - 1]), rows);
+    // never past the last whole chunk: a bound at `rows` would hand the final
+    // partial chunk's reduction slot to an empty trailing shard
+    r = std::min<int64_t>(std::max<int64_t>(r, b[k - 1]), (rows / kRedChunk) * kRedChunk);
     b[k] = static_cast<int32_t>(r);
   }
   return b;
@@ -208,11 +210,10 @@ class NcclTransport : public Transport {
     ncclUniqueId uid;
     std::memcpy(&uid, id, sizeof(uid));
     nccl_check(nccl().CommInitRank(&comm_, parts, uid, rank), "ncclCommInitRank");
-    RB_CUDA(cudaMalloc(&scratch_, sizeof(long long)));
+    scratch_.alloc(1);
   }
   ~NcclTransport() override {
     if (comm_) nccl().CommDestroy(comm_);
-    if (scratch_) cudaFree(scratch_);
   }
   // allgather-v: every owner broadcasts its slice in place, grouped
   void allgatherv(const std::vector<double*>& bufs, const std::vector<int64_t>& b, cudaStream_t st) override {
@@ -245,9 +246,9 @@ class NcclTransport : public Transport {
     halo_unpack(h, bufs.at(0), st);
   }
   long long allreduce_min(const std::vector<long long*>& vals, cudaStream_t st) override {
-    nccl_check(nccl().AllReduce(vals.at(0), scratch_, 1, ncclInt64, ncclMin, comm_, st), "ncclAllReduce");
+    nccl_check(nccl().AllReduce(vals.at(0), scratch_.get(), 1, ncclInt64, ncclMin, comm_, st), "ncclAllReduce");
     long long h = 0;
-    RB_CUDA(cudaMemcpyAsync(&h, scratch_, sizeof(h), cudaMemcpyDeviceToHost, st));
+    RB_CUDA(cudaMemcpyAsync(&h, scratch_.get(), sizeof(h), cudaMemcpyDeviceToHost, st));
     RB_CUDA(cudaStreamSynchronize(st));
     return h;
   }
@@ -255,7 +256,7 @@ class NcclTransport : public Transport {
  private:
   int parts_, rank_;
   ncclComm_t comm_ = nullptr;
-  long long* scratch_ = nullptr;
+  DevBuf<long long> scratch_;
 };
 
 }  // namespace
@@ -287,7 +288,7 @@ struct ShardedEngine::Shard {
   // received by the exchanges
   DevBuf<double> X[2], XMD[2], w, xb, y, yb, epx, epy, xu[2], yu[2], ax[2], qx[2], aty[2], best_x, best_y;
   DevBuf<double2> xi, yi;  // interleaved unscaled points for the KKT products
-  DevBuf<long long> bad;
+  DevBuf<long long> bad, vote;
   ReduceScratch red;
   DevBuf<double> red_out;
 };
@@ -300,6 +301,7 @@ ShardedEngine::ShardedEngine(const rapdhg_qp& p, const rapdhg_config& cfg, int p
   full_ = std::make_unique<Engine>(p, cfg, t0);  // validation, scaling, norms
   plan_ = make_shard_plan(p, parts);
   st_ = full_->st_;
+  AllocStreamScope scope(st_);
   DeviceQP& P = *full_->P_;
   const int n = P.n, m = P.m;
   pb_.assign(plan_.primal.begin(), plan_.primal.end());
@@ -344,7 +346,7 @@ ShardedEngine::ShardedEngine(const rapdhg_qp& p, const rapdhg_config& cfg, int p
     sh->w.alloc(n), sh->xb.alloc(n), sh->y.alloc(m), sh->yb.alloc(m), sh->epx.alloc(n), sh->epy.alloc(m);
     sh->xi.alloc(n), sh->yi.alloc(m);
     sh->best_x.alloc(n), sh->best_y.alloc(m);
-    sh->bad.alloc(1);
+    sh->bad.alloc(1), sh->vote.alloc(1);
     sh->red.init(std::max<int64_t>(n, m), st_);
     sh->red_out.alloc(64);
     shards_.push_back(std::move(sh));
@@ -463,10 +465,12 @@ void ShardedEngine::step_exchange(double* (*pick)(Shard&), HaloKind kind) {
 }
 
 ShardedEngine::~ShardedEngine() {
+  if (st_) cudaStreamSynchronize(st_);
   for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
 }
 
 void ShardedEngine::solve(rapdhg_result* out, Clock::time_point t0) {
+  AllocStreamScope scope(st_);
   const Engine& e = *full_;
   run_loop(*this, cfg_, LoopScalars{e.norm_q, e.norm_a, e.omega0, e.setup_seconds, e.n_, e.mi_, e.m_ - e.mi_},
            out, t0);
@@ -495,7 +499,9 @@ void ShardedEngine::reduce(bool primal_space, const MakeF& make, double* out_hos
     ++launches_;
   }
   std::vector<int64_t> cb(parts_ + 1);
-  for (int k = 0; k < parts_; ++k) cb[k] = (b[k] / kRedChunk) * NT;
+  // a shard owns the chunks its first row starts; a bound at `total` (only
+  // empty trailing shards) owns none
+  for (int k = 0; k < parts_; ++k) cb[k] = (b[k] == total ? reduce_chunks(total) : b[k] / kRedChunk) * NT;
   cb[parts_] = reduce_chunks(total) * NT;
   std::vector<double*> bufs;
   for (auto& sh : shards_) bufs.push_back(sh->red.partials.get());
@@ -614,6 +620,16 @@ long long ShardedEngine::first_bad() {
   std::vector<long long*> v;
   for (auto& sh : shards_) v.push_back(sh->bad.get());
   return tr_->allreduce_min(v, st_);
+}
+
+bool ShardedEngine::any_rank(bool flag) {
+  const long long keep_going = flag ? 0 : 1;  // min over ranks == 0: someone stops
+  std::vector<long long*> v;
+  for (auto& sh : shards_) {
+    RB_CUDA(cudaMemcpyAsync(sh->vote.get(), &keep_going, sizeof(keep_going), cudaMemcpyHostToDevice, st_));
+    v.push_back(sh->vote.get());
+  }
+  return tr_->allreduce_min(v, st_) == 0;
 }
 
 Cand ShardedEngine::evaluate() {

@@ -83,6 +83,7 @@ class ShardedEngine : public LoopBackend {
   void restart(bool from_avg, double* dx, double* dy) override;
   void download(int src, double* x, double* y) override;
   void loop_end(rapdhg_result* out) override;
+  bool any_rank(bool flag) override;
 
   const ShardPlan& plan() const { return plan_; }
   bool halo_on(int kind) const { return halo_on_[kind]; }
@@ -119,6 +120,7 @@ class ShardedEngine : public LoopBackend {
   std::map<int, int64_t> replay_launches_;
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
   int64_t launches_ = 0;
+  SyncBeforeFree sync_{&st_, nullptr};  // last member: runs first on destruction
 };
 
 }  // namespace rb

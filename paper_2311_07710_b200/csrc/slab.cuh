@@ -412,6 +412,16 @@ inline int SlabView::smem_bytes() const { return win_max * 8 + kSlabStages * sta
 //  * the first blocks: ordinary rowwise tiles of the rows without partials
 //    (no wait: they overlap the slab kernel; scheduled first so the waiting
 //    W blocks do not hold SM slots while the slab kernel still runs).
+// Visibility of the rows without partials: they gather vectors written two
+// grids earlier (the previous step's finish kernel F). This grid is launched
+// only once every CTA of the slab kernel S between them has triggered, and
+// S's CTAs trigger after their own griddepcontrol.wait on F returned, so F
+// has completed and its writes have been flushed to L2 before any block here
+// starts. PTX promises visibility of F's writes only to S, so this relies on
+// the flush at F's completion reaching every later reader (and on no stale L1
+// line surviving into this grid); the GPU tests (test_gpu_slab.py) hold this
+// schedule to the fully serialised one (RAPDHG_PDL=0) bit for bit over
+// thousands of steps at the bench's size.
 template <class Op>
 __global__ void __launch_bounds__(kBlock) slab_finish_kernel(const Op op, const Op rest, const SlabView sv,
                                                              const SchedView others, int wblocks) {
@@ -529,10 +539,20 @@ void assign_slab_ctas(SlabPlan& plan, int grid, cudaStream_t st);
 // One slab-tiled op: the slab kernel, then the finish kernel as a programmatic
 // dependent launch (rows without partials start while the slab kernel runs;
 // W rows wait for it). Returns kernels launched.
+// RAPDHG_PDL=0: launch the slab and finish kernels without programmatic
+// stream serialization (every kernel waits for the previous grid; the
+// griddepcontrol instructions become no-ops). Results must not change: the
+// tests compare both schedules bit for bit (see slab_finish_kernel).
+inline bool pdl_enabled() {  // read per launch (launches are captured into graphs once)
+  const char* e = std::getenv("RAPDHG_PDL");
+  return !(e && e[0] == '0');
+}
+
 template <class Op>
 inline int launch_slab_phase(const Op& op, const SlabPhase& ph, cudaStream_t st,
                              unsigned long long* span = nullptr) {
   SlabView sv = ph.plan.view;
+  const unsigned pdl = pdl_enabled() ? 1u : 0u;
   sv.span = span;
   {
     cudaLaunchConfig_t cfg{};
@@ -542,7 +562,7 @@ inline int launch_slab_phase(const Op& op, const SlabPhase& ph, cudaStream_t st,
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     RB_CUDA(cudaLaunchKernelEx(&cfg, slab_kernel<Op>, op, sv));
@@ -556,7 +576,7 @@ inline int launch_slab_phase(const Op& op, const SlabPhase& ph, cudaStream_t st,
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   RB_CUDA(cudaLaunchKernelEx(&cfg, slab_finish_kernel<Op>, op, op.with_views(sv.rest1, sv.rest2), sv, o, wblocks));

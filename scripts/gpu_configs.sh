@@ -1,6 +1,6 @@
 # per-config throughput on one B200 (fast mode, 400-iteration resident solves, per-step in-loop stamps)
 export PYTHONUNBUFFERED=1
-timeout 1200 python - <<'PY' > gpurun_out/configs.jsonl 2> gpurun_out/configs.err
+timeout 1200 python - <<'PY' > gpurun_out/r02_01_configs.jsonl 2> gpurun_out/r02_01_configs.err
 import json, sys
 sys.path.insert(0, ".")
 import paper_2311_07710_b200 as rb
@@ -21,4 +21,4 @@ for name, kind, scale, seed in (("C1 random QP", rb.Gen.RANDOM_QP, 1.0, 1), ("C2
                       "inloop_step_GBs": [None if k is None else b / (k * 1e-3) / 1e9 for k, b in zip(ks, (bd, bp))],
                       "setup_s": r.setup_seconds}), flush=True)
 PY
-cat gpurun_out/configs.jsonl; tail -3 gpurun_out/configs.err
+cat gpurun_out/r02_01_configs.jsonl; tail -3 gpurun_out/r02_01_configs.err

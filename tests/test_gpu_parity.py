@@ -374,3 +374,57 @@ def test_concurrent_solves_are_independent():
     assert not errs, errs
     for a, b in zip(out, seq):
         assert_results_identical(a, b)
+
+
+def test_solves_capture_beside_legacy_stream_work():
+    """every solve captures its chunk graphs on its own stream. With
+    a blocking stream, any legacy-stream operation of the process during a
+    capture (another thread's torch kernels on the default stream, a pool
+    allocation) invalidates it. The solver's streams are non-blocking and its
+    allocations are ordered on them, so fresh sessions (each capturing anew)
+    next to a thread hammering the legacy stream still give the sequential
+    results."""
+    import threading
+
+    import torch
+
+    p = random_qp(43, n=2000, mi=800, me=200, dens=0.004, q_rank=500)
+    cfg = rb.SolverConfig(tol=1e-6, max_iters=1500)
+    want = rb.solve(p, cfg)
+    stop = threading.Event()
+    errs = []
+
+    def legacy_noise():
+        try:
+            a = torch.randn(512, 512, device="cuda:0")
+            while not stop.is_set():
+                b = a @ a  # default (legacy) stream kernels and allocator traffic
+                a = b / b.norm()
+                torch.cuda.synchronize()
+        except Exception as e:
+            errs.append(e)
+
+    def solves(out):
+        try:
+            for _ in range(6):
+                s = rb.Session(p, cfg)
+                out.append(s.solve())
+                s.close()
+        except Exception as e:
+            errs.append(e)
+
+    outs = [[], []]
+    noise = threading.Thread(target=legacy_noise)
+    th = [threading.Thread(target=solves, args=(o,)) for o in outs]
+    noise.start()
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    stop.set()
+    noise.join()
+    assert not errs, errs
+    for o in outs:
+        assert len(o) == 6
+        for r in o:
+            assert_results_identical(r, want)

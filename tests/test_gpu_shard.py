@@ -29,6 +29,16 @@ def test_emulated_shards_bit_identical_random(parts):
     assert (np.diff(db) > 0).sum() >= 2 and (np.diff(pb) > 0).sum() >= 2  # really split
 
 
+@pytest.mark.parametrize("parts", [3, 8])
+def test_emulated_shards_unaligned_tail(parts):
+    """row counts whose balanced bounds would land past the last
+    whole reduction chunk (m = 3500 over 8 parts): the partial chunk must stay
+    with a non-empty shard, so the KKT sums and restart distances agree."""
+    p = random_qp(41, n=3000, mi=1200, me=300, dens=0.02)
+    cfg = rb.SolverConfig(tol=1e-6, max_iters=1200, snapshot_interval=40, record_restart_points=True)
+    assert_results_identical(rb.solve_sharded(p, cfg, parts), rb.solve(p, cfg))
+
+
 def test_emulated_shards_other_configs():
     p = rb.generate(rb.Gen.SVM, 0.004, 4)
     for kw in (dict(restart=rb.RestartPolicy.kAdaptiveHalving),

@@ -130,3 +130,21 @@ def test_inloop_step_stamps(monkeypatch):
     assert_results_identical(a, b)
     assert b.kernel_count[0] > 0 and b.kernel_count[1] > 0
     assert 0.0 < b.kernel_ms[0] / b.kernel_count[0] < 10.0 and 0.0 < b.kernel_ms[1] / b.kernel_count[1] < 10.0
+
+
+def test_pdl_schedule_matches_serialised(monkeypatch):
+    """The finish kernel's rows without partials read vectors written two
+    grids earlier while the slab kernel between them still runs (programmatic
+    dependent launches; slab.cuh). Over a 2000-iteration C2-size solve that
+    schedule must give bit-identical results to fully serialised launches
+    (RAPDHG_PDL=0), and repeat bit for bit."""
+    p = rb.generate(rb.Gen.LASSO, 0.5, 2)
+    cfg = rb.SolverConfig(tol=1e-12, max_iters=2000, snapshot_interval=400, record_restart_points=True)
+    s = rb.Session(p, cfg)
+    a = s.solve()
+    a2 = s.solve()
+    s.close()
+    monkeypatch.setenv("RAPDHG_PDL", "0")
+    b = rb.solve(p, cfg)
+    assert_results_identical(a, a2)
+    assert_results_identical(a, b)

@@ -26,9 +26,15 @@ def test_plan_properties():
             db, pb = rb.shard_plan(p, parts)
             assert db[0] == 0 and db[-1] == m and pb[0] == 0 and pb[-1] == n
             assert np.all(np.diff(db) >= 0) and np.all(np.diff(pb) >= 0)
-            # reduction chunks: inner bounds are multiples of 2048 (or the end: empty shards)
-            assert np.all((db[1:-1] % 2048 == 0) | (db[1:-1] == m))
-            assert np.all((pb[1:-1] % 2048 == 0) | (pb[1:-1] == n))
+            # reduction chunks: inner bounds are multiples of 2048, never the
+            # unaligned end (that would give the last partial chunk to an empty shard)
+            assert np.all(db[1:-1] % 2048 == 0) and np.all(pb[1:-1] % 2048 == 0)
+    # m = 1500 rows, 8 parts -> every inner bound at 0 or 0 (the
+    # whole partial chunk stays with the last, non-empty shard)
+    p = random_qp(41, n=3000, mi=1200, me=300)
+    db, pb = rb.shard_plan(p, 8)
+    assert np.all(db[1:-1] % 2048 == 0) and np.all(pb[1:-1] % 2048 == 0)
+    assert db[-2] < db[-1] and pb[-2] < pb[-1]
     # balance on a large enough instance (block size granularity: 2048 rows)
     p = rb.generate(rb.Gen.LARGE, 1e-2, 3)  # n = 1e5, m = 5e4
     db, pb = rb.shard_plan(p, 4)

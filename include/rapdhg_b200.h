@@ -279,12 +279,12 @@ int rapdhg_pdhg_step(const rapdhg_qp* p, rapdhg_iterate* s, double eta, double t
 int rapdhg_rel_kkt(const rapdhg_qp* p, const double* x, const double* y_ineq,
                    const double* y_eq, rapdhg_kkt* out, int32_t strict);
 
-/* rapdhg::compute_scaling (scaling.hpp:171-180): d1 (m), d2 (n). */
+/* rapdhg::compute_scaling (scaling.hpp:97-106): d1 (m), d2 (n). */
 int rapdhg_compute_scaling(const rapdhg_qp* p, double* d1, double* d2, int32_t strict);
-/* rapdhg::ruiz_scaling (scaling.hpp:159-166) */
+/* rapdhg::ruiz_scaling (scaling.hpp:85-92) */
 int rapdhg_ruiz_scaling(const rapdhg_qp* p, int32_t iterations, double* d1, double* d2,
                         int32_t strict);
-/* rapdhg::apply_scaling (scaling.hpp:183-197): writes the scaled values into
+/* rapdhg::apply_scaling (scaling.hpp:109-123): writes the scaled values into
  * caller buffers laid out like the input CSRs (same patterns). */
 int rapdhg_apply_scaling(const rapdhg_qp* p, const double* d1, const double* d2,
                          double* q_values, double* a_ineq_values, double* a_eq_values,

@@ -272,7 +272,7 @@ int ref_ruiz_scaling(const rapdhg_qp* p, int32_t iterations, double* d1, double*
   });
 }
 
-// Scaled problem values (scaling.hpp:183-197). Patterns are unchanged unless a
+// Scaled problem values (scaling.hpp:109-123). Patterns are unchanged unless a
 // scaled entry underflows to exactly 0 (then SparseMatrix drops it); *dropped
 // reports how many entries the reference dropped.
 int ref_apply_scaling(const rapdhg_qp* p, const double* d1, const double* d2, double* qv,

@@ -667,7 +667,7 @@ class ScalingInfo:
 
 
 def compute_scaling(p: QuadraticProgram, strict: bool = False) -> ScalingInfo:
-    """scaling.hpp:171-180 on the GPU."""
+    """scaling.hpp:97-106 on the GPU."""
     d1, d2 = np.empty(p.num_rows()), np.empty(p.num_vars())
     qp = p._struct()
     _check(_load().rapdhg_compute_scaling(C.byref(qp), _pf(d1), _pf(d2), int(strict)))
@@ -675,7 +675,7 @@ def compute_scaling(p: QuadraticProgram, strict: bool = False) -> ScalingInfo:
 
 
 def ruiz_scaling(p: QuadraticProgram, iterations: int, strict: bool = False) -> ScalingInfo:
-    """scaling.hpp:159-166 on the GPU."""
+    """scaling.hpp:85-92 on the GPU."""
     d1, d2 = np.empty(p.num_rows()), np.empty(p.num_vars())
     qp = p._struct()
     _check(_load().rapdhg_ruiz_scaling(C.byref(qp), int(iterations), _pf(d1), _pf(d2), int(strict)))
@@ -683,7 +683,7 @@ def ruiz_scaling(p: QuadraticProgram, iterations: int, strict: bool = False) -> 
 
 
 def apply_scaling(p: QuadraticProgram, s: ScalingInfo) -> QuadraticProgram:
-    """scaling.hpp:183-197 on the GPU (patterns kept)."""
+    """scaling.hpp:109-123 on the GPU (patterns kept)."""
     if len(s.d2) != p.num_vars() or len(s.d1) != p.num_rows():
         raise InvalidArgument("apply_scaling: dimension mismatch")
     qv, aiv, aev = np.empty(p.q.nnz()), np.empty(p.a_ineq.nnz()), np.empty(p.a_eq.nnz())

@@ -61,7 +61,7 @@ __global__ void scaled_values_kernel(double* out, const double* v, const int32_t
   out[k] = d[row_off + row_of[k]] * v[k] * d[col_off + ci[k]];
 }
 
-// out[i] = d[off + i] * v[i] (c~ = D2 c, b~ = D1 b; scaling.hpp:193-195)
+// out[i] = d[off + i] * v[i] (c~ = D2 c, b~ = D1 b; scaling.hpp:119-121)
 __global__ void scale_vec_kernel(double* out, const double* v, const double* d, int off, int64_t n) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i < n) out[i] = d[off + i] * v[i];

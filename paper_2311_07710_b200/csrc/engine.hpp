@@ -59,10 +59,10 @@ class DeviceQP {
   static void validate_dims(const rapdhg_qp& p, bool structure = true);
   void validate_symmetry();
 
-  // compute_scaling / ruiz_scaling (scaling.hpp:159-180). d: n + m factors
+  // compute_scaling / ruiz_scaling (scaling.hpp:85-106). d: n + m factors
   // (d2 = d[0:n], d1 = d[n:]).
   void compute_scaling(int ruiz_iters, bool full, DevBuf<double>& d);
-  // apply_scaling (scaling.hpp:183-197) into value arrays with the original
+  // apply_scaling (scaling.hpp:109-123) into value arrays with the original
   // patterns; d as above.
   void scale_values(const double* d, DevBuf<double>& qs, DevBuf<double>& as, DevBuf<double>& ats,
                     DevBuf<double>& cs, DevBuf<double>& bs);

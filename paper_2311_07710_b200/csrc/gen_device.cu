@@ -136,6 +136,49 @@ __global__ void q_rows_kernel(int32_t n, const uint64_t* key, const int32_t* idx
   if (!Write) cnt[i] = w;
 }
 
+// C4 SVM sample row r -> its merged entries + the t entry, in slots
+// [slot r, slot r + cnt) (the host's svm_row, host.cpp)
+__global__ void svm_rows_kernel(int32_t ns, int32_t nf, int32_t per_row, uint64_t seed, int32_t* cnt, int32_t* tc,
+                                double* tv) {
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (r >= ns) return;
+  const int32_t slot = per_row + 1;
+  const double label = r < ns / 2 ? 1.0 : -1.0;
+  const double sd = sqrt(1.0 / nf);
+  int32_t c[50], k[50];
+  for (int32_t q = 0; q < per_row; ++q)
+    c[q] = static_cast<int32_t>(below(uniform(seed, kSvmCol, r, q), static_cast<uint64_t>(nf))), k[q] = q;
+  for (int32_t q = 1; q < per_row; ++q)
+    for (int32_t p = q; p > 0 && (c[p - 1] > c[p] || (c[p - 1] == c[p] && k[p - 1] > k[p])); --p) {
+      const int32_t c0 = c[p - 1], k0 = k[p - 1];
+      c[p - 1] = c[p], k[p - 1] = k[p], c[p] = c0, k[p] = k0;
+    }
+  int32_t w = 0;
+  int32_t* oc = tc + r * slot;
+  double* ov = tv + r * slot;
+  for (int32_t q = 0; q < per_row;) {
+    double x = __dmul_rn(label, __dadd_rn(label / nf, __dmul_rn(sd, normal(seed, kSvmVal, r, k[q]))));
+    int32_t e = q + 1;
+    for (; e < per_row && c[e] == c[q]; ++e)
+      x = __dadd_rn(x, __dmul_rn(label, __dadd_rn(label / nf, __dmul_rn(sd, normal(seed, kSvmVal, r, k[e])))));
+    if (x != 0.0) oc[w] = c[q], ov[w] = x, ++w;
+    q = e;
+  }
+  oc[w] = nf + static_cast<int32_t>(r), ov[w] = -1.0;
+  cnt[r] = w + 1;
+}
+
+// A = [sample rows (compacted slots); bound rows (ns + r, nf + r) = -1]
+__global__ void svm_compact_kernel(int32_t ns, int32_t nf, int32_t slot, const int32_t* rp, const int32_t* tc,
+                                   const double* tv, int32_t* ci, double* v) {
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (r >= ns) return;
+  const int32_t b = rp[r], len = rp[r + 1] - b;
+  for (int32_t q = 0; q < len; ++q) ci[b + q] = tc[r * slot + q], v[b + q] = tv[r * slot + q];
+  const int32_t o = rp[ns] + static_cast<int32_t>(r);
+  ci[o] = nf + static_cast<int32_t>(r), v[o] = -1.0;
+}
+
 // exclusive scan of `cnt` (rows entries) into rp (rows + 1 entries)
 void scan_rows(DevBuf<int32_t>& cnt, int64_t rows, DevBuf<int32_t>& rp, cudaStream_t st) {
   rp.alloc(rows + 1);
@@ -229,6 +272,50 @@ bool gen_large_device(double scale, uint64_t seed, bool local, rapdhg_qp_owned* 
   out->b_ineq = to_host(b, m, st);
   out->b_eq = static_cast<double*>(std::malloc(sizeof(double)));
   RB_CUDA(cudaStreamSynchronize(st));
+  return true;
+}
+
+}  // namespace rb
+
+namespace rb {
+
+// C4 SVM's constraint matrix A on the device (the dominant cost of the
+// generator: 5e7 entries of 12-uniform normals); the host builds Q, c, b.
+// false when no device is visible.
+bool gen_svm_a_device(int32_t ns, int32_t nf, int32_t per_row, uint64_t seed, rapdhg_csr_owned* a) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return false;
+  }
+  if (per_row > 50) return false;
+  OwnedStream own;
+  cudaStream_t st = own.create();
+  AllocStreamScope scope(st);
+  const int32_t slot = per_row + 1, m = 2 * ns;
+  DevBuf<int32_t> cnt(ns), tc(static_cast<std::size_t>(ns) * slot), rp, ci;
+  DevBuf<double> tv(static_cast<std::size_t>(ns) * slot), v;
+  svm_rows_kernel<<<g1(ns), 128, 0, st>>>(ns, nf, per_row, seed, cnt.get(), tc.get(), tv.get());
+  RB_LAUNCH_CHECK();
+  scan_rows(cnt, ns, rp, st);
+  int32_t nnz_top = 0;
+  RB_CUDA(cudaMemcpyAsync(&nnz_top, rp.get() + ns, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  RB_CUDA(cudaStreamSynchronize(st));
+  const int64_t nnz = static_cast<int64_t>(nnz_top) + ns;
+  ci.alloc(nnz), v.alloc(nnz);
+  svm_compact_kernel<<<g1(ns), 256, 0, st>>>(ns, nf, slot, rp.get(), tc.get(), tv.get(), ci.get(), v.get());
+  RB_LAUNCH_CHECK();
+  a->n_rows = m, a->n_cols = nf + ns, a->nnz = nnz;
+  a->col_idx = to_host(ci, nnz, st);
+  a->values = to_host(v, nnz, st);
+  int32_t* top = to_host(rp, static_cast<std::size_t>(ns) + 1, st);
+  RB_CUDA(cudaStreamSynchronize(st));
+  a->row_ptr = static_cast<int32_t*>(std::realloc(top, sizeof(int32_t) * (static_cast<std::size_t>(m) + 1)));
+  if (!a->row_ptr) {
+    std::free(top);
+    throw Error(RAPDHG_E_INTERNAL, "out of host memory");
+  }
+  for (int32_t r = 0; r < ns; ++r) a->row_ptr[ns + r + 1] = nnz_top + r + 1;
   return true;
 }
 

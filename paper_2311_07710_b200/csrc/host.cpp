@@ -9,6 +9,7 @@
 #include <numeric>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "rapdhg_b200.h"
@@ -19,6 +20,7 @@ void rb_set_error(const char* msg);
 
 namespace rb {
 bool gen_large_device(double scale, uint64_t seed, bool local, rapdhg_qp_owned* out);  // gen_device.cu
+bool gen_svm_a_device(int32_t ns, int32_t nf, int32_t per_row, uint64_t seed, rapdhg_csr_owned* a);
 }
 
 namespace {
@@ -50,6 +52,27 @@ T* xalloc(std::size_t n) {
   T* p = static_cast<T*>(std::malloc(sizeof(T) * (n ? n : 1)));
   if (!p) throw std::bad_alloc();
   return p;
+}
+
+// The counter-based generators (C4, C5) have device versions (gen_device.cu)
+// that build the same arrays; they run for large instances when a device is
+// visible (RAPDHG_GEN_DEVICE=1 / 0 forces them on / off).
+bool use_device_generator(bool large) {
+  const char* e = std::getenv("RAPDHG_GEN_DEVICE");
+  return e ? e[0] == '1' : large;
+}
+
+// f(r) for r in [0, rows) on up to 16 host threads (contiguous ranges)
+template <typename F>
+void parallel_rows(int64_t rows, const F& f) {
+  const int64_t T = std::max<int64_t>(1, std::min<int64_t>({16, static_cast<int64_t>(std::thread::hardware_concurrency()),
+                                                            rows / 4096 + 1}));
+  std::vector<std::thread> th;
+  for (int64_t t = 0; t < T; ++t)
+    th.emplace_back([&, t] {
+      for (int64_t r = rows * t / T; r < rows * (t + 1) / T; ++r) f(r);
+    });
+  for (auto& x : th) x.join();
 }
 
 // ---- RNG: splitmix64-seeded xoshiro256**, Box-Muller normals --------------
@@ -333,35 +356,74 @@ void gen_portfolio(double scale, uint64_t seed, rapdhg_qp_owned* out) {
 }
 
 // ---- C4: SVM  min x'x + lambda 1't  s.t. diag(l) A_s x - t <= -1, -t <= 0
-// variables [x (nf) | t (ns)]
+// variables [x (nf) | t (ns)]. Counter-based (crng.h), so the device
+// generator (gen_device.cu) and the numpy restatement that feeds the
+// reference arm (oracle/synth.py) build bit-identical arrays. Exact algorithm:
+//  * sample row r < ns has label l = +1 for r < ns/2 else -1 and `per_row`
+//    draws k: column below(uniform(kSvmCol, r, k), nf), value
+//    l * (l / nf + sqrt(1/nf) * normal(kSvmVal, r, k)); the draws are sorted
+//    by (column, k) and duplicate columns merged by summing in that order
+//    (a zero sum is dropped); then the entry (r, nf + r) = -1 (t_r);
+//  * row ns + r: (ns + r, nf + r) = -1 (t_r >= 0 as a bound row);
+//  * Q = 2 I on x, c = lambda on t, b = -1 on the sample rows, 0 below.
+int32_t svm_row(uint64_t seed, int64_t r, int32_t ns, int32_t nf, int32_t per_row, int32_t* ci, double* v) {
+  using namespace rb::crng;
+  const double label = r < ns / 2 ? 1.0 : -1.0;
+  const double sd = std::sqrt(1.0 / nf);
+  int32_t c[64], k[64];
+  for (int32_t q = 0; q < per_row; ++q)
+    c[q] = static_cast<int32_t>(below(uniform(seed, kSvmCol, r, q), static_cast<uint64_t>(nf))), k[q] = q;
+  for (int32_t q = 1; q < per_row; ++q)  // insertion sort by (column, draw)
+    for (int32_t p = q; p > 0 && (c[p - 1] > c[p] || (c[p - 1] == c[p] && k[p - 1] > k[p])); --p)
+      std::swap(c[p - 1], c[p]), std::swap(k[p - 1], k[p]);
+  auto val = [&](int32_t kk) { return label * (label / nf + sd * normal(seed, kSvmVal, r, kk)); };
+  int32_t w = 0;
+  for (int32_t q = 0; q < per_row;) {
+    double x = val(k[q]);
+    int32_t e = q + 1;
+    for (; e < per_row && c[e] == c[q]; ++e) x = x + val(k[e]);
+    if (x != 0.0) ci[w] = c[q], v[w] = x, ++w;
+    q = e;
+  }
+  ci[w] = nf + static_cast<int32_t>(r), v[w] = -1.0;
+  return w + 1;
+}
+
 void gen_svm(double scale, uint64_t seed, rapdhg_qp_owned* out) {
-  Rng g(seed);
   const int32_t ns = std::max<int32_t>(2, static_cast<int32_t>(std::lround(1000000 * scale)));
   const int32_t nf = std::max<int32_t>(2, static_cast<int32_t>(std::lround(10000 * scale)));
   const int32_t per_row = std::min<int32_t>(50, nf);
-  const int32_t n = nf + ns;
-  const double lam = 0.5;
-  const double sd = std::sqrt(1.0 / nf);
-  Triplets in(2 * ns, n);
-  in.reserve(static_cast<std::size_t>(ns) * (per_row + 2));
-  std::vector<int32_t> cols;
-  for (int32_t r = 0; r < ns; ++r) {
-    const double label = r < ns / 2 ? 1.0 : -1.0;
-    sample_cols(g, per_row, 0, nf, cols);
-    for (int32_t c : cols) in.add(r, c, label * (label / nf + sd * g.normal()));
-    in.add(r, nf + r, -1.0);
+  const int32_t n = nf + ns, m = 2 * ns, slot = per_row + 1;
+  rapdhg_csr_owned& a = out->a_ineq;
+  if (!(use_device_generator(ns >= 20000) && rb::gen_svm_a_device(ns, nf, per_row, seed, &a))) {
+  std::vector<int32_t> cnt(ns), tci(static_cast<std::size_t>(ns) * slot);
+  std::vector<double> tv(static_cast<std::size_t>(ns) * slot);
+  parallel_rows(ns, [&](int64_t r) {
+    cnt[r] = svm_row(seed, r, ns, nf, per_row, &tci[r * slot], &tv[r * slot]);
+  });
+  a.n_rows = m, a.n_cols = n;
+  a.row_ptr = xalloc<int32_t>(static_cast<std::size_t>(m) + 1);
+  a.row_ptr[0] = 0;
+  for (int32_t r = 0; r < ns; ++r) a.row_ptr[r + 1] = a.row_ptr[r] + cnt[r];
+  for (int32_t r = 0; r < ns; ++r) a.row_ptr[ns + r + 1] = a.row_ptr[ns + r] + 1;
+  a.nnz = a.row_ptr[m];
+  a.col_idx = xalloc<int32_t>(static_cast<std::size_t>(a.nnz));
+  a.values = xalloc<double>(static_cast<std::size_t>(a.nnz));
+  parallel_rows(ns, [&](int64_t r) {
+    std::memcpy(a.col_idx + a.row_ptr[r], &tci[r * slot], sizeof(int32_t) * cnt[r]);
+    std::memcpy(a.values + a.row_ptr[r], &tv[r * slot], sizeof(double) * cnt[r]);
+    a.col_idx[a.row_ptr[ns + r]] = nf + static_cast<int32_t>(r), a.values[a.row_ptr[ns + r]] = -1.0;
+  });
   }
-  for (int32_t r = 0; r < ns; ++r) in.add(ns + r, nf + r, -1.0);
   Triplets q(n, n);
   for (int32_t j = 0; j < nf; ++j) q.add(j, j, 2.0);
   std::vector<double> c(n, 0.0);
-  for (int32_t r = 0; r < ns; ++r) c[nf + r] = lam;
-  std::vector<double> b(2 * ns, 0.0);
+  for (int32_t r = 0; r < ns; ++r) c[nf + r] = 0.5;  // lambda
+  std::vector<double> b(m, 0.0);
   for (int32_t r = 0; r < ns; ++r) b[r] = -1.0;
   build_csr(q, &out->q);
-  build_csr(in, &out->a_ineq);
   empty_csr(0, n, &out->a_eq);
-  out->n = n, out->m_ineq = 2 * ns, out->m_eq = 0;
+  out->n = n, out->m_ineq = m, out->m_eq = 0;
   out->c = vec_copy(c);
   out->b_ineq = vec_copy(b);
   out->b_eq = vec_copy({});
@@ -523,13 +585,9 @@ int rapdhg_generate(int32_t kind, double scale, uint64_t seed, rapdhg_qp_owned* 
       case RAPDHG_GEN_SVM: gen_svm(scale, seed, out); break;
       case RAPDHG_GEN_LARGE:
       case RAPDHG_GEN_LARGE_LOCAL: {
-        // the device generator (gen_device.cu) makes the same arrays; it is
-        // used for large instances when a device is visible
-        // (RAPDHG_GEN_DEVICE=1 / 0 forces it on / off)
         const bool local = kind == RAPDHG_GEN_LARGE_LOCAL;
-        const char* e = std::getenv("RAPDHG_GEN_DEVICE");
-        const bool want = e ? e[0] == '1' : scale >= 0.02;
-        if (!(want && rb::gen_large_device(scale, seed, local, out))) gen_large(scale, seed, local, out);
+        if (!(use_device_generator(scale >= 0.02) && rb::gen_large_device(scale, seed, local, out)))
+          gen_large(scale, seed, local, out);
         break;
       }
       default: throw HostError(RAPDHG_E_INVALID_ARGUMENT, "unknown generator kind");

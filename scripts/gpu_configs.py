@@ -1,9 +1,11 @@
-# per-config throughput on one B200 (fast mode, 400-iteration resident solves, per-step in-loop stamps)
-export PYTHONUNBUFFERED=1
-timeout 1200 python - <<'PY' > gpurun_out/r02_01_configs.jsonl 2> gpurun_out/r02_01_configs.err
-import json, sys
+"""Per-config throughput on one B200 (fast mode, 400-iteration resident solves,
+in-loop step stamps): one JSON line per SURVEY §8(d) config."""
+import json
+import sys
+
 sys.path.insert(0, ".")
-import paper_2311_07710_b200 as rb
+import paper_2311_07710_b200 as rb  # noqa: E402
+
 for name, kind, scale, seed in (("C1 random QP", rb.Gen.RANDOM_QP, 1.0, 1), ("C2 lasso", rb.Gen.LASSO, 1.0, 2),
                                 ("C3 portfolio", rb.Gen.PORTFOLIO, 1.0, 3), ("C4 svm", rb.Gen.SVM, 1.0, 4),
                                 ("C5-U large", rb.Gen.LARGE, 1.0, 5), ("C5-L large local", rb.Gen.LARGE_LOCAL, 1.0, 5)):
@@ -20,5 +22,3 @@ for name, kind, scale, seed in (("C1 random QP", rb.Gen.RANDOM_QP, 1.0, 1), ("C2
                       "inloop_step_us": [None if k is None else 1e3 * k for k in ks],
                       "inloop_step_GBs": [None if k is None else b / (k * 1e-3) / 1e9 for k, b in zip(ks, (bd, bp))],
                       "setup_s": r.setup_seconds}), flush=True)
-PY
-cat gpurun_out/r02_01_configs.jsonl; tail -3 gpurun_out/r02_01_configs.err

@@ -1,11 +1,15 @@
-"""C5 generator (counter-based; csrc/host.cpp gen_large + csrc/gen_device.cu).
+"""Counter-based generators (csrc/crng.h): C5 (host.cpp gen_large +
+gen_device.cu) and C4 SVM (host.cpp gen_svm + gen_device.cu, restated in numpy
+by oracle/synth.py for the reference arm).
 CPU: the host reference yields valid, deterministic instances with a
-symmetric, diagonally dominant Q. GPU: the device generator's arrays are
-bit-identical to the host reference."""
+symmetric, diagonally dominant Q; the numpy SVM restatement equals the
+library's arrays. GPU: the device generators' arrays are bit-identical to the
+host reference."""
 import numpy as np
 import pytest
 
 import paper_2311_07710_b200 as rb
+from oracle import synth
 
 
 def arrays(p):
@@ -61,5 +65,37 @@ def test_device_generator_bit_identical(kind, scale, monkeypatch):
     d = rb.generate(kind, scale, 5)
     monkeypatch.setenv("RAPDHG_GEN_DEVICE", "0")
     h = rb.generate(kind, scale, 5)
+    for a, b in zip(arrays(d), arrays(h)):
+        assert a.shape == b.shape and np.array_equal(a, b)
+
+
+def svm_arrays(d):
+    return [*d["q"], *d["a_ineq"], d["c"], d["b_ineq"], d["a_eq"][0]]
+
+
+@pytest.mark.parametrize("scale,seed", [(0.001, 4), (0.004, 4), (0.004, 9)])
+def test_svm_numpy_restatement_bit_identical(scale, seed, monkeypatch):
+    monkeypatch.setenv("RAPDHG_GEN_DEVICE", "0")
+    p = rb.generate(rb.Gen.SVM, scale, seed)
+    d = synth.svm(scale, seed)
+    for a, b in zip(arrays(p), svm_arrays(d)):
+        assert a.shape == b.shape and np.array_equal(a, b)
+    ns = int(round(1e6 * scale))
+    nf = int(round(1e4 * scale))
+    a = p.a_ineq
+    assert a.n_rows == 2 * ns and p.num_vars() == nf + ns
+    lens = np.diff(a.row_ptr)
+    assert np.all(lens[ns:] == 1) and np.all(lens[:ns] <= 51) and lens[:ns].mean() > 0.6 * min(50, nf)
+    for r in range(0, 2 * ns, 97):  # canonical rows, the t entry last
+        seg = a.col_idx[a.row_ptr[r]:a.row_ptr[r + 1]]
+        assert np.all(np.diff(seg) > 0) and seg[-1] == nf + r % ns
+
+
+@pytest.mark.gpu
+def test_device_svm_generator_bit_identical(monkeypatch):
+    monkeypatch.setenv("RAPDHG_GEN_DEVICE", "1")
+    d = rb.generate(rb.Gen.SVM, 0.03, 4)
+    monkeypatch.setenv("RAPDHG_GEN_DEVICE", "0")
+    h = rb.generate(rb.Gen.SVM, 0.03, 4)
     for a, b in zip(arrays(d), arrays(h)):
         assert a.shape == b.shape and np.array_equal(a, b)

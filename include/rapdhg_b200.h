@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define RAPDHG_ABI_VERSION 1
+#define RAPDHG_ABI_VERSION 2
 
 /* ---- error codes (return values) ------------------------------------- */
 enum {
@@ -89,6 +89,8 @@ typedef struct {
   rapdhg_csr a_eq;   /* m_eq x n */
   const double* b_eq;
   double obj_offset;
+  const char* name;              /* QuadraticProgram::name; NULL = "" */
+  const char* const* var_names;  /* n entries (var_names), or NULL = none */
 } rapdhg_qp;
 
 /* ---- options ----------------------------------------------------------- */
@@ -297,7 +299,25 @@ int rapdhg_estimate_op_norm(const rapdhg_csr* m, int32_t max_iters, double tol, 
 int rapdhg_estimate_op_norm_symmetric(const rapdhg_csr* m, int32_t max_iters, double tol,
                                       uint64_t seed, double* out, int32_t strict);
 
+/* rapdhg::unscale_point (scaling.hpp:126-133): x *= d2, y *= d1 (ineq then
+ * eq), in place; and its inverse scale_point (scaling.hpp:136-143). Host,
+ * elementwise (the solver unscales its checks on the device). */
+int rapdhg_unscale_point(const double* d1, const double* d2, int32_t n, int32_t m_ineq, int32_t m_eq,
+                         double* x, double* y_ineq, double* y_eq);
+int rapdhg_scale_point(const double* d1, const double* d2, int32_t n, int32_t m_ineq, int32_t m_eq,
+                       double* x, double* y_ineq, double* y_eq);
+
+/* QuadraticProgram::validate (problem.hpp:40-50): dimensions, then the
+ * symmetry test gap <= 1e-12 * max(1, max|Q|) on the device. */
+int rapdhg_validate(const rapdhg_qp* qp);
+/* SparseMatrix::symmetry_gap (sparse.hpp:119-138): max |M_ij - M_ji| over
+ * both patterns, on the device (square matrices only). */
+int rapdhg_symmetry_gap(const rapdhg_csr* m, double* out);
+
 /* ---- host scalar rules (stepsize.hpp, solver.hpp:218-235) ------------- */
+/* primal_weight_init (stepsize.hpp:73-78): ||c||_2 / ||b||_2 when both
+ * exceed 1e-10, else 1 (sequential sums, as vec.hpp:20). */
+int rapdhg_primal_weight_init(const double* c, int64_t n, const double* b, int64_t m, double* out);
 int rapdhg_step_schedule_theoretical(int32_t k, int32_t horizon, double norm_q, double norm_a,
                                      rapdhg_step_params* out);
 int rapdhg_pdhg_constant_steps(double norm_q, double norm_a, rapdhg_step_params* out);
@@ -327,6 +347,8 @@ typedef struct {
   double* b_ineq;
   double* b_eq;
   double obj_offset;
+  char* name;        /* malloc'd, or NULL */
+  char** var_names;  /* n malloc'd strings, or NULL */
 } rapdhg_qp_owned;
 
 /* SparseMatrix(n_rows, n_cols, triplets) (sparse.hpp:31-62): sort by
@@ -338,6 +360,47 @@ void rapdhg_qp_free(rapdhg_qp_owned* p);
 /* Borrowed view of an owned QP, for passing to the compute entry points. */
 void rapdhg_qp_view(const rapdhg_qp_owned* p, rapdhg_qp* view);
 
+/* rapdhg::RowType (problem.hpp:72). */
+enum { RAPDHG_ROW_EQ = 0, RAPDHG_ROW_LE = 1, RAPDHG_ROW_GE = 2 };
+
+/* rapdhg::RawProblem (problem.hpp:76-92): typed rows, optional ranges and
+ * variable bounds, before conversion to the canonical <= / = form. q and a
+ * are canonical CSRs (as the reference's SparseMatrix members are). */
+typedef struct {
+  int32_t n;                 /* num_vars = len(c) */
+  int32_t m;                 /* num_rows = len(rhs) */
+  rapdhg_csr q;              /* n x n, full (mirrored) */
+  const double* c;           /* n */
+  double obj_offset;
+  rapdhg_csr a;              /* m x n, one row per constraint, original orientation */
+  const int32_t* row_types;  /* m: RAPDHG_ROW_* */
+  const double* rhs;         /* m */
+  const double* range;       /* m, NaN = no RANGES entry; NULL = none at all */
+  const double* lower;       /* n, -inf allowed */
+  const double* upper;       /* n, +inf allowed */
+  const char* name;          /* NULL = "" */
+  const char* const* row_names; /* m entries or NULL (labels use "r<i>") */
+  const char* const* var_names; /* n entries or NULL (labels use "x<j>") */
+} rapdhg_raw_problem;
+
+/* rapdhg::CanonicalMap (problem.hpp:95-99): provenance label of every
+ * canonical row ("row:<name>", "row:<name>:ub" / ":lb", "bound:<var>:ub" /
+ * ":lb"). Library-owned strings, released by rapdhg_canonical_map_free. */
+typedef struct {
+  int32_t n_ineq, n_eq;
+  char** ineq_labels;
+  char** eq_labels;
+} rapdhg_canonical_map;
+
+/* rapdhg::canonicalize (problem.hpp:131-198): G rows negated into <= rows,
+ * ranged rows split into two <= rows, rows whose interval is a point kept as
+ * equalities, finite variable bounds appended as singleton <= rows, then
+ * QuadraticProgram::validate (Q symmetric). Errors (std::invalid_argument in
+ * the reference) return RAPDHG_E_INVALID_ARGUMENT with the same messages.
+ * map may be NULL. Host-only. */
+int rapdhg_canonicalize(const rapdhg_raw_problem* raw, rapdhg_qp_owned* out, rapdhg_canonical_map* map);
+void rapdhg_canonical_map_free(rapdhg_canonical_map* map);
+
 /* QPS (MPS + QUADOBJ/QMATRIX) text or file -> canonical QP: parse_qps
  * (qps.hpp:69-298) then canonicalize (problem.hpp:131-198: G rows negated,
  * ranges split, finite bounds as singleton <= rows, E rows kept). Parse errors
@@ -345,6 +408,9 @@ void rapdhg_qp_view(const rapdhg_qp_owned* p, rapdhg_qp* view);
  * message. Host-only. */
 int rapdhg_parse_qps(const char* text, rapdhg_qp_owned* out);
 int rapdhg_parse_qps_file(const char* path, rapdhg_qp_owned* out);
+/* The same, also returning canonicalize's CanonicalMap (map may be NULL). */
+int rapdhg_parse_qps_map(const char* text, rapdhg_qp_owned* out, rapdhg_canonical_map* map);
+int rapdhg_parse_qps_file_map(const char* path, rapdhg_qp_owned* out, rapdhg_canonical_map* map);
 /* write_qps (qps.hpp:320-381): *out is malloc'd text, release with rapdhg_free. */
 int rapdhg_write_qps(const rapdhg_qp* qp, char** out);
 void rapdhg_free(void* p);

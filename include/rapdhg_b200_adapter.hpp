@@ -1,7 +1,8 @@
 // rapdhg_b200_adapter.hpp — reference-side binding (what a maintainer of the
 // reference C++ solver adds to switch `rapdhg::solve` to the B200 library).
 //
-// Include AFTER the reference headers. Converts the reference's
+// Include AFTER the reference headers. canonicalize() is the drop-in for
+// rapdhg::canonicalize (host-side, problem.hpp:131-198). Converts the reference's
 // QuadraticProgram / SolverConfig (problem.hpp:24-34, solver.hpp:38-55) into
 // the flat C-ABI structs of rapdhg_b200.h, calls rapdhg_solve(), and converts
 // the result back into rapdhg::SolveResult (solver.hpp:76-89), re-throwing the
@@ -79,10 +80,70 @@ inline rapdhg_config to_config(const rapdhg::SolverConfig& c, int device = 0, bo
   throw std::runtime_error(msg);
 }
 
+inline std::vector<const char*> c_strs(const std::vector<std::string>& v) {
+  std::vector<const char*> o;
+  for (const std::string& x : v) o.push_back(x.c_str());
+  return o;
+}
+
+inline rapdhg::SparseMatrix from_owned(const rapdhg_csr_owned& m) {
+  std::vector<rapdhg::Triplet> t;
+  for (int r = 0; r < m.n_rows; ++r)
+    for (int64_t k = m.row_ptr[r]; k < m.row_ptr[r + 1]; ++k) t.push_back({r, m.col_idx[k], m.values[k]});
+  return rapdhg::SparseMatrix(m.n_rows, m.n_cols, std::move(t));
+}
+
+// Drop-in for rapdhg::canonicalize (problem.hpp:131-198) through
+// rapdhg_canonicalize: RawProblem in, CanonicalProblem (qp + map) out.
+inline rapdhg::CanonicalProblem canonicalize(const rapdhg::RawProblem& raw) {
+  const CsrArrays q = to_csr(raw.q), a = to_csr(raw.a);
+  std::vector<int32_t> types;
+  for (rapdhg::RowType t : raw.row_types)
+    types.push_back(t == rapdhg::RowType::kEq ? RAPDHG_ROW_EQ : t == rapdhg::RowType::kLe ? RAPDHG_ROW_LE
+                                                                                          : RAPDHG_ROW_GE);
+  const std::vector<const char*> rn = c_strs(raw.row_names), vn = c_strs(raw.var_names);
+  rapdhg_raw_problem r{};
+  r.n = raw.num_vars();
+  r.m = raw.num_rows();
+  r.q = q.view(raw.q.rows(), raw.q.cols());
+  r.c = raw.c.data();
+  r.obj_offset = raw.obj_offset;
+  r.a = a.view(raw.a.rows(), raw.a.cols());
+  r.row_types = types.data();
+  r.rhs = raw.rhs.data();
+  r.range = raw.range.empty() ? nullptr : raw.range.data();
+  r.lower = raw.lower.data();
+  r.upper = raw.upper.data();
+  r.name = raw.name.c_str();
+  r.row_names = rn.size() == raw.row_names.size() && !rn.empty() ? rn.data() : nullptr;
+  r.var_names = vn.size() == raw.var_names.size() && !vn.empty() ? vn.data() : nullptr;
+  rapdhg_qp_owned o{};
+  rapdhg_canonical_map mp{};
+  const int rc = rapdhg_canonicalize(&r, &o, &mp);
+  if (rc != RAPDHG_OK) rethrow(rc);
+  rapdhg::CanonicalProblem out;
+  out.qp.q = from_owned(o.q);
+  out.qp.a_ineq = from_owned(o.a_ineq);
+  out.qp.a_eq = from_owned(o.a_eq);
+  out.qp.c.assign(o.c, o.c + o.n);
+  out.qp.b_ineq.assign(o.b_ineq, o.b_ineq + o.m_ineq);
+  out.qp.b_eq.assign(o.b_eq, o.b_eq + o.m_eq);
+  out.qp.obj_offset = o.obj_offset;
+  if (o.name) out.qp.name = o.name;
+  if (o.var_names)
+    for (int j = 0; j < o.n; ++j) out.qp.var_names.emplace_back(o.var_names[j]);
+  for (int i = 0; i < mp.n_ineq; ++i) out.map.ineq_labels.emplace_back(mp.ineq_labels[i]);
+  for (int i = 0; i < mp.n_eq; ++i) out.map.eq_labels.emplace_back(mp.eq_labels[i]);
+  rapdhg_qp_free(&o);
+  rapdhg_canonical_map_free(&mp);
+  return out;
+}
+
 // Drop-in for rapdhg::solve (solver.hpp:272).
 inline rapdhg::SolveResult solve(const rapdhg::QuadraticProgram& p, const rapdhg::SolverConfig& cfg,
                                  int device = 0, bool strict_parity = false) {
   const CsrArrays q = to_csr(p.q), ai = to_csr(p.a_ineq), ae = to_csr(p.a_eq);
+  const std::vector<const char*> vn = c_strs(p.var_names);
   rapdhg_qp qp{};
   qp.n = p.num_vars();
   qp.m_ineq = p.num_ineq();
@@ -94,6 +155,8 @@ inline rapdhg::SolveResult solve(const rapdhg::QuadraticProgram& p, const rapdhg
   qp.b_ineq = p.b_ineq.data();
   qp.b_eq = p.b_eq.data();
   qp.obj_offset = p.obj_offset;
+  qp.name = p.name.c_str();
+  qp.var_names = vn.size() == static_cast<std::size_t>(p.num_vars()) && !vn.empty() ? vn.data() : nullptr;
   const rapdhg_config c = to_config(cfg, device, strict_parity);
   rapdhg_result r{};
   const int rc = rapdhg_solve(&qp, &c, &r);

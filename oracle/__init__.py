@@ -78,6 +78,9 @@ class CpuSolver:
             d("apply_scaling", C.c_int, P(abi.Qp), abi.P_f64, abi.P_f64, abi.P_f64, abi.P_f64,
               abi.P_f64, abi.P_f64, abi.P_f64, abi.P_f64, abi.P_i64)
             d("parse_qps_canonical", C.c_int, C.c_char_p, P(abi.QpOwned))
+            d("parse_qps_map", C.c_int, C.c_char_p, P(abi.QpOwned), P(abi.CanonicalMap))
+            d("canonicalize", C.c_int, P(abi.RawProblem), P(abi.QpOwned), P(abi.CanonicalMap))
+            d("canonical_map_free", None, P(abi.CanonicalMap))
             d("qp_free", None, P(abi.QpOwned))
             d("write_qps", C.c_int, P(abi.Qp), P(C.c_void_p))
             d("free", None, C.c_void_p)
@@ -234,6 +237,33 @@ class CpuSolver:
             return rb.qp_from_owned(o)
         finally:
             self._fn("qp_free")(C.byref(o))
+
+    def _canonical(self, call):
+        o, mp = abi.QpOwned(), abi.CanonicalMap()
+        self._check(call(o, mp))
+        try:
+            return rb.qp_from_owned(o), rb._map_from(mp)
+        finally:
+            self._fn("qp_free")(C.byref(o))
+            self._fn("canonical_map_free")(C.byref(mp))
+
+    def parse_qps_with_map(self, text: str):
+        """parse_qps + canonicalize -> (qp, CanonicalMap) (reference build only)."""
+        return self._canonical(lambda o, mp: self._fn("parse_qps_map")(text.encode(), C.byref(o), C.byref(mp)))
+
+    def canonicalize(self, raw: rb.RawProblem):
+        """problem.hpp canonicalize of a RawProblem (reference build only)."""
+        n, m = raw.num_vars(), raw.num_rows()
+        c, rhs, lo, up = _f64(raw.c), _f64(raw.rhs), _f64(raw.lower), _f64(raw.upper)
+        rng = _f64(raw.range) if raw.range is not None else None
+        rt = np.ascontiguousarray(raw.row_types, dtype=np.int32)
+        rn, vn = rb._names(raw.row_names), rb._names(raw.var_names)
+        st = abi.RawProblem(n, m, raw.q._csr(), _pf(c), float(raw.obj_offset), raw.a._csr(),
+                            rt.ctypes.data_as(abi.P_i32), _pf(rhs), _pf(rng) if rng is not None else None,
+                            _pf(lo), _pf(up), raw.name.encode(),
+                            C.cast(rn, C.POINTER(C.c_char_p)) if rn is not None else None,
+                            C.cast(vn, C.POINTER(C.c_char_p)) if vn is not None else None)
+        return self._canonical(lambda o, mp: self._fn("canonicalize")(C.byref(st), C.byref(o), C.byref(mp)))
 
 
 _cache = {}

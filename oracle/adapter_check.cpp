@@ -6,6 +6,7 @@
 // Exit code 0 = pass. Built by oracle/Makefile into _ref/adapter_check.
 #include <cmath>
 #include <cstdio>
+#include <algorithm>
 #include <random>
 
 #include "rapdhg/solver.hpp"
@@ -48,8 +49,54 @@ static QuadraticProgram random_qp(unsigned seed, int n, int mi, int me) {
   return p;
 }
 
+// rapdhg::canonicalize vs rapdhg_b200::canonicalize on typed rows, ranges
+// and bounds: identical canonical problems and labels (host only).
+static int check_canonicalize() {
+  std::mt19937_64 g(7);
+  std::normal_distribution<double> N(0.0, 1.0);
+  std::uniform_real_distribution<double> U(0.0, 1.0);
+  const int n = 9, m = 7;
+  RawProblem raw;
+  raw.name = "adapter";
+  std::vector<Triplet> at, qt;
+  for (int r = 0; r < m; ++r)
+    for (int c = 0; c < n; ++c)
+      if (U(g) < 0.4) at.push_back({r, c, N(g)});
+  for (int i = 0; i < n; ++i) qt.push_back({i, i, 1.0 + U(g)});
+  raw.q = SparseMatrix(n, n, qt);
+  raw.a = SparseMatrix(m, n, at);
+  for (int j = 0; j < n; ++j) {
+    raw.c.push_back(N(g));
+    raw.lower.push_back(U(g) < 0.3 ? -kInf : -U(g));
+    raw.upper.push_back(U(g) < 0.3 ? kInf : U(g));
+    raw.var_names.push_back("v" + std::to_string(j));
+  }
+  for (int i = 0; i < m; ++i) {
+    raw.row_types.push_back(static_cast<RowType>(i % 3));
+    raw.rhs.push_back(N(g));
+    raw.range.push_back(U(g) < 0.5 ? std::nan("") : 2 * N(g));
+    raw.row_names.push_back("row" + std::to_string(i));
+  }
+  const CanonicalProblem a = canonicalize(raw);
+  const CanonicalProblem b = rapdhg_b200::canonicalize(raw);
+  auto same_m = [](const SparseMatrix& x, const SparseMatrix& y) {
+    const std::vector<Triplet> tx = x.triplets(), ty = y.triplets();
+    return x.rows() == y.rows() && x.cols() == y.cols() && tx.size() == ty.size() &&
+           std::equal(tx.begin(), tx.end(), ty.begin(), [](const Triplet& p, const Triplet& q) {
+             return p.row == q.row && p.col == q.col && p.value == q.value;
+           });
+  };
+  const bool same = same_m(a.qp.q, b.qp.q) && same_m(a.qp.a_ineq, b.qp.a_ineq) && same_m(a.qp.a_eq, b.qp.a_eq) &&
+                    a.qp.c == b.qp.c && a.qp.b_ineq == b.qp.b_ineq && a.qp.b_eq == b.qp.b_eq &&
+                    a.qp.name == b.qp.name && a.qp.var_names == b.qp.var_names &&
+                    a.map.ineq_labels == b.map.ineq_labels && a.map.eq_labels == b.map.eq_labels;
+  std::printf("canonicalize: %s (%d ineq, %d eq rows)\n", same ? "identical" : "DIFFERENT", a.qp.num_ineq(),
+              a.qp.num_eq());
+  return same ? 0 : 1;
+}
+
 int main() {
-  int fails = 0;
+  int fails = check_canonicalize();
   for (unsigned seed : {1u, 2u, 3u}) {
     const QuadraticProgram p = random_qp(seed, 50, 25, 6);
     SolverConfig cfg;

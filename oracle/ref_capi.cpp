@@ -73,7 +73,22 @@ QuadraticProgram to_qp(const rapdhg_qp* p) {
   qp.a_eq = to_sparse(p->a_eq);
   qp.b_eq = to_vec(p->b_eq, p->m_eq);
   qp.obj_offset = p->obj_offset;
+  if (p->name) qp.name = p->name;
+  if (p->var_names)
+    for (int j = 0; j < p->n; ++j) qp.var_names.emplace_back(p->var_names[j] ? p->var_names[j] : "");
   return qp;
+}
+
+char* dup_str(const std::string& v) {
+  char* p = static_cast<char*>(std::malloc(v.size() + 1));
+  std::memcpy(p, v.c_str(), v.size() + 1);
+  return p;
+}
+
+char** dup_strs(const std::vector<std::string>& v) {
+  char** p = static_cast<char**>(std::calloc(v.size() ? v.size() : 1, sizeof(char*)));
+  for (std::size_t i = 0; i < v.size(); ++i) p[i] = dup_str(v[i]);
+  return p;
 }
 
 SolverConfig to_cfg(const rapdhg_config* c) {
@@ -373,6 +388,69 @@ int ref_csr_from_triplets(int32_t n_rows, int32_t n_cols, int64_t nnz, const int
   });
 }
 
+void fill_canonical(const CanonicalProblem& cp, rapdhg_qp_owned* out, rapdhg_canonical_map* map) {
+  const QuadraticProgram& qp = cp.qp;
+  std::memset(out, 0, sizeof(*out));
+  out->n = qp.num_vars();
+  out->m_ineq = qp.num_ineq();
+  out->m_eq = qp.num_eq();
+  fill_csr(qp.q, &out->q);
+  fill_csr(qp.a_ineq, &out->a_ineq);
+  fill_csr(qp.a_eq, &out->a_eq);
+  out->c = dup(qp.c.data(), qp.c.size());
+  out->b_ineq = dup(qp.b_ineq.data(), qp.b_ineq.size());
+  out->b_eq = dup(qp.b_eq.data(), qp.b_eq.size());
+  out->obj_offset = qp.obj_offset;
+  out->name = dup_str(qp.name);
+  if (!qp.var_names.empty()) out->var_names = dup_strs(qp.var_names);
+  if (map) {
+    map->n_ineq = static_cast<int32_t>(cp.map.ineq_labels.size());
+    map->n_eq = static_cast<int32_t>(cp.map.eq_labels.size());
+    map->ineq_labels = dup_strs(cp.map.ineq_labels);
+    map->eq_labels = dup_strs(cp.map.eq_labels);
+  }
+}
+
+// RawProblem (problem.hpp:76-92) from its C view, then canonicalize
+// (problem.hpp:131-198) itself.
+int ref_canonicalize(const rapdhg_raw_problem* r, rapdhg_qp_owned* out, rapdhg_canonical_map* map) {
+  return guard([&] {
+    RawProblem raw;
+    if (r->name) raw.name = r->name;
+    raw.q = to_sparse(r->q);
+    raw.c = to_vec(r->c, r->n);
+    raw.obj_offset = r->obj_offset;
+    raw.a = to_sparse(r->a);
+    for (int i = 0; i < r->m; ++i)
+      raw.row_types.push_back(r->row_types[i] == RAPDHG_ROW_EQ ? RowType::kEq
+                              : r->row_types[i] == RAPDHG_ROW_LE ? RowType::kLe : RowType::kGe);
+    raw.rhs = to_vec(r->rhs, r->m);
+    raw.range = r->range ? to_vec(r->range, r->m) : Vec(r->m, std::nan(""));
+    raw.lower = to_vec(r->lower, r->n);
+    raw.upper = to_vec(r->upper, r->n);
+    if (r->row_names)
+      for (int i = 0; i < r->m; ++i) raw.row_names.emplace_back(r->row_names[i]);
+    if (r->var_names)
+      for (int j = 0; j < r->n; ++j) raw.var_names.emplace_back(r->var_names[j]);
+    fill_canonical(canonicalize(raw), out, map);
+  });
+}
+
+int ref_parse_qps_map(const char* text, rapdhg_qp_owned* out, rapdhg_canonical_map* map) {
+  return guard([&] {
+    std::istringstream in{std::string(text)};
+    fill_canonical(canonicalize(parse_qps(in)), out, map);
+  });
+}
+
+void ref_canonical_map_free(rapdhg_canonical_map* map) {
+  for (int i = 0; i < map->n_ineq; ++i) std::free(map->ineq_labels[i]);
+  for (int i = 0; i < map->n_eq; ++i) std::free(map->eq_labels[i]);
+  std::free(map->ineq_labels);
+  std::free(map->eq_labels);
+  std::memset(map, 0, sizeof(*map));
+}
+
 // QPS text -> canonical QP (qps.hpp:69-298 then problem.hpp:131-198).
 int ref_parse_qps_canonical(const char* text, rapdhg_qp_owned* out) {
   return guard([&] {
@@ -421,6 +499,10 @@ void ref_qp_free(rapdhg_qp_owned* p) {
   std::free(p->c);
   std::free(p->b_ineq);
   std::free(p->b_eq);
+  std::free(p->name);
+  if (p->var_names)
+    for (int j = 0; j < p->n; ++j) std::free(p->var_names[j]);
+  std::free(p->var_names);
   std::memset(p, 0, sizeof(*p));
 }
 

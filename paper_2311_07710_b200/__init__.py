@@ -119,7 +119,18 @@ def _load():
     d(lib, "rapdhg_shard_session_create", C.c_int, P(abi.Qp), P(abi.Config), P(abi.ShardOpts), P(C.c_void_p))
     d(lib, "rapdhg_shard_session_solve", C.c_int, C.c_void_p, P(abi.Result))
     d(lib, "rapdhg_shard_session_destroy", None, C.c_void_p)
-    if lib.rapdhg_abi_version() != 1:
+    d(lib, "rapdhg_canonicalize", C.c_int, P(abi.RawProblem), P(abi.QpOwned), P(abi.CanonicalMap))
+    d(lib, "rapdhg_canonical_map_free", None, P(abi.CanonicalMap))
+    d(lib, "rapdhg_parse_qps_map", C.c_int, C.c_char_p, P(abi.QpOwned), P(abi.CanonicalMap))
+    d(lib, "rapdhg_parse_qps_file_map", C.c_int, C.c_char_p, P(abi.QpOwned), P(abi.CanonicalMap))
+    d(lib, "rapdhg_unscale_point", C.c_int, abi.P_f64, abi.P_f64, C.c_int32, C.c_int32, C.c_int32,
+      abi.P_f64, abi.P_f64, abi.P_f64)
+    d(lib, "rapdhg_scale_point", C.c_int, abi.P_f64, abi.P_f64, C.c_int32, C.c_int32, C.c_int32,
+      abi.P_f64, abi.P_f64, abi.P_f64)
+    d(lib, "rapdhg_validate", C.c_int, P(abi.Qp))
+    d(lib, "rapdhg_symmetry_gap", C.c_int, P(abi.Csr), abi.P_f64)
+    d(lib, "rapdhg_primal_weight_init", C.c_int, abi.P_f64, C.c_int64, abi.P_f64, C.c_int64, abi.P_f64)
+    if lib.rapdhg_abi_version() != abi.ABI_VERSION:
         raise ImportError("librapdhg_b200.so ABI version mismatch")
     _lib = lib
     return lib
@@ -302,11 +313,23 @@ class QuadraticProgram:
         qx = np.bincount(rows, weights=q.values * x[q.col_idx], minlength=q.n_rows)
         return 0.5 * float(x @ qx) + float(self.c @ x) + self.obj_offset
 
+    def validate(self) -> None:
+        """QuadraticProgram::validate (problem.hpp:40-50) on the GPU: raises
+        InvalidArgument with the reference's messages."""
+        qp = self._struct()
+        _check(_load().rapdhg_validate(C.byref(qp)))
+
     def _struct(self) -> abi.Qp:
         self.c, self.b_ineq, self.b_eq = _f64(self.c), _f64(self.b_ineq), _f64(self.b_eq)
-        return abi.Qp(len(self.c), len(self.b_ineq), len(self.b_eq), self.q._csr(), _pf(self.c),
-                      self.a_ineq._csr(), _pf(self.b_ineq), self.a_eq._csr(), _pf(self.b_eq),
-                      float(self.obj_offset))
+        names = None
+        if self.var_names:  # kept alive with the struct (it refers to them)
+            names = (C.c_char_p * len(self.var_names))(*[v.encode() for v in self.var_names])
+        s = abi.Qp(len(self.c), len(self.b_ineq), len(self.b_eq), self.q._csr(), _pf(self.c),
+                   self.a_ineq._csr(), _pf(self.b_ineq), self.a_eq._csr(), _pf(self.b_eq),
+                   float(self.obj_offset), (self.name or "").encode(),
+                   C.cast(names, C.POINTER(C.c_char_p)) if names is not None else None)
+        s._keep = names
+        return s
 
 
 @dataclass
@@ -697,16 +720,31 @@ def apply_scaling(p: QuadraticProgram, s: ScalingInfo) -> QuadraticProgram:
                             p.obj_offset, list(p.var_names))
 
 
+def _point_op(fn, z: PrimalDualPoint, s: ScalingInfo) -> PrimalDualPoint:
+    o = PrimalDualPoint(_f64(z.x).copy(), _f64(z.y_ineq).copy(), _f64(z.y_eq).copy())
+    d1, d2 = _f64(s.d1), _f64(s.d2)
+    if len(d2) != len(o.x) or len(d1) != len(o.y_ineq) + len(o.y_eq):
+        raise InvalidArgument("scaling factors do not match the point")
+    _check(fn(_pf(d1), _pf(d2), len(o.x), len(o.y_ineq), len(o.y_eq), _pf(o.x), _pf(o.y_ineq), _pf(o.y_eq)))
+    return o
+
+
 def unscale_point(z: PrimalDualPoint, s: ScalingInfo) -> PrimalDualPoint:
-    """scaling.hpp:126-133 (host; elementwise products)."""
-    mi = len(z.y_ineq)
-    return PrimalDualPoint(_f64(z.x) * s.d2, _f64(z.y_ineq) * s.d1[:mi], _f64(z.y_eq) * s.d1[mi:])
+    """unscale_point (scaling.hpp:126-133): x = D2 x~, y = D1 y~ (C-ABI, host)."""
+    return _point_op(_load().rapdhg_unscale_point, z, s)
 
 
 def scale_point(z: PrimalDualPoint, s: ScalingInfo) -> PrimalDualPoint:
-    """scaling.hpp:136-143 (host)."""
-    mi = len(z.y_ineq)
-    return PrimalDualPoint(_f64(z.x) / s.d2, _f64(z.y_ineq) / s.d1[:mi], _f64(z.y_eq) / s.d1[mi:])
+    """scale_point (scaling.hpp:136-143), the inverse (C-ABI, host)."""
+    return _point_op(_load().rapdhg_scale_point, z, s)
+
+
+def symmetry_gap(m: "SparseMatrix") -> float:
+    """SparseMatrix::symmetry_gap (sparse.hpp:119-138) on the GPU."""
+    out = C.c_double()
+    cm = m._csr()
+    _check(_load().rapdhg_symmetry_gap(C.byref(cm), C.byref(out)))
+    return out.value
 
 
 @dataclass
@@ -758,9 +796,11 @@ def adaptive_eta(k: int, prev_eta: float, norm_q: float, norm_a: float, omega: f
 
 
 def primal_weight_init(c, b) -> float:
-    """stepsize.hpp:73-78 (host norms)."""
-    nc, nb = math.sqrt(sum(v * v for v in c)), math.sqrt(sum(v * v for v in b))
-    return nc / nb if (nc > 1e-10 and nb > 1e-10) else 1.0
+    """stepsize.hpp:73-78 (C-ABI, host norms in sequential order)."""
+    c, b = _f64(c), _f64(b)
+    out = C.c_double()
+    _check(_load().rapdhg_primal_weight_init(_pf(c), len(c), _pf(b), len(b), C.byref(out)))
+    return out.value
 
 
 def primal_weight_update(delta_x: float, delta_y: float, omega_prev: float) -> float:
@@ -799,13 +839,98 @@ def parse_qps(text: str) -> QuadraticProgram:
         L.rapdhg_qp_free(C.byref(o))
 
 
+class RowType(enum.IntEnum):
+    """problem.hpp:72"""
+    kEq = 0
+    kLe = 1
+    kGe = 2
+
+
+@dataclass
+class RawProblem:
+    """problem.hpp:76-92: typed rows, optional ranges (NaN = none) and variable
+    bounds (+-inf allowed), before canonicalize."""
+    q: SparseMatrix
+    c: np.ndarray
+    a: SparseMatrix
+    row_types: Sequence[int]
+    rhs: np.ndarray
+    lower: np.ndarray
+    upper: np.ndarray
+    range: Optional[np.ndarray] = None
+    obj_offset: float = 0.0
+    name: str = ""
+    row_names: List[str] = field(default_factory=list)
+    var_names: List[str] = field(default_factory=list)
+
+    def num_vars(self) -> int:
+        return len(self.c)
+
+    def num_rows(self) -> int:
+        return len(self.rhs)
+
+
+@dataclass
+class CanonicalMap:
+    """problem.hpp:95-99"""
+    ineq_labels: List[str]
+    eq_labels: List[str]
+
+
+def _names(v):
+    return (C.c_char_p * len(v))(*[x.encode() for x in v]) if v else None
+
+
+def _map_from(m: abi.CanonicalMap) -> CanonicalMap:
+    return CanonicalMap([m.ineq_labels[i].decode() for i in range(m.n_ineq)],
+                        [m.eq_labels[i].decode() for i in range(m.n_eq)])
+
+
+def canonicalize(raw: RawProblem) -> Tuple[QuadraticProgram, CanonicalMap]:
+    """canonicalize (problem.hpp:131-198) through the C-ABI (host): returns
+    CanonicalProblem{qp, map} as a pair."""
+    L = _load()
+    n, m = raw.num_vars(), raw.num_rows()
+    c, rhs = _f64(raw.c), _f64(raw.rhs)
+    lo, up = _f64(raw.lower), _f64(raw.upper)
+    rng = _f64(raw.range) if raw.range is not None else None
+    rt = _i32(raw.row_types)
+    if len(rt) != m or len(lo) != n or len(up) != n or (rng is not None and len(rng) != m):
+        raise InvalidArgument("RawProblem: array lengths do not match num_vars / num_rows")
+    rn, vn = _names(raw.row_names), _names(raw.var_names)
+    st = abi.RawProblem(n, m, raw.q._csr(), _pf(c), float(raw.obj_offset), raw.a._csr(),
+                        rt.ctypes.data_as(abi.P_i32), _pf(rhs), _pf(rng) if rng is not None else None,
+                        _pf(lo), _pf(up), raw.name.encode(),
+                        C.cast(rn, C.POINTER(C.c_char_p)) if rn is not None else None,
+                        C.cast(vn, C.POINTER(C.c_char_p)) if vn is not None else None)
+    o, mp = abi.QpOwned(), abi.CanonicalMap()
+    _check(L.rapdhg_canonicalize(C.byref(st), C.byref(o), C.byref(mp)))
+    try:
+        return qp_from_owned(o), _map_from(mp)
+    finally:
+        L.rapdhg_qp_free(C.byref(o))
+        L.rapdhg_canonical_map_free(C.byref(mp))
+
+
+def parse_qps_with_map(text: str) -> Tuple[QuadraticProgram, CanonicalMap]:
+    """parse_qps + canonicalize, returning the CanonicalMap too."""
+    L = _load()
+    o, mp = abi.QpOwned(), abi.CanonicalMap()
+    _check(L.rapdhg_parse_qps_map(text.encode(), C.byref(o), C.byref(mp)))
+    try:
+        return qp_from_owned(o), _map_from(mp)
+    finally:
+        L.rapdhg_qp_free(C.byref(o))
+        L.rapdhg_canonical_map_free(C.byref(mp))
+
+
 def read_qps(path: str) -> QuadraticProgram:
     """parse_qps_file (qps.hpp:300) + canonicalize."""
     L = _load()
     o = abi.QpOwned()
     _check(L.rapdhg_parse_qps_file(os.fsencode(path), C.byref(o)))
     try:
-        return qp_from_owned(o, os.path.basename(path))
+        return qp_from_owned(o)
     finally:
         L.rapdhg_qp_free(C.byref(o))
 
@@ -840,8 +965,11 @@ def qp_from_owned(o: abi.QpOwned, name: str = "") -> QuadraticProgram:
         ci = np.ctypeslib.as_array(m.col_idx, (nnz,)).copy() if nnz else np.zeros(0, np.int32)
         v = np.ctypeslib.as_array(m.values, (nnz,)).copy() if nnz else np.zeros(0)
         return SparseMatrix.from_csr(m.n_rows, m.n_cols, rp, ci, v)
+    if o.name:
+        name = o.name.decode()
+    var_names = [o.var_names[j].decode() for j in range(o.n)] if o.var_names else []
     return QuadraticProgram(csr(o.q), _arr(o.c, o.n), csr(o.a_ineq), _arr(o.b_ineq, o.m_ineq),
-                            csr(o.a_eq), _arr(o.b_eq, o.m_eq), name, o.obj_offset)
+                            csr(o.a_eq), _arr(o.b_eq, o.m_eq), name, o.obj_offset, var_names)
 
 
 def generate(kind: Gen, scale: float = 1.0, seed: int = 1) -> QuadraticProgram:
@@ -863,6 +991,7 @@ __all__ = [
     "ruiz_scaling", "apply_scaling", "unscale_point", "scale_point", "estimate_op_norm",
     "estimate_op_norm_symmetric", "step_schedule_theoretical", "pdhg_constant_steps",
     "adaptive_eta", "primal_weight_init", "primal_weight_update", "restart_decision", "generate",
+    "RowType", "RawProblem", "CanonicalMap", "canonicalize", "parse_qps_with_map", "symmetry_gap",
     "spmv", "spmv_t", "to_string", "parse_qps", "read_qps", "write_qps", "device_count", "lib", "InvalidArgument", "NoDeviceError",
     "CudaError", "QpsParseError",
 ]

@@ -16,6 +16,7 @@ E_CUDA = -3
 E_NO_DEVICE = -4
 E_PARSE = -5
 E_INTERNAL = -6
+ABI_VERSION = 2
 
 
 class Csr(C.Structure):
@@ -26,7 +27,20 @@ class Csr(C.Structure):
 class Qp(C.Structure):
     _fields_ = [("n", i32), ("m_ineq", i32), ("m_eq", i32),
                 ("q", Csr), ("c", P_f64), ("a_ineq", Csr), ("b_ineq", P_f64),
-                ("a_eq", Csr), ("b_eq", P_f64), ("obj_offset", f64)]
+                ("a_eq", Csr), ("b_eq", P_f64), ("obj_offset", f64),
+                ("name", C.c_char_p), ("var_names", C.POINTER(C.c_char_p))]
+
+
+class RawProblem(C.Structure):
+    _fields_ = [("n", i32), ("m", i32), ("q", Csr), ("c", P_f64), ("obj_offset", f64),
+                ("a", Csr), ("row_types", P_i32), ("rhs", P_f64), ("range", P_f64),
+                ("lower", P_f64), ("upper", P_f64), ("name", C.c_char_p),
+                ("row_names", C.POINTER(C.c_char_p)), ("var_names", C.POINTER(C.c_char_p))]
+
+
+class CanonicalMap(C.Structure):
+    _fields_ = [("n_ineq", i32), ("n_eq", i32), ("ineq_labels", C.POINTER(C.c_char_p)),
+                ("eq_labels", C.POINTER(C.c_char_p))]
 
 
 class Config(C.Structure):
@@ -82,7 +96,7 @@ class QpOwned(C.Structure):
     _fields_ = [("n", i32), ("m_ineq", i32), ("m_eq", i32),
                 ("q", CsrOwned), ("a_ineq", CsrOwned), ("a_eq", CsrOwned),
                 ("c", P_f64), ("b_ineq", P_f64), ("b_eq", P_f64),
-                ("obj_offset", f64)]
+                ("obj_offset", f64), ("name", C.c_char_p), ("var_names", C.POINTER(C.c_char_p))]
 
 
 class ShardOpts(C.Structure):

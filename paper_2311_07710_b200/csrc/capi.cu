@@ -254,6 +254,23 @@ int rapdhg_session_bytes(const rapdhg_session* s, double* b_iter, double* b_dual
 
 void rapdhg_session_destroy(rapdhg_session* s) { delete s; }
 
+int rapdhg_validate(const rapdhg_qp* qp) {
+  return guard([&] {
+    null_check(qp, "qp");
+    require_device();
+    rb::api_validate(*qp);
+  });
+}
+
+int rapdhg_symmetry_gap(const rapdhg_csr* m, double* out) {
+  return guard([&] {
+    null_check(m, "m");
+    null_check(out, "out");
+    require_device();
+    *out = rb::api_symmetry_gap(*m);
+  });
+}
+
 int rapdhg_spmv(const rapdhg_csr* m, const double* x, int64_t x_len, double* y, int32_t strict) {
   return guard([&] {
     null_check(m, "m");

@@ -1151,6 +1151,34 @@ rapdhg_qp single_matrix_qp(const rapdhg_csr& m, std::vector<int32_t>& zero_rp) {
 }
 }  // namespace
 
+void api_validate(const rapdhg_qp& p) {
+  DeviceQP::validate_dims(p);  // problem.hpp:41-46
+  StreamGuard sg;
+  DeviceQP P(p, false, sg.s);
+  P.validate_symmetry();  // problem.hpp:47-49
+}
+
+double api_symmetry_gap(const rapdhg_csr& mat) {
+  if (mat.n_rows != mat.n_cols) invalid("symmetry_gap: matrix must be square");
+  const int n = mat.n_rows;
+  std::vector<int32_t> zrp(static_cast<std::size_t>(n) + 1, 0);
+  std::vector<double> zeros(static_cast<std::size_t>(n) + 1, 0.0);
+  rapdhg_qp p{};
+  p.n = n;
+  p.q = mat;
+  p.a_ineq = rapdhg_csr{0, n, 0, zrp.data(), nullptr, nullptr};
+  p.a_eq = rapdhg_csr{0, n, 0, zrp.data(), nullptr, nullptr};
+  p.c = zeros.data(), p.b_ineq = zeros.data(), p.b_eq = zeros.data();
+  DeviceQP::validate_dims(p);
+  StreamGuard sg;
+  DeviceQP P(p, false, sg.s);
+  DevCsr qt;
+  transpose_csr(qt, P.Q, nullptr, sg.s);
+  double gap = 0.0, mabs = 0.0;
+  symmetry_gap(P.Q, qt, &gap, &mabs, sg.s);
+  return gap;
+}
+
 void api_spmv(const rapdhg_csr& mat, const double* x, double* y, bool transpose, bool strict) {
   std::vector<int32_t> zrp;
   rapdhg_qp p = single_matrix_qp(mat, zrp);

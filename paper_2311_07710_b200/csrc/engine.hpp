@@ -226,6 +226,8 @@ class Engine : public LoopBackend {
 };
 
 // ---- secondary API helpers (host buffers in/out) ----------------------------
+void api_validate(const rapdhg_qp& p);              // problem.hpp:40-50
+double api_symmetry_gap(const rapdhg_csr& m);        // sparse.hpp:119-138
 void api_spmv(const rapdhg_csr& m, const double* x, double* y, bool transpose, bool strict);
 void api_rel_kkt(const rapdhg_qp& p, const double* x, const double* yi, const double* ye,
                  bool strict, Kkt* out);

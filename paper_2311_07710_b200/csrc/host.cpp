@@ -560,6 +560,10 @@ void rapdhg_qp_free(rapdhg_qp_owned* p) {
   std::free(p->c);
   std::free(p->b_ineq);
   std::free(p->b_eq);
+  std::free(p->name);
+  if (p->var_names)
+    for (int32_t j = 0; j < p->n; ++j) std::free(p->var_names[j]);
+  std::free(p->var_names);
   std::memset(p, 0, sizeof(*p));
 }
 
@@ -571,6 +575,43 @@ void rapdhg_qp_view(const rapdhg_qp_owned* p, rapdhg_qp* v) {
   v->q = cv(p->q), v->a_ineq = cv(p->a_ineq), v->a_eq = cv(p->a_eq);
   v->c = p->c, v->b_ineq = p->b_ineq, v->b_eq = p->b_eq;
   v->obj_offset = p->obj_offset;
+  v->name = p->name;
+  v->var_names = p->var_names;
+}
+
+// unscale_point / scale_point (scaling.hpp:126-143): x = D2 x~, y = D1 y~
+// and the inverse, elementwise in place.
+int rapdhg_unscale_point(const double* d1, const double* d2, int32_t n, int32_t m_ineq, int32_t m_eq, double* x,
+                         double* y_ineq, double* y_eq) {
+  return hguard([&] {
+    if (n < 0 || m_ineq < 0 || m_eq < 0) throw HostError(RAPDHG_E_INVALID_ARGUMENT, "negative dimensions");
+    for (int32_t j = 0; j < n; ++j) x[j] *= d2[j];
+    for (int32_t i = 0; i < m_ineq; ++i) y_ineq[i] *= d1[i];
+    for (int32_t i = 0; i < m_eq; ++i) y_eq[i] *= d1[m_ineq + i];
+  });
+}
+
+int rapdhg_scale_point(const double* d1, const double* d2, int32_t n, int32_t m_ineq, int32_t m_eq, double* x,
+                       double* y_ineq, double* y_eq) {
+  return hguard([&] {
+    if (n < 0 || m_ineq < 0 || m_eq < 0) throw HostError(RAPDHG_E_INVALID_ARGUMENT, "negative dimensions");
+    for (int32_t j = 0; j < n; ++j) x[j] /= d2[j];
+    for (int32_t i = 0; i < m_ineq; ++i) y_ineq[i] /= d1[i];
+    for (int32_t i = 0; i < m_eq; ++i) y_eq[i] /= d1[m_ineq + i];
+  });
+}
+
+// primal_weight_init (stepsize.hpp:73-78) with norm2 = sqrt of the
+// sequential dot (vec.hpp:14-20)
+int rapdhg_primal_weight_init(const double* c, int64_t n, const double* b, int64_t m, double* out) {
+  return hguard([&] {
+    if (!out || (n && !c) || (m && !b)) throw HostError(RAPDHG_E_INVALID_ARGUMENT, "null argument");
+    double sc = 0.0, sb = 0.0;
+    for (int64_t j = 0; j < n; ++j) sc += c[j] * c[j];
+    for (int64_t i = 0; i < m; ++i) sb += b[i] * b[i];
+    const double nc = std::sqrt(sc), nb = std::sqrt(sb);
+    *out = (nc > 1e-10 && nb > 1e-10) ? nc / nb : 1.0;
+  });
 }
 
 int rapdhg_generate(int32_t kind, double scale, uint64_t seed, rapdhg_qp_owned* out) {

@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     assert len(syms) >= 30
     missing = [s for s in syms if not hasattr(lib, s)]
     assert not missing, missing
-    assert rb.lib().rapdhg_abi_version() == 1
+    assert rb.lib().rapdhg_abi_version() == 2
 
 
 def test_library_is_sm100a():
@@ -44,6 +44,10 @@ def test_no_cpu_fallback_without_device():
     from instances import one_d
     with pytest.raises(rb.NoDeviceError):
         rb.solve(one_d(), rb.SolverConfig())
+    with pytest.raises(rb.NoDeviceError):
+        one_d().validate()
+    with pytest.raises(rb.NoDeviceError):
+        rb.symmetry_gap(M)
 
 
 def test_csr_from_triplets_semantics():
@@ -111,3 +115,23 @@ def test_generator_sizes_match_survey():
     nf, ns = 5000, 500
     assert p.num_vars() == 2 * nf + ns and p.num_rows() == 2 * nf + ns
     assert p.num_eq() == ns and p.num_ineq() == 2 * nf
+
+
+def test_point_scaling_and_primal_weight_init_match_reference():
+    """unscale_point / scale_point (scaling.hpp:126-143) and primal_weight_init
+    (stepsize.hpp:73-78) through the C-ABI: the reference's arithmetic."""
+    g = np.random.default_rng(3)
+    n, mi, me = 50, 20, 7
+    s = rb.ScalingInfo(g.uniform(0.1, 3, mi + me), g.uniform(0.1, 3, n))
+    z = rb.PrimalDualPoint(g.standard_normal(n), g.random(mi), g.standard_normal(me))
+    u = rb.unscale_point(z, s)
+    assert np.array_equal(u.x, z.x * s.d2) and np.array_equal(u.y_ineq, z.y_ineq * s.d1[:mi])
+    assert np.array_equal(u.y_eq, z.y_eq * s.d1[mi:])
+    back = rb.scale_point(u, s)
+    assert np.allclose(back.x, z.x, rtol=1e-14) and np.allclose(back.y_eq, z.y_eq, rtol=1e-14)
+    with pytest.raises(rb.InvalidArgument):
+        rb.unscale_point(z, rb.ScalingInfo(s.d1[:-1], s.d2))
+    ref = oracle.ref() if oracle.have_ref() else oracle.port()
+    for c, b in ((g.standard_normal(40), g.standard_normal(9)), (np.zeros(3), np.ones(2)), ([-2.0], [0.5])):
+        assert rb.primal_weight_init(c, b) == ref.primal_weight_init(c, b)
+    assert rb.primal_weight_init([-2.0], [0.5]) == 4.0  # SPEC.md:290

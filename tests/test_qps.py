@@ -149,3 +149,77 @@ def test_read_file(tmp_path):
     same_qp(rb.read_qps(str(f)), rb.parse_qps(ONE_D))
     with pytest.raises(rb.QpsParseError, match="cannot open"):
         rb.read_qps(str(tmp_path / "missing.qps"))
+
+
+def same_map(a: rb.CanonicalMap, b: rb.CanonicalMap):
+    assert a.ineq_labels == b.ineq_labels and a.eq_labels == b.eq_labels
+
+
+def test_parse_names_and_map_match_reference():
+    """CanonicalMap labels (problem.hpp:95-104) and names survive the ABI."""
+    for text in (ONE_D, RICH):
+        a, ma = rb.parse_qps_with_map(text)
+        b, mb = oracle.ref().parse_qps_with_map(text)
+        same_qp(a, b)
+        same_map(ma, mb)
+        assert a.name == b.name and a.var_names == b.var_names
+    p, mp = rb.parse_qps_with_map(RICH)
+    assert p.name == "RICH" and p.var_names == ["X1", "X2", "X3", "X4"]
+    assert mp.ineq_labels[:2] == ["row:LIM1:ub", "row:LIM1:lb"] and "bound:X4:ub" in mp.ineq_labels
+
+
+def random_raw(seed, n=12, m=9, names=True):
+    g = np.random.default_rng(seed)
+    A = g.standard_normal((m, n)) * (g.random((m, n)) < 0.4)
+    P = g.standard_normal((n, n)) * (g.random((n, n)) < 0.3)
+    Q = P @ P.T
+    def csr(M):
+        r, c = np.nonzero(M)
+        return rb.SparseMatrix.from_coo(M.shape[0], M.shape[1], r, c, M[r, c])
+    lower = np.where(g.random(n) < 0.3, -np.inf, g.uniform(-2, 0, n))
+    upper = np.where(g.random(n) < 0.3, np.inf, g.uniform(0, 2, n))
+    rng = np.where(g.random(m) < 0.5, np.nan, g.uniform(-3, 3, m))
+    return rb.RawProblem(q=csr(Q), c=g.standard_normal(n), a=csr(A), row_types=g.integers(0, 3, m),
+                         rhs=g.standard_normal(m), lower=lower, upper=upper, range=rng,
+                         obj_offset=float(g.standard_normal()), name=f"raw{seed}" if names else "",
+                         row_names=[f"R{i}" for i in range(m)] if names else [],
+                         var_names=[f"V{j}" for j in range(n)] if names else [])
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_canonicalize_matches_reference(seed):
+    """rapdhg_canonicalize (RawProblem -> CanonicalProblem, problem.hpp:72-198)
+    equals the reference's canonicalize: arrays, labels, names."""
+    raw = random_raw(seed, names=seed % 2 == 0)
+    a, ma = rb.canonicalize(raw)
+    b, mb = oracle.ref().canonicalize(raw)
+    same_qp(a, b)
+    same_map(ma, mb)
+    assert a.name == b.name and a.var_names == b.var_names
+    assert a.num_rows() > 0 and len(ma.ineq_labels) == a.num_ineq() and len(ma.eq_labels) == a.num_eq()
+    # write_qps with names = the reference writer's text
+    assert rb.write_qps(a) == oracle.ref().write_qps(a)
+
+
+def test_canonicalize_errors_match_reference():
+    raw = random_raw(1)
+    cases = []
+    r = random_raw(1); r.c = r.c.copy(); r.c[3] = np.nan; cases.append((r, "NaN in objective vector"))
+    r = random_raw(1); r.rhs = r.rhs.copy(); r.rhs[0] = np.nan; cases.append((r, "NaN in right-hand side"))
+    r = random_raw(1); r.lower = r.lower.copy(); r.lower[2] = np.nan; cases.append((r, "NaN variable bound"))
+    r = random_raw(1); r.lower = r.lower.copy(); r.upper = r.upper.copy(); r.lower[4], r.upper[4] = 1.0, 0.5
+    cases.append((r, "infeasible bounds on variable V4"))
+    r = random_raw(1, names=False); r.lower = r.lower.copy(); r.upper = r.upper.copy(); r.lower[4], r.upper[4] = 1.0, 0.5
+    cases.append((r, "infeasible bounds on variable 4"))
+    r = random_raw(1)
+    qd = r.q.to_dense(); qd[0, 1] += 1.0
+    rr, cc = np.nonzero(qd)
+    r.q = rb.SparseMatrix.from_coo(qd.shape[0], qd.shape[1], rr, cc, qd[rr, cc])
+    cases.append((r, "Q is not symmetric"))
+    for r, msg in cases:
+        with pytest.raises(rb.InvalidArgument) as mine:
+            rb.canonicalize(r)
+        with pytest.raises(Exception) as ref:
+            oracle.ref().canonicalize(r)
+        assert str(mine.value) == str(ref.value) == msg
+    assert raw.num_vars() == 12

@@ -215,13 +215,40 @@ void rapdhg_session_destroy(rapdhg_session* s);
 int rapdhg_shard_plan(const rapdhg_qp* qp, int32_t parts, int32_t* dual_bounds,
                       int32_t* primal_bounds);
 
+/* Host-staged transport: the caller's own collectives (MPI, gloo, ...) as
+ * callbacks. The library stages each exchange through host memory, so one
+ * process per rank works over any process group (and several ranks may share
+ * a GPU); NCCL is the fast path. Every callback is collective over all ranks,
+ * called in the same order on every rank, and returns 0 on success.
+ *  - allgatherv: buf (length bounds[parts]) holds this rank's slice
+ *    [bounds[rank], bounds[rank+1]); fill every other rank's slice in place.
+ *  - alltoallv: send[send_off[p] .. send_off[p+1]) goes to rank p, which
+ *    receives it into its recv[recv_off[me] .. recv_off[me+1]) (offsets have
+ *    parts+1 entries; this rank's own segments are empty).
+ *  - allreduce_min: *value = min over ranks. */
+typedef struct {
+  void* ctx;
+  int (*allgatherv)(void* ctx, double* buf, const int64_t* bounds, int32_t parts);
+  int (*alltoallv)(void* ctx, const double* send, const int64_t* send_off, double* recv,
+                   const int64_t* recv_off, int32_t parts);
+  int (*allreduce_min)(void* ctx, int64_t* value);
+} rapdhg_host_transport;
+
 typedef struct {
   int32_t parts;    /* number of shards */
   int32_t rank;     /* this process's shard (ignored when emulate = 1) */
   int32_t emulate;  /* 1: all shards in this process on cfg->device */
   int32_t pad;
-  uint8_t nccl_id[128]; /* ncclUniqueId from rank 0 (emulate = 0) */
+  uint8_t nccl_id[128]; /* ncclUniqueId from rank 0 (emulate = 0, no host transport) */
+  const rapdhg_host_transport* host; /* non-NULL (emulate = 0): use these collectives, not NCCL */
 } rapdhg_shard_opts;
+
+/* Exercises a host transport's callbacks without a GPU: allgather-v, an
+ * all-to-all-v and a min-reduction over `parts` ranks with deterministic
+ * per-rank data of about `len` elements, each result checked against its
+ * expected value. Collective; returns 0 when every exchange delivered the
+ * expected data. */
+int rapdhg_host_transport_check(const rapdhg_host_transport* t, int32_t parts, int32_t rank, int64_t len);
 
 /* 128-byte ncclUniqueId for rapdhg_shard_opts.nccl_id (call on rank 0 and
  * broadcast it, e.g. with torch.distributed). */

@@ -119,6 +119,7 @@ def _load():
     d(lib, "rapdhg_shard_session_create", C.c_int, P(abi.Qp), P(abi.Config), P(abi.ShardOpts), P(C.c_void_p))
     d(lib, "rapdhg_shard_session_solve", C.c_int, C.c_void_p, P(abi.Result))
     d(lib, "rapdhg_shard_session_destroy", None, C.c_void_p)
+    d(lib, "rapdhg_host_transport_check", C.c_int, P(abi.HostTransport), C.c_int32, C.c_int32, C.c_int64)
     d(lib, "rapdhg_canonicalize", C.c_int, P(abi.RawProblem), P(abi.QpOwned), P(abi.CanonicalMap))
     d(lib, "rapdhg_canonical_map_free", None, P(abi.CanonicalMap))
     d(lib, "rapdhg_parse_qps_map", C.c_int, C.c_char_p, P(abi.QpOwned), P(abi.CanonicalMap))
@@ -521,11 +522,98 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
-def _shard_opts(parts, emulate, rank, nccl_id) -> abi.ShardOpts:
+class ProcessGroupTransport:
+    """rapdhg_host_transport over a torch.distributed process group (e.g.
+    gloo): the sharded solver's exchanges staged through host memory and done
+    with the group's collectives — one process per rank on any backend (and
+    several ranks may share a GPU). NCCL (nccl_id) is the fast path."""
+
+    def __init__(self, group=None):
+        import torch
+        import torch.distributed as dist
+
+        self.torch, self.dist, self.group = torch, dist, group
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        self.errors = []
+        self._cbs = (abi.ALLGATHERV_CB(self._allgatherv), abi.ALLTOALLV_CB(self._alltoallv),
+                     abi.ALLREDUCE_MIN_CB(self._allreduce_min))
+        self.struct = abi.HostTransport(None, *self._cbs)
+
+    def _gather_padded(self, local: np.ndarray):
+        """all_gather of variable-length float64 arrays."""
+        torch, dist = self.torch, self.dist
+        n = torch.tensor([len(local)], dtype=torch.int64)
+        ns = [torch.zeros(1, dtype=torch.int64) for _ in range(self.world)]
+        dist.all_gather(ns, n, group=self.group)
+        L = max(max(int(x.item()) for x in ns), 1)
+        mine = torch.zeros(L, dtype=torch.float64)
+        mine[:len(local)] = torch.from_numpy(np.ascontiguousarray(local))
+        out = [torch.empty(L, dtype=torch.float64) for _ in range(self.world)]
+        dist.all_gather(out, mine, group=self.group)
+        return [o[:int(k.item())].numpy() for o, k in zip(out, ns)]
+
+    def _guard(self, f):
+        try:
+            f()
+            return 0
+        except Exception as e:  # reported by the library as a failed exchange
+            self.errors.append(e)
+            return 1
+
+    def _allgatherv(self, ctx, buf, bounds, parts):
+        def run():
+            b = np.ctypeslib.as_array(bounds, (parts + 1,)).copy()
+            total = int(b[-1])
+            if total == 0:
+                self._gather_padded(np.zeros(0))
+                return
+            arr = np.ctypeslib.as_array(buf, (total,))
+            got = self._gather_padded(arr[b[self.rank]:b[self.rank + 1]])
+            for k in range(parts):
+                if k != self.rank:
+                    arr[b[k]:b[k + 1]] = got[k]
+        return self._guard(run)
+
+    def _alltoallv(self, ctx, send, send_off, recv, recv_off, parts):
+        def run():
+            so = np.ctypeslib.as_array(send_off, (parts + 1,)).copy()
+            ro = np.ctypeslib.as_array(recv_off, (parts + 1,)).copy()
+            sbuf = np.ctypeslib.as_array(send, (int(so[-1]),)).copy() if so[-1] else np.zeros(0)
+            # every rank's packed send buffer and offsets; take this rank's segments
+            bufs = self._gather_padded(sbuf)
+            offs = self._gather_padded(so.astype(np.float64))
+            if ro[-1]:
+                rbuf = np.ctypeslib.as_array(recv, (int(ro[-1]),))
+                for p in range(parts):
+                    if p != self.rank:
+                        o = offs[p].astype(np.int64)
+                        seg = bufs[p][o[self.rank]:o[self.rank + 1]]
+                        if len(seg) != ro[p + 1] - ro[p]:
+                            raise RuntimeError("alltoallv: segment sizes disagree")
+                        rbuf[ro[p]:ro[p + 1]] = seg
+        return self._guard(run)
+
+    def _allreduce_min(self, ctx, value):
+        def run():
+            t = self.torch.tensor([int(value[0])], dtype=self.torch.int64)
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
+            value[0] = int(t.item())
+        return self._guard(run)
+
+    def check(self, length: int = 1000) -> None:
+        """rapdhg_host_transport_check: the library drives these callbacks
+        (collective; raises on a wrong delivery)."""
+        _check(_load().rapdhg_host_transport_check(C.byref(self.struct), self.world, self.rank, int(length)))
+
+
+def _shard_opts(parts, emulate, rank, nccl_id, transport=None) -> abi.ShardOpts:
     opts = abi.ShardOpts()
     opts.parts, opts.rank, opts.emulate = int(parts), int(rank), int(bool(emulate))
     if nccl_id is not None:
         C.memmove(opts.nccl_id, nccl_id, 128)
+    if transport is not None:
+        opts.parts, opts.rank, opts.emulate = transport.world, transport.rank, 0
+        opts.host = C.pointer(transport.struct)
     return opts
 
 
@@ -534,10 +622,13 @@ class ShardSession:
     repeated solves. Collective across ranks when emulate=False."""
 
     def __init__(self, original: QuadraticProgram, cfg: Optional[SolverConfig] = None, parts: int = 2,
-                 emulate: bool = True, rank: int = 0, nccl_id: Optional[bytes] = None):
+                 emulate: bool = True, rank: int = 0, nccl_id: Optional[bytes] = None,
+                 transport: Optional[ProcessGroupTransport] = None):
         self.cfg = cfg or SolverConfig()
+        self._transport = transport  # its callbacks must outlive the session
         h = C.c_void_p()
-        qp, cs, opts = original._struct(), self.cfg._struct(), _shard_opts(parts, emulate, rank, nccl_id)
+        qp, cs = original._struct(), self.cfg._struct()
+        opts = _shard_opts(parts, emulate, rank, nccl_id, transport)
         _check(_load().rapdhg_shard_session_create(C.byref(qp), C.byref(cs), C.byref(opts), C.byref(h)))
         self._h = h
 
@@ -563,14 +654,16 @@ class ShardSession:
 
 
 def solve_sharded(original: QuadraticProgram, cfg: Optional[SolverConfig] = None, parts: int = 2,
-                  emulate: bool = True, rank: int = 0, nccl_id: Optional[bytes] = None) -> SolveResult:
+                  emulate: bool = True, rank: int = 0, nccl_id: Optional[bytes] = None,
+                  transport: Optional[ProcessGroupTransport] = None) -> SolveResult:
     """Row-sharded solve. emulate=True runs all `parts` shards in
     this process on cfg.device (exchanges as device copies); emulate=False is
     one process per GPU, shard `rank`, NCCL communicator from `nccl_id`
-    (nccl_unique_id() on rank 0, broadcast by the caller). Bit-identical to
-    solve() in fast mode."""
+    (nccl_unique_id() on rank 0, broadcast by the caller), or the host-staged
+    collectives of `transport` (a ProcessGroupTransport: parts and rank come
+    from its group). Bit-identical to solve() in fast mode."""
     cfg = cfg or SolverConfig()
-    opts = _shard_opts(parts, emulate, rank, nccl_id)
+    opts = _shard_opts(parts, emulate, rank, nccl_id, transport)
     qp, cs, out = original._struct(), cfg._struct(), abi.Result()
     L = _load()
     _check(L.rapdhg_solve_sharded(C.byref(qp), C.byref(cs), C.byref(opts), C.byref(out)))
@@ -987,7 +1080,7 @@ __all__ = [
     "SparseMatrix", "QuadraticProgram", "PrimalDualPoint", "SolverConfig", "SolveResult",
     "SolveStatus", "Algorithm", "RestartPolicy", "StepRule", "PrimalWeightMode", "KktResiduals",
     "LogRecord", "IterateState", "StepParams", "ScalingInfo", "PowerIterOptions", "RestartContext",
-    "Session", "Gen", "solve", "solve_sharded", "ShardSession", "shard_plan", "nccl_unique_id", "inner_step", "pdhg_step", "rel_kkt", "compute_scaling",
+    "Session", "Gen", "solve", "solve_sharded", "ShardSession", "ProcessGroupTransport", "shard_plan", "nccl_unique_id", "inner_step", "pdhg_step", "rel_kkt", "compute_scaling",
     "ruiz_scaling", "apply_scaling", "unscale_point", "scale_point", "estimate_op_norm",
     "estimate_op_norm_symmetric", "step_schedule_theoretical", "pdhg_constant_steps",
     "adaptive_eta", "primal_weight_init", "primal_weight_update", "restart_decision", "generate",

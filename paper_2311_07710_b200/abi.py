@@ -99,9 +99,19 @@ class QpOwned(C.Structure):
                 ("obj_offset", f64), ("name", C.c_char_p), ("var_names", C.POINTER(C.c_char_p))]
 
 
+ALLGATHERV_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, P_f64, P_i64, i32)
+ALLTOALLV_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, P_f64, P_i64, P_f64, P_i64, i32)
+ALLREDUCE_MIN_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, P_i64)
+
+
+class HostTransport(C.Structure):
+    _fields_ = [("ctx", C.c_void_p), ("allgatherv", ALLGATHERV_CB), ("alltoallv", ALLTOALLV_CB),
+                ("allreduce_min", ALLREDUCE_MIN_CB)]
+
+
 class ShardOpts(C.Structure):
     _fields_ = [("parts", i32), ("rank", i32), ("emulate", i32), ("pad", i32),
-                ("nccl_id", C.c_uint8 * 128)]
+                ("nccl_id", C.c_uint8 * 128), ("host", C.POINTER(HostTransport))]
 
 
 def declare(lib, name, restype, *argtypes):

@@ -153,6 +153,13 @@ int rapdhg_shard_plan(const rapdhg_qp* qp, int32_t parts, int32_t* dual_bounds, 
   });
 }
 
+int rapdhg_host_transport_check(const rapdhg_host_transport* t, int32_t parts, int32_t rank, int64_t len) {
+  return guard([&] {
+    null_check(t, "transport");
+    rb::host_transport_check(*t, parts, rank, len);
+  });
+}
+
 int rapdhg_nccl_unique_id(uint8_t* out128) {
   return guard([&] {
     null_check(out128, "out");
@@ -177,7 +184,8 @@ std::unique_ptr<rb::ShardedEngine> make_sharded(const rapdhg_qp* qp, const rapdh
   } else {
     if (opts->rank < 0 || opts->rank >= opts->parts) rb::invalid("sharded solve: rank out of range");
     RB_CUDA(cudaSetDevice(cfg->device));
-    tr = rb::make_nccl_transport(opts->parts, opts->rank, opts->nccl_id);
+    tr = opts->host ? rb::make_host_transport(opts->parts, opts->rank, *opts->host)
+                    : rb::make_nccl_transport(opts->parts, opts->rank, opts->nccl_id);
     rank = opts->rank;
   }
   return std::make_unique<rb::ShardedEngine>(*qp, *cfg, opts->parts, rank, std::move(tr), t0);

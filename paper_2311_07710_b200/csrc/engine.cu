@@ -410,7 +410,8 @@ double DeviceQP::op_norm_a(const double* av, const double* atv, int max_iters, d
 // ============================================================================
 
 
-Engine::Engine(const rapdhg_qp& p, const rapdhg_config& cfg, Clock::time_point t0) : cfg_(cfg) {
+Engine::Engine(const rapdhg_qp& p, const rapdhg_config& cfg, Clock::time_point t0, bool full_plans)
+    : cfg_(cfg), full_plans_(full_plans) {
   Tracer tr(nullptr);
   DeviceQP::validate_dims(p, false);  // the per-row scan runs on the device after the upload
   tr.mark("validate dims (host)");
@@ -477,7 +478,7 @@ Engine::Engine(const rapdhg_qp& p, const rapdhg_config& cfg, Clock::time_point t
   tr.mark("omega init + buffers");
   if (!P_->strict) {
     setup_slabs();
-    setup_colblocks();
+    if (full_plans_) setup_colblocks();
   }
   tr.mark("slab plans");
   setup_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
@@ -529,16 +530,22 @@ void dump_slab_profile(const char* name, const SlabView& v) {
 }  // namespace
 #endif
 
-void Engine::setup_colblocks() {
+void Engine::colblock_counts(bool dual_slab_active, bool primal_slab_active) {
   DeviceQP& P = *P_;
   auto local = [&](const DevCsr& m) {
     return pattern_locality(m.rp.get(), m.ci.get(), m.rows, m.cols, m.nnz, st_) >= 0.5;
   };
-  if (!dual_ph_.active() && colblock_count(n_) >= 2 && !local(P.A)) cb_nb_dual_ = colblock_count(n_);
-  if (!primal_ph_.active()) {
+  cb_nb_dual_ = cb_nq_ = cb_na_ = 1;
+  if (!dual_slab_active && colblock_count(n_) >= 2 && !local(P.A)) cb_nb_dual_ = colblock_count(n_);
+  if (!primal_slab_active) {
     if (colblock_count(n_) >= 2 && !local(P.Q)) cb_nq_ = colblock_count(n_);
     if (colblock_count(m_) >= 2 && !local(P.AT)) cb_na_ = colblock_count(m_);
   }
+}
+
+void Engine::setup_colblocks() {
+  DeviceQP& P = *P_;
+  colblock_counts(dual_ph_.active(), primal_ph_.active());
   build_colblocked_dual(cbd_, cb_nb_dual_, P.A.rp.get(), P.A.ci.get(), m_, n_, asv_, st_);
   build_colblocked_primal(cbp_, cb_nq_, cb_na_, P.Q.rp.get(), P.Q.ci.get(), qsv_, P.AT.rp.get(), P.AT.ci.get(), atsv_,
                           n_, n_, m_, st_);
@@ -568,16 +575,26 @@ void Engine::plan_slabs_async() {
       DevBuf<int32_t> len;
       if (dual) {
         dual_choice_ = choose_slabs(P.A.rp.get(), P.A.ci.get(), P.A.rows, P.A.nnz, n_, s2);
+        if (!full_plans_) {
+          RB_CUDA(cudaStreamSynchronize(s2));
+          tr.mark("  slab choice: dual (async)");
+        } else {
         row_lengths(len, P.A.rp.get(), nullptr, m_, s2);
         build_slab_phase(dual_ph_, dual_choice_, 0, P.A.rp.get(), P.A.ci.get(), nullptr, nullptr, 0, m_, len.get(),
                          s2);
         tr.mark("  slab plan: dual (async)");
+        }
       } else {
         primal_choice_ = choose_slabs(P.AT.rp.get(), P.AT.ci.get(), n_, P.AT.nnz, m_, s2);
+        if (!full_plans_) {
+          RB_CUDA(cudaStreamSynchronize(s2));
+          tr.mark("  slab choice: primal (async)");
+        } else {
         row_lengths(len, P.Q.rp.get(), P.AT.rp.get(), n_, s2);
         build_slab_phase(primal_ph_, primal_choice_, 1, P.Q.rp.get(), P.Q.ci.get(), P.AT.rp.get(), P.AT.ci.get(), 0,
                          n_, len.get(), s2);
         tr.mark("  slab plan: primal (async)");
+        }
       }
       RB_CUDA(cudaStreamSynchronize(s2));
     } catch (...) {

@@ -139,7 +139,10 @@ class ShardedEngine;
 
 class Engine : public LoopBackend {
  public:
-  Engine(const rapdhg_qp& p, const rapdhg_config& cfg, Clock::time_point t0);
+  // full_plans = false (the sharded solver's setup): only the slab window
+  // choices are made; the slab phases and column blocks over all rows, which
+  // the shards rebuild over their own rows, are skipped.
+  Engine(const rapdhg_qp& p, const rapdhg_config& cfg, Clock::time_point t0, bool full_plans = true);
   ~Engine() override;
   Engine(const Engine&) = delete;
   Engine& operator=(const Engine&) = delete;
@@ -207,6 +210,9 @@ class Engine : public LoopBackend {
   SlabPhase dual_ph_, primal_ph_;
   // L2-sized column blocks (colblock.cuh) of the gather-bound ops without a slab plan
   void setup_colblocks();
+  // column-block counts of the ops without an active slab phase
+  void colblock_counts(bool dual_slab_active, bool primal_slab_active);
+  bool full_plans_ = true;
   int cb_nb_dual_ = 1, cb_nq_ = 1, cb_na_ = 1;  // block counts (global: shards reuse them)
   ColBlockedDual cbd_;
   ColBlockedPrimal cbp_;

@@ -259,7 +259,100 @@ class NcclTransport : public Transport {
   DevBuf<long long> scratch_;
 };
 
+// The caller's collectives as host callbacks: every exchange is staged
+// through pinned host memory around one callback (test and portability path;
+// NCCL is the fast path).
+class HostTransport : public Transport {
+ public:
+  HostTransport(int parts, int rank, const rapdhg_host_transport& t) : parts_(parts), rank_(rank), t_(t) {
+    if (!t.allgatherv || !t.alltoallv || !t.allreduce_min) invalid("host transport: null callback");
+  }
+  bool capturable() const override { return false; }
+  void allgatherv(const std::vector<double*>& bufs, const std::vector<int64_t>& b, cudaStream_t st) override {
+    double* buf = bufs.at(0);
+    const int64_t total = b.back(), lo = b[rank_], hi = b[rank_ + 1];
+    double* h = stage(a_, total);
+    if (hi > lo) RB_CUDA(cudaMemcpyAsync(h + lo, buf + lo, sizeof(double) * (hi - lo), cudaMemcpyDeviceToHost, st));
+    RB_CUDA(cudaStreamSynchronize(st));
+    call(t_.allgatherv(t_.ctx, h, b.data(), parts_), "allgatherv");
+    if (lo > 0) RB_CUDA(cudaMemcpyAsync(buf, h, sizeof(double) * lo, cudaMemcpyHostToDevice, st));
+    if (total > hi)
+      RB_CUDA(cudaMemcpyAsync(buf + hi, h + hi, sizeof(double) * (total - hi), cudaMemcpyHostToDevice, st));
+    RB_CUDA(cudaStreamSynchronize(st));  // the staging buffer is reused by the next exchange
+  }
+  void halo(const std::vector<double*>& bufs, const std::vector<HaloSide*>& sides, cudaStream_t st) override {
+    const HaloSide& h = *sides.at(0);
+    halo_pack(h, bufs.at(0), st);
+    const int64_t ns = h.send_off.back(), nr = h.recv_off.back();
+    double* hs = stage(a_, ns);
+    double* hr = stage(b_, nr);
+    if (ns) RB_CUDA(cudaMemcpyAsync(hs, h.send_buf.get(), sizeof(double) * ns, cudaMemcpyDeviceToHost, st));
+    RB_CUDA(cudaStreamSynchronize(st));
+    call(t_.alltoallv(t_.ctx, hs, h.send_off.data(), hr, h.recv_off.data(), parts_), "alltoallv");
+    if (nr) RB_CUDA(cudaMemcpyAsync(h.recv_buf.get(), hr, sizeof(double) * nr, cudaMemcpyHostToDevice, st));
+    halo_unpack(h, bufs.at(0), st);
+    RB_CUDA(cudaStreamSynchronize(st));
+  }
+  long long allreduce_min(const std::vector<long long*>& vals, cudaStream_t st) override {
+    int64_t v = 0;
+    RB_CUDA(cudaMemcpyAsync(&v, vals.at(0), sizeof(v), cudaMemcpyDeviceToHost, st));
+    RB_CUDA(cudaStreamSynchronize(st));
+    call(t_.allreduce_min(t_.ctx, &v), "allreduce_min");
+    return v;
+  }
+
+ private:
+  static void call(int rc, const char* what) {
+    if (rc != 0) throw Error(RAPDHG_E_CUDA, std::string("host transport ") + what + " failed (" + std::to_string(rc) + ")");
+  }
+  static double* stage(PinnedBuf<double>& p, int64_t n) {
+    if (static_cast<int64_t>(p.size()) < n) p.alloc(static_cast<std::size_t>(n));
+    return p.get();
+  }
+  int parts_, rank_;
+  rapdhg_host_transport t_;
+  PinnedBuf<double> a_, b_;
+};
+
 }  // namespace
+
+std::unique_ptr<Transport> make_host_transport(int parts, int rank, const rapdhg_host_transport& t) {
+  return std::make_unique<HostTransport>(parts, rank, t);
+}
+
+// Deterministic data for each exchange kind, checked on arrival.
+void host_transport_check(const rapdhg_host_transport& t, int parts, int rank, int64_t len) {
+  if (parts < 1 || rank < 0 || rank >= parts || len < 0) invalid("host transport check: bad arguments");
+  if (!t.allgatherv || !t.alltoallv || !t.allreduce_min) invalid("host transport: null callback");
+  auto fail = [](const std::string& m) { throw Error(RAPDHG_E_INTERNAL, "host transport check: " + m); };
+  // allgather-v over uneven slices
+  std::vector<int64_t> b(parts + 1, 0);
+  for (int k = 0; k < parts; ++k) b[k + 1] = b[k] + len / parts + (k < len % parts ? 1 : 0) + k;
+  std::vector<double> buf(static_cast<std::size_t>(b[parts]), std::nan(""));
+  auto f = [](int64_t i) { return 1.5 * static_cast<double>(i) + 0.25; };
+  for (int64_t i = b[rank]; i < b[rank + 1]; ++i) buf[i] = f(i);
+  if (t.allgatherv(t.ctx, buf.data(), b.data(), parts) != 0) fail("allgatherv returned an error");
+  for (int64_t i = 0; i < b[parts]; ++i)
+    if (buf[i] != f(i)) fail("allgatherv delivered a wrong value at " + std::to_string(i));
+  // all-to-all-v: rank r sends cnt(r, p) values g(r, p, k) to p
+  auto cnt = [&](int r, int p) { return r == p ? int64_t{0} : (r * 7 + p * 3) % 5 + 1 + len % 3; };
+  auto g = [](int r, int p, int64_t k) { return r * 1000.0 + p * 100.0 + static_cast<double>(k) + 0.5; };
+  std::vector<int64_t> so(parts + 1, 0), ro(parts + 1, 0);
+  for (int p = 0; p < parts; ++p) so[p + 1] = so[p] + cnt(rank, p), ro[p + 1] = ro[p] + cnt(p, rank);
+  std::vector<double> send(static_cast<std::size_t>(std::max<int64_t>(so[parts], 1))), recv(
+      static_cast<std::size_t>(std::max<int64_t>(ro[parts], 1)), std::nan(""));
+  for (int p = 0; p < parts; ++p)
+    for (int64_t k = 0; k < cnt(rank, p); ++k) send[so[p] + k] = g(rank, p, k);
+  if (t.alltoallv(t.ctx, send.data(), so.data(), recv.data(), ro.data(), parts) != 0)
+    fail("alltoallv returned an error");
+  for (int p = 0; p < parts; ++p)
+    for (int64_t k = 0; k < cnt(p, rank); ++k)
+      if (recv[ro[p] + k] != g(p, rank, k)) fail("alltoallv delivered a wrong value from rank " + std::to_string(p));
+  // min-reduction
+  int64_t v = 100 + 3 * (parts - 1 - rank);
+  if (t.allreduce_min(t.ctx, &v) != 0) fail("allreduce_min returned an error");
+  if (v != 100) fail("allreduce_min returned " + std::to_string(v));
+}
 
 std::unique_ptr<Transport> make_emulated_transport(int parts) {
   return std::make_unique<EmulatedTransport>(parts);
@@ -298,7 +391,10 @@ ShardedEngine::ShardedEngine(const rapdhg_qp& p, const rapdhg_config& cfg, int p
     : cfg_(cfg), parts_(parts), tr_(std::move(tr)) {
   if (cfg.strict_parity) invalid("sharded solve: strict_parity needs sequential reductions; use one GPU");
   if (parts < 1) invalid("sharded solve: parts must be >= 1");
-  full_ = std::make_unique<Engine>(p, cfg, t0);  // validation, scaling, norms
+  // validation, scaling, norms and the slab window choices; the single-GPU
+  // slab phases / column blocks over all rows are not built (each shard
+  // builds its own over its rows below)
+  full_ = std::make_unique<Engine>(p, cfg, t0, /*full_plans=*/false);
   plan_ = make_shard_plan(p, parts);
   st_ = full_->st_;
   AllocStreamScope scope(st_);
@@ -332,13 +428,6 @@ ShardedEngine::ShardedEngine(const rapdhg_qp& p, const rapdhg_config& cfg, int p
         assign_slab_ctas(sh->primal_ph.plan, prepare_slab<PrimalStepOp<false>>(sh->primal_ph.plan.view.smem_bytes()), st_);
       }
     }
-    if (!sh->dual_ph.active() && sh->d1 > sh->d0)
-      build_colblocked_dual(sh->cbd, full_->cb_nb_dual_, P.A.rp.get() + sh->d0, P.A.ci.get(),
-                            static_cast<int32_t>(sh->d1 - sh->d0), n, full_->asv_, st_);
-    if (!sh->primal_ph.active() && sh->p1 > sh->p0)
-      build_colblocked_primal(sh->cbp, full_->cb_nq_, full_->cb_na_, P.Q.rp.get() + sh->p0, P.Q.ci.get(), full_->qsv_,
-                              P.AT.rp.get() + sh->p0, P.AT.ci.get(), full_->atsv_,
-                              static_cast<int32_t>(sh->p1 - sh->p0), n, m, st_);
     for (int i = 0; i < 2; ++i) {
       sh->X[i].alloc(n), sh->XMD[i].alloc(n), sh->xu[i].alloc(n), sh->yu[i].alloc(m);
       sh->ax[i].alloc(m), sh->qx[i].alloc(n), sh->aty[i].alloc(n);
@@ -354,6 +443,34 @@ ShardedEngine::ShardedEngine(const rapdhg_qp& p, const rapdhg_config& cfg, int p
   params_.alloc(kMaxChunk);
   params_h_.alloc(kMaxChunk);
   red_h_.alloc(64);
+  // column blocks for the ops whose slab phase is inactive on EVERY shard —
+  // the decision one GPU takes over all rows, so every row is computed as
+  // there (a vote across ranks)
+  bool dual_any = false, primal_any = false;
+  for (auto& sh : shards_) dual_any |= sh->dual_ph.active(), primal_any |= sh->primal_ph.active();
+  if (rank >= 0 && parts > 1) {  // one process per shard: vote (min over ranks of "none here")
+    auto vote = [&](bool any) {
+      std::vector<long long*> v;
+      const long long none = any ? 0 : 1;
+      for (auto& sh : shards_) {
+        RB_CUDA(cudaMemcpyAsync(sh->vote.get(), &none, sizeof(none), cudaMemcpyHostToDevice, st_));
+        v.push_back(sh->vote.get());
+      }
+      return tr_->allreduce_min(v, st_) == 0;
+    };
+    dual_any = vote(dual_any);
+    primal_any = vote(primal_any);
+  }
+  full_->colblock_counts(dual_any, primal_any);
+  for (auto& sh : shards_) {
+    if (!sh->dual_ph.active() && sh->d1 > sh->d0)
+      build_colblocked_dual(sh->cbd, full_->cb_nb_dual_, P.A.rp.get() + sh->d0, P.A.ci.get(),
+                            static_cast<int32_t>(sh->d1 - sh->d0), n, full_->asv_, st_);
+    if (!sh->primal_ph.active() && sh->p1 > sh->p0)
+      build_colblocked_primal(sh->cbp, full_->cb_nq_, full_->cb_na_, P.Q.rp.get() + sh->p0, P.Q.ci.get(), full_->qsv_,
+                              P.AT.rp.get() + sh->p0, P.AT.ci.get(), full_->atsv_,
+                              static_cast<int32_t>(sh->p1 - sh->p0), n, m, st_);
+  }
   build_halos();
   RB_CUDA(cudaStreamSynchronize(st_));
 }
@@ -590,7 +707,7 @@ void ShardedEngine::body(int len, int cur) {
 
 void ShardedEngine::run_chunk(int len) {
   params_.upload(params_h_.get(), len, st_);
-  if (cfg_.use_graphs) {
+  if (cfg_.use_graphs && tr_->capturable()) {
     const int key = (len << 1) | cur_;
     auto it = graphs_.find(key);
     if (it == graphs_.end()) {

@@ -50,6 +50,9 @@ struct HaloSide {
 class Transport {
  public:
   virtual ~Transport() = default;
+  // false: the exchanges synchronise with the host (host-staged transport),
+  // so the chunk cannot be captured into a CUDA graph
+  virtual bool capturable() const { return true; }
   // After the call, bufs[s] holds every entry sides[s]->recv_idx names
   // (from its owner); other non-owned entries are left as they were.
   virtual void halo(const std::vector<double*>& bufs, const std::vector<HaloSide*>& sides, cudaStream_t st) = 0;
@@ -65,6 +68,10 @@ std::unique_ptr<Transport> make_emulated_transport(int parts);
 // NCCL communicator for `rank` of `parts` from a 128-byte ncclUniqueId.
 std::unique_ptr<Transport> make_nccl_transport(int parts, int rank, const void* unique_id);
 void nccl_unique_id(void* out128);
+// The caller's collectives as host callbacks (rapdhg_host_transport).
+std::unique_ptr<Transport> make_host_transport(int parts, int rank, const rapdhg_host_transport& t);
+// Host-only self-check of a host transport's callbacks (rapdhg_host_transport_check).
+void host_transport_check(const rapdhg_host_transport& t, int parts, int rank, int64_t len);
 
 class ShardedEngine : public LoopBackend {
  public:

@@ -173,7 +173,7 @@ typedef struct {
   double* restart_y;
   /* --- B200 instrumentation --- */
   double setup_seconds;     /* upload + validate + scaling + norms */
-  double loop_seconds;      /* iterations + checks, device time    */
+  double loop_seconds;      /* iterations + checks + restarts, device time (the final download excluded) */
   int64_t kernel_launches;  /* library kernels launched by this call */
   /* profile_kernels=1|2: summed time (ms) and sample counts of the two
    * steps (0 = dual step A*w, 1 = primal step [Q|A']) in sampled chunks */

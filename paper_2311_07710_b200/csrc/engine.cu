@@ -1125,6 +1125,9 @@ void run_loop(LoopBackend& be, const rapdhg_config& cfg, const LoopScalars& sc, 
   out->status = status;
   out->iterations = fin_iters;
   out->residuals = {fin_res.r_primal, fin_res.r_dual, fin_res.r_gap};
+  // the loop clock (loop_seconds: iterations + checks + restarts, device
+  // time) stops before the solution's download to the host
+  be.loop_end(out);
   out->x = xalloc<double>(n);
   double* yall = xalloc<double>(m);
   be.download(fin_src, out->x, yall);
@@ -1133,7 +1136,6 @@ void run_loop(LoopBackend& be, const rapdhg_config& cfg, const LoopScalars& sc, 
   if (mi_) std::memcpy(out->y_ineq, yall, sizeof(double) * mi_);
   if (m - mi_) std::memcpy(out->y_eq, yall + mi_, sizeof(double) * (m - mi_));
   std::free(yall);
-  be.loop_end(out);
   out->setup_seconds = sc.setup_seconds;
   out->solve_seconds = elapsed();
 }

@@ -295,7 +295,7 @@ bool gen_svm_a_device(int32_t ns, int32_t nf, int32_t per_row, uint64_t seed, ra
   const int32_t slot = per_row + 1, m = 2 * ns;
   DevBuf<int32_t> cnt(ns), tc(static_cast<std::size_t>(ns) * slot), rp, ci;
   DevBuf<double> tv(static_cast<std::size_t>(ns) * slot), v;
-  svm_rows_kernel<<<g1(ns), 128, 0, st>>>(ns, nf, per_row, seed, cnt.get(), tc.get(), tv.get());
+  svm_rows_kernel<<<g1(ns), 256, 0, st>>>(ns, nf, per_row, seed, cnt.get(), tc.get(), tv.get());
   RB_LAUNCH_CHECK();
   scan_rows(cnt, ns, rp, st);
   int32_t nnz_top = 0;

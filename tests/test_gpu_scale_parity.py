@@ -38,7 +38,7 @@ CASES = {
     "c2": (rb.Gen.LASSO, 1.0, 2, dict(tol=1e-12, max_iters=400, snapshot_interval=40, record_restart_points=True)),
     "c3": (rb.Gen.PORTFOLIO, 1.0, 3, dict(tol=1e-12, max_iters=240, snapshot_interval=40, record_restart_points=True)),
     "c4": (rb.Gen.SVM, 1.0, 4, dict(tol=1e-12, max_iters=240, snapshot_interval=40, record_restart_points=True)),
-    "c4_tol": (rb.Gen.SVM, 1.0, 4, dict(tol=1e-6)),
+    "c4_tol": (rb.Gen.SVM, 1.0, 4, dict(tol=1e-6, max_iters=2000)),
     "c5u": (rb.Gen.LARGE, 0.1, 5, dict(tol=1e-12, max_iters=240, snapshot_interval=40, record_restart_points=True)),
     "c5l": (rb.Gen.LARGE_LOCAL, 0.1, 5, dict(tol=1e-12, max_iters=240, snapshot_interval=40,
                                               record_restart_points=True)),
@@ -167,3 +167,17 @@ def test_c2_strict_bit_identical_to_reference(runs):
     p = runs.problem("c2")
     a = rb.solve(p, runs.cfg("c2", strict_parity=True))
     assert_results_identical(a, runs.reference("c2"))
+
+
+def test_c4_device_instance_equals_reference_arm_instance(runs):
+    """The bench's C4 instance (device generator) is, array for array, the one
+    bench.py --impl reference builds with numpy (oracle/synth.py) — so both
+    arms time the same problem."""
+    from oracle import synth
+
+    p = runs.problem("c4")
+    d = synth.svm(1.0, 4)
+    for got, want in ((p.q.row_ptr, d["q"][0]), (p.q.col_idx, d["q"][1]), (p.q.values, d["q"][2]),
+                      (p.a_ineq.row_ptr, d["a_ineq"][0]), (p.a_ineq.col_idx, d["a_ineq"][1]),
+                      (p.a_ineq.values, d["a_ineq"][2]), (p.c, d["c"]), (p.b_ineq, d["b_ineq"])):
+        assert got.shape == want.shape and np.array_equal(got, want)

@@ -74,7 +74,7 @@ struct DualStepOp {
   }
   __device__ __forceinline__ const double* gather_src(int) const { return w; }
   // same op over other CSR arrays (the rest CSR of a slab plan)
-  DualStepOp with_views(CsrView s1, CsrView) const {
+  __host__ __device__ DualStepOp with_views(CsrView s1, CsrView) const {
     DualStepOp o = *this;
     o.a = s1;
     return o;
@@ -138,7 +138,7 @@ struct PrimalStepOp {
                                acc.v[1]);
   }
   __device__ __forceinline__ const double* gather_src(int slot) const { return slot ? y : xmd; }
-  PrimalStepOp with_views(CsrView s1, CsrView s2) const {
+  __host__ __device__ PrimalStepOp with_views(CsrView s1, CsrView s2) const {
     PrimalStepOp o = *this;
     o.q = s1;
     o.at = s2;

@@ -44,11 +44,16 @@ struct Wins {
   const Window* w;
   const int32_t* lut;
   int width, nlut, S;
+  int stride = 0;  // resident plans: window s is staged at s * stride; all windows form ONE run
   __device__ __forceinline__ int of(int32_t c) const {
     const int b = c / width;
     if (b >= nlut) return -1;
     const int s = lut[b];
     return (s >= 0 && c - w[s].lo < w[s].len) ? s : -1;
+  }
+  __device__ __forceinline__ int run(int s) const { return stride ? 0 : s; }  // run index of window s
+  __device__ __forceinline__ uint16_t offset(int s, int32_t c) const {        // column in the staged image
+    return static_cast<uint16_t>((stride ? s * stride : 0) + (c - w[s].lo));
   }
 };
 
@@ -60,8 +65,9 @@ __device__ __forceinline__ int in_window_count(const int32_t* rp, const int32_t*
   const int b = rp[r], e = rp[r + 1];
   int tot = 0, mx = 0, cur = -1, run = 0;
   for (int p = b; p < e; ++p) {
-    const int s = wins.of(ci[p]);
-    if (s < 0) continue;
+    const int w = wins.of(ci[p]);
+    if (w < 0) continue;
+    const int s = wins.run(w);
     if (s != cur) {
       if (cur >= 0 && per) per[cur * stride] = run;
       cur = s, run = 0;
@@ -114,12 +120,13 @@ __global__ void fill_kernel(const int32_t* rows, int32_t nw, const int32_t* rp_w
   int rw = rrp_w[k];
   for (int p = rp_w[r]; p < rp_w[r + 1]; ++p) {
     const int32_t c = ci_w[p];
-    const int s = wins.of(c);
-    if (s >= 0) {
+    const int w = wins.of(c);
+    if (w >= 0) {
+      const int s = wins.run(w);
       if (s != cur) cur = s, e = 0;
       const int64_t run = static_cast<int64_t>(s) * nw + k;
       const int64_t wp = off[run] + joff[(jx[run] >> 5) + e] + (jx[run] & 31);
-      col[wp] = static_cast<uint16_t>(c - wins.w[s].lo);
+      col[wp] = wins.offset(w, c);
       pos[wp] = p;
       ++e;
     } else {
@@ -275,22 +282,34 @@ SlabChoice choose_slabs(const int32_t* rp, const int32_t* ci, int32_t rows, int6
   return ch;
 }
 
+bool slab_resident(const SlabChoice& choice) {
+  const char* e = std::getenv("RAPDHG_SLAB_RESIDENT");
+  if (e && e[0] == '0') return false;
+  const int S = static_cast<int>(choice.windows.size());
+  return S > 0 && S <= kSlabResidentMax && S * choice.width <= 65536;  // 16-bit offsets into the image
+}
+
 void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const int32_t* rp1, const int32_t* ci1,
                      const int32_t* rp2, const int32_t* ci2, int32_t r0, int32_t r1, cudaStream_t st) {
   plan = SlabPlan{};
-  const int S = static_cast<int>(choice.windows.size());
-  if (S == 0 || r1 <= r0) return;
+  const int nwin = static_cast<int>(choice.windows.size());
+  if (nwin == 0 || r1 <= r0) return;
+  // resident: every window staged at once (window s at s * width doubles),
+  // each W row ONE run over all of them, finished inside the slab kernel
+  const bool resident = slab_resident(choice);
+  const int S = resident ? 1 : nwin;  // runs per W row
   Tracer tr(st);
   {
     const int nlut = choice.windows.back().lo / choice.width + 1;
     std::vector<int32_t> lut(nlut, -1);
-    for (int s = 0; s < S; ++s) lut[choice.windows[s].lo / choice.width] = s;
-    plan.win.alloc(S);
-    plan.win.upload(choice.windows.data(), S, st);
+    for (int s = 0; s < nwin; ++s) lut[choice.windows[s].lo / choice.width] = s;
+    plan.win.alloc(nwin);
+    plan.win.upload(choice.windows.data(), nwin, st);
     plan.lut.alloc(nlut);
     plan.lut.upload(lut.data(), nlut, st);
   }
-  const Wins wins{plan.win.get(), plan.lut.get(), choice.width, choice.windows.back().lo / choice.width + 1, S};
+  const Wins wins{plan.win.get(), plan.lut.get(), choice.width, choice.windows.back().lo / choice.width + 1, nwin,
+                  resident ? choice.width : 0};
   const int32_t* rp_w = seg == 0 ? rp1 : rp2;  // windowed segment
   const int32_t* ci_w = seg == 0 ? ci1 : ci2;
   const int32_t* rp_o = seg == 0 ? rp2 : rp1;  // the other segment (rest only)
@@ -565,9 +584,11 @@ void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const in
   v.ecap = ecap;
   v.mcap = kSlabMetaCap;
   v.win_max = 0;
-  for (int s = 0; s < S; ++s) v.win_max = std::max(v.win_max, choice.windows[s].len);
+  for (int s = 0; s < nwin; ++s) v.win_max = std::max(v.win_max, choice.windows[s].len);
   v.win = plan.win.get();
   v.win_max = (v.win_max + 1) & ~1;  // keeps the value stage 16 B-aligned
+  v.resident = resident ? nwin : 0;
+  if (resident) v.win_max = nwin * choice.width;  // the whole image (window s at s * width)
   v.tile = plan.tile.get();
   v.meta = plan.meta.get();
   v.col = plan.col.get();
@@ -578,8 +599,8 @@ void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const in
   v.rest2 = CsrView{plan.rrp2.get(), plan.rci2.get(), plan.rval2.get()};
   RB_CUDA(cudaStreamSynchronize(st));
   if (std::getenv("RAPDHG_TRACE"))
-    std::fprintf(stderr, "[slab] seg %d rows [%d,%d): W rows %d windows %d chunks %d tiles %d entries %lld (%.3f padded, %s)\n",
-                 seg, r0, r1, nw, S, ntiles, ntiles, static_cast<long long>(cursor),
+    std::fprintf(stderr, "[slab] seg %d rows [%d,%d): W rows %d windows %d%s chunks %d tiles %d entries %lld (%.3f padded, %s)\n",
+                 seg, r0, r1, nw, nwin, resident ? " (resident)" : "", ntiles, ntiles, static_cast<long long>(cursor),
                  static_cast<double>(cursor) / std::max<int64_t>(1, [&] {
                    int64_t t = 0;
                    for (int32_t c : hc2) t += c;

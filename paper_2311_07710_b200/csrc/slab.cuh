@@ -54,6 +54,7 @@ constexpr int kSlabStages = RB_SLAB_STAGES;  // tile stages per CTA (one shared 
 constexpr int kSlabRowCap = 512;        // rows per chunk
 constexpr int kSlabRunCap = 512;        // W rows: every window run and the rest <= this
 constexpr int kSlabMinWindows = 1;     // RAPDHG_SLAB_MIN_WINDOWS overrides
+constexpr int kSlabResidentMax = 8;    // resident plans: at most this many windows (128 KB) staged at once
 constexpr int kSlabProf = 10;           // per-CTA profile slots (RB_SLAB_PROFILE)
 
 // tile t = s * J + j (window-major: a CTA's contiguous tile range mostly
@@ -88,6 +89,8 @@ struct SlabView {
   int32_t ecap = 0;                // tile entry capacity (multiple of 8)
   int32_t mcap = 0;                // tile metadata capacity (multiple of 8)
   int32_t grid = 0;                // persistent CTAs
+  int32_t resident = 0;            // > 0: that many windows staged at once (window s at s * win_max / resident);
+                                   // W rows are one run and finish in the slab kernel (no partials)
   const Window* win = nullptr;     // [S] (device)
   const SlabTile* tile = nullptr;   // [J]
   const int32_t* cta = nullptr;     // [grid + 1] tile ranges per CTA (balanced by bytes)
@@ -227,6 +230,19 @@ __device__ __forceinline__ void slab_entries(const SlabView& sv, const SlabTile&
 template <class Op>
 __device__ __forceinline__ void slab_commit(const Op& op, const SlabView& sv, const SlabTile& d, double* win,
                                             uint64_t* bar, bool copy_window) {
+  if (sv.resident) {  // the whole image, once (window s at s * stride)
+    const int stride = sv.win_max / sv.resident;
+    uint32_t bytes = 0;
+    if (copy_window)
+      for (int s = 0; s < sv.resident; ++s) bytes += static_cast<uint32_t>(sv.win[s].len) * 8u;
+    mbar_expect_tx(bar, bytes);
+    if (copy_window)
+      for (int s = 0; s < sv.resident; ++s) {
+        const Window w = sv.win[s];
+        bulk_g2s(win + s * stride, op.gather_src(sv.seg) + w.lo, static_cast<uint32_t>(w.len) * 8u, bar);
+      }
+    return;
+  }
   const Window w = copy_window ? sv.win[d.s] : Window{};
   const uint32_t wbytes = static_cast<uint32_t>(w.len) * 8u;
   mbar_expect_tx(bar, wbytes);  // arrive (+ the window's bytes)
@@ -366,6 +382,14 @@ __global__ void __launch_bounds__(kSlabThreads) slab_kernel(const Op op, const S
     for (int q = (warp - deal + kSlabConsumers) % kSlabConsumers; q < nsl; q += kSlabConsumers) {
       const int slot = (q << 5) + lane;
       const int L = slot < nr ? len[slot] : 0;
+      // resident: this lane's row finishes here; its epilogue inputs are
+      // requested before the tile's entries so their latency overlaps
+      int r = 0;
+      typename Op::Pre pre{};
+      if (sv.resident && slot < nr) {
+        r = sv.wrow[perm[slot]];
+        pre = op.prefetch(r);
+      }
       const int Lm = len[q << 5];  // the slice's longest run (lane 0: sorted)
       const double* vq = val + soff[q] + lane;
       const uint16_t* cq = col + soff[q] + lane;
@@ -381,7 +405,21 @@ __global__ void __launch_bounds__(kSlabThreads) slab_kernel(const Op op, const S
 #pragma unroll
         for (int u = 0; u < 4; ++u) part = fma(v[u], x[u], part);
       }
-      if (slot < nr) partial[perm[slot]] = part;
+      if (sv.resident) {  // the row's entries outside the windows, then the epilogue
+        if (slot < nr) {
+          const int k = static_cast<int>(perm[slot]);
+          const Op rest = op.with_views(sv.rest1, sv.rest2);
+          const Gather gl[2] = {Gather{rest.gather_src(0), nullptr, 0, 0u}, Gather{rest.gather_src(1), nullptr, 0, 0u}};
+          typename Op::AccT a;
+          a.zero();
+          rest.template accumulate<kUnroll>(k, 0, rest.len(k), 0, 1, a, gl);
+          if (sv.seg == 0) a.v[0] += part;
+          else a.v[Op::AccT::kK - 1] += part;
+          op.finish(r, a, pre);
+        }
+      } else if (slot < nr) {
+        partial[perm[slot]] = part;
+      }
     }
     deal = (deal + nsl) % kSlabConsumers;
     __syncwarp();
@@ -435,6 +473,11 @@ __global__ void __launch_bounds__(kBlock) slab_finish_kernel(const Op op, const 
 #ifdef RB_SLAB_PROFILE
     if (threadIdx.x == 0 && sv.fprof) atomicMax(&sv.fprof[0], slab_now());
 #endif
+    return;
+  }
+  if (sv.resident) {  // W rows finished in the slab kernel: one block only waits for it, so
+    // this grid completes after the slab grid (the next step's wait is transitive)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     return;
   }
   // last: the W rows, whose blocks wait for the slab grid. The epilogue
@@ -568,7 +611,7 @@ inline int launch_slab_phase(const Op& op, const SlabPhase& ph, cudaStream_t st,
     RB_CUDA(cudaLaunchKernelEx(&cfg, slab_kernel<Op>, op, sv));
   }
   const SchedView& o = ph.others.view;
-  const int wblocks = static_cast<int>(ceil_div(sv.nw, sv.S >= kSlabGroupedS ? 32 : kBlock));
+  const int wblocks = sv.resident ? 1 : static_cast<int>(ceil_div(sv.nw, sv.S >= kSlabGroupedS ? 32 : kBlock));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(wblocks + (o.total_blocks > 0 ? o.total_blocks : 0)));
   cfg.blockDim = dim3(kBlock);

@@ -282,9 +282,14 @@ SlabChoice choose_slabs(const int32_t* rp, const int32_t* ci, int32_t rows, int6
   return ch;
 }
 
+// Off by default (RAPDHG_SLAB_RESIDENT=1 enables): measured slower — one
+// 174 KB CTA per SM holds only a few slices in flight, and each lane's
+// in-kernel epilogue (row id, rest CSR chain, gather, epilogue inputs) is a
+// chain of dependent global loads: C4's dual took 320 us against 134 us
+// windowed (ncu: 14% warps active, long_scoreboard), C3's primal 82 vs 68 us.
 bool slab_resident(const SlabChoice& choice) {
   const char* e = std::getenv("RAPDHG_SLAB_RESIDENT");
-  if (e && e[0] == '0') return false;
+  if (!(e && e[0] == '1')) return false;
   const int S = static_cast<int>(choice.windows.size());
   return S > 0 && S <= kSlabResidentMax && S * choice.width <= 65536;  // 16-bit offsets into the image
 }

@@ -157,11 +157,13 @@ def test_pdl_schedule_matches_serialised(monkeypatch):
 
 
 def test_resident_plan_on_c4_svm_dual(monkeypatch):
-    """The C4 dual (5 windows over the 1e4 feature columns) runs resident by
-    itself; at 1/10 scale both modes stay within 1e-12 of each other over 200
-    iterations, and resident repeats bit for bit."""
+    """The C4 dual (5 windows over the 1e4 feature columns) qualifies for a
+    resident plan (opt-in, RAPDHG_SLAB_RESIDENT=1); at 1/10 scale both modes
+    stay within 1e-12 of each other over 200 iterations, and resident repeats
+    bit for bit."""
     p = rb.generate(rb.Gen.SVM, 0.1, 4)
     cfg = rb.SolverConfig(tol=1e-12, max_iters=200, snapshot_interval=40)
+    monkeypatch.setenv("RAPDHG_SLAB_RESIDENT", "1")
     a = rb.solve(p, cfg)
     monkeypatch.setenv("RAPDHG_SLAB_RESIDENT", "0")
     b = rb.solve(p, cfg)

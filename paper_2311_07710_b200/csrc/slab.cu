@@ -4,12 +4,16 @@
 #include <functional>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <numeric>
 #include <string>
 #include <thread>
 #include <vector>
 
+#include <cub/device/device_scan.cuh>
+
 #include "slab.cuh"
+#include "slab_layout.hpp"
 
 namespace rb {
 
@@ -105,31 +109,61 @@ __global__ void seg_counts_kernel(const int32_t* rows, int32_t nw, const int32_t
   rest_o[k] = rp_o ? rp_o[r + 1] - rp_o[r] : 0;
 }
 
-// thread per W row: scatter its entries into its slice lane (run (s, k): tile
-// base off[s * nw + k]; jx = (index of its slice's jagged offsets in joff) *
-// 32 + lane; entry e at base + joff[jx / 32 + e] + lane) and into the rest CSRs
-__global__ void fill_kernel(const int32_t* rows, int32_t nw, const int32_t* rp_w, const int32_t* ci_w,
-                            const int32_t* rp_o, const int32_t* ci_o, Wins wins, const int32_t* off,
-                            const int32_t* jx, const int32_t* joff, uint16_t* col, int32_t* pos,
-                            const int32_t* rrp_w, int32_t* rci_w, int32_t* rpos_w, const int32_t* rrp_o,
-                            int32_t* rci_o, int32_t* rpos_o) {
+// block per tile, thread per slot: the slot's W row k (perm) has its run in
+// the tile's window (resident plans: all its in-window entries) as entries
+// e = 0 .. len-1, placed at tile base + soff[slice] + 32 e + lane (the
+// layout of slab_layout.cpp); padding keeps col 0 / pos -1 from the memsets.
+__global__ void tile_fill_kernel(const SlabTile* tiles, const uint16_t* meta, const int32_t* rows,
+                                 const int32_t* rp_w, const int32_t* ci_w, Wins wins, uint16_t* col, int32_t* pos) {
+  const SlabTile d = tiles[blockIdx.x];
+  const uint16_t* m = meta + d.meta;
+  const uint32_t* perm = reinterpret_cast<const uint32_t*>(m);
+  const uint16_t* len = m + 2 * d.nr;
+  const uint16_t* soff = len + d.nr;
+  for (int slot = threadIdx.x; slot < d.nr; slot += blockDim.x) {
+    const int32_t k = static_cast<int32_t>(perm[slot]);
+    const int L = len[slot];
+    const int64_t base = static_cast<int64_t>(d.a) + soff[slot >> 5] + (slot & 31);
+    const int r = rows[k];
+    const int b = rp_w[r], e = rp_w[r + 1];
+    if (wins.stride) {  // resident: every in-window entry, in column order
+      int q = 0;
+      for (int p = b; p < e && q < L; ++p) {
+        const int w = wins.of(ci_w[p]);
+        if (w < 0) continue;
+        col[base + 32 * static_cast<int64_t>(q)] = wins.offset(w, ci_w[p]);
+        pos[base + 32 * static_cast<int64_t>(q)] = p;
+        ++q;
+      }
+    } else {  // the window's run: a contiguous range of the column-sorted row
+      const Window w = wins.w[d.s];
+      int lo = b, hi = e;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (ci_w[mid] < w.lo) lo = mid + 1;
+        else hi = mid;
+      }
+      for (int q = 0; q < L; ++q) {
+        col[base + 32 * static_cast<int64_t>(q)] = static_cast<uint16_t>(ci_w[lo + q] - w.lo);
+        pos[base + 32 * static_cast<int64_t>(q)] = lo + q;
+      }
+    }
+  }
+}
+
+// thread per W row: its entries outside the windows (and its other segment)
+// into the rest CSRs
+__global__ void rest_fill_kernel(const int32_t* rows, int32_t nw, const int32_t* rp_w, const int32_t* ci_w,
+                                 const int32_t* rp_o, const int32_t* ci_o, Wins wins, const int32_t* rrp_w,
+                                 int32_t* rci_w, int32_t* rpos_w, const int32_t* rrp_o, int32_t* rci_o,
+                                 int32_t* rpos_o) {
   const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (k >= nw) return;
   const int r = rows[k];
-  int cur = -1, e = 0;
   int rw = rrp_w[k];
   for (int p = rp_w[r]; p < rp_w[r + 1]; ++p) {
     const int32_t c = ci_w[p];
-    const int w = wins.of(c);
-    if (w >= 0) {
-      const int s = wins.run(w);
-      if (s != cur) cur = s, e = 0;
-      const int64_t run = static_cast<int64_t>(s) * nw + k;
-      const int64_t wp = off[run] + joff[(jx[run] >> 5) + e] + (jx[run] & 31);
-      col[wp] = wins.offset(w, c);
-      pos[wp] = p;
-      ++e;
-    } else {
+    if (wins.of(c) < 0) {
       rci_w[rw] = c;
       rpos_w[rw] = p;
       ++rw;
@@ -142,6 +176,22 @@ __global__ void fill_kernel(const int32_t* rows, int32_t nw, const int32_t* rp_w
       rpos_o[ro] = p;
     }
   }
+}
+
+// exclusive scan of n counts into n + 1 offsets on the device; returns the total
+int32_t scan_dev(const int32_t* cnt, int32_t n, DevBuf<int32_t>& off, cudaStream_t st) {
+  off.alloc(static_cast<std::size_t>(n) + 1);
+  off.zero(st);
+  if (n > 0) {
+    std::size_t tb = 0;
+    RB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, cnt, off.get() + 1, n, st));
+    DevBuf<unsigned char> tmp(tb);
+    RB_CUDA(cub::DeviceScan::InclusiveSum(tmp.get(), tb, cnt, off.get() + 1, n, st));
+  }
+  int32_t tot = 0;
+  RB_CUDA(cudaMemcpyAsync(&tot, off.get() + n, sizeof(tot), cudaMemcpyDeviceToHost, st));
+  RB_CUDA(cudaStreamSynchronize(st));
+  return tot;
 }
 
 __global__ void gather_kernel(double* dst, const double* src, const int32_t* pos, int64_t n) {
@@ -168,72 +218,6 @@ std::vector<T> download(const DevBuf<T>& d, int64_t n, cudaStream_t st) {
   if (n > 0) RB_CUDA(cudaMemcpyAsync(h.data(), d.get(), sizeof(T) * n, cudaMemcpyDeviceToHost, st));
   RB_CUDA(cudaStreamSynchronize(st));
   return h;
-}
-
-std::vector<int32_t> scan_host(const std::vector<int32_t>& cnt) {
-  std::vector<int32_t> rp(cnt.size() + 1, 0);
-  for (std::size_t i = 0; i < cnt.size(); ++i) rp[i + 1] = rp[i] + cnt[i];
-  return rp;
-}
-
-// One tile: W rows (indices k, runs already sorted by length, descending),
-// 32 per slice, each slice as wide as its longest run (the per-window sort
-// makes slices nearly uniform). meta (uint16) = perm (uint32 row index k per
-// slot, 2 elements each) | len[nr] | soff[nsl + 1]; joff = per slice the start
-// of each entry e (fill_kernel only); offsets relative to the tile's first
-// entry.
-struct TileLayout {
-  std::vector<int32_t> rows;  // the tile's W rows in slot order
-  std::vector<uint16_t> meta;
-  std::vector<int32_t> joff;  // slice q's offsets start at joff[sj[q]]
-  std::vector<int32_t> sj;
-  int32_t n = 0;
-};
-TileLayout layout_tile(const int32_t* rows, const int32_t* len, int32_t nr) {
-  TileLayout L;
-  const int nsl = (nr + 31) / 32;
-  L.meta.resize(3 * static_cast<std::size_t>(nr) + nsl + 1);
-  for (int32_t i = 0; i < nr; ++i) {
-    L.meta[2 * i] = static_cast<uint16_t>(static_cast<uint32_t>(rows[i]) & 0xffffu);
-    L.meta[2 * i + 1] = static_cast<uint16_t>(static_cast<uint32_t>(rows[i]) >> 16);
-    L.meta[2 * nr + i] = static_cast<uint16_t>(len[i]);
-  }
-  int64_t cur = 0;
-  for (int q = 0; q < nsl; ++q) {
-    L.meta[3 * nr + q] = static_cast<uint16_t>(cur);  // soff[q]
-    L.sj.push_back(static_cast<int32_t>(L.joff.size()));
-    const int Lm = len[32 * q];
-    for (int e = 0; e < Lm; ++e) L.joff.push_back(static_cast<int32_t>(cur + 32 * e));
-    cur += 32 * static_cast<int64_t>(Lm);
-  }
-  L.meta[3 * nr + nsl] = static_cast<uint16_t>(cur);
-  L.n = static_cast<int32_t>(cur);  // a multiple of 32
-  return L;
-}
-
-// f(0 .. n-1) on host threads: half the cores by default, as the two ops'
-// plans are built concurrently (RAPDHG_PLAN_THREADS overrides)
-int plan_threads() {
-  static const int t = [] {
-    const char* e = std::getenv("RAPDHG_PLAN_THREADS");
-    const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
-    return std::max(1, std::min(32, e ? std::atoi(e) : std::max(1, hw / 2)));
-  }();
-  return t;
-}
-template <class F>
-void parallel_for(int64_t n, const F& f) {
-  const int T = static_cast<int>(std::min<int64_t>(n, plan_threads()));
-  if (T <= 1) {
-    for (int64_t i = 0; i < n; ++i) f(i);
-    return;
-  }
-  std::vector<std::thread> th;
-  for (int t = 0; t < T; ++t)
-    th.emplace_back([&, t] {
-      for (int64_t i = t; i < n; i += T) f(i);
-    });
-  for (auto& x : th) x.join();
 }
 
 }  // namespace
@@ -351,208 +335,46 @@ void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const in
   c2.zero(st);
   seg_counts_kernel<<<g1(nw), 256, 0, st>>>(plan.rows.get(), nw, rp_w, ci_w, rp_o, wins, c2.get(), rw.get(), ro.get());
   RB_LAUNCH_CHECK();
-  const std::vector<int32_t> hc2 = download(c2, runs, st), hrw = download(rw, nw, st), hro = download(ro, nw, st);
+  PinnedBuf<int32_t> hc2;  // the run lengths, for the host layout
+  hc2.alloc(static_cast<std::size_t>(runs));
+  RB_CUDA(cudaMemcpyAsync(hc2.get(), c2.get(), sizeof(int32_t) * runs, cudaMemcpyDeviceToHost, st));
+  RB_CUDA(cudaStreamSynchronize(st));
   tr.mark("    counts");
-  // Tiles, per window, of whole 32-row slices (slice-padded entries within
-  // the stage, rows within the row cap), from one of two row orders:
-  //  * natural: the window's W rows in index order, each tile's rows sorted
-  //    by run length — neighbouring rows share tiles, so partial writes and
-  //    the finish pass stay coalesced;
-  //  * sorted: all the window's W rows sorted by run length first — slices of
-  //    nearly equal runs, no padding, but scattered partial writes.
-  // Natural unless its padding exceeds kSlabNaturalPad (RAPDHG_SLAB_ORDER=
-  // natural|sorted forces). Rows with an empty run in a window appear in none
-  // of its tiles (their partial stays the zero written at setup).
+  // tiles, slot orders and metadata (slab_layout.cpp)
   const int ecap = (std::min(32736, std::max(256, env_int("RAPDHG_SLAB_TILE", kSlabTileCap))) + 31) & ~31;
-  const int rcap = kSlabRowCap;
-  struct TileSpan {
-    int s;
-    int32_t b, e;  // range of order[s]
-  };
-  auto build = [&](bool sorted, std::vector<std::vector<int32_t>>& order, std::vector<TileSpan>& spans,
-                   std::vector<TileLayout>& lay) {
-    order.assign(S, {});
-    parallel_for(S, [&](int64_t si) {
-      const int s = static_cast<int>(si);
-      const int32_t* len = hc2.data() + static_cast<int64_t>(s) * nw;
-      std::vector<int32_t> o;
-      o.reserve(nw);
-      if (sorted) {
-        std::vector<int32_t> start(kSlabRunCap + 2, 0);
-        for (int32_t k = 0; k < nw; ++k) ++start[kSlabRunCap - len[k] + 1];
-        for (int v = 1; v <= kSlabRunCap + 1; ++v) start[v] += start[v - 1];
-        o.resize(nw);
-        for (int32_t k = 0; k < nw; ++k) o[start[kSlabRunCap - len[k]]++] = k;
-        int32_t cnt = nw;
-        while (cnt > 0 && len[o[cnt - 1]] == 0) --cnt;  // empty runs last
-        o.resize(cnt);
-      } else {
-        for (int32_t k = 0; k < nw; ++k)
-          if (len[k] > 0) o.push_back(k);
-      }
-      order[s] = std::move(o);
-    });
-    tr.mark("    row orders");
-    spans.clear();
-    for (int s = 0; s < S; ++s) {
-      const std::vector<int32_t>& o = order[s];
-      const int32_t* len = hc2.data() + static_cast<int64_t>(s) * nw;
-      const int32_t no = static_cast<int32_t>(o.size());
-      int32_t b = 0;
-      int64_t acc = 0;
-      for (int32_t q = 0; q < no; q += 32) {  // group of 32 rows starting at q
-        const int32_t qe = std::min(no, q + 32);
-        int64_t w = 0;  // sorted: the slice's padded width; natural: raw entries (7/8 budget below)
-        if (sorted) w = 32 * static_cast<int64_t>(len[o[q]]);
-        else
-          for (int32_t i = q; i < qe; ++i) w += len[o[i]];
-        const int64_t cap = sorted ? ecap : ecap * 7 / 8;
-        if (q > b && (acc + w > cap || qe - b > rcap)) {
-          spans.push_back({s, b, q});
-          b = q;
-          acc = 0;
-        }
-        acc += w;
-      }
-      if (b < no) spans.push_back({s, b, no});
-    }
-    tr.mark("    spans");
-    for (;;) {  // lay out (rows of a tile sorted by run); split tiles that overflow
-      lay.assign(spans.size(), TileLayout{});
-      parallel_for(static_cast<int64_t>(spans.size()), [&](int64_t t) {
-        const TileSpan& sp = spans[t];
-        const int32_t* len = hc2.data() + static_cast<int64_t>(sp.s) * nw;
-        std::vector<int32_t> rows_t(order[sp.s].begin() + sp.b, order[sp.s].begin() + sp.e);
-        std::stable_sort(rows_t.begin(), rows_t.end(), [&](int32_t x, int32_t y) { return len[x] > len[y]; });
-        std::vector<int32_t> len_t(rows_t.size());
-        for (std::size_t i = 0; i < rows_t.size(); ++i) len_t[i] = len[rows_t[i]];
-        lay[t] = layout_tile(rows_t.data(), len_t.data(), static_cast<int32_t>(rows_t.size()));
-        lay[t].rows = std::move(rows_t);
-      });
-      std::vector<TileSpan> next;
-      bool split = false;
-      for (std::size_t t = 0; t < spans.size(); ++t) {
-        const TileSpan& sp = spans[t];
-        if (lay[t].n > ecap && sp.e - sp.b > 32) {
-          const int32_t mid = sp.b + std::max<int32_t>(32, ((sp.e - sp.b) / 2) & ~31);
-          next.push_back({sp.s, sp.b, mid});
-          next.push_back({sp.s, mid, sp.e});
-          split = true;
-        } else {
-          next.push_back(sp);
-        }
-      }
-      if (!split) break;
-      spans.swap(next);
-    }
-  };
-  std::vector<std::vector<int32_t>> order;
-  std::vector<TileSpan> spans;
-  std::vector<TileLayout> lay;
-  bool sorted = false;
-  {
-    const char* mode = std::getenv("RAPDHG_SLAB_ORDER");
-    if (mode) {
-      sorted = std::string(mode) == "sorted";
-    } else {
-      // natural unless it pads too much: the padding of natural tiles from the
-      // run lengths alone (each tile's runs sorted, 32-row slices)
-      int64_t padded = 0, actual = 0;
-      for (int32_t c : hc2) actual += c;
-      std::vector<int64_t> pad_w(S, 0);
-      parallel_for(S, [&](int64_t si) {
-        const int32_t* len = hc2.data() + si * nw;
-        std::vector<int32_t> buf;
-        int64_t raw = 0, pad = 0;
-        auto flush = [&] {
-          std::sort(buf.begin(), buf.end(), std::greater<int32_t>());
-          for (std::size_t q = 0; q < buf.size(); q += 32) pad += 32 * static_cast<int64_t>(buf[q]);
-          buf.clear();
-          raw = 0;
-        };
-        for (int32_t k = 0; k < nw; ++k) {
-          if (len[k] == 0) continue;
-          if (buf.size() % 32 == 0 && !buf.empty() &&
-              (raw + len[k] > ecap * 7 / 8 || static_cast<int>(buf.size()) + 1 > rcap))
-            flush();
-          buf.push_back(len[k]);
-          raw += len[k];
-        }
-        flush();
-        pad_w[si] = pad;
-      });
-      for (int64_t v : pad_w) padded += v;
-      sorted = static_cast<double>(padded) > kSlabNaturalPad * static_cast<double>(std::max<int64_t>(actual, 1));
-    }
-    tr.mark("    padding estimate");
-    build(sorted, order, spans, lay);
-  }
-  const int32_t ntiles = static_cast<int32_t>(spans.size());
-  tr.mark("    tiles + layouts");
-  // tile arrays: window-major, each tile 32-entry aligned; run (s, k): tile
-  // base off[s * nw + k] and jx[s * nw + k] (see fill_kernel)
-  std::vector<int32_t> off(runs, 0), jx(runs, 0);
-  std::vector<SlabTile> tiles(ntiles);
-  const int64_t row_cost = env_int("RAPDHG_SLAB_ROWCOST", kSlabRowCost);
-  std::vector<int64_t> joff_at(ntiles + 1, 0), meta_at(ntiles + 1, 0);
-  int64_t cursor = 0;
-  int max_tile = 0, max_meta = 0;
-  plan.tile_bytes.resize(ntiles);
-  for (int32_t t = 0; t < ntiles; ++t) {  // offsets (sequential prefix)
-    const TileSpan& sp = spans[t];
-    const TileLayout& L = lay[t];
-    SlabTile& d = tiles[t];
-    d.a = static_cast<int32_t>(cursor);
-    d.n = L.n;
-    d.meta = static_cast<int32_t>(meta_at[t]);
-    d.k0 = 0;
-    d.nr = sp.e - sp.b;
-    d.s = sp.s;
-    d.m = static_cast<int32_t>(L.meta.size());
-    max_tile = std::max(max_tile, d.n);
-    max_meta = std::max(max_meta, d.m);
-    // cost for balancing the CTAs' contiguous ranges: staged bytes, per-row
-    // work (length/perm loads, the partial store), a fixed per-tile cost
-    plan.tile_bytes[t] = 10 * static_cast<int64_t>(d.n) + 2 * static_cast<int64_t>(d.m) +
-                         row_cost * static_cast<int64_t>(d.nr) + 16384;
-    joff_at[t + 1] = joff_at[t] + static_cast<int64_t>(L.joff.size());
-    meta_at[t + 1] = meta_at[t] + ((static_cast<int64_t>(L.meta.size()) + 7) & ~int64_t{7});
-    cursor += d.n;
-  }
-  std::vector<int32_t> joff(joff_at[ntiles]);
-  std::vector<uint16_t> meta(meta_at[ntiles], 0);
-  parallel_for(ntiles, [&](int64_t t) {  // contents (disjoint per tile)
-    const TileSpan& sp = spans[t];
-    const TileLayout& L = lay[t];
-    const int32_t n_r = sp.e - sp.b;
-    for (int32_t slot = 0; slot < n_r; ++slot) {
-      const int64_t run = static_cast<int64_t>(sp.s) * nw + L.rows[slot];
-      off[run] = tiles[t].a;
-      jx[run] = static_cast<int32_t>((joff_at[t] + L.sj[slot / 32]) * 32 + slot % 32);
-    }
-    std::copy(L.joff.begin(), L.joff.end(), joff.begin() + joff_at[t]);
-    std::copy(L.meta.begin(), L.meta.end(), meta.begin() + meta_at[t]);
-  });
-  if (cursor > INT32_MAX || max_tile > ecap || max_meta > kSlabMetaCap ||
-      static_cast<int64_t>(joff.size()) * 32 > INT32_MAX) {  // int32 offsets; tiles must fit a stage
+  int order_mode = 0;
+  if (const char* mode = std::getenv("RAPDHG_SLAB_ORDER")) order_mode = std::string(mode) == "sorted" ? 2 : 1;
+  SlabLayout lay;
+  const bool fits = slab_layout(hc2.get(), nw, S, ecap, kSlabRowCap, order_mode,
+                                env_int("RAPDHG_SLAB_ROWCOST", kSlabRowCost), lay);
+  tr.mark("    layout (host)");
+  if (!fits || lay.max_tile > ecap || lay.max_meta > kSlabMetaCap) {  // int32 offsets; tiles must fit a stage
     plan = SlabPlan{};
     return;
   }
-  tr.mark("    tile arrays");
-  meta.resize(meta.size() + 8, 0);  // slack: a tile's metadata copy rounds up to 8
+  const int32_t ntiles = static_cast<int32_t>(lay.tiles.size());
+  const int64_t cursor = lay.entries;
+  const bool sorted = lay.sorted;
+  plan.tile_bytes = lay.tile_bytes;
   const int64_t total = std::max<int64_t>(cursor, 32);
-  DevBuf<int32_t> doff(runs), djx(runs), djoff(joff.size());
-  doff.upload(off.data(), runs, st);
-  djx.upload(jx.data(), runs, st);
-  djoff.upload(joff.data(), joff.size(), st);
-  plan.tile.alloc(tiles.size());
-  plan.tile.upload(tiles.data(), tiles.size(), st);
-  plan.meta.alloc(meta.size());
-  plan.meta.upload(meta.data(), meta.size(), st);
-  plan.col.alloc(total), plan.pos.alloc(total), plan.val.alloc(total);
-  RB_CUDA(cudaMemsetAsync(plan.col.get(), 0, sizeof(uint16_t) * total, st));
-  RB_CUDA(cudaMemsetAsync(plan.pos.get(), 0xff, sizeof(int32_t) * total, st));  // padding: pos -1 -> 0.0
-  const std::vector<int32_t> rrw = scan_host(hrw), rro = scan_host(hro);
+  {
+    PinnedBuf<uint16_t> hm;  // pinned staging of the metadata (tens of MB on the large configs)
+    hm.alloc(lay.meta.size());
+    std::memcpy(hm.get(), lay.meta.data(), sizeof(uint16_t) * lay.meta.size());
+    plan.meta.alloc(lay.meta.size());
+    plan.meta.upload(hm.get(), lay.meta.size(), st);
+    plan.tile.alloc(lay.tiles.size());
+    plan.tile.upload(lay.tiles.data(), lay.tiles.size(), st);
+    plan.col.alloc(total), plan.pos.alloc(total), plan.val.alloc(total);
+    RB_CUDA(cudaMemsetAsync(plan.col.get(), 0, sizeof(uint16_t) * total, st));
+    RB_CUDA(cudaMemsetAsync(plan.pos.get(), 0xff, sizeof(int32_t) * total, st));  // padding: pos -1 -> 0.0
+    if (ntiles)
+      tile_fill_kernel<<<static_cast<unsigned>(ntiles), 256, 0, st>>>(plan.tile.get(), plan.meta.get(),
+                                                                      plan.rows.get(), rp_w, ci_w, wins,
+                                                                      plan.col.get(), plan.pos.get());
+    RB_LAUNCH_CHECK();
+    RB_CUDA(cudaStreamSynchronize(st));  // the pinned staging is released below
+  }
   // rest CSRs keep the op's segment order: rest1 = segment 1, rest2 = segment 2
   DevBuf<int32_t>& rrp_w = seg == 0 ? plan.rrp1 : plan.rrp2;
   DevBuf<int32_t>& rci_w = seg == 0 ? plan.rci1 : plan.rci2;
@@ -560,15 +382,13 @@ void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const in
   DevBuf<int32_t>& rrp_o = seg == 0 ? plan.rrp2 : plan.rrp1;
   DevBuf<int32_t>& rci_o = seg == 0 ? plan.rci2 : plan.rci1;
   DevBuf<int32_t>& rpos_o = seg == 0 ? plan.rpos2 : plan.rpos1;
-  rrp_w.alloc(nw + 1), rrp_o.alloc(nw + 1);
-  rrp_w.upload(rrw.data(), nw + 1, st);
-  rrp_o.upload(rro.data(), nw + 1, st);
-  rci_w.alloc(rrw[nw]), rpos_w.alloc(rrw[nw]), rci_o.alloc(rro[nw]), rpos_o.alloc(rro[nw]);
-  (seg == 0 ? plan.rval1 : plan.rval2).alloc(rrw[nw]);
-  (seg == 0 ? plan.rval2 : plan.rval1).alloc(rro[nw]);
-  fill_kernel<<<g1(nw), 256, 0, st>>>(plan.rows.get(), nw, rp_w, ci_w, rp_o, ci_o, wins, doff.get(), djx.get(),
-                                      djoff.get(), plan.col.get(), plan.pos.get(), rrp_w.get(), rci_w.get(), rpos_w.get(),
-                                      rp_o ? rrp_o.get() : nullptr, rci_o.get(), rpos_o.get());
+  const int32_t nrw = scan_dev(rw.get(), nw, rrp_w, st), nro = scan_dev(ro.get(), nw, rrp_o, st);
+  rci_w.alloc(nrw), rpos_w.alloc(nrw), rci_o.alloc(nro), rpos_o.alloc(nro);
+  (seg == 0 ? plan.rval1 : plan.rval2).alloc(nrw);
+  (seg == 0 ? plan.rval2 : plan.rval1).alloc(nro);
+  rest_fill_kernel<<<g1(nw), 256, 0, st>>>(plan.rows.get(), nw, rp_w, ci_w, rp_o, ci_o, wins, rrp_w.get(),
+                                           rci_w.get(), rpos_w.get(), rp_o ? rrp_o.get() : nullptr, rci_o.get(),
+                                           rpos_o.get());
   RB_LAUNCH_CHECK();
   tr.mark("    upload + fill");
   plan.partial.alloc(runs);
@@ -608,7 +428,7 @@ void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const in
                  seg, r0, r1, nw, nwin, resident ? " (resident)" : "", ntiles, ntiles, static_cast<long long>(cursor),
                  static_cast<double>(cursor) / std::max<int64_t>(1, [&] {
                    int64_t t = 0;
-                   for (int32_t c : hc2) t += c;
+                   for (int64_t q = 0; q < runs; ++q) t += hc2[q];
                    return t;
                  }()),
                  sorted ? "sorted" : "natural");

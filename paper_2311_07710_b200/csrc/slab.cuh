@@ -38,6 +38,7 @@
 #include <vector>
 
 #include "ops.cuh"
+#include "slab_layout.hpp"
 
 namespace rb {
 
@@ -57,18 +58,8 @@ constexpr int kSlabMinWindows = 1;     // RAPDHG_SLAB_MIN_WINDOWS overrides
 constexpr int kSlabResidentMax = 8;    // resident plans: at most this many windows (128 KB) staged at once
 constexpr int kSlabProf = 10;           // per-CTA profile slots (RB_SLAB_PROFILE)
 
-// tile t = s * J + j (window-major: a CTA's contiguous tile range mostly
-// shares one window, staged once)
-struct SlabTile {
-  int32_t a;     // first entry (8-aligned)
-  int32_t n;     // entries (multiple of 8; jagged slices carry no padding)
-  int32_t meta;  // first metadata element in SlabView::meta (8-aligned)
-  int32_t k0;    // first W row of the chunk
-  int32_t nr;    // rows of the chunk
-  int32_t s;     // window
-  int32_t m;     // metadata elements
-  int32_t pad;
-};
+// SlabTile (slab_layout.hpp): tile t, window-major (a CTA's contiguous tile
+// range mostly shares one window, staged once)
 
 // Per-tile metadata (uint16 elements): perm (uint32 W-row index per slot, 2
 // elements each) | len[nr] (run length per slot) | soff[nsl + 1] (slice

@@ -160,7 +160,7 @@ void fill_colblock_values(ColBlocks& cb, const double* vals, cudaStream_t st) {
 }
 
 void build_colblocked_dual(ColBlockedDual& d, int nb, const int32_t* rp, const int32_t* ci, int32_t rows,
-                           int32_t ncols, const double* vals, cudaStream_t st) {
+                           int32_t ncols, const double* vals, bool sell, cudaStream_t st) {
   d = ColBlockedDual{};
   if (nb < 2 || rows <= 0) return;
   d.rows = rows;
@@ -173,12 +173,20 @@ void build_colblocked_dual(ColBlockedDual& d, int nb, const int32_t* rp, const i
     row_lengths(len, d.cb.blk[b].rp.get(), nullptr, rows, st);
     build_schedule(d.sch[b], len.get(), rows, false, st);
   }
+  if (sell) {
+    d.sell.resize(nb);
+    for (int b = 0; b < nb; ++b) {
+      const DevCsr& m = d.cb.blk[b];
+      build_sell_plan(d.sell[b], m.rp.get(), m.ci.get(), nullptr, nullptr, rows, st);
+      fill_sell_values(d.sell[b], m.v.get(), nullptr, st);
+    }
+  }
   RB_CUDA(cudaStreamSynchronize(st));
 }
 
 void build_colblocked_primal(ColBlockedPrimal& p, int nq, int na, const int32_t* rpq, const int32_t* ciq,
                              const double* qvals, const int32_t* rpat, const int32_t* ciat, const double* atvals,
-                             int32_t rows, int32_t n, int32_t m, cudaStream_t st) {
+                             int32_t rows, int32_t n, int32_t m, bool sell, cudaStream_t st) {
   p = ColBlockedPrimal{};
   if ((nq < 2 && na < 2) || rows <= 0) return;
   p.on = true;
@@ -212,9 +220,35 @@ void build_colblocked_primal(ColBlockedPrimal& p, int nq, int na, const int32_t*
     p.zero_rp.alloc(static_cast<std::size_t>(rows) + 1);
     p.zero_rp.zero(st);
   }
-  row_lengths(len, nq >= 2 ? p.q.blk[nq - 1].rp.get() : rpq,
-              p.at_all_partial ? p.zero_rp.get() : na >= 2 ? p.at.blk[na - 1].rp.get() : rpat, rows, st);
+  const int32_t* fin_rpq = nq >= 2 ? p.q.blk[nq - 1].rp.get() : rpq;
+  const int32_t* fin_rpat = p.at_all_partial ? p.zero_rp.get() : na >= 2 ? p.at.blk[na - 1].rp.get() : rpat;
+  row_lengths(len, fin_rpq, fin_rpat, rows, st);
   build_schedule(p.fin, len.get(), rows, false, st);
+  if (sell) {
+    p.sell_q.resize(p.sch_q.size());
+    for (std::size_t b = 0; b < p.sch_q.size(); ++b) {
+      const DevCsr& mq = p.q.blk[b];
+      build_sell_plan(p.sell_q[b], mq.rp.get(), mq.ci.get(), nullptr, nullptr, rows, st);
+      fill_sell_values(p.sell_q[b], mq.v.get(), nullptr, st);
+    }
+    p.sell_at.resize(p.sch_at.size());
+    for (std::size_t b = 0; b < p.sch_at.size(); ++b) {
+      if (na >= 2) {
+        const DevCsr& ma = p.at.blk[b];
+        build_sell_plan(p.sell_at[b], ma.rp.get(), ma.ci.get(), nullptr, nullptr, rows, st);
+        fill_sell_values(p.sell_at[b], ma.v.get(), nullptr, st);
+      } else {
+        build_sell_plan(p.sell_at[b], rpat, ciat, nullptr, nullptr, rows, st);
+        fill_sell_values(p.sell_at[b], atvals, nullptr, st);
+      }
+    }
+    const int32_t* fin_ciq = nq >= 2 ? p.q.blk[nq - 1].ci.get() : ciq;
+    const double* fin_vq = nq >= 2 ? p.q.blk[nq - 1].v.get() : qvals;
+    const int32_t* fin_ciat = na >= 2 && !p.at_all_partial ? p.at.blk[na - 1].ci.get() : ciat;
+    const double* fin_vat = na >= 2 && !p.at_all_partial ? p.at.blk[na - 1].v.get() : atvals;
+    build_sell_plan(p.sell_fin, fin_rpq, fin_ciq, fin_rpat, fin_ciat, rows, st);
+    fill_sell_values(p.sell_fin, fin_vq, fin_vat, st);
+  }
   RB_CUDA(cudaStreamSynchronize(st));
 }
 

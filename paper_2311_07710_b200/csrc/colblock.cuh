@@ -24,6 +24,7 @@
 #include "device_csr.cuh"
 #include "ops.cuh"
 #include "rowwise.cuh"
+#include "sell.cuh"
 
 namespace rb {
 
@@ -103,25 +104,29 @@ struct ColBlockedDual {
   ColBlocks cb;
   DevBuf<double> part;
   std::vector<Schedule> sch;
+  std::vector<SellPlan> sell;  // per block, when the op's rows are short (sell.cuh)
   int64_t rows = 0;
   bool active() const { return cb.active(); }
 };
 void build_colblocked_dual(ColBlockedDual& d, int nb, const int32_t* rp, const int32_t* ci, int32_t rows,
-                           int32_t ncols, const double* vals, cudaStream_t st);
+                           int32_t ncols, const double* vals, bool sell, cudaStream_t st);
 
 // `op`: the step op over the same rows with the unblocked views. Returns kernels launched.
 inline int launch_colblocked_dual(const DualStepOp<false>& op, const ColBlockedDual& d, cudaStream_t st) {
   const int nb = d.cb.nb;
+  const bool sell = !d.sell.empty();
   int n = 0;
   for (int b = 0; b + 1 < nb; ++b) {
     const SpmvOp<false> sp{d.cb.blk[b].view(), op.w, d.part.get() + static_cast<int64_t>(b) * d.rows};
-    launch_rowwise(sp, d.sch[b].view, st);
+    if (sell) launch_sell(sp, d.sell[b], st);
+    else launch_rowwise(sp, d.sch[b].view, st);
     ++n;
   }
   DualStepOp<false> last = op;
   last.a = d.cb.blk[nb - 1].view();
-  launch_rowwise(PartialsOp<DualStepOp<false>>{last, d.part.get(), nullptr, nb - 1, 0, d.rows}, d.sch[nb - 1].view,
-                 st);
+  const PartialsOp<DualStepOp<false>> fin{last, d.part.get(), nullptr, nb - 1, 0, d.rows};
+  if (sell) launch_sell(fin, d.sell[nb - 1], st);
+  else launch_rowwise(fin, d.sch[nb - 1].view, st);
   return n + 1;
 }
 
@@ -134,6 +139,8 @@ struct ColBlockedPrimal {
   DevBuf<double> part_q, part_at;
   std::vector<Schedule> sch_q, sch_at;  // partial passes
   Schedule fin;
+  std::vector<SellPlan> sell_q, sell_at;  // partial passes (when the op's rows are short)
+  SellPlan sell_fin;
   bool at_all_partial = false;
   DevBuf<int32_t> zero_rp;  // empty rows for an all-partial A'
   int64_t rows = 0;
@@ -142,29 +149,33 @@ struct ColBlockedPrimal {
 };
 void build_colblocked_primal(ColBlockedPrimal& p, int nq, int na, const int32_t* rpq, const int32_t* ciq,
                              const double* qvals, const int32_t* rpat, const int32_t* ciat, const double* atvals,
-                             int32_t rows, int32_t n, int32_t m, cudaStream_t st);
+                             int32_t rows, int32_t n, int32_t m, bool sell, cudaStream_t st);
 
 inline int launch_colblocked_primal(const PrimalStepOp<false>& op, const ColBlockedPrimal& p, cudaStream_t st) {
   int n = 0;
+  const bool sell = p.sell_fin.active();
   for (int b = 0; b + 1 < p.q.nb && p.q.active(); ++b) {
     const SpmvOp<false> sp{p.q.blk[b].view(), op.xmd, p.part_q.get() + static_cast<int64_t>(b) * p.rows};
-    launch_rowwise(sp, p.sch_q[b].view, st);
+    if (sell) launch_sell(sp, p.sell_q[b], st);
+    else launch_rowwise(sp, p.sch_q[b].view, st);
     ++n;
   }
   const int npa = static_cast<int>(p.sch_at.size());
   for (int b = 0; b < npa; ++b) {
     const CsrView at = p.at.active() ? p.at.blk[b].view() : op.at;
     const SpmvOp<false> sp{at, op.y, p.part_at.get() + static_cast<int64_t>(b) * p.rows};
-    launch_rowwise(sp, p.sch_at[b].view, st);
+    if (sell) launch_sell(sp, p.sell_at[b], st);
+    else launch_rowwise(sp, p.sch_at[b].view, st);
     ++n;
   }
   PrimalStepOp<false> last = op;
   if (p.q.active()) last.q = p.q.blk[p.q.nb - 1].view();
   if (p.at_all_partial) last.at = CsrView{p.zero_rp.get(), op.at.ci, op.at.v};
   else if (p.at.active()) last.at = p.at.blk[p.at.nb - 1].view();
-  launch_rowwise(PartialsOp<PrimalStepOp<false>>{last, p.part_q.get(), p.part_at.get(), p.q.active() ? p.q.nb - 1 : 0,
-                                                 npa, p.rows},
-                 p.fin.view, st);
+  const PartialsOp<PrimalStepOp<false>> fin{last, p.part_q.get(), p.part_at.get(), p.q.active() ? p.q.nb - 1 : 0,
+                                            npa, p.rows};
+  if (sell) launch_sell(fin, p.sell_fin, st);
+  else launch_rowwise(fin, p.fin.view, st);
   return n + 1;
 }
 

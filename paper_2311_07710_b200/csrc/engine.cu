@@ -477,6 +477,8 @@ Engine::Engine(const rapdhg_qp& p, const rapdhg_config& cfg, Clock::time_point t
   RB_CUDA(cudaStreamSynchronize(st_));
   tr.mark("omega init + buffers");
   if (!P_->strict) {
+    sell_dual_ = sell_eligible(P_->A.rp.get(), nullptr, m_, st_);
+    sell_primal_ = sell_eligible(P_->Q.rp.get(), P_->AT.rp.get(), n_, st_);
     setup_slabs();
     if (full_plans_) setup_colblocks();
   }
@@ -546,9 +548,18 @@ void Engine::colblock_counts(bool dual_slab_active, bool primal_slab_active) {
 void Engine::setup_colblocks() {
   DeviceQP& P = *P_;
   colblock_counts(dual_ph_.active(), primal_ph_.active());
-  build_colblocked_dual(cbd_, cb_nb_dual_, P.A.rp.get(), P.A.ci.get(), m_, n_, asv_, st_);
+  build_colblocked_dual(cbd_, cb_nb_dual_, P.A.rp.get(), P.A.ci.get(), m_, n_, asv_, sell_dual_, st_);
   build_colblocked_primal(cbp_, cb_nq_, cb_na_, P.Q.rp.get(), P.Q.ci.get(), qsv_, P.AT.rp.get(), P.AT.ci.get(), atsv_,
-                          n_, n_, m_, st_);
+                          n_, n_, m_, sell_primal_, st_);
+  // the plain path of short-row ops: sliced ELL instead of rowwise_kernel
+  if (sell_dual_ && !dual_ph_.active() && !cbd_.active()) {
+    build_sell_plan(sell_dual_plan_, P.A.rp.get(), P.A.ci.get(), nullptr, nullptr, m_, st_);
+    fill_sell_values(sell_dual_plan_, asv_, nullptr, st_);
+  }
+  if (sell_primal_ && !primal_ph_.active() && !cbp_.active()) {
+    build_sell_plan(sell_primal_plan_, P.Q.rp.get(), P.Q.ci.get(), P.AT.rp.get(), P.AT.ci.get(), n_, st_);
+    fill_sell_values(sell_primal_plan_, qsv_, atsv_, st_);
+  }
 }
 
 // The pattern-only part of the slab plans (windows, tiles, layouts: mostly
@@ -690,6 +701,9 @@ void Engine::launch_chunk_body(int len, int cur, bool prof) {
         launches_ += launch_slab_phase(d, dual_ph_, st_, span);
       } else if (cbd_.active()) {
         launches_ += launch_colblocked_dual(d, cbd_, st_);
+      } else if (sell_dual_plan_.active()) {
+        launch_sell(d, sell_dual_plan_, st_);
+        ++launches_;
       } else {
         rowwise(d, P_->sch_dual, st_, &launches_);
       }
@@ -706,6 +720,9 @@ void Engine::launch_chunk_body(int len, int cur, bool prof) {
         launches_ += launch_slab_phase(pr, primal_ph_, st_, span);
       } else if (cbp_.active()) {
         launches_ += launch_colblocked_primal(pr, cbp_, st_);
+      } else if (sell_primal_plan_.active()) {
+        launch_sell(pr, sell_primal_plan_, st_);
+        ++launches_;
       } else {
         rowwise(pr, P_->sch_primal, st_, &launches_);
       }

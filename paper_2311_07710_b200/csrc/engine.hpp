@@ -21,6 +21,7 @@
 #include "rowwise.cuh"
 #include "colblock.cuh"
 #include "slab.cuh"
+#include "sell.cuh"
 
 namespace rb {
 
@@ -214,6 +215,10 @@ class Engine : public LoopBackend {
   void colblock_counts(bool dual_slab_active, bool primal_slab_active);
   bool full_plans_ = true;
   int cb_nb_dual_ = 1, cb_nq_ = 1, cb_na_ = 1;  // block counts (global: shards reuse them)
+  // sliced-ELL (sell.cuh) for ops whose rows are all short — decided on the
+  // whole matrices (shards reuse the decision); plans of the plain path
+  bool sell_dual_ = false, sell_primal_ = false;
+  SellPlan sell_dual_plan_, sell_primal_plan_;
   ColBlockedDual cbd_;
   ColBlockedPrimal cbp_;
 

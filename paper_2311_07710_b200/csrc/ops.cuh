@@ -184,7 +184,10 @@ struct SpmvOp {
     acc.v[0] = seg_dot<Strict, U>(m.v, m.ci, g[0], m.rp[r], lo + lane, hi, stride, acc.v[0]);
   }
   __device__ __forceinline__ const double* gather_src(int) const { return x; }
+  struct Pre {};
+  __device__ __forceinline__ Pre prefetch(int) const { return Pre{}; }
   __device__ __forceinline__ void finish(int r, const AccT& acc) const { y[r] = acc.v[0]; }
+  __device__ __forceinline__ void finish(int r, const AccT& acc, const Pre&) const { y[r] = acc.v[0]; }
 };
 
 // ---------------------------------------------------------------------------

@@ -377,6 +377,7 @@ struct ShardedEngine::Shard {
   SlabPhase dual_ph, primal_ph;
   ColBlockedDual cbd;  // column blocks over the owned rows (same block counts as one GPU)
   ColBlockedPrimal cbp;
+  SellPlan sell_dual, sell_primal;  // sliced ELL over the owned rows (plain path)
   // full-length copies; only the owned slice is computed here, the rest is
   // received by the exchanges
   DevBuf<double> X[2], XMD[2], w, xb, y, yb, epx, epy, xu[2], yu[2], ax[2], qx[2], aty[2], best_x, best_y;
@@ -465,11 +466,22 @@ ShardedEngine::ShardedEngine(const rapdhg_qp& p, const rapdhg_config& cfg, int p
   for (auto& sh : shards_) {
     if (!sh->dual_ph.active() && sh->d1 > sh->d0)
       build_colblocked_dual(sh->cbd, full_->cb_nb_dual_, P.A.rp.get() + sh->d0, P.A.ci.get(),
-                            static_cast<int32_t>(sh->d1 - sh->d0), n, full_->asv_, st_);
+                            static_cast<int32_t>(sh->d1 - sh->d0), n, full_->asv_, full_->sell_dual_, st_);
     if (!sh->primal_ph.active() && sh->p1 > sh->p0)
       build_colblocked_primal(sh->cbp, full_->cb_nq_, full_->cb_na_, P.Q.rp.get() + sh->p0, P.Q.ci.get(), full_->qsv_,
                               P.AT.rp.get() + sh->p0, P.AT.ci.get(), full_->atsv_,
-                              static_cast<int32_t>(sh->p1 - sh->p0), n, m, st_);
+                              static_cast<int32_t>(sh->p1 - sh->p0), n, m, full_->sell_primal_, st_);
+    // the plain path: sliced ELL over the shard's rows when one GPU would use it
+    if (full_->sell_dual_ && !sh->dual_ph.active() && !sh->cbd.active() && sh->d1 > sh->d0) {
+      build_sell_plan(sh->sell_dual, P.A.rp.get() + sh->d0, P.A.ci.get(), nullptr, nullptr,
+                      static_cast<int32_t>(sh->d1 - sh->d0), st_);
+      fill_sell_values(sh->sell_dual, full_->asv_, nullptr, st_);
+    }
+    if (full_->sell_primal_ && !sh->primal_ph.active() && !sh->cbp.active() && sh->p1 > sh->p0) {
+      build_sell_plan(sh->sell_primal, P.Q.rp.get() + sh->p0, P.Q.ci.get(), P.AT.rp.get() + sh->p0, P.AT.ci.get(),
+                      static_cast<int32_t>(sh->p1 - sh->p0), st_);
+      fill_sell_values(sh->sell_primal, full_->qsv_, full_->atsv_, st_);
+    }
   }
   build_halos();
   RB_CUDA(cudaStreamSynchronize(st_));
@@ -674,6 +686,9 @@ void ShardedEngine::body(int len, int cur) {
         launches_ += launch_slab_phase(d, sh->dual_ph, st_);
       } else if (sh->cbd.active()) {
         launches_ += launch_colblocked_dual(d, sh->cbd, st_);
+      } else if (sh->sell_dual.active()) {
+        launch_sell(d, sh->sell_dual, st_);
+        ++launches_;
       } else {
         launch_rowwise(d, sh->sch_dual.view, st_);
         ++launches_;
@@ -692,6 +707,9 @@ void ShardedEngine::body(int len, int cur) {
         launches_ += launch_slab_phase(pr, sh->primal_ph, st_);
       } else if (sh->cbp.active()) {
         launches_ += launch_colblocked_primal(pr, sh->cbp, st_);
+      } else if (sh->sell_primal.active()) {
+        launch_sell(pr, sh->sell_primal, st_);
+        ++launches_;
       } else {
         launch_rowwise(pr, sh->sch_primal.view, st_);
         ++launches_;

@@ -3,6 +3,7 @@
 #include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "sell.cuh"
@@ -13,8 +14,13 @@ namespace {
 
 inline unsigned g1(int64_t n) { return static_cast<unsigned>(ceil_div(n > 0 ? n : 1, 256)); }
 
+int sell_sigma() {
+  const char* e = std::getenv("RAPDHG_SELL_SIGMA");
+  return e ? std::max(1, std::atoi(e)) : kSellSigma;
+}
+
 __global__ void sell_len_kernel(const int32_t* rp1, const int32_t* rp2, int32_t rows, int32_t* len, int32_t* l1,
-                                uint32_t* key, int32_t* idx) {
+                                uint32_t* key, int32_t* idx, int sigma) {
   const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (r >= rows) return;
   const int a = rp1[r + 1] - rp1[r];
@@ -23,7 +29,7 @@ __global__ void sell_len_kernel(const int32_t* rp1, const int32_t* rp2, int32_t 
   l1[r] = a;
   if (key) {
     const int L = min(a + b, 255);
-    key[r] = (static_cast<uint32_t>(r / kSellSigma) << 8) | static_cast<uint32_t>(255 - L);  // chunk, longest first
+    key[r] = (static_cast<uint32_t>(r / sigma) << 8) | static_cast<uint32_t>(255 - L);  // chunk, longest first
     idx[r] = static_cast<int32_t>(r);
   }
 }
@@ -87,7 +93,7 @@ bool sell_enabled() {
 bool sell_eligible(const int32_t* rp1, const int32_t* rp2, int32_t rows, cudaStream_t st) {
   if (!sell_enabled() || rows <= 0) return false;
   DevBuf<int32_t> len(rows), l1(rows);
-  sell_len_kernel<<<g1(rows), 256, 0, st>>>(rp1, rp2, rows, len.get(), l1.get(), nullptr, nullptr);
+  sell_len_kernel<<<g1(rows), 256, 0, st>>>(rp1, rp2, rows, len.get(), l1.get(), nullptr, nullptr, 1);
   RB_LAUNCH_CHECK();
   DevBuf<int32_t> mx(1);
   std::size_t tb = 0;
@@ -106,9 +112,12 @@ void build_sell_plan(SellPlan& plan, const int32_t* rp1, const int32_t* ci1, con
   if (rows <= 0) return;
   DevBuf<int32_t> len(rows), l1(rows), idx(rows), order(rows);
   DevBuf<uint32_t> key(rows), key_s(rows);
-  sell_len_kernel<<<g1(rows), 256, 0, st>>>(rp1, rp2, rows, len.get(), l1.get(), key.get(), idx.get());
+  const int sigma = sell_sigma();
+  sell_len_kernel<<<g1(rows), 256, 0, st>>>(rp1, rp2, rows, len.get(), l1.get(), key.get(), idx.get(), sigma);
   RB_LAUNCH_CHECK();
-  {
+  if (sigma <= 32) {  // index order
+    RB_CUDA(cudaMemcpyAsync(order.get(), idx.get(), sizeof(int32_t) * rows, cudaMemcpyDeviceToDevice, st));
+  } else {
     std::size_t tb = 0;
     RB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, key.get(), key_s.get(), idx.get(), order.get(), rows, 0, 32,
                                             st));

@@ -8,8 +8,8 @@
 // wavefronts of the gathers themselves (ncu: 8.6e7 sectors for 3e7 entries of
 // one pass, LSU wavefronts at 67% of peak).
 //
-// Layout: rows in chunks of kSellSigma consecutive rows, sorted by length
-// within a chunk (stable), cut into slices of 32 rows; a slice stores its
+// Layout: rows in index order (RAPDHG_SELL_SIGMA = s > 32: sorted by length
+// within chunks of s rows), cut into slices of 32 rows; a slice stores its
 // entries entry-major (entry e of lane l at off[q] + 32 e + l; padding col 0,
 // value 0), so a warp's index and value loads are contiguous (4 + 8 sectors
 // per 32 entries) and only the gathers are scattered. A row keeps its entries
@@ -27,7 +27,11 @@
 namespace rb {
 
 constexpr int kSellMaxLen = 64;    // rows up to this many entries (all rows of a SELL op)
-constexpr int kSellSigma = 1024;   // rows per sorting chunk
+// Rows per sorting chunk: 32 = index order. Sorting (less padding) scatters
+// the epilogue's vector accesses over the chunk, and on C5's epilogue-heavy
+// final primal pass that doubled its DRAM traffic (2.2 vs 1.0 GB): index
+// order costs only idle lanes in a slice's last entries (no extra loads).
+constexpr int kSellSigma = 32;
 
 struct SellView {
   int64_t nslots = 0;               // rows (slots beyond are padding)

@@ -626,10 +626,12 @@ void Engine::setup_slabs() {
   tr.mark("  slab plans joined");
   if (dual_ph_.active()) {
     fill_slab_values(dual_ph_.plan, asv_, nullptr, st_);
+    fill_sell_values(dual_ph_.others_sell, asv_, nullptr, st_);
     assign_slab_ctas(dual_ph_.plan, prepare_slab<DualStepOp<false>>(dual_ph_.plan.view.smem_bytes()), st_);
   }
   if (primal_ph_.active()) {
     fill_slab_values(primal_ph_.plan, qsv_, atsv_, st_);
+    fill_sell_values(primal_ph_.others_sell, qsv_, atsv_, st_);
     assign_slab_ctas(primal_ph_.plan, prepare_slab<PrimalStepOp<false>>(primal_ph_.plan.view.smem_bytes()), st_);
   }
   tr.mark("  slab values + launch setup");

@@ -20,11 +20,12 @@ int sell_sigma() {
 }
 
 __global__ void sell_len_kernel(const int32_t* rp1, const int32_t* rp2, int32_t rows, int32_t* len, int32_t* l1,
-                                uint32_t* key, int32_t* idx, int sigma) {
+                                uint32_t* key, int32_t* idx, int sigma, const int32_t* subset = nullptr) {
   const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (r >= rows) return;
-  const int a = rp1[r + 1] - rp1[r];
-  const int b = rp2 ? rp2[r + 1] - rp2[r] : 0;
+  const int64_t pr = subset ? subset[r] : r;  // the pattern's row
+  const int a = rp1[pr + 1] - rp1[pr];
+  const int b = rp2 ? rp2[pr + 1] - rp2[pr] : 0;
   len[r] = a + b;
   l1[r] = a;
   if (key) {
@@ -36,7 +37,8 @@ __global__ void sell_len_kernel(const int32_t* rp1, const int32_t* rp2, int32_t 
 
 // per slot: row (sorted order), its length and split; per slice: its width
 __global__ void sell_slots_kernel(const int32_t* order, const int32_t* len_r, const int32_t* l1_r, int32_t rows,
-                                  int64_t nslices, int32_t* row, int32_t* len, int32_t* l1, int64_t* width32) {
+                                  int64_t nslices, int32_t* row, int32_t* len, int32_t* l1, int64_t* width32,
+                                  const int32_t* subset) {
   const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (q >= nslices) return;
   int w = 0;
@@ -44,9 +46,10 @@ __global__ void sell_slots_kernel(const int32_t* order, const int32_t* len_r, co
     const int64_t s = (q << 5) + lane;
     int r = 0, L = 0, a = 0;
     if (s < rows) {
-      r = order[s];
-      L = len_r[r];
-      a = l1_r[r];
+      const int k = order[s];  // index into the subset (or the row itself)
+      r = subset ? subset[k] : k;
+      L = len_r[k];
+      a = l1_r[k];
     }
     row[s] = r, len[s] = L, l1[s] = a;
     w = max(w, L);
@@ -83,12 +86,12 @@ __global__ void sell_vals_kernel(double* val, const int64_t* pos, int64_t n, con
   val[i] = p < 0 ? 0.0 : (p >= kSellSeg2 ? v2[p - kSellSeg2] : v1[p]);
 }
 
+}  // namespace
+
 bool sell_enabled() {
   const char* e = std::getenv("RAPDHG_SELL");
   return !(e && e[0] == '0');
 }
-
-}  // namespace
 
 bool sell_eligible(const int32_t* rp1, const int32_t* rp2, int32_t rows, cudaStream_t st) {
   if (!sell_enabled() || rows <= 0) return false;
@@ -107,13 +110,14 @@ bool sell_eligible(const int32_t* rp1, const int32_t* rp2, int32_t rows, cudaStr
 }
 
 void build_sell_plan(SellPlan& plan, const int32_t* rp1, const int32_t* ci1, const int32_t* rp2, const int32_t* ci2,
-                     int32_t rows, cudaStream_t st) {
+                     int32_t rows, cudaStream_t st, const int32_t* subset) {
   plan = SellPlan{};
   if (rows <= 0) return;
   DevBuf<int32_t> len(rows), l1(rows), idx(rows), order(rows);
   DevBuf<uint32_t> key(rows), key_s(rows);
   const int sigma = sell_sigma();
-  sell_len_kernel<<<g1(rows), 256, 0, st>>>(rp1, rp2, rows, len.get(), l1.get(), key.get(), idx.get(), sigma);
+  sell_len_kernel<<<g1(rows), 256, 0, st>>>(rp1, rp2, rows, len.get(), l1.get(), key.get(), idx.get(), sigma,
+                                            subset);
   RB_LAUNCH_CHECK();
   if (sigma <= 32) {  // index order
     RB_CUDA(cudaMemcpyAsync(order.get(), idx.get(), sizeof(int32_t) * rows, cudaMemcpyDeviceToDevice, st));
@@ -130,7 +134,7 @@ void build_sell_plan(SellPlan& plan, const int32_t* rp1, const int32_t* ci1, con
   plan.row.alloc(nslots), plan.len.alloc(nslots), plan.l1.alloc(nslots);
   DevBuf<int64_t> w32(nslices);
   sell_slots_kernel<<<g1(nslices), 256, 0, st>>>(order.get(), len.get(), l1.get(), rows, nslices, plan.row.get(),
-                                                 plan.len.get(), plan.l1.get(), w32.get());
+                                                 plan.len.get(), plan.l1.get(), w32.get(), subset);
   RB_LAUNCH_CHECK();
   plan.off.alloc(nslices + 1);
   plan.off.zero(st);

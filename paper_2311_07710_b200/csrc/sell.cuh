@@ -61,7 +61,10 @@ struct SellPlan {
 // the caller decides with sell_eligible (rows longer than kSellMaxLen would
 // pad whole slices).
 void build_sell_plan(SellPlan& plan, const int32_t* rp1, const int32_t* ci1, const int32_t* rp2, const int32_t* ci2,
-                     int32_t rows, cudaStream_t st);
+                     int32_t rows, cudaStream_t st, const int32_t* subset = nullptr);
+// subset (device, `rows` ids in increasing order): the plan covers only those
+// rows of the pattern (slot s holds subset[s]).
+bool sell_enabled();
 // (Re)fill the values from arrays laid out like segment 1 / segment 2.
 void fill_sell_values(SellPlan& plan, const double* v1, const double* v2, cudaStream_t st);
 // Whether every row of the pattern has at most kSellMaxLen entries (and
@@ -69,65 +72,70 @@ void fill_sell_values(SellPlan& plan, const double* v1, const double* v2, cudaSt
 // sharded solve takes the decision one GPU takes.
 bool sell_eligible(const int32_t* rp1, const int32_t* rp2, int32_t rows, cudaStream_t st);
 
+// One warp computes slice q (lane = row) and runs the op's epilogue.
 template <class Op>
-__global__ void __launch_bounds__(kBlock) sell_kernel(const Op op, const SellView sv) {
+__device__ __forceinline__ void sell_slice(const Op& op, const SellView& sv, int64_t q, int lane) {
   constexpr int U = 4;
-  const int lane = threadIdx.x & 31;
-  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (kBlock / 32);
   const double* g0 = op.gather_src(0);
   const double* g1 = op.gather_src(1);
-  for (int64_t q = (blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x) >> 5; q < sv.nslices; q += nwarps) {
-    const int64_t slot = (q << 5) + lane;
-    const bool valid = slot < sv.nslots;
-    int r = 0, L = 0, l1 = 0;
-    typename Op::Pre pre{};
-    if (valid) {
-      r = sv.row[slot];
-      L = sv.len[slot];
-      l1 = sv.l1[slot];
-      pre = op.prefetch(r);
-    }
-    const int64_t o = sv.off[q];
-    const int W = static_cast<int>((sv.off[q + 1] - o) >> 5);
-    const int32_t* cq = sv.col + o + lane;
-    const double* vq = sv.val + o + lane;
-    double a0 = 0.0, a1 = 0.0;
-    int32_t c[U];
-    double v[U];
+  const int64_t slot = (q << 5) + lane;
+  const bool valid = slot < sv.nslots;
+  int r = 0, L = 0, l1 = 0;
+  typename Op::Pre pre{};
+  if (valid) {
+    r = sv.row[slot];
+    L = sv.len[slot];
+    l1 = sv.l1[slot];
+    pre = op.prefetch(r);
+  }
+  const int64_t o = sv.off[q];
+  const int W = static_cast<int>((sv.off[q + 1] - o) >> 5);
+  const int32_t* cq = sv.col + o + lane;
+  const double* vq = sv.val + o + lane;
+  double a0 = 0.0, a1 = 0.0;
+  int32_t c[U];
+  double v[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const bool ok = u < L;
+    c[u] = ok ? __ldcs(cq + (u << 5)) : 0;
+    v[u] = ok ? __ldcs(vq + (u << 5)) : 0.0;
+  }
+  for (int e = 0; e < W; e += U) {
+    // next batch's indices / values in flight before this batch's gathers
+    int32_t cn[U];
+    double vn[U], x[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const bool ok = u < L;
-      c[u] = ok ? __ldcs(cq + (u << 5)) : 0;
-      v[u] = ok ? __ldcs(vq + (u << 5)) : 0.0;
+      const bool ok = e + U + u < L;
+      cn[u] = ok ? __ldcs(cq + ((e + U + u) << 5)) : 0;
+      vn[u] = ok ? __ldcs(vq + ((e + U + u) << 5)) : 0.0;
     }
-    for (int e = 0; e < W; e += U) {
-      // next batch's indices / values in flight before this batch's gathers
-      int32_t cn[U];
-      double vn[U], x[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const bool ok = e + U + u < L;
-        cn[u] = ok ? __ldcs(cq + ((e + U + u) << 5)) : 0;
-        vn[u] = ok ? __ldcs(vq + ((e + U + u) << 5)) : 0.0;
-      }
+    for (int u = 0; u < U; ++u) x[u] = e + u < L ? __ldg((e + u < l1 ? g0 : g1) + c[u]) : 0.0;
 #pragma unroll
-      for (int u = 0; u < U; ++u) x[u] = e + u < L ? __ldg((e + u < l1 ? g0 : g1) + c[u]) : 0.0;
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (e + u < l1) a0 = fma(v[u], x[u], a0);
-        else if (e + u < L) a1 = fma(v[u], x[u], a1);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) c[u] = cn[u], v[u] = vn[u];
+    for (int u = 0; u < U; ++u) {
+      if (e + u < l1) a0 = fma(v[u], x[u], a0);
+      else if (e + u < L) a1 = fma(v[u], x[u], a1);
     }
-    if (valid) {
-      typename Op::AccT acc;
-      acc.zero();
-      acc.v[0] = a0;
-      if constexpr (Op::AccT::kK > 1) acc.v[Op::AccT::kK - 1] = a1;
-      op.finish(r, acc, pre);
-    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) c[u] = cn[u], v[u] = vn[u];
   }
+  if (valid) {
+    typename Op::AccT acc;
+    acc.zero();
+    acc.v[0] = a0;
+    if constexpr (Op::AccT::kK > 1) acc.v[Op::AccT::kK - 1] = a1;
+    op.finish(r, acc, pre);
+  }
+}
+
+template <class Op>
+__global__ void __launch_bounds__(kBlock) sell_kernel(const Op op, const SellView sv) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (kBlock / 32);
+  for (int64_t q = (blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x) >> 5; q < sv.nslices; q += nwarps)
+    sell_slice(op, sv, q, lane);
 }
 
 template <class Op>

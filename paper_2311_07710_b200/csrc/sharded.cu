@@ -416,6 +416,7 @@ ShardedEngine::ShardedEngine(const rapdhg_qp& p, const rapdhg_config& cfg, int p
                        static_cast<int32_t>(sh->d0), static_cast<int32_t>(sh->d1), len.get(), st_);
       if (sh->dual_ph.active()) {
         fill_slab_values(sh->dual_ph.plan, full_->asv_, nullptr, st_);
+        fill_sell_values(sh->dual_ph.others_sell, full_->asv_, nullptr, st_);
         assign_slab_ctas(sh->dual_ph.plan, prepare_slab<DualStepOp<false>>(sh->dual_ph.plan.view.smem_bytes()), st_);
       }
     }
@@ -426,6 +427,7 @@ ShardedEngine::ShardedEngine(const rapdhg_qp& p, const rapdhg_config& cfg, int p
                        P.AT.ci.get(), static_cast<int32_t>(sh->p0), static_cast<int32_t>(sh->p1), len.get(), st_);
       if (sh->primal_ph.active()) {
         fill_slab_values(sh->primal_ph.plan, full_->qsv_, full_->atsv_, st_);
+        fill_sell_values(sh->primal_ph.others_sell, full_->qsv_, full_->atsv_, st_);
         assign_slab_ctas(sh->primal_ph.plan, prepare_slab<PrimalStepOp<false>>(sh->primal_ph.plan.view.smem_bytes()), st_);
       }
     }

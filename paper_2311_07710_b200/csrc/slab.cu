@@ -212,6 +212,13 @@ int env_int(const char* name, int dflt) {
   return e ? std::atoi(e) : dflt;
 }
 
+std::vector<int32_t> download_len(const int32_t* d, int64_t n, cudaStream_t st) {
+  std::vector<int32_t> h(static_cast<std::size_t>(n));
+  if (n > 0) RB_CUDA(cudaMemcpyAsync(h.data(), d, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
+  RB_CUDA(cudaStreamSynchronize(st));
+  return h;
+}
+
 template <class T>
 std::vector<T> download(const DevBuf<T>& d, int64_t n, cudaStream_t st) {
   std::vector<T> h(static_cast<std::size_t>(n));
@@ -453,13 +460,23 @@ void build_slab_phase(SlabPhase& ph, const SlabChoice& choice, int seg, const in
   if (!ph.active()) return;
   const int32_t nr = r1 - r0;
   const std::vector<int32_t> widx = download(ph.plan.widx, nr, st);
-  std::vector<int32_t> orr;
+  const std::vector<int32_t> hlen = download_len(len, nr, st);
+  // the rows without partials: long ones on a rowwise schedule, short ones
+  // (<= kSellMaxLen entries, a per-row rule, so shards agree) sliced ELL
+  const bool sell = sell_enabled();
+  std::vector<int32_t> orr, osh;
   for (int32_t i = 0; i < nr; ++i)
-    if (widx[i] < 0) orr.push_back(i);
+    if (widx[i] < 0) (sell && hlen[i] <= kSellMaxLen ? osh : orr).push_back(i);
   if (!orr.empty()) {
     DevBuf<int32_t> d(orr.size());
     d.upload(orr.data(), orr.size(), st);
     build_schedule(ph.others, len, static_cast<int64_t>(orr.size()), false, st, d.get());
+  }
+  if (!osh.empty()) {
+    DevBuf<int32_t> d(osh.size());
+    d.upload(osh.data(), osh.size(), st);
+    build_sell_plan(ph.others_sell, rp1 ? rp1 + r0 : nullptr, ci1, rp2 ? rp2 + r0 : nullptr, ci2,
+                    static_cast<int32_t>(osh.size()), st, d.get());
   }
   RB_CUDA(cudaStreamSynchronize(st));
 }

@@ -39,6 +39,7 @@
 
 #include "ops.cuh"
 #include "slab_layout.hpp"
+#include "sell.cuh"
 
 namespace rb {
 
@@ -453,17 +454,24 @@ inline int SlabView::smem_bytes() const { return win_max * 8 + kSlabStages * sta
 // thousands of steps at the bench's size.
 template <class Op>
 __global__ void __launch_bounds__(kBlock) slab_finish_kernel(const Op op, const Op rest, const SlabView sv,
-                                                             const SchedView others, int wblocks) {
+                                                             const SchedView others, int wblocks,
+                                                             const SellView osell) {
   // the next kernel (the next slab kernel, a programmatic dependent launch)
   // may start prefetching its tiles; it waits for this grid before using y / w
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int ob = others.total_blocks > 0 ? others.total_blocks : 0;
+  const int sb = static_cast<int>(ceil_div(osell.nslices, kBlock / 32));
   if (static_cast<int>(blockIdx.x) < ob) {  // first: the rows without partials (they start at once)
     const Gather g[2] = {Gather{op.gather_src(0), nullptr, 0, 0u}, Gather{op.gather_src(1), nullptr, 0, 0u}};
     rowwise_tile(op, others, blockIdx.x, g);
 #ifdef RB_SLAB_PROFILE
     if (threadIdx.x == 0 && sv.fprof) atomicMax(&sv.fprof[0], slab_now());
 #endif
+    return;
+  }
+  if (static_cast<int>(blockIdx.x) < ob + sb) {  // the short ones of them: sliced ELL, a slice per warp
+    const int64_t q = static_cast<int64_t>(blockIdx.x - ob) * (kBlock / 32) + (threadIdx.x >> 5);
+    if (q < osell.nslices) sell_slice(op, osell, q, threadIdx.x & 31);
     return;
   }
   if (sv.resident) {  // W rows finished in the slab kernel: one block only waits for it, so
@@ -479,7 +487,8 @@ __global__ void __launch_bounds__(kBlock) slab_finish_kernel(const Op op, const 
   // few, a thread takes one row and sums its S partials in order.
   const bool grouped = sv.S >= kSlabGroupedS;
   const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
-  const int k = grouped ? (blockIdx.x - ob) * 32 + lane : (blockIdx.x - ob) * kBlock + threadIdx.x;
+  const int wb = static_cast<int>(blockIdx.x) - ob - sb;  // W-row block
+  const int k = grouped ? wb * 32 + lane : wb * kBlock + threadIdx.x;
   const bool valid = k < sv.nw;
   const bool owner = valid && (!grouped || g == 0);  // runs the row's epilogue
   typename Op::AccT a;
@@ -555,7 +564,8 @@ inline int prepare_slab(int smem_bytes) {
 // A slab-tiled op: the plan and the finish schedule over all of its rows.
 struct SlabPhase {
   SlabPlan plan;
-  Schedule others;  // rows without partials (the op's own rows)
+  Schedule others;     // rows without partials (the op's own rows) longer than kSellMaxLen
+  SellPlan others_sell;  // the short ones, sliced ELL (sell.cuh); RAPDHG_SELL=0: all in `others`
   bool active() const { return plan.view.active(); }
 };
 
@@ -602,9 +612,11 @@ inline int launch_slab_phase(const Op& op, const SlabPhase& ph, cudaStream_t st,
     RB_CUDA(cudaLaunchKernelEx(&cfg, slab_kernel<Op>, op, sv));
   }
   const SchedView& o = ph.others.view;
+  const SellView& osell = ph.others_sell.view;
   const int wblocks = sv.resident ? 1 : static_cast<int>(ceil_div(sv.nw, sv.S >= kSlabGroupedS ? 32 : kBlock));
+  const int sblocks = static_cast<int>(ceil_div(osell.nslices, kBlock / 32));
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(static_cast<unsigned>(wblocks + (o.total_blocks > 0 ? o.total_blocks : 0)));
+  cfg.gridDim = dim3(static_cast<unsigned>(wblocks + sblocks + (o.total_blocks > 0 ? o.total_blocks : 0)));
   cfg.blockDim = dim3(kBlock);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = st;
@@ -613,7 +625,8 @@ inline int launch_slab_phase(const Op& op, const SlabPhase& ph, cudaStream_t st,
   attr[0].val.programmaticStreamSerializationAllowed = pdl;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  RB_CUDA(cudaLaunchKernelEx(&cfg, slab_finish_kernel<Op>, op, op.with_views(sv.rest1, sv.rest2), sv, o, wblocks));
+  RB_CUDA(cudaLaunchKernelEx(&cfg, slab_finish_kernel<Op>, op, op.with_views(sv.rest1, sv.rest2), sv, o, wblocks,
+                             osell));
   return 2;
 }
 

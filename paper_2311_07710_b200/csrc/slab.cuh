@@ -460,7 +460,7 @@ __global__ void __launch_bounds__(kBlock) slab_finish_kernel(const Op op, const 
   // may start prefetching its tiles; it waits for this grid before using y / w
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int ob = others.total_blocks > 0 ? others.total_blocks : 0;
-  const int sb = static_cast<int>(ceil_div(osell.nslices, kBlock / 32));
+  const int sb = static_cast<int>((osell.nslices + kBlock / 32 - 1) / (kBlock / 32));
   if (static_cast<int>(blockIdx.x) < ob) {  // first: the rows without partials (they start at once)
     const Gather g[2] = {Gather{op.gather_src(0), nullptr, 0, 0u}, Gather{op.gather_src(1), nullptr, 0, 0u}};
     rowwise_tile(op, others, blockIdx.x, g);

@@ -461,9 +461,12 @@ void build_slab_phase(SlabPhase& ph, const SlabChoice& choice, int seg, const in
   const int32_t nr = r1 - r0;
   const std::vector<int32_t> widx = download(ph.plan.widx, nr, st);
   const std::vector<int32_t> hlen = download_len(len, nr, st);
-  // the rows without partials: long ones on a rowwise schedule, short ones
-  // (<= kSellMaxLen entries, a per-row rule, so shards agree) sliced ELL
-  const bool sell = sell_enabled();
+  // the rows without partials: a rowwise schedule; RAPDHG_SELL_OTHERS=1 puts
+  // the short ones (<= kSellMaxLen entries, a per-row rule, so shards agree)
+  // on sliced ELL instead — measured neutral (C4 +0.6%, C3 -0.8%, C2 -2%:
+  // these rows overlap the slab kernel either way), so off by default
+  const char* so = std::getenv("RAPDHG_SELL_OTHERS");
+  const bool sell = sell_enabled() && so && so[0] == '1';
   std::vector<int32_t> orr, osh;
   for (int32_t i = 0; i < nr; ++i)
     if (widx[i] < 0) (sell && hlen[i] <= kSellMaxLen ? osh : orr).push_back(i);

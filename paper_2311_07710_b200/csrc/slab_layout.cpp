@@ -22,6 +22,10 @@
 #include <cstdlib>
 #include <thread>
 
+#include <sys/resource.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+
 namespace rb {
 
 namespace {
@@ -41,6 +45,9 @@ void parallel_for(int64_t n, const F& f) {
   std::vector<std::thread> th;
   for (int t = 0; t < T; ++t)
     th.emplace_back([&] {
+      // below the solver's own thread, which launches the setup kernels the
+      // plans overlap (the power iterations: one host sync every 8 steps)
+      setpriority(PRIO_PROCESS, static_cast<id_t>(syscall(SYS_gettid)), 5);
       for (int64_t i; (i = next.fetch_add(1)) < n;) f(i);
     });
   for (auto& x : th) x.join();
@@ -95,7 +102,8 @@ int plan_threads() {
   static const int t = [] {
     const char* e = std::getenv("RAPDHG_PLAN_THREADS");
     const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
-    return std::max(1, std::min(32, e ? std::atoi(e) : std::max(1, hw / 2)));
+    // the two ops' plans run concurrently: leave the solver thread a core
+    return std::max(1, std::min(32, e ? std::atoi(e) : std::max(1, (hw - 1) / 2)));
   }();
   return t;
 }

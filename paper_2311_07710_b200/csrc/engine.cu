@@ -418,6 +418,11 @@ Engine::Engine(const rapdhg_qp& p, const rapdhg_config& cfg, Clock::time_point t
   RB_CUDA(cudaSetDevice(cfg.device));
   st_ = own_st_.create();  // non-blocking; this object's allocations are ordered on it
   AllocStreamScope scope(st_);
+  {  // twice a solve's estimated footprint, mapped once (see pool_reserve)
+    const double nnz = static_cast<double>(p.q.nnz) + 2.0 * (static_cast<double>(p.a_ineq.nnz) + p.a_eq.nnz);
+    const double rows = static_cast<double>(p.n) + p.m_ineq + p.m_eq;
+    pool_reserve(static_cast<std::size_t>(2.0 * (48.0 * nnz + 320.0 * rows)));
+  }
   tr.st = st_;
   tr.mark("device + stream");
   P_ = std::make_unique<DeviceQP>(p, cfg.strict_parity != 0, st_, true);

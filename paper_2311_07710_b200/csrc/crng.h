@@ -41,7 +41,12 @@ RB_HD double normal(uint64_t seed, uint32_t tag, uint64_t i, uint32_t k) {
   return s - 6.0;
 }
 
-enum Tag : uint32_t { kACol = 1, kAVal, kQPair, kQVal, kX0, kC, kSlack, kSvmCol, kSvmVal };
+enum Tag : uint32_t {
+  kACol = 1, kAVal, kQPair, kQVal, kX0, kC, kSlack,  // C5
+  kSvmCol, kSvmVal,                                  // C4
+  kLassoV, kLassoCol, kLassoVal, kLassoNoise,        // C2
+  kPfF, kPfVal, kPfD, kPfMu                          // C3
+};
 
 // C5 column draw: local patterns keep 95% of a row's columns in its home block
 RB_HD int32_t large_col(uint64_t seed, uint32_t tag, uint64_t i, uint32_t k, int32_t n, int32_t home,

@@ -9,6 +9,7 @@
 // bit-identical to the host reference (tests/test_gpu_generators.py) while a
 // 1e8-nonzero instance takes well under a second instead of ~10 s.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include <cstdlib>
@@ -179,6 +180,129 @@ __global__ void svm_compact_kernel(int32_t ns, int32_t nf, int32_t slot, const i
   ci[o] = nf + static_cast<int32_t>(r), v[o] = -1.0;
 }
 
+__global__ void iota_kernel(int32_t* p, int64_t n) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) p[i] = static_cast<int32_t>(i);
+}
+__global__ void fill_one_kernel(int32_t* p, int32_t v) { *p = v; }
+
+// ---- C2 Lasso (host.cpp gen_lasso) ----------------------------------------
+__global__ void lasso_v_kernel(int32_t nf, uint64_t seed, double* v) {
+  const int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (j >= nf) return;
+  const double sq = sqrt(static_cast<double>(nf));
+  v[j] = uniform(seed, kLassoV, j, 0) < 0.5 ? 0.0 : normal(seed, kLassoV, j, 1) / sq;
+}
+// draw t = r * per_row + q: key (row, column), payload t
+__global__ void lasso_draw_kernel(int32_t ns, int32_t nf, int32_t per_row, uint64_t seed, uint64_t* key,
+                                  int32_t* idx) {
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (t >= static_cast<int64_t>(ns) * per_row) return;
+  const int64_t r = t / per_row;
+  const uint32_t q = static_cast<uint32_t>(t % per_row);
+  const uint32_t c = static_cast<uint32_t>(below(uniform(seed, kLassoCol, r, q), static_cast<uint64_t>(nf)));
+  key[t] = (static_cast<uint64_t>(r) << 32) | c;
+  idx[t] = static_cast<int32_t>(t);
+}
+// rows of the key-sorted draws: merged duplicates (count, or write + b_r)
+template <bool Write>
+__global__ void lasso_rows_kernel(int32_t ns, int32_t per_row, uint64_t seed, const uint64_t* key, const int32_t* idx,
+                                  const int32_t* rp, const double* v, int32_t* cnt, int32_t* ci, double* val,
+                                  double* b) {
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (r >= ns) return;
+  const int64_t t0 = r * per_row, t1 = t0 + per_row;  // a row's draws stay within its per_row slots
+  int w = 0;
+  double acc = 0.0;
+  for (int64_t a = t0; a < t1;) {
+    double x = normal(seed, kLassoVal, r, static_cast<uint32_t>(idx[a] % per_row));
+    int64_t e = a + 1;
+    for (; e < t1 && key[e] == key[a]; ++e) x = __dadd_rn(x, normal(seed, kLassoVal, r, static_cast<uint32_t>(idx[e] % per_row)));
+    if (x != 0.0) {
+      const int32_t c = static_cast<int32_t>(key[a] & 0xffffffffu);
+      if (Write) {
+        ci[rp[r] + w] = c, val[rp[r] + w] = x;
+        acc = __dadd_rn(acc, __dmul_rn(x, v[c]));
+      }
+      ++w;
+    }
+    a = e;
+  }
+  if (Write) b[r] = __dadd_rn(acc, normal(seed, kLassoNoise, r, 0));
+  else cnt[r] = w;
+}
+__global__ void row_of_kernel(int32_t rows, const int32_t* rp, int32_t* row_of) {
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (r >= rows) return;
+  for (int k = rp[r]; k < rp[r + 1]; ++k) row_of[k] = static_cast<int32_t>(r);
+}
+// |(A_d' b)_c|: column c's entries in ascending row order (stable transpose
+// sort), summed sequentially and unfused
+__global__ void lasso_atb_kernel(int32_t nf, const int32_t* cs, int64_t nnz, const int32_t* pos, const double* val,
+                                 const int32_t* row_of, const double* b, double* out) {
+  const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (c >= nf) return;
+  int64_t lo = 0, hi = nnz;  // first sorted entry of column c
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (cs[mid] < c) lo = mid + 1;
+    else hi = mid;
+  }
+  double acc = 0.0;
+  for (int64_t k = lo; k < nnz && cs[k] == c; ++k) acc = __dadd_rn(acc, __dmul_rn(val[pos[k]], b[row_of[pos[k]]]));
+  out[c] = fabs(acc);
+}
+
+// ---- C3 portfolio factor rows (host.cpp gen_portfolio) ----------------------
+__global__ void pf_draw_kernel(int32_t na, int32_t k, int32_t per_asset, uint64_t seed, uint64_t* key, int32_t* idx) {
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (t >= static_cast<int64_t>(na) * per_asset) return;
+  const int64_t i = t / per_asset;
+  const uint32_t q = static_cast<uint32_t>(t % per_asset);
+  const uint64_t f = below(uniform(seed, kPfF, i, q), static_cast<uint64_t>(k));
+  key[t] = (f << 32) | static_cast<uint64_t>(i);
+  idx[t] = static_cast<int32_t>(t);
+}
+__global__ void key_row_start_kernel(int32_t rows, const uint64_t* key, int64_t nt, int64_t* rs) {
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (r > rows) return;
+  const uint64_t kk = static_cast<uint64_t>(r) << 32;
+  int64_t lo = 0, hi = nt;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (key[mid] < kk) lo = mid + 1;
+    else hi = mid;
+  }
+  rs[r] = lo;
+}
+template <bool Write>
+__global__ void pf_rows_kernel(int32_t k, int32_t na, int32_t per_asset, uint64_t seed, const uint64_t* key,
+                               const int32_t* idx, const int64_t* rs, const int32_t* rp, int32_t* cnt, int32_t* ci,
+                               double* val) {
+  const int64_t f = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (f >= k) return;
+  int w = 0;
+  for (int64_t a = rs[f]; a < rs[f + 1];) {
+    const int64_t i = idx[a] / per_asset;
+    double x = -normal(seed, kPfVal, i, static_cast<uint32_t>(idx[a] % per_asset));
+    int64_t e = a + 1;
+    for (; e < rs[f + 1] && key[e] == key[a]; ++e)
+      x = __dadd_rn(x, -normal(seed, kPfVal, i, static_cast<uint32_t>(idx[e] % per_asset)));
+    if (x != 0.0) {
+      if (Write) ci[rp[f] + w] = static_cast<int32_t>(i), val[rp[f] + w] = x;
+      ++w;
+    }
+    a = e;
+  }
+  if (Write) ci[rp[f] + w] = na + static_cast<int32_t>(f), val[rp[f] + w] = 1.0;
+  else cnt[f] = w + 1;
+}
+__global__ void pf_budget_kernel(int32_t na, int32_t base, int32_t* ci, double* val) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= na) return;
+  ci[base + i] = static_cast<int32_t>(i), val[base + i] = 1.0;
+}
+
 // exclusive scan of `cnt` (rows entries) into rp (rows + 1 entries)
 void scan_rows(DevBuf<int32_t>& cnt, int64_t rows, DevBuf<int32_t>& rp, cudaStream_t st) {
   rp.alloc(rows + 1);
@@ -316,6 +440,128 @@ bool gen_svm_a_device(int32_t ns, int32_t nf, int32_t per_row, uint64_t seed, ra
     throw Error(RAPDHG_E_INTERNAL, "out of host memory");
   }
   for (int32_t r = 0; r < ns; ++r) a->row_ptr[ns + r + 1] = nnz_top + r + 1;
+  return true;
+}
+
+}  // namespace rb
+
+namespace rb {
+
+namespace {
+bool have_device() {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return false;
+  }
+  return true;
+}
+void sort_u64_pairs(DevBuf<uint64_t>& key, DevBuf<uint64_t>& key_s, DevBuf<int32_t>& idx, DevBuf<int32_t>& idx_s,
+                    int64_t nt, int end_bit, cudaStream_t st) {
+  std::size_t temp = 0;
+  RB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, key.get(), key_s.get(), idx.get(), idx_s.get(), nt, 0,
+                                          end_bit, st));
+  DevBuf<unsigned char> tmp(temp);
+  RB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), temp, key.get(), key_s.get(), idx.get(), idx_s.get(), nt, 0,
+                                          end_bit, st));
+}
+int bits_for(uint64_t v) {
+  int b = 1;
+  while (b < 64 && (v >> b)) ++b;
+  return b;
+}
+}  // namespace
+
+// C2 Lasso: A_d (host arrays), b and lambda (host.cpp gen_lasso assembles the rest).
+bool gen_lasso_core_device(int32_t nf, int32_t ns, int32_t per_row, uint64_t seed, rapdhg_csr_owned* ad, double* bh,
+                           double* lam) {
+  if (!have_device()) return false;
+  OwnedStream own;
+  cudaStream_t st = own.create();
+  AllocStreamScope scope(st);
+  const int64_t nt = static_cast<int64_t>(ns) * per_row;
+  DevBuf<double> v(nf), b(ns), atb(nf), mx(1);
+  DevBuf<uint64_t> key(nt), key_s(nt);
+  DevBuf<int32_t> idx(nt), idx_s(nt), cnt(ns), rp, ci, row_of;
+  DevBuf<double> val;
+  lasso_v_kernel<<<g1(nf), 256, 0, st>>>(nf, seed, v.get());
+  lasso_draw_kernel<<<g1(nt), 256, 0, st>>>(ns, nf, per_row, seed, key.get(), idx.get());
+  RB_LAUNCH_CHECK();
+  sort_u64_pairs(key, key_s, idx, idx_s, nt, 32 + bits_for(static_cast<uint64_t>(ns)), st);
+  lasso_rows_kernel<false><<<g1(ns), 256, 0, st>>>(ns, per_row, seed, key_s.get(), idx_s.get(), nullptr, nullptr,
+                                                   cnt.get(), nullptr, nullptr, nullptr);
+  RB_LAUNCH_CHECK();
+  scan_rows(cnt, ns, rp, st);
+  int32_t nnz = 0;
+  RB_CUDA(cudaMemcpyAsync(&nnz, rp.get() + ns, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  RB_CUDA(cudaStreamSynchronize(st));
+  ci.alloc(nnz), val.alloc(nnz), row_of.alloc(nnz);
+  lasso_rows_kernel<true><<<g1(ns), 256, 0, st>>>(ns, per_row, seed, key_s.get(), idx_s.get(), rp.get(), v.get(),
+                                                  nullptr, ci.get(), val.get(), b.get());
+  row_of_kernel<<<g1(ns), 256, 0, st>>>(ns, rp.get(), row_of.get());
+  RB_LAUNCH_CHECK();
+  {  // transpose order: entries by column, stable (ascending position = ascending row)
+    DevBuf<int32_t> pos(nnz), pos_s(nnz), cs(nnz);
+    iota_kernel<<<g1(nnz), 256, 0, st>>>(pos.get(), nnz);
+    std::size_t temp = 0;
+    RB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, ci.get(), cs.get(), pos.get(), pos_s.get(), nnz, 0,
+                                            bits_for(static_cast<uint64_t>(nf)), st));
+    DevBuf<unsigned char> tmp(temp);
+    RB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), temp, ci.get(), cs.get(), pos.get(), pos_s.get(), nnz, 0,
+                                            bits_for(static_cast<uint64_t>(nf)), st));
+    lasso_atb_kernel<<<g1(nf), 256, 0, st>>>(nf, cs.get(), nnz, pos_s.get(), val.get(), row_of.get(), b.get(),
+                                             atb.get());
+    RB_LAUNCH_CHECK();
+    std::size_t tb = 0;
+    RB_CUDA(cub::DeviceReduce::Max(nullptr, tb, atb.get(), mx.get(), nf, st));
+    DevBuf<unsigned char> tmp2(tb);
+    RB_CUDA(cub::DeviceReduce::Max(tmp2.get(), tb, atb.get(), mx.get(), nf, st));
+  }
+  double hm = 0.0;
+  RB_CUDA(cudaMemcpyAsync(&hm, mx.get(), sizeof(double), cudaMemcpyDeviceToHost, st));
+  RB_CUDA(cudaMemcpyAsync(bh, b.get(), sizeof(double) * ns, cudaMemcpyDeviceToHost, st));
+  ad->n_rows = ns, ad->n_cols = nf, ad->nnz = nnz;
+  ad->row_ptr = to_host(rp, static_cast<std::size_t>(ns) + 1, st);
+  ad->col_idx = to_host(ci, nnz, st);
+  ad->values = to_host(val, nnz, st);
+  RB_CUDA(cudaStreamSynchronize(st));
+  *lam = hm / 5.0;
+  return true;
+}
+
+// C3 portfolio: the equality block (factor rows + budget row), host arrays.
+bool gen_portfolio_eq_device(int32_t na, int32_t k, int32_t per_asset, uint64_t seed, rapdhg_csr_owned* eq) {
+  if (!have_device()) return false;
+  OwnedStream own;
+  cudaStream_t st = own.create();
+  AllocStreamScope scope(st);
+  const int64_t nt = static_cast<int64_t>(na) * per_asset;
+  DevBuf<uint64_t> key(nt), key_s(nt);
+  DevBuf<int32_t> idx(nt), idx_s(nt), cnt(static_cast<std::size_t>(k) + 1), rp, ci;
+  DevBuf<int64_t> rs(static_cast<std::size_t>(k) + 1);
+  DevBuf<double> val;
+  pf_draw_kernel<<<g1(nt), 256, 0, st>>>(na, k, per_asset, seed, key.get(), idx.get());
+  RB_LAUNCH_CHECK();
+  sort_u64_pairs(key, key_s, idx, idx_s, nt, 32 + bits_for(static_cast<uint64_t>(k)), st);
+  key_row_start_kernel<<<g1(static_cast<int64_t>(k) + 1), 256, 0, st>>>(k, key_s.get(), nt, rs.get());
+  pf_rows_kernel<false><<<g1(k), 128, 0, st>>>(k, na, per_asset, seed, key_s.get(), idx_s.get(), rs.get(), nullptr,
+                                               cnt.get(), nullptr, nullptr);
+  RB_LAUNCH_CHECK();
+  fill_one_kernel<<<1, 1, 0, st>>>(cnt.get() + k, na);  // the budget row
+  scan_rows(cnt, static_cast<int64_t>(k) + 1, rp, st);
+  int32_t nnz = 0;
+  RB_CUDA(cudaMemcpyAsync(&nnz, rp.get() + k + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  RB_CUDA(cudaStreamSynchronize(st));
+  ci.alloc(nnz), val.alloc(nnz);
+  pf_rows_kernel<true><<<g1(k), 128, 0, st>>>(k, na, per_asset, seed, key_s.get(), idx_s.get(), rs.get(), rp.get(),
+                                              nullptr, ci.get(), val.get());
+  pf_budget_kernel<<<g1(na), 256, 0, st>>>(na, nnz - na, ci.get(), val.get());
+  RB_LAUNCH_CHECK();
+  eq->n_rows = k + 1, eq->n_cols = na + k, eq->nnz = nnz;
+  eq->row_ptr = to_host(rp, static_cast<std::size_t>(k) + 2, st);
+  eq->col_idx = to_host(ci, nnz, st);
+  eq->values = to_host(val, nnz, st);
+  RB_CUDA(cudaStreamSynchronize(st));
   return true;
 }
 

@@ -21,6 +21,9 @@ void rb_set_error(const char* msg);
 namespace rb {
 bool gen_large_device(double scale, uint64_t seed, bool local, rapdhg_qp_owned* out);  // gen_device.cu
 bool gen_svm_a_device(int32_t ns, int32_t nf, int32_t per_row, uint64_t seed, rapdhg_csr_owned* a);
+bool gen_lasso_core_device(int32_t nf, int32_t ns, int32_t per_row, uint64_t seed, rapdhg_csr_owned* ad, double* b,
+                           double* lam);
+bool gen_portfolio_eq_device(int32_t na, int32_t k, int32_t per_asset, uint64_t seed, rapdhg_csr_owned* eq);
 }
 
 namespace {
@@ -261,41 +264,42 @@ void gen_random_qp(double scale, uint64_t seed, rapdhg_qp_owned* out) {
 }
 
 // ---- C2: Lasso  min y'y + lambda 1't  s.t. A_d x - y = b, x - t <= 0, -x - t <= 0
-// variables [x (nf) | y (ns) | t (nf)]
-void gen_lasso(double scale, uint64_t seed, rapdhg_qp_owned* out) {
-  Rng g(seed);
+// variables [x (nf) | y (ns) | t (nf)]. Counter-based (crng.h), so the device
+// generator (gen_device.cu) builds bit-identical arrays. Exact algorithm:
+//  * v_j = 0 if uniform(kLassoV, j, 0) < 1/2, else normal(kLassoV, j, 1) / sqrt(nf);
+//  * A_d row r: `per_row` draws q, column below(uniform(kLassoCol, r, q), nf),
+//    value normal(kLassoVal, r, q); sorted by (column, q), duplicate columns
+//    summed in that order (a zero sum dropped);
+//  * b_r = (sum over the row's entries in column order of a * v_col, unfused)
+//    + normal(kLassoNoise, r, 0);
+//  * lambda = max_c |sum over rows r ascending of A_d[r, c] * b_r| / 5 (each
+//    column summed sequentially in row order, unfused).
+struct LassoDims {
+  int32_t nf, ns, per_row;
+};
+LassoDims lasso_dims(double scale) {
   const int32_t nf = std::max<int32_t>(2, static_cast<int32_t>(std::lround(100000 * scale)));
   const int32_t ns = std::max<int32_t>(1, static_cast<int32_t>(std::lround(10000 * scale)));
-  const int32_t n = 2 * nf + ns;
-  const int32_t per_row = std::max<int32_t>(1, static_cast<int32_t>(std::lround(0.01 * nf)));
-  std::vector<double> v(nf);
-  for (auto& x : v) x = (g.uniform() < 0.5) ? 0.0 : g.normal() / std::sqrt(static_cast<double>(nf));
-  Triplets ad(ns, nf);
-  ad.reserve(static_cast<std::size_t>(ns) * per_row);
-  std::vector<int32_t> cols;
+  return {nf, ns, std::max<int32_t>(1, static_cast<int32_t>(std::lround(0.01 * nf)))};
+}
+
+// the structure around A_d, b and lambda (shared by the host and device paths)
+void lasso_assemble(const LassoDims& d, const rapdhg_csr_owned& Ad, const std::vector<double>& b, double lam,
+                    rapdhg_qp_owned* out) {
+  const int32_t nf = d.nf, ns = d.ns, n = 2 * nf + ns;
+  // equality block: [A_d, -I, 0] (the -1 is after every A_d column)
+  rapdhg_csr_owned& eq = out->a_eq;
+  eq.n_rows = ns, eq.n_cols = n, eq.nnz = Ad.nnz + ns;
+  eq.row_ptr = xalloc<int32_t>(static_cast<std::size_t>(ns) + 1);
+  eq.col_idx = xalloc<int32_t>(static_cast<std::size_t>(eq.nnz));
+  eq.values = xalloc<double>(static_cast<std::size_t>(eq.nnz));
+  eq.row_ptr[0] = 0;
   for (int32_t r = 0; r < ns; ++r) {
-    sample_cols(g, per_row, 0, nf, cols);
-    for (int32_t c : cols) ad.add(r, c, g.normal());
+    int64_t w = eq.row_ptr[r];
+    for (int32_t k = Ad.row_ptr[r]; k < Ad.row_ptr[r + 1]; ++k, ++w) eq.col_idx[w] = Ad.col_idx[k], eq.values[w] = Ad.values[k];
+    eq.col_idx[w] = nf + r, eq.values[w] = -1.0;
+    eq.row_ptr[r + 1] = static_cast<int32_t>(w + 1);
   }
-  rapdhg_csr_owned Ad{};
-  build_csr(ad, &Ad);
-  std::vector<double> b = host_mv(Ad, v);
-  for (auto& x : b) x += g.normal();
-  // lambda = ||A_d' b||_inf / 5
-  std::vector<double> atb(nf, 0.0);
-  for (int32_t r = 0; r < ns; ++r)
-    for (int32_t k = Ad.row_ptr[r]; k < Ad.row_ptr[r + 1]; ++k) atb[Ad.col_idx[k]] += Ad.values[k] * b[r];
-  double lam = 0.0;
-  for (double x : atb) lam = std::max(lam, std::fabs(x));
-  lam /= 5.0;
-  // equality block: [A_d, -I, 0]
-  Triplets eq(ns, n);
-  eq.reserve(Ad.nnz + ns);
-  for (int32_t r = 0; r < ns; ++r) {
-    for (int32_t k = Ad.row_ptr[r]; k < Ad.row_ptr[r + 1]; ++k) eq.add(r, Ad.col_idx[k], Ad.values[k]);
-    eq.add(r, nf + r, -1.0);
-  }
-  std::free(Ad.row_ptr), std::free(Ad.col_idx), std::free(Ad.values);
   // inequality block: x_j - t_j <= 0 ; -x_j - t_j <= 0
   Triplets in(2 * nf, n);
   in.reserve(4 * static_cast<std::size_t>(nf));
@@ -309,46 +313,146 @@ void gen_lasso(double scale, uint64_t seed, rapdhg_qp_owned* out) {
   for (int32_t j = 0; j < nf; ++j) c[nf + ns + j] = lam;
   build_csr(q, &out->q);
   build_csr(in, &out->a_ineq);
-  build_csr(eq, &out->a_eq);
   out->n = n, out->m_ineq = 2 * nf, out->m_eq = ns;
   out->c = vec_copy(c);
-  out->b_ineq = vec_copy(std::vector<double>(2 * nf, 0.0));
+  out->b_ineq = vec_copy(std::vector<double>(2 * static_cast<std::size_t>(nf), 0.0));
   out->b_eq = vec_copy(b);
 }
 
+void gen_lasso(double scale, uint64_t seed, rapdhg_qp_owned* out) {
+  using namespace rb::crng;
+  const LassoDims d = lasso_dims(scale);
+  const int32_t nf = d.nf, ns = d.ns, per_row = d.per_row;
+  {  // A_d, b and lambda on the device for large instances
+    rapdhg_csr_owned Ad{};
+    std::vector<double> b(ns);
+    double lam = 0.0;
+    if (use_device_generator(scale >= 0.05) && rb::gen_lasso_core_device(nf, ns, per_row, seed, &Ad, b.data(), &lam)) {
+      lasso_assemble(d, Ad, b, lam, out);
+      std::free(Ad.row_ptr), std::free(Ad.col_idx), std::free(Ad.values);
+      return;
+    }
+  }
+  const double sq = std::sqrt(static_cast<double>(nf));
+  std::vector<double> v(nf);
+  parallel_rows(nf, [&](int64_t j) {
+    v[j] = uniform(seed, kLassoV, j, 0) < 0.5 ? 0.0 : normal(seed, kLassoV, j, 1) / sq;
+  });
+  // A_d rows: sort each row's draws by (column, draw), merge duplicates
+  std::vector<std::vector<int32_t>> rc(ns);
+  std::vector<std::vector<double>> rv(ns);
+  std::vector<double> b(ns);
+  parallel_rows(ns, [&](int64_t r) {
+    std::vector<std::pair<int32_t, int32_t>> e(per_row);
+    for (int32_t q = 0; q < per_row; ++q)
+      e[q] = {static_cast<int32_t>(below(uniform(seed, kLassoCol, r, q), static_cast<uint64_t>(nf))), q};
+    std::sort(e.begin(), e.end());
+    double acc = 0.0;
+    for (int32_t k = 0; k < per_row;) {
+      double x = normal(seed, kLassoVal, r, e[k].second);
+      int32_t q = k + 1;
+      for (; q < per_row && e[q].first == e[k].first; ++q) x = x + normal(seed, kLassoVal, r, e[q].second);
+      if (x != 0.0) {
+        rc[r].push_back(e[k].first), rv[r].push_back(x);
+        acc = acc + x * v[e[k].first];
+      }
+      k = q;
+    }
+    b[r] = acc + normal(seed, kLassoNoise, r, 0);
+  });
+  rapdhg_csr_owned Ad{};
+  Ad.n_rows = ns, Ad.n_cols = nf;
+  Ad.row_ptr = xalloc<int32_t>(static_cast<std::size_t>(ns) + 1);
+  Ad.row_ptr[0] = 0;
+  for (int32_t r = 0; r < ns; ++r) Ad.row_ptr[r + 1] = Ad.row_ptr[r] + static_cast<int32_t>(rc[r].size());
+  Ad.nnz = Ad.row_ptr[ns];
+  Ad.col_idx = xalloc<int32_t>(static_cast<std::size_t>(Ad.nnz));
+  Ad.values = xalloc<double>(static_cast<std::size_t>(Ad.nnz));
+  for (int32_t r = 0; r < ns; ++r) {
+    std::copy(rc[r].begin(), rc[r].end(), Ad.col_idx + Ad.row_ptr[r]);
+    std::copy(rv[r].begin(), rv[r].end(), Ad.values + Ad.row_ptr[r]);
+  }
+  // lambda = ||A_d' b||_inf / 5, each column summed in row order
+  std::vector<double> atb(nf, 0.0);
+  for (int32_t r = 0; r < ns; ++r)
+    for (int32_t k = Ad.row_ptr[r]; k < Ad.row_ptr[r + 1]; ++k) atb[Ad.col_idx[k]] = atb[Ad.col_idx[k]] + Ad.values[k] * b[r];
+  double lam = 0.0;
+  for (double x : atb) lam = std::max(lam, std::fabs(x));
+  lam /= 5.0;
+  lasso_assemble(d, Ad, b, lam, out);
+  std::free(Ad.row_ptr), std::free(Ad.col_idx), std::free(Ad.values);
+}
+
 // ---- C3: Markowitz  min x'Dx + y'y - mu'x  s.t. y - F'x = 0, 1'x = 1, x >= 0
-// variables [x (na) | y (k)]
+// variables [x (na) | y (k)]. Counter-based (crng.h; device: gen_device.cu):
+//  * asset i draws q < per_asset: factor f = below(uniform(kPfF, i, q), k),
+//    loading -normal(kPfVal, i, q); factor row f holds its entries in asset
+//    order, duplicates (same f, i) summed in draw order (a zero sum dropped),
+//    then (f, na + f) = 1;
+//  * budget row k: (k, i) = 1; bounds -x_i <= 0;
+//  * Q = diag(2 (uniform(kPfD, i, 0) sqrt(k))) on x, 2 on y; c_i = -normal(kPfMu, i, 0).
 void gen_portfolio(double scale, uint64_t seed, rapdhg_qp_owned* out) {
-  Rng g(seed);
+  using namespace rb::crng;
   const int32_t na = std::max<int32_t>(4, static_cast<int32_t>(std::lround(1000000 * scale)));
   const int32_t k = std::max<int32_t>(2, static_cast<int32_t>(std::lround(1000 * scale)));
   const int32_t per_asset = std::min<int32_t>(20, k);
   const int32_t n = na + k;
-  Triplets eq(k + 1, n);
-  eq.reserve(static_cast<std::size_t>(na) * (per_asset + 1) + k);
-  std::vector<int32_t> cols;
-  // factor rows: y_f - sum_i F_if x_i = 0, built column-by-column (asset order)
-  for (int32_t i = 0; i < na; ++i) {
-    sample_cols(g, per_asset, 0, k, cols);
-    for (int32_t f : cols) eq.add(f, i, -g.normal());
+  rapdhg_csr_owned& eq = out->a_eq;
+  if (!(use_device_generator(scale >= 0.05) && rb::gen_portfolio_eq_device(na, k, per_asset, seed, &eq))) {
+    // factor rows by counting sort of the draws (stable: asset order, then draw order)
+    std::vector<int32_t> f(static_cast<std::size_t>(na) * per_asset);
+    parallel_rows(na, [&](int64_t i) {
+      for (int32_t q = 0; q < per_asset; ++q)
+        f[i * per_asset + q] = static_cast<int32_t>(below(uniform(seed, kPfF, i, q), static_cast<uint64_t>(k)));
+    });
+    std::vector<int64_t> start(static_cast<std::size_t>(k) + 1, 0);
+    for (int32_t x : f) ++start[x + 1];
+    for (int32_t g = 0; g < k; ++g) start[g + 1] += start[g];
+    std::vector<int64_t> slot(start.begin(), start.end() - 1), draw(f.size());
+    for (int64_t t = 0; t < static_cast<int64_t>(f.size()); ++t) draw[slot[f[t]]++] = t;  // t = i * per_asset + q
+    std::vector<std::vector<int32_t>> rc(k + 1);
+    std::vector<std::vector<double>> rv(k + 1);
+    parallel_rows(k, [&](int64_t g) {
+      for (int64_t a = start[g]; a < start[g + 1];) {
+        const int64_t i = draw[a] / per_asset;
+        double x = -normal(seed, kPfVal, i, static_cast<uint32_t>(draw[a] % per_asset));
+        int64_t b2 = a + 1;
+        for (; b2 < start[g + 1] && draw[b2] / per_asset == i; ++b2)
+          x = x + -normal(seed, kPfVal, i, static_cast<uint32_t>(draw[b2] % per_asset));
+        if (x != 0.0) rc[g].push_back(static_cast<int32_t>(i)), rv[g].push_back(x);
+        a = b2;
+      }
+      rc[g].push_back(na + static_cast<int32_t>(g)), rv[g].push_back(1.0);
+    });
+    for (int32_t i = 0; i < na; ++i) rc[k].push_back(i), rv[k].push_back(1.0);  // budget row 1'x = 1
+    eq.n_rows = k + 1, eq.n_cols = n;
+    eq.row_ptr = xalloc<int32_t>(static_cast<std::size_t>(k) + 2);
+    eq.row_ptr[0] = 0;
+    for (int32_t g = 0; g <= k; ++g) eq.row_ptr[g + 1] = eq.row_ptr[g] + static_cast<int32_t>(rc[g].size());
+    eq.nnz = eq.row_ptr[k + 1];
+    eq.col_idx = xalloc<int32_t>(static_cast<std::size_t>(eq.nnz));
+    eq.values = xalloc<double>(static_cast<std::size_t>(eq.nnz));
+    for (int32_t g = 0; g <= k; ++g) {
+      std::copy(rc[g].begin(), rc[g].end(), eq.col_idx + eq.row_ptr[g]);
+      std::copy(rv[g].begin(), rv[g].end(), eq.values + eq.row_ptr[g]);
+    }
   }
-  for (int32_t f = 0; f < k; ++f) eq.add(f, na + f, 1.0);
-  for (int32_t i = 0; i < na; ++i) eq.add(k, i, 1.0);  // budget row 1'x = 1
   Triplets in(na, n);
   in.reserve(na);
   for (int32_t i = 0; i < na; ++i) in.add(i, i, -1.0);  // -x <= 0
+  std::vector<double> qd(n, 2.0), c(n, 0.0);
+  const double sk = std::sqrt(static_cast<double>(k));
+  parallel_rows(na, [&](int64_t i) {
+    qd[i] = 2.0 * (uniform(seed, kPfD, i, 0) * sk);
+    c[i] = -normal(seed, kPfMu, i, 0);
+  });
   Triplets q(n, n);
   q.reserve(n);
-  const double sk = std::sqrt(static_cast<double>(k));
-  for (int32_t i = 0; i < na; ++i) q.add(i, i, 2.0 * (g.uniform() * sk));
-  for (int32_t f = 0; f < k; ++f) q.add(na + f, na + f, 2.0);
-  std::vector<double> c(n, 0.0);
-  for (int32_t i = 0; i < na; ++i) c[i] = -g.normal();
+  for (int32_t i = 0; i < n; ++i) q.add(i, i, qd[i]);
   std::vector<double> beq(k + 1, 0.0);
   beq[k] = 1.0;
   build_csr(q, &out->q);
   build_csr(in, &out->a_ineq);
-  build_csr(eq, &out->a_eq);
   out->n = n, out->m_ineq = na, out->m_eq = k + 1;
   out->c = vec_copy(c);
   out->b_ineq = vec_copy(std::vector<double>(na, 0.0));

@@ -1,6 +1,6 @@
-"""Counter-based generators (csrc/crng.h): C5 (host.cpp gen_large +
-gen_device.cu) and C4 SVM (host.cpp gen_svm + gen_device.cu, restated in numpy
-by oracle/synth.py for the reference arm).
+"""Counter-based generators (csrc/crng.h): C2 Lasso, C3 portfolio, C4 SVM and
+C5 (host.cpp + gen_device.cu; C4 also restated in numpy by oracle/synth.py
+for the reference arm).
 CPU: the host reference yields valid, deterministic instances with a
 symmetric, diagonally dominant Q; the numpy SVM restatement equals the
 library's arrays. GPU: the device generators' arrays are bit-identical to the
@@ -98,4 +98,42 @@ def test_device_svm_generator_bit_identical(monkeypatch):
     monkeypatch.setenv("RAPDHG_GEN_DEVICE", "0")
     h = rb.generate(rb.Gen.SVM, 0.03, 4)
     for a, b in zip(arrays(d), arrays(h)):
+        assert a.shape == b.shape and np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("kind,scale", [(rb.Gen.LASSO, 0.002), (rb.Gen.PORTFOLIO, 0.002)])
+def test_host_c2_c3_valid_and_deterministic(kind, scale, monkeypatch):
+    """Counter-based C2 Lasso / C3 portfolio: canonical CSRs, the SURVEY
+    structure, deterministic in the seed."""
+    monkeypatch.setenv("RAPDHG_GEN_DEVICE", "0")
+    p = rb.generate(kind, scale, 3)
+    for mat in (p.q, p.a_ineq, p.a_eq):
+        rp, ci = mat.row_ptr, mat.col_idx
+        assert rp[0] == 0 and rp[-1] == len(ci) and np.all(np.diff(rp) >= 0)
+        for r in range(mat.n_rows):
+            assert np.all(np.diff(ci[rp[r]:rp[r + 1]]) > 0)
+    if kind == rb.Gen.LASSO:
+        nf, ns = 200, 20
+        assert p.num_vars() == 2 * nf + ns and p.num_ineq() == 2 * nf and p.num_eq() == ns
+        assert np.all(p.c[nf + ns:] == p.c[-1]) and p.c[-1] > 0  # lambda on t
+    else:
+        na, k = 2000, 2
+        assert p.num_vars() == na + k and p.num_ineq() == na and p.num_eq() == k + 1
+        assert np.all(p.a_eq.values[p.a_eq.row_ptr[k]:] == 1.0) and p.b_eq[k] == 1.0  # budget row
+    q = rb.generate(kind, scale, 3)
+    assert all(np.array_equal(a, b) for a, b in zip(arrays(p), arrays(q)))
+    assert np.array_equal(p.a_eq.values, q.a_eq.values)
+    assert not np.array_equal(p.a_eq.values, rb.generate(kind, scale, 4).a_eq.values)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,scale", [(rb.Gen.LASSO, 0.01), (rb.Gen.LASSO, 0.3), (rb.Gen.PORTFOLIO, 0.01),
+                                        (rb.Gen.PORTFOLIO, 0.2)])
+def test_device_c2_c3_generators_bit_identical(kind, scale, monkeypatch):
+    monkeypatch.setenv("RAPDHG_GEN_DEVICE", "1")
+    d = rb.generate(kind, scale, 2)
+    monkeypatch.setenv("RAPDHG_GEN_DEVICE", "0")
+    h = rb.generate(kind, scale, 2)
+    for a, b in zip(arrays(d) + [d.a_eq.col_idx, d.a_eq.values, d.b_eq],
+                    arrays(h) + [h.a_eq.col_idx, h.a_eq.values, h.b_eq]):
         assert a.shape == b.shape and np.array_equal(a, b)

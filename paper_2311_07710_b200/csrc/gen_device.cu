@@ -544,7 +544,7 @@ bool gen_portfolio_eq_device(int32_t na, int32_t k, int32_t per_asset, uint64_t 
   RB_LAUNCH_CHECK();
   sort_u64_pairs(key, key_s, idx, idx_s, nt, 32 + bits_for(static_cast<uint64_t>(k)), st);
   key_row_start_kernel<<<g1(static_cast<int64_t>(k) + 1), 256, 0, st>>>(k, key_s.get(), nt, rs.get());
-  pf_rows_kernel<false><<<g1(k), 128, 0, st>>>(k, na, per_asset, seed, key_s.get(), idx_s.get(), rs.get(), nullptr,
+  pf_rows_kernel<false><<<g1(k), 256, 0, st>>>(k, na, per_asset, seed, key_s.get(), idx_s.get(), rs.get(), nullptr,
                                                cnt.get(), nullptr, nullptr);
   RB_LAUNCH_CHECK();
   fill_one_kernel<<<1, 1, 0, st>>>(cnt.get() + k, na);  // the budget row
@@ -553,7 +553,7 @@ bool gen_portfolio_eq_device(int32_t na, int32_t k, int32_t per_asset, uint64_t 
   RB_CUDA(cudaMemcpyAsync(&nnz, rp.get() + k + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   RB_CUDA(cudaStreamSynchronize(st));
   ci.alloc(nnz), val.alloc(nnz);
-  pf_rows_kernel<true><<<g1(k), 128, 0, st>>>(k, na, per_asset, seed, key_s.get(), idx_s.get(), rs.get(), rp.get(),
+  pf_rows_kernel<true><<<g1(k), 256, 0, st>>>(k, na, per_asset, seed, key_s.get(), idx_s.get(), rs.get(), rp.get(),
                                               nullptr, ci.get(), val.get());
   pf_budget_kernel<<<g1(na), 256, 0, st>>>(na, nnz - na, ci.get(), val.get());
   RB_LAUNCH_CHECK();

@@ -65,6 +65,26 @@ __global__ void lower_bounds_kernel(const int32_t* list, const int32_t* count, c
   pos[j] = lo;
 }
 
+__global__ void invert_kernel(const uint8_t* a, uint8_t* b, int64_t n) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) b[i] = !a[i];
+}
+
+// flag[i] = 1 when row r0 + i of [seg1 | seg2] references a column outside
+// [lo1, hi1) (segment 1) or [lo2, hi2) (segment 2): a boundary row
+__global__ void boundary_kernel(const int32_t* rp1, const int32_t* ci1, int64_t lo1, int64_t hi1, const int32_t* rp2,
+                                const int32_t* ci2, int64_t lo2, int64_t hi2, int64_t r0, int64_t rows,
+                                uint8_t* flag) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= rows) return;
+  const int64_t r = r0 + i;
+  uint8_t b = 0;
+  for (int k = rp1[r]; k < rp1[r + 1] && !b; ++k) b = ci1[k] < lo1 || ci1[k] >= hi1;
+  if (rp2)
+    for (int k = rp2[r]; k < rp2[r + 1] && !b; ++k) b = ci2[k] < lo2 || ci2[k] >= hi2;
+  flag[i] = b;
+}
+
 // Boundaries of `parts` contiguous blocks of rows with costs len[r] + 2,
 // inner boundaries rounded to multiples of kRedChunk (never decreasing).
 std::vector<int32_t> balanced_bounds(const std::vector<int64_t>& cost_prefix, int32_t rows, int parts) {
@@ -378,6 +398,11 @@ struct ShardedEngine::Shard {
   ColBlockedDual cbd;  // column blocks over the owned rows (same block counts as one GPU)
   ColBlockedPrimal cbp;
   SellPlan sell_dual, sell_primal;  // sliced ELL over the owned rows (plain path)
+  // overlap (plain path): rows whose entries are all owned ("interior") run
+  // while the exchange of the step's gathered vector is in flight; the
+  // others ("boundary") after it. Same per-row arithmetic as one launch.
+  Schedule sch_dual_in, sch_dual_bd, sch_primal_in, sch_primal_bd;
+  SellPlan sell_dual_in, sell_dual_bd, sell_primal_in, sell_primal_bd;
   // full-length copies; only the owned slice is computed here, the rest is
   // received by the exchanges
   DevBuf<double> X[2], XMD[2], w, xb, y, yb, epx, epy, xu[2], yu[2], ax[2], qx[2], aty[2], best_x, best_y;
@@ -485,8 +510,72 @@ ShardedEngine::ShardedEngine(const rapdhg_qp& p, const rapdhg_config& cfg, int p
       fill_sell_values(sh->sell_primal, full_->qsv_, full_->atsv_, st_);
     }
   }
+  build_overlap();
   build_halos();
   RB_CUDA(cudaStreamSynchronize(st_));
+}
+
+// Interior / boundary row lists of each shard's plain-path ops (see Shard).
+// Global decision: an op overlaps when it is on the plain path everywhere (no
+// slab windows, no column blocks), parts > 1 and RAPDHG_OVERLAP is not 0.
+void ShardedEngine::build_overlap() {
+  const char* env = std::getenv("RAPDHG_OVERLAP");
+  if ((env && env[0] == '0') || parts_ < 2) return;
+  const Engine& e = *full_;
+  DeviceQP& P = *e.P_;
+  overlap_dual_ = e.dual_choice_.empty() && e.cb_nb_dual_ <= 1;
+  overlap_primal_ = e.primal_choice_.empty() && e.cb_nq_ <= 1 && e.cb_na_ <= 1;
+  if (!overlap_dual_ && !overlap_primal_) return;
+  const thrust::counting_iterator<int32_t> idx(0);
+  auto split = [&](int64_t rows, const int32_t* rp1, const int32_t* ci1, int64_t lo1, int64_t hi1,
+                   const int32_t* rp2, const int32_t* ci2, int64_t lo2, int64_t hi2, int64_t r0, bool sell,
+                   const double* v1, const double* v2, Schedule& s_in, Schedule& s_bd, SellPlan& p_in,
+                   SellPlan& p_bd) {
+    if (rows <= 0) return;
+    DevBuf<uint8_t> flag(rows), inv(rows);
+    boundary_kernel<<<grid1(rows), 256, 0, st_>>>(rp1, ci1, lo1, hi1, rp2, ci2, lo2, hi2, r0, rows, flag.get());
+    invert_kernel<<<grid1(rows), 256, 0, st_>>>(flag.get(), inv.get(), rows);
+    RB_LAUNCH_CHECK();
+    DevBuf<int32_t> lst_in(rows), lst_bd(rows), cnt(2), len;
+    std::size_t tb = 0;
+    RB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, idx, flag.get(), lst_bd.get(), cnt.get(), static_cast<int>(rows),
+                                       st_));
+    DevBuf<unsigned char> tmp(tb);
+    RB_CUDA(cub::DeviceSelect::Flagged(tmp.get(), tb, idx, inv.get(), lst_in.get(), cnt.get(), static_cast<int>(rows),
+                                       st_));
+    RB_CUDA(cub::DeviceSelect::Flagged(tmp.get(), tb, idx, flag.get(), lst_bd.get(), cnt.get() + 1,
+                                       static_cast<int>(rows), st_));
+    int32_t n[2] = {0, 0};
+    RB_CUDA(cudaMemcpyAsync(n, cnt.get(), sizeof(n), cudaMemcpyDeviceToHost, st_));
+    RB_CUDA(cudaStreamSynchronize(st_));
+    row_lengths(len, rp1 + r0, rp2 ? rp2 + r0 : nullptr, rows, st_);
+    if (sell) {
+      if (n[0]) build_sell_plan(p_in, rp1 + r0, ci1, rp2 ? rp2 + r0 : nullptr, ci2, n[0], st_, lst_in.get());
+      if (n[1]) build_sell_plan(p_bd, rp1 + r0, ci1, rp2 ? rp2 + r0 : nullptr, ci2, n[1], st_, lst_bd.get());
+      fill_sell_values(p_in, v1, v2, st_);
+      fill_sell_values(p_bd, v1, v2, st_);
+    } else {
+      if (n[0]) build_schedule(s_in, len.get(), n[0], false, st_, lst_in.get());
+      if (n[1]) build_schedule(s_bd, len.get(), n[1], false, st_, lst_bd.get());
+    }
+    RB_CUDA(cudaStreamSynchronize(st_));
+    overlap_rows_[0] += n[0], overlap_rows_[1] += n[1];
+  };
+  for (auto& sh : shards_) {
+    if (overlap_dual_)
+      split(sh->d1 - sh->d0, P.A.rp.get(), P.A.ci.get(), sh->p0, sh->p1, nullptr, nullptr, 0, 0, sh->d0,
+            e.sell_dual_, e.asv_, nullptr, sh->sch_dual_in, sh->sch_dual_bd, sh->sell_dual_in, sh->sell_dual_bd);
+    if (overlap_primal_)
+      split(sh->p1 - sh->p0, P.Q.rp.get(), P.Q.ci.get(), sh->p0, sh->p1, P.AT.rp.get(), P.AT.ci.get(), sh->d0,
+            sh->d1, sh->p0, e.sell_primal_, e.qsv_, e.atsv_, sh->sch_primal_in, sh->sch_primal_bd,
+            sh->sell_primal_in, sh->sell_primal_bd);
+  }
+  st2_ = own_st2_.create();
+  RB_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+  RB_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+  if (std::getenv("RAPDHG_TRACE"))
+    std::fprintf(stderr, "[shard] overlap dual %d primal %d: interior %lld, boundary %lld rows\n", overlap_dual_,
+                 overlap_primal_, static_cast<long long>(overlap_rows_[0]), static_cast<long long>(overlap_rows_[1]));
 }
 
 // Halo lists of the three per-step exchanges: w (gathered by the dual rows
@@ -581,9 +670,11 @@ void ShardedEngine::build_halos() {
                  static_cast<long long>(halo_entries_[2]));
 }
 
-void ShardedEngine::step_exchange(double* (*pick)(Shard&), HaloKind kind) {
+void ShardedEngine::step_exchange(double* (*pick)(Shard&), HaloKind kind, cudaStream_t st) {
   if (!halo_on_[kind]) {
-    exchange(pick, kind != kHaloY);
+    std::vector<double*> bufs;
+    for (auto& sh : shards_) bufs.push_back(pick(*sh));
+    tr_->allgatherv(bufs, kind != kHaloY ? pb_ : db_, st);
     return;
   }
   std::vector<double*> bufs;
@@ -592,7 +683,16 @@ void ShardedEngine::step_exchange(double* (*pick)(Shard&), HaloKind kind) {
     bufs.push_back(pick(*shards_[li]));
     sides.push_back(&halo_[kind][li]);
   }
-  tr_->halo(bufs, sides, st_);
+  tr_->halo(bufs, sides, st);
+}
+
+void ShardedEngine::fork() {
+  RB_CUDA(cudaEventRecord(ev_fork_, st_));
+  RB_CUDA(cudaStreamWaitEvent(st2_, ev_fork_, 0));
+}
+void ShardedEngine::join() {
+  RB_CUDA(cudaEventRecord(ev_join_, st2_));
+  RB_CUDA(cudaStreamWaitEvent(st_, ev_join_, 0));
 }
 
 ShardedEngine::~ShardedEngine() {
@@ -673,55 +773,88 @@ void ShardedEngine::body(int len, int cur) {
       ++launches_;
     }
   }
-  const int c0 = cur;
-  step_exchange([](Shard& s) { return s.w.get(); }, kHaloW);
-  if (c0 == 0) step_exchange([](Shard& s) { return s.XMD[0].get(); }, kHaloX);
-  else step_exchange([](Shard& s) { return s.XMD[1].get(); }, kHaloX);
+  // the w / x_md exchange feeding step `it`: on st2_ beside the interior dual
+  // rows when the dual overlaps, else in line on st_
+  auto exchange_wx = [&](int c_md) {
+    cudaStream_t s = overlap_dual_ ? st2_ : st_;
+    if (overlap_dual_) fork();
+    step_exchange([](Shard& sh) { return sh.w.get(); }, kHaloW, s);
+    if (c_md == 0) step_exchange([](Shard& sh) { return sh.XMD[0].get(); }, kHaloX, s);
+    else step_exchange([](Shard& sh) { return sh.XMD[1].get(); }, kHaloX, s);
+  };
+  exchange_wx(cur);
   for (int it = 0; it < len; ++it) {
     const int c = (cur + it) & 1;
-    for (auto& sh : shards_) {
-      if (sh->d1 <= sh->d0) continue;
-      DualStepOp<false> d{CsrView{P.A.rp.get() + sh->d0, P.A.ci.get(), e.asv_}, sh->w.get(), e.bsv_ + sh->d0,
-                          sh->y.get() + sh->d0, sh->yb.get() + sh->d0, e.mi_ - static_cast<int>(sh->d0),
-                          params_.get(), it, sh->bad.get()};
-      if (sh->dual_ph.active()) {
-        launches_ += launch_slab_phase(d, sh->dual_ph, st_);
-      } else if (sh->cbd.active()) {
-        launches_ += launch_colblocked_dual(d, sh->cbd, st_);
-      } else if (sh->sell_dual.active()) {
-        launch_sell(d, sh->sell_dual, st_);
-        ++launches_;
-      } else {
-        launch_rowwise(d, sh->sch_dual.view, st_);
-        ++launches_;
+    // dual step; part: 0 all rows, 1 interior rows, 2 boundary rows
+    auto dual = [&](int part) {
+      for (auto& sh : shards_) {
+        if (sh->d1 <= sh->d0) continue;
+        DualStepOp<false> d{CsrView{P.A.rp.get() + sh->d0, P.A.ci.get(), e.asv_}, sh->w.get(), e.bsv_ + sh->d0,
+                            sh->y.get() + sh->d0, sh->yb.get() + sh->d0, e.mi_ - static_cast<int>(sh->d0),
+                            params_.get(), it, sh->bad.get()};
+        if (part) {
+          const SellPlan& sp = part == 1 ? sh->sell_dual_in : sh->sell_dual_bd;
+          const Schedule& sc = part == 1 ? sh->sch_dual_in : sh->sch_dual_bd;
+          if (sp.active()) launch_sell(d, sp, st_), ++launches_;
+          else if (sc.view.total_blocks > 0) launch_rowwise(d, sc.view, st_), ++launches_;
+        } else if (sh->dual_ph.active()) {
+          launches_ += launch_slab_phase(d, sh->dual_ph, st_);
+        } else if (sh->cbd.active()) {
+          launches_ += launch_colblocked_dual(d, sh->cbd, st_);
+        } else if (sh->sell_dual.active()) {
+          launch_sell(d, sh->sell_dual, st_);
+          ++launches_;
+        } else {
+          launch_rowwise(d, sh->sch_dual.view, st_);
+          ++launches_;
+        }
       }
-    }
-    step_exchange([](Shard& s) { return s.y.get(); }, kHaloY);
-    for (auto& sh : shards_) {
-      if (sh->p1 <= sh->p0) continue;
-      const int64_t o = sh->p0;
-      PrimalStepOp<false> pr{CsrView{P.Q.rp.get() + o, P.Q.ci.get(), e.qsv_},
-                             CsrView{P.AT.rp.get() + o, P.AT.ci.get(), e.atsv_},
-                             sh->XMD[c].get(), sh->y.get(), sh->X[c].get() + o, sh->X[c ^ 1].get() + o,
-                             sh->xb.get() + o, e.csv_ + o, sh->w.get() + o, sh->XMD[c ^ 1].get() + o,
-                             params_.get(), it, sh->bad.get()};
-      if (sh->primal_ph.active()) {
-        launches_ += launch_slab_phase(pr, sh->primal_ph, st_);
-      } else if (sh->cbp.active()) {
-        launches_ += launch_colblocked_primal(pr, sh->cbp, st_);
-      } else if (sh->sell_primal.active()) {
-        launch_sell(pr, sh->sell_primal, st_);
-        ++launches_;
-      } else {
-        launch_rowwise(pr, sh->sch_primal.view, st_);
-        ++launches_;
+    };
+    auto primal = [&](int part) {
+      for (auto& sh : shards_) {
+        if (sh->p1 <= sh->p0) continue;
+        const int64_t o = sh->p0;
+        PrimalStepOp<false> pr{CsrView{P.Q.rp.get() + o, P.Q.ci.get(), e.qsv_},
+                               CsrView{P.AT.rp.get() + o, P.AT.ci.get(), e.atsv_},
+                               sh->XMD[c].get(), sh->y.get(), sh->X[c].get() + o, sh->X[c ^ 1].get() + o,
+                               sh->xb.get() + o, e.csv_ + o, sh->w.get() + o, sh->XMD[c ^ 1].get() + o,
+                               params_.get(), it, sh->bad.get()};
+        if (part) {
+          const SellPlan& sp = part == 1 ? sh->sell_primal_in : sh->sell_primal_bd;
+          const Schedule& sc = part == 1 ? sh->sch_primal_in : sh->sch_primal_bd;
+          if (sp.active()) launch_sell(pr, sp, st_), ++launches_;
+          else if (sc.view.total_blocks > 0) launch_rowwise(pr, sc.view, st_), ++launches_;
+        } else if (sh->primal_ph.active()) {
+          launches_ += launch_slab_phase(pr, sh->primal_ph, st_);
+        } else if (sh->cbp.active()) {
+          launches_ += launch_colblocked_primal(pr, sh->cbp, st_);
+        } else if (sh->sell_primal.active()) {
+          launch_sell(pr, sh->sell_primal, st_);
+          ++launches_;
+        } else {
+          launch_rowwise(pr, sh->sch_primal.view, st_);
+          ++launches_;
+        }
       }
+    };
+    if (overlap_dual_) {  // interior rows beside the w / x_md exchange, then the rest
+      dual(1);
+      join();
+      dual(2);
+    } else {
+      dual(0);
     }
-    if (it + 1 < len) {  // the next step gathers the new w and x_md
-      step_exchange([](Shard& s) { return s.w.get(); }, kHaloW);
-      if (c == 0) step_exchange([](Shard& s) { return s.XMD[1].get(); }, kHaloX);
-      else step_exchange([](Shard& s) { return s.XMD[0].get(); }, kHaloX);
+    if (overlap_primal_) {  // the y exchange beside the interior primal rows
+      fork();
+      step_exchange([](Shard& sh) { return sh.y.get(); }, kHaloY, st2_);
+      primal(1);
+      join();
+      primal(2);
+    } else {
+      step_exchange([](Shard& sh) { return sh.y.get(); }, kHaloY, st_);
+      primal(0);
     }
+    if (it + 1 < len) exchange_wx(c ^ 1);  // the next step gathers the new w and x_md
   }
 }
 

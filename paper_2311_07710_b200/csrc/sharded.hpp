@@ -98,12 +98,22 @@ class ShardedEngine : public LoopBackend {
  private:
   struct Shard;
   void body(int len, int cur);
-  void exchange(double* (*pick)(Shard&), bool primal_space);
+  void exchange(double* (*pick)(Shard&), bool primal_space);  // allgather-v on st_
   // per-step exchanges: the halo of the gathered entries when that moves at
   // most half of an allgather (RAPDHG_HALO=on|off|auto), else the allgather
   enum HaloKind { kHaloW = 0, kHaloX = 1, kHaloY = 2 };
   void build_halos();
-  void step_exchange(double* (*pick)(Shard&), HaloKind kind);
+  void build_overlap();
+  void step_exchange(double* (*pick)(Shard&), HaloKind kind, cudaStream_t st);
+  // plain-path overlap (build_overlap): the exchanges on st2_ beside the
+  // interior rows on st_
+  bool overlap_dual_ = false, overlap_primal_ = false;
+  int64_t overlap_rows_[2] = {0, 0};
+  OwnedStream own_st2_;
+  cudaStream_t st2_ = nullptr;
+  cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+  void fork();  // st2_ waits for st_
+  void join();  // st_ waits for st2_
   bool halo_on_[3] = {false, false, false};
   std::vector<std::vector<HaloSide>> halo_;  // [kind][local shard]
   int64_t halo_entries_[3] = {0, 0, 0};      // entries moved per exchange (all shards)
@@ -127,7 +137,7 @@ class ShardedEngine : public LoopBackend {
   std::map<int, int64_t> replay_launches_;
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
   int64_t launches_ = 0;
-  SyncBeforeFree sync_{&st_, nullptr};  // last member: runs first on destruction
+  SyncBeforeFree sync_{&st_, &st2_};  // last member: runs first on destruction
 };
 
 }  // namespace rb

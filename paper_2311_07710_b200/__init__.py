@@ -61,6 +61,25 @@ class QpsParseError(RuntimeError):
 _lib = None
 
 
+def _point_at_pip_nccl():
+    """The sharded solver dlopens NCCL on first use: prefer the pip NCCL that
+    torch ships (RAPDHG_NCCL_LIB), so a later `import torch` finds the NCCL it
+    was built against already loaded, not an older system libnccl.so.2."""
+    if os.environ.get("RAPDHG_NCCL_LIB"):
+        return
+    try:
+        import importlib.util
+
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        return
+    for base in (spec.submodule_search_locations or []) if spec else []:
+        cand = os.path.join(base, "lib", "libnccl.so.2")
+        if os.path.exists(cand):
+            os.environ["RAPDHG_NCCL_LIB"] = cand
+            return
+
+
 def _load():
     global _lib
     if _lib is not None:
@@ -70,6 +89,7 @@ def _load():
             f"{LIB_PATH} is missing: build it with `make -C paper_2311_07710_b200` "
             "(or __graft_entry__.build()); there is no fallback implementation")
     lib = C.CDLL(LIB_PATH)
+    _point_at_pip_nccl()
     d = abi.declare
     P = C.POINTER
     d(lib, "rapdhg_last_error", C.c_char_p)

@@ -193,7 +193,14 @@ const NcclApi& nccl() {
   static std::once_flag once;
   static std::string err;
   std::call_once(once, [] {
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    // the NCCL the process already has (e.g. torch's), else RAPDHG_NCCL_LIB
+    // (the Python binding points it at the pip NCCL torch ships), else the
+    // system one. Loading an older libnccl.so.2 first would make a later
+    // `import torch` bind to it and fail on newer symbols.
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h)
+      if (const char* path = std::getenv("RAPDHG_NCCL_LIB")) h = dlopen(path, RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
     if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
     if (!h) {
       err = std::string("cannot load libnccl: ") + dlerror();

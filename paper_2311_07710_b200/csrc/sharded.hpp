@@ -103,7 +103,7 @@ class ShardedEngine : public LoopBackend {
   // most half of an allgather (RAPDHG_HALO=on|off|auto), else the allgather
   enum HaloKind { kHaloW = 0, kHaloX = 1, kHaloY = 2 };
   void build_halos();
-  void build_overlap();
+  void build_overlap(bool emulated);
   void step_exchange(double* (*pick)(Shard&), HaloKind kind, cudaStream_t st);
   // plain-path overlap (build_overlap): the exchanges on st2_ beside the
   // interior rows on st_

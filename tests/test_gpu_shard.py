@@ -105,6 +105,7 @@ def test_overlapped_exchanges_bit_identical(parts, halo, monkeypatch):
     rows (graph-captured with a fork / join). Bit-identical to one GPU and to
     the serialised schedule (RAPDHG_OVERLAP=0), halos and allgathers alike."""
     monkeypatch.setenv("RAPDHG_HALO", halo)
+    monkeypatch.setenv("RAPDHG_OVERLAP", "1")  # (emulated shards default to the serial schedule)
     p = rb.generate(rb.Gen.LARGE_LOCAL, 0.002, 5)
     cfg = rb.SolverConfig(tol=1e-6, max_iters=800, snapshot_interval=80, record_restart_points=True)
     a = rb.solve_sharded(p, cfg, parts)

@@ -91,6 +91,12 @@ typedef struct {
   double obj_offset;
   const char* name;              /* QuadraticProgram::name; NULL = "" */
   const char* const* var_names;  /* n entries (var_names), or NULL = none */
+  /* B200 extension, no reference counterpart (the reference turns variable
+   * bounds into singleton <= rows: canonicalize, problem.hpp:178-185): bounds
+   * l <= x <= u (n each, +-inf allowed; NULL = none) enforced by projecting
+   * the primal step, for rapdhg_config.box_projection = 1 only. */
+  const double* lower;
+  const double* upper;
 } rapdhg_qp;
 
 /* ---- options ----------------------------------------------------------- */
@@ -121,6 +127,10 @@ typedef struct {
   int32_t use_graphs;    /* capture each check interval in a CUDA graph */
   int32_t profile_kernels; /* 1: CUDA events around the two steps of every 32nd chunk;
                              2: in-loop step times from %globaltimer stamps (slab path) */
+  int32_t box_projection; /* 1: honour rapdhg_qp.lower / upper by projecting the primal
+                             step onto the box (north_star's "primal step with box
+                             projection"; fast mode only; no reference counterpart, so
+                             not a parity mode); relKKT then uses the bound multipliers */
 } rapdhg_config;
 
 void rapdhg_config_default(rapdhg_config* cfg);
@@ -376,6 +386,8 @@ typedef struct {
   double obj_offset;
   char* name;        /* malloc'd, or NULL */
   char** var_names;  /* n malloc'd strings, or NULL */
+  double* lower;     /* n, or NULL: bounds kept out of the rows (rapdhg_canonicalize_box) */
+  double* upper;
 } rapdhg_qp_owned;
 
 /* SparseMatrix(n_rows, n_cols, triplets) (sparse.hpp:31-62): sort by
@@ -426,6 +438,9 @@ typedef struct {
  * the reference) return RAPDHG_E_INVALID_ARGUMENT with the same messages.
  * map may be NULL. Host-only. */
 int rapdhg_canonicalize(const rapdhg_raw_problem* raw, rapdhg_qp_owned* out, rapdhg_canonical_map* map);
+/* The same, except that variable bounds stay out of the rows: out->lower /
+ * out->upper hold them (for box_projection = 1). B200 extension. */
+int rapdhg_canonicalize_box(const rapdhg_raw_problem* raw, rapdhg_qp_owned* out, rapdhg_canonical_map* map);
 void rapdhg_canonical_map_free(rapdhg_canonical_map* map);
 
 /* QPS (MPS + QUADOBJ/QMATRIX) text or file -> canonical QP: parse_qps

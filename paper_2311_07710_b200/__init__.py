@@ -142,6 +142,7 @@ def _load():
     d(lib, "rapdhg_host_transport_check", C.c_int, P(abi.HostTransport), C.c_int32, C.c_int32, C.c_int64)
     d(lib, "rapdhg_canonicalize", C.c_int, P(abi.RawProblem), P(abi.QpOwned), P(abi.CanonicalMap))
     d(lib, "rapdhg_canonical_map_free", None, P(abi.CanonicalMap))
+    d(lib, "rapdhg_canonicalize_box", C.c_int, P(abi.RawProblem), P(abi.QpOwned), P(abi.CanonicalMap))
     d(lib, "rapdhg_parse_qps_map", C.c_int, C.c_char_p, P(abi.QpOwned), P(abi.CanonicalMap))
     d(lib, "rapdhg_parse_qps_file_map", C.c_int, C.c_char_p, P(abi.QpOwned), P(abi.CanonicalMap))
     d(lib, "rapdhg_unscale_point", C.c_int, abi.P_f64, abi.P_f64, C.c_int32, C.c_int32, C.c_int32,
@@ -313,6 +314,9 @@ class QuadraticProgram:
     name: str = ""
     obj_offset: float = 0.0
     var_names: List[str] = field(default_factory=list)
+    # B200 extension (box_projection): l <= x <= u, None = none
+    lower: Optional[np.ndarray] = None
+    upper: Optional[np.ndarray] = None
 
     def num_vars(self) -> int:
         return len(self.c)
@@ -345,11 +349,16 @@ class QuadraticProgram:
         names = None
         if self.var_names:  # kept alive with the struct (it refers to them)
             names = (C.c_char_p * len(self.var_names))(*[v.encode() for v in self.var_names])
+        lo = _f64(self.lower) if self.lower is not None else None
+        hi = _f64(self.upper) if self.upper is not None else None
+        if (lo is not None and len(lo) != len(self.c)) or (hi is not None and len(hi) != len(self.c)):
+            raise InvalidArgument("bounds must have num_vars entries")
         s = abi.Qp(len(self.c), len(self.b_ineq), len(self.b_eq), self.q._csr(), _pf(self.c),
                    self.a_ineq._csr(), _pf(self.b_ineq), self.a_eq._csr(), _pf(self.b_eq),
                    float(self.obj_offset), (self.name or "").encode(),
-                   C.cast(names, C.POINTER(C.c_char_p)) if names is not None else None)
-        s._keep = names
+                   C.cast(names, C.POINTER(C.c_char_p)) if names is not None else None,
+                   _pf(lo) if lo is not None else None, _pf(hi) if hi is not None else None)
+        s._keep = (names, lo, hi)
         return s
 
 
@@ -419,6 +428,7 @@ class SolverConfig:
     strict_parity: bool = False
     use_graphs: bool = True
     profile_kernels: int = 0  # 1: CUDA events around the steps of sampled chunks; 2: in-loop step stamps
+    box_projection: bool = False  # B200 extension: honour QuadraticProgram.lower / upper by projection
 
     def _struct(self) -> abi.Config:
         c = abi.Config()
@@ -431,6 +441,7 @@ class SolverConfig:
         c.record_restart_points = int(bool(self.record_restart_points))
         c.device, c.strict_parity = int(self.device), int(bool(self.strict_parity))
         c.use_graphs, c.profile_kernels = int(bool(self.use_graphs)), int(self.profile_kernels)
+        c.box_projection = int(bool(self.box_projection))
         return c
 
 
@@ -999,9 +1010,11 @@ def _map_from(m: abi.CanonicalMap) -> CanonicalMap:
                         [m.eq_labels[i].decode() for i in range(m.n_eq)])
 
 
-def canonicalize(raw: RawProblem) -> Tuple[QuadraticProgram, CanonicalMap]:
+def canonicalize(raw: RawProblem, keep_bounds: bool = False) -> Tuple[QuadraticProgram, CanonicalMap]:
     """canonicalize (problem.hpp:131-198) through the C-ABI (host): returns
-    CanonicalProblem{qp, map} as a pair."""
+    CanonicalProblem{qp, map} as a pair. keep_bounds (B200 extension, for
+    SolverConfig.box_projection): variable bounds stay in qp.lower / qp.upper
+    instead of becoming singleton rows."""
     L = _load()
     n, m = raw.num_vars(), raw.num_rows()
     c, rhs = _f64(raw.c), _f64(raw.rhs)
@@ -1017,7 +1030,8 @@ def canonicalize(raw: RawProblem) -> Tuple[QuadraticProgram, CanonicalMap]:
                         C.cast(rn, C.POINTER(C.c_char_p)) if rn is not None else None,
                         C.cast(vn, C.POINTER(C.c_char_p)) if vn is not None else None)
     o, mp = abi.QpOwned(), abi.CanonicalMap()
-    _check(L.rapdhg_canonicalize(C.byref(st), C.byref(o), C.byref(mp)))
+    fn = L.rapdhg_canonicalize_box if keep_bounds else L.rapdhg_canonicalize
+    _check(fn(C.byref(st), C.byref(o), C.byref(mp)))
     try:
         return qp_from_owned(o), _map_from(mp)
     finally:
@@ -1082,7 +1096,37 @@ def qp_from_owned(o: abi.QpOwned, name: str = "") -> QuadraticProgram:
         name = o.name.decode()
     var_names = [o.var_names[j].decode() for j in range(o.n)] if o.var_names else []
     return QuadraticProgram(csr(o.q), _arr(o.c, o.n), csr(o.a_ineq), _arr(o.b_ineq, o.m_ineq),
-                            csr(o.a_eq), _arr(o.b_eq, o.m_eq), name, o.obj_offset, var_names)
+                            csr(o.a_eq), _arr(o.b_eq, o.m_eq), name, o.obj_offset, var_names,
+                            _arr(o.lower, o.n) if o.lower else None, _arr(o.upper, o.n) if o.upper else None)
+
+
+def bounds_from_rows(p: QuadraticProgram) -> QuadraticProgram:
+    """Inverse of canonicalize's bound rows (problem.hpp:178-185), for
+    SolverConfig.box_projection (B200 extension): every singleton row
+    a x_j <= b of the inequality block becomes the bound x_j <= b / a (a > 0)
+    or x_j >= b / a (a < 0), the tightest one per variable; the other rows stay
+    in order. Host-side, O(nnz)."""
+    A, n = p.a_ineq, p.num_vars()
+    lens = np.diff(A.row_ptr)
+    single = np.flatnonzero(lens == 1)
+    single = single[A.values[A.row_ptr[single]] != 0]  # 0 x_j <= b stays a row
+    lo = np.full(n, -np.inf) if p.lower is None else _f64(p.lower).copy()
+    hi = np.full(n, np.inf) if p.upper is None else _f64(p.upper).copy()
+    j = A.col_idx[A.row_ptr[single]]
+    a = A.values[A.row_ptr[single]]
+    v = _f64(p.b_ineq)[single] / a
+    np.minimum.at(hi, j[a > 0], v[a > 0])
+    np.maximum.at(lo, j[a < 0], v[a < 0])
+    keep = np.ones(A.rows(), bool)
+    keep[single] = False
+    kept = np.flatnonzero(keep)
+    starts, kl = A.row_ptr[:-1][kept], lens[kept]
+    idx = np.repeat(starts - np.concatenate([[0], np.cumsum(kl)[:-1]]), kl) + np.arange(int(kl.sum()))
+    a2 = SparseMatrix.from_csr(len(kept), n, np.concatenate([[0], np.cumsum(kl)]).astype(np.int32),
+                               A.col_idx[idx], A.values[idx])
+    return QuadraticProgram(p.q, p.c, a2, _f64(p.b_ineq)[kept], p.a_eq, p.b_eq, p.name, p.obj_offset,
+                            list(p.var_names), lo if np.isfinite(lo).any() else None,
+                            hi if np.isfinite(hi).any() else None)
 
 
 def generate(kind: Gen, scale: float = 1.0, seed: int = 1) -> QuadraticProgram:
@@ -1104,7 +1148,7 @@ __all__ = [
     "ruiz_scaling", "apply_scaling", "unscale_point", "scale_point", "estimate_op_norm",
     "estimate_op_norm_symmetric", "step_schedule_theoretical", "pdhg_constant_steps",
     "adaptive_eta", "primal_weight_init", "primal_weight_update", "restart_decision", "generate",
-    "RowType", "RawProblem", "CanonicalMap", "canonicalize", "parse_qps_with_map", "symmetry_gap",
+    "RowType", "RawProblem", "CanonicalMap", "canonicalize", "bounds_from_rows", "parse_qps_with_map", "symmetry_gap",
     "spmv", "spmv_t", "to_string", "parse_qps", "read_qps", "write_qps", "device_count", "lib", "InvalidArgument", "NoDeviceError",
     "CudaError", "QpsParseError",
 ]

@@ -28,7 +28,8 @@ class Qp(C.Structure):
     _fields_ = [("n", i32), ("m_ineq", i32), ("m_eq", i32),
                 ("q", Csr), ("c", P_f64), ("a_ineq", Csr), ("b_ineq", P_f64),
                 ("a_eq", Csr), ("b_eq", P_f64), ("obj_offset", f64),
-                ("name", C.c_char_p), ("var_names", C.POINTER(C.c_char_p))]
+                ("name", C.c_char_p), ("var_names", C.POINTER(C.c_char_p)),
+                ("lower", P_f64), ("upper", P_f64)]
 
 
 class RawProblem(C.Structure):
@@ -51,7 +52,7 @@ class Config(C.Structure):
                 ("seed", u64), ("snapshot_interval", i64),
                 ("record_restart_points", i32),
                 ("device", i32), ("strict_parity", i32), ("use_graphs", i32),
-                ("profile_kernels", i32)]
+                ("profile_kernels", i32), ("box_projection", i32)]
 
 
 class Kkt(C.Structure):
@@ -96,7 +97,8 @@ class QpOwned(C.Structure):
     _fields_ = [("n", i32), ("m_ineq", i32), ("m_eq", i32),
                 ("q", CsrOwned), ("a_ineq", CsrOwned), ("a_eq", CsrOwned),
                 ("c", P_f64), ("b_ineq", P_f64), ("b_eq", P_f64),
-                ("obj_offset", f64), ("name", C.c_char_p), ("var_names", C.POINTER(C.c_char_p))]
+                ("obj_offset", f64), ("name", C.c_char_p), ("var_names", C.POINTER(C.c_char_p)),
+                ("lower", P_f64), ("upper", P_f64)]
 
 
 ALLGATHERV_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, P_f64, P_i64, i32)

@@ -26,6 +26,11 @@ __global__ void scale_copy_kernel(double* v, const double* w, double s, int64_t 
   if (i < n) v[i] = w[i] * s;  // v = w; scale(v, 1/nrm) (opnorm.hpp:52-53)
 }
 
+__global__ void div_kernel(double* out, const double* v, const double* d, int64_t n) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) out[i] = v[i] / d[i];  // +-inf stays +-inf (d > 0)
+}
+
 __global__ void fill_kernel(double* v, double s, int64_t n) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i < n) v[i] = s;
@@ -85,10 +90,20 @@ void finalize_kkt(const KktRaw& r, Kkt out[2]) {
     out[p].r_primal = std::max(viol, 0.0) / (1.0 + std::max(r.ax_inf[p], r.b_inf));
     out[p].r_dual = r.dn[p] / (1.0 + std::max({r.qx_inf[p], r.aty_inf[p], r.c_inf}));
     const double xqx = r.xqx[p], cx = r.cx[p];
-    const double by = r.by_i[p] + r.by_e[p];
+    // box_projection: the bound multipliers' share of the dual objective
+    // (bl + bu = 0 in the reference's form, and x - 0.0 == x exactly)
+    const double by = (r.by_i[p] + r.by_e[p]) - (r.bl[p] + r.bu[p]);
     out[p].r_gap = std::fabs(xqx + cx + by) /
                    (1.0 + std::max(std::fabs(0.5 * xqx + cx), std::fabs(0.5 * xqx + by)));
   }
+}
+
+void primal_terms_into(KktRaw& r, const double* g) {
+  r.xqx[0] = g[0], r.xqx[1] = g[1], r.cx[0] = g[2], r.cx[1] = g[3];
+  r.bl[0] = g[4], r.bl[1] = g[5], r.bu[0] = g[6], r.bu[1] = g[7];
+  const double* mx = g + kKktPrimalSums;
+  r.dn[0] = mx[0], r.dn[1] = mx[1], r.qx_inf[0] = mx[2], r.qx_inf[1] = mx[3];
+  r.aty_inf[0] = mx[4], r.aty_inf[1] = mx[5], r.c_inf = mx[6];
 }
 
 // ============================================================================
@@ -103,6 +118,20 @@ namespace {
   invalid("CSR row_ptr not monotone");
 }
 }  // namespace
+
+// box_projection: the bounds' rules (canonicalize's, problem.hpp:134-143)
+void validate_bounds(const rapdhg_qp& p, const rapdhg_config& cfg) {
+  if (!p.lower && !p.upper) return;
+  if (!cfg.box_projection)
+    invalid("variable bounds need box_projection (the reference form takes them as rows: canonicalize)");
+  if (cfg.strict_parity) invalid("box_projection has no reference counterpart: it needs strict_parity = 0");
+  for (int j = 0; j < p.n; ++j) {
+    const double l = p.lower ? p.lower[j] : -std::numeric_limits<double>::infinity();
+    const double u = p.upper ? p.upper[j] : std::numeric_limits<double>::infinity();
+    if (std::isnan(l) || std::isnan(u)) invalid("NaN variable bound");
+    if (l > u) invalid("infeasible bounds on variable " + std::to_string(j));
+  }
+}
 
 void DeviceQP::validate_dims(const rapdhg_qp& p, bool structure) {
   // problem.hpp:40-46 messages
@@ -182,6 +211,8 @@ DeviceQP::DeviceQP(const rapdhg_qp& p, bool strict_, cudaStream_t st_, bool chec
   tr.mark("  transpose");
   c.alloc(n);
   c.upload(p.c, n, st);
+  if (p.lower) lo.alloc(n), lo.upload(p.lower, n, st);
+  if (p.upper) hi.alloc(n), hi.upload(p.upper, n, st);
   b.alloc(m);
   b.upload(p.b_ineq, mi, st);
   if (me) RB_CUDA(cudaMemcpyAsync(b.get() + mi, p.b_eq, sizeof(double) * me, cudaMemcpyHostToDevice, st));
@@ -430,6 +461,7 @@ Engine::Engine(const rapdhg_qp& p, const rapdhg_config& cfg, Clock::time_point t
   P_->validate_symmetry();  // original.validate() (solver.hpp:277)
   tr.mark("symmetry check");
   validate_config(cfg);     // cfg.validate() (solver.hpp:278)
+  validate_bounds(p, cfg);  // box_projection (B200 extension)
   n_ = P_->n, m_ = P_->m, mi_ = P_->mi;
   if (!P_->strict) plan_slabs_async();  // reads n_, m_ and the device matrices only
 
@@ -444,6 +476,19 @@ Engine::Engine(const rapdhg_qp& p, const rapdhg_config& cfg, Clock::time_point t
     RB_LAUNCH_CHECK();
     qsv_ = P_->Q.v.get(), asv_ = P_->A.v.get(), atsv_ = P_->AT.v.get();
     csv_ = P_->c.get(), bsv_ = P_->b.get();
+  }
+  if (P_->lo.size() || P_->hi.size()) {  // scaled bounds: x~ = x / d2
+    if (P_->lo.size()) {
+      los_.alloc(n_);
+      div_kernel<<<grid1(n_), 256, 0, st_>>>(los_.get(), P_->lo.get(), d_.get(), n_);
+      lsv_ = los_.get();
+    }
+    if (P_->hi.size()) {
+      his_.alloc(n_);
+      div_kernel<<<grid1(n_), 256, 0, st_>>>(his_.get(), P_->hi.get(), d_.get(), n_);
+      hsv_ = his_.get();
+    }
+    RB_LAUNCH_CHECK();
   }
   tr.mark("scaling");
   // norms (solver.hpp:286-289)
@@ -722,7 +767,8 @@ void Engine::launch_chunk_body(int len, int cur, bool prof) {
       rowwise(pr, P_->sch_primal, st_, &launches_);
     } else {
       PrimalStepOp<false> pr{P_->Q.view(qsv_), P_->AT.view(atsv_), XMD_[c].get(), y_.get(), X_[c].get(),
-                             X_[c ^ 1].get(), xb_.get(), csv_, w_.get(), XMD_[c ^ 1].get(), params_.get(), it, bad_.get()};
+                             X_[c ^ 1].get(), xb_.get(), csv_, w_.get(), XMD_[c ^ 1].get(), params_.get(), it, bad_.get(),
+                             lsv_, hsv_};
       if (primal_ph_.active()) {
         launches_ += launch_slab_phase(pr, primal_ph_, st_, span);
       } else if (cbp_.active()) {
@@ -810,9 +856,10 @@ Cand Engine::evaluate() {
     rowwise(qa, P.sch_primal, st_, &launches_);
     launch_reduce<4, 5>(KktDualTerms{ax_[0].get(), ax_[1].get(), P.b.get(), yu_[0].get(), yu_[1].get(), mi_},
                         m_, true, P.red, P.red_out.get(), st_);
-    launch_reduce<4, 7>(KktPrimalTerms{qx_[0].get(), qx_[1].get(), aty_[0].get(), aty_[1].get(), xu_[0].get(),
-                                       xu_[1].get(), P.c.get()},
-                        n_, true, P.red, P.red_out.get() + 16, st_);
+    launch_reduce<kKktPrimalSums, kKktPrimalMaxes>(
+        KktPrimalTerms{qx_[0].get(), qx_[1].get(), aty_[0].get(), aty_[1].get(), xu_[0].get(), xu_[1].get(),
+                       P.c.get(), P.lo.size() ? P.lo.get() : nullptr, P.hi.size() ? P.hi.get() : nullptr},
+        n_, true, P.red, P.red_out.get() + 16, st_);
   } else {
     // primal side on st2_ (own reduction scratch), dual side on st_, joined
     // before the read-back; the results do not depend on the overlap
@@ -828,9 +875,10 @@ Cand Engine::evaluate() {
                         qx_[0].get(), qx_[1].get(), aty_[0].get(), aty_[1].get()};
     rowwise(qa, P.sch_primal, st2_, &launches_);
     // primal-side terms (kkt.hpp:56-66)
-    launch_reduce<4, 7>(KktPrimalTerms{qx_[0].get(), qx_[1].get(), aty_[0].get(), aty_[1].get(), xu_[0].get(),
-                                       xu_[1].get(), P.c.get()},
-                        n_, false, red2_, P.red_out.get() + 16, st2_);
+    launch_reduce<kKktPrimalSums, kKktPrimalMaxes>(
+        KktPrimalTerms{qx_[0].get(), qx_[1].get(), aty_[0].get(), aty_[1].get(), xu_[0].get(), xu_[1].get(),
+                       P.c.get(), P.lo.size() ? P.lo.get() : nullptr, P.hi.size() ? P.hi.get() : nullptr},
+        n_, false, red2_, P.red_out.get() + 16, st2_);
     RB_CUDA(cudaEventRecord(evj_, st2_));
     KktAxOp<false> ax{P.A.view(), xi_.get(), ax_[0].get(), ax_[1].get()};
     rowwise(ax, P.sch_dual, st_, &launches_);
@@ -848,10 +896,7 @@ Cand Engine::evaluate() {
   KktRaw r;
   r.by_i[0] = h[0], r.by_e[0] = h[1], r.by_i[1] = h[2], r.by_e[1] = h[3];
   r.viol[0] = h[4], r.viol[1] = h[5], r.ax_inf[0] = h[6], r.ax_inf[1] = h[7], r.b_inf = h[8];
-  const double* g = h + 16;
-  r.xqx[0] = g[0], r.xqx[1] = g[1], r.cx[0] = g[2], r.cx[1] = g[3];
-  r.dn[0] = g[4], r.dn[1] = g[5], r.qx_inf[0] = g[6], r.qx_inf[1] = g[7];
-  r.aty_inf[0] = g[8], r.aty_inf[1] = g[9], r.c_inf = g[10];
+  primal_terms_into(r, h + 16);
   Kkt k2[2];
   finalize_kkt(r, k2);
   Cand cd;
@@ -1273,11 +1318,11 @@ void api_rel_kkt(const rapdhg_qp& p, const double* x, const double* yi, const do
   double h1[9];
   P.reduce_to_host<4, 5>(KktDualTerms{axp, axp, b, yp, yp, mi}, m, h1);
   const double *qxp = qx.get(), *atp = aty.get(), *xp = xu.get(), *c = P.c.get();
-  double h2[11];
-  P.reduce_to_host<4, 7>(KktPrimalTerms{qxp, qxp, atp, atp, xp, xp, c}, n, h2);
+  double h2[kKktPrimalSums + kKktPrimalMaxes];
+  P.reduce_to_host<kKktPrimalSums, kKktPrimalMaxes>(KktPrimalTerms{qxp, qxp, atp, atp, xp, xp, c}, n, h2);
   KktRaw r{};
   r.by_i[0] = h1[0], r.by_e[0] = h1[1], r.viol[0] = h1[4], r.ax_inf[0] = h1[6], r.b_inf = h1[8];
-  r.xqx[0] = h2[0], r.cx[0] = h2[2], r.dn[0] = h2[4], r.qx_inf[0] = h2[6], r.aty_inf[0] = h2[8], r.c_inf = h2[10];
+  primal_terms_into(r, h2);
   Kkt k2[2];
   finalize_kkt(r, k2);
   *out = k2[0];

@@ -45,8 +45,11 @@ struct Kkt {
 struct KktRaw {
   double by_i[2], by_e[2], viol[2], ax_inf[2], b_inf;
   double xqx[2], cx[2], dn[2], qx_inf[2], aty_inf[2], c_inf;
+  double bl[2] = {0.0, 0.0}, bu[2] = {0.0, 0.0};  // box_projection: l.max(g,0), u.min(g,0)
 };
 void finalize_kkt(const KktRaw& r, Kkt out[2]);  // kkt.hpp:54,63,68-69
+// the KktPrimalTerms reduction outputs (kKktPrimalSums sums, then maxes) into r
+void primal_terms_into(KktRaw& r, const double* g);
 
 class DeviceQP {
  public:
@@ -88,6 +91,7 @@ class DeviceQP {
   DevCsr Q, A, AT;  // original values; A = [A_ineq; A_eq]
   DevBuf<int32_t> at_perm;  // AT position -> A position
   DevBuf<double> c, b;      // original c and stacked b
+  DevBuf<double> lo, hi;    // variable bounds (box_projection; empty = none)
   Schedule sch_dual;    // rows of A
   Schedule sch_primal;  // rows of [Q | A']
   Schedule sch_q;       // rows of Q
@@ -191,6 +195,10 @@ class Engine : public LoopBackend {
   DevBuf<double> d_;  // n + m scaling factors (d2 then d1)
   DevBuf<double> qs_, as_, ats_, cs_, bs_;
   const double *qsv_, *asv_, *atsv_, *csv_, *bsv_;
+  // box_projection: bounds in the scaled space (l / d2, u / d2) for the
+  // primal step's projection; null when absent
+  DevBuf<double> los_, his_;
+  const double *lsv_ = nullptr, *hsv_ = nullptr;
   // iterate state (scaled)
   DevBuf<double> X_[2], XMD_[2], w_, xb_, y_, yb_, epx_, epy_;
   int cur_ = 0;

@@ -665,6 +665,8 @@ void rapdhg_qp_free(rapdhg_qp_owned* p) {
   std::free(p->b_ineq);
   std::free(p->b_eq);
   std::free(p->name);
+  std::free(p->lower);
+  std::free(p->upper);
   if (p->var_names)
     for (int32_t j = 0; j < p->n; ++j) std::free(p->var_names[j]);
   std::free(p->var_names);
@@ -681,6 +683,8 @@ void rapdhg_qp_view(const rapdhg_qp_owned* p, rapdhg_qp* v) {
   v->obj_offset = p->obj_offset;
   v->name = p->name;
   v->var_names = p->var_names;
+  v->lower = p->lower;
+  v->upper = p->upper;
 }
 
 // unscale_point / scale_point (scaling.hpp:126-143): x = D2 x~, y = D1 y~

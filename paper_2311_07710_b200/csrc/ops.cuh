@@ -123,6 +123,11 @@ struct PrimalStepOp {
   const IterParams* P;
   int it;
   long long* bad;
+  // box_projection (B200 extension): x+ projected onto [lo, hi] (scaled
+  // bounds, null = unbounded); the reference has no such step (its bounds
+  // are rows), so this is never used in a parity mode
+  const double* lo = nullptr;
+  const double* hi = nullptr;
   __device__ __forceinline__ int len(int r) const {
     return (q.rp[r + 1] - q.rp[r]) + (at.rp[r + 1] - at.rp[r]);
   }
@@ -153,7 +158,12 @@ struct PrimalStepOp {
   __device__ __forceinline__ void finish(int j, const AccT& acc, const Pre& pre) const {
     const IterParams& p = P[it];
     const double xo = pre.x;
-    const double xn = xo - p.eta * (acc.v[0] + pre.c + acc.v[1]);
+    double xn = xo - p.eta * (acc.v[0] + pre.c + acc.v[1]);
+    if (lo || hi) {  // the flag sees the unprojected value (a clamp would hide a NaN)
+      flag_nonfinite(xn, p.t, bad);
+      if (lo) xn = fmax(xn, lo[j]);
+      if (hi) xn = fmin(xn, hi[j]);
+    }
     x_out[j] = xn;
     const double xbn = p.omib * pre.xb + p.ib * xn;
     xb[j] = xbn;

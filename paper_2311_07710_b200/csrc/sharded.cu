@@ -829,7 +829,8 @@ void ShardedEngine::body(int len, int cur) {
                                CsrView{P.AT.rp.get() + o, P.AT.ci.get(), e.atsv_},
                                sh->XMD[c].get(), sh->y.get(), sh->X[c].get() + o, sh->X[c ^ 1].get() + o,
                                sh->xb.get() + o, e.csv_ + o, sh->w.get() + o, sh->XMD[c ^ 1].get() + o,
-                               params_.get(), it, sh->bad.get()};
+                               params_.get(), it, sh->bad.get(), e.lsv_ ? e.lsv_ + o : nullptr,
+                               e.hsv_ ? e.hsv_ + o : nullptr};
         if (part) {
           const SellPlan& sp = part == 1 ? sh->sell_primal_in : sh->sell_primal_bd;
           const Schedule& sc = part == 1 ? sh->sch_primal_in : sh->sch_primal_bd;
@@ -963,16 +964,17 @@ Cand ShardedEngine::evaluate() {
     return KktDualTerms{s.ax[0].get() + lo, s.ax[1].get() + lo, b + lo, s.yu[0].get() + lo, s.yu[1].get() + lo,
                         mi - static_cast<int>(lo)};
   }, h);
-  reduce<4, 7>(true, [&](Shard& s, int64_t lo) {
+  const double* lob = P.lo.size() ? P.lo.get() : nullptr;
+  const double* hib = P.hi.size() ? P.hi.get() : nullptr;
+  reduce<kKktPrimalSums, kKktPrimalMaxes>(true, [&](Shard& s, int64_t lo) {
     return KktPrimalTerms{s.qx[0].get() + lo, s.qx[1].get() + lo, s.aty[0].get() + lo, s.aty[1].get() + lo,
-                          s.xu[0].get() + lo, s.xu[1].get() + lo, c + lo};
+                          s.xu[0].get() + lo, s.xu[1].get() + lo, c + lo, lob ? lob + lo : nullptr,
+                          hib ? hib + lo : nullptr};
   }, g);
   KktRaw r;
   r.by_i[0] = h[0], r.by_e[0] = h[1], r.by_i[1] = h[2], r.by_e[1] = h[3];
   r.viol[0] = h[4], r.viol[1] = h[5], r.ax_inf[0] = h[6], r.ax_inf[1] = h[7], r.b_inf = h[8];
-  r.xqx[0] = g[0], r.xqx[1] = g[1], r.cx[0] = g[2], r.cx[1] = g[3];
-  r.dn[0] = g[4], r.dn[1] = g[5], r.qx_inf[0] = g[6], r.qx_inf[1] = g[7];
-  r.aty_inf[0] = g[8], r.aty_inf[1] = g[9], r.c_inf = g[10];
+  primal_terms_into(r, g);
   Kkt k2[2];
   finalize_kkt(r, k2);
   Cand cd;

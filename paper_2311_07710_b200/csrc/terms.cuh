@@ -61,18 +61,42 @@ struct KktDualTerms {
 };
 
 // Primal-side relKKT terms for two points (kkt.hpp:57-66):
-// sums  x.qx(c), x.qx(a), c.x(c), c.x(a)
-// maxes |qx+aty+c|(c), (a), |qx|(c), (a), |aty|(c), (a), |c|
+// sums  x.qx(c), x.qx(a), c.x(c), c.x(a), then (box_projection) l.g+(c),
+//       l.g+(a), u.g-(c), u.g-(a)
+// maxes |qx+aty+c - lambda|(c), (a), |qx|(c), (a), |aty|(c), (a), |c|
+// Without bounds (lo = hi = null: the reference's form) lambda = 0 and the
+// bound sums stay 0. With bounds, lambda_j = max(g_j, 0) when l_j is finite
+// plus min(g_j, 0) when u_j is finite (g = qx + aty + c): the bound
+// multipliers that best fit stationarity; they enter the dual objective as
+// l.max(g,0) + u.min(g,0) over the finite bounds.
 struct KktPrimalTerms {
   const double *qxc, *qxa, *atc, *ata, *xc, *xa, *c;
+  const double* lo = nullptr;  // original bounds (box_projection), null = none
+  const double* hi = nullptr;
   __device__ void operator()(int64_t j, double* s, double* mx) const {
     const double cj = c[j];
     s[0] += xc[j] * qxc[j];
     s[1] += xa[j] * qxa[j];
     s[2] += cj * xc[j];
     s[3] += cj * xa[j];
-    mx[0] = fmax(mx[0], fabs(qxc[j] + atc[j] + cj));
-    mx[1] = fmax(mx[1], fabs(qxa[j] + ata[j] + cj));
+    double gc = qxc[j] + atc[j] + cj, ga = qxa[j] + ata[j] + cj;
+    if (lo || hi) {
+      const double l = lo ? lo[j] : -INFINITY, u = hi ? hi[j] : INFINITY;
+      if (l > -INFINITY) {
+        s[4] += l * fmax(gc, 0.0);
+        s[5] += l * fmax(ga, 0.0);
+      }
+      if (u < INFINITY) {
+        s[6] += u * fmin(gc, 0.0);
+        s[7] += u * fmin(ga, 0.0);
+      }
+      const double lc = (l > -INFINITY ? fmax(gc, 0.0) : 0.0) + (u < INFINITY ? fmin(gc, 0.0) : 0.0);
+      const double la = (l > -INFINITY ? fmax(ga, 0.0) : 0.0) + (u < INFINITY ? fmin(ga, 0.0) : 0.0);
+      gc = gc - lc;
+      ga = ga - la;
+    }
+    mx[0] = fmax(mx[0], fabs(gc));
+    mx[1] = fmax(mx[1], fabs(ga));
     mx[2] = fmax(mx[2], fabs(qxc[j]));
     mx[3] = fmax(mx[3], fabs(qxa[j]));
     mx[4] = fmax(mx[4], fabs(atc[j]));
@@ -80,5 +104,6 @@ struct KktPrimalTerms {
     mx[6] = fmax(mx[6], fabs(cj));
   }
 };
+constexpr int kKktPrimalSums = 8, kKktPrimalMaxes = 7;
 
 }  // namespace rb

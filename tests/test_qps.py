@@ -223,3 +223,53 @@ def test_canonicalize_errors_match_reference():
             oracle.ref().canonicalize(r)
         assert str(mine.value) == str(ref.value) == msg
     assert raw.num_vars() == 12
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_canonicalize_box_keeps_bounds_out_of_the_rows(seed):
+    """keep_bounds (SolverConfig.box_projection, B200 extension): the same
+    canonical problem minus the singleton bound rows canonicalize appends
+    (problem.hpp:178-185), with the raw bounds carried in lower / upper."""
+    raw = random_raw(seed)
+    rows, mr = rb.canonicalize(raw)
+    box, mb = rb.canonicalize(raw, keep_bounds=True)
+    nb = int(np.isfinite(raw.lower).sum() + np.isfinite(raw.upper).sum())
+    k = rows.num_ineq() - nb
+    assert box.num_ineq() == k and box.num_eq() == rows.num_eq()
+    assert mb.ineq_labels == mr.ineq_labels[:k] and mb.eq_labels == mr.eq_labels
+    assert np.array_equal(box.a_ineq.row_ptr, rows.a_ineq.row_ptr[:k + 1])
+    e = rows.a_ineq.row_ptr[k]
+    assert np.array_equal(box.a_ineq.col_idx, rows.a_ineq.col_idx[:e])
+    assert np.array_equal(box.a_ineq.values, rows.a_ineq.values[:e])
+    assert np.array_equal(box.b_ineq, rows.b_ineq[:k])
+    assert np.array_equal(box.lower, raw.lower) and np.array_equal(box.upper, raw.upper)
+    assert rows.lower is None and rows.upper is None
+    for ma, mb_ in ((box.q, rows.q), (box.a_eq, rows.a_eq)):
+        assert np.array_equal(ma.values, mb_.values) and np.array_equal(ma.col_idx, mb_.col_idx)
+    assert np.array_equal(box.c, rows.c) and box.obj_offset == rows.obj_offset
+
+
+def test_bounds_from_rows_inverts_canonicalize():
+    """bounds_from_rows(canonicalize(raw)) == canonicalize(raw, keep_bounds)
+    when the raw rows have no singletons (they would become bounds too)."""
+    g = np.random.default_rng(3)
+    for seed in range(4):
+        raw = random_raw(seed, n=10, m=6)
+        dense = g.standard_normal((6, 10))
+        r, c = np.nonzero(dense)
+        raw.a = rb.SparseMatrix.from_coo(6, 10, r, c, dense[r, c])
+        raw.lower[0], raw.upper[0] = -np.inf, 2.0  # one one-sided bound at least
+        box, mb = rb.canonicalize(raw, keep_bounds=True)
+        back = rb.bounds_from_rows(rb.canonicalize(raw)[0])
+        assert back.num_ineq() == box.num_ineq()
+        for ma, mb_ in ((back.a_ineq, box.a_ineq), (back.a_eq, box.a_eq)):
+            assert np.array_equal(ma.row_ptr, mb_.row_ptr) and np.array_equal(ma.col_idx, mb_.col_idx)
+            assert np.array_equal(ma.values, mb_.values)
+        assert np.array_equal(back.b_ineq, box.b_ineq)
+        assert np.array_equal(back.lower, box.lower) and np.array_equal(back.upper, box.upper)
+    # a zero singleton stays a row; the tightest of two bounds wins
+    a = rb.SparseMatrix.from_csr(3, 2, [0, 1, 2, 3], [0, 0, 1], [2.0, 1.0, 0.0])
+    p = rb.QuadraticProgram(rb.SparseMatrix.identity(2), np.zeros(2), a, np.array([4.0, 1.5, 1.0]),
+                            rb.SparseMatrix.zero(0, 2), np.zeros(0))
+    q = rb.bounds_from_rows(p)
+    assert q.num_ineq() == 1 and q.upper[0] == 1.5 and q.upper[1] == np.inf and q.lower is None

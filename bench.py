@@ -156,6 +156,33 @@ def qp_bytes(p):
     return b + p.c.nbytes + p.b_ineq.nbytes + p.b_eq.nbytes
 
 
+def pinned_qp(p):
+    """The e2e leg's inputs: the instance's arrays copied once (untimed) into
+    page-locked host memory, the contract's "pinned host memory" — the library
+    then DMAs them directly instead of staging pageable arrays."""
+    try:
+        import torch
+        if not torch.cuda.is_available():
+            return p
+    except ImportError:
+        return p
+    import copy
+
+    def pin(a):
+        t = torch.empty(a.shape, dtype=getattr(torch, a.dtype.name), pin_memory=True)
+        out = t.numpy()
+        out[...] = a
+        return out
+
+    q = copy.copy(p)
+    for name in ("q", "a_ineq", "a_eq"):
+        m = copy.copy(getattr(p, name))
+        m.row_ptr, m.col_idx, m.values = pin(m.row_ptr), pin(m.col_idx), pin(m.values)
+        setattr(q, name, m)
+    q.c, q.b_ineq, q.b_eq = pin(p.c), pin(p.b_ineq), pin(p.b_eq)
+    return q
+
+
 def make_instance(args):
     import paper_2311_07710_b200 as rb
 
@@ -450,11 +477,12 @@ def main():
 
     # ---- e2e through the public C-ABI from host arrays ----------------------
     ecfg = rb.SolverConfig(tol=args.tol, max_iters=args.max_iters, device=local, strict_parity=args.strict)
-    rb.solve(p, ecfg)  # warm-up (untimed), like the device-timed arm
+    ph = pinned_qp(p)
+    rb.solve(ph, ecfg)  # warm-up (untimed), like the device-timed arm
     e2e_its, e2e_each, e2e_res = 0, [], None
     for _ in range(max(args.e2e_steps, 1)):
         t = time.perf_counter()
-        e2e_res = rb.solve(p, ecfg)
+        e2e_res = rb.solve(ph, ecfg)
         e2e_each.append(time.perf_counter() - t)
         e2e_its += e2e_res.iterations
     e2e_wall = allmax(sum(e2e_each))
@@ -477,7 +505,8 @@ def main():
         "e2e": {"value": world * e2e_its / e2e_wall, "unit": "iter/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "wall_s_per_step": e2e_wall / len(e2e_each),
                 "wall_s_each": [round(w, 4) for w in e2e_each],
-                "path": "rapdhg_solve (C-ABI) from host arrays: upload, validation, scaling, norms, loop, download"},
+                "path": "rapdhg_solve (C-ABI) from pinned host arrays: upload, validation, scaling, norms, loop, "
+                        "download"},
         "roofline": roof, "gpu_launches": launches, "clocks": clk,
         "mode": "strict (bit-exact)" if args.strict else "fast (deterministic)",
         "generator_s": gen_s,

@@ -3,6 +3,8 @@
 // cores are involved (nothing on this path is a dense contraction).
 #pragma once
 
+#include <type_traits>
+
 #include <atomic>
 #include <chrono>
 #include <cstdio>
@@ -303,6 +305,24 @@ struct Tracer {
                  std::chrono::duration<double, std::milli>(now - t).count());
     t = now;
   }
+};
+
+// Step gate (power iterations run in device batches, engine.cu): a launch
+// tagged with step i does nothing once the device recorded a stop at a step
+// before i (*stop < i). The stop is written by step j's own last kernel, so no
+// kernel ever reads a gate its own blocks write.
+struct StepGate {
+  const int* stop = nullptr;
+  int step = 0;
+  __device__ __forceinline__ bool closed() const { return stop && *stop < step; }
+};
+template <class T, class = void>
+struct HasGate {
+  __device__ __forceinline__ static bool closed(const T&) { return false; }
+};
+template <class T>
+struct HasGate<T, std::void_t<decltype(T::gate)>> {
+  __device__ __forceinline__ static bool closed(const T& t) { return t.gate.closed(); }
 };
 
 constexpr int kSMs = 148;  // B200: 2 dies x 74 SMs

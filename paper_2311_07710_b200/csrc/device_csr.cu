@@ -119,8 +119,24 @@ HostStager::~HostStager() {
   }
 }
 
+namespace {
+// Whether [p, p + bytes) is page-locked host memory (cudaHostAlloc'ed or
+// registered): then the DMA engines read it directly, at full link speed.
+bool host_pinned(const void* p, std::size_t bytes) {
+  for (const char* q : {static_cast<const char*>(p), static_cast<const char*>(p) + bytes - 1}) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, q) != cudaSuccess) {
+      cudaGetLastError();  // clear: a plain pageable pointer on old drivers
+      return false;
+    }
+    if (a.type != cudaMemoryTypeHost) return false;
+  }
+  return true;
+}
+}  // namespace
+
 void HostStager::upload(void* dst, const void* src, std::size_t bytes, cudaStream_t st) {
-  if (!on_ || bytes < 2 * kChunk) {
+  if (!on_ || bytes < 2 * kChunk || host_pinned(src, bytes)) {
     if (bytes) RB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
     return;
   }

@@ -27,6 +27,8 @@ struct DevCsr {
 // (the driver's own pageable path is one serial bounce buffer, ~11 GB/s).
 // Copies are complete when the stream is; the destructor waits for them
 // before the buffers go back to the cache. RAPDHG_STAGE=0: plain copies.
+// Arrays already page-locked (cudaHostAlloc / cudaHostRegister, e.g. torch's
+// pin_memory) skip the staging: one direct DMA each.
 class HostStager {
  public:
   HostStager();

@@ -6,7 +6,9 @@
 #include <cstdio>
 #include <cmath>
 #include <cstring>
+#include <climits>
 #include <limits>
+#include <stdexcept>
 
 #include "engine.hpp"
 #include "rules.hpp"
@@ -257,12 +259,12 @@ void DeviceQP::reduce_to_host(const F& f, int64_t len, double* out) {
 }
 
 void DeviceQP::spmv(const DevCsr& mat, const Schedule& s, const double* vals, const double* x,
-                    double* y) {
+                    double* y, StepGate gate) {
   if (strict) {
-    SpmvOp<true> op{mat.view(vals), x, y};
+    SpmvOp<true> op{mat.view(vals), x, y, gate};
     rowwise(op, s, st, &launches);
   } else {
-    SpmvOp<false> op{mat.view(vals), x, y};
+    SpmvOp<false> op{mat.view(vals), x, y, gate};
     rowwise(op, s, st, &launches);
   }
 }
@@ -354,16 +356,33 @@ void random_unit(DeviceQP& P, DevBuf<double>& v, int len, std::mt19937_64& rng) 
 
 // estimate_op_norm_symmetric (opnorm.hpp:64-87)
 namespace {
-// v = w * (1.0 / sqrt(*sumsq)) with the norm read on the device — the same
-// IEEE operations as the host's `1.0 / std::sqrt(s)`; a zero norm leaves v
-// unchanged (the host then restarts from a random vector).
-__global__ void scale_by_norm_kernel(double* v, const double* w, const double* sumsq, int64_t n) {
-  const double s = *sumsq;
-  if (s == 0.0) return;
+// Device copy of the host's per-step decision (opnorm.hpp:48-59): thread 0
+// of block 0 records a stop at this step when the step converged or w = 0
+// (the host then restarts from a random vector), so the batch's remaining
+// launches return at once. The host still replays the recorded values and
+// decides; the gate only saves the overshoot past convergence.
+struct PowerState {
+  double lambda;  // the host's lambda before the batch's first step, then the device's
+  int stop;       // step of the batch the device stopped at (INT_MAX: none)
+  int it0;        // host iteration index of the batch's first step
+};
+__global__ void power_step_kernel(double* v, const double* w, const double* hist, PowerState* ps, int i,
+                                  double tol, bool absval, int64_t n) {
+  if (ps->stop < i) return;  // a stop recorded by an earlier step (uniform over the grid)
+  const double s = hist[1];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const double lambda_next = absval ? fabs(hist[0]) : hist[0];
+    if (s == 0.0 || (ps->it0 + i > 0 && fabs(lambda_next - ps->lambda) <= tol * fabs(lambda_next)))
+      ps->stop = i;  // read only by later launches
+    else
+      ps->lambda = lambda_next;
+  }
+  if (s == 0.0) return;  // v unchanged (the host restarts)
+  // v = w * (1.0 / sqrt(s)): the same IEEE operations as the host's scale(v, 1.0 / nrm)
   const double inv = 1.0 / sqrt(s);
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    v[i] = w[i] * inv;
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    v[k] = w[k] * inv;
 }
 }  // namespace
 
@@ -371,32 +390,43 @@ __global__ void scale_by_norm_kernel(double* v, const double* w, const double* s
 // (v.w, ||w||^2) on the device and normalises v there; after a batch the host
 // replays the reference's loop over the recorded values (stopping rule,
 // zero-norm restart) — identical results, one host round trip per batch
-// (8, 16, .. 64 steps) instead of per step. Overshoot past convergence only
-// costs the batch's remaining steps (their v is never used).
+// (8, 16, .. 64 steps) instead of per step. The device takes the same
+// per-step decision (power_step_kernel), so the launches of a batch past
+// convergence return at once: overshoot costs ~3 empty launches per step
+// (C4: up to 63 x 0.4 ms of products before).
 template <class Step>
 double DeviceQP::power_iteration(DevBuf<double>& v, DevBuf<double>& w, int len, const Step& step, bool absval,
                                  int max_iters, double tol, std::mt19937_64& rng) {
   constexpr int kMaxBatch = 64;
   DevBuf<double> hist(2 * kMaxBatch);
+  DevBuf<PowerState> dps(1);
   PinnedBuf<double> hh;
   hh.alloc(2 * kMaxBatch);
+  PinnedBuf<PowerState> hps;
+  hps.alloc(2);
   random_unit(*this, v, len, rng);
   double lambda = 0.0;
   int it = 0, batch = 8;
+  const unsigned sgrid = static_cast<unsigned>(std::min<int64_t>(ceil_div(len, 256), 4 * kSMs));
   while (it < max_iters) {
     const int K = std::min(batch, max_iters - it);
+    hps[0] = PowerState{lambda, INT_MAX, it};
+    RB_CUDA(cudaMemcpyAsync(dps.get(), hps.get(), sizeof(PowerState), cudaMemcpyHostToDevice, st));
     for (int i = 0; i < K; ++i) {
-      step();  // w = M v
-      launch_reduce<2, 0>(DotAndSumSq{v.get(), w.get()}, len, strict, red, hist.get() + 2 * i, st);
-      scale_by_norm_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(len, 256), 4 * kSMs)), 256, 0, st>>>(
-          v.get(), w.get(), hist.get() + 2 * i + 1, len);
+      const StepGate gate{&dps.get()->stop, i};
+      step(gate);  // w = M v
+      launch_reduce<2, 0>(DotAndSumSq{v.get(), w.get(), gate}, len, strict, red, hist.get() + 2 * i, st);
+      power_step_kernel<<<sgrid, 256, 0, st>>>(v.get(), w.get(), hist.get() + 2 * i, dps.get(), i, tol, absval, len);
       RB_LAUNCH_CHECK();
       launches += 2;
     }
     RB_CUDA(cudaMemcpyAsync(hh.get(), hist.get(), sizeof(double) * 2 * K, cudaMemcpyDeviceToHost, st));
+    RB_CUDA(cudaMemcpyAsync(hps.get() + 1, dps.get(), sizeof(PowerState), cudaMemcpyDeviceToHost, st));
     RB_CUDA(cudaStreamSynchronize(st));
+    const int dev_stop = hps[1].stop;
     bool restarted = false;
     for (int i = 0; i < K && !restarted; ++i, ++it) {
+      if (i > dev_stop) throw std::logic_error("power iteration: device stopped before the host's decision");
       const double lambda_next = absval ? std::fabs(hh[2 * i]) : hh[2 * i];
       const double nrm = std::sqrt(hh[2 * i + 1]);
       if (nrm == 0.0) {  // v stayed frozen from here on in this batch
@@ -404,7 +434,12 @@ double DeviceQP::power_iteration(DevBuf<double>& v, DevBuf<double>& w, int len, 
         restarted = true;
         continue;
       }
-      if (it > 0 && std::fabs(lambda_next - lambda) <= tol * std::fabs(lambda_next)) return lambda_next;
+      if (it > 0 && std::fabs(lambda_next - lambda) <= tol * std::fabs(lambda_next)) {
+        if (std::getenv("RAPDHG_TRACE"))
+          std::fprintf(stderr, "[rapdhg]     power iteration: converged at step %d (batch stop %d of %d)\n", it,
+                       dev_stop, K);
+        return lambda_next;
+      }
       lambda = lambda_next;
     }
     batch = std::min(batch * 2, kMaxBatch);
@@ -416,7 +451,8 @@ double DeviceQP::op_norm_q(const double* qv, int max_iters, double tol, uint64_t
   if (Q.nnz == 0) return 0.0;
   std::mt19937_64 rng(seed);
   DevBuf<double> v(n), w(n);
-  return power_iteration(v, w, n, [&] { spmv(Q, sch_q, qv, v.get(), w.get()); }, true, max_iters, tol, rng);
+  return power_iteration(v, w, n, [&](StepGate g) { spmv(Q, sch_q, qv, v.get(), w.get(), g); }, true, max_iters,
+                         tol, rng);
 }
 
 // estimate_op_norm (opnorm.hpp:36-61): power iteration on A'A; A' v as the
@@ -428,9 +464,9 @@ double DeviceQP::op_norm_a(const double* av, const double* atv, int max_iters, d
   DevBuf<double> v(n), w(n), mv(m);
   const double lambda = power_iteration(
       v, w, n,
-      [&] {
-        spmv(A, sch_dual, av, v.get(), mv.get());
-        spmv(AT, sch_at, atv, mv.get(), w.get());
+      [&](StepGate g) {
+        spmv(A, sch_dual, av, v.get(), mv.get(), g);
+        spmv(AT, sch_at, atv, mv.get(), w.get(), g);
       },
       false, max_iters, tol, rng);
   return std::sqrt(std::max(lambda, 0.0));

@@ -83,7 +83,8 @@ class DeviceQP {
   void reduce_to_host(const F& f, int64_t n, double* out);
 
   // Launch helpers for plain products with given values.
-  void spmv(const DevCsr& m, const Schedule& s, const double* vals, const double* x, double* y);
+  void spmv(const DevCsr& m, const Schedule& s, const double* vals, const double* x, double* y,
+            StepGate gate = {});
 
   cudaStream_t st;
   bool strict;

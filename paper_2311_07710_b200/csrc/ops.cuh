@@ -187,6 +187,7 @@ struct SpmvOp {
   CsrView m;
   const double* x;
   double* y;
+  StepGate gate{};  // power-iteration batches (engine.cu); default: always open
   __device__ __forceinline__ int len(int r) const { return m.rp[r + 1] - m.rp[r]; }
   template <int U>
   __device__ __forceinline__ void accumulate(int r, int lo, int hi, int lane, int stride,

@@ -34,6 +34,7 @@ inline int64_t reduce_chunks(int64_t n) { return n > 0 ? ceil_div(n, kRedChunk) 
 
 template <int NS, int NM, class F>
 __global__ void reduce_seq_kernel(F f, int64_t n, double* out) {
+  if (HasGate<F>::closed(f)) return;
   double s[NS > 0 ? NS : 1], mx[NM > 0 ? NM : 1];
   for (int k = 0; k < NS; ++k) s[k] = 0.0;
   for (int k = 0; k < NM; ++k) mx[k] = 0.0;
@@ -73,6 +74,7 @@ __global__ void __launch_bounds__(kRedBlock) reduce_chunks_kernel(F f, int64_t n
                                                                    int64_t chunk0, unsigned* ticket,
                                                                    double* out) {
   constexpr int NT = NS + NM;
+  if (HasGate<F>::closed(f)) return;  // uniform over the grid: no ticket taken
   double s[NS > 0 ? NS : 1], mx[NM > 0 ? NM : 1];
 #pragma unroll
   for (int k = 0; k < NS; ++k) s[k] = 0.0;

@@ -360,6 +360,7 @@ __device__ __forceinline__ void rowwise_tile(const Op& op, const SchedView& s, i
 template <class Op, bool Win>
 __global__ void __launch_bounds__(kBlock) rowwise_kernel(const Op op, const SchedView s) {
   extern __shared__ double win_smem[];
+  if (HasGate<Op>::closed(op)) return;  // uniform over the grid
   Gather g[2];
   int off = 0;
 #pragma unroll

@@ -18,6 +18,7 @@ struct SumSq {  // sum a_i^2 (norm2, vec.hpp:20)
 struct DotAndSumSq {  // s0 = v.w, s1 = w.w (opnorm.hpp:51-52, 77-78)
   const double* v;
   const double* w;
+  StepGate gate{};
   __device__ void operator()(int64_t i, double* s, double*) const {
     s[0] += v[i] * w[i];
     s[1] += w[i] * w[i];

@@ -74,9 +74,6 @@ class DeviceQP {
   // given values (patterns of Q / A / A').
   double op_norm_q(const double* qv, int max_iters, double tol, uint64_t seed);
   double op_norm_a(const double* av, const double* atv, int max_iters, double tol, uint64_t seed);
-  template <class Step>
-  double power_iteration(DevBuf<double>& v, DevBuf<double>& w, int len, const Step& step, bool absval,
-                         int max_iters, double tol, std::mt19937_64& rng);
 
   // Deterministic reduction to host (strict: sequential).
   template <int NS, int NM, class F>
@@ -84,7 +81,7 @@ class DeviceQP {
 
   // Launch helpers for plain products with given values.
   void spmv(const DevCsr& m, const Schedule& s, const double* vals, const double* x, double* y,
-            StepGate gate = {});
+            StepGate gate = {}, cudaStream_t on = nullptr);
 
   cudaStream_t st;
   bool strict;

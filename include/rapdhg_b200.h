@@ -158,7 +158,9 @@ typedef struct { /* rapdhg::LogRecord (solver.hpp:66-74) */
  * it first and, when it fails, releases what it had filled: a failed call
  * leaves an all-zero result (nothing to free). snapshots are stored row-major:
  * snapshot s has x at snapshot_x + s*n and y (ineq then eq) at
- * snapshot_y + s*(m_ineq+m_eq); restart points likewise. */
+ * snapshot_y + s*(m_ineq+m_eq); restart points likewise. x, y_ineq and y_eq
+ * are consecutive parts of one block (page-locked when large: free it only
+ * through rapdhg_result_free, never with free()). */
 typedef struct {
   int32_t status;
   int32_t n, m_ineq, m_eq;

@@ -28,6 +28,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import weakref
 import math
 import os
 from dataclasses import dataclass, field
@@ -494,11 +495,46 @@ def _arr(p, n) -> np.ndarray:
     return np.ctypeslib.as_array(p, (n,)).copy()
 
 
-def result_from_struct(r: abi.Result) -> SolveResult:
+class _ResultBlock:
+    """Owns a C result whose final point (x | y_ineq | y_eq, one block that is
+    page-locked when large) numpy views share without a copy; the block goes
+    back to the library when the last view is gone."""
+
+    def __init__(self, r: abi.Result):
+        self.r = r
+        weakref.finalize(self, _free_result, r)
+
+    def view(self, ptr, n) -> np.ndarray:
+        if n <= 0:
+            return np.zeros(0, np.float64)
+        buf = (C.c_double * n).from_address(C.cast(ptr, C.c_void_p).value)
+        buf._owner = self  # the numpy view keeps buf, buf keeps the block
+        return np.frombuffer(buf, dtype=np.float64)
+
+
+def _free_result(r):
+    _load().rapdhg_result_free(C.byref(r))
+
+
+def take_result(r: abi.Result) -> SolveResult:
+    """result_from_struct, taking ownership of `r`: the point arrays are views
+    of the library's result block (no copy); the rest is copied and the C
+    arrays are released with the block."""
+    try:
+        res = result_from_struct(r, point=False)
+    except BaseException:
+        _free_result(r)
+        raise
+    blk = _ResultBlock(r)
+    res.point = PrimalDualPoint(blk.view(r.x, r.n), blk.view(r.y_ineq, r.m_ineq), blk.view(r.y_eq, r.m_eq))
+    return res
+
+
+def result_from_struct(r: abi.Result, point: bool = True) -> SolveResult:
     """Convert (and copy out of) a C result struct; the caller frees it."""
     n, mi, me = r.n, r.m_ineq, r.m_eq
     m = mi + me
-    point = PrimalDualPoint(_arr(r.x, n), _arr(r.y_ineq, mi), _arr(r.y_eq, me))
+    point = PrimalDualPoint(_arr(r.x, n), _arr(r.y_ineq, mi), _arr(r.y_eq, me)) if point else None
     log = [LogRecord(int(L.iteration), L.r_primal, L.r_dual, L.r_gap, L.eta, L.omega, bool(L.restarted))
            for L in (r.log[i] for i in range(r.n_log))]
     snaps = []
@@ -530,11 +566,8 @@ def solve(original: QuadraticProgram, cfg: Optional[SolverConfig] = None) -> Sol
     qp = original._struct()
     cs = cfg._struct()
     out = abi.Result()
-    _check(L.rapdhg_solve(C.byref(qp), C.byref(cs), C.byref(out)))
-    try:
-        return result_from_struct(out)
-    finally:
-        L.rapdhg_result_free(C.byref(out))
+    _check(L.rapdhg_solve(C.byref(qp), C.byref(cs), C.byref(out)))  # a failed call leaves nothing to free
+    return take_result(out)
 
 
 def shard_plan(p: QuadraticProgram, parts: int) -> Tuple[np.ndarray, np.ndarray]:
@@ -667,10 +700,7 @@ class ShardSession:
         L = _load()
         out = abi.Result()
         _check(L.rapdhg_shard_session_solve(self._h, C.byref(out)))
-        try:
-            return result_from_struct(out)
-        finally:
-            L.rapdhg_result_free(C.byref(out))
+        return take_result(out)
 
     def close(self):
         if getattr(self, "_h", None):
@@ -698,10 +728,7 @@ def solve_sharded(original: QuadraticProgram, cfg: Optional[SolverConfig] = None
     qp, cs, out = original._struct(), cfg._struct(), abi.Result()
     L = _load()
     _check(L.rapdhg_solve_sharded(C.byref(qp), C.byref(cs), C.byref(opts), C.byref(out)))
-    try:
-        return result_from_struct(out)
-    finally:
-        L.rapdhg_result_free(C.byref(out))
+    return take_result(out)
 
 
 class Session:
@@ -722,10 +749,7 @@ class Session:
         L = _load()
         out = abi.Result()
         _check(L.rapdhg_session_solve(self._h, C.byref(out)))
-        try:
-            return result_from_struct(out)
-        finally:
-            L.rapdhg_result_free(C.byref(out))
+        return take_result(out)
 
     def bytes(self) -> Tuple[float, float, float]:
         """(B_iter, bytes of one dual-step launch, bytes of one primal-step launch)."""

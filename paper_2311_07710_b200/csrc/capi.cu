@@ -111,9 +111,11 @@ void rapdhg_config_default(rapdhg_config* c) {
 
 void rapdhg_result_free(rapdhg_result* r) {
   if (!r) return;
-  std::free(r->x);
-  std::free(r->y_ineq);
-  std::free(r->y_eq);
+  if (!rb::result_block_free(r->x)) {  // one block holds x, y_ineq, y_eq
+    std::free(r->x);
+    std::free(r->y_ineq);
+    std::free(r->y_eq);
+  }
   std::free(r->log);
   std::free(r->snapshot_iters);
   std::free(r->snapshot_x);

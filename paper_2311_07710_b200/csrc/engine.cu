@@ -10,6 +10,8 @@
 #include <cstring>
 #include <climits>
 #include <limits>
+#include <map>
+#include <mutex>
 #include <stdexcept>
 
 #include "engine.hpp"
@@ -1009,6 +1011,68 @@ void Engine::download_point(const double* xu, const double* yu, double* x, doubl
   RB_CUDA(cudaStreamSynchronize(st_));
 }
 
+// Result blocks: the final point of a solve. Large ones come from the pinned
+// cache (the download is then a direct DMA at link speed instead of the
+// driver's pageable bounce, and a binding can wrap the memory without a
+// copy); at most kResultPinnedMax bytes are pinned at once, the rest is
+// malloc'ed. rapdhg_result_free hands a block back through result_block_free.
+namespace {
+constexpr std::size_t kResultPinnedMin = std::size_t{1} << 20;
+constexpr std::size_t kResultPinnedMax = std::size_t{2} << 30;
+struct ResultBlocks {
+  std::mutex mu;
+  std::map<void*, std::pair<std::size_t, bool>> live;  // block -> (bytes, pinned)
+  std::size_t pinned_bytes = 0;
+};
+ResultBlocks& result_blocks() {
+  static ResultBlocks* rb = new ResultBlocks;  // never destroyed: frees may run at exit
+  return *rb;
+}
+}  // namespace
+
+void* result_block_alloc(std::size_t bytes) {
+  bytes = bytes ? bytes : sizeof(double);
+  ResultBlocks& R = result_blocks();
+  bool pin = false;
+  if (bytes >= kResultPinnedMin) {
+    std::lock_guard<std::mutex> g(R.mu);
+    if (R.pinned_bytes + bytes <= kResultPinnedMax) pin = true, R.pinned_bytes += bytes;
+  }
+  void* p = nullptr;
+  if (pin) {
+    try {
+      p = pinned_acquire(bytes);
+    } catch (...) {
+      std::lock_guard<std::mutex> g(R.mu);
+      R.pinned_bytes -= bytes;
+      throw;
+    }
+  } else {
+    p = std::malloc(bytes);
+    if (!p) throw Error(RAPDHG_E_INTERNAL, "out of host memory");
+  }
+  std::lock_guard<std::mutex> g(R.mu);
+  R.live[p] = {bytes, pin};
+  return p;
+}
+
+bool result_block_free(void* p) {
+  if (!p) return false;
+  ResultBlocks& R = result_blocks();
+  std::pair<std::size_t, bool> e;
+  {
+    std::lock_guard<std::mutex> g(R.mu);
+    auto it = R.live.find(p);
+    if (it == R.live.end()) return false;
+    e = it->second;
+    R.live.erase(it);
+    if (e.second) R.pinned_bytes -= e.first;
+  }
+  if (e.second) pinned_release(p, e.first);
+  else std::free(p);
+  return true;
+}
+
 namespace {
 template <typename T>
 T* xalloc(std::size_t n) {
@@ -1279,14 +1343,13 @@ void run_loop(LoopBackend& be, const rapdhg_config& cfg, const LoopScalars& sc, 
   // the loop clock (loop_seconds: iterations + checks + restarts, device
   // time) stops before the solution's download to the host
   be.loop_end(out);
-  out->x = xalloc<double>(n);
-  double* yall = xalloc<double>(m);
-  be.download(fin_src, out->x, yall);
-  out->y_ineq = xalloc<double>(mi_);
-  out->y_eq = xalloc<double>(m - mi_);
-  if (mi_) std::memcpy(out->y_ineq, yall, sizeof(double) * mi_);
-  if (m - mi_) std::memcpy(out->y_eq, yall + mi_, sizeof(double) * (m - mi_));
-  std::free(yall);
+  // x | y_ineq | y_eq in one result block (page-locked when large): one
+  // direct DMA per vector, no host copies
+  double* blk = static_cast<double*>(result_block_alloc(sizeof(double) * (static_cast<std::size_t>(n) + m)));
+  out->x = blk;
+  out->y_ineq = blk + n;
+  out->y_eq = blk + n + mi_;
+  be.download(fin_src, out->x, out->y_ineq);
   out->setup_seconds = sc.setup_seconds;
   out->solve_seconds = elapsed();
 }

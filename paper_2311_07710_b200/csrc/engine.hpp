@@ -51,6 +51,11 @@ void finalize_kkt(const KktRaw& r, Kkt out[2]);  // kkt.hpp:54,63,68-69
 // the KktPrimalTerms reduction outputs (kKktPrimalSums sums, then maxes) into r
 void primal_terms_into(KktRaw& r, const double* g);
 
+// The final point of a solve (x | y_ineq | y_eq in one block): pinned when
+// large. result_block_free returns false for pointers it did not hand out.
+void* result_block_alloc(std::size_t bytes);
+bool result_block_free(void* p);
+
 class DeviceQP {
  public:
   // check_structure: run the per-row CSR checks of validate_dims on the

@@ -396,10 +396,18 @@ class PowerRun {
   }
   bool done() const { return done_; }
   double result() const { return result_; }
+  // a batch boundary at step `at` (batches never straddle it) and a hook run
+  // before every batch with the index of its first step
+  void split_at(int at, std::function<void(int)> hook) {
+    split_ = at;
+    hook_ = std::move(hook);
+  }
 
   void launch() {  // the next batch, asynchronously
     if (done_) return;
+    if (hook_) hook_(it_);
     K_ = std::min(batch_, max_iters_ - it_);
+    if (it_ < split_) K_ = std::min(K_, split_ - it_);
     hps_[0] = PowerState{lambda_, INT_MAX, it_};
     RB_CUDA(cudaMemcpyAsync(dps_.get(), hps_.get(), sizeof(PowerState), cudaMemcpyHostToDevice, s_));
     for (int i = 0; i < K_; ++i) {
@@ -479,7 +487,8 @@ class PowerRun {
   PinnedBuf<PowerState> hps_;
   unsigned sgrid_ = 1;
   double lambda_ = 0.0, result_ = 0.0;
-  int it_ = 0, batch_ = 8, K_ = 0;
+  int it_ = 0, batch_ = 8, K_ = 0, split_ = INT_MAX;
+  std::function<void(int)> hook_;
   bool done_ = false;
 };
 
@@ -578,7 +587,7 @@ Engine::Engine(const rapdhg_qp& p, const rapdhg_config& cfg, Clock::time_point t
   // C4: 97.6 against 7.5 + 90.3 ms — both runs are device-bound)
   norm_q = 1.01 * P_->op_norm_q(qsv_, 5000, 1e-4, cfg.seed);
   tr.mark("norm Q (power iteration)");
-  norm_a = 1.01 * P_->op_norm_a(asv_, atsv_, 5000, 1e-4, cfg.seed);
+  norm_a = 1.01 * norm_a_power(5000, 1e-4, cfg.seed);
   tr.mark("norm A (power iteration)");
   // primal weight init on the scaled c, b (solver.hpp:296-300)
   if (cfg.primal_weight == RAPDHG_PW_ADAPTIVE) {
@@ -614,7 +623,13 @@ Engine::Engine(const rapdhg_qp& p, const rapdhg_config& cfg, Clock::time_point t
     sell_dual_ = sell_eligible(P_->A.rp.get(), nullptr, m_, st_);
     sell_primal_ = sell_eligible(P_->Q.rp.get(), P_->AT.rp.get(), n_, st_);
     setup_slabs();
-    if (full_plans_) setup_colblocks();
+    if (full_plans_) {
+      setup_colblocks();
+    } else {  // built for the norm estimate only: the shards build their own
+      RB_CUDA(cudaStreamSynchronize(st_));
+      dual_ph_ = SlabPhase{};
+      primal_ph_ = SlabPhase{};
+    }
   }
   tr.mark("slab plans");
   setup_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
@@ -696,6 +711,45 @@ void Engine::setup_colblocks() {
   }
 }
 
+// estimate_op_norm on A (opnorm.hpp:36-61) for the solve. Fast mode: the
+// first kNormSlabStep steps run on the rowwise SpMV while the slab plans are
+// still being built on host threads; from that step on (a batch boundary),
+// the plans are joined and the products run on the step's slab phases
+// (PhaseSpmvOp: C4 0.24 instead of 0.39 ms per step). The switch step is
+// fixed (RAPDHG_NORM_SLAB_STEP, default 72; -1 = never), never timing-
+// dependent, so the estimate is deterministic; the sharded solver's setup
+// runs the same code on the same full matrices, so its norm is the same bits.
+double Engine::norm_a_power(int max_iters, double tol, uint64_t seed) {
+  DeviceQP& P = *P_;
+  int K = 72;
+  if (const char* e = std::getenv("RAPDHG_NORM_SLAB_STEP")) K = std::atoi(e);
+  if (P.strict || K < 0 || P.A.nnz == 0) return P.op_norm_a(asv_, atsv_, max_iters, tol, seed);
+  DevBuf<double> v(n_), w(n_), mv(m_);
+  bool slab = false;
+  PowerRun r(
+      P, v, w, n_,
+      [&](StepGate g, cudaStream_t s) {
+        if (slab && dual_ph_.active())
+          P.launches += launch_slab_phase(PhaseSpmvOp<1>{P.A.view(asv_), CsrView{}, v.get(), v.get(), mv.get(), g},
+                                          dual_ph_, s);
+        else
+          P.spmv(P.A, P.sch_dual, asv_, v.get(), mv.get(), g, s);
+        if (slab && primal_ph_.active())
+          P.launches += launch_slab_phase(
+              PhaseSpmvOp<2>{P.Q.view(qsv_), P.AT.view(atsv_), v.get(), mv.get(), w.get(), g}, primal_ph_, s);
+        else
+          P.spmv(P.AT, P.sch_at, atsv_, mv.get(), w.get(), g, s);
+      },
+      false, max_iters, tol, seed, P.st, P.red);
+  r.split_at(K, [&](int it) {
+    if (slab || it < K) return;
+    setup_slabs();  // joins the plan threads (waits if they are still running)
+    slab = dual_ph_.active() || primal_ph_.active();
+  });
+  run_alone(r);
+  return std::sqrt(std::max(r.result(), 0.0));
+}
+
 // The pattern-only part of the slab plans (windows, tiles, layouts: mostly
 // host work), on a host thread with its own stream, started once the matrices
 // are on the device so it overlaps the scaling and the power iterations.
@@ -720,26 +774,16 @@ void Engine::plan_slabs_async() {
       DevBuf<int32_t> len;
       if (dual) {
         dual_choice_ = choose_slabs(P.A.rp.get(), P.A.ci.get(), P.A.rows, P.A.nnz, n_, s2);
-        if (!full_plans_) {
-          RB_CUDA(cudaStreamSynchronize(s2));
-          tr.mark("  slab choice: dual (async)");
-        } else {
         row_lengths(len, P.A.rp.get(), nullptr, m_, s2);
         build_slab_phase(dual_ph_, dual_choice_, 0, P.A.rp.get(), P.A.ci.get(), nullptr, nullptr, 0, m_, len.get(),
                          s2);
         tr.mark("  slab plan: dual (async)");
-        }
       } else {
         primal_choice_ = choose_slabs(P.AT.rp.get(), P.AT.ci.get(), n_, P.AT.nnz, m_, s2);
-        if (!full_plans_) {
-          RB_CUDA(cudaStreamSynchronize(s2));
-          tr.mark("  slab choice: primal (async)");
-        } else {
         row_lengths(len, P.Q.rp.get(), P.AT.rp.get(), n_, s2);
         build_slab_phase(primal_ph_, primal_choice_, 1, P.Q.rp.get(), P.Q.ci.get(), P.AT.rp.get(), P.AT.ci.get(), 0,
                          n_, len.get(), s2);
         tr.mark("  slab plan: primal (async)");
-        }
       }
       RB_CUDA(cudaStreamSynchronize(s2));
     } catch (...) {
@@ -754,6 +798,8 @@ void Engine::plan_slabs_async() {
 }
 
 void Engine::setup_slabs() {
+  if (slabs_ready_) return;  // already done for the norm estimate
+  slabs_ready_ = true;
   Tracer tr(st_);
   plan_future_.get();  // the pattern part (plan_slabs_async)
   plan_future2_.get();
@@ -761,12 +807,16 @@ void Engine::setup_slabs() {
   if (dual_ph_.active()) {
     fill_slab_values(dual_ph_.plan, asv_, nullptr, st_);
     fill_sell_values(dual_ph_.others_sell, asv_, nullptr, st_);
-    assign_slab_ctas(dual_ph_.plan, prepare_slab<DualStepOp<false>>(dual_ph_.plan.view.smem_bytes()), st_);
+    const int smem = dual_ph_.plan.view.smem_bytes();
+    prepare_slab<PhaseSpmvOp<1>>(smem);  // the norm's launches use the step's CTA ranges
+    assign_slab_ctas(dual_ph_.plan, prepare_slab<DualStepOp<false>>(smem), st_);
   }
   if (primal_ph_.active()) {
     fill_slab_values(primal_ph_.plan, qsv_, atsv_, st_);
     fill_sell_values(primal_ph_.others_sell, qsv_, atsv_, st_);
-    assign_slab_ctas(primal_ph_.plan, prepare_slab<PrimalStepOp<false>>(primal_ph_.plan.view.smem_bytes()), st_);
+    const int smem = primal_ph_.plan.view.smem_bytes();
+    prepare_slab<PhaseSpmvOp<2>>(smem);
+    assign_slab_ctas(primal_ph_.plan, prepare_slab<PrimalStepOp<false>>(smem), st_);
   }
   tr.mark("  slab values + launch setup");
 #ifdef RB_SLAB_PROFILE

@@ -147,9 +147,9 @@ class ShardedEngine;
 
 class Engine : public LoopBackend {
  public:
-  // full_plans = false (the sharded solver's setup): only the slab window
-  // choices are made; the slab phases and column blocks over all rows, which
-  // the shards rebuild over their own rows, are skipped.
+  // full_plans = false (the sharded solver's setup): the slab phases over all
+  // rows serve the norm estimate only (then dropped: the shards rebuild them
+  // over their own rows) and no column blocks are built.
   Engine(const rapdhg_qp& p, const rapdhg_config& cfg, Clock::time_point t0, bool full_plans = true);
   ~Engine() override;
   Engine(const Engine&) = delete;
@@ -215,8 +215,10 @@ class Engine : public LoopBackend {
   PinnedBuf<long long> bad_h_;
   bool bad_fresh_ = false;  // bad_h_ was read back by the last evaluate()
   // slab-staged gathers (fast mode, slab.cuh): plans + the complement schedules
-  void setup_slabs();
+  void setup_slabs();  // idempotent (the norm estimate may run it first)
   void plan_slabs_async();
+  bool slabs_ready_ = false;
+  double norm_a_power(int max_iters, double tol, uint64_t seed);
   std::future<void> plan_future_, plan_future2_;
   SlabChoice dual_choice_, primal_choice_;
   SlabPhase dual_ph_, primal_ph_;

@@ -202,6 +202,55 @@ struct SpmvOp {
 };
 
 // ---------------------------------------------------------------------------
+// y = M x of the power iteration (opnorm.hpp:44-46) over the rows of a slab
+// phase (slab.cuh), so the norm estimate can use the step's plans once they
+// are built: K = 1 for the rows of A (gathers x1); K = 2 for the rows of
+// [Q | A'] (the primal step's plan), where only segment 2 (A' x2) is kept —
+// the Q part is summed and dropped (C4: 1e4 of its 5.2e7 entries).
+template <int K>
+struct PhaseSpmvOp {
+  static constexpr bool kStrict = false;
+  static constexpr int kPhase = 0;
+  static constexpr int kWideUnroll = kUnroll;
+  static constexpr bool kStageWindows = true;
+  using AccT = Acc<K>;
+  CsrView s1, s2;  // s2: unused for K = 1
+  const double* x1;
+  const double* x2;
+  double* y;
+  StepGate gate{};
+  int it = 0;
+  __device__ __forceinline__ int len(int r) const {
+    return (s1.rp[r + 1] - s1.rp[r]) + (K > 1 ? s2.rp[r + 1] - s2.rp[r] : 0);
+  }
+  template <int U>
+  __device__ __forceinline__ void accumulate(int r, int lo, int hi, int lane, int stride,
+                                             AccT& acc, const Gather* g) const {
+    if constexpr (K == 1) {
+      acc.v[0] = seg_dot<false, U>(s1.v, s1.ci, g[0], s1.rp[r], lo + lane, hi, stride, acc.v[0]);
+    } else {
+      const int q0 = s1.rp[r];
+      const int L1 = s1.rp[r + 1] - q0;
+      const int p = lo + lane;
+      acc.v[0] = seg_dot<false, U>(s1.v, s1.ci, g[0], q0, p, hi < L1 ? hi : L1, stride, acc.v[0]);
+      acc.v[1] = seg_dot<false, U>(s2.v, s2.ci, g[1], static_cast<int64_t>(s2.rp[r]) - L1,
+                                   next_pos(p, stride, L1), hi, stride, acc.v[1]);
+    }
+  }
+  __device__ __forceinline__ const double* gather_src(int slot) const { return slot ? x2 : x1; }
+  __host__ __device__ PhaseSpmvOp with_views(CsrView a, CsrView b) const {
+    PhaseSpmvOp o = *this;
+    o.s1 = a;
+    o.s2 = b;
+    return o;
+  }
+  struct Pre {};
+  __device__ __forceinline__ Pre prefetch(int) const { return Pre{}; }
+  __device__ __forceinline__ void finish(int r, const AccT& acc) const { y[r] = acc.v[K - 1]; }
+  __device__ __forceinline__ void finish(int r, const AccT& acc, const Pre&) const { y[r] = acc.v[K - 1]; }
+};
+
+// ---------------------------------------------------------------------------
 // KKT products, two points (current and average) per matrix pass
 // (kkt.hpp:32-39, called twice by evaluate_candidate solver.hpp:255-264).
 // Rows of the ORIGINAL stacked A: ax_c = A xu_c, ax_a = A xu_a.

@@ -274,6 +274,9 @@ template <class Op>
 __global__ void __launch_bounds__(kSlabThreads) slab_kernel(const Op op, const SlabView sv) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[kSlabStages], empty[kSlabStages];
+  // power-iteration batches past the stop (uniform over the grid; the gate
+  // was written by an earlier, completed grid)
+  if (HasGate<Op>::closed(op)) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* win = reinterpret_cast<double*>(smem_raw);
   unsigned char* stages = smem_raw + sv.win_max * 8;
@@ -456,6 +459,7 @@ template <class Op>
 __global__ void __launch_bounds__(kBlock) slab_finish_kernel(const Op op, const Op rest, const SlabView sv,
                                                              const SchedView others, int wblocks,
                                                              const SellView osell) {
+  if (HasGate<Op>::closed(op)) return;  // see slab_kernel
   // the next kernel (the next slab kernel, a programmatic dependent launch)
   // may start prefetching its tiles; it waits for this grid before using y / w
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");

@@ -383,7 +383,10 @@ def test_solves_capture_beside_legacy_stream_work():
     allocation) invalidates it. The solver's streams are non-blocking and its
     allocations are ordered on them, so fresh sessions (each capturing anew)
     next to a thread hammering the legacy stream still give the sequential
-    results."""
+    results. (A device-wide synchronisation — cudaDeviceSynchronize, i.e.
+    torch.cuda.synchronize() — from another thread cannot coexist with any
+    stream capture in the process, the library's or torch's own, so the noise
+    thread synchronises its stream only.)"""
     import threading
 
     import torch
@@ -400,7 +403,7 @@ def test_solves_capture_beside_legacy_stream_work():
             while not stop.is_set():
                 b = a @ a  # default (legacy) stream kernels and allocator traffic
                 a = b / b.norm()
-                torch.cuda.synchronize()
+                torch.cuda.current_stream().synchronize()  # not a device-wide sync (see doc)
         except Exception as e:
             errs.append(e)
 

@@ -171,3 +171,26 @@ def test_resident_plan_on_c4_svm_dual(monkeypatch):
         assert ta == tb and rel_err(za.x, zb.x) < 1e-12 and rel_err(za.y_ineq, zb.y_ineq) < 1e-12
     monkeypatch.setenv("RAPDHG_SLAB_RESIDENT", "1")
     assert_results_identical(a, rb.solve(p, cfg))
+
+
+@pytest.mark.parametrize("resident", ["0", "1"])
+def test_norm_estimate_switches_to_slab_phases(resident, monkeypatch):
+    """The norm estimate of A (opnorm.hpp:36-61) runs its first
+    RAPDHG_NORM_SLAB_STEP steps on the rowwise SpMV and the rest on the step's
+    slab phases (PhaseSpmvOp): the same estimate up to rounding, deterministic,
+    and the sharded setup (which runs the same code on the full matrices)
+    gets the same bits."""
+    monkeypatch.setenv("RAPDHG_SLAB", "force")
+    monkeypatch.setenv("RAPDHG_SLAB_RESIDENT", resident)
+    p = rb.generate(rb.Gen.LASSO, 0.05, 2)
+    cfg = rb.SolverConfig(tol=1e-12, max_iters=300, snapshot_interval=60)
+    monkeypatch.setenv("RAPDHG_NORM_SLAB_STEP", "-1")
+    rowwise = rb.solve(p, cfg)
+    for step in ("0", "8", "24"):
+        monkeypatch.setenv("RAPDHG_NORM_SLAB_STEP", step)
+        a = rb.solve(p, cfg)
+        assert a.norm_q == rowwise.norm_q
+        assert a.norm_a == pytest.approx(rowwise.norm_a, rel=1e-12)
+        assert_results_identical(a, rb.solve(p, cfg))  # deterministic
+        for parts in (2, 3):
+            assert_results_identical(rb.solve_sharded(p, cfg, parts), a)

@@ -1,5 +1,6 @@
 // device_csr.cu — structural CSR setup on the device (see device_csr.cuh).
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include <atomic>
 #include <climits>
@@ -25,16 +26,15 @@ __global__ void iota_kernel(int32_t* p, int64_t n) {
 }
 
 // row_of[k]: upper_bound(rp, k) - 1
-__global__ void expand_rows_kernel(int32_t* row_of, const int32_t* rp, int32_t rows, int64_t nnz) {
-  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (k >= nnz) return;
-  int lo = 0, hi = rows;  // find last r with rp[r] <= k
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (rp[mid] <= k) lo = mid;
-    else hi = mid;
-  }
-  row_of[k] = lo;
+// row_of[k] = the row of entry k: each non-empty row writes its id at its
+// first entry (row_of zeroed first), then an inclusive max-scan carries it
+// over the row's other entries (a binary search per entry: 0.39 ms on C4's
+// 5.2e7 entries).
+__global__ void row_starts_kernel(int32_t* row_of, const int32_t* rp, int32_t rows) {
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (r >= rows) return;
+  const int32_t b = rp[r];
+  if (rp[r + 1] > b) row_of[b] = static_cast<int32_t>(r);
 }
 
 __global__ void transpose_fill_kernel(int32_t* out_ci, double* out_v, const int32_t* perm,
@@ -263,10 +263,18 @@ void stack_csr(DevCsr& out, const DevCsr& top, const DevCsr& bot, cudaStream_t s
 
 void expand_rows(DevBuf<int32_t>& row_of, const DevCsr& m, cudaStream_t st) {
   row_of.alloc(static_cast<std::size_t>(m.nnz));
-  if (m.nnz) {
-    expand_rows_kernel<<<grid_for(m.nnz), 256, 0, st>>>(row_of.get(), m.rp.get(), m.rows, m.nnz);
-    RB_LAUNCH_CHECK();
-  }
+  if (!m.nnz) return;
+  if (m.nnz > INT_MAX) throw Error(RAPDHG_E_INTERNAL, "expand_rows: more than 2^31 entries");
+  DevBuf<int32_t> starts(static_cast<std::size_t>(m.nnz));
+  RB_CUDA(cudaMemsetAsync(starts.get(), 0, sizeof(int32_t) * static_cast<std::size_t>(m.nnz), st));
+  row_starts_kernel<<<grid_for(m.rows), 256, 0, st>>>(starts.get(), m.rp.get(), m.rows);
+  RB_LAUNCH_CHECK();
+  std::size_t tb = 0;
+  RB_CUDA(cub::DeviceScan::InclusiveScan(nullptr, tb, starts.get(), row_of.get(), cub::Max(),
+                                         static_cast<int>(m.nnz), st));
+  DevBuf<unsigned char> temp(tb);
+  RB_CUDA(cub::DeviceScan::InclusiveScan(temp.get(), tb, starts.get(), row_of.get(), cub::Max(),
+                                         static_cast<int>(m.nnz), st));
 }
 
 void transpose_csr(DevCsr& out, const DevCsr& m, DevBuf<int32_t>* perm_out, cudaStream_t st) {

@@ -19,15 +19,24 @@ namespace rb {
 
 namespace {
 
+// Counts per bin: a shared-memory histogram per block, then one global
+// atomic per (block, bin) — a global atomic per row serialised 2e6 rows on
+// the 8 counters (C4: 0.78 ms per schedule). Integer counts: exact.
 __global__ void bin_kernel(int32_t* bin, int32_t* idx, const int32_t* len, const int32_t* subset,
                            int64_t rows, int* counts, int epl, int block_min) {
+  __shared__ int h[kNumBins];
+  if (threadIdx.x < kNumBins) h[threadIdx.x] = 0;
+  __syncthreads();
   const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (k >= rows) return;
-  const int32_t r = subset ? subset[k] : static_cast<int32_t>(k);
-  const int b = bin_of_len(len[r], epl, block_min);
-  bin[k] = b;
-  idx[k] = r;
-  atomicAdd(&counts[b], 1);  // integer counts: exact
+  if (k < rows) {
+    const int32_t r = subset ? subset[k] : static_cast<int32_t>(k);
+    const int b = bin_of_len(len[r], epl, block_min);
+    bin[k] = b;
+    idx[k] = r;
+    atomicAdd(&h[b], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x < kNumBins && h[threadIdx.x]) atomicAdd(&counts[threadIdx.x], h[threadIdx.x]);
 }
 
 constexpr int kWinBucket = 128;  // histogram granularity (columns)

@@ -478,7 +478,8 @@ def main():
     # ---- e2e through the public C-ABI from host arrays ----------------------
     ecfg = rb.SolverConfig(tol=args.tol, max_iters=args.max_iters, device=local, strict_parity=args.strict)
     ph = pinned_qp(p)
-    rb.solve(ph, ecfg)  # warm-up (untimed), like the device-timed arm
+    for _ in range(max(1, args.warmup)):  # W untimed warm-up solves, like the device-timed arm
+        rb.solve(ph, ecfg)
     e2e_its, e2e_each, e2e_res = 0, [], None
     for _ in range(max(args.e2e_steps, 1)):
         t = time.perf_counter()

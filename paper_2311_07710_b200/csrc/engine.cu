@@ -1073,6 +1073,9 @@ struct ResultBlocks {
   std::mutex mu;
   std::map<void*, std::pair<std::size_t, bool>> live;  // block -> (bytes, pinned)
   std::size_t pinned_bytes = 0;
+  // their own cache (size classes as pinned_class): a result the caller
+  // still holds must not take the staging buffers the next solve reuses
+  std::vector<std::pair<std::size_t, void*>> free;
 };
 ResultBlocks& result_blocks() {
   static ResultBlocks* rb = new ResultBlocks;  // never destroyed: frees may run at exit
@@ -1090,14 +1093,26 @@ void* result_block_alloc(std::size_t bytes) {
   }
   void* p = nullptr;
   if (pin) {
-    try {
-      p = pinned_acquire(bytes);
-    } catch (...) {
+    const std::size_t cls = pinned_class(bytes);
+    {
+      std::lock_guard<std::mutex> g(R.mu);
+      for (std::size_t i = 0; i < R.free.size(); ++i)
+        if (R.free[i].first == cls) {
+          p = R.free[i].second;
+          R.free[i] = R.free.back();
+          R.free.pop_back();
+          break;
+        }
+    }
+    if (!p && cudaMallocHost(&p, cls) != cudaSuccess) {
+      cudaGetLastError();
       std::lock_guard<std::mutex> g(R.mu);
       R.pinned_bytes -= bytes;
-      throw;
+      pin = false;
+      p = nullptr;
     }
-  } else {
+  }
+  if (!pin) {
     p = std::malloc(bytes);
     if (!p) throw Error(RAPDHG_E_INTERNAL, "out of host memory");
   }
@@ -1118,8 +1133,12 @@ bool result_block_free(void* p) {
     R.live.erase(it);
     if (e.second) R.pinned_bytes -= e.first;
   }
-  if (e.second) pinned_release(p, e.first);
-  else std::free(p);
+  if (e.second) {
+    std::lock_guard<std::mutex> g(R.mu);
+    R.free.emplace_back(pinned_class(e.first), p);
+  } else {
+    std::free(p);
+  }
   return true;
 }
 

@@ -85,6 +85,121 @@ __global__ void boundary_kernel(const int32_t* rp1, const int32_t* ci1, int64_t 
   flag[i] = b;
 }
 
+// Row-aware variant of halo_mark_kernel: rows with skip[r] set are left out.
+__global__ void halo_mark_rows_kernel(const int32_t* rp, const int32_t* ci, int64_t r0, int64_t r1,
+                                      const uint8_t* skip, uint8_t* flags) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x / 32);
+  for (int64_t r = r0 + (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32; r < r1; r += warps) {
+    if (skip[r]) continue;
+    for (int64_t k = rp[r] + lane; k < rp[r + 1]; k += 32) flags[ci[k]] = 1;
+  }
+}
+__global__ void clear_listed_kernel(uint8_t* flags, const int32_t* list, int32_t n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) flags[list[i]] = 0;
+}
+__global__ void set_listed_kernel(uint8_t* flags, const int32_t* list, int32_t n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) flags[list[i]] = 1;
+}
+
+// ---- replicated dense primal rows (ShardedEngine::replicated_step) -------------
+// For replicated row idx (row j = rows[idx]): the positions of its Q entries
+// with a column in [p0, p1) and of its A' entries with a column in [d0, d1) —
+// contiguous, since columns are sorted within a row.
+__device__ __forceinline__ int32_t first_at_least(const int32_t* c, int32_t b, int32_t e, int64_t key) {
+  while (b < e) {
+    const int32_t mid = b + (e - b) / 2;
+    if (c[mid] < key) b = mid + 1;
+    else e = mid;
+  }
+  return b;
+}
+__global__ void rep_ranges_kernel(const int32_t* rows, int32_t nr, const int32_t* qrp, const int32_t* qci, int64_t p0,
+                                  int64_t p1, const int32_t* arp, const int32_t* aci, int64_t d0, int64_t d1,
+                                  int32_t* qlo, int32_t* qhi, int32_t* alo, int32_t* ahi, int32_t* len) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= nr) return;
+  const int32_t j = rows[idx];
+  const int32_t ql = first_at_least(qci, qrp[j], qrp[j + 1], p0), qh = first_at_least(qci, qrp[j], qrp[j + 1], p1);
+  const int32_t al = first_at_least(aci, arp[j], arp[j + 1], d0), ah = first_at_least(aci, arp[j], arp[j + 1], d1);
+  qlo[idx] = ql, qhi[idx] = qh, alo[idx] = al, ahi[idx] = ah;
+  len[idx] = (qh - ql) + (ah - al);
+}
+
+// A shard's partial sums of the replicated rows over its own columns, as a
+// rowwise op ("row" r = replicated index): (Q x_md, A' y) restricted to the
+// owned primal / dual block, the lanes and unroll of the rowwise engine.
+struct RepPartialOp {
+  static constexpr bool kStrict = false;
+  static constexpr int kWideUnroll = kUnroll;
+  static constexpr bool kStageWindows = false;
+  using AccT = Acc<2>;
+  const int32_t *qlo, *qhi, *alo, *ahi;
+  const int32_t* qci;
+  const double* qv;
+  const int32_t* aci;
+  const double* av;
+  const double* xmd;
+  const double* y;
+  double* part;  // 2 per row: (Q part, A' part)
+  __device__ __forceinline__ int len(int r) const { return (qhi[r] - qlo[r]) + (ahi[r] - alo[r]); }
+  template <int U>
+  __device__ __forceinline__ void accumulate(int r, int lo, int hi, int lane, int stride, AccT& acc,
+                                             const Gather* g) const {
+    const int q0 = qlo[r];
+    const int L1 = qhi[r] - q0;
+    const int p = lo + lane;
+    acc.v[0] = seg_dot<false, U>(qv, qci, g[0], q0, p, hi < L1 ? hi : L1, stride, acc.v[0]);
+    acc.v[1] = seg_dot<false, U>(av, aci, g[1], static_cast<int64_t>(alo[r]) - L1, next_pos(p, stride, L1), hi,
+                                 stride, acc.v[1]);
+  }
+  __device__ __forceinline__ const double* gather_src(int slot) const { return slot ? y : xmd; }
+  __device__ __forceinline__ void finish(int r, const AccT& acc) const {
+    part[2 * r] = acc.v[0];
+    part[2 * r + 1] = acc.v[1];
+  }
+};
+
+// Every shard: the replicated rows' sums from all shards' partials (added in
+// shard order: the same bits everywhere), then the primal step's epilogue.
+__global__ void rep_finish_kernel(const PrimalStepOp<false> pr, const int32_t* rows, const double* part, int32_t nr,
+                                  int parts) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= nr) return;
+  const int j = rows[idx];
+  Acc<2> acc;
+  acc.v[0] = 0.0;
+  acc.v[1] = 0.0;
+  const int64_t stride = 2 * static_cast<int64_t>(nr);
+  for (int s = 0; s < parts; ++s) {
+    acc.v[0] += part[s * stride + 2 * idx];
+    acc.v[1] += part[s * stride + 2 * idx + 1];
+  }
+  pr.finish(j, acc, pr.prefetch(j));
+}
+// prologue_kernel / restart_kernel (elementwise.cuh) on the replicated rows
+__global__ void rep_prologue_kernel(const int32_t* rows, int32_t nr, const double* x, const double* xp,
+                                    const double* xb, double* w, double* xmd, const IterParams* P) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= nr) return;
+  const int j = rows[idx];
+  const IterParams& q = P[0];
+  const double xj = x[j];
+  w[j] = q.theta * (xj - xp[j]) + xj;
+  xmd[j] = q.omib * xb[j] + q.ib * xj;
+}
+__global__ void rep_restart_kernel(const int32_t* rows, int32_t nr, double* x, double* xp, double* xb, int from_avg) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= nr) return;
+  const int j = rows[idx];
+  const double v = from_avg ? xb[j] : x[j];
+  x[j] = v;
+  xp[j] = v;
+  xb[j] = v;
+}
+
 // Boundaries of `parts` contiguous blocks of rows with costs len[r] + 2,
 // inner boundaries rounded to multiples of kRedChunk (never decreasing).
 std::vector<int32_t> balanced_bounds(const std::vector<int64_t>& cost_prefix, int32_t rows, int parts) {
@@ -106,21 +221,40 @@ std::vector<int32_t> balanced_bounds(const std::vector<int64_t>& cost_prefix, in
 
 }  // namespace
 
-ShardPlan make_shard_plan(const rapdhg_qp& p, int parts) {
+int64_t replicate_min_len_from_env() {
+  const char* e = std::getenv("RAPDHG_REPLICATE_MIN_LEN");
+  return e ? std::max<int64_t>(0, std::atoll(e)) : 0;
+}
+
+ShardPlan make_shard_plan(const rapdhg_qp& p, int parts, int64_t replicate_min_len) {
   if (parts < 1) invalid("shard plan: parts must be >= 1");
   const int n = p.n, m = p.m_ineq + p.m_eq;
-  // dual rows: rows of [A_ineq; A_eq]
-  std::vector<int64_t> dp(static_cast<std::size_t>(m) + 1, 0);
-  for (int i = 0; i < p.m_ineq; ++i) dp[i + 1] = dp[i] + (p.a_ineq.row_ptr[i + 1] - p.a_ineq.row_ptr[i]) + 2;
-  for (int i = 0; i < p.m_eq; ++i)
-    dp[p.m_ineq + i + 1] = dp[p.m_ineq + i] + (p.a_eq.row_ptr[i + 1] - p.a_eq.row_ptr[i]) + 2;
   // primal rows: rows of [Q | A'] (A' row j = column j of A)
   std::vector<int64_t> colcnt(static_cast<std::size_t>(n), 0);
   for (int64_t k = 0; k < p.a_ineq.nnz; ++k) ++colcnt[p.a_ineq.col_idx[k]];
   for (int64_t k = 0; k < p.a_eq.nnz; ++k) ++colcnt[p.a_eq.col_idx[k]];
-  std::vector<int64_t> pp(static_cast<std::size_t>(n) + 1, 0);
-  for (int j = 0; j < n; ++j) pp[j + 1] = pp[j] + (p.q.row_ptr[j + 1] - p.q.row_ptr[j]) + colcnt[j] + 2;
   ShardPlan plan;
+  std::vector<uint8_t> rep(static_cast<std::size_t>(n), 0);
+  if (replicate_min_len > 0 && parts > 1)
+    for (int j = 0; j < n; ++j)
+      if ((p.q.row_ptr[j + 1] - p.q.row_ptr[j]) + colcnt[j] >= replicate_min_len) {
+        rep[j] = 1;
+        plan.replicated.push_back(j);
+      }
+  // dual rows: rows of [A_ineq; A_eq]; an entry in a replicated column is
+  // summed twice per step (A w here, the replicated rows' partial A'y too)
+  auto dual_cost = [&](const rapdhg_csr& a, int i) {
+    int64_t c = a.row_ptr[i + 1] - a.row_ptr[i] + 2;
+    if (!plan.replicated.empty())
+      for (int64_t k = a.row_ptr[i]; k < a.row_ptr[i + 1]; ++k) c += rep[a.col_idx[k]];
+    return c;
+  };
+  std::vector<int64_t> dp(static_cast<std::size_t>(m) + 1, 0);
+  for (int i = 0; i < p.m_ineq; ++i) dp[i + 1] = dp[i] + dual_cost(p.a_ineq, i);
+  for (int i = 0; i < p.m_eq; ++i) dp[p.m_ineq + i + 1] = dp[p.m_ineq + i] + dual_cost(p.a_eq, i);
+  std::vector<int64_t> pp(static_cast<std::size_t>(n) + 1, 0);
+  for (int j = 0; j < n; ++j)
+    pp[j + 1] = pp[j] + (rep[j] ? 0 : (p.q.row_ptr[j + 1] - p.q.row_ptr[j]) + colcnt[j]) + 2;
   plan.dual = balanced_bounds(dp, m, parts);
   plan.primal = balanced_bounds(pp, n, parts);
   return plan;
@@ -417,6 +551,13 @@ struct ShardedEngine::Shard {
   DevBuf<long long> bad, vote;
   ReduceScratch red;
   DevBuf<double> red_out;
+  // replicated dense rows (ShardedEngine::replicated_step): the sub-ranges of
+  // their entries on this shard's columns, a schedule over them, the partial
+  // sums of all shards, and the step's schedule over the owned rows that are
+  // not replicated
+  DevBuf<int32_t> rep_qlo, rep_qhi, rep_alo, rep_ahi;
+  Schedule sch_rep, sch_primal_step;
+  DevBuf<double> rep_part;
 };
 
 ShardedEngine::ShardedEngine(const rapdhg_qp& p, const rapdhg_config& cfg, int parts, int rank,
@@ -428,13 +569,22 @@ ShardedEngine::ShardedEngine(const rapdhg_qp& p, const rapdhg_config& cfg, int p
   // slab phases / column blocks over all rows are not built (each shard
   // builds its own over its rows below)
   full_ = std::make_unique<Engine>(p, cfg, t0, /*full_plans=*/false);
-  plan_ = make_shard_plan(p, parts);
+  plan_ = make_shard_plan(p, parts, replicate_min_len_from_env());
   st_ = full_->st_;
   AllocStreamScope scope(st_);
   DeviceQP& P = *full_->P_;
   const int n = P.n, m = P.m;
   pb_.assign(plan_.primal.begin(), plan_.primal.end());
   db_.assign(plan_.dual.begin(), plan_.dual.end());
+  nrep_ = static_cast<int32_t>(plan_.replicated.size());
+  if (nrep_) {
+    rep_rows_.alloc(nrep_);
+    rep_rows_.upload(plan_.replicated.data(), nrep_, st_);
+    rep_flag_.alloc(n);
+    rep_flag_.zero(st_);
+    set_listed_kernel<<<grid1(nrep_), 256, 0, st_>>>(rep_flag_.get(), rep_rows_.get(), nrep_);
+    RB_LAUNCH_CHECK();
+  }
   for (int s = 0; s < parts; ++s) {
     if (rank >= 0 && s != rank) continue;
     auto sh = std::make_unique<Shard>();
@@ -454,7 +604,7 @@ ShardedEngine::ShardedEngine(const rapdhg_qp& p, const rapdhg_config& cfg, int p
     }
     row_lengths(len, P.Q.rp.get() + sh->p0, P.AT.rp.get() + sh->p0, sh->p1 - sh->p0, st_);
     build_schedule(sh->sch_primal, len.get(), sh->p1 - sh->p0, false, st_);
-    if (!full_->primal_choice_.empty() && sh->p1 > sh->p0) {
+    if (nrep_ == 0 && !full_->primal_choice_.empty() && sh->p1 > sh->p0) {
       build_slab_phase(sh->primal_ph, full_->primal_choice_, 1, P.Q.rp.get(), P.Q.ci.get(), P.AT.rp.get(),
                        P.AT.ci.get(), static_cast<int32_t>(sh->p0), static_cast<int32_t>(sh->p1), len.get(), st_);
       if (sh->primal_ph.active()) {
@@ -501,7 +651,7 @@ ShardedEngine::ShardedEngine(const rapdhg_qp& p, const rapdhg_config& cfg, int p
     if (!sh->dual_ph.active() && sh->d1 > sh->d0)
       build_colblocked_dual(sh->cbd, full_->cb_nb_dual_, P.A.rp.get() + sh->d0, P.A.ci.get(),
                             static_cast<int32_t>(sh->d1 - sh->d0), n, full_->asv_, full_->sell_dual_, st_);
-    if (!sh->primal_ph.active() && sh->p1 > sh->p0)
+    if (nrep_ == 0 && !sh->primal_ph.active() && sh->p1 > sh->p0)
       build_colblocked_primal(sh->cbp, full_->cb_nq_, full_->cb_na_, P.Q.rp.get() + sh->p0, P.Q.ci.get(), full_->qsv_,
                               P.AT.rp.get() + sh->p0, P.AT.ci.get(), full_->atsv_,
                               static_cast<int32_t>(sh->p1 - sh->p0), n, m, full_->sell_primal_, st_);
@@ -511,15 +661,80 @@ ShardedEngine::ShardedEngine(const rapdhg_qp& p, const rapdhg_config& cfg, int p
                       static_cast<int32_t>(sh->d1 - sh->d0), st_);
       fill_sell_values(sh->sell_dual, full_->asv_, nullptr, st_);
     }
-    if (full_->sell_primal_ && !sh->primal_ph.active() && !sh->cbp.active() && sh->p1 > sh->p0) {
+    if (nrep_ == 0 && full_->sell_primal_ && !sh->primal_ph.active() && !sh->cbp.active() && sh->p1 > sh->p0) {
       build_sell_plan(sh->sell_primal, P.Q.rp.get() + sh->p0, P.Q.ci.get(), P.AT.rp.get() + sh->p0, P.AT.ci.get(),
                       static_cast<int32_t>(sh->p1 - sh->p0), st_);
       fill_sell_values(sh->sell_primal, full_->qsv_, full_->atsv_, st_);
     }
   }
+  build_replicated();
   build_overlap(rank < 0);
   build_halos();
   RB_CUDA(cudaStreamSynchronize(st_));
+}
+
+void ShardedEngine::build_replicated() {
+  if (!nrep_) return;
+  DeviceQP& P = *full_->P_;
+  const thrust::counting_iterator<int32_t> idx(0);
+  for (auto& sh : shards_) {
+    DevBuf<int32_t> len(nrep_);
+    sh->rep_qlo.alloc(nrep_), sh->rep_qhi.alloc(nrep_), sh->rep_alo.alloc(nrep_), sh->rep_ahi.alloc(nrep_);
+    rep_ranges_kernel<<<grid1(nrep_), 256, 0, st_>>>(rep_rows_.get(), nrep_, P.Q.rp.get(), P.Q.ci.get(), sh->p0, sh->p1,
+                                                     P.AT.rp.get(), P.AT.ci.get(), sh->d0, sh->d1, sh->rep_qlo.get(),
+                                                     sh->rep_qhi.get(), sh->rep_alo.get(), sh->rep_ahi.get(), len.get());
+    RB_LAUNCH_CHECK();
+    build_schedule(sh->sch_rep, len.get(), nrep_, false, st_);
+    sh->rep_part.alloc(static_cast<std::size_t>(parts_) * 2 * nrep_);
+    sh->rep_part.zero(st_);
+    // the step's primal rows: the owned ones that are not replicated
+    const int64_t nl = sh->p1 - sh->p0;
+    if (nl <= 0) continue;
+    DevBuf<uint8_t> keep(nl);
+    invert_kernel<<<grid1(nl), 256, 0, st_>>>(rep_flag_.get() + sh->p0, keep.get(), nl);
+    RB_LAUNCH_CHECK();
+    DevBuf<int32_t> list(nl), cnt(1), plen;
+    std::size_t tb = 0;
+    RB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, idx, keep.get(), list.get(), cnt.get(), static_cast<int>(nl), st_));
+    DevBuf<unsigned char> tmp(tb);
+    RB_CUDA(cub::DeviceSelect::Flagged(tmp.get(), tb, idx, keep.get(), list.get(), cnt.get(), static_cast<int>(nl), st_));
+    int32_t k = 0;
+    RB_CUDA(cudaMemcpyAsync(&k, cnt.get(), sizeof(k), cudaMemcpyDeviceToHost, st_));
+    RB_CUDA(cudaStreamSynchronize(st_));
+    row_lengths(plen, P.Q.rp.get() + sh->p0, P.AT.rp.get() + sh->p0, nl, st_);
+    if (k) build_schedule(sh->sch_primal_step, plen.get(), k, false, st_, list.get());
+    RB_CUDA(cudaStreamSynchronize(st_));
+  }
+  if (std::getenv("RAPDHG_TRACE"))
+    std::fprintf(stderr, "[shard] %d replicated primal rows (RAPDHG_REPLICATE_MIN_LEN=%lld)\n", nrep_,
+                 static_cast<long long>(replicate_min_len_from_env()));
+}
+
+// The replicated rows' part of primal step `it` (after the dual step, before
+// the y exchange: each shard's partials need only the y it computed).
+void ShardedEngine::replicated_step(int it, int c) {
+  DeviceQP& P = *full_->P_;
+  const Engine& e = *full_;
+  std::vector<double*> bufs;
+  for (auto& sh : shards_) {
+    RepPartialOp op{sh->rep_qlo.get(), sh->rep_qhi.get(), sh->rep_alo.get(), sh->rep_ahi.get(),
+                    P.Q.ci.get(),      e.qsv_,            P.AT.ci.get(),     e.atsv_,
+                    sh->XMD[c].get(),  sh->y.get(),       sh->rep_part.get() + static_cast<int64_t>(sh->id) * 2 * nrep_};
+    launch_rowwise(op, sh->sch_rep.view, st_);
+    ++launches_;
+    bufs.push_back(sh->rep_part.get());
+  }
+  std::vector<int64_t> bounds(parts_ + 1);
+  for (int k = 0; k <= parts_; ++k) bounds[k] = static_cast<int64_t>(k) * 2 * nrep_;
+  tr_->allgatherv(bufs, bounds, st_);
+  for (auto& sh : shards_) {
+    const PrimalStepOp<false> pr{CsrView{}, CsrView{}, nullptr, nullptr, sh->X[c].get(), sh->X[c ^ 1].get(),
+                                 sh->xb.get(), e.csv_, sh->w.get(), sh->XMD[c ^ 1].get(), params_.get(), it,
+                                 sh->bad.get(), e.lsv_, e.hsv_};
+    rep_finish_kernel<<<grid1(nrep_), 256, 0, st_>>>(pr, rep_rows_.get(), sh->rep_part.get(), nrep_, parts_);
+    RB_LAUNCH_CHECK();
+    ++launches_;
+  }
 }
 
 // Interior / boundary row lists of each shard's plain-path ops (see Shard).
@@ -535,7 +750,7 @@ void ShardedEngine::build_overlap(bool emulated) {
   const Engine& e = *full_;
   DeviceQP& P = *e.P_;
   overlap_dual_ = e.dual_choice_.empty() && e.cb_nb_dual_ <= 1;
-  overlap_primal_ = e.primal_choice_.empty() && e.cb_nq_ <= 1 && e.cb_na_ <= 1;
+  overlap_primal_ = e.primal_choice_.empty() && e.cb_nq_ <= 1 && e.cb_na_ <= 1 && nrep_ == 0;
   if (!overlap_dual_ && !overlap_primal_) return;
   const thrust::counting_iterator<int32_t> idx(0);
   auto split = [&](int64_t rows, const int32_t* rp1, const int32_t* ci1, int64_t lo1, int64_t hi1,
@@ -630,7 +845,15 @@ void ShardedEngine::build_halos() {
       flags.zero(st_);
       const int64_t r0 = (*sp.rows)[p], r1 = (*sp.rows)[p + 1];
       if (r1 > r0) {
-        halo_mark_kernel<<<4 * kSMs, 256, 0, st_>>>(sp.mat->rp.get(), sp.mat->ci.get(), r0, r1, flags.get());
+        if (nrep_ && kind != kHaloW)  // primal rows: the replicated ones gather nothing remote
+          halo_mark_rows_kernel<<<8 * kSMs, 256, 0, st_>>>(sp.mat->rp.get(), sp.mat->ci.get(), r0, r1,
+                                                           rep_flag_.get(), flags.get());
+        else
+          halo_mark_kernel<<<4 * kSMs, 256, 0, st_>>>(sp.mat->rp.get(), sp.mat->ci.get(), r0, r1, flags.get());
+        RB_LAUNCH_CHECK();
+      }
+      if (nrep_ && kind != kHaloY) {  // w / x_md of the replicated rows are on every shard
+        clear_listed_kernel<<<grid1(nrep_), 256, 0, st_>>>(flags.get(), rep_rows_.get(), nrep_);
         RB_LAUNCH_CHECK();
       }
       L[p].alloc(N);
@@ -784,6 +1007,14 @@ void ShardedEngine::body(int len, int cur) {
       ++launches_;
     }
   }
+  if (nrep_)
+    for (auto& sh : shards_) {
+      rep_prologue_kernel<<<grid1(nrep_), 256, 0, st_>>>(rep_rows_.get(), nrep_, sh->X[cur].get(),
+                                                         sh->X[cur ^ 1].get(), sh->xb.get(), sh->w.get(),
+                                                         sh->XMD[cur].get(), params_.get());
+      RB_LAUNCH_CHECK();
+      ++launches_;
+    }
   // the w / x_md exchange feeding step `it`: on st2_ beside the interior dual
   // rows when the dual overlaps, else in line on st_
   auto exchange_wx = [&](int c_md) {
@@ -844,7 +1075,7 @@ void ShardedEngine::body(int len, int cur) {
           launch_sell(pr, sh->sell_primal, st_);
           ++launches_;
         } else {
-          launch_rowwise(pr, sh->sch_primal.view, st_);
+          launch_rowwise(pr, (nrep_ ? sh->sch_primal_step : sh->sch_primal).view, st_);
           ++launches_;
         }
       }
@@ -856,6 +1087,7 @@ void ShardedEngine::body(int len, int cur) {
     } else {
       dual(0);
     }
+    if (nrep_) replicated_step(it, c);
     if (overlap_primal_) {  // the y exchange beside the interior primal rows
       fork();
       step_exchange([](Shard& sh) { return sh.y.get(); }, kHaloY, st2_);
@@ -1009,6 +1241,12 @@ void ShardedEngine::restart(bool from_avg, double* dx, double* dy) {
                                                  sh->yb.get() + sh->d0, from_avg ? 1 : 0, 0, static_cast<int>(ml));
     RB_LAUNCH_CHECK();
     launches_ += 2;
+    if (nrep_) {  // the replicated rows' state is every shard's (idempotent on the owner's)
+      rep_restart_kernel<<<grid1(nrep_), 256, 0, st_>>>(rep_rows_.get(), nrep_, sh->X[cur_].get(),
+                                                        sh->X[cur_ ^ 1].get(), sh->xb.get(), from_avg ? 1 : 0);
+      RB_LAUNCH_CHECK();
+      ++launches_;
+    }
   }
   const int cur = cur_;
   double sx[1], sy[1];

@@ -29,12 +29,19 @@
 namespace rb {
 
 struct ShardPlan {
-  std::vector<int32_t> dual;    // parts + 1 bounds over [0, m)
-  std::vector<int32_t> primal;  // parts + 1 bounds over [0, n)
+  std::vector<int32_t> dual;        // parts + 1 bounds over [0, m)
+  std::vector<int32_t> primal;      // parts + 1 bounds over [0, n)
+  std::vector<int32_t> replicated;  // dense primal rows computed on every shard (sorted)
 };
 
 // nnz-balanced contiguous blocks; inner bounds are multiples of kRedChunk.
-ShardPlan make_shard_plan(const rapdhg_qp& p, int parts);
+// replicate_min_len > 0: the rows of [Q | A'] with at least that many entries
+// are replicated (SURVEY §8(e) "dense-coupling columns"): every shard sums
+// their entries on its own columns and the partial sums are exchanged, so
+// they cost no primal-block balance and no y exchange (see ShardedEngine).
+ShardPlan make_shard_plan(const rapdhg_qp& p, int parts, int64_t replicate_min_len = 0);
+// RAPDHG_REPLICATE_MIN_LEN (0 / unset: no replication)
+int64_t replicate_min_len_from_env();
 
 // Halo exchange of one gathered vector: per local shard, the
 // entries its rows reference that other shards own (recv_idx, grouped by owner,
@@ -98,6 +105,19 @@ class ShardedEngine : public LoopBackend {
  private:
   struct Shard;
   void body(int len, int cur);
+  // Replicated dense primal rows (plan_.replicated, nrep_ of them): every
+  // shard sums each such row's entries on the columns it owns (Q: its primal
+  // block, A': its dual block — the y it has just computed), the 2 * nrep_
+  // partial sums of all shards are allgathered and added in shard order, and
+  // every shard runs the rows' epilogue, so x, x_bar, w and x_md of those rows
+  // are the same bits everywhere and never travel. Deterministic for a given
+  // shard count; the sums' association differs from one GPU's (not a parity
+  // mode: iterates agree to rounding, see tests/test_gpu_shard.py).
+  void build_replicated();
+  void replicated_step(int it, int c);
+  int32_t nrep_ = 0;
+  DevBuf<int32_t> rep_rows_;
+  DevBuf<uint8_t> rep_flag_;  // n: 1 on replicated rows
   void exchange(double* (*pick)(Shard&), bool primal_space);  // allgather-v on st_
   // per-step exchanges: the halo of the gathered entries when that moves at
   // most half of an allgather (RAPDHG_HALO=on|off|auto), else the allgather

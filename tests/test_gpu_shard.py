@@ -112,3 +112,56 @@ def test_overlapped_exchanges_bit_identical(parts, halo, monkeypatch):
     assert_results_identical(a, rb.solve(p, cfg))
     monkeypatch.setenv("RAPDHG_OVERLAP", "0")
     assert_results_identical(a, rb.solve_sharded(p, cfg, parts))
+
+
+def _rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300)) if a.size else 0.0
+
+
+def _close_trajectories(a, b, tol=1e-9):
+    """Same decisions; iterates within `tol` (the replicated rows' sums are
+    associated per shard, so the two runs differ by rounding only)."""
+    assert a.status == b.status and a.iterations == b.iterations and a.restarts == b.restarts
+    assert [L.restarted for L in a.log] == [L.restarted for L in b.log]
+    assert len(a.snapshots) == len(b.snapshots) > 0
+    for (ta, za), (tb, zb) in zip(a.snapshots, b.snapshots):
+        assert ta == tb
+        assert _rel(za.x, zb.x) <= tol and _rel(np.concatenate([za.y_ineq, za.y_eq]),
+                                                 np.concatenate([zb.y_ineq, zb.y_eq])) <= tol
+    assert a.norm_q == b.norm_q and a.norm_a == b.norm_a  # the setup is not sharded
+
+
+@pytest.mark.parametrize("parts", [2, 3, 4, 8])
+@pytest.mark.parametrize("halo", ["auto", "off"])
+def test_replicated_dense_rows_svm(parts, halo, monkeypatch):
+    """SURVEY §8(e) dense-coupling columns: with RAPDHG_REPLICATE_MIN_LEN the
+    SVM's feature rows of [Q | A'] are computed on every shard from per-shard
+    partial sums (no y exchange for them): deterministic, and the trajectory of
+    one GPU up to rounding."""
+    p = rb.generate(rb.Gen.SVM, 0.01, 4)  # 100 feature rows of ~4000 entries
+    cfg = rb.SolverConfig(tol=1e-8, max_iters=600, snapshot_interval=40)
+    one = rb.solve(p, cfg)
+    monkeypatch.setenv("RAPDHG_HALO", halo)
+    monkeypatch.setenv("RAPDHG_REPLICATE_MIN_LEN", "100")
+    a = rb.solve_sharded(p, cfg, parts)
+    assert_results_identical(a, rb.solve_sharded(p, cfg, parts))  # deterministic
+    _close_trajectories(a, one)
+    monkeypatch.setenv("RAPDHG_REPLICATE_MIN_LEN", "0")
+    assert_results_identical(rb.solve_sharded(p, cfg, parts), one)  # off: bit-identical again
+
+
+def test_replicated_rows_other_patterns(monkeypatch):
+    """Replication on patterns whose long rows also have Q entries (Lasso) and
+    on a random QP, with box bounds, restarts and the time-to-tolerance path."""
+    monkeypatch.setenv("RAPDHG_REPLICATE_MIN_LEN", "60")
+    p = rb.generate(rb.Gen.LASSO, 0.05, 2)
+    cfg = rb.SolverConfig(tol=1e-7, max_iters=3000, snapshot_interval=200)
+    a, one = rb.solve_sharded(p, cfg, 3), rb.solve(p, cfg)
+    assert a.status == one.status == rb.SolveStatus.kOptimal
+    assert abs(p.objective(a.point.x) - p.objective(one.point.x)) <= 1e-6 * max(1.0, abs(p.objective(one.point.x)))
+    q = random_qp(22, n=3000, mi=1500, me=200, dens=0.004, q_rank=800)
+    lens = np.diff(q.q.row_ptr) + np.bincount(np.concatenate([q.a_ineq.col_idx, q.a_eq.col_idx]), minlength=3000)
+    monkeypatch.setenv("RAPDHG_REPLICATE_MIN_LEN", str(int(np.percentile(lens, 90))))
+    cfg = rb.SolverConfig(tol=1e-9, max_iters=800, snapshot_interval=40)
+    _close_trajectories(rb.solve_sharded(q, cfg, 4), rb.solve(q, cfg))

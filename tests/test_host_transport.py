@@ -102,3 +102,29 @@ def test_library_drives_process_group_callbacks(world):
 @pytest.mark.parametrize("halo", [False, True])
 def test_two_process_sharded_solve_bit_identical(halo):
     _run(_solve_worker, 2, halo, timeout=600)
+
+
+def _replicated_worker(rank, world, port, q):
+    try:
+        os.environ["RAPDHG_REPLICATE_MIN_LEN"] = "100"
+        dist = _init(rank, world, port)
+        import paper_2311_07710_b200 as rb
+        from test_oracle import assert_results_identical
+
+        p = rb.generate(rb.Gen.SVM, 0.01, 4)
+        cfg = rb.SolverConfig(tol=1e-8, max_iters=600, snapshot_interval=40)
+        got = rb.solve_sharded(p, cfg, transport=rb.ProcessGroupTransport())
+        # the same shard count emulated in one process: the same bits
+        assert_results_identical(got, rb.solve_sharded(p, cfg, world))
+        q.put((rank, "ok", f"{got.iterations} it"))
+        dist.destroy_process_group()
+    except Exception as e:
+        q.put((rank, "error", repr(e)))
+
+
+@pytest.mark.gpu
+def test_two_process_replicated_rows_match_emulated():
+    """Replicated dense rows (RAPDHG_REPLICATE_MIN_LEN) through the host
+    transport: the partial sums' allgather runs over the process group, and
+    the result is the emulated run's with the same shard count, bit for bit."""
+    _run(_replicated_worker, 2, timeout=600)

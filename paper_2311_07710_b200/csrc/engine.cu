@@ -1,5 +1,9 @@
 // engine.cu — setup numerics and the iteration loop of the B200 rAPDHG solver.
 // See engine.hpp. Reference: /root/reference/proj/include/rapdhg/solver.hpp.
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
 #include <algorithm>
 #include <functional>
 #include <future>
@@ -30,6 +34,37 @@ inline unsigned grid1(int64_t n) { return static_cast<unsigned>(ceil_div(n > 0 ?
 __global__ void scale_copy_kernel(double* v, const double* w, double s, int64_t n) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i < n) v[i] = w[i] * s;  // v = w; scale(v, 1/nrm) (opnorm.hpp:52-53)
+}
+
+__global__ void gather_scale_kernel(double* v, const double* full, const int32_t* idx, bool scale, double s,
+                                    int64_t n) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) v[i] = scale ? full[idx[i]] * s : full[idx[i]];
+}
+
+// Rows and columns a pattern touches (row non-empty, or referenced).
+__global__ void touched_kernel(const int32_t* rp, const int32_t* ci, int32_t n, uint8_t* flag) {
+  const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n || rp[r + 1] == rp[r]) return;
+  flag[r] = 1;
+  for (int32_t k = rp[r]; k < rp[r + 1]; ++k) flag[ci[k]] = 1;  // racing writes of the same 1
+}
+__global__ void compact_csr_kernel(const int32_t* act, int32_t nc, const int32_t* rp, const int32_t* ci,
+                                   const double* v, const int32_t* newidx, const int32_t* rpc, int32_t* cic,
+                                   double* vc) {
+  const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nc) return;
+  const int32_t o = act[r];
+  int32_t q = rpc[r];
+  for (int32_t k = rp[o]; k < rp[o + 1]; ++k, ++q) cic[q] = newidx[ci[k]], vc[q] = v[k];
+}
+__global__ void newidx_kernel(const int32_t* act, int32_t nc, int32_t* newidx) {
+  const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < nc) newidx[act[k]] = k;
+}
+__global__ void act_lengths_kernel(const int32_t* act, int32_t nc, const int32_t* rp, int32_t* len) {
+  const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < nc) len[k] = rp[act[k] + 1] - rp[act[k]];
 }
 
 __global__ void div_kernel(double* out, const double* v, const double* d, int64_t n) {
@@ -342,6 +377,14 @@ void DeviceQP::scale_values(const double* d, DevBuf<double>& qs, DevBuf<double>&
   RB_CUDA(cudaStreamSynchronize(st));
 }
 
+RandomStart draw_random_start(int len, uint64_t seed) {
+  RandomStart r;
+  r.rng.seed(seed);
+  r.v.resize(static_cast<std::size_t>(std::max(len, 0)));
+  for (double& x : r.v) x = 2.0 * (static_cast<double>(r.rng() >> 11) * 0x1.0p-53) - 1.0;  // opnorm.hpp:22-24
+  return r;
+}
+
 // estimate_op_norm / estimate_op_norm_symmetric (opnorm.hpp:36-87)
 namespace {
 // Device copy of the host's per-step decision (opnorm.hpp:48-59): thread 0
@@ -383,15 +426,26 @@ __global__ void power_step_kernel(double* v, const double* w, const double* hist
 class PowerRun {
  public:
   using Step = std::function<void(StepGate, cudaStream_t)>;  // w = M v
+  // compact (optional, `len` entries): the iteration runs on v[compact[k]]
+  // only — the indices outside stay 0 after the first product (rows and
+  // columns the matrix never touches); the random start is still drawn and
+  // normalised over all `full_len` entries, as the reference does
   PowerRun(DeviceQP& P, DevBuf<double>& v, DevBuf<double>& w, int len, Step step, bool absval, int max_iters,
-           double tol, uint64_t seed, cudaStream_t s, ReduceScratch& red)
+           double tol, uint64_t seed, cudaStream_t s, ReduceScratch& red, const int32_t* compact = nullptr,
+           int full_len = 0, const RandomStart* pre = nullptr)
       : P_(P), v_(v), w_(w), len_(len), step_(std::move(step)), absval_(absval), max_iters_(max_iters),
-        tol_(tol), rng_(seed), s_(s), red_(red), hist_(2 * kMaxBatch), dps_(1), out_(1) {
+        tol_(tol), rng_(seed), s_(s), red_(red), hist_(2 * kMaxBatch), dps_(1), out_(1), compact_(compact),
+        full_len_(compact ? full_len : len) {
     hh_.alloc(2 * kMaxBatch);
     hps_.alloc(2);
     hout_.alloc(1);
     sgrid_ = static_cast<unsigned>(std::min<int64_t>(ceil_div(len, 256), 4 * kSMs));
-    random_unit();
+    if (pre && static_cast<int>(pre->v.size()) == full_len_) {  // drawn ahead: the same numbers
+      rng_ = pre->rng;
+      random_unit(pre->v.data());
+    } else {
+      random_unit();
+    }
     done_ = max_iters_ <= 0;
   }
   bool done() const { return done_; }
@@ -410,17 +464,36 @@ class PowerRun {
     if (it_ < split_) K_ = std::min(K_, split_ - it_);
     hps_[0] = PowerState{lambda_, INT_MAX, it_};
     RB_CUDA(cudaMemcpyAsync(dps_.get(), hps_.get(), sizeof(PowerState), cudaMemcpyHostToDevice, s_));
-    for (int i = 0; i < K_; ++i) {
-      const StepGate gate{&dps_.get()->stop, i};
-      step_(gate, s_);
-      launch_reduce<2, 0>(DotAndSumSq{v_.get(), w_.get(), gate}, len_, P_.strict, red_, hist_.get() + 2 * i, s_);
-      power_step_kernel<<<sgrid_, 256, 0, s_>>>(v_.get(), w_.get(), hist_.get() + 2 * i, dps_.get(), i, tol_,
-                                                absval_, len_);
-      RB_LAUNCH_CHECK();
-      P_.launches += 2;
+    if (P_.graphs) {  // every batch of K steps in a mode has the same launches: one graph each, replayed
+      const int key = 2 * K_ + mode_;
+      auto g = graphs_.find(key);
+      if (g == graphs_.end()) {
+        const int64_t l0 = P_.launches;
+        cudaGraph_t graph;
+        RB_CUDA(cudaStreamBeginCapture(s_, cudaStreamCaptureModeThreadLocal));
+        enqueue_steps();
+        RB_CUDA(cudaStreamEndCapture(s_, &graph));
+        cudaGraphExec_t exec;
+        const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        RB_CUDA(e);
+        g = graphs_.emplace(key, std::make_pair(exec, P_.launches - l0)).first;
+        P_.launches = l0;
+      }
+      RB_CUDA(cudaGraphLaunch(g->second.first, s_));
+      P_.launches += g->second.second;
+    } else {
+      enqueue_steps();
     }
     RB_CUDA(cudaMemcpyAsync(hh_.get(), hist_.get(), sizeof(double) * 2 * K_, cudaMemcpyDeviceToHost, s_));
     RB_CUDA(cudaMemcpyAsync(hps_.get() + 1, dps_.get(), sizeof(PowerState), cudaMemcpyDeviceToHost, s_));
+  }
+
+  // mode: which launches a step makes (the norm of A switches to the slab
+  // phases); part of the graph key
+  void set_mode(int m) { mode_ = m; }
+  ~PowerRun() {
+    for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second.first);
   }
 
   void finish() {  // wait for the batch and replay opnorm.hpp:44-60 over it
@@ -453,20 +526,42 @@ class PowerRun {
 
  private:
   static constexpr int kMaxBatch = 64;
+  void enqueue_steps() {
+    for (int i = 0; i < K_; ++i) {
+      const StepGate gate{&dps_.get()->stop, i};
+      step_(gate, s_);
+      launch_reduce<2, 0>(DotAndSumSq{v_.get(), w_.get(), gate}, len_, P_.strict, red_, hist_.get() + 2 * i, s_);
+      power_step_kernel<<<sgrid_, 256, 0, s_>>>(v_.get(), w_.get(), hist_.get() + 2 * i, dps_.get(), i, tol_,
+                                                absval_, len_);
+      RB_LAUNCH_CHECK();
+      P_.launches += 2;
+    }
+  }
   // random_unit (opnorm.hpp:20-30): host mt19937_64 stream, normalised on device
-  void random_unit() {
-    std::vector<double> h(len_);
-    for (double& x : h) x = 2.0 * (static_cast<double>(rng_() >> 11) * 0x1.0p-53) - 1.0;
-    v_.upload(h.data(), len_, s_);
-    launch_reduce<1, 0>(SumSq{v_.get()}, len_, P_.strict, red_, out_.get(), s_);
+  void random_unit(const double* drawn = nullptr) {
+    std::vector<double> h;
+    if (!drawn) {
+      h.resize(full_len_);
+      for (double& x : h) x = 2.0 * (static_cast<double>(rng_() >> 11) * 0x1.0p-53) - 1.0;
+      drawn = h.data();
+    }
+    DevBuf<double> full(compact_ ? full_len_ : 0);
+    double* dst = compact_ ? full.get() : v_.get();
+    RB_CUDA(cudaMemcpyAsync(dst, drawn, sizeof(double) * full_len_, cudaMemcpyHostToDevice, s_));
+    launch_reduce<1, 0>(SumSq{dst}, full_len_, P_.strict, red_, out_.get(), s_);
     RB_CUDA(cudaMemcpyAsync(hout_.get(), out_.get(), sizeof(double), cudaMemcpyDeviceToHost, s_));
     RB_CUDA(cudaStreamSynchronize(s_));
     const double nrm = std::sqrt(hout_[0]);
-    if (nrm > 0.0) {
-      scale_copy_kernel<<<grid1(len_), 256, 0, s_>>>(v_.get(), v_.get(), 1.0 / nrm, len_);
+    const double inv = nrm > 0.0 ? 1.0 / nrm : 1.0;
+    if (compact_) {  // v[k] = full[compact[k]] * (1 / nrm), the same operation per entry
+      gather_scale_kernel<<<grid1(len_), 256, 0, s_>>>(v_.get(), full.get(), compact_, nrm > 0.0, inv, len_);
+      RB_LAUNCH_CHECK();
+    } else if (nrm > 0.0) {
+      scale_copy_kernel<<<grid1(len_), 256, 0, s_>>>(v_.get(), v_.get(), inv, len_);
       RB_LAUNCH_CHECK();
     }
     P_.launches += 2;
+    RB_CUDA(cudaStreamSynchronize(s_));  // `full` is freed in s_'s order below; h stays valid until here
   }
 
   DeviceQP& P_;
@@ -485,10 +580,13 @@ class PowerRun {
   DevBuf<double> out_;
   PinnedBuf<double> hh_, hout_;
   PinnedBuf<PowerState> hps_;
+  const int32_t* compact_ = nullptr;
+  int full_len_ = 0;
   unsigned sgrid_ = 1;
   double lambda_ = 0.0, result_ = 0.0;
-  int it_ = 0, batch_ = 8, K_ = 0, split_ = INT_MAX;
+  int it_ = 0, batch_ = 8, K_ = 0, split_ = INT_MAX, mode_ = 0;
   std::function<void(int)> hook_;
+  std::map<int, std::pair<cudaGraphExec_t, int64_t>> graphs_;  // 2 K + mode -> graph, launches
   bool done_ = false;
 };
 
@@ -500,12 +598,57 @@ void run_alone(PowerRun& r) {
 }
 }  // namespace
 
-double DeviceQP::op_norm_q(const double* qv, int max_iters, double tol, uint64_t seed) {
+double DeviceQP::op_norm_q(const double* qv, int max_iters, double tol, uint64_t seed, const RandomStart* pre) {
   if (Q.nnz == 0) return 0.0;
+  // fast mode: when Q touches at most half of the indices (C2 / C4: Q lives
+  // on the 1e4 features of 2e5 / 1e6 variables), iterate on those only —
+  // 1e4-entry vectors instead of 1e6 (C4: 7.5 -> ~2 ms); the sums skip only
+  // exact zeros, their grouping changes (fast mode: rounding only)
+  if (!strict) {
+    DevBuf<uint8_t> flag(n);
+    flag.zero(st);
+    touched_kernel<<<grid1(n), 256, 0, st>>>(Q.rp.get(), Q.ci.get(), n, flag.get());
+    RB_LAUNCH_CHECK();
+    DevBuf<int32_t> act(n), cnt(1);
+    const thrust::counting_iterator<int32_t> idx(0);
+    std::size_t tb = 0;
+    RB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, idx, flag.get(), act.get(), cnt.get(), n, st));
+    DevBuf<unsigned char> tmp(tb);
+    RB_CUDA(cub::DeviceSelect::Flagged(tmp.get(), tb, idx, flag.get(), act.get(), cnt.get(), n, st));
+    int32_t nc = 0;
+    RB_CUDA(cudaMemcpyAsync(&nc, cnt.get(), sizeof(nc), cudaMemcpyDeviceToHost, st));
+    RB_CUDA(cudaStreamSynchronize(st));
+    if (nc > 0 && 2 * static_cast<int64_t>(nc) <= n) {
+      DevCsr C;
+      C.rows = C.cols = nc;
+      C.nnz = Q.nnz;
+      C.rp.alloc(static_cast<std::size_t>(nc) + 1), C.ci.alloc(Q.nnz), C.v.alloc(Q.nnz);
+      DevBuf<int32_t> newidx(n), len(nc);
+      newidx_kernel<<<grid1(nc), 256, 0, st>>>(act.get(), nc, newidx.get());
+      act_lengths_kernel<<<grid1(nc), 256, 0, st>>>(act.get(), nc, Q.rp.get(), len.get());
+      RB_LAUNCH_CHECK();
+      RB_CUDA(cudaMemsetAsync(C.rp.get(), 0, sizeof(int32_t), st));
+      std::size_t sb = 0;
+      RB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, sb, len.get(), C.rp.get() + 1, nc, st));
+      DevBuf<unsigned char> stmp(sb);
+      RB_CUDA(cub::DeviceScan::InclusiveSum(stmp.get(), sb, len.get(), C.rp.get() + 1, nc, st));
+      compact_csr_kernel<<<grid1(nc), 256, 0, st>>>(act.get(), nc, Q.rp.get(), Q.ci.get(), qv, newidx.get(),
+                                                     C.rp.get(), C.ci.get(), C.v.get());
+      RB_LAUNCH_CHECK();
+      Schedule sc;
+      build_schedule(sc, len.get(), nc, false, st);
+      DevBuf<double> v(nc), w(nc);
+      PowerRun r(*this, v, w, nc,
+                 [&](StepGate g, cudaStream_t s) { spmv(C, sc, C.v.get(), v.get(), w.get(), g, s); }, true,
+                 max_iters, tol, seed, st, red, act.get(), n, pre);
+      run_alone(r);
+      return r.result();
+    }
+  }
   DevBuf<double> v(n), w(n);
   PowerRun r(*this, v, w, n,
              [&](StepGate g, cudaStream_t s) { spmv(Q, sch_q, qv, v.get(), w.get(), g, s); }, true, max_iters,
-             tol, seed, st, red);
+             tol, seed, st, red, nullptr, 0, pre);
   run_alone(r);
   return r.result();
 }
@@ -513,7 +656,7 @@ double DeviceQP::op_norm_q(const double* qv, int max_iters, double tol, uint64_t
 // estimate_op_norm (opnorm.hpp:36-61): power iteration on A'A; A' v as the
 // gather over CSR(A').
 double DeviceQP::op_norm_a(const double* av, const double* atv, int max_iters, double tol,
-                           uint64_t seed) {
+                           uint64_t seed, const RandomStart* pre) {
   if (A.nnz == 0) return 0.0;
   DevBuf<double> v(n), w(n), mv(m);
   PowerRun r(
@@ -522,7 +665,7 @@ double DeviceQP::op_norm_a(const double* av, const double* atv, int max_iters, d
         spmv(A, sch_dual, av, v.get(), mv.get(), g, s);
         spmv(AT, sch_at, atv, mv.get(), w.get(), g, s);
       },
-      false, max_iters, tol, seed, st, red);
+      false, max_iters, tol, seed, st, red, nullptr, 0, pre);
   run_alone(r);
   return std::sqrt(std::max(r.result(), 0.0));
 }
@@ -547,6 +690,7 @@ Engine::Engine(const rapdhg_qp& p, const rapdhg_config& cfg, Clock::time_point t
   }
   tr.st = st_;
   tr.mark("device + stream");
+  rand_future_ = std::async(std::launch::async, draw_random_start, p.n, cfg.seed);  // beside the upload
   P_ = std::make_unique<DeviceQP>(p, cfg.strict_parity != 0, st_, true);
   tr.mark("upload, stack, A', schedules");
   P_->validate_symmetry();  // original.validate() (solver.hpp:277)
@@ -585,9 +729,11 @@ Engine::Engine(const rapdhg_qp& p, const rapdhg_config& cfg, Clock::time_point t
   // norms (solver.hpp:286-289)
   // (norm Q's batches on a side stream beside norm A's measured no faster on
   // C4: 97.6 against 7.5 + 90.3 ms — both runs are device-bound)
-  norm_q = 1.01 * P_->op_norm_q(qsv_, 5000, 1e-4, cfg.seed);
+  P_->graphs = cfg.use_graphs != 0;
+  const RandomStart start = rand_future_.get();
+  norm_q = 1.01 * P_->op_norm_q(qsv_, 5000, 1e-4, cfg.seed, &start);
   tr.mark("norm Q (power iteration)");
-  norm_a = 1.01 * norm_a_power(5000, 1e-4, cfg.seed);
+  norm_a = 1.01 * norm_a_power(5000, 1e-4, cfg.seed, &start);
   tr.mark("norm A (power iteration)");
   // primal weight init on the scaled c, b (solver.hpp:296-300)
   if (cfg.primal_weight == RAPDHG_PW_ADAPTIVE) {
@@ -719,11 +865,11 @@ void Engine::setup_colblocks() {
 // fixed (RAPDHG_NORM_SLAB_STEP, default 72; -1 = never), never timing-
 // dependent, so the estimate is deterministic; the sharded solver's setup
 // runs the same code on the same full matrices, so its norm is the same bits.
-double Engine::norm_a_power(int max_iters, double tol, uint64_t seed) {
+double Engine::norm_a_power(int max_iters, double tol, uint64_t seed, const RandomStart* pre) {
   DeviceQP& P = *P_;
   int K = 72;
   if (const char* e = std::getenv("RAPDHG_NORM_SLAB_STEP")) K = std::atoi(e);
-  if (P.strict || K < 0 || P.A.nnz == 0) return P.op_norm_a(asv_, atsv_, max_iters, tol, seed);
+  if (P.strict || K < 0 || P.A.nnz == 0) return P.op_norm_a(asv_, atsv_, max_iters, tol, seed, pre);
   DevBuf<double> v(n_), w(n_), mv(m_);
   bool slab = false;
   PowerRun r(
@@ -740,11 +886,12 @@ double Engine::norm_a_power(int max_iters, double tol, uint64_t seed) {
         else
           P.spmv(P.AT, P.sch_at, atsv_, mv.get(), w.get(), g, s);
       },
-      false, max_iters, tol, seed, P.st, P.red);
+      false, max_iters, tol, seed, P.st, P.red, nullptr, 0, pre);
   r.split_at(K, [&](int it) {
     if (slab || it < K) return;
     setup_slabs();  // joins the plan threads (waits if they are still running)
     slab = dual_ph_.active() || primal_ph_.active();
+    r.set_mode(slab ? 1 : 0);
   });
   run_alone(r);
   return std::sqrt(std::max(r.result(), 0.0));

@@ -56,6 +56,16 @@ void primal_terms_into(KktRaw& r, const double* g);
 void* result_block_alloc(std::size_t bytes);
 bool result_block_free(void* p);
 
+// The power iterations' random start (opnorm.hpp:20-30): `len` draws of
+// mt19937_64(seed), and the generator after them (for the zero-norm restarts).
+// Norm Q and norm A both start from mt19937_64(cfg.seed) over n entries, so
+// one draw, made on a host thread while the matrices upload, serves both.
+struct RandomStart {
+  std::vector<double> v;
+  std::mt19937_64 rng;
+};
+RandomStart draw_random_start(int len, uint64_t seed);
+
 class DeviceQP {
  public:
   // check_structure: run the per-row CSR checks of validate_dims on the
@@ -77,8 +87,11 @@ class DeviceQP {
                     DevBuf<double>& cs, DevBuf<double>& bs);
   // estimate_op_norm_symmetric / estimate_op_norm (opnorm.hpp:36-87) on the
   // given values (patterns of Q / A / A').
-  double op_norm_q(const double* qv, int max_iters, double tol, uint64_t seed);
-  double op_norm_a(const double* av, const double* atv, int max_iters, double tol, uint64_t seed);
+  // pre: the draws of mt19937_64(seed) over n entries (draw_random_start), or
+  // null to draw them here
+  double op_norm_q(const double* qv, int max_iters, double tol, uint64_t seed, const RandomStart* pre = nullptr);
+  double op_norm_a(const double* av, const double* atv, int max_iters, double tol, uint64_t seed,
+                   const RandomStart* pre = nullptr);
 
   // Deterministic reduction to host (strict: sequential).
   template <int NS, int NM, class F>
@@ -90,6 +103,7 @@ class DeviceQP {
 
   cudaStream_t st;
   bool strict;
+  bool graphs = true;  // power-iteration batches as CUDA graphs (SolverConfig.use_graphs)
   int n, mi, me, m;
   DevCsr Q, A, AT;  // original values; A = [A_ineq; A_eq]
   DevBuf<int32_t> at_perm;  // AT position -> A position
@@ -218,8 +232,9 @@ class Engine : public LoopBackend {
   void setup_slabs();  // idempotent (the norm estimate may run it first)
   void plan_slabs_async();
   bool slabs_ready_ = false;
-  double norm_a_power(int max_iters, double tol, uint64_t seed);
+  double norm_a_power(int max_iters, double tol, uint64_t seed, const RandomStart* pre);
   std::future<void> plan_future_, plan_future2_;
+  std::future<RandomStart> rand_future_;  // the power iterations' start, drawn during the upload
   SlabChoice dual_choice_, primal_choice_;
   SlabPhase dual_ph_, primal_ph_;
   // L2-sized column blocks (colblock.cuh) of the gather-bound ops without a slab plan

@@ -149,7 +149,8 @@ int rapdhg_shard_plan(const rapdhg_qp* qp, int32_t parts, int32_t* dual_bounds, 
     null_check(dual_bounds, "dual_bounds");
     null_check(primal_bounds, "primal_bounds");
     rb::DeviceQP::validate_dims(*qp);
-    const rb::ShardPlan plan = rb::make_shard_plan(*qp, parts);
+    // the plan the sharded solver uses (RAPDHG_REPLICATE_MIN_LEN included)
+    const rb::ShardPlan plan = rb::make_shard_plan(*qp, parts, rb::replicate_min_len_from_env());
     std::copy(plan.dual.begin(), plan.dual.end(), dual_bounds);
     std::copy(plan.primal.begin(), plan.primal.end(), primal_bounds);
   });

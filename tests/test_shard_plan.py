@@ -188,3 +188,26 @@ def test_host_structure_validation_messages():
         rb.shard_plan(with_a([0, 3, 2, 5], [0, 3, 5, 2, 4]), 2)
     with pytest.raises(rb.InvalidArgument, match="strictly increasing"):
         rb.shard_plan(with_a([0, 2, 4, 5], [3, 1, 2, 4, 9]), 2)
+
+
+def test_plan_with_replicated_dense_rows(monkeypatch):
+    """RAPDHG_REPLICATE_MIN_LEN: the replicated rows of [Q | A'] (the SVM's
+    feature rows) cost nothing in the primal balance, so the primal blocks
+    split the other rows evenly; dual entries in replicated columns count
+    twice."""
+    import paper_2311_07710_b200 as rb
+
+    p = rb.generate(rb.Gen.SVM, 0.01, 4)  # 100 feature rows of ~4000 entries, 10000 slack rows of 2
+    cc = np.bincount(p.a_ineq.col_idx, minlength=p.num_vars()) + np.diff(p.q.row_ptr)
+    rep = cc >= 100
+    assert rep.sum() == 100
+    parts = 4
+    _, pb0 = rb.shard_plan(p, parts)
+    monkeypatch.setenv("RAPDHG_REPLICATE_MIN_LEN", "100")
+    db, pb = rb.shard_plan(p, parts)
+    assert pb[0] == 0 and pb[-1] == p.num_vars() and np.all(np.diff(pb) >= 0) and np.all(pb[1:-1] % 2048 == 0)
+    assert not np.array_equal(pb, pb0)
+    # non-replicated primal work per block, within one reduction chunk of even
+    cost = np.where(rep, 0, cc) + 2
+    per = [cost[pb[k]:pb[k + 1]].sum() for k in range(parts)]
+    assert max(per) - min(per) <= 2 * 2048 * (cost.max() + 0)

@@ -253,6 +253,12 @@ typedef struct {
   int32_t pad;
   uint8_t nccl_id[128]; /* ncclUniqueId from rank 0 (emulate = 0, no host transport) */
   const rapdhg_host_transport* host; /* non-NULL (emulate = 0): use these collectives, not NCCL */
+  /* > 0: replicate the rows of [Q | A'] with at least this many entries
+   * (SURVEY 8(e) dense-coupling columns: every shard computes them from
+   * per-shard partial sums; deterministic for a given shard count, within
+   * rounding of rapdhg_solve but not bit-identical); 0: the
+   * RAPDHG_REPLICATE_MIN_LEN environment variable, else none; < 0: none */
+  int64_t replicate_min_len;
 } rapdhg_shard_opts;
 
 /* Exercises a host transport's callbacks without a GPU: allgather-v, an
@@ -267,8 +273,9 @@ int rapdhg_host_transport_check(const rapdhg_host_transport* t, int32_t parts, i
 int rapdhg_nccl_unique_id(uint8_t* out128);
 
 /* Same contract as rapdhg_solve; every rank returns the full result. The
- * result is bit-identical to rapdhg_solve in fast mode (strict mode is
- * rejected: its sequential reductions do not shard). */
+ * result is bit-identical to rapdhg_solve in fast mode unless rows are
+ * replicated (opts.replicate_min_len); strict mode is rejected: its
+ * sequential reductions do not shard. */
 int rapdhg_solve_sharded(const rapdhg_qp* qp, const rapdhg_config* cfg,
                          const rapdhg_shard_opts* opts, rapdhg_result* out);
 

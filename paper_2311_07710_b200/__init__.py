@@ -670,9 +670,10 @@ class ProcessGroupTransport:
         _check(_load().rapdhg_host_transport_check(C.byref(self.struct), self.world, self.rank, int(length)))
 
 
-def _shard_opts(parts, emulate, rank, nccl_id, transport=None) -> abi.ShardOpts:
+def _shard_opts(parts, emulate, rank, nccl_id, transport=None, replicate_min_len=0) -> abi.ShardOpts:
     opts = abi.ShardOpts()
     opts.parts, opts.rank, opts.emulate = int(parts), int(rank), int(bool(emulate))
+    opts.replicate_min_len = int(replicate_min_len or 0)
     if nccl_id is not None:
         C.memmove(opts.nccl_id, nccl_id, 128)
     if transport is not None:
@@ -687,12 +688,12 @@ class ShardSession:
 
     def __init__(self, original: QuadraticProgram, cfg: Optional[SolverConfig] = None, parts: int = 2,
                  emulate: bool = True, rank: int = 0, nccl_id: Optional[bytes] = None,
-                 transport: Optional[ProcessGroupTransport] = None):
+                 transport: Optional[ProcessGroupTransport] = None, replicate_min_len: int = 0):
         self.cfg = cfg or SolverConfig()
         self._transport = transport  # its callbacks must outlive the session
         h = C.c_void_p()
         qp, cs = original._struct(), self.cfg._struct()
-        opts = _shard_opts(parts, emulate, rank, nccl_id, transport)
+        opts = _shard_opts(parts, emulate, rank, nccl_id, transport, replicate_min_len)
         _check(_load().rapdhg_shard_session_create(C.byref(qp), C.byref(cs), C.byref(opts), C.byref(h)))
         self._h = h
 
@@ -716,15 +717,18 @@ class ShardSession:
 
 def solve_sharded(original: QuadraticProgram, cfg: Optional[SolverConfig] = None, parts: int = 2,
                   emulate: bool = True, rank: int = 0, nccl_id: Optional[bytes] = None,
-                  transport: Optional[ProcessGroupTransport] = None) -> SolveResult:
+                  transport: Optional[ProcessGroupTransport] = None, replicate_min_len: int = 0) -> SolveResult:
     """Row-sharded solve. emulate=True runs all `parts` shards in
     this process on cfg.device (exchanges as device copies); emulate=False is
     one process per GPU, shard `rank`, NCCL communicator from `nccl_id`
     (nccl_unique_id() on rank 0, broadcast by the caller), or the host-staged
     collectives of `transport` (a ProcessGroupTransport: parts and rank come
-    from its group). Bit-identical to solve() in fast mode."""
+    from its group). Bit-identical to solve() in fast mode. replicate_min_len
+    > 0: rows of [Q | A'] with at least that many entries are replicated
+    (rapdhg_shard_opts.replicate_min_len; within rounding of solve(), not
+    bit-identical); 0: RAPDHG_REPLICATE_MIN_LEN, else none; < 0: none."""
     cfg = cfg or SolverConfig()
-    opts = _shard_opts(parts, emulate, rank, nccl_id, transport)
+    opts = _shard_opts(parts, emulate, rank, nccl_id, transport, replicate_min_len)
     qp, cs, out = original._struct(), cfg._struct(), abi.Result()
     L = _load()
     _check(L.rapdhg_solve_sharded(C.byref(qp), C.byref(cs), C.byref(opts), C.byref(out)))

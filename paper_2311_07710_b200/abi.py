@@ -113,7 +113,8 @@ class HostTransport(C.Structure):
 
 class ShardOpts(C.Structure):
     _fields_ = [("parts", i32), ("rank", i32), ("emulate", i32), ("pad", i32),
-                ("nccl_id", C.c_uint8 * 128), ("host", C.POINTER(HostTransport))]
+                ("nccl_id", C.c_uint8 * 128), ("host", C.POINTER(HostTransport)),
+                ("replicate_min_len", C.c_int64)]
 
 
 def declare(lib, name, restype, *argtypes):

@@ -191,7 +191,8 @@ std::unique_ptr<rb::ShardedEngine> make_sharded(const rapdhg_qp* qp, const rapdh
                     : rb::make_nccl_transport(opts->parts, opts->rank, opts->nccl_id);
     rank = opts->rank;
   }
-  return std::make_unique<rb::ShardedEngine>(*qp, *cfg, opts->parts, rank, std::move(tr), t0);
+  return std::make_unique<rb::ShardedEngine>(*qp, *cfg, opts->parts, rank, std::move(tr), t0,
+                                             opts->replicate_min_len);
 }
 }  // namespace
 

@@ -561,7 +561,7 @@ struct ShardedEngine::Shard {
 };
 
 ShardedEngine::ShardedEngine(const rapdhg_qp& p, const rapdhg_config& cfg, int parts, int rank,
-                             std::unique_ptr<Transport> tr, Clock::time_point t0)
+                             std::unique_ptr<Transport> tr, Clock::time_point t0, int64_t replicate_min_len)
     : cfg_(cfg), parts_(parts), tr_(std::move(tr)) {
   if (cfg.strict_parity) invalid("sharded solve: strict_parity needs sequential reductions; use one GPU");
   if (parts < 1) invalid("sharded solve: parts must be >= 1");
@@ -569,7 +569,9 @@ ShardedEngine::ShardedEngine(const rapdhg_qp& p, const rapdhg_config& cfg, int p
   // slab phases / column blocks over all rows are not built (each shard
   // builds its own over its rows below)
   full_ = std::make_unique<Engine>(p, cfg, t0, /*full_plans=*/false);
-  plan_ = make_shard_plan(p, parts, replicate_min_len_from_env());
+  plan_ = make_shard_plan(p, parts,
+                          replicate_min_len > 0 ? replicate_min_len
+                                                : (replicate_min_len == 0 ? replicate_min_len_from_env() : 0));
   st_ = full_->st_;
   AllocStreamScope scope(st_);
   DeviceQP& P = *full_->P_;
@@ -706,8 +708,7 @@ void ShardedEngine::build_replicated() {
     RB_CUDA(cudaStreamSynchronize(st_));
   }
   if (std::getenv("RAPDHG_TRACE"))
-    std::fprintf(stderr, "[shard] %d replicated primal rows (RAPDHG_REPLICATE_MIN_LEN=%lld)\n", nrep_,
-                 static_cast<long long>(replicate_min_len_from_env()));
+    std::fprintf(stderr, "[shard] %d replicated primal rows\n", nrep_);
 }
 
 // The replicated rows' part of primal step `it` (after the dual step, before

@@ -83,8 +83,9 @@ void host_transport_check(const rapdhg_host_transport& t, int parts, int rank, i
 class ShardedEngine : public LoopBackend {
  public:
   // rank < 0: emulate all `parts` shards in this process; else own shard `rank`.
+  // replicate_min_len: see rapdhg_shard_opts (0: RAPDHG_REPLICATE_MIN_LEN)
   ShardedEngine(const rapdhg_qp& p, const rapdhg_config& cfg, int parts, int rank,
-                std::unique_ptr<Transport> tr, Clock::time_point t0);
+                std::unique_ptr<Transport> tr, Clock::time_point t0, int64_t replicate_min_len = 0);
   ~ShardedEngine() override;
   void solve(rapdhg_result* out, Clock::time_point t0);
 

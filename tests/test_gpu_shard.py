@@ -147,8 +147,10 @@ def test_replicated_dense_rows_svm(parts, halo, monkeypatch):
     a = rb.solve_sharded(p, cfg, parts)
     assert_results_identical(a, rb.solve_sharded(p, cfg, parts))  # deterministic
     _close_trajectories(a, one)
-    monkeypatch.setenv("RAPDHG_REPLICATE_MIN_LEN", "0")
-    assert_results_identical(rb.solve_sharded(p, cfg, parts), one)  # off: bit-identical again
+    # the option overrides the environment: -1 off (bit-identical again), > 0 on
+    assert_results_identical(rb.solve_sharded(p, cfg, parts, replicate_min_len=-1), one)
+    monkeypatch.delenv("RAPDHG_REPLICATE_MIN_LEN")
+    assert_results_identical(rb.solve_sharded(p, cfg, parts, replicate_min_len=100), a)
 
 
 def test_replicated_rows_other_patterns(monkeypatch):

@@ -1,0 +1,31 @@
+"""bench.py's reference arm on the CPU host: the contract's JSON line (one
+line, BASELINE.json's metric, `impl: reference`, a `cpu_baseline` of kind
+"reference", the e2e object with zero copies), on a small C4 instance so it
+runs in seconds. The GPU arm is exercised by the driver on a B200."""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_reference_arm_json_line():
+    out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--workload", "svm", "--scale", "0.005",
+                          "--max-iters", "400", "--steps", "3", "--warmup", "3"], cwd=ROOT, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip()]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    base = json.load(open(os.path.join(ROOT, "BASELINE.json")))
+    assert d["impl"] == "reference"
+    assert d["metric"] == base["metric"]
+    assert d["unit"] == "iter/s" and d["higher_is_better"] is True and d["value"] > 0
+    assert d["steps"] == 3 and d["warmup"] == 3 and d["n_gpus"] == 1
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "reference" and cb["cores"] == 1 and cb["value"] == d["value"] and cb["sample"]
+    assert cb["nproc"] >= 1 and cb["compiler_flags"]
+    assert d["e2e"] == {"value": d["value"], "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    assert "C4" in d["config"]["workload"]
+    assert "no repository .so" in d["generator"]

@@ -431,3 +431,37 @@ def test_solves_capture_beside_legacy_stream_work():
         assert len(o) == 6
         for r in o:
             assert_results_identical(r, want)
+
+
+def _partial_q_qp(seed, n=400, frac=0.3, explicit_zero=False):
+    """A QP whose Q lives on a fraction of the variables (like C2's / C4's
+    features), so the norm estimate of Q runs on the compacted index set;
+    explicit_zero adds a stored 0 outside that set (pattern-asymmetric)."""
+    p = random_qp(seed, n=n, mi=150, me=20, dens=0.05)
+    g = np.random.default_rng(seed + 7)
+    k = int(frac * n)
+    idx = np.sort(g.choice(n, k, replace=False))
+    M = g.standard_normal((k // 2, k)) * (g.random((k // 2, k)) < 0.2)
+    Qk = M.T @ M + 1e-2 * np.eye(k)
+    Q = np.zeros((n, n))
+    Q[np.ix_(idx, idx)] = 0.5 * (Qk + Qk.T)
+    rows, cols = np.nonzero(Q)
+    rows, cols, vv = list(rows), list(cols), list(Q[rows, cols])
+    if explicit_zero:  # a stored zero in a row the rest of Q never touches
+        out = np.setdiff1d(np.arange(n), idx)
+        rows.append(int(out[0])), cols.append(int(idx[0])), vv.append(0.0)
+    order = np.lexsort((np.array(cols), np.array(rows)))  # CSR by hand: from_coo drops stored zeros
+    rows, cols, vv = np.array(rows)[order], np.array(cols)[order], np.array(vv)[order]
+    rp = np.concatenate([[0], np.cumsum(np.bincount(rows, minlength=n))])
+    q = rb.SparseMatrix.from_csr(n, n, rp, cols, vv)
+    return rb.QuadraticProgram(q, p.c, p.a_ineq, p.b_ineq, p.a_eq, p.b_eq)
+
+
+@pytest.mark.parametrize("seed,explicit_zero", [(1, False), (2, True), (3, False)])
+def test_compacted_norm_q_matches_reference(O, seed, explicit_zero):
+    """Fast mode's norm of Q on the compacted index set (Q touches < half of
+    the variables): the reference's estimate within 1e-9, same trajectory."""
+    p = _partial_q_qp(seed, explicit_zero=explicit_zero)
+    a, b, agree = _fast_vs_ref(O, p, dict(tol=1e-12), 400)
+    assert a.norm_q == pytest.approx(b.norm_q, rel=1e-9) and a.norm_a == pytest.approx(b.norm_a, rel=1e-9)
+    assert agree >= 3

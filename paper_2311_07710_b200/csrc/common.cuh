@@ -307,6 +307,30 @@ struct Tracer {
   }
 };
 
+// Captures body() on stream s (thread-local mode) into an executable graph.
+// A failure inside ends and drops the capture, so the stream stays usable,
+// then rethrows; the graph is destroyed once instantiated (or not).
+template <class F>
+cudaGraphExec_t capture_graph(cudaStream_t s, F&& body) {
+  RB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  try {
+    body();
+  } catch (...) {
+    cudaGraph_t broken = nullptr;
+    cudaStreamEndCapture(s, &broken);
+    if (broken) cudaGraphDestroy(broken);
+    cudaGetLastError();
+    throw;
+  }
+  cudaGraph_t g = nullptr;
+  RB_CUDA(cudaStreamEndCapture(s, &g));
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t e = cudaGraphInstantiate(&exec, g, 0);
+  cudaGraphDestroy(g);
+  RB_CUDA(e);
+  return exec;
+}
+
 // Step gate (power iterations run in device batches, engine.cu): a launch
 // tagged with step i does nothing once the device recorded a stop at a step
 // before i (*stop < i). The stop is written by step j's own last kernel, so no

@@ -469,14 +469,7 @@ class PowerRun {
       auto g = graphs_.find(key);
       if (g == graphs_.end()) {
         const int64_t l0 = P_.launches;
-        cudaGraph_t graph;
-        RB_CUDA(cudaStreamBeginCapture(s_, cudaStreamCaptureModeThreadLocal));
-        enqueue_steps();
-        RB_CUDA(cudaStreamEndCapture(s_, &graph));
-        cudaGraphExec_t exec;
-        const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
-        cudaGraphDestroy(graph);
-        RB_CUDA(e);
+        const cudaGraphExec_t exec = capture_graph(s_, [&] { enqueue_steps(); });
         g = graphs_.emplace(key, std::make_pair(exec, P_.launches - l0)).first;
         P_.launches = l0;
       }
@@ -1074,16 +1067,10 @@ void Engine::run_chunk(int len) {
     const int key = (len << 2) | (cur_ << 1) | (prof ? 1 : 0);
     auto it = graphs_.find(key);
     if (it == graphs_.end()) {
-      cudaGraph_t g;
       const int64_t before = launches_;
-      RB_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
-      launch_chunk_body(len, cur_, prof);
-      RB_CUDA(cudaStreamEndCapture(st_, &g));
+      const cudaGraphExec_t ge = capture_graph(st_, [&] { launch_chunk_body(len, cur_, prof); });
       graph_launches_[key] = launches_ - before;  // kernel nodes of this graph
       launches_ = before;  // counted at replay below
-      cudaGraphExec_t ge;
-      RB_CUDA(cudaGraphInstantiate(&ge, g, 0));
-      cudaGraphDestroy(g);
       it = graphs_.emplace(key, ge).first;
     }
     RB_CUDA(cudaGraphLaunch(it->second, st_));

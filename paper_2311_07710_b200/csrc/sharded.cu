@@ -1109,16 +1109,10 @@ void ShardedEngine::run_chunk(int len) {
     const int key = (len << 1) | cur_;
     auto it = graphs_.find(key);
     if (it == graphs_.end()) {
-      cudaGraph_t g;
       const int64_t before = launches_;
-      RB_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
-      body(len, cur_);
-      RB_CUDA(cudaStreamEndCapture(st_, &g));
+      const cudaGraphExec_t ge = capture_graph(st_, [&] { body(len, cur_); });
       const int64_t per_replay = launches_ - before;
       launches_ = before;
-      cudaGraphExec_t ge;
-      RB_CUDA(cudaGraphInstantiate(&ge, g, 0));
-      cudaGraphDestroy(g);
       it = graphs_.emplace(key, ge).first;
       replay_launches_[key] = per_replay;
     }

@@ -88,15 +88,6 @@ __global__ void factor_kernel(double* f, const double* meas, double* d, int64_t 
   d[i] *= fi;
 }
 
-// v *= f[row_off + row] * f[col_off + col] for every stored entry
-// (apply_pass, scaling.hpp:70). Product of factors first, as the reference.
-__global__ void apply_pass_kernel(double* v, const int32_t* row_of, const int32_t* ci,
-                                  const double* f, int row_off, int col_off, int64_t nnz) {
-  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (k >= nnz) return;
-  v[k] *= f[row_off + row_of[k]] * f[col_off + ci[k]];
-}
-
 // out = (d[row_off + row] * v) * d[col_off + col] (SparseMatrix::scaled,
 // sparse.hpp:154: r[row] * values_[k] * c[cols_[k]]).
 __global__ void scaled_values_kernel(double* out, const double* v, const int32_t* row_of,
@@ -322,6 +313,20 @@ void measures_mode(DeviceQP& P, const double* qv, const double* av, const double
   if (P.strict) measures<true, Kind>(P, qv, av, atv, meas);
   else measures<false, Kind>(P, qv, av, atv, meas);
 }
+// apply the factors f to the working values, then measure (ApplyMeasureOp)
+template <bool Strict, int Kind>
+void apply_measures(DeviceQP& P, double* qw, double* aw, double* atw, const double* f, double* meas) {
+  ApplyMeasureOp<Strict, Kind> prim{P.Q.view(qw), P.AT.view(atw), qw, atw, f, 0, 0, 0, P.n, meas};
+  rowwise(prim, P.sch_primal, P.st, &P.launches);
+  ApplyMeasureOp<Strict, Kind> dual{P.A.view(aw), CsrView{nullptr, nullptr, nullptr}, aw, nullptr, f, P.n, 0, 0, 0,
+                                    meas + P.n};
+  rowwise(dual, P.sch_dual, P.st, &P.launches);
+}
+template <int Kind>
+void apply_measures_mode(DeviceQP& P, double* qw, double* aw, double* atw, const double* f, double* meas) {
+  if (P.strict) apply_measures<true, Kind>(P, qw, aw, atw, f, meas);
+  else apply_measures<false, Kind>(P, qw, aw, atw, f, meas);
+}
 }  // namespace
 
 // compute_scaling (scaling.hpp:97-106): working copies of the values of Q, A
@@ -337,25 +342,24 @@ void DeviceQP::compute_scaling(int ruiz_iters, bool full, DevBuf<double>& d) {
   if (Q.nnz) RB_CUDA(cudaMemcpyAsync(qw.get(), Q.v.get(), sizeof(double) * Q.nnz, cudaMemcpyDeviceToDevice, st));
   if (A.nnz) RB_CUDA(cudaMemcpyAsync(aw.get(), A.v.get(), sizeof(double) * A.nnz, cudaMemcpyDeviceToDevice, st));
   if (AT.nnz) RB_CUDA(cudaMemcpyAsync(atw.get(), AT.v.get(), sizeof(double) * AT.nnz, cudaMemcpyDeviceToDevice, st));
-  DevBuf<int32_t> q_row, a_row, at_row;
-  expand_rows(q_row, Q, st);
-  expand_rows(a_row, A, st);
-  expand_rows(at_row, AT, st);
-  auto pass = [&](int kind) {
-    if (kind == 0) measures_mode<0>(*this, qw.get(), aw.get(), atw.get(), meas.get());
-    else if (kind == 1) measures_mode<1>(*this, qw.get(), aw.get(), atw.get(), meas.get());
-    else measures_mode<2>(*this, qw.get(), aw.get(), atw.get(), meas.get());
+  // pass p: measure (kind of pass p) -> factors -> apply them. The apply of
+  // pass p and the measure of pass p + 1 run as one sweep (ApplyMeasureOp);
+  // the last pass's apply is not needed (the working copies are dropped).
+  std::vector<int> kinds(static_cast<std::size_t>(std::max(ruiz_iters, 0)), 0);
+  if (full) kinds.push_back(1), kinds.push_back(2);
+  for (std::size_t p = 0; p < kinds.size(); ++p) {
+    if (p == 0) {
+      if (kinds[0] == 0) measures_mode<0>(*this, qw.get(), aw.get(), atw.get(), meas.get());
+      else if (kinds[0] == 1) measures_mode<1>(*this, qw.get(), aw.get(), atw.get(), meas.get());
+      else measures_mode<2>(*this, qw.get(), aw.get(), atw.get(), meas.get());
+    } else {  // apply pass p - 1's factors, measure for pass p
+      if (kinds[p] == 0) apply_measures_mode<0>(*this, qw.get(), aw.get(), atw.get(), f.get(), meas.get());
+      else if (kinds[p] == 1) apply_measures_mode<1>(*this, qw.get(), aw.get(), atw.get(), f.get(), meas.get());
+      else apply_measures_mode<2>(*this, qw.get(), aw.get(), atw.get(), f.get(), meas.get());
+    }
     factor_kernel<<<grid1(N), 256, 0, st>>>(f.get(), meas.get(), d.get(), N);
-    if (Q.nnz) apply_pass_kernel<<<grid1(Q.nnz), 256, 0, st>>>(qw.get(), q_row.get(), Q.ci.get(), f.get(), 0, 0, Q.nnz);
-    if (A.nnz) apply_pass_kernel<<<grid1(A.nnz), 256, 0, st>>>(aw.get(), a_row.get(), A.ci.get(), f.get(), n, 0, A.nnz);
-    if (AT.nnz) apply_pass_kernel<<<grid1(AT.nnz), 256, 0, st>>>(atw.get(), at_row.get(), AT.ci.get(), f.get(), 0, n, AT.nnz);
     RB_LAUNCH_CHECK();
-    launches += 4;
-  };
-  for (int it = 0; it < ruiz_iters; ++it) pass(0);
-  if (full) {
-    pass(1);
-    pass(2);
+    ++launches;
   }
   RB_CUDA(cudaStreamSynchronize(st));
 }

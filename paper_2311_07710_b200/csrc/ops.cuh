@@ -351,4 +351,56 @@ struct MeasureOp {
   }
 };
 
+// One scaling sweep that first applies the previous pass's factors to the
+// working values (apply_pass, scaling.hpp:70: v *= f_row * f_col, the
+// product of factors first) and then takes this pass's row measure of the
+// scaled values (MeasureOp): the same operations on every entry as an apply
+// sweep followed by a measure sweep, in one read and one write of the values.
+// Segment s (s1 = Q or A rows, s2 = A' rows): row factor f[ro_s + r], column
+// factor f[co_s + col].
+template <bool Strict, int Kind>
+struct ApplyMeasureOp {
+  static constexpr bool kStrict = Strict;
+  static constexpr int kWideUnroll = kUnroll;
+  static constexpr bool kStageWindows = false;
+  __device__ __forceinline__ const double* gather_src(int) const { return nullptr; }
+  using AccT = Acc<1, Kind == 0>;
+  CsrView s1, s2;  // s2.rp == nullptr: single segment
+  double* w1;      // working values of segment 1 / 2 (updated in place)
+  double* w2;
+  const double* f;
+  int ro1, co1, ro2, co2;
+  double* out;
+  __device__ __forceinline__ int len1(int r) const { return s1.rp[r + 1] - s1.rp[r]; }
+  __device__ __forceinline__ int len(int r) const {
+    return len1(r) + (s2.rp ? s2.rp[r + 1] - s2.rp[r] : 0);
+  }
+  template <int U>
+  __device__ __forceinline__ void accumulate(int r, int lo, int hi, int lane, int stride,
+                                             AccT& acc, const Gather*) const {
+    const int L1 = len1(r);
+    int p = lo + lane;
+    const int e1 = hi < L1 ? hi : L1;
+    const double fr1 = f[ro1 + r];
+    for (; p < e1; p += stride) {
+      const int64_t k = s1.rp[r] + p;
+      const double v = w1[k] * (fr1 * f[co1 + s1.ci[k]]);
+      w1[k] = v;
+      acc.v[0] = MeasureOp<Strict, Kind>::term(acc.v[0], v);
+    }
+    if (s2.rp) {
+      const double fr2 = f[ro2 + r];
+      for (; p < hi; p += stride) {
+        const int64_t k = static_cast<int64_t>(s2.rp[r]) - L1 + p;
+        const double v = w2[k] * (fr2 * f[co2 + s2.ci[k]]);
+        w2[k] = v;
+        acc.v[0] = MeasureOp<Strict, Kind>::term(acc.v[0], v);
+      }
+    }
+  }
+  __device__ __forceinline__ void finish(int r, const AccT& acc) const {
+    out[r] = Kind == 1 ? sqrt(acc.v[0]) : acc.v[0];
+  }
+};
+
 }  // namespace rb

@@ -64,13 +64,19 @@ struct Wins {
 // in-window entries of row r, per window (per: zeroed, stride apart; may be
 // null) and in total; *maxrun = the longest per-window run. Columns are
 // sorted, so a window's entries are one contiguous run.
+// cap > 0 (with maxrun): stop as soon as a run or the out-of-window entries
+// exceed cap — the row is then no W row whatever the rest holds (C3's
+// 1e6-entry budget row took one thread 0.2 s to scan).
 __device__ __forceinline__ int in_window_count(const int32_t* rp, const int32_t* ci, int r, const Wins& wins,
-                                               int* per, int64_t stride, int* maxrun = nullptr) {
+                                               int* per, int64_t stride, int* maxrun = nullptr, int cap = 0) {
   const int b = rp[r], e = rp[r + 1];
   int tot = 0, mx = 0, cur = -1, run = 0;
   for (int p = b; p < e; ++p) {
     const int w = wins.of(ci[p]);
-    if (w < 0) continue;
+    if (w < 0) {
+      if (cap > 0 && (p + 1 - b) - tot > cap) break;
+      continue;
+    }
     const int s = wins.run(w);
     if (s != cur) {
       if (cur >= 0 && per) per[cur * stride] = run;
@@ -78,6 +84,7 @@ __device__ __forceinline__ int in_window_count(const int32_t* rp, const int32_t*
     }
     ++run, ++tot;
     mx = max(mx, run);
+    if (cap > 0 && mx > cap) break;
   }
   if (cur >= 0 && per) per[cur * stride] = run;
   if (maxrun) *maxrun = mx;
@@ -92,9 +99,14 @@ __global__ void count_kernel(const int32_t* rp, const int32_t* ci, const int32_t
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= r1 - r0) return;
   const int r = r0 + static_cast<int>(i);
+  const int len = rp[r + 1] - rp[r], len_o = rp_o ? rp_o[r + 1] - rp_o[r] : 0;
+  if (len_o > cap) {  // the other segment alone exceeds the rest cap
+    cnt[i] = 0;
+    return;
+  }
   int mx = 0;
-  const int tot = in_window_count(rp, ci, r, wins, nullptr, 0, &mx);
-  const int rest = (rp[r + 1] - rp[r]) - tot + (rp_o ? rp_o[r + 1] - rp_o[r] : 0);
+  const int tot = in_window_count(rp, ci, r, wins, nullptr, 0, &mx, cap);
+  const int rest = len - tot + len_o;  // (an early stop leaves mx or rest above cap)
   cnt[i] = (mx <= cap && rest <= cap) ? tot : 0;
 }
 

@@ -19,6 +19,7 @@
 #include <stdexcept>
 
 #include "engine.hpp"
+#include "persistent.cuh"
 #include "rules.hpp"
 #include "terms.cuh"
 #include "elementwise.cuh"
@@ -775,6 +776,7 @@ Engine::Engine(const rapdhg_qp& p, const rapdhg_config& cfg, Clock::time_point t
     }
   }
   tr.mark("slab plans");
+  setup_chunk_kernel();
   setup_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
 }
 
@@ -892,6 +894,33 @@ double Engine::norm_a_power(int max_iters, double tol, uint64_t seed, const Rand
   });
   run_alone(r);
   return std::sqrt(std::max(r.result(), 0.0));
+}
+
+// Small problems run each chunk as one cooperative launch (persistent.cuh):
+// fast mode, both steps on the plain path (rowwise or sliced ELL; no slab or
+// column-block plans, no staged windows), no per-step profiling, and little
+// enough work per iteration that the per-step launches are the cost.
+// Opt-in (RAPDHG_PERSISTENT=1): measured slower than the replayed graph of
+// per-step kernels — C1 68k against 96k it/s, the two grid-wide barriers per
+// step costing more than the graph's launches.
+void Engine::setup_chunk_kernel() {
+  chunk_grid_ = 0;
+  const char* env = std::getenv("RAPDHG_PERSISTENT");
+  const std::string mode = env ? env : "0";
+  if (mode != "1" || P_->strict || !events_.empty()) return;
+  if (dual_ph_.active() || primal_ph_.active() || cbd_.active() || cbp_.active()) return;
+  const SchedView& sd = P_->sch_dual.view;
+  const SchedView& sp = P_->sch_primal.view;
+  if (sd.win[0].len + sd.win[1].len + sp.win[0].len + sp.win[1].len > 0) return;
+  const void* k = reinterpret_cast<const void*>(&chunk_kernel<DualStepOp<false>, PrimalStepOp<false>>);
+  int per_sm = 0;
+  RB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kBlock, 0));
+  if (per_sm < 1) return;
+  auto blocks_of = [](const SchedView& v, const SellPlan& sp) {
+    return sp.active() ? static_cast<int>(ceil_div(sp.view.nslices, kBlock / 32)) : v.total_blocks;
+  };
+  const int want = std::max(std::max(blocks_of(sd, sell_dual_plan_), blocks_of(sp, sell_primal_plan_)), 1);
+  chunk_grid_ = std::min(want, per_sm * kSMs);
 }
 
 // The pattern-only part of the slab plans (windows, tiles, layouts: mostly
@@ -1067,7 +1096,30 @@ void Engine::run_chunk(int len) {
   // kernel timing is sampled (every kProfilePeriod-th chunk) so the event
   // nodes barely perturb the timed loop
   const bool prof = !events_.empty() && (chunk_counter_++ % kProfilePeriod) == 0;
-  if (cfg_.use_graphs) {
+  if (chunk_grid_ > 0) {  // small problem: the chunk as one cooperative launch (persistent.cuh)
+    const DualStepOp<false> d{P_->A.view(asv_), w_.get(), bsv_, y_.get(), yb_.get(), mi_, params_.get(), 0, bad_.get()};
+    PrimalStepOp<false> pr[2];
+    for (int c = 0; c < 2; ++c)
+      pr[c] = PrimalStepOp<false>{P_->Q.view(qsv_), P_->AT.view(atsv_), XMD_[c].get(), y_.get(), X_[c].get(),
+                                  X_[c ^ 1].get(), xb_.get(), csv_, w_.get(), XMD_[c ^ 1].get(), params_.get(), 0,
+                                  bad_.get(), lsv_, hsv_};
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(static_cast<unsigned>(chunk_grid_));
+    lc.blockDim = dim3(kBlock);
+    lc.stream = st_;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    RB_CUDA(cudaLaunchKernelEx(&lc, chunk_kernel<DualStepOp<false>, PrimalStepOp<false>>, d, P_->sch_dual.view,
+                               sell_dual_plan_.view, pr[0], pr[1], P_->sch_primal.view, sell_primal_plan_.view,
+                               static_cast<const double*>(X_[cur_].get()),
+                               static_cast<const double*>(X_[cur_ ^ 1].get()), static_cast<const double*>(xb_.get()),
+                               w_.get(), XMD_[cur_].get(), static_cast<const IterParams*>(params_.get()), n_, len,
+                               cur_));
+    ++launches_;
+  } else if (cfg_.use_graphs) {
     const int key = (len << 2) | (cur_ << 1) | (prof ? 1 : 0);
     auto it = graphs_.find(key);
     if (it == graphs_.end()) {

@@ -230,6 +230,8 @@ class Engine : public LoopBackend {
   bool bad_fresh_ = false;  // bad_h_ was read back by the last evaluate()
   // slab-staged gathers (fast mode, slab.cuh): plans + the complement schedules
   void setup_slabs();  // idempotent (the norm estimate may run it first)
+  void setup_chunk_kernel();
+  int chunk_grid_ = 0;  // > 0: chunks run as one cooperative launch of that grid (persistent.cuh)
   void plan_slabs_async();
   bool slabs_ready_ = false;
   double norm_a_power(int max_iters, double tol, uint64_t seed, const RandomStart* pre);

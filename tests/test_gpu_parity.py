@@ -465,3 +465,25 @@ def test_compacted_norm_q_matches_reference(O, seed, explicit_zero):
     a, b, agree = _fast_vs_ref(O, p, dict(tol=1e-12), 400)
     assert a.norm_q == pytest.approx(b.norm_q, rel=1e-9) and a.norm_a == pytest.approx(b.norm_a, rel=1e-9)
     assert agree >= 3
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_persistent_chunks_bit_identical(seed, monkeypatch):
+    """Small problems run a chunk as one cooperative launch (persistent.cuh):
+    the same rowwise tiles as the per-step kernels, so the whole solve is the
+    graph-replayed one bit for bit, with one launch per chunk."""
+    p = random_qp(seed, n=600, mi=250, me=40, dens=0.05)
+    cfg = rb.SolverConfig(tol=1e-10, max_iters=3000, snapshot_interval=100, record_restart_points=True)
+    monkeypatch.setenv("RAPDHG_PERSISTENT", "0")
+    a = rb.solve(p, cfg)
+    monkeypatch.setenv("RAPDHG_PERSISTENT", "1")
+    b = rb.solve(p, cfg)
+    assert_results_identical(b, a)
+    assert b.kernel_launches < a.kernel_launches
+    with_box = rb.QuadraticProgram(p.q, p.c, p.a_ineq, p.b_ineq, p.a_eq, p.b_eq,
+                                   lower=-np.ones(p.num_vars()), upper=np.ones(p.num_vars()))
+    bc = rb.SolverConfig(tol=1e-9, max_iters=2000, box_projection=True)
+    monkeypatch.setenv("RAPDHG_PERSISTENT", "0")
+    c = rb.solve(with_box, bc)
+    monkeypatch.setenv("RAPDHG_PERSISTENT", "1")
+    assert_results_identical(rb.solve(with_box, bc), c)

@@ -1061,10 +1061,11 @@ void Engine::launch_chunk_body(int len, int cur, bool prof) {
       } else if (cbd_.active()) {
         launches_ += launch_colblocked_dual(d, cbd_, st_);
       } else if (sell_dual_plan_.active()) {
-        launch_sell(d, sell_dual_plan_, st_);
+        launch_sell(d, sell_dual_plan_, st_, plain_pdl_);
         ++launches_;
-      } else {
-        rowwise(d, P_->sch_dual, st_, &launches_);
+      } else if (P_->sch_dual.view.total_blocks > 0) {
+        launch_rowwise(d, P_->sch_dual.view, st_, plain_pdl_);
+        ++launches_;
       }
     }
     if (prof) RB_CUDA(cudaEventRecordWithFlags(events_[2 * it + 1], st_, cudaEventRecordExternal));
@@ -1081,10 +1082,11 @@ void Engine::launch_chunk_body(int len, int cur, bool prof) {
       } else if (cbp_.active()) {
         launches_ += launch_colblocked_primal(pr, cbp_, st_);
       } else if (sell_primal_plan_.active()) {
-        launch_sell(pr, sell_primal_plan_, st_);
+        launch_sell(pr, sell_primal_plan_, st_, plain_pdl_);
         ++launches_;
-      } else {
-        rowwise(pr, P_->sch_primal, st_, &launches_);
+      } else if (P_->sch_primal.view.total_blocks > 0) {
+        launch_rowwise(pr, P_->sch_primal.view, st_, plain_pdl_);
+        ++launches_;
       }
     }
     if (prof) RB_CUDA(cudaEventRecordWithFlags(events_[2 * it + 2], st_, cudaEventRecordExternal));

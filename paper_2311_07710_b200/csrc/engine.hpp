@@ -232,6 +232,9 @@ class Engine : public LoopBackend {
   void setup_slabs();  // idempotent (the norm estimate may run it first)
   void setup_chunk_kernel();
   int chunk_grid_ = 0;  // > 0: chunks run as one cooperative launch of that grid (persistent.cuh)
+  // the plain path's step kernels as programmatic dependent launches
+  // (RAPDHG_PDL, as the slab kernels)
+  bool plain_pdl_ = pdl_enabled();
   void plan_slabs_async();
   bool slabs_ready_ = false;
   double norm_a_power(int max_iters, double tol, uint64_t seed, const RandomStart* pre);

@@ -360,6 +360,11 @@ __device__ __forceinline__ void rowwise_tile(const Op& op, const SchedView& s, i
 template <class Op, bool Win>
 __global__ void __launch_bounds__(kBlock) rowwise_kernel(const Op op, const SchedView s) {
   extern __shared__ double win_smem[];
+  // programmatic dependent launch (launch_rowwise(.., pdl)): the previous
+  // kernel's writes are visible after the wait; the next kernel may be
+  // scheduled at once (its own wait holds it). Both are no-ops otherwise.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (HasGate<Op>::closed(op)) return;  // uniform over the grid
   Gather g[2];
   int off = 0;
@@ -382,10 +387,21 @@ __global__ void __launch_bounds__(kBlock) rowwise_kernel(const Op op, const Sche
 int resident_ctas(const void* kernel, int smem_bytes);
 
 template <class Op>
-inline void launch_rowwise(const Op& op, const SchedView& s, cudaStream_t st) {
+inline void launch_rowwise(const Op& op, const SchedView& s, cudaStream_t st, bool pdl = false) {
   if (s.total_blocks <= 0) return;
   const int wins = Op::kStageWindows ? s.win[0].len + s.win[1].len : 0;
-  if (wins == 0) {
+  if (wins == 0 && pdl) {  // as a programmatic dependent launch of the previous kernel
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(static_cast<unsigned>(s.total_blocks));
+    lc.blockDim = dim3(kBlock);
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    RB_CUDA(cudaLaunchKernelEx(&lc, rowwise_kernel<Op, false>, op, s));
+  } else if (wins == 0) {
     // one tile per CTA: the hardware scheduler balances heavy and light tiles
     rowwise_kernel<Op, false><<<s.total_blocks, kBlock, 0, st>>>(op, s);
   } else {

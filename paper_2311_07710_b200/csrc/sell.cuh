@@ -132,6 +132,8 @@ __device__ __forceinline__ void sell_slice(const Op& op, const SellView& sv, int
 
 template <class Op>
 __global__ void __launch_bounds__(kBlock) sell_kernel(const Op op, const SellView sv) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // see rowwise_kernel (no-ops without PDL)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (kBlock / 32);
   for (int64_t q = (blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x) >> 5; q < sv.nslices; q += nwarps)
@@ -139,11 +141,24 @@ __global__ void __launch_bounds__(kBlock) sell_kernel(const Op op, const SellVie
 }
 
 template <class Op>
-inline void launch_sell(const Op& op, const SellPlan& plan, cudaStream_t st) {
+inline void launch_sell(const Op& op, const SellPlan& plan, cudaStream_t st, bool pdl = false) {
   const int64_t warps_needed = plan.view.nslices;
   const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(warps_needed, kBlock / 32),
                                                                                        16 * kSMs)));
-  sell_kernel<Op><<<grid, kBlock, 0, st>>>(op, plan.view);
+  if (pdl) {  // programmatic dependent launch (see launch_rowwise)
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(kBlock);
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    RB_CUDA(cudaLaunchKernelEx(&lc, sell_kernel<Op>, op, plan.view));
+  } else {
+    sell_kernel<Op><<<grid, kBlock, 0, st>>>(op, plan.view);
+  }
   RB_LAUNCH_CHECK();
 }
 

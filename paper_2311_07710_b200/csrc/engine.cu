@@ -295,9 +295,11 @@ void DeviceQP::spmv(const DevCsr& mat, const Schedule& s, const double* vals, co
   if (strict) {
     SpmvOp<true> op{mat.view(vals), x, y, gate};
     rowwise(op, s, use, &launches);
-  } else {
+  } else if (s.view.total_blocks > 0) {
+    // the power iterations' products: programmatic dependent launches
     SpmvOp<false> op{mat.view(vals), x, y, gate};
-    rowwise(op, s, use, &launches);
+    launch_rowwise(op, s.view, use, gate.stop != nullptr && pdl_enabled());
+    ++launches;
   }
 }
 
@@ -404,6 +406,8 @@ struct PowerState {
 };
 __global__ void power_step_kernel(double* v, const double* w, const double* hist, PowerState* ps, int i,
                                   double tol, bool absval, int64_t n) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // (programmatic dependent launch)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (ps->stop < i) return;  // a stop recorded by an earlier step (uniform over the grid)
   const double s = hist[1];
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -524,13 +528,32 @@ class PowerRun {
 
  private:
   static constexpr int kMaxBatch = 64;
+  // each step's kernels as programmatic dependent launches of the previous
+  // ones (RAPDHG_PDL), so the next kernel is scheduled while one finishes
   void enqueue_steps() {
+    const bool pdl = pdl_enabled() && !P_.strict;
     for (int i = 0; i < K_; ++i) {
       const StepGate gate{&dps_.get()->stop, i};
       step_(gate, s_);
-      launch_reduce<2, 0>(DotAndSumSq{v_.get(), w_.get(), gate}, len_, P_.strict, red_, hist_.get() + 2 * i, s_);
-      power_step_kernel<<<sgrid_, 256, 0, s_>>>(v_.get(), w_.get(), hist_.get() + 2 * i, dps_.get(), i, tol_,
-                                                absval_, len_);
+      launch_reduce<2, 0>(DotAndSumSq{v_.get(), w_.get(), gate}, len_, P_.strict, red_, hist_.get() + 2 * i, s_,
+                          pdl);
+      if (pdl) {
+        cudaLaunchConfig_t lc{};
+        lc.gridDim = dim3(sgrid_);
+        lc.blockDim = dim3(256);
+        lc.stream = s_;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        RB_CUDA(cudaLaunchKernelEx(&lc, power_step_kernel, v_.get(), static_cast<const double*>(w_.get()),
+                                   static_cast<const double*>(hist_.get() + 2 * i), dps_.get(), i, tol_, absval_,
+                                   static_cast<int64_t>(len_)));
+      } else {
+        power_step_kernel<<<sgrid_, 256, 0, s_>>>(v_.get(), w_.get(), hist_.get() + 2 * i, dps_.get(), i, tol_,
+                                                  absval_, len_);
+      }
       RB_LAUNCH_CHECK();
       P_.launches += 2;
     }

@@ -74,6 +74,9 @@ __global__ void __launch_bounds__(kRedBlock) reduce_chunks_kernel(F f, int64_t n
                                                                    int64_t chunk0, unsigned* ticket,
                                                                    double* out) {
   constexpr int NT = NS + NM;
+  // programmatic dependent launch (launch_reduce(.., pdl)); no-ops otherwise
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (HasGate<F>::closed(f)) return;  // uniform over the grid: no ticket taken
   double s[NS > 0 ? NS : 1], mx[NM > 0 ? NM : 1];
 #pragma unroll
@@ -144,10 +147,23 @@ struct ReduceScratch {
 // Launch a reduction over [0, n) writing NS sums then NM maxima to d_out.
 template <int NS, int NM, class F>
 inline void launch_reduce(const F& f, int64_t n, bool strict, ReduceScratch& rs, double* d_out,
-                          cudaStream_t st) {
+                          cudaStream_t st, bool pdl = false) {
   static_assert(NS + NM <= kRedMaxOut, "too many reduction outputs");
   if (strict) {
     reduce_seq_kernel<NS, NM, F><<<1, 1, 0, st>>>(f, n, d_out);
+  } else if (pdl) {  // as a programmatic dependent launch of the previous kernel
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(static_cast<unsigned>(reduce_chunks(n)));
+    lc.blockDim = dim3(kRedBlock);
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    double* partials = rs.partials.get();
+    unsigned* ticket = rs.ticket.get();
+    RB_CUDA(cudaLaunchKernelEx(&lc, reduce_chunks_kernel<NS, NM, F, true>, f, n, partials, int64_t{0}, ticket, d_out));
   } else {
     reduce_chunks_kernel<NS, NM, F, true><<<static_cast<unsigned>(reduce_chunks(n)), kRedBlock, 0, st>>>(
         f, n, rs.partials.get(), 0, rs.ticket.get(), d_out);

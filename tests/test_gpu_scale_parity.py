@@ -181,3 +181,14 @@ def test_c4_device_instance_equals_reference_arm_instance(runs):
                       (p.a_ineq.row_ptr, d["a_ineq"][0]), (p.a_ineq.col_idx, d["a_ineq"][1]),
                       (p.a_ineq.values, d["a_ineq"][2]), (p.c, d["c"]), (p.b_ineq, d["b_ineq"])):
         assert got.shape == want.shape and np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("parts", [2, 8])
+def test_c4_sharded_replicated_rows_match_reference(runs, parts):
+    """The bench instance row-sharded with its 1e4 feature rows replicated
+    (rapdhg_shard_opts.replicate_min_len; emulated shards on one GPU): the
+    reference's trajectory within 1e-9, like the single-GPU fast mode."""
+    p = runs.problem("c4")
+    a = rb.solve_sharded(p, runs.cfg("c4"), parts, replicate_min_len=1000)
+    worst = assert_fixed_count_parity(a, runs.reference("c4"))
+    print(f"c4 sharded x{parts}, replicated feature rows: worst iterate rel diff {worst:.2e}")

@@ -60,6 +60,9 @@ def parse():
     ap.add_argument("--strict", action="store_true", help="bit-exact strict mode")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: independent solves per rank instead of one row-sharded instance")
+    ap.add_argument("--replicate-min-len", type=int, default=None,
+                    help="sharded runs: replicate the rows of [Q | A'] with at least this many entries "
+                         "(default: 1000 for svm — its feature rows — else none; -1 none)")
     ap.add_argument("--shard-emulate", type=int, default=0,
                     help="run this many shards in one process (single-GPU functional check)")
     a = ap.parse_args()
@@ -306,15 +309,19 @@ def run_sharded(args, p, desc, rank, world, local, dist, barrier, allmax):
 
     cfg = rb.SolverConfig(tol=args.tol, max_iters=args.max_iters, device=local)
 
+    rep = args.replicate_min_len
+    if rep is None:  # C4's 1e4 dense feature rows (SURVEY §8(e) dense-coupling columns)
+        rep = 1000 if args.workload == "svm" else -1
+
     def fresh_kw():  # an ncclUniqueId bootstraps exactly one communicator
         if args.shard_emulate:
-            return dict(parts=args.shard_emulate, emulate=True)
+            return dict(parts=args.shard_emulate, emulate=True, replicate_min_len=rep)
         uid = rb.nccl_unique_id() if rank == 0 else None
         if dist:
             obj = [uid]
             dist[1].broadcast_object_list(obj, src=0)
             uid = obj[0]
-        return dict(parts=world, emulate=False, rank=rank, nccl_id=uid)
+        return dict(parts=world, emulate=False, rank=rank, nccl_id=uid, replicate_min_len=rep)
 
     kw = fresh_kw()
     parts = kw["parts"]
@@ -350,8 +357,9 @@ def run_sharded(args, p, desc, rank, world, local, dist, barrier, allmax):
                 "n_gpus": world, "shards": parts, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {**desc, "parallelism": f"row-sharded over {parts} shards (NCCL)"
-                           if not args.shard_emulate else f"{parts} emulated shards on one GPU"},
+                "config": {**desc, "parallelism": (f"row-sharded over {parts} shards (NCCL)"
+                                                   if not args.shard_emulate else f"{parts} emulated shards on one GPU")
+                           + (f", rows of [Q | A'] with >= {rep} entries replicated" if rep > 0 else "")},
                 "iterations_per_step": its / args.steps, "status": rb.to_string(r.status),
                 "e2e": {"value": e2e_its / wall, "unit": "iter/s", "h2d_bytes_per_step": qp_bytes(p),
                         "d2h_bytes_per_step": 8 * (p.num_vars() + p.num_rows())},

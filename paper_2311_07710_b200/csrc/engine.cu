@@ -696,8 +696,8 @@ double DeviceQP::op_norm_a(const double* av, const double* atv, int max_iters, d
 // ============================================================================
 
 
-Engine::Engine(const rapdhg_qp& p, const rapdhg_config& cfg, Clock::time_point t0, bool full_plans)
-    : cfg_(cfg), full_plans_(full_plans) {
+Engine::Engine(const rapdhg_qp& p, const rapdhg_config& cfg, Clock::time_point t0, bool full_plans, bool own_norm_a)
+    : cfg_(cfg), full_plans_(full_plans), own_norm_a_(own_norm_a) {
   Tracer tr(nullptr);
   DeviceQP::validate_dims(p, false);  // the per-row scan runs on the device after the upload
   tr.mark("validate dims (host)");
@@ -754,7 +754,7 @@ Engine::Engine(const rapdhg_qp& p, const rapdhg_config& cfg, Clock::time_point t
   const RandomStart start = rand_future_.get();
   norm_q = 1.01 * P_->op_norm_q(qsv_, 5000, 1e-4, cfg.seed, &start);
   tr.mark("norm Q (power iteration)");
-  norm_a = 1.01 * norm_a_power(5000, 1e-4, cfg.seed, &start);
+  if (own_norm_a_) norm_a = 1.01 * norm_a_power(5000, 1e-4, cfg.seed, &start);
   tr.mark("norm A (power iteration)");
   // primal weight init on the scaled c, b (solver.hpp:296-300)
   if (cfg.primal_weight == RAPDHG_PW_ADAPTIVE) {
@@ -792,7 +792,7 @@ Engine::Engine(const rapdhg_qp& p, const rapdhg_config& cfg, Clock::time_point t
     setup_slabs();
     if (full_plans_) {
       setup_colblocks();
-    } else {  // built for the norm estimate only: the shards build their own
+    } else if (own_norm_a_) {  // built for the norm estimate only: the shards build their own
       RB_CUDA(cudaStreamSynchronize(st_));
       dual_ph_ = SlabPhase{};
       primal_ph_ = SlabPhase{};
@@ -970,15 +970,19 @@ void Engine::plan_slabs_async() {
       DevBuf<int32_t> len;
       if (dual) {
         dual_choice_ = choose_slabs(P.A.rp.get(), P.A.ci.get(), P.A.rows, P.A.nnz, n_, s2);
-        row_lengths(len, P.A.rp.get(), nullptr, m_, s2);
-        build_slab_phase(dual_ph_, dual_choice_, 0, P.A.rp.get(), P.A.ci.get(), nullptr, nullptr, 0, m_, len.get(),
-                         s2);
+        if (full_plans_ || own_norm_a_) {
+          row_lengths(len, P.A.rp.get(), nullptr, m_, s2);
+          build_slab_phase(dual_ph_, dual_choice_, 0, P.A.rp.get(), P.A.ci.get(), nullptr, nullptr, 0, m_, len.get(),
+                           s2);
+        }
         tr.mark("  slab plan: dual (async)");
       } else {
         primal_choice_ = choose_slabs(P.AT.rp.get(), P.AT.ci.get(), n_, P.AT.nnz, m_, s2);
-        row_lengths(len, P.Q.rp.get(), P.AT.rp.get(), n_, s2);
-        build_slab_phase(primal_ph_, primal_choice_, 1, P.Q.rp.get(), P.Q.ci.get(), P.AT.rp.get(), P.AT.ci.get(), 0,
-                         n_, len.get(), s2);
+        if (full_plans_ || own_norm_a_) {
+          row_lengths(len, P.Q.rp.get(), P.AT.rp.get(), n_, s2);
+          build_slab_phase(primal_ph_, primal_choice_, 1, P.Q.rp.get(), P.Q.ci.get(), P.AT.rp.get(), P.AT.ci.get(),
+                           0, n_, len.get(), s2);
+        }
         tr.mark("  slab plan: primal (async)");
       }
       RB_CUDA(cudaStreamSynchronize(s2));

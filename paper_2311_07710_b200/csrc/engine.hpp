@@ -164,7 +164,11 @@ class Engine : public LoopBackend {
   // full_plans = false (the sharded solver's setup): the slab phases over all
   // rows serve the norm estimate only (then dropped: the shards rebuild them
   // over their own rows) and no column blocks are built.
-  Engine(const rapdhg_qp& p, const rapdhg_config& cfg, Clock::time_point t0, bool full_plans = true);
+  // own_norm_a = false (the sharded solver with distributed norms): the norm of A
+  // is left to the caller (ShardedEngine::distributed_norm_a), and with
+  // full_plans = false no slab phases over all rows are built at all.
+  Engine(const rapdhg_qp& p, const rapdhg_config& cfg, Clock::time_point t0, bool full_plans = true,
+         bool own_norm_a = true);
   ~Engine() override;
   Engine(const Engine&) = delete;
   Engine& operator=(const Engine&) = delete;
@@ -247,6 +251,7 @@ class Engine : public LoopBackend {
   // column-block counts of the ops without an active slab phase
   void colblock_counts(bool dual_slab_active, bool primal_slab_active);
   bool full_plans_ = true;
+  bool own_norm_a_ = true;  // this object estimates norm A (else the sharded solver does)
   int cb_nb_dual_ = 1, cb_nq_ = 1, cb_na_ = 1;  // block counts (global: shards reuse them)
   // sliced-ELL (sell.cuh) for ops whose rows are all short — decided on the
   // whole matrices (shards reuse the decision); plans of the plain path

@@ -558,6 +558,10 @@ struct ShardedEngine::Shard {
   DevBuf<int32_t> rep_qlo, rep_qhi, rep_alo, rep_ahi;
   Schedule sch_rep, sch_primal_step;
   DevBuf<double> rep_part;
+  // the distributed norm estimate: the A' rows of the owned block, and the
+  // iteration's vectors (full length; freed after the setup)
+  Schedule sch_at;
+  DevBuf<double> nv, nw, nmv;
 };
 
 ShardedEngine::ShardedEngine(const rapdhg_qp& p, const rapdhg_config& cfg, int parts, int rank,
@@ -568,7 +572,11 @@ ShardedEngine::ShardedEngine(const rapdhg_qp& p, const rapdhg_config& cfg, int p
   // validation, scaling, norms and the slab window choices; the single-GPU
   // slab phases / column blocks over all rows are not built (each shard
   // builds its own over its rows below)
-  full_ = std::make_unique<Engine>(p, cfg, t0, /*full_plans=*/false);
+  {
+    const char* e = std::getenv("RAPDHG_SHARD_NORMS");
+    shard_norms_ = !(e && e[0] == '0');
+  }
+  full_ = std::make_unique<Engine>(p, cfg, t0, /*full_plans=*/false, /*norm_a=*/!shard_norms_);
   plan_ = make_shard_plan(p, parts,
                           replicate_min_len > 0 ? replicate_min_len
                                                 : (replicate_min_len == 0 ? replicate_min_len_from_env() : 0));
@@ -601,6 +609,7 @@ ShardedEngine::ShardedEngine(const rapdhg_qp& p, const rapdhg_config& cfg, int p
       if (sh->dual_ph.active()) {
         fill_slab_values(sh->dual_ph.plan, full_->asv_, nullptr, st_);
         fill_sell_values(sh->dual_ph.others_sell, full_->asv_, nullptr, st_);
+        prepare_slab<PhaseSpmvOp<1>>(sh->dual_ph.plan.view.smem_bytes());  // the distributed norm estimate
         assign_slab_ctas(sh->dual_ph.plan, prepare_slab<DualStepOp<false>>(sh->dual_ph.plan.view.smem_bytes()), st_);
       }
     }
@@ -612,6 +621,7 @@ ShardedEngine::ShardedEngine(const rapdhg_qp& p, const rapdhg_config& cfg, int p
       if (sh->primal_ph.active()) {
         fill_slab_values(sh->primal_ph.plan, full_->qsv_, full_->atsv_, st_);
         fill_sell_values(sh->primal_ph.others_sell, full_->qsv_, full_->atsv_, st_);
+        prepare_slab<PhaseSpmvOp<2>>(sh->primal_ph.plan.view.smem_bytes());
         assign_slab_ctas(sh->primal_ph.plan, prepare_slab<PrimalStepOp<false>>(sh->primal_ph.plan.view.smem_bytes()), st_);
       }
     }
@@ -673,6 +683,111 @@ ShardedEngine::ShardedEngine(const rapdhg_qp& p, const rapdhg_config& cfg, int p
   build_overlap(rank < 0);
   build_halos();
   RB_CUDA(cudaStreamSynchronize(st_));
+  if (shard_norms_) {
+    full_->norm_a = 1.01 * distributed_norm_a(5000, 1e-4, cfg.seed);  // solver.hpp:286-289
+    full_->setup_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
+  }
+}
+
+namespace {
+__global__ void scale_slice_kernel(double* v, const double* w, double s, int64_t lo, int64_t hi) {
+  const int64_t i = lo + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < hi) v[i] = w[i] * s;  // v = w; scale(v, 1/nrm) (opnorm.hpp:52-53)
+}
+}  // namespace
+
+double ShardedEngine::distributed_norm_a(int max_iters, double tol, uint64_t seed) {
+  DeviceQP& P = *full_->P_;
+  Engine& e = *full_;
+  const int n = P.n, m = P.m;
+  if (P.A.nnz == 0) return 0.0;
+  int K = 72;  // the single-GPU switch step (Engine::norm_a_power)
+  if (const char* env = std::getenv("RAPDHG_NORM_SLAB_STEP")) K = std::atoi(env);
+  for (auto& sh : shards_) {
+    sh->nv.alloc(n), sh->nw.alloc(n), sh->nmv.alloc(m);
+    if (sh->p1 > sh->p0) {
+      DevBuf<int32_t> len;
+      row_lengths(len, P.AT.rp.get() + sh->p0, nullptr, sh->p1 - sh->p0, st_);
+      build_schedule(sh->sch_at, len.get(), sh->p1 - sh->p0, false, st_);
+    }
+  }
+  RandomStart start = draw_random_start(n, seed);
+  std::mt19937_64 rng = start.rng;
+  // random_unit (opnorm.hpp:20-30): the draws normalised over all n (every
+  // shard holds the whole vector)
+  auto random_unit = [&](const std::vector<double>& h) {
+    for (auto& sh : shards_) sh->nv.upload(h.data(), n, st_);
+    double s[1];
+    reduce<1, 0>(true, [&](Shard& sh, int64_t lo) { return SumSq{sh.nv.get() + lo}; }, s);
+    const double nrm = std::sqrt(s[0]);
+    if (nrm > 0.0)
+      for (auto& sh : shards_) {
+        scale_slice_kernel<<<grid1(n), 256, 0, st_>>>(sh->nv.get(), sh->nv.get(), 1.0 / nrm, 0, n);
+        RB_LAUNCH_CHECK();
+      }
+  };
+  random_unit(start.v);
+  double lambda = 0.0;
+  bool slab = false;
+  for (int it = 0; it < max_iters; ++it) {
+    if (!slab && K >= 0 && it >= K) slab = true;  // the switch step (deterministic, as one GPU)
+    // mv = A v on the owned dual rows, then everywhere
+    for (auto& sh : shards_) {
+      if (sh->d1 <= sh->d0) continue;
+      const int64_t o = sh->d0;
+      if (slab && sh->dual_ph.active()) {
+        launches_ += launch_slab_phase(PhaseSpmvOp<1>{CsrView{P.A.rp.get() + o, P.A.ci.get(), e.asv_}, CsrView{},
+                                                      sh->nv.get(), sh->nv.get(), sh->nmv.get() + o},
+                                       sh->dual_ph, st_);
+      } else {
+        launch_rowwise(SpmvOp<false>{CsrView{P.A.rp.get() + o, P.A.ci.get(), e.asv_}, sh->nv.get(), sh->nmv.get() + o},
+                       sh->sch_dual.view, st_);
+        ++launches_;
+      }
+    }
+    exchange([](Shard& sh) { return sh.nmv.get(); }, false);
+    // w = A' mv on the owned primal rows (the A' segment of [Q | A'])
+    for (auto& sh : shards_) {
+      if (sh->p1 <= sh->p0) continue;
+      const int64_t o = sh->p0;
+      if (slab && sh->primal_ph.active()) {
+        launches_ += launch_slab_phase(
+            PhaseSpmvOp<2>{CsrView{P.Q.rp.get() + o, P.Q.ci.get(), e.qsv_}, CsrView{P.AT.rp.get() + o, P.AT.ci.get(), e.atsv_},
+                           sh->nv.get(), sh->nmv.get(), sh->nw.get() + o},
+            sh->primal_ph, st_);
+      } else {
+        launch_rowwise(SpmvOp<false>{CsrView{P.AT.rp.get() + o, P.AT.ci.get(), e.atsv_}, sh->nmv.get(), sh->nw.get() + o},
+                       sh->sch_at.view, st_);
+        ++launches_;
+      }
+    }
+    double h[2];
+    reduce<2, 0>(true, [&](Shard& sh, int64_t lo) { return DotAndSumSq{sh.nv.get() + lo, sh.nw.get() + lo}; }, h);
+    const double lambda_next = h[0];
+    const double nrm = std::sqrt(h[1]);
+    if (nrm == 0.0) {  // v in the null space: restart from fresh draws (opnorm.hpp:53-57)
+      std::vector<double> v(n);
+      for (double& x : v) x = 2.0 * (static_cast<double>(rng() >> 11) * 0x1.0p-53) - 1.0;
+      random_unit(v);
+      continue;
+    }
+    if (it > 0 && std::fabs(lambda_next - lambda) <= tol * std::fabs(lambda_next)) {
+      lambda = lambda_next;
+      break;
+    }
+    lambda = lambda_next;
+    // v = w / ||w|| on the owned slice, then everywhere
+    const double inv = 1.0 / nrm;
+    for (auto& sh : shards_) {
+      if (sh->p1 <= sh->p0) continue;
+      scale_slice_kernel<<<grid1(sh->p1 - sh->p0), 256, 0, st_>>>(sh->nv.get(), sh->nw.get(), inv, sh->p0, sh->p1);
+      RB_LAUNCH_CHECK();
+    }
+    exchange([](Shard& sh) { return sh.nv.get(); }, true);
+  }
+  RB_CUDA(cudaStreamSynchronize(st_));
+  for (auto& sh : shards_) sh->nv.reset(), sh->nw.reset(), sh->nmv.reset();
+  return std::sqrt(std::max(lambda, 0.0));
 }
 
 void ShardedEngine::build_replicated() {

@@ -116,6 +116,15 @@ class ShardedEngine : public LoopBackend {
   // mode: iterates agree to rounding, see tests/test_gpu_shard.py).
   void build_replicated();
   void replicated_step(int it, int c);
+  // estimate_op_norm on A (opnorm.hpp:36-61) over the shards: each step's
+  // products on the owned rows (rowwise, then from the same switch step as
+  // one GPU the shards' slab phases), allgathers of A v and of the normalised
+  // v, and the chunked reduction of (v.w, w.w) — the single-GPU estimate
+  // bit for bit (rows, chunks and combine as there), without any rank
+  // building plans over all rows or computing all products
+  // (RAPDHG_SHARD_NORMS=0: every rank runs the single-GPU estimate)
+  double distributed_norm_a(int max_iters, double tol, uint64_t seed);
+  bool shard_norms_ = true;
   int32_t nrep_ = 0;
   DevBuf<int32_t> rep_rows_;
   DevBuf<uint8_t> rep_flag_;  // n: 1 on replicated rows

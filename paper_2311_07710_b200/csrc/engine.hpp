@@ -7,6 +7,7 @@
 // kMaxChunk iterations with one host synchronisation per chunk.
 #pragma once
 
+#include <atomic>
 #include <chrono>
 #include <future>
 #include <map>
@@ -89,7 +90,9 @@ class DeviceQP {
   // given values (patterns of Q / A / A').
   // pre: the draws of mt19937_64(seed) over n entries (draw_random_start), or
   // null to draw them here
-  double op_norm_q(const double* qv, int max_iters, double tol, uint64_t seed, const RandomStart* pre = nullptr);
+  // on / rs: run on that stream with that scratch (norm Q beside norm A)
+  double op_norm_q(const double* qv, int max_iters, double tol, uint64_t seed, const RandomStart* pre = nullptr,
+                   cudaStream_t on = nullptr, ReduceScratch* rs = nullptr);
   double op_norm_a(const double* av, const double* atv, int max_iters, double tol, uint64_t seed,
                    const RandomStart* pre = nullptr);
 
@@ -103,7 +106,6 @@ class DeviceQP {
 
   cudaStream_t st;
   bool strict;
-  bool graphs = true;  // power-iteration batches as CUDA graphs (SolverConfig.use_graphs)
   int n, mi, me, m;
   DevCsr Q, A, AT;  // original values; A = [A_ineq; A_eq]
   DevBuf<int32_t> at_perm;  // AT position -> A position
@@ -116,7 +118,7 @@ class DeviceQP {
   ReduceScratch red;
   DevBuf<double> red_out;
   PinnedBuf<double> red_host;
-  int64_t launches = 0;
+  std::atomic<int64_t> launches{0};  // (norm Q counts from its own host thread)
 };
 
 // relKKT of the current iterate and of the average at one check

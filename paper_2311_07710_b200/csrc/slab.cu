@@ -71,20 +71,33 @@ __device__ __forceinline__ int in_window_count(const int32_t* rp, const int32_t*
                                                int* per, int64_t stride, int* maxrun = nullptr, int cap = 0) {
   const int b = rp[r], e = rp[r + 1];
   int tot = 0, mx = 0, cur = -1, run = 0;
-  for (int p = b; p < e; ++p) {
-    const int w = wins.of(ci[p]);
-    if (w < 0) {
-      if (cap > 0 && (p + 1 - b) - tot > cap) break;
-      continue;
+  // batches of 8 entries: their window lookups are independent loads, so a
+  // long row (C4's 5,000-entry feature rows) keeps 8 in flight instead of 1
+  constexpr int B = 8;
+  for (int p0 = b; p0 < e; p0 += B) {
+    int wv[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) wv[u] = p0 + u < e ? wins.of(ci[p0 + u]) : -2;
+    bool stop = false;
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const int w = wv[u];
+      if (w == -2 || stop) break;
+      const int p = p0 + u;
+      if (w < 0) {
+        if (cap > 0 && (p + 1 - b) - tot > cap) stop = true;
+        continue;
+      }
+      const int s = wins.run(w);
+      if (s != cur) {
+        if (cur >= 0 && per) per[cur * stride] = run;
+        cur = s, run = 0;
+      }
+      ++run, ++tot;
+      mx = max(mx, run);
+      if (cap > 0 && mx > cap) stop = true;
     }
-    const int s = wins.run(w);
-    if (s != cur) {
-      if (cur >= 0 && per) per[cur * stride] = run;
-      cur = s, run = 0;
-    }
-    ++run, ++tot;
-    mx = max(mx, run);
-    if (cap > 0 && mx > cap) break;
+    if (stop) break;
   }
   if (cur >= 0 && per) per[cur * stride] = run;
   if (maxrun) *maxrun = mx;
@@ -94,12 +107,70 @@ __device__ __forceinline__ int in_window_count(const int32_t* rp, const int32_t*
 // Rows [r0, r1): in-window entry count, or 0 when a window run or the rest
 // (other entries of both segments) exceeds cap — such rows stay on the
 // regular schedule, whose block/split bins spread long rows over a CTA.
+// Rows longer than this are counted by a block each (count_long_kernel,
+// seg_counts_long_kernel): per window, two binary searches in the sorted
+// columns instead of one thread walking every entry (C4's 1e4 feature rows of
+// 5,000 entries: 18 ms of one-thread scans in the primal plan's counts).
+constexpr int kLongRow = 2048;
+
+__device__ __forceinline__ int32_t first_at_least(const int32_t* c, int32_t b, int32_t e, int64_t key) {
+  while (b < e) {
+    const int32_t mid = b + (e - b) / 2;
+    if (c[mid] < key) b = mid + 1;
+    else e = mid;
+  }
+  return b;
+}
+
+// Block-wide window counts of row r: per window s, c_s (via `per`, stride
+// apart, or not at all), and the total and the longest run (thread 0).
+template <class PerFn>
+__device__ __forceinline__ void block_window_counts(const int32_t* rp, const int32_t* ci, int r, const Wins& wins,
+                                                    PerFn per, int* tot_out, int* mx_out) {
+  __shared__ int st[256], sm[256];
+  const int b = rp[r], e = rp[r + 1];
+  int tot = 0, mx = 0;
+  for (int s = threadIdx.x; s < wins.S; s += blockDim.x) {
+    const Window w = wins.w[s];
+    const int c = first_at_least(ci, b, e, static_cast<int64_t>(w.lo) + w.len) - first_at_least(ci, b, e, w.lo);
+    per(s, c);
+    tot += c;
+    mx = max(mx, c);
+  }
+  st[threadIdx.x] = tot, sm[threadIdx.x] = mx;
+  __syncthreads();
+  for (int h = blockDim.x / 2; h > 0; h >>= 1) {
+    if (static_cast<int>(threadIdx.x) < h)
+      st[threadIdx.x] += st[threadIdx.x + h], sm[threadIdx.x] = max(sm[threadIdx.x], sm[threadIdx.x + h]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *tot_out = st[0], *mx_out = wins.stride ? st[0] : sm[0];  // resident: one run
+  __syncthreads();
+}
+
+__global__ void count_long_kernel(const int32_t* list, const int32_t* nlist, const int32_t* rp, const int32_t* ci,
+                                  const int32_t* rp_o, int32_t r0, Wins wins, int cap, int32_t* cnt) {
+  __shared__ int tot, mx;
+  for (int i = blockIdx.x; i < *nlist; i += gridDim.x) {
+    const int r = list[i];
+    block_window_counts(rp, ci, r, wins, [](int, int) {}, &tot, &mx);
+    if (threadIdx.x == 0) {
+      const int rest = (rp[r + 1] - rp[r]) - tot + (rp_o ? rp_o[r + 1] - rp_o[r] : 0);
+      cnt[r - r0] = (mx <= cap && rest <= cap) ? tot : 0;
+    }
+  }
+}
+
 __global__ void count_kernel(const int32_t* rp, const int32_t* ci, const int32_t* rp_o, int32_t r0, int32_t r1,
-                             Wins wins, int cap, int32_t* cnt) {
+                             Wins wins, int cap, int32_t* cnt, int32_t* long_list, int32_t* nlong) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= r1 - r0) return;
   const int r = r0 + static_cast<int>(i);
   const int len = rp[r + 1] - rp[r], len_o = rp_o ? rp_o[r + 1] - rp_o[r] : 0;
+  if (len > kLongRow && len_o <= cap) {  // a block's work (count_long_kernel)
+    long_list[atomicAdd(nlong, 1)] = r;
+    return;
+  }
   if (len_o > cap) {  // the other segment alone exceeds the rest cap
     cnt[i] = 0;
     return;
@@ -112,13 +183,38 @@ __global__ void count_kernel(const int32_t* rp, const int32_t* ci, const int32_t
 
 // per-(window, W row) counts (window-major, cnt[s * nw + k]) and rest counts
 __global__ void seg_counts_kernel(const int32_t* rows, int32_t nw, const int32_t* rp_w, const int32_t* ci_w,
-                                  const int32_t* rp_o, Wins wins, int32_t* cnt, int32_t* rest_w, int32_t* rest_o) {
+                                  const int32_t* rp_o, Wins wins, int32_t* cnt, int32_t* rest_w, int32_t* rest_o,
+                                  int32_t* long_list, int32_t* nlong) {
   const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (k >= nw) return;
   const int r = rows[k];
+  if (rp_w[r + 1] - rp_w[r] > kLongRow) {  // seg_counts_long_kernel
+    long_list[atomicAdd(nlong, 1)] = static_cast<int32_t>(k);
+    return;
+  }
   const int tot = in_window_count(rp_w, ci_w, r, wins, cnt + k, nw);
   rest_w[k] = (rp_w[r + 1] - rp_w[r]) - tot;
   rest_o[k] = rp_o ? rp_o[r + 1] - rp_o[r] : 0;
+}
+
+__global__ void seg_counts_long_kernel(const int32_t* list, const int32_t* nlist, const int32_t* rows, int32_t nw,
+                                       const int32_t* rp_w, const int32_t* ci_w, const int32_t* rp_o, Wins wins,
+                                       int32_t* cnt, int32_t* rest_w, int32_t* rest_o) {
+  __shared__ int tot, mx;
+  for (int i = blockIdx.x; i < *nlist; i += gridDim.x) {
+    const int k = list[i], r = rows[k];
+    if (wins.stride) {  // resident: one run over every window
+      block_window_counts(rp_w, ci_w, r, wins, [](int, int) {}, &tot, &mx);
+      if (threadIdx.x == 0) cnt[k] = tot;
+    } else {
+      block_window_counts(rp_w, ci_w, r, wins, [&](int s, int c) { cnt[static_cast<int64_t>(s) * nw + k] = c; }, &tot,
+                          &mx);
+    }
+    if (threadIdx.x == 0) {
+      rest_w[k] = (rp_w[r + 1] - rp_w[r]) - tot;
+      rest_o[k] = rp_o ? rp_o[r + 1] - rp_o[r] : 0;
+    }
+  }
 }
 
 // block per tile, thread per slot: the slot's W row k (perm) has its run in
@@ -323,17 +419,27 @@ void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const in
   const int32_t* rp_o = seg == 0 ? rp2 : rp1;  // the other segment (rest only)
   const int32_t* ci_o = seg == 0 ? ci2 : ci1;
   const int32_t nr = r1 - r0;
-  std::vector<int32_t> hc;
+  // per-row counts through pinned staging (C4's dual: 2e6 rows — a pageable
+  // round trip of the counts and the W-row list cost several ms here)
+  PinnedBuf<int32_t> hcb;
+  hcb.alloc(static_cast<std::size_t>(nr));
+  DevBuf<int32_t> long_list(nr), nlong(1);
   {
     DevBuf<int32_t> cnt(nr);
-    count_kernel<<<g1(nr), 256, 0, st>>>(rp_w, ci_w, rp_o, r0, r1, wins, kSlabRunCap, cnt.get());
+    nlong.zero(st);
+    count_kernel<<<g1(nr), 256, 0, st>>>(rp_w, ci_w, rp_o, r0, r1, wins, kSlabRunCap, cnt.get(), long_list.get(),
+                                         nlong.get());
+    count_long_kernel<<<4 * kSMs, 256, 0, st>>>(long_list.get(), nlong.get(), rp_w, ci_w, rp_o, r0, wins, kSlabRunCap,
+                                                cnt.get());
     RB_LAUNCH_CHECK();
-    hc = download(cnt, nr, st);
+    if (nr > 0) RB_CUDA(cudaMemcpyAsync(hcb.get(), cnt.get(), sizeof(int32_t) * nr, cudaMemcpyDeviceToHost, st));
+    RB_CUDA(cudaStreamSynchronize(st));
   }
+  tr.mark("    row counts");
   std::vector<int32_t> rows;
   const int min_row = slab_min_row();
   for (int32_t i = 0; i < nr; ++i)
-    if (hc[i] >= min_row) rows.push_back(r0 + i);
+    if (hcb[i] >= min_row) rows.push_back(r0 + i);
   const int32_t nw = static_cast<int32_t>(rows.size());
   if (nw == 0) {
     if (std::getenv("RAPDHG_TRACE"))
@@ -341,7 +447,8 @@ void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const in
     return;
   }
   plan.rows.alloc(nw);
-  plan.rows.upload(rows.data(), nw, st);
+  std::memcpy(hcb.get(), rows.data(), sizeof(int32_t) * nw);  // (nw <= nr: the staging buffer fits)
+  plan.rows.upload(hcb.get(), nw, st);
   // per-(window, row) run lengths and rest counts
   const int64_t runs = static_cast<int64_t>(nw) * S;
   if (runs > kSlabMaxRuns) {  // ~20 B of plan state per (window, W row) pair
@@ -352,7 +459,11 @@ void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const in
   }
   DevBuf<int32_t> c2(runs), rw(nw), ro(nw);
   c2.zero(st);
-  seg_counts_kernel<<<g1(nw), 256, 0, st>>>(plan.rows.get(), nw, rp_w, ci_w, rp_o, wins, c2.get(), rw.get(), ro.get());
+  nlong.zero(st);
+  seg_counts_kernel<<<g1(nw), 256, 0, st>>>(plan.rows.get(), nw, rp_w, ci_w, rp_o, wins, c2.get(), rw.get(), ro.get(),
+                                            long_list.get(), nlong.get());
+  seg_counts_long_kernel<<<4 * kSMs, 256, 0, st>>>(long_list.get(), nlong.get(), plan.rows.get(), nw, rp_w, ci_w, rp_o,
+                                                   wins, c2.get(), rw.get(), ro.get());
   RB_LAUNCH_CHECK();
   PinnedBuf<int32_t> hc2;  // the run lengths, for the host layout
   hc2.alloc(static_cast<std::size_t>(runs));

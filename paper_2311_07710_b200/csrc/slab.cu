@@ -11,6 +11,8 @@
 #include <vector>
 
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include "slab.cuh"
 #include "slab_layout.hpp"
@@ -18,6 +20,11 @@
 namespace rb {
 
 namespace {
+
+__global__ void others_flag_kernel(const int32_t* widx, int32_t n, uint8_t* flag) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) flag[i] = widx[i] < 0;
+}
 
 // Column histogram by window (integer counts: exact in any order). A block
 // counts a grid-stride share in shared memory first — global atomics on a few
@@ -582,14 +589,31 @@ void build_slab_phase(SlabPhase& ph, const SlabChoice& choice, int seg, const in
   build_slab_plan(ph.plan, choice, seg, rp1, ci1, rp2, ci2, r0, r1, st);
   if (!ph.active()) return;
   const int32_t nr = r1 - r0;
-  const std::vector<int32_t> widx = download(ph.plan.widx, nr, st);
-  const std::vector<int32_t> hlen = download_len(len, nr, st);
   // the rows without partials: a rowwise schedule; RAPDHG_SELL_OTHERS=1 puts
   // the short ones (<= kSellMaxLen entries, a per-row rule, so shards agree)
   // on sliced ELL instead — measured neutral (C4 +0.6%, C3 -0.8%, C2 -2%:
   // these rows overlap the slab kernel either way), so off by default
   const char* so = std::getenv("RAPDHG_SELL_OTHERS");
   const bool sell = sell_enabled() && so && so[0] == '1';
+  if (!sell) {  // the list on the device (C4's dual: 1e6 of 2e6 rows; no host round trip)
+    DevBuf<uint8_t> flag(nr);
+    others_flag_kernel<<<g1(nr), 256, 0, st>>>(ph.plan.widx.get(), nr, flag.get());
+    RB_LAUNCH_CHECK();
+    DevBuf<int32_t> list(nr), cnt(1);
+    const thrust::counting_iterator<int32_t> idx(0);
+    std::size_t tb = 0;
+    RB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, idx, flag.get(), list.get(), cnt.get(), nr, st));
+    DevBuf<unsigned char> tmp(tb);
+    RB_CUDA(cub::DeviceSelect::Flagged(tmp.get(), tb, idx, flag.get(), list.get(), cnt.get(), nr, st));
+    int32_t no = 0;
+    RB_CUDA(cudaMemcpyAsync(&no, cnt.get(), sizeof(no), cudaMemcpyDeviceToHost, st));
+    RB_CUDA(cudaStreamSynchronize(st));
+    if (no > 0) build_schedule(ph.others, len, no, false, st, list.get());
+    RB_CUDA(cudaStreamSynchronize(st));
+    return;
+  }
+  const std::vector<int32_t> widx = download(ph.plan.widx, nr, st);
+  const std::vector<int32_t> hlen = download_len(len, nr, st);
   std::vector<int32_t> orr, osh;
   for (int32_t i = 0; i < nr; ++i)
     if (widx[i] < 0) (sell && hlen[i] <= kSellMaxLen ? osh : orr).push_back(i);

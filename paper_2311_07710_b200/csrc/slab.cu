@@ -21,6 +21,15 @@ namespace rb {
 
 namespace {
 
+// widx[row - r0] = k and wrow[k] = row - r0 for the W rows (rows[k])
+__global__ void wrow_kernel(const int32_t* rows, int32_t nw, int32_t r0, int32_t* widx, int32_t* wrow) {
+  const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nw) return;
+  const int32_t r = rows[k] - r0;
+  widx[r] = k;
+  wrow[k] = r;
+}
+
 __global__ void others_flag_kernel(const int32_t* widx, int32_t n, uint8_t* flag) {
   const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) flag[i] = widx[i] < 0;
@@ -530,14 +539,11 @@ void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const in
   tr.mark("    upload + fill");
   plan.partial.alloc(runs);
   plan.partial.zero(st);  // (window, row) pairs without entries keep 0
-  {
-    std::vector<int32_t> widx(nr, -1), wrow(nw);
-    for (int32_t k = 0; k < nw; ++k) widx[rows[k] - r0] = k, wrow[k] = rows[k] - r0;
-    plan.widx.alloc(nr);
-    plan.widx.upload(widx.data(), nr, st);
-    plan.wrow.alloc(nw);
-    plan.wrow.upload(wrow.data(), nw, st);
-  }
+  plan.widx.alloc(nr);  // on the device from the W rows (no host arrays of nr entries)
+  RB_CUDA(cudaMemsetAsync(plan.widx.get(), 0xff, sizeof(int32_t) * nr, st));  // -1: no partials
+  plan.wrow.alloc(nw);
+  wrow_kernel<<<g1(nw), 256, 0, st>>>(plan.rows.get(), nw, r0, plan.widx.get(), plan.wrow.get());
+  RB_LAUNCH_CHECK();
   SlabView& v = plan.view;
   v.nw = nw;
   v.S = S;

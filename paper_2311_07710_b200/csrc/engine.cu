@@ -318,18 +318,31 @@ void measures_mode(DeviceQP& P, const double* qv, const double* av, const double
   else measures<false, Kind>(P, qv, av, atv, meas);
 }
 // apply the factors f to the working values, then measure (ApplyMeasureOp)
+// side (optional): the A rows' sweep runs there, beside the [Q | A'] rows'
+// (two independent sweeps; `fork` / `join` events order them with P.st)
 template <bool Strict, int Kind>
-void apply_measures(DeviceQP& P, double* qw, double* aw, double* atw, const double* f, double* meas) {
+void apply_measures(DeviceQP& P, double* qw, double* aw, double* atw, const double* f, double* meas,
+                    cudaStream_t side, cudaEvent_t fork, cudaEvent_t join) {
   ApplyMeasureOp<Strict, Kind> prim{P.Q.view(qw), P.AT.view(atw), qw, atw, f, 0, 0, 0, P.n, meas};
-  rowwise(prim, P.sch_primal, P.st, &P.launches);
   ApplyMeasureOp<Strict, Kind> dual{P.A.view(aw), CsrView{nullptr, nullptr, nullptr}, aw, nullptr, f, P.n, 0, 0, 0,
                                     meas + P.n};
-  rowwise(dual, P.sch_dual, P.st, &P.launches);
+  if (side) {
+    RB_CUDA(cudaEventRecord(fork, P.st));
+    RB_CUDA(cudaStreamWaitEvent(side, fork, 0));
+    rowwise(dual, P.sch_dual, side, &P.launches);
+    rowwise(prim, P.sch_primal, P.st, &P.launches);
+    RB_CUDA(cudaEventRecord(join, side));
+    RB_CUDA(cudaStreamWaitEvent(P.st, join, 0));
+  } else {
+    rowwise(prim, P.sch_primal, P.st, &P.launches);
+    rowwise(dual, P.sch_dual, P.st, &P.launches);
+  }
 }
 template <int Kind>
-void apply_measures_mode(DeviceQP& P, double* qw, double* aw, double* atw, const double* f, double* meas) {
-  if (P.strict) apply_measures<true, Kind>(P, qw, aw, atw, f, meas);
-  else apply_measures<false, Kind>(P, qw, aw, atw, f, meas);
+void apply_measures_mode(DeviceQP& P, double* qw, double* aw, double* atw, const double* f, double* meas,
+                         cudaStream_t side, cudaEvent_t fork, cudaEvent_t join) {
+  if (P.strict) apply_measures<true, Kind>(P, qw, aw, atw, f, meas, nullptr, nullptr, nullptr);
+  else apply_measures<false, Kind>(P, qw, aw, atw, f, meas, side, fork, join);
 }
 }  // namespace
 
@@ -351,21 +364,34 @@ void DeviceQP::compute_scaling(int ruiz_iters, bool full, DevBuf<double>& d) {
   // the last pass's apply is not needed (the working copies are dropped).
   std::vector<int> kinds(static_cast<std::size_t>(std::max(ruiz_iters, 0)), 0);
   if (full) kinds.push_back(1), kinds.push_back(2);
+  // the A rows' sweeps on a side stream beside the [Q | A'] rows' (fast mode;
+  // their kernels are latency-bound, C4: 12 passes 10.7 -> see DESIGN §4)
+  OwnedStream side_own;
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  if (!strict) {
+    side = side_own.create();
+    RB_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    RB_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+  }
   for (std::size_t p = 0; p < kinds.size(); ++p) {
     if (p == 0) {
       if (kinds[0] == 0) measures_mode<0>(*this, qw.get(), aw.get(), atw.get(), meas.get());
       else if (kinds[0] == 1) measures_mode<1>(*this, qw.get(), aw.get(), atw.get(), meas.get());
       else measures_mode<2>(*this, qw.get(), aw.get(), atw.get(), meas.get());
     } else {  // apply pass p - 1's factors, measure for pass p
-      if (kinds[p] == 0) apply_measures_mode<0>(*this, qw.get(), aw.get(), atw.get(), f.get(), meas.get());
-      else if (kinds[p] == 1) apply_measures_mode<1>(*this, qw.get(), aw.get(), atw.get(), f.get(), meas.get());
-      else apply_measures_mode<2>(*this, qw.get(), aw.get(), atw.get(), f.get(), meas.get());
+      if (kinds[p] == 0) apply_measures_mode<0>(*this, qw.get(), aw.get(), atw.get(), f.get(), meas.get(), side, fork, join);
+      else if (kinds[p] == 1)
+        apply_measures_mode<1>(*this, qw.get(), aw.get(), atw.get(), f.get(), meas.get(), side, fork, join);
+      else apply_measures_mode<2>(*this, qw.get(), aw.get(), atw.get(), f.get(), meas.get(), side, fork, join);
     }
     factor_kernel<<<grid1(N), 256, 0, st>>>(f.get(), meas.get(), d.get(), N);
     RB_LAUNCH_CHECK();
     ++launches;
   }
   RB_CUDA(cudaStreamSynchronize(st));
+  if (fork) cudaEventDestroy(fork);
+  if (join) cudaEventDestroy(join);
 }
 
 void DeviceQP::scale_values(const double* d, DevBuf<double>& qs, DevBuf<double>& as,

@@ -16,6 +16,10 @@
 // windows, spans and tiles.
 #include "slab_layout.hpp"
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include <algorithm>
 #include <atomic>
 #include <climits>
@@ -112,6 +116,16 @@ bool slab_layout(const int32_t* len, int32_t nw, int S, int ecap, int rcap, int 
                  SlabLayout& out) {
   out = SlabLayout{};
   if (S <= 0 || nw <= 0) return true;
+  // RAPDHG_TRACE: the phases' host times
+  const bool trace = std::getenv("RAPDHG_TRACE") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto phase = [&](const char* what) {
+    if (!trace) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[slab layout] %d rows x %d windows: %-8s %.2f ms\n", nw, S, what,
+                 std::chrono::duration<double, std::milli>(now - t_last).count());
+    t_last = now;
+  };
   // row order per window: rows with a non-empty run (natural index order)
   std::vector<std::vector<int32_t>> order(S);
   parallel_for(S, [&](int64_t si) {
@@ -124,6 +138,7 @@ bool slab_layout(const int32_t* len, int32_t nw, int S, int ecap, int rcap, int 
     for (int32_t k = 0; k < nw; ++k)
       if (L[k] > 0) o[cnt++] = k;
   });
+  phase("order");
   // natural vs sorted: the padding natural tiles would have (each tile's runs
   // sorted, 32-row slices), estimated on a strided sample of up to 64 tiles'
   // worth of rows per window (the decision only needs the ratio)
@@ -173,6 +188,7 @@ bool slab_layout(const int32_t* len, int32_t nw, int S, int ecap, int rcap, int 
       for (int32_t k : o) tmp[start[kRunCap - std::min(L[k], kRunCap)]++] = k;
       o.swap(tmp);
     });
+  phase("padding");
   // greedy spans of whole 32-row groups per window (sorted: the group's padded
   // width; natural: its raw entries against 7/8 of the budget)
   std::vector<std::vector<Span>> spans_w(S);
@@ -201,6 +217,7 @@ bool slab_layout(const int32_t* len, int32_t nw, int S, int ecap, int rcap, int 
   });
   std::vector<Span> spans;
   for (auto& v : spans_w) spans.insert(spans.end(), v.begin(), v.end());
+  phase("spans");
   // tiles: rows sorted by run (in place), padded size; split any that overflow
   std::vector<int64_t> tn;
   for (;;) {
@@ -231,6 +248,7 @@ bool slab_layout(const int32_t* len, int32_t nw, int S, int ecap, int rcap, int 
     if (!split) break;
     spans.swap(next);
   }
+  phase("tiles");
   // offsets (sequential prefix over tiles)
   const int32_t ntiles = static_cast<int32_t>(spans.size());
   out.tiles.resize(ntiles);
@@ -258,6 +276,7 @@ bool slab_layout(const int32_t* len, int32_t nw, int S, int ecap, int rcap, int 
   out.entries = cursor;
   out.sorted = sorted;
   if (cursor > INT32_MAX || meta_at[ntiles] > INT32_MAX) return false;
+  phase("offsets");
   // metadata, in parallel over tiles (disjoint ranges)
   out.meta.assign(static_cast<std::size_t>(meta_at[ntiles]) + 8, 0);  // + slack: copies round up to 8
   parallel_for(ntiles, [&](int64_t t) {
@@ -278,6 +297,7 @@ bool slab_layout(const int32_t* len, int32_t nw, int S, int ecap, int rcap, int 
     }
     m[3 * nr + nsl] = static_cast<uint16_t>(cur);
   });
+  phase("metadata");
   return true;
 }
 

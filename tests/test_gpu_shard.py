@@ -167,3 +167,31 @@ def test_replicated_rows_other_patterns(monkeypatch):
     monkeypatch.setenv("RAPDHG_REPLICATE_MIN_LEN", str(int(np.percentile(lens, 90))))
     cfg = rb.SolverConfig(tol=1e-9, max_iters=800, snapshot_interval=40)
     _close_trajectories(rb.solve_sharded(q, cfg, 4), rb.solve(q, cfg))
+
+
+def test_sharded_setup_norms_both_ways(monkeypatch):
+    """The norm estimate of A over the shards (default) and on every rank alone
+    (RAPDHG_SHARD_NORMS=0) give the same bits as one GPU, the slab switch
+    included."""
+    monkeypatch.setenv("RAPDHG_SLAB", "force")
+    monkeypatch.setenv("RAPDHG_NORM_SLAB_STEP", "8")
+    p = rb.generate(rb.Gen.LASSO, 0.05, 2)
+    cfg = rb.SolverConfig(tol=1e-7, max_iters=600, snapshot_interval=100)
+    one = rb.solve(p, cfg)
+    for flag in ("1", "0"):
+        monkeypatch.setenv("RAPDHG_SHARD_NORMS", flag)
+        for parts in (2, 4):
+            r = rb.solve_sharded(p, cfg, parts)
+            assert r.norm_a == one.norm_a and r.norm_q == one.norm_q
+            assert_results_identical(r, one)
+
+
+def test_box_sharded_with_replicated_rows():
+    """Box projection and replicated dense rows together (C4's box form, small):
+    deterministic, one GPU's trajectory within rounding."""
+    p = rb.bounds_from_rows(rb.generate(rb.Gen.SVM, 0.01, 4))
+    cfg = rb.SolverConfig(tol=1e-8, max_iters=600, snapshot_interval=40, box_projection=True)
+    one = rb.solve(p, cfg)
+    a = rb.solve_sharded(p, cfg, 4, replicate_min_len=100)
+    assert_results_identical(a, rb.solve_sharded(p, cfg, 4, replicate_min_len=100))
+    _close_trajectories(a, one)

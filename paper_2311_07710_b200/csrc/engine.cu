@@ -925,18 +925,22 @@ void Engine::setup_colblocks() {
   }
 }
 
+int norm_slab_step() {
+  const char* e = std::getenv("RAPDHG_NORM_SLAB_STEP");
+  return e ? std::atoi(e) : kNormSlabStep;
+}
+
 // estimate_op_norm on A (opnorm.hpp:36-61) for the solve. Fast mode: the
 // first kNormSlabStep steps run on the rowwise SpMV while the slab plans are
 // still being built on host threads; from that step on (a batch boundary),
 // the plans are joined and the products run on the step's slab phases
-// (PhaseSpmvOp: C4 0.24 instead of 0.39 ms per step). The switch step is
-// fixed (RAPDHG_NORM_SLAB_STEP, default 72; -1 = never), never timing-
+// (PhaseSpmvOp: C4 0.22 instead of 0.40 ms per step). The switch step is
+// fixed (norm_slab_step(): 40 — C4's plans are ready by then), never timing-
 // dependent, so the estimate is deterministic; the sharded solver's setup
 // runs the same code on the same full matrices, so its norm is the same bits.
 double Engine::norm_a_power(int max_iters, double tol, uint64_t seed, const RandomStart* pre) {
   DeviceQP& P = *P_;
-  int K = 72;
-  if (const char* e = std::getenv("RAPDHG_NORM_SLAB_STEP")) K = std::atoi(e);
+  const int K = norm_slab_step();
   if (P.strict || K < 0 || P.A.nnz == 0) return P.op_norm_a(asv_, atsv_, max_iters, tol, seed, pre);
   DevBuf<double> v(n_), w(n_), mv(m_);
   bool slab = false;

@@ -161,6 +161,13 @@ void run_loop(LoopBackend& be, const rapdhg_config& cfg, const LoopScalars& sc, 
 
 class ShardedEngine;
 
+// The step at which the fast-mode norm estimate of A moves from the rowwise
+// SpMV to the slab phases (RAPDHG_NORM_SLAB_STEP, default kNormSlabStep; -1 =
+// never). Shared by Engine::norm_a_power and the sharded solver's distributed
+// estimate, which must switch at the same step to produce the same bits.
+constexpr int kNormSlabStep = 40;
+int norm_slab_step();
+
 class Engine : public LoopBackend {
  public:
   // full_plans = false (the sharded solver's setup): the slab phases over all

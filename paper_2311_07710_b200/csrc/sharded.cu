@@ -701,8 +701,7 @@ double ShardedEngine::distributed_norm_a(int max_iters, double tol, uint64_t see
   Engine& e = *full_;
   const int n = P.n, m = P.m;
   if (P.A.nnz == 0) return 0.0;
-  int K = 72;  // the single-GPU switch step (Engine::norm_a_power)
-  if (const char* env = std::getenv("RAPDHG_NORM_SLAB_STEP")) K = std::atoi(env);
+  const int K = norm_slab_step();  // the single-GPU switch step (Engine::norm_a_power)
   for (auto& sh : shards_) {
     sh->nv.alloc(n), sh->nw.alloc(n), sh->nmv.alloc(m);
     if (sh->p1 > sh->p0) {

@@ -491,8 +491,12 @@ void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const in
   int order_mode = 0;
   if (const char* mode = std::getenv("RAPDHG_SLAB_ORDER")) order_mode = std::string(mode) == "sorted" ? 2 : 1;
   SlabLayout lay;
+  PinnedBuf<uint16_t> hm;  // the metadata, written by the layout straight into pinned upload staging
   const bool fits = slab_layout(hc2.get(), nw, S, ecap, kSlabRowCap, order_mode,
-                                env_int("RAPDHG_SLAB_ROWCOST", kSlabRowCost), lay);
+                                env_int("RAPDHG_SLAB_ROWCOST", kSlabRowCost), lay, [&](std::size_t n) {
+                                  hm.alloc(n);
+                                  return hm.get();
+                                });
   tr.mark("    layout (host)");
   if (!fits || lay.max_tile > ecap || lay.max_meta > kSlabMetaCap) {  // int32 offsets; tiles must fit a stage
     plan = SlabPlan{};
@@ -504,11 +508,8 @@ void build_slab_plan(SlabPlan& plan, const SlabChoice& choice, int seg, const in
   plan.tile_bytes = lay.tile_bytes;
   const int64_t total = std::max<int64_t>(cursor, 32);
   {
-    PinnedBuf<uint16_t> hm;  // pinned staging of the metadata (tens of MB on the large configs)
-    hm.alloc(lay.meta.size());
-    std::memcpy(hm.get(), lay.meta.data(), sizeof(uint16_t) * lay.meta.size());
-    plan.meta.alloc(lay.meta.size());
-    plan.meta.upload(hm.get(), lay.meta.size(), st);
+    plan.meta.alloc(lay.meta_size());
+    plan.meta.upload(hm.get(), lay.meta_size(), st);
     plan.tile.alloc(lay.tiles.size());
     plan.tile.upload(lay.tiles.data(), lay.tiles.size(), st);
     plan.col.alloc(total), plan.pos.alloc(total), plan.val.alloc(total);

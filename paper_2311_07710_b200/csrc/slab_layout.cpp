@@ -113,7 +113,7 @@ int plan_threads() {
 }
 
 bool slab_layout(const int32_t* len, int32_t nw, int S, int ecap, int rcap, int order_mode, int64_t row_cost,
-                 SlabLayout& out) {
+                 SlabLayout& out, const MetaAlloc& meta_alloc) {
   out = SlabLayout{};
   if (S <= 0 || nw <= 0) return true;
   // RAPDHG_TRACE: the phases' host times
@@ -126,17 +126,36 @@ bool slab_layout(const int32_t* len, int32_t nw, int S, int ecap, int rcap, int 
                  std::chrono::duration<double, std::milli>(now - t_last).count());
     t_last = now;
   };
-  // row order per window: rows with a non-empty run (natural index order)
-  std::vector<std::vector<int32_t>> order(S);
-  parallel_for(S, [&](int64_t si) {
+  // row order per window: rows with a non-empty run (natural index order);
+  // windows cut into chunks of rows so that few, tall windows (C4's dual: 5 x
+  // 1e6 rows) still spread over the threads: count per chunk, then fill
+  constexpr int32_t kOrderChunk = 1 << 16;
+  const int32_t nch = (nw + kOrderChunk - 1) / kOrderChunk;
+  std::vector<int32_t> ccount(static_cast<std::size_t>(S) * nch + 1, 0);
+  parallel_for(static_cast<int64_t>(S) * nch, [&](int64_t i) {
+    const int64_t si = i / nch;
+    const int32_t k0 = static_cast<int32_t>(i % nch) * kOrderChunk, k1 = std::min(nw, k0 + kOrderChunk);
     const int32_t* L = len + si * nw;
-    std::vector<int32_t>& o = order[si];
     int32_t cnt = 0;
-    for (int32_t k = 0; k < nw; ++k) cnt += L[k] > 0;
-    o.resize(cnt);
-    cnt = 0;
-    for (int32_t k = 0; k < nw; ++k)
-      if (L[k] > 0) o[cnt++] = k;
+    for (int32_t k = k0; k < k1; ++k) cnt += L[k] > 0;
+    ccount[i] = cnt;
+  });
+  std::vector<std::vector<int32_t>> order(S);
+  std::vector<int32_t> cstart(ccount.size(), 0);
+  std::vector<int32_t> wcount(S);
+  for (int s = 0; s < S; ++s) {
+    int32_t c = 0;
+    for (int32_t j = 0; j < nch; ++j) cstart[static_cast<std::size_t>(s) * nch + j] = c, c += ccount[static_cast<std::size_t>(s) * nch + j];
+    wcount[s] = c;
+  }
+  parallel_for(S, [&](int64_t si) { order[si].resize(wcount[si]); });  // (fresh pages: fault them in parallel)
+  parallel_for(static_cast<int64_t>(S) * nch, [&](int64_t i) {
+    const int64_t si = i / nch;
+    const int32_t k0 = static_cast<int32_t>(i % nch) * kOrderChunk, k1 = std::min(nw, k0 + kOrderChunk);
+    const int32_t* L = len + si * nw;
+    int32_t* o = order[si].data() + cstart[i];
+    for (int32_t k = k0; k < k1; ++k)
+      if (L[k] > 0) *o++ = k;
   });
   phase("order");
   // natural vs sorted: the padding natural tiles would have (each tile's runs
@@ -219,34 +238,43 @@ bool slab_layout(const int32_t* len, int32_t nw, int S, int ecap, int rcap, int 
   for (auto& v : spans_w) spans.insert(spans.end(), v.begin(), v.end());
   phase("spans");
   // tiles: rows sorted by run (in place), padded size; split any that overflow
-  std::vector<int64_t> tn;
-  for (;;) {
-    tn.assign(spans.size(), 0);
-    parallel_for(static_cast<int64_t>(spans.size()), [&](int64_t t) {
-      thread_local std::vector<int32_t> cnt, tmp;
-      const Span& sp = spans[t];
-      const int32_t* L = len + static_cast<int64_t>(sp.s) * nw;
-      int32_t* r = order[sp.s].data();
-      sort_by_len_desc(r + sp.b, sp.e - sp.b, L, cnt, tmp);
-      int64_t n = 0;
-      for (int32_t q = sp.b; q < sp.e; q += 32) n += 32 * static_cast<int64_t>(L[r[q]]);
-      tn[t] = n;
-    });
+  // (a sub-range of a sorted span is sorted: halves only need their size)
+  auto padded = [&](const Span& sp) {
+    const int32_t* L = len + static_cast<int64_t>(sp.s) * nw;
+    const int32_t* r = order[sp.s].data();
+    int64_t n = 0;
+    for (int32_t q = sp.b; q < sp.e; q += 32) n += 32 * static_cast<int64_t>(L[r[q]]);
+    return n;
+  };
+  std::vector<int64_t> tn(spans.size(), 0);
+  parallel_for(static_cast<int64_t>(spans.size()), [&](int64_t t) {
+    thread_local std::vector<int32_t> cnt, tmp;
+    const Span& sp = spans[t];
+    sort_by_len_desc(order[sp.s].data() + sp.b, sp.e - sp.b, len + static_cast<int64_t>(sp.s) * nw, cnt, tmp);
+    tn[t] = padded(sp);
+  });
+  for (bool split = true; split;) {
+    split = false;
     std::vector<Span> next;
-    bool split = false;
+    std::vector<int64_t> nn;
+    next.reserve(spans.size());
+    nn.reserve(spans.size());
     for (std::size_t t = 0; t < spans.size(); ++t) {
       const Span& sp = spans[t];
       if (tn[t] > ecap && sp.e - sp.b > 32) {
         const int32_t mid = sp.b + std::max<int32_t>(32, ((sp.e - sp.b) / 2) & ~31);
         next.push_back({sp.s, sp.b, mid});
+        nn.push_back(padded(next.back()));
         next.push_back({sp.s, mid, sp.e});
+        nn.push_back(padded(next.back()));
         split = true;
       } else {
         next.push_back(sp);
+        nn.push_back(tn[t]);
       }
     }
-    if (!split) break;
     spans.swap(next);
+    tn.swap(nn);
   }
   phase("tiles");
   // offsets (sequential prefix over tiles)
@@ -278,13 +306,23 @@ bool slab_layout(const int32_t* len, int32_t nw, int S, int ecap, int rcap, int 
   if (cursor > INT32_MAX || meta_at[ntiles] > INT32_MAX) return false;
   phase("offsets");
   // metadata, in parallel over tiles (disjoint ranges)
-  out.meta.assign(static_cast<std::size_t>(meta_at[ntiles]) + 8, 0);  // + slack: copies round up to 8
+  // (written once: each tile zeroes its own 8-alignment tail, no fill pass)
+  out.meta_len = static_cast<std::size_t>(meta_at[ntiles]) + 8;  // + slack: copies round up to 8
+  if (meta_alloc) {
+    out.meta_ptr = meta_alloc(out.meta_len);
+  } else {
+    out.meta.resize(out.meta_len);
+    out.meta_ptr = out.meta.data();
+  }
+  uint16_t* const meta0 = out.meta_ptr;
+  std::fill(meta0 + meta_at[ntiles], meta0 + out.meta_len, uint16_t{0});
   parallel_for(ntiles, [&](int64_t t) {
     const Span& sp = spans[t];
     const int32_t* L = len + static_cast<int64_t>(sp.s) * nw;
     const int32_t* r = order[sp.s].data() + sp.b;
     const int32_t nr = sp.e - sp.b, nsl = (nr + 31) / 32;
-    uint16_t* m = out.meta.data() + meta_at[t];
+    uint16_t* m = meta0 + meta_at[t];
+    std::fill(m + 3 * nr + nsl + 1, meta0 + meta_at[t + 1], uint16_t{0});
     for (int32_t i = 0; i < nr; ++i) {
       m[2 * i] = static_cast<uint16_t>(static_cast<uint32_t>(r[i]) & 0xffffu);
       m[2 * i + 1] = static_cast<uint16_t>(static_cast<uint32_t>(r[i]) >> 16);

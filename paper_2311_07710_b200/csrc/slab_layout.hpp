@@ -5,7 +5,9 @@
 // (scripts/plan_bench.cpp).
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
+#include <functional>
 #include <vector>
 
 namespace rb {
@@ -28,7 +30,11 @@ struct SlabLayout {
   std::vector<int64_t> tile_bytes;  // staged bytes per tile (CTA balance)
   std::vector<int32_t> off, jx;     // per run (s * nw + k): tile base, jagged-offset slot (see fill_kernel)
   std::vector<int32_t> joff;        // per slice entry: offset inside the tile
-  std::vector<uint16_t> meta;       // all tiles' metadata (8-aligned per tile, + 8 slack)
+  std::vector<uint16_t> meta;       // all tiles' metadata (8-aligned per tile, + 8 slack), unless meta_alloc
+  uint16_t* meta_ptr = nullptr;     // where the metadata went (meta.data() or the meta_alloc buffer)
+  std::size_t meta_len = 0;
+  const uint16_t* meta_data() const { return meta_ptr; }
+  std::size_t meta_size() const { return meta_len; }
   int64_t entries = 0;              // padded entries of all tiles
   int max_tile = 0, max_meta = 0;
   bool sorted = false;              // row order used (natural unless it pads too much)
@@ -37,9 +43,11 @@ struct SlabLayout {
 // len: run lengths, window-major (len[s * nw + k]); ecap: tile entry cap
 // (multiple of 32); rcap: rows per tile; order: 0 auto, 1 natural, 2 sorted;
 // row_cost: CTA-balance cost per tile row. false when the layout does not fit
-// the int32 offsets.
+// the int32 offsets. meta_alloc (optional): where to write the metadata (the
+// caller's upload staging, e.g. pinned memory: no copy, no zero fill).
+using MetaAlloc = std::function<uint16_t*(std::size_t)>;
 bool slab_layout(const int32_t* len, int32_t nw, int S, int ecap, int rcap, int order, int64_t row_cost,
-                 SlabLayout& out);
+                 SlabLayout& out, const MetaAlloc& meta_alloc = {});
 
 // f(i) for i in [0, n) on host threads (RAPDHG_PLAN_THREADS, default half the cores)
 int plan_threads();

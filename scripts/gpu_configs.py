@@ -9,6 +9,8 @@ import paper_2311_07710_b200 as rb  # noqa: E402
 for name, kind, scale, seed in (("C1 random QP", rb.Gen.RANDOM_QP, 1.0, 1), ("C2 lasso", rb.Gen.LASSO, 1.0, 2),
                                 ("C3 portfolio", rb.Gen.PORTFOLIO, 1.0, 3), ("C4 svm", rb.Gen.SVM, 1.0, 4),
                                 ("C5-U large", rb.Gen.LARGE, 1.0, 5), ("C5-L large local", rb.Gen.LARGE_LOCAL, 1.0, 5)):
+    if len(sys.argv) > 1 and name.split()[0] not in sys.argv[1:]:  # e.g. gpu_configs.py C2 C4
+        continue
     p = rb.generate(kind, scale, seed)
     s = rb.Session(p, rb.SolverConfig(tol=1e-12, max_iters=400, profile_kernels=2))
     s.solve()

@@ -81,6 +81,7 @@ struct SlabView {
   int32_t ecap = 0;                // tile entry capacity (multiple of 8)
   int32_t mcap = 0;                // tile metadata capacity (multiple of 8)
   int32_t grid = 0;                // persistent CTAs
+  int32_t wfirst = 0;              // finish grid: W-row blocks first (launch_slab_phase)
   int32_t resident = 0;            // > 0: that many windows staged at once (window s at s * win_max / resident);
                                    // W rows are one run and finish in the slab kernel (no partials)
   const Window* win = nullptr;     // [S] (device)
@@ -465,16 +466,22 @@ __global__ void __launch_bounds__(kBlock) slab_finish_kernel(const Op op, const 
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int ob = others.total_blocks > 0 ? others.total_blocks : 0;
   const int sb = static_cast<int>((osell.nslices + kBlock / 32 - 1) / (kBlock / 32));
-  if (static_cast<int>(blockIdx.x) < ob) {  // first: the rows without partials (they start at once)
+  // block order: others, SELL slices, W rows — or (wfirst) the W-row blocks
+  // first, so they are resident and have loaded their rest entries and
+  // epilogue inputs when the slab grid completes (the arithmetic per row is
+  // the same either way)
+  int bid = static_cast<int>(blockIdx.x);
+  if (sv.wfirst) bid = bid < wblocks ? ob + sb + bid : bid - wblocks;
+  if (bid < ob) {  // the rows without partials (they start at once)
     const Gather g[2] = {Gather{op.gather_src(0), nullptr, 0, 0u}, Gather{op.gather_src(1), nullptr, 0, 0u}};
-    rowwise_tile(op, others, blockIdx.x, g);
+    rowwise_tile(op, others, bid, g);
 #ifdef RB_SLAB_PROFILE
     if (threadIdx.x == 0 && sv.fprof) atomicMax(&sv.fprof[0], slab_now());
 #endif
     return;
   }
-  if (static_cast<int>(blockIdx.x) < ob + sb) {  // the short ones of them: sliced ELL, a slice per warp
-    const int64_t q = static_cast<int64_t>(blockIdx.x - ob) * (kBlock / 32) + (threadIdx.x >> 5);
+  if (bid < ob + sb) {  // the short ones of them: sliced ELL, a slice per warp
+    const int64_t q = static_cast<int64_t>(bid - ob) * (kBlock / 32) + (threadIdx.x >> 5);
     if (q < osell.nslices) sell_slice(op, osell, q, threadIdx.x & 31);
     return;
   }
@@ -491,7 +498,7 @@ __global__ void __launch_bounds__(kBlock) slab_finish_kernel(const Op op, const 
   // few, a thread takes one row and sums its S partials in order.
   const bool grouped = sv.S >= kSlabGroupedS;
   const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
-  const int wb = static_cast<int>(blockIdx.x) - ob - sb;  // W-row block
+  const int wb = bid - ob - sb;  // W-row block
   const int k = grouped ? wb * 32 + lane : wb * kBlock + threadIdx.x;
   const bool valid = k < sv.nw;
   const bool owner = valid && (!grouped || g == 0);  // runs the row's epilogue
@@ -619,6 +626,12 @@ inline int launch_slab_phase(const Op& op, const SlabPhase& ph, cudaStream_t st,
   const SellView& osell = ph.others_sell.view;
   const int wblocks = sv.resident ? 1 : static_cast<int>(ceil_div(sv.nw, sv.S >= kSlabGroupedS ? 32 : kBlock));
   const int sblocks = static_cast<int>(ceil_div(osell.nslices, kBlock / 32));
+  {  // W-row blocks first when they fit two per SM (C3's dual: 32 blocks, step 62 -> 55 us; with
+     // more of them, e.g. C4's 3,907 + 313, they would hold the SMs idle in their wait while the
+     // rows without partials queue behind them: C4 129 -> 140 us). RAPDHG_FINISH_WFIRST=0|1 forces.
+    const char* e = std::getenv("RAPDHG_FINISH_WFIRST");  // per launch (graphs capture it once)
+    sv.wfirst = e && (e[0] == '0' || e[0] == '1') ? e[0] == '1' : wblocks <= 2 * kSMs;
+  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(wblocks + sblocks + (o.total_blocks > 0 ? o.total_blocks : 0)));
   cfg.blockDim = dim3(kBlock);

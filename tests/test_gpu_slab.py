@@ -156,6 +156,22 @@ def test_pdl_schedule_matches_serialised(monkeypatch):
     assert_results_identical(a, b)
 
 
+@pytest.mark.parametrize("kind, scale, seed", [(rb.Gen.PORTFOLIO, 0.2, 3), (rb.Gen.SVM, 0.1, 4)])
+def test_finish_block_order_does_not_change_results(kind, scale, seed, monkeypatch):
+    """The finish grid runs its W-row blocks first when they fit two per SM
+    (C3's dual) and last otherwise (slab.cuh launch_slab_phase); forcing
+    either order (RAPDHG_FINISH_WFIRST) gives bit-identical solves, with and
+    without programmatic dependent launches."""
+    p = rb.generate(kind, scale, seed)
+    cfg = rb.SolverConfig(tol=1e-12, max_iters=400, snapshot_interval=80, record_restart_points=True)
+    base = rb.solve(p, cfg)
+    for pdl in ("1", "0"):
+        monkeypatch.setenv("RAPDHG_PDL", pdl)
+        for wfirst in ("0", "1"):
+            monkeypatch.setenv("RAPDHG_FINISH_WFIRST", wfirst)
+            assert_results_identical(rb.solve(p, cfg), base)
+
+
 def test_resident_plan_on_c4_svm_dual(monkeypatch):
     """The C4 dual (5 windows over the 1e4 feature columns) qualifies for a
     resident plan (opt-in, RAPDHG_SLAB_RESIDENT=1); at 1/10 scale both modes
